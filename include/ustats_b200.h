@@ -1,0 +1,145 @@
+/*
+ * ustats_b200 — C-ABI of the B200 exact-U-statistic engine.
+ *
+ * Drop-in boundary for the reference's FFI on this path: the pybind11 module
+ * `_ustats` (proj/python/ustats_py.cpp:68-174) and the C++ entry points it
+ * wraps (proj/include/ustats/engine.hpp:32-65, einsum.hpp:41-52). Every
+ * function is `extern "C"`, takes plain pointers and sizes, never throws, and
+ * returns 0 on success or 1 + the reference ErrorCode value
+ * (proj/include/ustats/errors.hpp:10-28; CudaError = 18, CollectiveError = 19)
+ * with the message in us_last_error() (thread-local).
+ *
+ * Problem encoding shared by the statistic calls (the tensor-backed form of
+ * MDKernel, kernel.hpp:39-54, after tensorize):
+ *   m          kernel arity
+ *   K          number of components
+ *   tuple_len  K entries: |signature[k]|
+ *   tuple_idx  concatenated 0-based slots of signature[k]
+ *   factors    K pointers: component k materialized over [0,n)^|sig[k]|,
+ *              row-major f64, NOT sparsified (the engine sparsifies on device).
+ *              Equal pointers denote the same tensor and are uploaded once.
+ *   n          sample size (shared extent)
+ *   on_device  0: factors are host memory; 1: CUDA device memory (read-only)
+ */
+#ifndef USTATS_B200_H
+#define USTATS_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define US_API __attribute__((visibility("default")))
+#else
+#define US_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Config (proj/include/ustats/config.hpp:17-44) plus the device section. */
+typedef struct us_config {
+    uint64_t memory_cap_entries; /* 0 = reference default 2^31 */
+    int32_t threads;             /* host threads for tensorization (0 = hw) */
+    int32_t strategy;            /* OrderStrategy: 0 Auto, 1 MinDegree, 2 MinFill, 3 Exhaustive */
+    int32_t exhaustive_index_bound; /* 0 = 12 */
+    int32_t exact_treewidth_bound;  /* 0 = 10 */
+    int32_t device;              /* CUDA ordinal, -1 = current */
+    int32_t rank;                /* term-sharding rank */
+    int32_t world_size;          /* term-sharding world size (1 = all terms here) */
+    int32_t flags;               /* bit0 share, bit1 fuse epilogues, bit2 symmetry, bit3 reorder;
+                                    US_FLAGS_DEFAULT = 0xF */
+} us_config;
+
+#define US_FLAGS_DEFAULT 0xF
+
+/* RunStats (engine.hpp:17-25) + device counters. */
+typedef struct us_stats {
+    double tensorize_seconds;       /* upload + on-device sparsify */
+    double contract_seconds;
+    uint64_t einsum_calls;
+    uint64_t partitions_enumerated;
+    uint64_t partitions_evaluated;
+    uint64_t multiply_adds;         /* reference-plan counting rules */
+    uint64_t peak_intermediate_entries;
+    uint64_t executed_gemm_macs;    /* DMMA multiply-adds issued */
+    uint64_t executed_stream_entries;
+    uint64_t gemm_launches;
+    uint64_t stream_launches;
+    uint64_t shared_hits;
+} us_stats;
+
+US_API const char* us_version(void);
+US_API const char* us_last_error(void);
+US_API void us_config_default(us_config* cfg);
+
+/* u_statistic after tensorize (engine.cpp:173-193; ustats_py.cpp:92-101). */
+US_API int us_u_statistic(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
+                   const double* const* factors, int64_t n, int32_t on_device,
+                   const us_config* cfg, double* u_out, us_stats* stats);
+
+/* Same evaluation, also returning every survivor in enumeration order:
+ * rgs_out[t*m + i], mu_out[t], v_out[t] (raw V; 0 when owned by another rank),
+ * owner_out[t] (rank). Capacity max_terms; *count receives the survivor count.
+ * lattice_combination per-term values (engine.cpp:67-73). */
+US_API int us_u_terms(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
+               const double* const* factors, int64_t n, int32_t on_device, const us_config* cfg,
+               int32_t max_terms, int32_t* count, int32_t* rgs_out, int64_t* mu_out, double* v_out,
+               int32_t* owner_out, double* u_out, us_stats* stats);
+
+/* u_statistic_unsparsified (engine.cpp:195-211): every lattice partition. */
+US_API int us_u_statistic_unsparsified(int32_t m, int32_t K, const int32_t* tuple_len,
+                                const int32_t* tuple_idx, const double* const* factors, int64_t n,
+                                int32_t on_device, const us_config* cfg, double* u_out,
+                                us_stats* stats);
+
+/* v_statistic (engine.cpp:138-151): one contraction of the raw signature. */
+US_API int us_v_statistic(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
+                   const double* const* factors, int64_t n, const us_config* cfg, double* v_out,
+                   us_stats* stats);
+
+/* restricted_v (engine.cpp:153-171): contraction of the induced signature of rgs. */
+US_API int us_restricted_v(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
+                    const double* const* factors, int64_t n, const int32_t* rgs,
+                    const us_config* cfg, double* v_out, us_stats* stats);
+
+/* einsum (einsum.hpp:41-43; ustats_py.cpp:73-90): tensors[k] has order
+ * tuple_len[k] over extent n (host memory); output tuple out_idx[0..out_len);
+ * `order` (nullable, order_len entries) an explicit elimination order over
+ * the canonical ids. out receives n^out_len entries. */
+US_API int us_einsum(int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
+              const double* const* tensors, int64_t n, int32_t out_len, const int32_t* out_idx,
+              const int32_t* order, int32_t order_len, const us_config* cfg, double* out,
+              uint64_t* multiply_adds, uint64_t* peak_entries, int32_t* steps);
+
+/* eliminate_index (einsum.hpp:49-52): result over the ascending union of the
+ * other ids, written to out (capacity out_cap entries) and out_tuple. */
+US_API int us_eliminate_index(int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
+                       const double* const* tensors, int64_t n, int32_t index,
+                       const us_config* cfg, double* out, uint64_t out_cap, int32_t* out_tuple,
+                       int32_t* out_tuple_len);
+
+/* The reference's combination of per-term values (engine.cpp:47-104):
+ * term_t = mu_t * v_t, pairwise tree per 512-term chunk, chunks summed in order.
+ * Pure host arithmetic; bit-identical to the reference given identical v. */
+US_API double us_combine_terms(int32_t count, const int64_t* mu, const double* v);
+
+/* Host-side lattice/planning helpers (no GPU needed). */
+US_API uint64_t us_bell_number(int32_t m);
+US_API int us_survivors(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
+                 int32_t max_terms, int32_t* count, int32_t* rgs_out, int64_t* mu_out,
+                 uint64_t* enumerated);
+US_API int us_optimize_order(int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
+                      int32_t strategy, int32_t* order_out, int32_t* index_count,
+                      int32_t* width_out);
+US_API int us_treewidth(int32_t n, int32_t edge_count, const int32_t* edges, int32_t* width_out,
+                 int32_t* order_out);
+
+/* Device plumbing. */
+US_API int us_device_count(int32_t* count);
+US_API int us_device_synchronize(int32_t device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* USTATS_B200_H */

@@ -1,0 +1,395 @@
+// extern "C" boundary (include/ustats_b200.h): decodes plain arguments into
+// the host API types, runs the engine, and maps exceptions to status codes.
+#include "../../include/ustats_b200.h"
+
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "device/executor.hpp"
+#include "ustats/ustats.hpp"
+
+namespace ustats::dev {
+double combine_terms(const std::vector<double>& terms);
+}
+
+namespace {
+
+thread_local std::string g_error;
+
+int fail_status(const std::exception& e) {
+    g_error = e.what();
+    if (const auto* ue = dynamic_cast<const ustats::Error*>(&e)) return 1 + static_cast<int>(ue->code());
+    return 1 + static_cast<int>(ustats::ErrorCode::InvalidArgument);
+}
+
+template <typename F>
+int guarded(F&& body) {
+    try {
+        body();
+        return 0;
+    } catch (const std::exception& e) {
+        return fail_status(e);
+    } catch (...) {
+        g_error = "unknown failure";
+        return 1 + static_cast<int>(ustats::ErrorCode::InvalidArgument);
+    }
+}
+
+ustats::Config to_config(const us_config* c) {
+    ustats::Config cfg;
+    if (!c) return cfg;
+    if (c->memory_cap_entries) cfg.memory_cap_entries = c->memory_cap_entries;
+    cfg.threads = c->threads;
+    if (c->strategy < 0 || c->strategy > 3)
+        ustats::fail(ustats::ErrorCode::InvalidArgument, "unknown order strategy");
+    cfg.strategy = static_cast<ustats::OrderStrategy>(c->strategy);
+    if (c->exhaustive_index_bound) cfg.exhaustive_index_bound = c->exhaustive_index_bound;
+    if (c->exact_treewidth_bound) cfg.exact_treewidth_bound = c->exact_treewidth_bound;
+    cfg.device.device = c->device;
+    cfg.device.rank = c->rank;
+    cfg.device.world_size = c->world_size < 1 ? 1 : c->world_size;
+    if (cfg.device.rank < 0 || cfg.device.rank >= cfg.device.world_size)
+        ustats::fail(ustats::ErrorCode::InvalidArgument, "rank outside [0, world_size)");
+    cfg.device.share_subexpressions = c->flags & 1;
+    cfg.device.fuse_epilogues = c->flags & 2;
+    cfg.device.exploit_symmetry = c->flags & 4;
+    cfg.device.reorder_for_sharing = c->flags & 8;
+    return cfg;
+}
+
+std::vector<ustats::IndexTuple> decode(int32_t K, const int32_t* len, const int32_t* idx) {
+    if (K < 1) ustats::fail(ustats::ErrorCode::InvalidArgument, "need at least one component");
+    std::vector<ustats::IndexTuple> sig;
+    int off = 0;
+    for (int k = 0; k < K; ++k) {
+        if (len[k] < 0) ustats::fail(ustats::ErrorCode::InvalidArgument, "negative tuple length");
+        sig.emplace_back(idx + off, idx + off + len[k]);
+        off += len[k];
+    }
+    return sig;
+}
+
+// MDKernel::validate (kernel.cpp:10-37) on the 0-based encoding.
+void validate_signature(int m, const std::vector<ustats::IndexTuple>& sig) {
+    if (m < 1) ustats::fail(ustats::ErrorCode::InvalidArgument, "kernel arity must be >= 1");
+    std::vector<char> covered(static_cast<std::size_t>(m), 0);
+    for (const auto& t : sig) {
+        if (t.empty()) ustats::fail(ustats::ErrorCode::InvalidArgument, "signature tuples must be non-empty");
+        std::vector<char> here(static_cast<std::size_t>(m), 0);
+        for (int s : t) {
+            if (s < 0 || s >= m)
+                ustats::fail(ustats::ErrorCode::InvalidArgument,
+                             "signature slot " + std::to_string(s + 1) + " outside 1.." + std::to_string(m));
+            if (here[static_cast<std::size_t>(s)])
+                ustats::fail(ustats::ErrorCode::InvalidArgument,
+                             "signature slot " + std::to_string(s + 1) + " repeated within one tuple");
+            here[static_cast<std::size_t>(s)] = covered[static_cast<std::size_t>(s)] = 1;
+        }
+    }
+    for (int s = 0; s < m; ++s)
+        if (!covered[static_cast<std::size_t>(s)])
+            ustats::fail(ustats::ErrorCode::InvalidArgument,
+                         "argument slot " + std::to_string(s + 1) + " appears in no signature tuple");
+}
+
+void export_stats(const ustats::RunStats& rs, us_stats* s) {
+    if (!s) return;
+    s->tensorize_seconds = rs.tensorize_seconds;
+    s->contract_seconds = rs.contract_seconds;
+    s->einsum_calls = rs.einsum_calls;
+    s->partitions_enumerated = rs.partitions_enumerated;
+    s->partitions_evaluated = rs.partitions_evaluated;
+    s->multiply_adds = rs.multiply_adds;
+    s->peak_intermediate_entries = rs.peak_intermediate_entries;
+    s->executed_gemm_macs = rs.executed_gemm_macs;
+    s->executed_stream_entries = rs.executed_stream_entries;
+    s->gemm_launches = rs.gemm_launches;
+    s->stream_launches = rs.stream_launches;
+    s->shared_hits = rs.shared_hits;
+}
+
+void export_dev(const ustats::dev::StatisticResult& r, int rank, us_stats* s) {
+    if (!s) return;
+    ustats::RunStats rs;
+    rs.tensorize_seconds = r.upload_seconds;
+    rs.contract_seconds = r.contract_seconds;
+    std::uint64_t mine = 0;
+    for (int o : r.owner) mine += o == rank;
+    rs.einsum_calls = mine;
+    rs.partitions_enumerated = r.enumerated;
+    rs.partitions_evaluated = mine;
+    rs.multiply_adds = r.stats.ref_madds;
+    rs.peak_intermediate_entries = r.stats.ref_peak;
+    rs.executed_gemm_macs = r.stats.gemm_macs;
+    rs.executed_stream_entries = r.stats.stream_entries;
+    rs.gemm_launches = r.stats.gemm_launches;
+    rs.stream_launches = r.stats.stream_launches;
+    rs.shared_hits = r.stats.shared_hits;
+    export_stats(rs, s);
+}
+
+ustats::dev::StatisticResult run_lattice(int32_t m, int32_t K, const int32_t* tuple_len,
+                                         const int32_t* tuple_idx, const double* const* factors, int64_t n,
+                                         int32_t on_device, const us_config* cfg,
+                                         ustats::dev::LatticeMode mode) {
+    ustats::Config config = to_config(cfg);
+    auto sig = decode(K, tuple_len, tuple_idx);
+    validate_signature(m, sig);
+    if (n < 1) ustats::fail(ustats::ErrorCode::InvalidArgument, "sample is empty");
+    if (n < m)
+        ustats::fail(ustats::ErrorCode::SampleTooSmall,
+                     "need at least " + std::to_string(m) + " observations, have " + std::to_string(n));
+    std::vector<const double*> ptrs(factors, factors + K);
+    return ustats::dev::lattice_statistic(ptrs, on_device != 0, sig, m, n, mode, config);
+}
+
+std::vector<ustats::DenseTensor> host_tensors(const std::vector<ustats::IndexTuple>& sig,
+                                              const double* const* data, int64_t n,
+                                              const ustats::Config& config) {
+    std::vector<ustats::DenseTensor> ts;
+    for (std::size_t k = 0; k < sig.size(); ++k) {
+        ustats::DenseTensor t(static_cast<int>(sig[k].size()), static_cast<int>(n), config);
+        std::memcpy(t.data.data(), data[k], t.data.size() * sizeof(double));
+        ts.push_back(std::move(t));
+    }
+    return ts;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* us_version(void) { return "ustats_b200 0.1 (sm_100a)"; }
+const char* us_last_error(void) { return g_error.c_str(); }
+
+void us_config_default(us_config* cfg) {
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->device = -1;
+    cfg->world_size = 1;
+    cfg->flags = US_FLAGS_DEFAULT;
+}
+
+int us_u_statistic(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
+                   const double* const* factors, int64_t n, int32_t on_device, const us_config* cfg,
+                   double* u_out, us_stats* stats) {
+    return guarded([&] {
+        auto r = run_lattice(m, K, tuple_len, tuple_idx, factors, n, on_device, cfg,
+                             ustats::dev::LatticeMode::Sparsified);
+        *u_out = r.value;
+        export_dev(r, cfg ? cfg->rank : 0, stats);
+    });
+}
+
+int us_u_terms(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
+               const double* const* factors, int64_t n, int32_t on_device, const us_config* cfg,
+               int32_t max_terms, int32_t* count, int32_t* rgs_out, int64_t* mu_out, double* v_out,
+               int32_t* owner_out, double* u_out, us_stats* stats) {
+    return guarded([&] {
+        auto r = run_lattice(m, K, tuple_len, tuple_idx, factors, n, on_device, cfg,
+                             ustats::dev::LatticeMode::Sparsified);
+        const int T = static_cast<int>(r.v.size());
+        *count = T;
+        if (T > max_terms) ustats::fail(ustats::ErrorCode::TooManyTerms, "term buffer too small");
+        for (int t = 0; t < T; ++t) {
+            for (int i = 0; i < m; ++i) rgs_out[t * m + i] = r.rgs[static_cast<std::size_t>(t)][static_cast<std::size_t>(i)];
+            mu_out[t] = r.mu[static_cast<std::size_t>(t)];
+            v_out[t] = r.v[static_cast<std::size_t>(t)];
+            if (owner_out) owner_out[t] = r.owner[static_cast<std::size_t>(t)];
+        }
+        if (u_out) *u_out = r.value;
+        export_dev(r, cfg ? cfg->rank : 0, stats);
+    });
+}
+
+int us_u_statistic_unsparsified(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
+                                const double* const* factors, int64_t n, int32_t on_device,
+                                const us_config* cfg, double* u_out, us_stats* stats) {
+    return guarded([&] {
+        auto r = run_lattice(m, K, tuple_len, tuple_idx, factors, n, on_device, cfg,
+                             ustats::dev::LatticeMode::Unsparsified);
+        *u_out = r.value;
+        export_dev(r, cfg ? cfg->rank : 0, stats);
+    });
+}
+
+int us_v_statistic(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
+                   const double* const* factors, int64_t n, const us_config* cfg, double* v_out,
+                   us_stats* stats) {
+    return guarded([&] {
+        ustats::Config config = to_config(cfg);
+        auto sig = decode(K, tuple_len, tuple_idx);
+        validate_signature(m, sig);
+        if (n < 1) ustats::fail(ustats::ErrorCode::InvalidArgument, "sample is empty");
+        auto ts = host_tensors(sig, factors, n, config);
+        ustats::EinsumNotation notation(sig);
+        ustats::ExecStats es;
+        ustats::RunStats rs;
+        *v_out = ustats::einsum(ts, notation, config, nullptr, &es).scalar();
+        rs.einsum_calls = 1;
+        rs.multiply_adds = es.multiply_adds;
+        rs.peak_intermediate_entries = es.peak_intermediate_entries;
+        export_stats(rs, stats);
+    });
+}
+
+int us_restricted_v(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
+                    const double* const* factors, int64_t n, const int32_t* rgs, const us_config* cfg,
+                    double* v_out, us_stats* stats) {
+    return guarded([&] {
+        ustats::Config config = to_config(cfg);
+        auto sig = decode(K, tuple_len, tuple_idx);
+        validate_signature(m, sig);
+        ustats::SetPartition part(std::vector<int>(rgs, rgs + m));
+        auto ts = host_tensors(sig, factors, n, config);
+        ustats::EinsumNotation notation(ustats::induced_signature(sig, part));
+        ustats::ExecStats es;
+        *v_out = ustats::einsum(ts, notation, config, nullptr, &es).scalar();
+        ustats::RunStats rs;
+        rs.einsum_calls = 1;
+        rs.multiply_adds = es.multiply_adds;
+        rs.peak_intermediate_entries = es.peak_intermediate_entries;
+        export_stats(rs, stats);
+    });
+}
+
+int us_einsum(int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx, const double* const* tensors,
+              int64_t n, int32_t out_len, const int32_t* out_idx, const int32_t* order, int32_t order_len,
+              const us_config* cfg, double* out, uint64_t* multiply_adds, uint64_t* peak_entries,
+              int32_t* steps) {
+    return guarded([&] {
+        ustats::Config config = to_config(cfg);
+        if (K < 1) ustats::fail(ustats::ErrorCode::InvalidNotation, "a notation needs at least one input tuple");
+        std::vector<ustats::IndexTuple> raw;
+        int off = 0;
+        for (int k = 0; k < K; ++k) {
+            raw.emplace_back(tuple_idx + off, tuple_idx + off + tuple_len[k]);
+            off += tuple_len[k];
+        }
+        ustats::EinsumNotation notation =
+            ustats::validate_notation(raw, ustats::IndexTuple(out_idx, out_idx + out_len));
+        std::vector<ustats::DenseTensor> ts;
+        for (int k = 0; k < K; ++k) {
+            ustats::DenseTensor t(tuple_len[k], static_cast<int>(n), config);
+            std::memcpy(t.data.data(), tensors[k], t.data.size() * sizeof(double));
+            ts.push_back(std::move(t));
+        }
+        ustats::EliminationOrder eo;
+        const ustats::EliminationOrder* eop = nullptr;
+        if (order) {
+            eo.order.assign(order, order + order_len);
+            eop = &eo;
+        }
+        ustats::ExecStats es;
+        ustats::DenseTensor r = ustats::einsum(ts, notation, config, eop, &es);
+        std::memcpy(out, r.data.data(), r.data.size() * sizeof(double));
+        if (multiply_adds) *multiply_adds = es.multiply_adds;
+        if (peak_entries) *peak_entries = es.peak_intermediate_entries;
+        if (steps) *steps = es.steps;
+    });
+}
+
+int us_eliminate_index(int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
+                       const double* const* tensors, int64_t n, int32_t index, const us_config* cfg,
+                       double* out, uint64_t out_cap, int32_t* out_tuple, int32_t* out_tuple_len) {
+    return guarded([&] {
+        ustats::Config config = to_config(cfg);
+        if (K < 1) ustats::fail(ustats::ErrorCode::ShapeMismatch, "need one tuple per tensor");
+        std::vector<ustats::IndexTuple> tuples;
+        std::vector<ustats::DenseTensor> ts;
+        int off = 0;
+        for (int k = 0; k < K; ++k) {
+            tuples.emplace_back(tuple_idx + off, tuple_idx + off + tuple_len[k]);
+            off += tuple_len[k];
+            ustats::DenseTensor t(tuple_len[k], static_cast<int>(n), config);
+            std::memcpy(t.data.data(), tensors[k], t.data.size() * sizeof(double));
+            ts.push_back(std::move(t));
+        }
+        auto [r, tuple] = ustats::eliminate_index(ts, tuples, index, config);
+        if (r.data.size() > out_cap) ustats::fail(ustats::ErrorCode::InvalidArgument, "output buffer too small");
+        std::memcpy(out, r.data.data(), r.data.size() * sizeof(double));
+        for (std::size_t i = 0; i < tuple.size(); ++i) out_tuple[i] = tuple[i];
+        *out_tuple_len = static_cast<int32_t>(tuple.size());
+    });
+}
+
+double us_combine_terms(int32_t count, const int64_t* mu, const double* v) {
+    std::vector<double> terms(static_cast<std::size_t>(count < 0 ? 0 : count));
+    for (std::size_t t = 0; t < terms.size(); ++t) terms[t] = static_cast<double>(mu[t]) * v[t];
+    return ustats::dev::combine_terms(terms);
+}
+
+uint64_t us_bell_number(int32_t m) {
+    try {
+        return ustats::bell_number(m);
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return 0;
+    }
+}
+
+int us_survivors(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx, int32_t max_terms,
+                 int32_t* count, int32_t* rgs_out, int64_t* mu_out, uint64_t* enumerated) {
+    return guarded([&] {
+        auto sig = decode(K, tuple_len, tuple_idx);
+        ustats::SparsifiedPartitionStream s(m, sig);
+        ustats::SetPartition p;
+        int c = 0;
+        while (s.next(p)) {
+            if (c >= max_terms) ustats::fail(ustats::ErrorCode::TooManyTerms, "term buffer too small");
+            for (int i = 0; i < m; ++i) rgs_out[c * m + i] = p.rgs()[static_cast<std::size_t>(i)];
+            mu_out[c] = ustats::mobius_coefficient(p);
+            ++c;
+        }
+        *count = c;
+        if (enumerated) *enumerated = s.enumerated();
+    });
+}
+
+int us_optimize_order(int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx, int32_t strategy,
+                      int32_t* order_out, int32_t* index_count, int32_t* width_out) {
+    return guarded([&] {
+        std::vector<ustats::IndexTuple> raw;
+        int off = 0;
+        for (int k = 0; k < K; ++k) {
+            raw.emplace_back(tuple_idx + off, tuple_idx + off + tuple_len[k]);
+            off += tuple_len[k];
+        }
+        ustats::EinsumNotation notation(raw);
+        if (strategy < 0 || strategy > 3) ustats::fail(ustats::ErrorCode::InvalidArgument, "unknown strategy");
+        auto o = ustats::optimize_order(notation, 2, static_cast<ustats::OrderStrategy>(strategy));
+        for (std::size_t i = 0; i < o.order.size(); ++i) order_out[i] = o.order[i];
+        *index_count = notation.index_count;
+        *width_out = o.predicted_width;
+    });
+}
+
+int us_treewidth(int32_t n, int32_t edge_count, const int32_t* edges, int32_t* width_out, int32_t* order_out) {
+    return guarded([&] {
+        std::vector<std::pair<int, int>> es;
+        for (int i = 0; i < edge_count; ++i) es.emplace_back(edges[2 * i], edges[2 * i + 1]);
+        auto g = ustats::SimpleGraph::from_edges(n, es);
+        ustats::Config c;
+        c.exact_treewidth_bound = std::max(c.exact_treewidth_bound, g.vertex_count());
+        auto r = ustats::treewidth_exact(g, c);
+        *width_out = r.width;
+        for (std::size_t i = 0; i < r.order.size(); ++i) order_out[i] = r.order[i];
+    });
+}
+
+int us_device_count(int32_t* count) {
+    return guarded([&] {
+        int c = 0;
+        ustats::dev::check_cuda(cudaGetDeviceCount(&c), "cudaGetDeviceCount");
+        *count = c;
+    });
+}
+
+int us_device_synchronize(int32_t device) {
+    return guarded([&] { ustats::dev::Runtime::get(device).sync(); });
+}
+
+}  // extern "C"

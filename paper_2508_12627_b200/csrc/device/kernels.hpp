@@ -1,0 +1,87 @@
+// Argument blocks and launchers of the sm_100a kernels. Shared by the .cu
+// kernel files and the host-side executor (plain C++: no CUDA types beyond
+// cudaStream_t leak into the planner).
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace ustats::dev {
+
+constexpr int kMaxDims = 12;         // iteration dims of one stream (bandwidth) kernel
+constexpr int kMaxFactors = 8;       // factors multiplied inside one kernel
+constexpr int kMaxGemmFactors = 6;   // factors per GEMM operand (prologue product)
+constexpr int kMaxRowDims = 3;       // ids folded into one GEMM row / column index
+
+// Broadcast-product-reduce ("stream") kernel:
+//   out[o] = scale * sum_{s} prod_f F_f[ sum_d digit_d * stride[f][d] ]
+// iteration dims [0, n_out) are the output (row-major, last fastest),
+// [n_out, n_out + n_sum) are summed (last fastest). Every dim has extent n.
+struct StreamArgs {
+    int nf = 0;
+    int n_out = 0;
+    int n_sum = 0;
+    long long n = 1;
+    const double* ptr[kMaxFactors] = {};
+    long long stride[kMaxFactors][kMaxDims] = {};
+    double* out = nullptr;
+    double scale = 1.0;
+};
+
+// One GEMM operand: value(r, k) = prod_f ptr_f[ off_f(r) + kstride_f * k ]
+// with off_f(r) = sum over the nr row digits of r (base n, row-major) times rstride.
+struct GemmSide {
+    int nf = 0;
+    int nr = 1;
+    const double* ptr[kMaxGemmFactors] = {};
+    long long rstride[kMaxGemmFactors][kMaxRowDims] = {};
+    long long kstride[kMaxGemmFactors] = {};
+};
+
+enum EpilogueMode : int {
+    kEpiStore = 0,      // out[r * cols + c] = scale * C * W
+    kEpiSumAll = 1,     // partial[tile] = sum_{r,c} C * W      (then finalize)
+    kEpiSumCols = 2,    // partial[tile_n][r] = sum_c C * W     (then finalize -> out[r])
+    kEpiSumRows = 3,    // partial[tile_m][c] = sum_r C * W     (then finalize -> out[c])
+};
+
+// Epilogue factors W(r, c) = prod_g ptr_g[ roff_g(r) + coff_g(c) ].
+struct EpilogueSide {
+    int nf = 0;
+    const double* ptr[kMaxGemmFactors] = {};
+    long long rstride[kMaxGemmFactors][kMaxRowDims] = {};
+    long long cstride[kMaxGemmFactors][kMaxRowDims] = {};
+};
+
+struct GemmArgs {
+    GemmSide a;          // rows x k
+    GemmSide b;          // cols x k (described by its column digits)
+    EpilogueSide w;
+    long long n = 1;     // extent of every id, including k
+    long long rows = 0;
+    long long cols = 0;
+    int mode = kEpiStore;
+    double* out = nullptr;      // store target, or finalize target
+    double* partial = nullptr;  // scratch for reduce modes
+    double scale = 1.0;
+    int a_kmajor = 1;           // loader orientation hints (coalescing)
+    int b_kmajor = 1;
+    int symmetric_out = 0;      // rows==cols and C symmetric: compute upper tiles only
+};
+
+// ------------------------------------------------------------- launchers
+void launch_stream(const StreamArgs& a, double* scratch, std::size_t scratch_entries,
+                   int sm_count, cudaStream_t s);
+std::size_t stream_scratch_entries(const StreamArgs& a, int sm_count);
+
+void launch_gemm(const GemmArgs& a, cudaStream_t s);
+std::size_t gemm_partial_entries(const GemmArgs& a);
+
+// Zero every entry of an order-`order` tensor whose multi-index repeats a
+// coordinate (tensor.cpp:54-76), in place.
+void launch_sparsify(double* data, int order, long long n, cudaStream_t s);
+// flag[0] = 0 if the n x n matrix is bitwise symmetric, else 1.
+void launch_symmetry_check(const double* data, long long n, int* flag, cudaStream_t s);
+
+}  // namespace ustats::dev

@@ -1,0 +1,334 @@
+// Bandwidth-bound kernels of the V-term executor: the fused
+// broadcast-Hadamard-reduce ("stream") kernel that replaces the reference's
+// fold_into / marginalize / generic_step / assembly walkers
+// (proj/src/einsum.cpp:134-178, 263-301, 466-485), plus on-device
+// sparsification (tensor.cpp:54-76) and a bitwise symmetry probe.
+//
+// Every variant iterates (row, inner): `inner` is one iteration dim mapped to
+// consecutive threads (chosen by the planner to be the unit-stride dim of the
+// dominant factors, so loads coalesce); `row` enumerates the other dims.
+// Reductions are fixed-order (per-thread sequential, then a fixed shuffle /
+// shared-memory tree, then an in-order pass over block partials): results are
+// bit-reproducible run to run.
+#include <cstdio>
+
+#include "kernels.hpp"
+
+namespace ustats::dev {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+struct Digits {
+    // Decomposes `flat` over `count` dims (row-major, base n) and accumulates
+    // per-factor offsets for dims [first, first+count).
+    __device__ static void offsets(const StreamArgs& a, unsigned long long flat, int first,
+                                   int count, long long* off) {
+        for (int d = first + count - 1; d >= first; --d) {
+            const unsigned long long q = flat / static_cast<unsigned long long>(a.n);
+            const long long digit = static_cast<long long>(flat - q * static_cast<unsigned long long>(a.n));
+            flat = q;
+#pragma unroll
+            for (int f = 0; f < kMaxFactors; ++f)
+                if (f < a.nf) off[f] += digit * a.stride[f][d];
+        }
+    }
+};
+
+__device__ __forceinline__ double product_at(const StreamArgs& a, const long long* off,
+                                             long long i, int inner) {
+    double v = 1.0;
+#pragma unroll
+    for (int f = 0; f < kMaxFactors; ++f)
+        if (f < a.nf) v *= __ldg(a.ptr[f] + off[f] + i * a.stride[f][inner]);
+    return v;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ double block_sum(double v, double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (warp == 0) {
+        t = lane < (blockDim.x >> 5) ? red[lane] : 0.0;
+        t = warp_sum(t);
+    }
+    __syncthreads();
+    return t;  // valid in thread 0
+}
+
+// Elementwise: n_sum == 0. Dims [0, n_out); inner = last output dim.
+__global__ void stream_elementwise(StreamArgs a, unsigned long long rows) {
+    const int inner = a.n_out - 1;
+    for (unsigned long long row = blockIdx.y; row < rows; row += gridDim.y) {
+        long long off[kMaxFactors] = {};
+        Digits::offsets(a, row, 0, a.n_out - 1, off);
+        for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < a.n;
+             i += static_cast<long long>(gridDim.x) * blockDim.x)
+            a.out[row * a.n + i] = a.scale * product_at(a, off, i, inner);
+    }
+}
+
+// Full reduction: n_out == 0. `inner` chosen by the host (its dims order puts
+// it last). Block b reduces rows [b*rows/B, (b+1)*rows/B).
+__global__ void stream_reduce_all(StreamArgs a, unsigned long long rows, double* partial) {
+    __shared__ double red[32];
+    const int D = a.n_sum;
+    const int inner = D - 1;
+    const unsigned long long B = gridDim.x;
+    const unsigned long long lo = rows * blockIdx.x / B, hi = rows * (blockIdx.x + 1) / B;
+    double acc = 0.0;
+    for (unsigned long long row = lo; row < hi; ++row) {
+        long long off[kMaxFactors] = {};
+        Digits::offsets(a, row, 0, D - 1, off);
+        for (long long i = threadIdx.x; i < a.n; i += blockDim.x) acc += product_at(a, off, i, inner);
+    }
+    const double t = block_sum(acc, red);
+    if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+// Summed-dim-fast reduction: one warp per output; lanes walk the innermost
+// summed dim (unit stride in the dominant factors), the other summed dims
+// are the "rows".
+__global__ void stream_reduce_warp(StreamArgs a, unsigned long long outputs,
+                                   unsigned long long srows) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long o =
+        blockIdx.x * static_cast<unsigned long long>(blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (o >= outputs) return;
+    const int inner = a.n_out + a.n_sum - 1;
+    long long base[kMaxFactors] = {};
+    Digits::offsets(a, o, 0, a.n_out, base);
+    double acc = 0.0;
+    for (unsigned long long sr = 0; sr < srows; ++sr) {
+        long long off[kMaxFactors];
+#pragma unroll
+        for (int f = 0; f < kMaxFactors; ++f) off[f] = base[f];
+        Digits::offsets(a, sr, a.n_out, a.n_sum - 1, off);
+        for (long long i = lane; i < a.n; i += 32) acc += product_at(a, off, i, inner);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) a.out[o] = a.scale * acc;
+}
+
+// Output-dim-fast reduction: one thread per output (consecutive threads along
+// the innermost output dim), sequential sum over a slice of the summed space.
+// gridDim.y slices split the summed space for parallelism; slice partials go
+// to partial[slice * outputs + o] and are added in slice order afterwards.
+__global__ void stream_reduce_thread(StreamArgs a, unsigned long long outputs,
+                                     unsigned long long sflat, double* partial) {
+    const unsigned long long o = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (o >= outputs) return;
+    const unsigned long long S = gridDim.y;
+    const unsigned long long lo = sflat * blockIdx.y / S, hi = sflat * (blockIdx.y + 1) / S;
+    long long base[kMaxFactors] = {};
+    Digits::offsets(a, o, 0, a.n_out, base);
+    // odometer over the summed dims, starting at `lo`
+    const int first = a.n_out, D = a.n_sum;
+    long long digit[kMaxDims];
+    {
+        unsigned long long flat = lo;
+        for (int d = D - 1; d >= 0; --d) {
+            digit[d] = static_cast<long long>(flat % static_cast<unsigned long long>(a.n));
+            flat /= static_cast<unsigned long long>(a.n);
+        }
+    }
+    long long off[kMaxFactors];
+#pragma unroll
+    for (int f = 0; f < kMaxFactors; ++f) {
+        off[f] = base[f];
+        if (f < a.nf)
+            for (int d = 0; d < D; ++d) off[f] += digit[d] * a.stride[f][first + d];
+    }
+    double acc = 0.0;
+    for (unsigned long long s = lo; s < hi; ++s) {
+        double v = 1.0;
+#pragma unroll
+        for (int f = 0; f < kMaxFactors; ++f)
+            if (f < a.nf) v *= __ldg(a.ptr[f] + off[f]);
+        acc += v;
+        for (int d = D - 1; d >= 0; --d) {
+            if (++digit[d] < a.n) {
+#pragma unroll
+                for (int f = 0; f < kMaxFactors; ++f)
+                    if (f < a.nf) off[f] += a.stride[f][first + d];
+                break;
+            }
+            digit[d] = 0;
+#pragma unroll
+            for (int f = 0; f < kMaxFactors; ++f)
+                if (f < a.nf) off[f] -= (a.n - 1) * a.stride[f][first + d];
+        }
+    }
+    if (S == 1)
+        a.out[o] = a.scale * acc;
+    else
+        partial[blockIdx.y * outputs + o] = acc;
+}
+
+// out[o] = scale * sum_{p < P} partial[p * outputs + o], in p order.
+__global__ void finalize_columns(const double* partial, unsigned long long P,
+                                 unsigned long long outputs, double scale, double* out) {
+    const unsigned long long o = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (o >= outputs) return;
+    double acc = 0.0;
+    for (unsigned long long p = 0; p < P; ++p) acc += partial[p * outputs + o];
+    out[o] = scale * acc;
+}
+
+// out[0] = scale * sum of P partials: fixed strided split + fixed tree.
+__global__ void finalize_scalar(const double* partial, unsigned long long P, double scale,
+                                double* out) {
+    __shared__ double red[32];
+    double acc = 0.0;
+    for (unsigned long long p = threadIdx.x; p < P; p += blockDim.x) acc += partial[p];
+    const double t = block_sum(acc, red);
+    if (threadIdx.x == 0) out[0] = scale * t;
+}
+
+unsigned long long ipow(long long n, int e) {
+    unsigned long long v = 1;
+    while (e-- > 0) v *= static_cast<unsigned long long>(n);
+    return v;
+}
+
+int blocks_for_all(unsigned long long rows, long long n, int sm_count) {
+    // enough blocks to fill the GPU ~4x, never more than the rows, and each
+    // block should stream at least ~64 KiB
+    const unsigned long long work = rows * static_cast<unsigned long long>(n);
+    unsigned long long want = static_cast<unsigned long long>(sm_count) * 8;
+    const unsigned long long cap_by_work = work / 8192 + 1;
+    if (want > cap_by_work) want = cap_by_work;
+    if (want > rows) want = rows;
+    return static_cast<int>(want < 1 ? 1 : want);
+}
+
+}  // namespace
+
+std::size_t stream_scratch_entries(const StreamArgs& a, int sm_count) {
+    if (a.n_sum == 0) return 0;
+    if (a.n_out == 0) return static_cast<std::size_t>(blocks_for_all(ipow(a.n, a.n_sum - 1), a.n, sm_count));
+    const unsigned long long outputs = ipow(a.n, a.n_out);
+    const unsigned long long sflat = ipow(a.n, a.n_sum);
+    const unsigned long long threads_wanted = static_cast<unsigned long long>(sm_count) * 2048;
+    unsigned long long slices = 1;
+    while (outputs * slices < threads_wanted && slices * 2 <= sflat / 64 && slices < 1024) slices *= 2;
+    return slices > 1 ? static_cast<std::size_t>(slices * outputs) : 0;
+}
+
+// Host chooses the variant from the factor strides:
+//  - n_sum == 0          -> elementwise
+//  - n_out == 0          -> two-stage full reduction
+//  - innermost summed dim has the unit strides -> warp per output
+//  - otherwise           -> thread per output (+ summed-space slicing)
+void launch_stream(const StreamArgs& a, double* scratch, std::size_t scratch_entries,
+                   int sm_count, cudaStream_t s) {
+    if (a.n_sum == 0) {
+        const unsigned long long rows = ipow(a.n, a.n_out - 1);
+        const unsigned gx = static_cast<unsigned>((a.n + kThreads - 1) / kThreads);
+        unsigned long long gy = rows;
+        if (gy > 65535) gy = 65535;
+        stream_elementwise<<<dim3(gx, static_cast<unsigned>(gy)), kThreads, 0, s>>>(a, rows);
+        return;
+    }
+    if (a.n_out == 0) {
+        const unsigned long long rows = ipow(a.n, a.n_sum - 1);
+        const int blocks = blocks_for_all(rows, a.n, sm_count);
+        stream_reduce_all<<<blocks, kThreads, 0, s>>>(a, rows, scratch);
+        finalize_scalar<<<1, 1024, 0, s>>>(scratch, static_cast<unsigned long long>(blocks), a.scale, a.out);
+        return;
+    }
+    const unsigned long long outputs = ipow(a.n, a.n_out);
+    const int last = a.n_out + a.n_sum - 1;
+    const int out_last = a.n_out - 1;
+    int unit_sum = 0, unit_out = 0;
+    for (int f = 0; f < a.nf; ++f) {
+        unit_sum += a.stride[f][last] == 1;
+        unit_out += a.stride[f][out_last] == 1;
+    }
+    if (unit_sum > unit_out || (unit_sum == unit_out && outputs < static_cast<unsigned long long>(sm_count) * 256)) {
+        const unsigned long long srows = ipow(a.n, a.n_sum - 1);
+        const unsigned long long blocks = (outputs + (kThreads / 32) - 1) / (kThreads / 32);
+        stream_reduce_warp<<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(a, outputs, srows);
+        return;
+    }
+    const unsigned long long sflat = ipow(a.n, a.n_sum);
+    unsigned long long slices = 1;
+    if (scratch_entries >= 2 * outputs) {
+        slices = scratch_entries / outputs;
+        if (slices > 1024) slices = 1024;
+    }
+    const unsigned gx = static_cast<unsigned>((outputs + kThreads - 1) / kThreads);
+    stream_reduce_thread<<<dim3(gx, static_cast<unsigned>(slices)), kThreads, 0, s>>>(a, outputs, sflat,
+                                                                                   scratch);
+    if (slices > 1)
+        finalize_columns<<<gx, kThreads, 0, s>>>(scratch, slices, outputs, a.scale, a.out);
+}
+
+// ---------------------------------------------------------------- sparsify
+namespace {
+__global__ void zero_diagonal(double* d, long long n) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        d[i * n + i] = 0.0;
+}
+
+__global__ void zero_repeated(double* d, int order, long long n, unsigned long long total) {
+    for (unsigned long long flat = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+         flat < total; flat += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+        long long dig[16];
+        unsigned long long r = flat;
+        for (int k = order - 1; k >= 0; --k) {
+            dig[k] = static_cast<long long>(r % static_cast<unsigned long long>(n));
+            r /= static_cast<unsigned long long>(n);
+        }
+        bool rep = false;
+        for (int x = 0; x < order && !rep; ++x)
+            for (int y = x + 1; y < order && !rep; ++y) rep = dig[x] == dig[y];
+        if (rep) d[flat] = 0.0;
+    }
+}
+
+__global__ void asymmetry_probe(const double* d, long long n, int* flag) {
+    // flag starts at 0; any mismatching pair sets it (benign race: all writers store 1)
+    const long long total = n * n;
+    for (long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; f < total;
+         f += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = f / n, j = f - i * n;
+        if (j > i) {
+            const unsigned long long x = __double_as_longlong(d[i * n + j]);
+            const unsigned long long y = __double_as_longlong(d[j * n + i]);
+            if (x != y) *flag = 1;
+        }
+    }
+}
+}  // namespace
+
+void launch_sparsify(double* data, int order, long long n, cudaStream_t s) {
+    if (order < 2) return;
+    if (order == 2) {
+        zero_diagonal<<<static_cast<unsigned>((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, s>>>(data, n);
+        return;
+    }
+    const unsigned long long total = ipow(n, order);
+    unsigned long long blocks = (total + 255) / 256;
+    if (blocks > 148ull * 32) blocks = 148ull * 32;
+    zero_repeated<<<static_cast<unsigned>(blocks), 256, 0, s>>>(data, order, n, total);
+}
+
+void launch_symmetry_check(const double* data, long long n, int* flag, cudaStream_t s) {
+    cudaMemsetAsync(flag, 0, sizeof(int), s);
+    unsigned long long blocks = (static_cast<unsigned long long>(n) * n + 255) / 256;
+    if (blocks > 148ull * 16) blocks = 148ull * 16;
+    asymmetry_probe<<<static_cast<unsigned>(blocks), 256, 0, s>>>(data, n, flag);
+}
+
+}  // namespace ustats::dev

@@ -1,0 +1,36 @@
+// Engine knobs. The host fields mirror the reference Config
+// (proj/include/ustats/config.hpp:17-44) field for field; `device` is the
+// B200 section (which GPU, how the V-terms are shared across ranks, and which
+// plan rewrites are enabled).
+#pragma once
+
+#include <cstdint>
+
+namespace ustats {
+
+enum class OrderStrategy { Auto, GreedyMinDegree, GreedyMinFill, Exhaustive };
+
+struct DeviceConfig {
+    int device = -1;               ///< CUDA device ordinal; -1 = current device
+    int rank = 0;                  ///< this process's share of the V-terms (term sharding)
+    int world_size = 1;            ///< number of ranks the V-terms are spread over
+    bool share_subexpressions = true;  ///< hash-cons identical GEMMs/reductions across V-terms
+    bool fuse_epilogues = true;        ///< fold+marginalize consumers into GEMM epilogues
+    bool exploit_symmetry = true;      ///< detect bitwise-symmetric matrices, read either orientation
+    bool reorder_for_sharing = true;   ///< choose among equal-width orders to maximize sharing
+};
+
+struct Config {
+    std::uint64_t memory_cap_entries = std::uint64_t{1} << 31;
+    int threads = 0;
+    OrderStrategy strategy = OrderStrategy::Auto;
+    int exhaustive_index_bound = 12;
+    int exact_treewidth_bound = 10;
+    std::uint64_t brute_force_term_cap = 10'000'000;
+    bool strict_nonfinite = false;
+    DeviceConfig device;
+
+    int effective_threads() const;
+};
+
+}  // namespace ustats

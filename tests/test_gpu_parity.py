@@ -1,0 +1,212 @@
+"""Parity of the B200 engine with the reference algorithm (CUDA path vs oracle).
+
+Oracles: the numpy restatement (oracle/ustats_np.py) and, when present, the
+reference library compiled from its own sources (oracle/_ref). Tolerance is
+the north_star's: |U_gpu - U_ref| <= 1e-9 * max_pi |V_pi| (per-term values
+compared too).
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle import ref as REF
+from oracle import ustats_np as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+
+
+def oracle_terms(factors, sig, m):
+    if REF.available():
+        rgs, mu, v, _ = REF.u_terms(factors, sig, m)
+        return O.combine(mu, v), rgs, mu, v
+    u, rows = O.u_statistic(factors, sig, m)
+    return u, np.array([r[0] for r in rows]), np.array([r[1] for r in rows]), np.array([r[2] for r in rows])
+
+
+def check_u(engine, factors, sig, m, config=None):
+    u_ref, rgs, mu, v = oracle_terms(factors, sig, m)
+    got = engine.u_terms(factors, sig, m, config)
+    assert np.array_equal(got.rgs, rgs)
+    assert np.array_equal(got.mu, mu)
+    scale = max(np.max(np.abs(v)), 1e-300)
+    per_term = np.abs(got.v - v) / scale
+    assert per_term.max() <= TOL, (per_term, got.v, v)
+    assert abs(got.value - u_ref) <= TOL * scale, (got.value, u_ref)
+    return got, u_ref
+
+
+def test_prod2_golden(engine):
+    # test_engine.cpp:106-116 / test_smoke.py:43-46
+    data = np.array([[1.0], [2.0], [3.0]])
+    assert engine.u_statistic("prod2", data) == pytest.approx(22.0, rel=1e-12)
+    assert engine.v_statistic("prod2", data) == pytest.approx(36.0, rel=1e-12)
+
+
+@pytest.mark.parametrize("name,n", [("C1", 64), ("C1", 257), ("C2", 96), ("C2", 130), ("C3", 96),
+                                    ("C3", 129), ("C4", 24), ("C4", 33), ("C5", 96), ("C5", 130)])
+def test_configs_small(engine, name, n):
+    from paper_2508_12627_b200.workloads import generate
+    factors, sig, m, _ = generate(name, n)
+    check_u(engine, factors, sig, m)
+
+
+@pytest.mark.parametrize("name,n", [("C1", 2000), ("C2", 512), ("C3", 512), ("C4", 64), ("C5", 256)])
+def test_configs_medium(engine, name, n):
+    from paper_2508_12627_b200.workloads import generate
+    factors, sig, m, _ = generate(name, n)
+    check_u(engine, factors, sig, m)
+
+
+def random_kernel(m, rng):
+    # acceptance_main.cpp:92-125 shape: one or two covering tuples + up to two extras
+    slots = list(range(m))
+    rng.shuffle(slots)
+    cut = int(rng.integers(1, m + 1))
+    tuples = [slots[:cut]] + ([slots[cut:]] if cut < m else [])
+    for _ in range(int(rng.integers(0, 3))):
+        t = [int(rng.integers(0, m))]
+        if rng.integers(0, 3) > 0:
+            s = int(rng.integers(0, m))
+            if s != t[0]:
+                t.append(s)
+        tuples.append(t)
+    return tuples
+
+
+def test_random_kernels_vs_brute_force(engine):
+    # acceptance criterion 1: U == literal sum, m in {2,3,4}, n in [m, 8]
+    rng = np.random.default_rng(101)
+    for trial in range(60):
+        m = int(rng.integers(2, 5))
+        n = int(rng.integers(m, 9))
+        sig = random_kernel(m, rng)
+        factors = [rng.uniform(-1, 1, size=(n,) * len(t)) for t in sig]
+        want = O.u_brute_force(factors, sig, m)
+        got = engine.u_statistic_tensors(factors, sig, m)
+        assert abs(got - want) <= 1e-9 * max(1.0, abs(want)), (trial, sig, got, want)
+        unsp = engine.u_statistic_unsparsified_tensors(factors, sig, m)
+        assert abs(unsp - want) <= 1e-9 * max(1.0, abs(want)), (trial, sig, unsp, want)
+
+
+def test_v_statistic_and_restricted(engine):
+    rng = np.random.default_rng(404)
+    m, n = 4, 6
+    sig = [[0, 1], [1, 2], [2, 3], [0, 2]]
+    factors = [rng.uniform(-1, 1, size=(n, n)) for _ in sig]
+    v = engine.v_statistic_tensors(factors, sig, m)
+    want = O.contract(factors, sig)
+    assert abs(v - want) <= 1e-12 * max(1, abs(want))
+    for p in O.partitions(m):
+        got = engine.restricted_v_tensors(factors, sig, p, m)
+        want = O.contract(factors, O.induced(sig, p))
+        assert abs(got - want) <= 1e-11 * max(1, abs(want)), p
+
+
+def test_random_notations_vs_numpy(engine):
+    # test_einsum.cpp:120-157 / acceptance criterion 2
+    rng = np.random.default_rng(2024)
+    letters = "abcdefgh"
+    for trial in range(80):
+        k = int(rng.integers(1, 5))
+        n = int(rng.integers(2, 6))
+        inputs = [[int(rng.integers(0, 5)) for _ in range(int(rng.integers(1, 4)))] for _ in range(k)]
+        present = []
+        for t in inputs:
+            for i in t:
+                if i not in present:
+                    present.append(i)
+        rng.shuffle(present)
+        out = present[: int(rng.integers(0, min(2, len(present)) + 1))]
+        tensors = [rng.uniform(-1, 1, size=(n,) * len(t)) for t in inputs]
+        got = engine.einsum(tensors, inputs, out)
+        spec = ",".join("".join(letters[i] for i in t) for t in inputs) + "->" + "".join(letters[i] for i in out)
+        want = np.einsum(spec, *tensors)
+        assert np.allclose(got, want, rtol=1e-11, atol=1e-11), (trial, inputs, out)
+
+
+def test_every_order_same_value(engine):
+    # test_einsum.cpp:159-176
+    rng = np.random.default_rng(55)
+    n = 3
+    inputs = [[0, 1, 2], [2, 3], [3, 4], [4, 0]]
+    tensors = [rng.uniform(-1, 1, size=(n,) * len(t)) for t in inputs]
+    want = np.einsum("abc,cd,de,ea->b", *tensors)
+    for perm in itertools.permutations(range(5)):
+        got = engine.einsum(tensors, inputs, [1], order=list(perm))
+        assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
+
+
+def test_gemm_shapes_and_transposes(engine):
+    # exercises every DMMA loader orientation and ragged tile edges
+    rng = np.random.default_rng(7)
+    for n in (5, 127, 128, 129, 300):
+        a = rng.normal(size=(n, n))
+        b = rng.normal(size=(n, n))
+        for ins, out, spec in [([[0, 1], [1, 2]], [0, 2], "ij,jk->ik"), ([[1, 0], [1, 2]], [0, 2], "ji,jk->ik"),
+                               ([[0, 1], [2, 1]], [0, 2], "ij,kj->ik"), ([[1, 0], [2, 1]], [2, 0], "ji,kj->ki")]:
+            got = engine.einsum([a, b], ins, out)
+            assert np.allclose(got, np.einsum(spec, a, b), rtol=1e-12, atol=1e-10), (n, spec)
+
+
+def test_khatri_rao_step(engine):
+    # K=3 operands sharing only the eliminated index (generic_step, einsum.cpp:263-301)
+    rng = np.random.default_rng(21)
+    n = 9
+    a, b, c = (rng.uniform(-1, 1, size=(n, n)) for _ in range(3))
+    out, tup = engine.eliminate_index([a, b, c], [[0, 1], [0, 2], [0, 3]], 0)
+    assert tup == [1, 2, 3]
+    assert np.allclose(out, np.einsum("si,sj,sk->ijk", a, b, c), rtol=1e-12)
+
+
+def test_errors(engine):
+    from paper_2508_12627_b200 import UStatsError, Config
+    x = np.ones((3, 3))
+    with pytest.raises(UStatsError) as e:
+        engine.u_statistic_tensors([x, x, x], [[0, 1], [1, 2], [2, 3]], 4)
+    assert e.value.code == "SampleTooSmall"
+    a = np.ones((10, 10))
+    with pytest.raises(UStatsError) as e:
+        engine.einsum([a, a], [[0, 1], [1, 2]], [0, 2], config=Config(memory_cap_entries=50))
+    assert e.value.code == "MemoryCapExceeded"
+    with pytest.raises(UStatsError) as e:
+        engine.einsum([a, a], [[0, 1], [1, 2]], [0, 2], order=[0, 1])
+    assert e.value.code == "InvalidArgument"
+
+
+def test_nonfinite_propagates(engine):
+    x = np.array([np.nan, 1.0, 2.0])
+    assert np.isnan(engine.v_statistic_tensors([x, np.ones(3)], [[0], [1]], 2))
+
+
+def test_minimum_sample(engine):
+    rng = np.random.default_rng(3)
+    for m in (2, 3, 4):
+        sig = [[i, i + 1] for i in range(m - 1)]
+        A = rng.normal(size=(m, m))
+        check_u(engine, [A] * (m - 1), sig, m)
+
+
+def test_deterministic_bits(engine):
+    from paper_2508_12627_b200.workloads import generate
+    factors, sig, m, _ = generate("C3", 300)
+    a = engine.u_statistic_tensors(factors, sig, m)
+    b = engine.u_statistic_tensors(factors, sig, m)
+    assert a == b
+
+
+def test_device_resident_inputs(engine):
+    import torch
+    from paper_2508_12627_b200.workloads import generate
+    factors, sig, m, _ = generate("C2", 200)
+    host = engine.u_statistic_tensors(factors, sig, m)
+    dev = {}
+    dfac = []
+    for f in factors:
+        if id(f) not in dev:
+            dev[id(f)] = torch.from_numpy(f).cuda()
+        dfac.append(dev[id(f)])
+    got = engine.u_statistic_tensors(dfac, sig, m)
+    assert got == host
