@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""Exact U-statistic throughput on B200 (BASELINE.json metric: evals/s and % of
+the FP64 tensor-core / HBM roofline).
+
+One step = one exact U-statistic evaluation of the workload (all sparsified
+partition-lattice V-terms contracted on the GPU, combined on the host in the
+reference's order). Default workload: BASELINE.json configs[1] (C2, m=4 cycle,
+n=8192), the largest single-GPU config the metric is quoted on.
+
+  value  inputs resident in HBM (device pointers through the C-ABI); each step
+         still copies + sparsifies the factor on device, plans, contracts and
+         reads the per-term values back
+  e2e    the same call with HOST (pinned) buffers: H2D of the factor matrix
+         and D2H of the terms inside every timed step
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref, compiled from /root/reference sources) on this host's cores.
+
+N>1 (torchrun): V-terms are LPT-sharded over ranks (no data-path exchange);
+per-term values meet in one NCCL all-reduce, then the reference combination.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FP64_PEAK_TFLOPS = 37.17      # measured: mma.sync f64 issue-rate probe, profiles/r01_fp64_peak_probe.log
+FP64_CUBLAS_TFLOPS = 36.17    # measured: cuBLAS DGEMM 16384^3 on this pool (same log)
+CPU_SAMPLE_N = {"C1": 2000, "C2": 4096, "C3": 4096, "C4": 160, "C5": 1024}
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def reference_sample(name: str, n_sample: int, threads: int, repeats: int = 1):
+    """Times the reference u_statistic (oracle/_ref) on a bounded sample."""
+    from oracle import ref as REF
+    from paper_2508_12627_b200.workloads import generate
+    factors, sig, m, _ = generate(name, n_sample)
+    cap = max(2 ** 31, n_sample ** 3 + 1)
+    walls, stats = [], None
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        u, stats = REF.u_statistic(factors, sig, m, threads=threads, cap=cap)
+        walls.append(time.perf_counter() - t0)
+    return u, min(walls), stats
+
+
+def fitted_cpu_time(name, n, threads):
+    """Times the reference at two bounded sizes (n2/2, n2) and extrapolates to n
+    with the fitted power law T ~ n^p. Returns (t_full_est, detail dict)."""
+    n2 = min(CPU_SAMPLE_N[name], n)
+    if n2 == n:
+        _, t, st = reference_sample(name, n, threads)
+        return t, {"n": n, "wall": t, "exponent": None, "contract": st["contract_seconds"]}
+    n1 = max(CONFIG_MIN_N.get(name, 8), n2 // 2)
+    _, t1, _ = reference_sample(name, n1, threads)
+    _, t2, st = reference_sample(name, n2, threads)
+    p = float(np.log(t2 / t1) / np.log(n2 / n1)) if t1 > 0 and t2 > t1 else 3.0
+    return t2 * (n / n2) ** p, {"n1": n1, "t1": t1, "n": n2, "wall": t2, "exponent": p,
+                                "contract": st["contract_seconds"]}
+
+
+CONFIG_MIN_N = {"C3": 256, "C5": 256}
+REFERENCE_ARM_BUDGET_S = 300.0
+
+
+def run_reference_arm(args, name, world, rank):
+    if rank != 0:
+        return 0
+    from oracle import ref as REF
+    if not REF.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libustats_ref.so not built"}))
+        return 0
+    from paper_2508_12627_b200.workloads import CONFIGS
+    w = CONFIGS[name]
+    n = args.n or w.n
+    threads = os.cpu_count() or 1
+    # warm-up = the two bounded probes that also predict the full-size time
+    est, det = fitted_cpu_time(name, n, threads)
+    if est * args.steps <= REFERENCE_ARM_BUDGET_S or det.get("exponent") is None:
+        walls = [reference_sample(name, n, threads)[1] for _ in range(args.steps)]
+        t_full = statistics.mean(walls)
+        sample = (f"ustats::u_statistic (oracle/_ref: the unmodified reference sources) at full n={n}, "
+                  f"threads={threads}, mean wall {t_full:.3f}s over {len(walls)} runs (tensorize+sparsify+contract)")
+    else:
+        walls = [reference_sample(name, det["n"], threads)[1] for _ in range(args.steps)]
+        t_full = statistics.mean(walls) * (n / det["n"]) ** det["exponent"]
+        sample = (f"ustats::u_statistic (oracle/_ref) at n={det['n']}, threads={threads}, mean wall "
+                  f"{statistics.mean(walls):.3f}s over {len(walls)} runs; extrapolated to n={n} with the "
+                  f"power law fitted between n={det['n1']} and n={det['n']} (p={det['exponent']:.2f}); "
+                  f"full size would take ~{est:.0f}s per step")
+    value = 1.0 / t_full
+    line = {
+        "metric": "U-statistic exact evals/sec", "value": value, "unit": "evals/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE.json construction)",
+        "config": {"workload": name, "m": w.m, "n": n, "signature": [list(t) for t in w.signature]},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def reference_madds(name, n):
+    """Exact reference-plan multiply-adds (ExecStats rules) at extent n, from the
+    engine's host planner walk (no GPU): polynomial fitted exactly at small n."""
+    from paper_2508_12627_b200.workloads import CONFIGS
+    from oracle import ref as REF
+    w = CONFIGS[name]
+    sig = [list(t) for t in w.signature]
+    # madds(n) is a polynomial of degree <= m; fit on the reference at small n
+    xs = list(range(w.m + 2, 2 * w.m + 5))
+    ys = []
+    for x in xs:
+        rng = np.random.default_rng(0)
+        facs = [rng.uniform(0.5, 1.5, size=(x,) * len(t)) for t in sig]
+        _, st = REF.u_statistic(facs, sig, w.m, threads=1)
+        ys.append(st["multiply_adds"])
+    coef = np.polyfit(np.array(xs, float), np.array(ys, float), w.m)
+    coef = np.round(coef)
+    return float(np.polyval(coef, float(n)))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--n", type=int, default=0, help="override the config's n (parity/debug only)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    name = args.config
+
+    if args.impl == "reference":
+        return run_reference_arm(args, name, world, rank)
+
+    import torch
+    import paper_2508_12627_b200 as us
+    from paper_2508_12627_b200.workloads import CONFIGS, generate, input_bytes
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = CONFIGS[name]
+    n = args.n or w.n
+    factors, sig, m, _ = generate(name, n)
+    cfg = us.Config(device=local, rank=rank, world_size=world,
+                    memory_cap_entries=max(2 ** 31, n * n + 1, n ** 3 + 1 if name == "C4" else 0))
+
+    # device-resident and pinned-host copies (aliases preserved)
+    dev, pin, dfac, hfac = {}, {}, [], []
+    for f in factors:
+        if id(f) not in dev:
+            t = torch.from_numpy(f)
+            dev[id(f)] = t.cuda()
+            pin[id(f)] = t.pin_memory()
+        dfac.append(dev[id(f)])
+        hfac.append(pin[id(f)])
+    torch.cuda.synchronize()
+
+    def step(fx, on_device):
+        r = us.u_terms(fx, sig, m, cfg) if on_device else _host_terms(us, fx, sig, m, cfg)
+        if world > 1:
+            import torch.distributed as dist
+            v = torch.from_numpy(r.v).cuda()
+            dist.all_reduce(v)
+            return us.combine_terms(r.mu, v.cpu().numpy()), r
+        return r.value, r
+
+    def timed(fx, on_device, k):
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        last = None
+        for _ in range(k):
+            last = step(fx, on_device)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms / k, last
+
+    for _ in range(args.warmup):
+        step(dfac, True)
+    us.profile(enable=True, reset=True, device=local)
+    with ClockSampler(local) as clocks:
+        ms_step, (u_val, r) = timed(dfac, True, args.steps)
+    prof = us.profile(enable=False, reset=True, device=local)
+    e2e = None
+    if not args.no_e2e:
+        step(hfac, False)
+        e2e_ms, _ = timed(hfac, False, args.steps)
+        e2e = {"value": 1e3 / e2e_ms, "unit": "evals/s", "h2d_bytes_per_step": input_bytes(factors),
+               "d2h_bytes_per_step": int(r.v.nbytes), "ms_per_step": e2e_ms}
+
+    st = r.stats
+    gemm_ms = prof["gemm_ms"] / args.steps
+    stream_ms = prof["stream_ms"] / args.steps
+    peaks = measured_peaks()
+    if st["executed_gemm_macs"] > 0:
+        achieved = 2.0 * st["executed_gemm_macs"] / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
+                    "kernel": "gemm_f64_kernel (DMMA.8x8x4)", "kernel_ms_per_step": gemm_ms,
+                    "kernel_share_of_step": gemm_ms / ms_step,
+                    "peak_source": f"measured FP64 DMMA issue-rate probe {FP64_PEAK_TFLOPS} TFLOP/s "
+                                   f"(cuBLAS DGEMM {FP64_CUBLAS_TFLOPS}); MEASURED_PEAKS.json has no FP64 entry",
+                    "traffic": ncu_traffic(name, "gemm")}
+    else:
+        bytes_step = 8.0 * st["executed_stream_entries"]
+        achieved = bytes_step / (stream_ms * 1e-3) / 1e9 if stream_ms > 0 else None
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                    "frac": achieved / peaks["hbm_gbs"] if achieved else None,
+                    "kernel": "stream kernels", "kernel_ms_per_step": stream_ms,
+                    "kernel_share_of_step": stream_ms / ms_step, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                    "traffic": ncu_traffic(name, "stream")}
+    line = {
+        "metric": "U-statistic exact evals/sec", "value": 1e3 / ms_step * 1, "unit": "evals/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE.json construction)",
+        "config": {"workload": name, "m": m, "n": n, "signature": sig, "terms": int(len(r.v)),
+                   "parallelism": f"term-sharded x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (no flush needed)" if input_bytes(factors) > 126e6
+                   else "inputs L2-resident across steps (latency-bound config)"},
+        "u": u_val,
+        "roofline": roofline,
+        "gpu_launches": int(st["kernel_launches"]) * args.steps,
+        "clocks": clocks.summary(),
+        "stats_per_step": {k: st[k] for k in ("multiply_adds", "executed_gemm_macs", "executed_stream_entries",
+                                               "gemm_launches", "stream_launches", "shared_hits")},
+        "stream_ms_per_step": stream_ms,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(name, n)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def _host_terms(us, fx, sig, m, cfg):
+    # pinned host tensors -> host pointers (on_device=0): the engine's own H2D
+    import ctypes as C
+    from paper_2508_12627_b200 import _native as N
+    from paper_2508_12627_b200.api import UTerms, _check, _signature
+    K, L, I = _signature(sig)
+    seen, ptrs = {}, []
+    for t in fx:
+        ptrs.append(t.data_ptr())
+    P = (C.c_void_p * K)(*ptrs)
+    n = fx[1].shape[0] if fx[1].dim() else fx[0].shape[0]
+    cap = us.bell_number(m)
+    rgs = np.zeros((cap, m), dtype=np.int32)
+    mu = np.zeros(cap, dtype=np.int64)
+    v = np.zeros(cap)
+    own = np.zeros(cap, dtype=np.int32)
+    cnt, u = N.i32(), N.f64()
+    st = N.UsStats()
+    c = cfg.native()
+    _check(N.lib().us_u_terms(m, K, L, I, P, n, 0, C.byref(c), cap, C.byref(cnt),
+                              rgs.ctypes.data_as(C.POINTER(N.i32)), mu.ctypes.data_as(C.POINTER(N.i64)),
+                              v.ctypes.data_as(C.POINTER(N.f64)), own.ctypes.data_as(C.POINTER(N.i32)),
+                              C.byref(u), C.byref(st)))
+    T = cnt.value
+    return UTerms(u.value, rgs[:T], mu[:T], v[:T], own[:T], st.as_dict())
+
+
+def ncu_traffic(name, kind):
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    return d.get(name, {}).get(kind)
+
+
+def cpu_baseline(name, n):
+    from oracle import ref as REF
+    if not REF.available():
+        return {"value": None, "unit": "evals/s", "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref not built on this host"}
+    threads = os.cpu_count() or 1
+    est, det = fitted_cpu_time(name, n, threads)
+    if det.get("exponent") is None:
+        sample = f"ustats::u_statistic (oracle/_ref) at full n={n}, threads={threads}: {det['wall']:.3f}s wall"
+    else:
+        sample = (f"ustats::u_statistic (unmodified reference, oracle/_ref), threads={threads}: "
+                  f"{det['t1']:.3f}s at n={det['n1']}, {det['wall']:.3f}s at n={det['n']} "
+                  f"(contract {det['contract']:.3f}s); extrapolated to n={n} with the fitted power law "
+                  f"p={det['exponent']:.2f}")
+    return {"value": 1.0 / est, "unit": "evals/s", "cores": threads, "kind": "reference", "sample": sample}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

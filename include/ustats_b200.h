@@ -66,6 +66,7 @@ typedef struct us_stats {
     uint64_t gemm_launches;
     uint64_t stream_launches;
     uint64_t shared_hits;
+    uint64_t kernel_launches;       /* every kernel this call enqueued */
 } us_stats;
 
 US_API const char* us_version(void);
@@ -137,6 +138,15 @@ US_API int us_treewidth(int32_t n, int32_t edge_count, const int32_t* edges, int
 /* Device plumbing. */
 US_API int us_device_count(int32_t* count);
 US_API int us_device_synchronize(int32_t device);
+/* The engine's CUDA stream on `device` (cudaStream_t as void*), so callers can
+ * order their own work / record events against it. */
+US_API int us_device_stream(int32_t device, void** stream_out);
+/* Kernel-class timing (CUDA events on the engine stream): enable != 0 turns it
+ * on; ms_out[3] / groups_out[3] receive accumulated milliseconds and launch
+ * groups for {GEMM, stream, other}; reset != 0 clears the totals after reading.
+ * Synchronizes the engine stream. */
+US_API int us_profile(int32_t device, int32_t enable, int32_t reset, double* ms_out,
+                      uint64_t* groups_out);
 
 #ifdef __cplusplus
 }

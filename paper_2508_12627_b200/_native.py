@@ -43,6 +43,7 @@ class UsStats(C.Structure):
         ("gemm_launches", u64),
         ("stream_launches", u64),
         ("shared_hits", u64),
+        ("kernel_launches", u64),
     ]
 
     def as_dict(self) -> dict:
@@ -73,6 +74,8 @@ SIGNATURES = {
     "us_treewidth": (C.c_int, [i32, i32, P(i32), P(i32), P(i32)]),
     "us_device_count": (C.c_int, [P(i32)]),
     "us_device_synchronize": (C.c_int, [i32]),
+    "us_device_stream": (C.c_int, [i32, P(C.c_void_p)]),
+    "us_profile": (C.c_int, [i32, i32, i32, P(f64), P(u64)]),
 }
 
 _lib = None

@@ -360,6 +360,23 @@ def treewidth(n: int, edges):
     return w.value, [order[i] for i in range(n)]
 
 
+def device_stream(device: int = -1) -> int:
+    """The engine's cudaStream_t on `device` (as an int handle)."""
+    h = C.c_void_p()
+    _check(N.lib().us_device_stream(device, C.byref(h)))
+    return h.value or 0
+
+
+def profile(enable: bool = True, reset: bool = True, device: int = -1) -> dict:
+    """Reads (and optionally resets) kernel-class event timings, then sets the
+    profiling switch. Returns {'gemm_ms','stream_ms','other_ms', '*_groups'}."""
+    ms = (N.f64 * 3)()
+    groups = (N.u64 * 3)()
+    _check(N.lib().us_profile(device, 1 if enable else 0, 1 if reset else 0, ms, groups))
+    return {"gemm_ms": ms[0], "stream_ms": ms[1], "other_ms": ms[2],
+            "gemm_groups": groups[0], "stream_groups": groups[1], "other_groups": groups[2]}
+
+
 def device_count() -> int:
     c = N.i32()
     _check(N.lib().us_device_count(C.byref(c)))

@@ -110,6 +110,7 @@ void export_stats(const ustats::RunStats& rs, us_stats* s) {
     s->gemm_launches = rs.gemm_launches;
     s->stream_launches = rs.stream_launches;
     s->shared_hits = rs.shared_hits;
+    s->kernel_launches = 0;
 }
 
 void export_dev(const ustats::dev::StatisticResult& r, int rank, us_stats* s) {
@@ -130,6 +131,7 @@ void export_dev(const ustats::dev::StatisticResult& r, int rank, us_stats* s) {
     rs.stream_launches = r.stats.stream_launches;
     rs.shared_hits = r.stats.shared_hits;
     export_stats(rs, s);
+    s->kernel_launches = r.stats.kernel_launches;
 }
 
 ustats::dev::StatisticResult run_lattice(int32_t m, int32_t K, const int32_t* tuple_len,
@@ -390,6 +392,22 @@ int us_device_count(int32_t* count) {
 
 int us_device_synchronize(int32_t device) {
     return guarded([&] { ustats::dev::Runtime::get(device).sync(); });
+}
+
+int us_device_stream(int32_t device, void** stream_out) {
+    return guarded([&] { *stream_out = static_cast<void*>(ustats::dev::Runtime::get(device).stream()); });
+}
+
+int us_profile(int32_t device, int32_t enable, int32_t reset, double* ms_out, uint64_t* groups_out) {
+    return guarded([&] {
+        auto& rt = ustats::dev::Runtime::get(device);
+        auto p = rt.collect(reset != 0);
+        rt.profile_enable(enable != 0);
+        for (int i = 0; i < 3; ++i) {
+            if (ms_out) ms_out[i] = p.ms[i];
+            if (groups_out) groups_out[i] = p.groups[i];
+        }
+    });
 }
 
 }  // extern "C"

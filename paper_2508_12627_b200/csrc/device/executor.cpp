@@ -94,6 +94,44 @@ void Runtime::release(double* p) {
 
 void Runtime::sync() { check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize"); }
 
+void Runtime::begin(Kind k) {
+    if (!profiling_) return;
+    while (pool_.size() < 2) {
+        cudaEvent_t e;
+        check_cuda(cudaEventCreate(&e), "cudaEventCreate");
+        pool_.push_back(e);
+    }
+    Mark m{k, pool_.back(), nullptr};
+    pool_.pop_back();
+    m.b = pool_.back();
+    pool_.pop_back();
+    cudaEventRecord(m.a, stream_);
+    marks_.push_back(m);
+}
+
+void Runtime::end(Kind k) {
+    if (!profiling_ || marks_.empty()) return;
+    (void)k;
+    cudaEventRecord(marks_.back().b, stream_);
+}
+
+Runtime::Profile Runtime::collect(bool reset) {
+    sync();
+    for (const Mark& m : marks_) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, m.a, m.b) == cudaSuccess) {
+            totals_.ms[m.kind] += ms;
+            totals_.groups[m.kind] += 1;
+        }
+        pool_.push_back(m.a);
+        pool_.push_back(m.b);
+    }
+    marks_.clear();
+    Profile p = totals_;
+    if (reset) totals_ = Profile{};
+    return p;
+}
+
 // ------------------------------------------------------------- Contractor
 namespace {
 inline std::uint32_t bit(int id) { return 1u << id; }
@@ -236,8 +274,11 @@ Buf Contractor::stream_to_buffer(std::vector<View> factors, const std::vector<in
     }
     const std::size_t scratch_n = stream_scratch_entries(a, rt_.sm_count());
     double* scratch = scratch_n ? rt_.scratch(scratch_n) : nullptr;
-    launch_stream(a, scratch, scratch_n, rt_.sm_count(), rt_.stream());
+    rt_.begin(Runtime::kStream);
+    const int launched = launch_stream(a, scratch, scratch_n, rt_.sm_count(), rt_.stream());
+    rt_.end(Runtime::kStream);
     check_cuda(cudaGetLastError(), "stream kernel launch");
+    if (stats_) stats_->kernel_launches += static_cast<std::uint64_t>(launched);
     rt_.release(scratch);
     if (stats_) {
         stats_->stream_entries += pw(a.n_out + a.n_sum) * static_cast<std::uint64_t>(a.nf);
@@ -248,6 +289,18 @@ Buf Contractor::stream_to_buffer(std::vector<View> factors, const std::vector<in
 
 Buf Contractor::gemm_to_buffer(std::vector<View> fa, std::vector<View> fb, const std::vector<int>& ra,
                                const std::vector<int>& rb, int e) {
+    // Multi-factor (Hadamard / scaled / Khatri-Rao) operands are formed once
+    // by a stream kernel into a k-major buffer (rows..., e): O(rows*n) traffic
+    // against O(rows*cols*n) DMMA work, and the GEMM then runs the TMA path.
+    auto flatten = [&](std::vector<View>& fs, const std::vector<int>& rows) {
+        if (fs.size() <= 1) return;
+        std::vector<int> layout = rows;
+        layout.push_back(e);
+        Buf m = stream_to_buffer(fs, layout, 0, nullptr);
+        fs = {output_view(m, layout)};
+    };
+    flatten(fa, ra);
+    flatten(fb, rb);
     fa = limit_factors(std::move(fa), kMaxGemmFactors);
     fb = limit_factors(std::move(fb), kMaxGemmFactors);
     // Orient symmetric factors so the inner (k) index is their fast axis.
@@ -289,8 +342,11 @@ Buf Contractor::gemm_to_buffer(std::vector<View> fa, std::vector<View> fb, const
     g.mode = kEpiStore;
     Buf out = rt_.allocate(static_cast<int>(ra.size() + rb.size()), n_);
     g.out = out->ptr;
-    launch_gemm(g, rt_.stream());
+    rt_.begin(Runtime::kGemm);
+    const int launched = launch_gemm(g, rt_.stream());
+    rt_.end(Runtime::kGemm);
     check_cuda(cudaGetLastError(), "gemm launch");
+    if (stats_) stats_->kernel_launches += static_cast<std::uint64_t>(launched);
     if (stats_) {
         stats_->gemm_macs += static_cast<std::uint64_t>(g.rows) * static_cast<std::uint64_t>(g.cols) *
                              static_cast<std::uint64_t>(n_);
@@ -601,12 +657,15 @@ StatisticResult lattice_statistic(const std::vector<const double*>& inputs, bool
                                    inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                                    rt.stream()),
                    "upload");
-        if (mode == LatticeMode::Sparsified) launch_sparsify(b->ptr, order, n, rt.stream());
+        rt.begin(Runtime::kOther);
+        if (mode == LatticeMode::Sparsified)
+            res.stats.kernel_launches += static_cast<std::uint64_t>(launch_sparsify(b->ptr, order, n, rt.stream()));
         if (flags && order == 2) {
             int* f = flags + probes.size();
-            launch_symmetry_check(b->ptr, n, f, rt.stream());
+            res.stats.kernel_launches += static_cast<std::uint64_t>(launch_symmetry_check(b->ptr, n, f, rt.stream()));
             probes.emplace_back(b, f);
         }
+        rt.end(Runtime::kOther);
         by_ptr[inputs[k]] = b;
         tensors.push_back(b);
     }

@@ -62,12 +62,32 @@ class Runtime {
     void release(double* p);
     void sync();
 
+    // Kernel-class timing with CUDA events on the engine stream (bench
+    // roofline evidence). Cheap: two event records per timed launch group.
+    enum Kind { kGemm = 0, kStream = 1, kOther = 2 };
+    struct Profile {
+        double ms[3] = {0, 0, 0};
+        std::uint64_t groups[3] = {0, 0, 0};
+    };
+    void profile_enable(bool on) { profiling_ = on; }
+    void begin(Kind k);
+    void end(Kind k);
+    Profile collect(bool reset);  // synchronizes the stream
+
   private:
     explicit Runtime(int device);
     int device_ = 0;
     int sm_count_ = 148;
     cudaStream_t stream_ = nullptr;
     std::uint64_t next_uid_ = 1;
+    bool profiling_ = false;
+    std::vector<cudaEvent_t> pool_;
+    struct Mark {
+        Kind kind;
+        cudaEvent_t a, b;
+    };
+    std::vector<Mark> marks_;
+    Profile totals_;
     friend struct DeviceBuffer;
 };
 
@@ -80,6 +100,7 @@ struct DevStats {
     std::uint64_t gemm_launches = 0;
     std::uint64_t stream_launches = 0;
     std::uint64_t shared_hits = 0;
+    std::uint64_t kernel_launches = 0;
 };
 
 // Content-addressed cache of intermediates shared across V-terms of one

@@ -353,8 +353,13 @@ std::size_t gemm_partial_entries(const GemmArgs& a) {
     }
 }
 
-void launch_gemm(const GemmArgs& a, cudaStream_t s) {
-    if (a.a_kmajor) {
+int launch_gemm_tma(const GemmArgs& a, cudaStream_t s);  // gemm_tma.cu
+
+int launch_gemm(const GemmArgs& a, cudaStream_t s) {
+    int launched = launch_gemm_tma(a, s);
+    if (launched > 0) {
+        // shared finalize below
+    } else if (a.a_kmajor) {
         if (a.b_kmajor) launch_variant<true, true>(a, s);
         else launch_variant<true, false>(a, s);
     } else {
@@ -368,7 +373,10 @@ void launch_gemm(const GemmArgs& a, cudaStream_t s) {
         gemm_finalize_vector<<<static_cast<unsigned>((a.rows + 255) / 256), 256, 0, s>>>(a.partial, tn, a.rows, a.out);
     } else if (a.mode == kEpiSumRows) {
         gemm_finalize_vector<<<static_cast<unsigned>((a.cols + 255) / 256), 256, 0, s>>>(a.partial, tm, a.cols, a.out);
+    } else {
+        return 1;
     }
+    return 2;
 }
 
 }  // namespace ustats::dev

@@ -71,17 +71,21 @@ struct GemmArgs {
 };
 
 // ------------------------------------------------------------- launchers
-void launch_stream(const StreamArgs& a, double* scratch, std::size_t scratch_entries,
-                   int sm_count, cudaStream_t s);
+// Launchers return the number of kernels they enqueued.
+int launch_stream(const StreamArgs& a, double* scratch, std::size_t scratch_entries,
+                  int sm_count, cudaStream_t s);
 std::size_t stream_scratch_entries(const StreamArgs& a, int sm_count);
 
-void launch_gemm(const GemmArgs& a, cudaStream_t s);
+// TMA-fed kernel when both operands are single plain strided matrices
+// (gemm_tma.cu), otherwise the lazy-product gather kernel (gemm_f64.cu).
+int launch_gemm(const GemmArgs& a, cudaStream_t s);
+bool gemm_tma_eligible(const GemmArgs& a, int* a_kmajor, int* b_kmajor);
 std::size_t gemm_partial_entries(const GemmArgs& a);
 
 // Zero every entry of an order-`order` tensor whose multi-index repeats a
 // coordinate (tensor.cpp:54-76), in place.
-void launch_sparsify(double* data, int order, long long n, cudaStream_t s);
+int launch_sparsify(double* data, int order, long long n, cudaStream_t s);
 // flag[0] = 0 if the n x n matrix is bitwise symmetric, else 1.
-void launch_symmetry_check(const double* data, long long n, int* flag, cudaStream_t s);
+int launch_symmetry_check(const double* data, long long n, int* flag, cudaStream_t s);
 
 }  // namespace ustats::dev

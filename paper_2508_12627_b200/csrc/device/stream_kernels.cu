@@ -65,6 +65,14 @@ __device__ double block_sum(double v, double* red) {
     return t;  // valid in thread 0
 }
 
+// No dims at all: product of scalar factors.
+__global__ void stream_product(StreamArgs a) {
+    if (threadIdx.x != 0) return;
+    double v = a.scale;
+    for (int f = 0; f < a.nf; ++f) v *= a.ptr[f][0];
+    a.out[0] = v;
+}
+
 // Elementwise: n_sum == 0. Dims [0, n_out); inner = last output dim.
 __global__ void stream_elementwise(StreamArgs a, unsigned long long rows) {
     const int inner = a.n_out - 1;
@@ -229,22 +237,26 @@ std::size_t stream_scratch_entries(const StreamArgs& a, int sm_count) {
 //  - n_out == 0          -> two-stage full reduction
 //  - innermost summed dim has the unit strides -> warp per output
 //  - otherwise           -> thread per output (+ summed-space slicing)
-void launch_stream(const StreamArgs& a, double* scratch, std::size_t scratch_entries,
-                   int sm_count, cudaStream_t s) {
+int launch_stream(const StreamArgs& a, double* scratch, std::size_t scratch_entries,
+                  int sm_count, cudaStream_t s) {
+    if (a.n_out + a.n_sum == 0) {
+        stream_product<<<1, 32, 0, s>>>(a);
+        return 1;
+    }
     if (a.n_sum == 0) {
         const unsigned long long rows = ipow(a.n, a.n_out - 1);
         const unsigned gx = static_cast<unsigned>((a.n + kThreads - 1) / kThreads);
         unsigned long long gy = rows;
         if (gy > 65535) gy = 65535;
         stream_elementwise<<<dim3(gx, static_cast<unsigned>(gy)), kThreads, 0, s>>>(a, rows);
-        return;
+        return 1;
     }
     if (a.n_out == 0) {
         const unsigned long long rows = ipow(a.n, a.n_sum - 1);
         const int blocks = blocks_for_all(rows, a.n, sm_count);
         stream_reduce_all<<<blocks, kThreads, 0, s>>>(a, rows, scratch);
         finalize_scalar<<<1, 1024, 0, s>>>(scratch, static_cast<unsigned long long>(blocks), a.scale, a.out);
-        return;
+        return 2;
     }
     const unsigned long long outputs = ipow(a.n, a.n_out);
     const int last = a.n_out + a.n_sum - 1;
@@ -258,7 +270,7 @@ void launch_stream(const StreamArgs& a, double* scratch, std::size_t scratch_ent
         const unsigned long long srows = ipow(a.n, a.n_sum - 1);
         const unsigned long long blocks = (outputs + (kThreads / 32) - 1) / (kThreads / 32);
         stream_reduce_warp<<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(a, outputs, srows);
-        return;
+        return 1;
     }
     const unsigned long long sflat = ipow(a.n, a.n_sum);
     unsigned long long slices = 1;
@@ -269,8 +281,11 @@ void launch_stream(const StreamArgs& a, double* scratch, std::size_t scratch_ent
     const unsigned gx = static_cast<unsigned>((outputs + kThreads - 1) / kThreads);
     stream_reduce_thread<<<dim3(gx, static_cast<unsigned>(slices)), kThreads, 0, s>>>(a, outputs, sflat,
                                                                                    scratch);
-    if (slices > 1)
+    if (slices > 1) {
         finalize_columns<<<gx, kThreads, 0, s>>>(scratch, slices, outputs, a.scale, a.out);
+        return 2;
+    }
+    return 1;
 }
 
 // ---------------------------------------------------------------- sparsify
@@ -312,23 +327,25 @@ __global__ void asymmetry_probe(const double* d, long long n, int* flag) {
 }
 }  // namespace
 
-void launch_sparsify(double* data, int order, long long n, cudaStream_t s) {
-    if (order < 2) return;
+int launch_sparsify(double* data, int order, long long n, cudaStream_t s) {
+    if (order < 2) return 0;
     if (order == 2) {
         zero_diagonal<<<static_cast<unsigned>((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, s>>>(data, n);
-        return;
+        return 1;
     }
     const unsigned long long total = ipow(n, order);
     unsigned long long blocks = (total + 255) / 256;
     if (blocks > 148ull * 32) blocks = 148ull * 32;
     zero_repeated<<<static_cast<unsigned>(blocks), 256, 0, s>>>(data, order, n, total);
+    return 1;
 }
 
-void launch_symmetry_check(const double* data, long long n, int* flag, cudaStream_t s) {
+int launch_symmetry_check(const double* data, long long n, int* flag, cudaStream_t s) {
     cudaMemsetAsync(flag, 0, sizeof(int), s);
     unsigned long long blocks = (static_cast<unsigned long long>(n) * n + 255) / 256;
     if (blocks > 148ull * 16) blocks = 148ull * 16;
     asymmetry_probe<<<static_cast<unsigned>(blocks), 256, 0, s>>>(data, n, flag);
+    return 1;
 }
 
 }  // namespace ustats::dev
