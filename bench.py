@@ -285,7 +285,7 @@ def main():
         achieved = 2.0 * st["executed_gemm_macs"] / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
         roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                     "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
-                    "kernel": "gemm_f64_kernel (DMMA.8x8x4)", "kernel_ms_per_step": gemm_ms,
+                    "kernel": "gemm_tma_kernel (TMA + DMMA.8x8x4)", "kernel_ms_per_step": gemm_ms,
                     "kernel_share_of_step": gemm_ms / ms_step,
                     "peak_source": f"measured FP64 DMMA issue-rate probe {FP64_PEAK_TFLOPS} TFLOP/s "
                                    f"(cuBLAS DGEMM {FP64_CUBLAS_TFLOPS}); MEASURED_PEAKS.json has no FP64 entry",
@@ -358,7 +358,8 @@ def ncu_traffic(name, kind):
     if not p.exists():
         return None
     d = json.loads(p.read_text())
-    return d.get(name, {}).get(kind)
+    entry = d.get(name, {}).get(kind)
+    return entry.get("bytes_per_launch") if isinstance(entry, dict) else entry
 
 
 def cpu_baseline(name, n):

@@ -124,7 +124,9 @@ US_API int us_eliminate_index(int32_t K, const int32_t* tuple_len, const int32_t
  * Pure host arithmetic; bit-identical to the reference given identical v. */
 US_API double us_combine_terms(int32_t count, const int64_t* mu, const double* v);
 
-/* Host-side lattice/planning helpers (no GPU needed). */
+/* Host-side lattice/planning helpers (no GPU needed). us_survivors always
+ * sets *count to the full survivor count; when it exceeds max_terms it
+ * returns TooManyTerms after writing the first max_terms. */
 US_API uint64_t us_bell_number(int32_t m);
 US_API int us_survivors(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
                  int32_t max_terms, int32_t* count, int32_t* rgs_out, int64_t* mu_out,
@@ -134,6 +136,13 @@ US_API int us_optimize_order(int32_t K, const int32_t* tuple_len, const int32_t*
                       int32_t* width_out);
 US_API int us_treewidth(int32_t n, int32_t edge_count, const int32_t* edges, int32_t* width_out,
                  int32_t* order_out);
+
+/* Term sharding plan (host only): for the sparsified lattice of the
+ * signature at extent n over world_size ranks, owner_out[t] receives the rank
+ * that evaluates survivor t (LPT on n^(width+1)), cost_out[t] its estimate. */
+US_API int us_plan_terms(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
+                         int64_t n, int32_t world_size, int32_t max_terms, int32_t* count,
+                         int32_t* owner_out, double* cost_out);
 
 /* Device plumbing. */
 US_API int us_device_count(int32_t* count);

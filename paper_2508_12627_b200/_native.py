@@ -72,6 +72,7 @@ SIGNATURES = {
     "us_survivors": (C.c_int, [i32, i32, P(i32), P(i32), i32, P(i32), P(i32), P(i64), P(u64)]),
     "us_optimize_order": (C.c_int, [i32, P(i32), P(i32), i32, P(i32), P(i32), P(i32)]),
     "us_treewidth": (C.c_int, [i32, i32, P(i32), P(i32), P(i32)]),
+    "us_plan_terms": (C.c_int, [i32, i32, P(i32), P(i32), i64, i32, i32, P(i32), P(i32), P(f64)]),
     "us_device_count": (C.c_int, [P(i32)]),
     "us_device_synchronize": (C.c_int, [i32]),
     "us_device_stream": (C.c_int, [i32, P(C.c_void_p)]),

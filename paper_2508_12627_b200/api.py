@@ -332,13 +332,30 @@ def bell_number(m: int) -> int:
 def survivors(signature, m: int):
     """Sparsification survivors in enumeration order: (rgs (T,m), mu (T,), enumerated)."""
     K, L, I = _signature(signature)
+    cap = 1024
+    while True:
+        rgs = np.zeros((cap, max(m, 1)), dtype=np.int32)
+        mu = np.zeros(cap, dtype=np.int64)
+        count, en = N.i32(), N.u64()
+        st = N.lib().us_survivors(m, K, L, I, cap, C.byref(count), rgs.ctypes.data_as(C.POINTER(N.i32)),
+                                  mu.ctypes.data_as(C.POINTER(N.i64)), C.byref(en))
+        if st == 1 + ERROR_CODES.index("TooManyTerms") and count.value > cap:
+            cap = count.value
+            continue
+        _check(st)
+        return rgs[: count.value].copy(), mu[: count.value].copy(), en.value
+
+
+def plan_terms(signature, m: int, n: int, world_size: int):
+    """Term-sharding plan: (owner (T,), cost (T,)) for the sparsified lattice."""
+    K, L, I = _signature(signature)
     cap = bell_number(m)
-    rgs = np.zeros((cap, m), dtype=np.int32)
-    mu = np.zeros(cap, dtype=np.int64)
-    count, en = N.i32(), N.u64()
-    _check(N.lib().us_survivors(m, K, L, I, cap, C.byref(count), rgs.ctypes.data_as(C.POINTER(N.i32)),
-                                mu.ctypes.data_as(C.POINTER(N.i64)), C.byref(en)))
-    return rgs[: count.value].copy(), mu[: count.value].copy(), en.value
+    owner = np.zeros(cap, dtype=np.int32)
+    cost = np.zeros(cap)
+    cnt = N.i32()
+    _check(N.lib().us_plan_terms(m, K, L, I, n, world_size, cap, C.byref(cnt),
+                                 owner.ctypes.data_as(C.POINTER(N.i32)), cost.ctypes.data_as(C.POINTER(N.f64))))
+    return owner[: cnt.value].copy(), cost[: cnt.value].copy()
 
 
 def optimize_order(inputs, strategy: str = "auto"):

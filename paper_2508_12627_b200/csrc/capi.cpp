@@ -341,13 +341,15 @@ int us_survivors(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* 
         ustats::SetPartition p;
         int c = 0;
         while (s.next(p)) {
-            if (c >= max_terms) ustats::fail(ustats::ErrorCode::TooManyTerms, "term buffer too small");
-            for (int i = 0; i < m; ++i) rgs_out[c * m + i] = p.rgs()[static_cast<std::size_t>(i)];
-            mu_out[c] = ustats::mobius_coefficient(p);
+            if (c < max_terms) {
+                for (int i = 0; i < m; ++i) rgs_out[c * m + i] = p.rgs()[static_cast<std::size_t>(i)];
+                mu_out[c] = ustats::mobius_coefficient(p);
+            }
             ++c;
         }
         *count = c;
         if (enumerated) *enumerated = s.enumerated();
+        if (c > max_terms) ustats::fail(ustats::ErrorCode::TooManyTerms, "term buffer too small");
     });
 }
 
@@ -379,6 +381,24 @@ int us_treewidth(int32_t n, int32_t edge_count, const int32_t* edges, int32_t* w
         auto r = ustats::treewidth_exact(g, c);
         *width_out = r.width;
         for (std::size_t i = 0; i < r.order.size(); ++i) order_out[i] = r.order[i];
+    });
+}
+
+int us_plan_terms(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx, int64_t n,
+                  int32_t world_size, int32_t max_terms, int32_t* count, int32_t* owner_out, double* cost_out) {
+    return guarded([&] {
+        auto sig = decode(K, tuple_len, tuple_idx);
+        validate_signature(m, sig);
+        ustats::Config config;
+        config.device.world_size = world_size < 1 ? 1 : world_size;
+        auto plan = ustats::dev::plan_terms(sig, m, n, ustats::dev::LatticeMode::Sparsified, config);
+        const int T = static_cast<int>(plan.owner.size());
+        *count = T;
+        if (T > max_terms) ustats::fail(ustats::ErrorCode::TooManyTerms, "term buffer too small");
+        for (int t = 0; t < T; ++t) {
+            owner_out[t] = plan.owner[static_cast<std::size_t>(t)];
+            if (cost_out) cost_out[t] = plan.cost[static_cast<std::size_t>(t)];
+        }
     });
 }
 

@@ -631,6 +631,48 @@ double combine_terms(const std::vector<double>& terms) {
     return total;
 }
 
+TermPlan plan_terms(const std::vector<IndexTuple>& zero_sig, int m, long long n, LatticeMode mode,
+                    const Config& config) {
+    TermPlan plan;
+    std::vector<SetPartition> parts;
+    {
+        SetPartition p;
+        if (mode == LatticeMode::Sparsified) {
+            SparsifiedPartitionStream s(m, zero_sig);
+            while (s.next(p)) parts.push_back(p);
+            plan.enumerated = s.enumerated();
+        } else {
+            PartitionStream s(m);
+            while (s.next(p)) parts.push_back(p);
+            plan.enumerated = bell_number(m);
+        }
+    }
+    const std::size_t T = parts.size();
+    for (std::size_t t = 0; t < T; ++t) {
+        plan.rgs.push_back(parts[t].rgs());
+        plan.mu.push_back(mobius_coefficient(parts[t]));
+        plan.notation.emplace_back(induced_signature(zero_sig, parts[t]));
+        plan.order.push_back(optimize_order(plan.notation.back(), static_cast<int>(n), config.strategy, config));
+        plan.cost.push_back(static_cast<double>(plan.order.back().predicted_peak_entries));
+    }
+    // LPT: heaviest term first onto the least-loaded rank (ties: lowest rank).
+    plan.owner.assign(T, 0);
+    const int W = std::max(1, config.device.world_size);
+    if (W > 1) {
+        std::vector<std::size_t> idx(T);
+        std::iota(idx.begin(), idx.end(), 0);
+        std::stable_sort(idx.begin(), idx.end(),
+                         [&](std::size_t a, std::size_t b) { return plan.cost[a] > plan.cost[b]; });
+        std::vector<double> load(static_cast<std::size_t>(W), 0.0);
+        for (std::size_t t : idx) {
+            auto w = static_cast<std::size_t>(std::min_element(load.begin(), load.end()) - load.begin());
+            plan.owner[t] = static_cast<int>(w);
+            load[w] += plan.cost[t];
+        }
+    }
+    return plan;
+}
+
 StatisticResult lattice_statistic(const std::vector<const double*>& inputs, bool inputs_on_device,
                                   const std::vector<IndexTuple>& zero_sig, int m, long long n,
                                   LatticeMode mode, const Config& config) {
@@ -681,51 +723,18 @@ StatisticResult lattice_statistic(const std::vector<const double*>& inputs, bool
     rt.sync();
     res.upload_seconds = std::chrono::duration<double>(Clock::now() - t_up).count();
 
-    // Enumerate the lattice (partition.cpp:210-234) and plan every term.
     const auto t0 = Clock::now();
-    std::vector<SetPartition> parts;
-    {
-        SetPartition p;
-        if (mode == LatticeMode::Sparsified) {
-            SparsifiedPartitionStream s(m, zero_sig);
-            while (s.next(p)) parts.push_back(p);
-            res.enumerated = s.enumerated();
-        } else {
-            PartitionStream s(m);
-            while (s.next(p)) parts.push_back(p);
-            res.enumerated = bell_number(m);
-        }
-    }
-    const std::size_t T = parts.size();
-    std::vector<EinsumNotation> notes(T);
-    std::vector<EliminationOrder> orders(T);
-    std::vector<double> cost(T);
-    for (std::size_t t = 0; t < T; ++t) {
-        notes[t] = EinsumNotation(induced_signature(zero_sig, parts[t]));
-        orders[t] = optimize_order(notes[t], static_cast<int>(n), config.strategy, config);
-        cost[t] = static_cast<double>(orders[t].predicted_peak_entries);
-    }
-    // LPT distribution of terms over ranks (term sharding, no data exchange).
-    res.owner.assign(T, 0);
-    const int W = std::max(1, config.device.world_size);
-    if (W > 1) {
-        std::vector<std::size_t> idx(T);
-        std::iota(idx.begin(), idx.end(), 0);
-        std::stable_sort(idx.begin(), idx.end(), [&](std::size_t a, std::size_t b) { return cost[a] > cost[b]; });
-        std::vector<double> load(static_cast<std::size_t>(W), 0.0);
-        for (std::size_t t : idx) {
-            auto w = static_cast<std::size_t>(std::min_element(load.begin(), load.end()) - load.begin());
-            res.owner[t] = static_cast<int>(w);
-            load[w] += cost[t];
-        }
-    }
+    TermPlan plan = plan_terms(zero_sig, m, n, mode, config);
+    const std::size_t T = plan.rgs.size();
+    res.enumerated = plan.enumerated;
+    res.owner = plan.owner;
 
     double* d_v = rt.scratch(std::max<std::size_t>(T, 1));
     check_cuda(cudaMemsetAsync(d_v, 0, sizeof(double) * std::max<std::size_t>(T, 1), rt.stream()), "memset");
     for (std::size_t t = 0; t < T; ++t) {
         if (res.owner[t] != config.device.rank) continue;
         Contractor c(rt, n, config, &res.stats);
-        c.run(tensors, notes[t], orders[t], d_v + t);
+        c.run(tensors, plan.notation[t], plan.order[t], d_v + t);
     }
     res.v.assign(T, 0.0);
     if (T) check_cuda(cudaMemcpyAsync(res.v.data(), d_v, sizeof(double) * T, cudaMemcpyDeviceToHost, rt.stream()), "D2H");
@@ -740,8 +749,8 @@ StatisticResult lattice_statistic(const std::vector<const double*>& inputs, bool
     res.mu.resize(T);
     res.rgs.resize(T);
     for (std::size_t t = 0; t < T; ++t) {
-        res.mu[t] = mobius_coefficient(parts[t]);
-        res.rgs[t] = parts[t].rgs();
+        res.mu[t] = plan.mu[t];
+        res.rgs[t] = plan.rgs[t];
         res.terms[t] = static_cast<double>(res.mu[t]) * res.v[t];
     }
     res.value = combine_terms(res.terms);

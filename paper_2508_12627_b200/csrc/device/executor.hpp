@@ -189,6 +189,21 @@ struct StatisticResult {
 
 enum class LatticeMode { Sparsified, Unsparsified };
 
+// Host-only planning of one statistic: the evaluated partitions in
+// enumeration order, their induced notations and elimination orders, and the
+// LPT assignment of terms to ranks (term sharding; no GPU needed).
+struct TermPlan {
+    std::vector<std::vector<int>> rgs;
+    std::vector<long long> mu;
+    std::vector<EinsumNotation> notation;
+    std::vector<EliminationOrder> order;
+    std::vector<double> cost;   // relative work estimate (n^(width+1) per term)
+    std::vector<int> owner;
+    std::uint64_t enumerated = 0;
+};
+TermPlan plan_terms(const std::vector<IndexTuple>& zero_sig, int m, long long n, LatticeMode mode,
+                    const Config& config);
+
 // `inputs[k]` points at factor k (row-major, n^|sig[k]| entries) in host memory
 // (inputs_on_device = false) or device memory. Aliased pointers are uploaded
 // and sparsified once.

@@ -1,9 +1,10 @@
 # bench sweep on one B200: default line (C2) + the other single-GPU configs
-set -x
 cd $GRAFT_REPO_ROOT
 python bench.py --steps 3 --warmup 3 > gpurun_out/bench_C2.json 2> gpurun_out/bench_C2.err
 for c in C1 C3 C4; do
   timeout 900 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
 done
-cat gpurun_out/bench_*.json
-tail -5 gpurun_out/bench_*.err
+for c in C1 C2 C3 C4; do python -c "
+import json,sys; d=json.load(open('gpurun_out/bench_$c.json'))
+print('$c', 'value %.4g evals/s'%d['value'], 'ms %.3f'%d['ms_per_step'], 'e2e %.4g'%d.get('e2e',{}).get('value',0), 'roof %s %.3g %.3f'%(d['roofline']['unit'], d['roofline']['achieved'] or 0, d['roofline']['frac'] or 0), 'gemm_ms %.2f'%d['roofline']['kernel_ms_per_step'], 'stream_ms %.2f'%d['stream_ms_per_step'], d.get('cpu_baseline',{}).get('value'))
+" || tail -5 gpurun_out/bench_$c.err; done
