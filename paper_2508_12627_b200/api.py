@@ -358,6 +358,18 @@ def plan_terms(signature, m: int, n: int, world_size: int):
     return owner[: cnt.value].copy(), cost[: cnt.value].copy()
 
 
+def plan_summary(signature, m: int, n: int, config: Config | None = None, inputs_symmetric: bool = True):
+    """Host-only view of the optimized device program: (text, totals dict)."""
+    K, L, I = _signature(signature)
+    cap = 1 << 22
+    buf = C.create_string_buffer(cap)
+    tot = (N.u64 * 6)()
+    cfg = _cfg(config)
+    _check(N.lib().us_plan_summary(m, K, L, I, n, C.byref(cfg), 1 if inputs_symmetric else 0, buf, cap, tot))
+    names = ["gemms", "gemm_macs", "streams", "stream_entries", "fused_epilogues", "symmetric_gemms"]
+    return buf.value.decode(), dict(zip(names, list(tot)))
+
+
 def optimize_order(inputs, strategy: str = "auto"):
     K, L, I = _signature(inputs)
     ids = len({s for t in inputs for s in t})

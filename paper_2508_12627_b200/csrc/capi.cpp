@@ -402,6 +402,30 @@ int us_plan_terms(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t*
     });
 }
 
+int us_plan_summary(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx, int64_t n,
+                    const us_config* cfg, int32_t inputs_symmetric, char* text, uint64_t cap, uint64_t* totals) {
+    return guarded([&] {
+        auto sig = decode(K, tuple_len, tuple_idx);
+        validate_signature(m, sig);
+        ustats::Config config = to_config(cfg);
+        ustats::dev::Program::Totals t;
+        std::string s = ustats::dev::plan_summary(sig, m, n, config, inputs_symmetric != 0, &t);
+        if (text && cap) {
+            const std::size_t k = std::min<std::size_t>(s.size(), cap - 1);
+            std::memcpy(text, s.data(), k);
+            text[k] = 0;
+        }
+        if (totals) {
+            totals[0] = t.gemms;
+            totals[1] = t.gemm_macs;
+            totals[2] = t.streams;
+            totals[3] = t.stream_entries;
+            totals[4] = t.fused;
+            totals[5] = t.symmetric;
+        }
+    });
+}
+
 int us_device_count(int32_t* count) {
     return guarded([&] {
         int c = 0;

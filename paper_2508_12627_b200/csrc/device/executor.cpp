@@ -1,5 +1,4 @@
-// Device executor (see executor.hpp). Host C++; launches the sm_100a kernels
-// of stream_kernels.cu and gemm_f64.cu on one stream per device.
+// Device executor (see executor.hpp).
 #include "executor.hpp"
 
 #include <algorithm>
@@ -8,7 +7,6 @@
 #include <cstring>
 #include <mutex>
 #include <numeric>
-#include <unordered_map>
 
 #include "ustats/errors.hpp"
 #include "ustats/partition.hpp"
@@ -17,8 +15,7 @@
 namespace ustats::dev {
 
 void check_cuda(cudaError_t e, const char* what) {
-    if (e != cudaSuccess)
-        fail(ErrorCode::CudaError, std::string(what) + ": " + cudaGetErrorString(e));
+    if (e != cudaSuccess) fail(ErrorCode::CudaError, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
 // ---------------------------------------------------------------- Runtime
@@ -45,8 +42,7 @@ Runtime& Runtime::get(int device) {
 
 Runtime::Runtime(int device) : device_(device) {
     check_cuda(cudaSetDevice(device), "cudaSetDevice");
-    check_cuda(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, device),
-               "cudaDeviceGetAttribute");
+    check_cuda(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, device), "cudaDeviceGetAttribute");
     check_cuda(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -62,7 +58,6 @@ Buf Runtime::allocate(int order, long long n) {
     b->order = order;
     b->n = n;
     b->rt = this;
-    b->uid = next_uid_++;
     void* p = nullptr;
     check_cuda(cudaMallocAsync(&p, std::max<std::uint64_t>(b->entries(), 1) * sizeof(double), stream_),
                "cudaMallocAsync");
@@ -77,14 +72,12 @@ Buf Runtime::borrow(const double* ptr, int order, long long n) {
     b->n = n;
     b->borrowed = true;
     b->rt = this;
-    b->uid = next_uid_++;
     return b;
 }
 
 double* Runtime::scratch(std::size_t entries) {
     void* p = nullptr;
-    check_cuda(cudaMallocAsync(&p, std::max<std::size_t>(entries, 1) * sizeof(double), stream_),
-               "cudaMallocAsync(scratch)");
+    check_cuda(cudaMallocAsync(&p, std::max<std::size_t>(entries, 1) * sizeof(double), stream_), "cudaMallocAsync");
     return static_cast<double*>(p);
 }
 
@@ -109,9 +102,8 @@ void Runtime::begin(Kind k) {
     marks_.push_back(m);
 }
 
-void Runtime::end(Kind k) {
+void Runtime::end(Kind) {
     if (!profiling_ || marks_.empty()) return;
-    (void)k;
     cudaEventRecord(marks_.back().b, stream_);
 }
 
@@ -132,7 +124,7 @@ Runtime::Profile Runtime::collect(bool reset) {
     return p;
 }
 
-// ------------------------------------------------------------- Contractor
+// ----------------------------------------------------------------- helpers
 namespace {
 inline std::uint32_t bit(int id) { return 1u << id; }
 
@@ -141,87 +133,377 @@ std::vector<int> ids_of(std::uint32_t mask) {
     for (std::uint32_t r = mask; r; r &= r - 1) v.push_back(std::countr_zero(r));
     return v;
 }
-}  // namespace
 
-std::uint64_t Contractor::pw(int e) const {
+std::uint64_t ipow(long long n, int e) {
     std::uint64_t v = 1;
-    while (e-- > 0) v *= static_cast<std::uint64_t>(n_);
+    while (e-- > 0) v *= static_cast<std::uint64_t>(n);
     return v;
 }
 
-void Contractor::ref_count_alloc(int order) {
-    checked_entry_count(order, static_cast<int>(n_), config_);
+std::uint32_t ids_of_views(const std::vector<View>& vs) {
+    std::uint32_t m = 0;
+    for (const View& v : vs) m |= v.ids;
+    return m;
+}
+}  // namespace
+
+// ----------------------------------------------------------------- Program
+int Program::add_input(const Buf& real) {
+    for (std::size_t i = 0; i < bufs_.size(); ++i)
+        if (bufs_[i].input && bufs_[i].real == real) return static_cast<int>(i);
+    SymBuf b;
+    b.order = real->order;
+    b.symmetric = real->symmetric;
+    b.input = true;
+    b.real = real;
+    b.content = static_cast<int>(bufs_.size());
+    bufs_.push_back(b);
+    return b.content;
 }
 
-void Contractor::ref_owned(int order) {
-    if (stats_) stats_->ref_peak = std::max(stats_->ref_peak, pw(order));
+int Program::add_symbolic_input(int order, bool symmetric) {
+    SymBuf b;
+    b.order = order;
+    b.symmetric = symmetric && order == 2;
+    b.input = true;
+    b.content = static_cast<int>(bufs_.size());
+    bufs_.push_back(b);
+    return b.content;
 }
 
-Contractor::View Contractor::view_of(const Buf& b, const IndexTuple& tuple) const {
+Program::Totals Program::totals() const {
+    Totals t;
+    for (const Op& op : ops_) {
+        if (op.dead) continue;
+        if (op.gemm) {
+            ++t.gemms;
+            const std::uint64_t tm = (ipow(n_, static_cast<int>(op.ra.size())) + 127) / 128;
+            std::uint64_t macs = ipow(n_, static_cast<int>(op.ra.size() + op.rb.size()) + 1);
+            const bool tri = op.symmetric_out && (op.mode == kEpiStore || op.mode == kEpiSumAll) &&
+                             op.ra.size() == 1 && op.rb.size() == 1;
+            if (tri) {
+                macs = macs / (tm * tm) * (tm * (tm + 1) / 2);
+                ++t.symmetric;
+            }
+            t.gemm_macs += macs;
+            if (op.mode != kEpiStore || !op.w.empty() || op.self_power != 1) ++t.fused;
+        } else {
+            ++t.streams;
+            t.stream_entries += ipow(n_, static_cast<int>(op.out_ids.size()) + std::popcount(op.sum)) *
+                                static_cast<std::uint64_t>(op.factors.size());
+        }
+    }
+    return t;
+}
+
+std::string Program::dump() const {
+    static const char* modes[] = {"store", "sum_all", "sum_cols", "sum_rows"};
+    std::string out;
+    auto vs = [&](const std::vector<View>& v) {
+        std::string s;
+        for (const View& x : v) {
+            s += " b" + std::to_string(x.buf) + "{";
+            for (int id : ids_of(x.ids)) s += std::to_string(id) + ":" + std::to_string(x.stride[static_cast<std::size_t>(id)]) + " ";
+            s += "}";
+        }
+        return s;
+    };
+    for (std::size_t i = 0; i < ops_.size(); ++i) {
+        const Op& op = ops_[i];
+        if (op.dead) continue;
+        std::string line = std::to_string(i) + ": ";
+        if (op.gemm) {
+            line += "GEMM rows=" + std::to_string(op.ra.size()) + " cols=" + std::to_string(op.rb.size()) + " e=" +
+                    std::to_string(op.e) + " A:" + vs(op.fa) + " B:" + vs(op.fb) + " epi=" + modes[op.mode] +
+                    " pow=" + std::to_string(op.self_power) + (op.symmetric_out ? " SYM" : "") +
+                    (op.w.empty() ? "" : " W:" + vs(op.w));
+        } else {
+            line += "STREAM out=[";
+            for (int id : op.out_ids) line += std::to_string(id) + " ";
+            line += "] sum=[";
+            for (int id : ids_of(op.sum)) line += std::to_string(id) + " ";
+            line += "]" + vs(op.factors);
+        }
+        line += op.ext ? " -> term" : " -> b" + std::to_string(op.out);
+        out += line + "\n";
+    }
+    return out;
+}
+
+int Program::new_buf(int order, bool symmetric) {
+    SymBuf b;
+    b.order = order;
+    b.symmetric = symmetric;
+    b.content = static_cast<int>(bufs_.size());
+    bufs_.push_back(b);
+    return b.content;
+}
+
+View Program::view_of(int buf, const IndexTuple& layout) const {
     View v;
-    v.buf = b;
+    v.buf = buf;
     long long s = 1;
-    for (std::size_t p = tuple.size(); p-- > 0;) {
-        if (tuple[p] >= kMaxIds) fail(ErrorCode::InvalidArgument, "too many indices for the device executor");
-        v.stride[static_cast<std::size_t>(tuple[p])] += s;
-        v.ids |= bit(tuple[p]);
+    for (std::size_t p = layout.size(); p-- > 0;) {
+        if (layout[p] < 0 || layout[p] >= kMaxIds)
+            fail(ErrorCode::InvalidArgument, "too many indices for the device executor");
+        v.stride[static_cast<std::size_t>(layout[p])] += s;
+        v.ids |= bit(layout[p]);
         s *= n_;
     }
     return v;
 }
 
-Contractor::View Contractor::output_view(const Buf& b, const std::vector<int>& layout) const {
-    return view_of(b, layout);
-}
-
-Contractor::Slot Contractor::slot_of(const Buf& b, const IndexTuple& tuple) {
-    Slot s;
-    s.factors.push_back(view_of(b, tuple));
-    s.ids = s.factors[0].ids;
-    IndexTuple distinct;
-    for (int id : tuple)
-        if (std::find(distinct.begin(), distinct.end(), id) == distinct.end()) distinct.push_back(id);
-    if (distinct.size() != tuple.size()) {  // extract_diagonal (einsum.cpp:183-206): a strided view here
-        ref_count_alloc(static_cast<int>(distinct.size()));
-        ref_owned(static_cast<int>(distinct.size()));
-        s.owned = true;
+// Canonical descriptor of a factor over an ordered list of local dims:
+// content id + stride per dim. A symmetric matrix reads the same either way,
+// so both orientations map to one descriptor.
+std::string Program::desc(const View& v, const std::vector<int>& dims) const {
+    std::vector<long long> s;
+    for (int d : dims) s.push_back(v.stride[static_cast<std::size_t>(d)]);
+    const SymBuf& b = bufs_[static_cast<std::size_t>(v.buf)];
+    if (b.symmetric && std::popcount(v.ids) == 2) {
+        std::vector<long long> t = s;
+        for (long long& x : t) x = x == 1 ? n_ : (x == n_ ? 1 : x);
+        if (n_ > 1 && t > s) s = t;
     }
-    s.tuple = distinct;
-    return s;
+    std::string out = "b" + std::to_string(b.content) + "[";
+    for (long long x : s) out += std::to_string(x) + ",";
+    return out + "]";
 }
 
-// Keeps at most `limit` factors by materializing the product of the leading
-// ones over their joint ids (rare: very long fold chains).
-std::vector<Contractor::View> Contractor::limit_factors(std::vector<View> fs, std::size_t limit) {
-    while (fs.size() > limit) {
-        const std::size_t take = std::min<std::size_t>(kMaxFactors, fs.size() - limit + 1);
-        std::vector<View> head(fs.begin(), fs.begin() + static_cast<std::ptrdiff_t>(take));
-        std::uint32_t ids = 0;
-        for (const View& v : head) ids |= v.ids;
-        std::vector<int> layout = ids_of(ids);
-        Buf b = stream_to_buffer(head, layout, 0, nullptr);
-        fs.erase(fs.begin(), fs.begin() + static_cast<std::ptrdiff_t>(take));
-        fs.insert(fs.begin(), output_view(b, layout));
+int Program::stream(std::vector<View> factors, const std::vector<int>& out_ids, std::uint32_t sum, double* ext) {
+    // keep within the kernel's factor budget: form the product of the leading
+    // factors over their own ids first
+    while (factors.size() > static_cast<std::size_t>(kMaxFactors)) {
+        std::vector<View> head(factors.begin(), factors.begin() + kMaxFactors);
+        std::vector<int> layout = ids_of(ids_of_views(head));
+        int b = stream(head, layout, 0, nullptr);
+        factors.erase(factors.begin(), factors.begin() + kMaxFactors);
+        factors.insert(factors.begin(), view_of(b, layout));
     }
-    return fs;
+    if (static_cast<int>(out_ids.size()) + std::popcount(sum) > kMaxDims)
+        fail(ErrorCode::InvalidArgument, "contraction step spans too many indices for the stream kernel");
+    std::string key;
+    if (!ext && sharing()) {
+        std::vector<int> sums = ids_of(sum);
+        std::sort(sums.begin(), sums.end());
+        std::string best;
+        do {
+            std::vector<int> dims = out_ids;
+            dims.insert(dims.end(), sums.begin(), sums.end());
+            std::vector<std::string> ds;
+            for (const View& v : factors) ds.push_back(desc(v, dims));
+            std::sort(ds.begin(), ds.end());
+            std::string k = "S" + std::to_string(out_ids.size()) + ":";
+            for (auto& d : ds) k += d;
+            if (best.empty() || k < best) best = k;
+        } while (std::next_permutation(sums.begin(), sums.end()));
+        key = best;
+        auto hit = memo_.find(key);
+        if (hit != memo_.end()) {
+            if (stats_) ++stats_->shared_hits;
+            return hit->second;
+        }
+    }
+    Op op;
+    op.factors = std::move(factors);
+    op.out_ids = out_ids;
+    op.sum = sum;
+    op.ext = ext;
+    if (!ext) op.out = new_buf(static_cast<int>(out_ids.size()), false);
+    ops_.push_back(op);
+    if (!key.empty()) {
+        memo_[key] = op.out;
+        memo_log_.push_back(key);
+    }
+    return op.out;
 }
 
-Buf Contractor::stream_to_buffer(std::vector<View> factors, const std::vector<int>& out_ids,
-                                 std::uint32_t sum_ids, double* out_ptr) {
-    factors = limit_factors(std::move(factors), kMaxFactors);
-    std::vector<int> sums = ids_of(sum_ids);
-    // Innermost summed dim: the one most factors read with unit stride
-    // (symmetric matrices can be read in either orientation).
+int Program::gemm(std::vector<View> fa, std::vector<View> fb, const std::vector<int>& ra_in,
+                  const std::vector<int>& rb_in, int e, std::vector<int>* layout) {
+    std::vector<int> ra = ra_in, rb = rb_in;
+    // Multi-factor (Hadamard / scaled / Khatri-Rao) operands are formed once,
+    // k-major (rows..., e): O(rows*n) traffic against O(rows*cols*n) DMMA work.
+    auto lower = [&](std::vector<View>& fs, const std::vector<int>& rows) {
+        if (fs.size() <= 1) return;
+        std::vector<int> lay = rows;
+        lay.push_back(e);
+        int b = stream(fs, lay, 0, nullptr);
+        fs = {view_of(b, lay)};
+    };
+    lower(fa, ra);
+    lower(fb, rb);
+    std::vector<int> da = ra, db = rb;
+    da.push_back(e);
+    db.push_back(e);
+    std::string ka = desc(fa[0], da), kb = desc(fb[0], db);
+    if (kb < ka) {
+        std::swap(fa, fb);
+        std::swap(ra, rb);
+        std::swap(ka, kb);
+    }
+    *layout = ra;
+    layout->insert(layout->end(), rb.begin(), rb.end());
+    std::string key = "G" + std::to_string(ra.size()) + "." + std::to_string(rb.size()) + ":" + ka + "|" + kb;
+    if (sharing()) {
+        auto hit = memo_.find(key);
+        if (hit != memo_.end()) {
+            if (stats_) ++stats_->shared_hits;
+            return hit->second;
+        }
+    }
+    const bool sym = ka == kb && ra.size() == 1 && rb.size() == 1 && config_.device.exploit_symmetry;
+    Op op;
+    op.gemm = true;
+    op.fa = std::move(fa);
+    op.fb = std::move(fb);
+    op.ra = ra;
+    op.rb = rb;
+    op.e = e;
+    op.symmetric_out = sym;
+    op.out = new_buf(static_cast<int>(ra.size() + rb.size()), sym);
+    ops_.push_back(op);
+    if (sharing()) {
+        memo_[key] = op.out;
+        memo_log_.push_back(key);
+    }
+    return op.out;
+}
+
+void Program::rollback(const Mark& m) {
+    for (std::size_t i = m.log; i < memo_log_.size(); ++i) memo_.erase(memo_log_[i]);
+    memo_log_.resize(m.log);
+    ops_.resize(m.ops);
+    bufs_.resize(m.bufs);
+}
+
+double Program::cost_since(const Mark& m) const {
+    // 1 streamed entry ~ 23 DMMA MACs on B200 (8 B at 6.5 TB/s vs 18.6 TMAC/s)
+    double c = 0.0;
+    for (std::size_t i = m.ops; i < ops_.size(); ++i) {
+        const Op& op = ops_[i];
+        if (op.gemm) {
+            c += static_cast<double>(ipow(n_, static_cast<int>(op.ra.size() + op.rb.size()) + 1));
+        } else {
+            const int dims = static_cast<int>(op.out_ids.size()) + std::popcount(op.sum);
+            c += 23.0 * static_cast<double>(ipow(n_, dims)) * static_cast<double>(op.factors.size());
+        }
+    }
+    return c;
+}
+
+// A reduction whose only input from a GEMM output is that GEMM, and whose
+// iteration space is exactly the GEMM's (row, col) space, runs in the GEMM's
+// epilogue: its other factors become epilogue weights, a second read of the
+// GEMM output becomes self_power = 2, and its result (scalar, vector or an
+// elementwise product) is written straight from the accumulators.
+void Program::fuse_into_gemm(std::size_t s_idx) {
+    Op& s = ops_[s_idx];
+    std::vector<int> uses(bufs_.size(), 0);
+    for (const Op& op : ops_) {
+        if (op.dead) continue;
+        for (const auto* vs : {&op.factors, &op.fa, &op.fb, &op.w})
+            for (const View& v : *vs) ++uses[static_cast<std::size_t>(v.buf)];
+    }
+    for (std::size_t g_idx = 0; g_idx < s_idx; ++g_idx) {
+        Op& g = ops_[g_idx];
+        if (g.dead || !g.gemm || g.mode != kEpiStore || g.ext || g.w.size() || g.ra.size() != 1 || g.rb.size() != 1)
+            continue;
+        const int gb = g.out;
+        std::vector<View> mine, rest;
+        for (const View& v : s.factors) (v.buf == gb ? mine : rest).push_back(v);
+        if (mine.empty() || mine.size() > 2 || uses[static_cast<std::size_t>(gb)] != static_cast<int>(mine.size()))
+            continue;
+        // the GEMM output's axes as seen by s: row -> x, col -> y
+        int x = -1, y = -1;
+        for (int id : ids_of(mine[0].ids)) {
+            if (mine[0].stride[static_cast<std::size_t>(id)] == n_) x = id;
+            if (mine[0].stride[static_cast<std::size_t>(id)] == 1) y = id;
+        }
+        if (x < 0 || y < 0 || x == y || std::popcount(mine[0].ids) != 2) continue;
+        bool consistent = true;
+        for (const View& v : mine) {
+            const bool same = v.stride[static_cast<std::size_t>(x)] == n_ && v.stride[static_cast<std::size_t>(y)] == 1;
+            const bool flip = v.stride[static_cast<std::size_t>(x)] == 1 && v.stride[static_cast<std::size_t>(y)] == n_;
+            if (!(same || (flip && g.symmetric_out)) || std::popcount(v.ids) != 2) consistent = false;
+        }
+        if (!consistent) continue;
+        std::uint32_t space = bit(x) | bit(y);
+        std::uint32_t iter = s.sum;
+        for (int id : s.out_ids) iter |= bit(id);
+        if (iter != space || (ids_of_views(rest) & ~space)) continue;
+        int mode;
+        bool transpose = false;
+        if (s.out_ids.empty()) mode = kEpiSumAll;
+        else if (s.out_ids.size() == 1 && s.out_ids[0] == x) mode = kEpiSumCols;
+        else if (s.out_ids.size() == 1 && s.out_ids[0] == y) mode = kEpiSumRows;
+        else if (s.out_ids.size() == 2 && s.out_ids[0] == x && s.out_ids[1] == y) mode = kEpiStore;
+        else if (s.out_ids.size() == 2 && s.out_ids[0] == y && s.out_ids[1] == x) {
+            mode = kEpiStore;
+            transpose = true;  // compute the transposed product instead: swap the operands
+        } else continue;
+        bool sym_ok = g.symmetric_out && (mode == kEpiSumAll || mode == kEpiStore) && !transpose;
+        for (const View& w : rest) {
+            if (!bufs_[static_cast<std::size_t>(w.buf)].symmetric || w.ids != space) sym_ok = false;
+            else if (!((w.stride[static_cast<std::size_t>(x)] == n_ && w.stride[static_cast<std::size_t>(y)] == 1) ||
+                       (w.stride[static_cast<std::size_t>(x)] == 1 && w.stride[static_cast<std::size_t>(y)] == n_)))
+                sym_ok = false;
+        }
+        Op fused = g;
+        if (transpose) {
+            std::swap(fused.fa, fused.fb);
+            std::swap(fused.ra, fused.rb);
+            std::swap(x, y);
+        }
+        // epilogue factors in (row=x, col=y) terms: strides carried by id
+        fused.w = rest;
+        fused.self_power = static_cast<int>(mine.size());
+        fused.mode = mode;
+        fused.symmetric_out = sym_ok;
+        fused.out = s.out;
+        fused.ext = s.ext;
+        fused.epi_row = x;
+        fused.epi_col = y;
+        g.dead = true;
+        s = fused;
+        if (stats_) ++stats_->fused_epilogues;
+        return;
+    }
+}
+
+void Program::optimize() {
+    if (config_.device.fuse_epilogues)
+        for (std::size_t i = 0; i < ops_.size(); ++i)
+            if (!ops_[i].dead && !ops_[i].gemm) fuse_into_gemm(i);
+    for (SymBuf& b : bufs_) b.last_use = -1;
+    for (std::size_t i = 0; i < ops_.size(); ++i) {
+        const Op& op = ops_[i];
+        if (op.dead) continue;
+        for (const auto* vs : {&op.factors, &op.fa, &op.fb, &op.w})
+            for (const View& v : *vs) bufs_[static_cast<std::size_t>(v.buf)].last_use = static_cast<int>(i);
+    }
+}
+
+double* Program::ptr(int buf) const {
+    const SymBuf& b = bufs_[static_cast<std::size_t>(buf)];
+    if (!b.real) fail(ErrorCode::InvalidArgument, "executor: operand buffer not materialized");
+    return b.real->ptr;
+}
+
+void Program::run_stream(const Op& op, double* out) {
+    std::vector<View> factors = op.factors;
+    std::vector<int> sums = ids_of(op.sum);
+    const std::vector<int>& out_ids = op.out_ids;
     auto unit = [&](const View& v, int id) {
         if (!(v.ids & bit(id))) return false;
         if (v.stride[static_cast<std::size_t>(id)] == 1) return true;
-        return v.buf->symmetric && std::popcount(v.ids) == 2;
+        return bufs_[static_cast<std::size_t>(v.buf)].symmetric && std::popcount(v.ids) == 2;
     };
     if (!sums.empty()) {
         int best = sums.back(), best_score = -1;
         for (int id : sums) {
             int score = 0;
-            for (const View& v : factors) score += unit(v, id) ? (v.buf->order >= 2 ? 4 : 1) : 0;
+            for (const View& v : factors)
+                score += unit(v, id) ? (bufs_[static_cast<std::size_t>(v.buf)].order >= 2 ? 4 : 1) : 0;
             if (score > best_score) {
                 best_score = score;
                 best = id;
@@ -234,7 +516,7 @@ Buf Contractor::stream_to_buffer(std::vector<View> factors, const std::vector<in
     if (!sums.empty()) {
         int cs = 0, co = 0;
         for (const View& v : factors) {
-            if (v.buf->symmetric) continue;
+            if (bufs_[static_cast<std::size_t>(v.buf)].symmetric) continue;
             cs += v.stride[static_cast<std::size_t>(sums.back())] == 1 && (v.ids & bit(sums.back()));
             if (!out_ids.empty())
                 co += v.stride[static_cast<std::size_t>(out_ids.back())] == 1 && (v.ids & bit(out_ids.back()));
@@ -245,68 +527,46 @@ Buf Contractor::stream_to_buffer(std::vector<View> factors, const std::vector<in
     }
     if (fast >= 0)
         for (View& v : factors) {
-            if (!v.buf->symmetric || std::popcount(v.ids) != 2 || !(v.ids & bit(fast))) continue;
+            if (!bufs_[static_cast<std::size_t>(v.buf)].symmetric || std::popcount(v.ids) != 2 || !(v.ids & bit(fast)))
+                continue;
             if (v.stride[static_cast<std::size_t>(fast)] == 1) continue;
             const int other = std::countr_zero(v.ids & ~bit(fast));
             std::swap(v.stride[static_cast<std::size_t>(fast)], v.stride[static_cast<std::size_t>(other)]);
         }
-
     StreamArgs a;
     a.nf = static_cast<int>(factors.size());
     a.n_out = static_cast<int>(out_ids.size());
     a.n_sum = static_cast<int>(sums.size());
     a.n = n_;
-    if (a.n_out + a.n_sum > kMaxDims)
-        fail(ErrorCode::InvalidArgument, "contraction step spans too many indices for the stream kernel");
     std::vector<int> dims = out_ids;
     dims.insert(dims.end(), sums.begin(), sums.end());
     for (int f = 0; f < a.nf; ++f) {
-        a.ptr[f] = factors[static_cast<std::size_t>(f)].buf->ptr;
+        a.ptr[f] = ptr(factors[static_cast<std::size_t>(f)].buf);
         for (std::size_t d = 0; d < dims.size(); ++d)
             a.stride[f][d] = factors[static_cast<std::size_t>(f)].stride[static_cast<std::size_t>(dims[d])];
     }
-    Buf result;
-    if (out_ptr) {
-        a.out = out_ptr;
-    } else {
-        result = rt_.allocate(static_cast<int>(out_ids.size()), n_);
-        a.out = result->ptr;
-    }
-    const std::size_t scratch_n = stream_scratch_entries(a, rt_.sm_count());
-    double* scratch = scratch_n ? rt_.scratch(scratch_n) : nullptr;
-    rt_.begin(Runtime::kStream);
-    const int launched = launch_stream(a, scratch, scratch_n, rt_.sm_count(), rt_.stream());
-    rt_.end(Runtime::kStream);
+    a.out = out;
+    const std::size_t scratch_n = stream_scratch_entries(a, rt_->sm_count());
+    double* scratch = scratch_n ? rt_->scratch(scratch_n) : nullptr;
+    rt_->begin(Runtime::kStream);
+    const int launched = launch_stream(a, scratch, scratch_n, rt_->sm_count(), rt_->stream());
+    rt_->end(Runtime::kStream);
     check_cuda(cudaGetLastError(), "stream kernel launch");
-    if (stats_) stats_->kernel_launches += static_cast<std::uint64_t>(launched);
-    rt_.release(scratch);
+    rt_->release(scratch);
     if (stats_) {
-        stats_->stream_entries += pw(a.n_out + a.n_sum) * static_cast<std::uint64_t>(a.nf);
+        stats_->stream_entries += ipow(n_, a.n_out + a.n_sum) * static_cast<std::uint64_t>(a.nf);
         ++stats_->stream_launches;
+        stats_->kernel_launches += static_cast<std::uint64_t>(launched);
     }
-    return result;
 }
 
-Buf Contractor::gemm_to_buffer(std::vector<View> fa, std::vector<View> fb, const std::vector<int>& ra,
-                               const std::vector<int>& rb, int e) {
-    // Multi-factor (Hadamard / scaled / Khatri-Rao) operands are formed once
-    // by a stream kernel into a k-major buffer (rows..., e): O(rows*n) traffic
-    // against O(rows*cols*n) DMMA work, and the GEMM then runs the TMA path.
-    auto flatten = [&](std::vector<View>& fs, const std::vector<int>& rows) {
-        if (fs.size() <= 1) return;
-        std::vector<int> layout = rows;
-        layout.push_back(e);
-        Buf m = stream_to_buffer(fs, layout, 0, nullptr);
-        fs = {output_view(m, layout)};
-    };
-    flatten(fa, ra);
-    flatten(fb, rb);
-    fa = limit_factors(std::move(fa), kMaxGemmFactors);
-    fb = limit_factors(std::move(fb), kMaxGemmFactors);
-    // Orient symmetric factors so the inner (k) index is their fast axis.
+void Program::run_gemm(const Op& op, double* out) {
+    std::vector<View> fa = op.fa, fb = op.fb;
+    const int e = op.e;
     for (auto* side : {&fa, &fb})
         for (View& v : *side) {
-            if (!v.buf->symmetric || std::popcount(v.ids) != 2 || !(v.ids & bit(e))) continue;
+            if (!bufs_[static_cast<std::size_t>(v.buf)].symmetric || std::popcount(v.ids) != 2 || !(v.ids & bit(e)))
+                continue;
             if (v.stride[static_cast<std::size_t>(e)] == 1) continue;
             const int other = std::countr_zero(v.ids & ~bit(e));
             std::swap(v.stride[static_cast<std::size_t>(e)], v.stride[static_cast<std::size_t>(other)]);
@@ -316,70 +576,135 @@ Buf Contractor::gemm_to_buffer(std::vector<View> fa, std::vector<View> fb, const
         side.nr = static_cast<int>(rows.size());
         for (int f = 0; f < side.nf; ++f) {
             const View& v = fs[static_cast<std::size_t>(f)];
-            side.ptr[f] = v.buf->ptr;
+            side.ptr[f] = ptr(v.buf);
             side.kstride[f] = v.stride[static_cast<std::size_t>(e)];
             for (int d = 0; d < side.nr; ++d)
                 side.rstride[f][d] = v.stride[static_cast<std::size_t>(rows[static_cast<std::size_t>(d)])];
         }
     };
-    // k-major loads when the biggest factor is contiguous along k.
     auto kmajor = [&](const std::vector<View>& fs, const std::vector<int>& rows) {
-        const View* big = &fs[0];
-        for (const View& v : fs)
-            if (v.buf->order > big->buf->order) big = &v;
-        if (big->stride[static_cast<std::size_t>(e)] == 1) return 1;
-        if (!rows.empty() && big->stride[static_cast<std::size_t>(rows.back())] == 1) return 0;
+        const View& big = fs[0];
+        if (big.stride[static_cast<std::size_t>(e)] == 1) return 1;
+        if (!rows.empty() && big.stride[static_cast<std::size_t>(rows.back())] == 1) return 0;
         return 1;
     };
     GemmArgs g;
-    fill(g.a, fa, ra);
-    fill(g.b, fb, rb);
+    fill(g.a, fa, op.ra);
+    fill(g.b, fb, op.rb);
     g.n = n_;
-    g.rows = static_cast<long long>(pw(static_cast<int>(ra.size())));
-    g.cols = static_cast<long long>(pw(static_cast<int>(rb.size())));
-    g.a_kmajor = kmajor(fa, ra);
-    g.b_kmajor = kmajor(fb, rb);
-    g.mode = kEpiStore;
-    Buf out = rt_.allocate(static_cast<int>(ra.size() + rb.size()), n_);
-    g.out = out->ptr;
-    rt_.begin(Runtime::kGemm);
-    const int launched = launch_gemm(g, rt_.stream());
-    rt_.end(Runtime::kGemm);
-    check_cuda(cudaGetLastError(), "gemm launch");
-    if (stats_) stats_->kernel_launches += static_cast<std::uint64_t>(launched);
-    if (stats_) {
-        stats_->gemm_macs += static_cast<std::uint64_t>(g.rows) * static_cast<std::uint64_t>(g.cols) *
-                             static_cast<std::uint64_t>(n_);
-        ++stats_->gemm_launches;
+    g.rows = static_cast<long long>(ipow(n_, static_cast<int>(op.ra.size())));
+    g.cols = static_cast<long long>(ipow(n_, static_cast<int>(op.rb.size())));
+    g.a_kmajor = kmajor(fa, op.ra);
+    g.b_kmajor = kmajor(fb, op.rb);
+    g.mode = op.mode;
+    g.self_power = op.self_power;
+    g.symmetric_out = op.symmetric_out ? 1 : 0;
+    g.out = out;
+    // epilogue weights over (row, col) = the consumer's ids epi_row / epi_col
+    g.w.nf = static_cast<int>(op.w.size());
+    for (int f = 0; f < g.w.nf; ++f) {
+        const View& v = op.w[static_cast<std::size_t>(f)];
+        g.w.ptr[f] = ptr(v.buf);
+        g.w.rstride[f][0] = v.stride[static_cast<std::size_t>(op.epi_row)];
+        g.w.cstride[f][0] = v.stride[static_cast<std::size_t>(op.epi_col)];
     }
-    return out;
+    const std::size_t part_n = gemm_partial_entries(g);
+    g.partial = part_n ? rt_->scratch(part_n) : nullptr;
+    rt_->begin(Runtime::kGemm);
+    const int launched = launch_gemm(g, rt_->stream());
+    rt_->end(Runtime::kGemm);
+    check_cuda(cudaGetLastError(), "gemm launch");
+    rt_->release(g.partial);
+    if (stats_) {
+        const bool tri = g.symmetric_out && g.rows == g.cols && (g.mode == kEpiStore || g.mode == kEpiSumAll) &&
+                         gemm_tma_eligible(g, nullptr, nullptr);
+        const long long tm = (g.rows + 127) / 128;
+        const std::uint64_t full = static_cast<std::uint64_t>(g.rows) * static_cast<std::uint64_t>(g.cols) *
+                                   static_cast<std::uint64_t>(n_);
+        stats_->gemm_macs += tri ? full / static_cast<std::uint64_t>(tm * tm) *
+                                       static_cast<std::uint64_t>(tm * (tm + 1) / 2)
+                                 : full;
+        ++stats_->gemm_launches;
+        stats_->kernel_launches += static_cast<std::uint64_t>(launched);
+        if (tri) ++stats_->symmetric_gemms;
+    }
 }
 
-// Lazy marginalization: the sum is recorded on the slot and formed by the
-// kernel that finally consumes (or materializes) it.
+void Program::launch(Op& op) {
+    double* out = op.ext;
+    if (!out) {
+        SymBuf& b = bufs_[static_cast<std::size_t>(op.out)];
+        if (!b.real) b.real = rt_->allocate(b.order, n_);
+        b.real->symmetric = b.symmetric;
+        out = b.real->ptr;
+    }
+    if (op.gemm) run_gemm(op, out);
+    else run_stream(op, out);
+}
+
+void Program::execute() {
+    for (std::size_t i = 0; i < ops_.size(); ++i) {
+        Op& op = ops_[i];
+        if (op.dead) continue;
+        launch(op);
+        for (const auto* vs : {&op.factors, &op.fa, &op.fb, &op.w})
+            for (const View& v : *vs) {
+                SymBuf& b = bufs_[static_cast<std::size_t>(v.buf)];
+                if (!b.input && b.last_use == static_cast<int>(i) && b.real && b.real.use_count() == 1 && !keep_.count(v.buf))
+                    b.real.reset();
+            }
+    }
+}
+
+Buf Program::take(int buf) { return bufs_[static_cast<std::size_t>(buf)].real; }
+
+// -------------------------------------------------------------- Contractor
+std::uint64_t Contractor::pw(int e) const { return ipow(p_.n(), e); }
+
+void Contractor::cap(int order) {
+    if (count_) checked_entry_count(order, static_cast<int>(p_.n()), p_.config());
+}
+
+void Contractor::owned(int order) {
+    if (count_) count_->ref_peak = std::max(count_->ref_peak, pw(order));
+}
+
+Contractor::Slot Contractor::slot_of(int buf, const IndexTuple& tuple) {
+    Slot s;
+    s.factors.push_back(p_.view_of(buf, tuple));
+    s.ids = s.factors[0].ids;
+    std::uint32_t seen = 0;
+    bool repeat = false;
+    for (int id : tuple) {
+        if (seen & bit(id)) repeat = true;
+        seen |= bit(id);
+    }
+    if (repeat) {  // extract_diagonal (einsum.cpp:183-206): a strided view here
+        cap(std::popcount(seen));
+        owned(std::popcount(seen));
+        s.owned = true;
+    }
+    return s;
+}
+
+std::vector<View> Contractor::formed(const Slot& s) {
+    const std::uint32_t pend = ids_of_views(s.factors) & ~s.ids;
+    if (!pend) return s.factors;
+    std::vector<int> layout = ids_of(s.ids);
+    int b = p_.stream(s.factors, layout, pend, nullptr);
+    return {p_.view_of(b, layout)};
+}
+
 Contractor::Slot Contractor::marginalize(const Slot& s, std::uint32_t summed) {
     const int kept = std::popcount(s.ids & ~summed);
-    ref_count_alloc(kept);
-    if (stats_) stats_->ref_madds += pw(std::popcount(s.ids));
-    ref_owned(kept);
+    cap(kept);
+    if (count_) count_->ref_madds += pw(std::popcount(s.ids));
+    owned(kept);
     Slot r = s;
     r.ids = s.ids & ~summed;
     r.owned = true;
-    IndexTuple t;
-    for (int id : s.tuple)
-        if (!(summed & bit(id))) t.push_back(id);
-    r.tuple = t;
-    // pending sums are the ids present in factors but not in the slot
     return r;
 }
-
-namespace {
-std::uint32_t pending_of(const Contractor::Slot& s) {
-    std::uint32_t all = 0;
-    for (const auto& v : s.factors) all |= v.ids;
-    return all & ~s.ids;
-}
-}  // namespace
 
 Contractor::Slot Contractor::gemm_step(const Slot& a, const Slot& b, int e) {
     std::vector<int> ra, rb;
@@ -387,36 +712,25 @@ Contractor::Slot Contractor::gemm_step(const Slot& a, const Slot& b, int e) {
         if (id != e) ra.push_back(id);
     for (int id : ids_of(b.ids))
         if (id != e) rb.push_back(id);
-    ref_count_alloc(std::popcount(a.ids));
-    ref_count_alloc(std::popcount(b.ids));
-    ref_count_alloc(static_cast<int>(ra.size() + rb.size()));
-    if (stats_) stats_->ref_madds += pw(static_cast<int>(ra.size())) * pw(1) * pw(static_cast<int>(rb.size()));
-    ref_owned(static_cast<int>(ra.size() + rb.size()));
-
-    auto operand = [&](const Slot& s) {
-        if (!pending_of(s)) return s.factors;
-        std::vector<int> layout = ids_of(s.ids);
-        Buf m = stream_to_buffer(s.factors, layout, pending_of(s), nullptr);
-        return std::vector<View>{output_view(m, layout)};
-    };
-    std::vector<int> layout = ra;
-    layout.insert(layout.end(), rb.begin(), rb.end());
-    Buf out;
-    if (ra.size() <= static_cast<std::size_t>(kMaxRowDims) && rb.size() <= static_cast<std::size_t>(kMaxRowDims)) {
-        out = gemm_to_buffer(operand(a), operand(b), ra, rb, e);
-    } else {
-        std::vector<View> all = operand(a);
-        std::vector<View> fb = operand(b);
-        all.insert(all.end(), fb.begin(), fb.end());
-        out = stream_to_buffer(all, layout, bit(e), nullptr);
-    }
+    cap(std::popcount(a.ids));
+    cap(std::popcount(b.ids));
+    cap(static_cast<int>(ra.size() + rb.size()));
+    if (count_) count_->ref_madds += pw(static_cast<int>(ra.size())) * pw(1) * pw(static_cast<int>(rb.size()));
+    owned(static_cast<int>(ra.size() + rb.size()));
     Slot r;
-    r.factors.push_back(output_view(out, layout));
-    r.ids = r.factors[0].ids;
     r.owned = true;
-    std::vector<int> t = ra;
-    t.insert(t.end(), rb.begin(), rb.end());
-    r.tuple = t;
+    r.ids = (a.ids | b.ids) & ~bit(e);
+    std::vector<View> fa = formed(a), fb = formed(b);
+    if (ra.size() <= static_cast<std::size_t>(kMaxRowDims) && rb.size() <= static_cast<std::size_t>(kMaxRowDims)) {
+        std::vector<int> layout;
+        int buf = p_.gemm(fa, fb, ra, rb, e, &layout);
+        r.factors.push_back(p_.view_of(buf, layout));
+    } else {
+        fa.insert(fa.end(), fb.begin(), fb.end());
+        std::vector<int> layout = ids_of(r.ids);
+        int buf = p_.stream(fa, layout, bit(e), nullptr);
+        r.factors.push_back(p_.view_of(buf, layout));
+    }
     return r;
 }
 
@@ -425,57 +739,46 @@ Contractor::Slot Contractor::generic_step(const std::vector<Slot>& parts, int e)
     for (const Slot& p : parts) uni |= p.ids;
     uni &= ~bit(e);
     const int out_order = std::popcount(uni);
-    ref_count_alloc(out_order);
-    if (stats_) stats_->ref_madds += pw(out_order) * pw(1) * parts.size();
-    ref_owned(out_order);
+    cap(out_order);
+    if (count_) count_->ref_madds += pw(out_order) * pw(1) * parts.size();
+    owned(out_order);
 
-    // Khatri-Rao lowering: operands meeting only at e -> (rows of all but the
-    // widest) x (rows of the widest) DMMA GEMM.
     bool disjoint = true;
     std::uint32_t seen = 0;
     for (const Slot& p : parts) {
-        std::uint32_t rest = p.ids & ~bit(e);
+        const std::uint32_t rest = p.ids & ~bit(e);
         if (rest & seen) disjoint = false;
         seen |= rest;
     }
-    std::vector<View> fa, fb;
     std::size_t widest = 0;
     for (std::size_t i = 1; i < parts.size(); ++i)
         if (std::popcount(parts[i].ids) >= std::popcount(parts[widest].ids)) widest = i;
-    std::uint32_t rows_mask = 0;
+    std::vector<View> fa, fb;
+    std::uint32_t rows = 0;
     for (std::size_t i = 0; i < parts.size(); ++i) {
-        std::vector<View> fs = parts[i].factors;
-        if (pending_of(parts[i])) {
-            std::vector<int> layout = ids_of(parts[i].ids);
-            Buf m = stream_to_buffer(fs, layout, pending_of(parts[i]), nullptr);
-            fs = {output_view(m, layout)};
-        }
+        std::vector<View> fs = formed(parts[i]);
         if (i == widest) {
             fb.insert(fb.end(), fs.begin(), fs.end());
         } else {
             fa.insert(fa.end(), fs.begin(), fs.end());
-            rows_mask |= parts[i].ids & ~bit(e);
+            rows |= parts[i].ids & ~bit(e);
         }
     }
-    const std::vector<int> ra = ids_of(rows_mask);
-    const std::vector<int> rb = ids_of(parts[widest].ids & ~bit(e));
-    std::vector<int> layout = ra;
-    layout.insert(layout.end(), rb.begin(), rb.end());
-    Buf out;
+    const std::vector<int> ra = ids_of(rows), rb = ids_of(parts[widest].ids & ~bit(e));
+    Slot r;
+    r.owned = true;
+    r.ids = uni;
     if (disjoint && !ra.empty() && !rb.empty() && ra.size() <= static_cast<std::size_t>(kMaxRowDims) &&
         rb.size() <= static_cast<std::size_t>(kMaxRowDims)) {
-        out = gemm_to_buffer(fa, fb, ra, rb, e);
+        std::vector<int> layout;
+        int buf = p_.gemm(fa, fb, ra, rb, e, &layout);
+        r.factors.push_back(p_.view_of(buf, layout));
     } else {
-        layout = ids_of(uni);
-        std::vector<View> all = fa;
-        all.insert(all.end(), fb.begin(), fb.end());
-        out = stream_to_buffer(all, layout, bit(e), nullptr);
+        fa.insert(fa.end(), fb.begin(), fb.end());
+        std::vector<int> layout = ids_of(uni);
+        int buf = p_.stream(fa, layout, bit(e), nullptr);
+        r.factors.push_back(p_.view_of(buf, layout));
     }
-    Slot r;
-    r.factors.push_back(output_view(out, layout));
-    r.ids = uni;
-    r.owned = true;
-    r.tuple = ids_of(uni);
     return r;
 }
 
@@ -492,7 +795,7 @@ void Contractor::eliminate_one(std::vector<Slot>& slots, int e) {
         }
     }
     if (parts.empty()) return;
-    if (stats_) ++stats_->steps;
+    if (count_) ++count_->steps;
 
     for (bool folded = true; folded && parts.size() > 1;) {
         folded = false;
@@ -502,17 +805,12 @@ void Contractor::eliminate_one(std::vector<Slot>& slots, int e) {
                 if (std::popcount(parts[i].ids) > std::popcount(parts[j].ids)) continue;
                 if ((parts[i].ids & ~parts[j].ids) != 0) continue;
                 if (!parts[j].owned) {
-                    ref_owned(std::popcount(parts[j].ids));
+                    owned(std::popcount(parts[j].ids));
                     parts[j].owned = true;
                 }
-                if (stats_) stats_->ref_madds += pw(std::popcount(parts[j].ids));
-                Slot src = parts[i];
-                if (pending_of(src)) {  // a pending sum must not leak into the target's space
-                    std::vector<int> layout = ids_of(src.ids);
-                    Buf m = stream_to_buffer(src.factors, layout, pending_of(src), nullptr);
-                    src.factors = {output_view(m, layout)};
-                }
-                parts[j].factors.insert(parts[j].factors.end(), src.factors.begin(), src.factors.end());
+                if (count_) count_->ref_madds += pw(std::popcount(parts[j].ids));
+                std::vector<View> src = formed(parts[i]);  // a pending sum must not leak into the target
+                parts[j].factors.insert(parts[j].factors.end(), src.begin(), src.end());
                 parts.erase(parts.begin() + static_cast<std::ptrdiff_t>(i));
                 folded = true;
                 break;
@@ -520,26 +818,22 @@ void Contractor::eliminate_one(std::vector<Slot>& slots, int e) {
     }
 
     Slot result;
-    if (parts.size() == 1) {
-        result = marginalize(parts[0], bit(e));
-    } else if (parts.size() == 2 && std::popcount(parts[0].ids & parts[1].ids) == 1) {
-        result = gemm_step(parts[0], parts[1], e);
-    } else {
-        result = generic_step(parts, e);
-    }
+    if (parts.size() == 1) result = marginalize(parts[0], bit(e));
+    else if (parts.size() == 2 && std::popcount(parts[0].ids & parts[1].ids) == 1) result = gemm_step(parts[0], parts[1], e);
+    else result = generic_step(parts, e);
     slots.push_back(std::move(result));
 }
 
-Buf Contractor::run(const std::vector<Buf>& inputs, const EinsumNotation& notation,
-                    const EliminationOrder& order, double* scalar_out) {
+int Contractor::run(const std::vector<int>& inputs, const EinsumNotation& notation, const EliminationOrder& order,
+                    double* scalar_out) {
     const std::size_t K = notation.inputs.size();
     if (inputs.size() != K)
-        fail(ErrorCode::ShapeMismatch, "notation expects " + std::to_string(K) + " tensors, got " +
-                                           std::to_string(inputs.size()));
+        fail(ErrorCode::ShapeMismatch,
+             "notation expects " + std::to_string(K) + " tensors, got " + std::to_string(inputs.size()));
     for (std::size_t k = 0; k < K; ++k)
-        if (inputs[k]->order != static_cast<int>(notation.inputs[k].size()))
+        if (p_.buf(inputs[k]).order != static_cast<int>(notation.inputs[k].size()))
             fail(ErrorCode::ShapeMismatch, "tensor " + std::to_string(k) + " has order " +
-                                               std::to_string(inputs[k]->order) + " but its tuple has " +
+                                               std::to_string(p_.buf(inputs[k]).order) + " but its tuple has " +
                                                std::to_string(notation.inputs[k].size()) + " indices");
     if (notation.index_count > kMaxIds)
         fail(ErrorCode::InvalidArgument, "device executor supports at most 16 indices per notation");
@@ -563,45 +857,39 @@ Buf Contractor::run(const std::vector<Buf>& inputs, const EinsumNotation& notati
         eliminate_one(slots, e);
     }
 
-    // assembly (einsum.cpp:466-485): product of the surviving slots. Pending
-    // sums of all but the widest slot are formed first so the final kernel
-    // iterates one slot's space only.
+    // assembly (einsum.cpp:466-485): one kernel over the widest slot's
+    // pending sums; other pending sums are formed first.
     const int out_order = static_cast<int>(notation.output.size());
-    ref_count_alloc(out_order);
-    if (stats_) stats_->ref_madds += pw(out_order) * slots.size();
+    cap(out_order);
+    if (count_) count_->ref_madds += pw(out_order) * slots.size();
     std::size_t widest = 0;
+    auto pend = [&](const Slot& s) { return ids_of_views(s.factors) & ~s.ids; };
     for (std::size_t i = 0; i < slots.size(); ++i)
-        if (std::popcount(pending_of(slots[i])) > std::popcount(pending_of(slots[widest]))) widest = i;
+        if (std::popcount(pend(slots[i])) > std::popcount(pend(slots[widest]))) widest = i;
     std::vector<View> all;
     std::uint32_t sum_ids = 0;
     for (std::size_t i = 0; i < slots.size(); ++i) {
-        std::uint32_t pend = pending_of(slots[i]);
-        if (pend && i != widest) {
-            std::vector<int> layout = ids_of(slots[i].ids);
-            Buf m = stream_to_buffer(slots[i].factors, layout, pend, nullptr);
-            all.push_back(output_view(m, layout));
+        if (i != widest) {
+            std::vector<View> f = formed(slots[i]);
+            all.insert(all.end(), f.begin(), f.end());
         } else {
             all.insert(all.end(), slots[i].factors.begin(), slots[i].factors.end());
-            sum_ids |= pend;
+            sum_ids |= pend(slots[i]);
         }
     }
     std::vector<int> out_ids(notation.output.begin(), notation.output.end());
-    if (out_ids.empty() && scalar_out) {
-        stream_to_buffer(all, out_ids, sum_ids, scalar_out);
-        return nullptr;
-    }
-    return stream_to_buffer(all, out_ids, sum_ids, nullptr);
+    return p_.stream(all, out_ids, sum_ids, out_ids.empty() ? scalar_out : nullptr);
 }
 
-Buf Contractor::eliminate_single(const std::vector<Buf>& inputs, const std::vector<IndexTuple>& tuples,
-                                 int index, IndexTuple* result_tuple) {
+int Contractor::eliminate_single(const std::vector<int>& inputs, const std::vector<IndexTuple>& tuples, int index,
+                                 IndexTuple* result_tuple) {
     std::vector<Slot> slots;
     for (std::size_t k = 0; k < inputs.size(); ++k) slots.push_back(slot_of(inputs[k], tuples[k]));
     eliminate_one(slots, index);
     const Slot& r = slots.back();
     std::vector<int> asc = ids_of(r.ids);
     if (result_tuple) *result_tuple = asc;
-    return stream_to_buffer(r.factors, asc, pending_of(r), nullptr);
+    return p_.stream(r.factors, asc, ids_of_views(r.factors) & ~r.ids, nullptr);
 }
 
 // ------------------------------------------------------- statistic drivers
@@ -609,7 +897,6 @@ namespace {
 
 using Clock = std::chrono::steady_clock;
 
-// Fixed-shape pairwise tree in term order (engine.cpp:25-34).
 double pairwise(const double* x, std::size_t count) {
     if (count == 0) return 0.0;
     if (count <= 4) {
@@ -619,6 +906,36 @@ double pairwise(const double* x, std::size_t count) {
     }
     const std::size_t half = count / 2;
     return pairwise(x, half) + pairwise(x + half, count - half);
+}
+
+// Lone ids (one occurrence) are marginalized before the ordered loop, so
+// orders that differ only in their positions are the same plan.
+std::vector<std::vector<int>> candidate_orders(const EinsumNotation& nt, const EliminationOrder& ref,
+                                               std::size_t limit) {
+    std::vector<int> occ(static_cast<std::size_t>(nt.index_count), 0);
+    for (const auto& t : nt.inputs) {
+        std::uint32_t seen = 0;
+        for (int id : t)
+            if (!(seen & bit(id))) {
+                seen |= bit(id);
+                ++occ[static_cast<std::size_t>(id)];
+            }
+    }
+    auto project = [&](const std::vector<int>& o) {
+        std::vector<int> p;
+        for (int id : o)
+            if (occ[static_cast<std::size_t>(id)] > 1) p.push_back(id);
+        return p;
+    };
+    std::vector<std::vector<int>> out{ref.order};
+    std::vector<std::vector<int>> seen{project(ref.order)};
+    for (auto& o : optimal_orders(nt, ref.predicted_width, limit)) {
+        auto p = project(o);
+        if (std::find(seen.begin(), seen.end(), p) != seen.end()) continue;
+        seen.push_back(p);
+        out.push_back(std::move(o));
+    }
+    return out;
 }
 
 }  // namespace
@@ -647,22 +964,20 @@ TermPlan plan_terms(const std::vector<IndexTuple>& zero_sig, int m, long long n,
             plan.enumerated = bell_number(m);
         }
     }
-    const std::size_t T = parts.size();
-    for (std::size_t t = 0; t < T; ++t) {
-        plan.rgs.push_back(parts[t].rgs());
-        plan.mu.push_back(mobius_coefficient(parts[t]));
-        plan.notation.emplace_back(induced_signature(zero_sig, parts[t]));
+    for (const SetPartition& p : parts) {
+        plan.rgs.push_back(p.rgs());
+        plan.mu.push_back(mobius_coefficient(p));
+        plan.notation.emplace_back(induced_signature(zero_sig, p));
         plan.order.push_back(optimize_order(plan.notation.back(), static_cast<int>(n), config.strategy, config));
         plan.cost.push_back(static_cast<double>(plan.order.back().predicted_peak_entries));
     }
-    // LPT: heaviest term first onto the least-loaded rank (ties: lowest rank).
+    const std::size_t T = parts.size();
     plan.owner.assign(T, 0);
     const int W = std::max(1, config.device.world_size);
     if (W > 1) {
         std::vector<std::size_t> idx(T);
         std::iota(idx.begin(), idx.end(), 0);
-        std::stable_sort(idx.begin(), idx.end(),
-                         [&](std::size_t a, std::size_t b) { return plan.cost[a] > plan.cost[b]; });
+        std::stable_sort(idx.begin(), idx.end(), [&](std::size_t a, std::size_t b) { return plan.cost[a] > plan.cost[b]; });
         std::vector<double> load(static_cast<std::size_t>(W), 0.0);
         for (std::size_t t : idx) {
             auto w = static_cast<std::size_t>(std::min_element(load.begin(), load.end()) - load.begin());
@@ -673,19 +988,58 @@ TermPlan plan_terms(const std::vector<IndexTuple>& zero_sig, int m, long long n,
     return plan;
 }
 
+// Records every owned term into one Program: the reference order is walked
+// once for the reference-rule counters; the recorded order is the
+// width-optimal one that adds the least new work given earlier terms.
+void record_terms(Program& prog, const TermPlan& plan, const std::vector<int>& inputs, int rank, double* d_v,
+                  DevStats* counters) {
+    const Config& cfg = prog.config();
+    const bool reorder = cfg.device.reorder_for_sharing && cfg.device.share_subexpressions;
+    for (std::size_t t = 0; t < plan.rgs.size(); ++t) {
+        if (plan.owner[t] != rank) continue;
+        const EinsumNotation& nt = plan.notation[t];
+        const EliminationOrder& ref = plan.order[t];
+        EliminationOrder best = ref;
+        if (reorder) {
+            double best_cost = -1.0;
+            for (const auto& cand : candidate_orders(nt, ref, 2048)) {
+                Program::Mark mk = prog.mark();
+                EliminationOrder o = ref;
+                o.order = cand;
+                Contractor(prog, nullptr).run(inputs, nt, o, d_v + t);
+                const double c = prog.cost_since(mk);
+                prog.rollback(mk);
+                if (best_cost < 0 || c < best_cost * (1 - 1e-12)) {
+                    best_cost = c;
+                    best = o;
+                }
+            }
+        }
+        if (best.order == ref.order) {
+            Contractor(prog, counters).run(inputs, nt, ref, d_v + t);
+        } else {
+            Program::Mark mk = prog.mark();
+            Contractor(prog, counters).run(inputs, nt, ref, d_v + t);  // counters + cap checks
+            prog.rollback(mk);
+            Contractor(prog, nullptr).run(inputs, nt, best, d_v + t);
+        }
+    }
+}
+
 StatisticResult lattice_statistic(const std::vector<const double*>& inputs, bool inputs_on_device,
-                                  const std::vector<IndexTuple>& zero_sig, int m, long long n,
-                                  LatticeMode mode, const Config& config) {
+                                  const std::vector<IndexTuple>& zero_sig, int m, long long n, LatticeMode mode,
+                                  const Config& config) {
     StatisticResult res;
     Runtime& rt = Runtime::get(config.device.device);
     const auto t_up = Clock::now();
 
-    // Upload each distinct factor once; sparsify on device (tensor.cpp:54-76).
     std::map<const double*, Buf> by_ptr;
     std::vector<Buf> tensors;
     std::vector<std::pair<Buf, int*>> probes;
     int* flags = nullptr;
-    if (config.device.exploit_symmetry) check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&flags), sizeof(int) * zero_sig.size() + 4, rt.stream()), "alloc flags");
+    if (config.device.exploit_symmetry)
+        check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&flags), sizeof(int) * zero_sig.size() + 4, rt.stream()),
+                   "alloc flags");
     for (std::size_t k = 0; k < zero_sig.size(); ++k) {
         const int order = static_cast<int>(zero_sig[k].size());
         checked_entry_count(order, static_cast<int>(n), config);
@@ -696,8 +1050,7 @@ StatisticResult lattice_statistic(const std::vector<const double*>& inputs, bool
         }
         Buf b = rt.allocate(order, n);
         check_cuda(cudaMemcpyAsync(b->ptr, inputs[k], b->entries() * sizeof(double),
-                                   inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                                   rt.stream()),
+                                   inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, rt.stream()),
                    "upload");
         rt.begin(Runtime::kOther);
         if (mode == LatticeMode::Sparsified)
@@ -713,8 +1066,7 @@ StatisticResult lattice_statistic(const std::vector<const double*>& inputs, bool
     }
     if (!probes.empty()) {
         std::vector<int> host(probes.size());
-        check_cuda(cudaMemcpyAsync(host.data(), flags, sizeof(int) * probes.size(), cudaMemcpyDeviceToHost,
-                                   rt.stream()),
+        check_cuda(cudaMemcpyAsync(host.data(), flags, sizeof(int) * probes.size(), cudaMemcpyDeviceToHost, rt.stream()),
                    "flags");
         rt.sync();
         for (std::size_t i = 0; i < probes.size(); ++i) probes[i].first->symmetric = host[i] == 0;
@@ -731,13 +1083,18 @@ StatisticResult lattice_statistic(const std::vector<const double*>& inputs, bool
 
     double* d_v = rt.scratch(std::max<std::size_t>(T, 1));
     check_cuda(cudaMemsetAsync(d_v, 0, sizeof(double) * std::max<std::size_t>(T, 1), rt.stream()), "memset");
-    for (std::size_t t = 0; t < T; ++t) {
-        if (res.owner[t] != config.device.rank) continue;
-        Contractor c(rt, n, config, &res.stats);
-        c.run(tensors, plan.notation[t], plan.order[t], d_v + t);
+    {
+        Program prog(&rt, n, config, &res.stats);
+        std::vector<int> ids;
+        for (const Buf& b : tensors) ids.push_back(prog.add_input(b));
+        record_terms(prog, plan, ids, config.device.rank, d_v, &res.stats);
+        prog.optimize();
+        res.plan_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+        prog.execute();
     }
     res.v.assign(T, 0.0);
-    if (T) check_cuda(cudaMemcpyAsync(res.v.data(), d_v, sizeof(double) * T, cudaMemcpyDeviceToHost, rt.stream()), "D2H");
+    if (T)
+        check_cuda(cudaMemcpyAsync(res.v.data(), d_v, sizeof(double) * T, cudaMemcpyDeviceToHost, rt.stream()), "D2H");
     rt.release(d_v);
     tensors.clear();
     by_ptr.clear();
@@ -746,21 +1103,16 @@ StatisticResult lattice_statistic(const std::vector<const double*>& inputs, bool
     res.contract_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
 
     res.terms.resize(T);
-    res.mu.resize(T);
-    res.rgs.resize(T);
-    for (std::size_t t = 0; t < T; ++t) {
-        res.mu[t] = plan.mu[t];
-        res.rgs[t] = plan.rgs[t];
-        res.terms[t] = static_cast<double>(res.mu[t]) * res.v[t];
-    }
+    res.mu = plan.mu;
+    res.rgs = plan.rgs;
+    for (std::size_t t = 0; t < T; ++t) res.terms[t] = static_cast<double>(res.mu[t]) * res.v[t];
     res.value = combine_terms(res.terms);
     return res;
 }
 
-std::vector<double> contract_host(const std::vector<const double*>& inputs, const std::vector<int>& orders,
-                                  long long n, const EinsumNotation& notation, const EliminationOrder* order,
-                                  const Config& config, DevStats* stats) {
-    Runtime& rt = Runtime::get(config.device.device);
+namespace {
+std::vector<Buf> upload_all(Runtime& rt, const std::vector<const double*>& inputs, const std::vector<int>& orders,
+                            long long n) {
     std::map<std::pair<const double*, int>, Buf> by_ptr;
     std::vector<Buf> tensors;
     for (std::size_t k = 0; k < inputs.size(); ++k) {
@@ -771,28 +1123,96 @@ std::vector<double> contract_host(const std::vector<const double*>& inputs, cons
             continue;
         }
         Buf b = rt.allocate(orders[k], n);
-        check_cuda(cudaMemcpyAsync(b->ptr, inputs[k], b->entries() * sizeof(double), cudaMemcpyHostToDevice,
-                                   rt.stream()),
+        check_cuda(cudaMemcpyAsync(b->ptr, inputs[k], b->entries() * sizeof(double), cudaMemcpyHostToDevice, rt.stream()),
                    "upload");
         by_ptr[key] = b;
         tensors.push_back(b);
     }
+    return tensors;
+}
+
+std::vector<double> download(Runtime& rt, const Buf& out) {
+    std::vector<double> host(out->entries());
+    check_cuda(cudaMemcpyAsync(host.data(), out->ptr, host.size() * sizeof(double), cudaMemcpyDeviceToHost, rt.stream()),
+               "D2H");
+    rt.sync();
+    return host;
+}
+}  // namespace
+
+std::vector<double> contract_host(const std::vector<const double*>& inputs, const std::vector<int>& orders, long long n,
+                                  const EinsumNotation& notation, const EliminationOrder* order, const Config& config,
+                                  DevStats* stats) {
+    Runtime& rt = Runtime::get(config.device.device);
+    std::vector<Buf> tensors = upload_all(rt, inputs, orders, n);
     EliminationOrder chosen;
     if (!order) {
         chosen = optimize_order(notation, static_cast<int>(n), config.strategy, config);
         order = &chosen;
     }
-    Contractor c(rt, n, config, stats);
-    Buf out = c.run(tensors, notation, *order, nullptr);
-    std::vector<double> host(out->entries());
-    check_cuda(cudaMemcpyAsync(host.data(), out->ptr, host.size() * sizeof(double), cudaMemcpyDeviceToHost,
-                               rt.stream()),
-               "D2H");
-    out.reset();
-    tensors.clear();
-    by_ptr.clear();
-    rt.sync();
-    return host;
+    Buf out;
+    {
+        Program prog(&rt, n, config, stats);
+        std::vector<int> ids;
+        for (const Buf& b : tensors) ids.push_back(prog.add_input(b));
+        const int res = Contractor(prog, stats).run(ids, notation, *order, nullptr);
+        prog.keep(res);
+        prog.optimize();
+        prog.execute();
+        out = prog.take(res);
+    }
+    return download(rt, out);
+}
+
+std::vector<double> eliminate_host(const std::vector<const double*>& inputs, const std::vector<IndexTuple>& tuples,
+                                   long long n, int index, const Config& config, DevStats* stats,
+                                   IndexTuple* result_tuple) {
+    Runtime& rt = Runtime::get(config.device.device);
+    std::vector<int> orders;
+    for (const auto& t : tuples) orders.push_back(static_cast<int>(t.size()));
+    std::vector<Buf> tensors = upload_all(rt, inputs, orders, n);
+    Buf out;
+    {
+        Program prog(&rt, n, config, stats);
+        std::vector<int> ids;
+        for (const Buf& b : tensors) ids.push_back(prog.add_input(b));
+        const int res = Contractor(prog, stats).eliminate_single(ids, tuples, index, result_tuple);
+        prog.keep(res);
+        prog.optimize();
+        prog.execute();
+        out = prog.take(res);
+    }
+    return download(rt, out);
+}
+
+std::string plan_summary(const std::vector<IndexTuple>& zero_sig, int m, long long n, const Config& config,
+                         bool inputs_symmetric, Program::Totals* totals) {
+    TermPlan plan = plan_terms(zero_sig, m, n, LatticeMode::Sparsified, config);
+    DevStats stats;
+    Program prog(nullptr, n, config, &stats);
+    std::vector<int> ids;
+    std::map<std::pair<int, int>, int> same;  // identical (order) inputs alias only if the caller says so
+    for (const IndexTuple& t : zero_sig) ids.push_back(prog.add_symbolic_input(static_cast<int>(t.size()), inputs_symmetric));
+    // Treat all factors of equal order as the same tensor when symmetric inputs
+    // are declared (the BASELINE configs alias one matrix).
+    if (inputs_symmetric) {
+        std::map<int, int> first;
+        for (std::size_t k = 0; k < ids.size(); ++k) {
+            const int order = static_cast<int>(zero_sig[k].size());
+            if (order == 2) {
+                auto it = first.find(order);
+                if (it == first.end()) first[order] = ids[k];
+                else ids[k] = it->second;
+            }
+        }
+    }
+    std::vector<double> dummy(plan.rgs.size() + 1);
+    record_terms(prog, plan, ids, 0, dummy.data(), &stats);
+    prog.optimize();
+    if (totals) *totals = prog.totals();
+    std::string head = "terms=" + std::to_string(plan.rgs.size()) + " shared_hits=" + std::to_string(stats.shared_hits) +
+                       " ref_madds=" + std::to_string(stats.ref_madds) + "\n";
+    return head + prog.dump();
 }
 
 }  // namespace ustats::dev

@@ -1,15 +1,24 @@
-// Device executor: runs one einsum notation over device-resident tensors with
-// the reference's elimination semantics (proj/src/einsum.cpp:310-486) lowered
-// to two kernel families:
-//   * lazy Hadamard folds — a fold (fold_into, einsum.cpp:134-147) just
-//     appends a factor view to the target slot; nothing is materialized;
-//   * a "stream" kernel for every marginalization / generic step / assembly
-//     (the lazy product is formed on the fly while reducing);
-//   * the DMMA GEMM for two-operand steps and for K-way steps whose operands
-//     only share the eliminated index (Khatri-Rao rows).
-// Reference-rule counters (ExecStats semantics) are tallied symbolically along
-// the same walk so RunStats.multiply_adds matches the reference plan, while
-// executed DMMA MACs and streamed entries are tallied separately.
+// Device executor. Each V-term's notation is *recorded* into a Program with
+// the reference's elimination semantics (proj/src/einsum.cpp:310-486), then
+// the whole statistic's Program is optimized and launched:
+//   * lazy folds / marginalizations: a fold (fold_into, einsum.cpp:134-147)
+//     appends a factor view; a marginalization records a pending sum; both are
+//     formed inside whichever kernel consumes the slot;
+//   * every materialized intermediate is content-addressed: an op whose
+//     canonical form (kind, operand buffers' content ids and the stride
+//     pattern over its local dims) was already recorded — in this V-term or
+//     an earlier one — is not recorded again (the reference recomputes every
+//     sub-contraction of every V-term);
+//   * among the width-optimal elimination orders of a V-term, the one whose
+//     new work (DMMA MACs + streamed entries) is smallest given what earlier
+//     terms already produced is chosen;
+//   * a reduction that is the only consumer of a GEMM output is fused into
+//     the GEMM epilogue (Hadamard with its other factors, the GEMM output
+//     itself when it appears twice, fixed-order reduction to a scalar or
+//     vector); a GEMM whose two operands are the same content is symmetric
+//     and only its upper tiles are computed.
+// Reference-rule counters (ExecStats semantics, einsum.cpp:146-484) are
+// tallied on a counting walk of the reference's own order.
 #pragma once
 
 #include <array>
@@ -17,6 +26,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -38,10 +48,9 @@ struct DeviceBuffer {
     double* ptr = nullptr;
     int order = 0;
     long long n = 1;
-    bool symmetric = false;  // order 2 and bitwise equal to its transpose
-    bool borrowed = false;   // caller memory: never freed, never written
+    bool symmetric = false;
+    bool borrowed = false;
     Runtime* rt = nullptr;
-    std::uint64_t uid = 0;   // stable identity for cross-term sharing keys
     ~DeviceBuffer();
     std::uint64_t entries() const;
 };
@@ -49,7 +58,7 @@ using Buf = std::shared_ptr<DeviceBuffer>;
 
 class Runtime {
   public:
-    static Runtime& get(int device);  // -1: current device
+    static Runtime& get(int device);
     ~Runtime();
 
     cudaStream_t stream() const { return stream_; }
@@ -62,8 +71,6 @@ class Runtime {
     void release(double* p);
     void sync();
 
-    // Kernel-class timing with CUDA events on the engine stream (bench
-    // roofline evidence). Cheap: two event records per timed launch group.
     enum Kind { kGemm = 0, kStream = 1, kOther = 2 };
     struct Profile {
         double ms[3] = {0, 0, 0};
@@ -72,14 +79,13 @@ class Runtime {
     void profile_enable(bool on) { profiling_ = on; }
     void begin(Kind k);
     void end(Kind k);
-    Profile collect(bool reset);  // synchronizes the stream
+    Profile collect(bool reset);
 
   private:
     explicit Runtime(int device);
     int device_ = 0;
     int sm_count_ = 148;
     cudaStream_t stream_ = nullptr;
-    std::uint64_t next_uid_ = 1;
     bool profiling_ = false;
     std::vector<cudaEvent_t> pool_;
     struct Mark {
@@ -88,7 +94,6 @@ class Runtime {
     };
     std::vector<Mark> marks_;
     Profile totals_;
-    friend struct DeviceBuffer;
 };
 
 struct DevStats {
@@ -101,120 +106,187 @@ struct DevStats {
     std::uint64_t stream_launches = 0;
     std::uint64_t shared_hits = 0;
     std::uint64_t kernel_launches = 0;
+    std::uint64_t fused_epilogues = 0;
+    std::uint64_t symmetric_gemms = 0;
 };
 
-// Content-addressed cache of intermediates shared across V-terms of one
-// statistic evaluation (reference: SPEC.md:469 — no deduplication).
-class ShareCache {
+// ------------------------------------------------------------------ Program
+struct View {
+    int buf = -1;
+    std::array<long long, kMaxIds> stride{};
+    std::uint32_t ids = 0;
+};
+
+struct SymBuf {
+    int order = 0;
+    bool symmetric = false;
+    bool input = false;
+    Buf real;
+    int content = -1;
+    int last_use = -1;
+};
+
+struct Op {
+    bool gemm = false;
+    // stream: out[out_ids] = sum_{sum} prod factors
+    std::vector<View> factors;
+    std::vector<int> out_ids;
+    std::uint32_t sum = 0;
+    // gemm: out[ra, rb] = sum_e prod(fa) prod(fb)   (fa, fb single views after lowering)
+    std::vector<View> fa, fb;
+    std::vector<int> ra, rb;
+    int e = -1;
+    int mode = kEpiStore;
+    std::vector<View> w;  // epilogue factors over ra ∪ rb
+    int self_power = 1;
+    bool symmetric_out = false;
+    int epi_row = -1, epi_col = -1;  // ids (in the weights' views) of the output row / column
+    // destination: a program buffer, or an external device pointer
+    int out = -1;
+    double* ext = nullptr;
+    bool dead = false;
+};
+
+class Program {
   public:
-    Buf find(const std::string& key) const {
-        auto it = map_.find(key);
-        return it == map_.end() ? nullptr : it->second;
-    }
-    void put(const std::string& key, Buf b) { map_[key] = std::move(b); }
-    void clear() { map_.clear(); }
+    Program(Runtime* rt, long long n, const Config& config, DevStats* stats)
+        : rt_(rt), n_(n), config_(config), stats_(stats) {}  // rt == nullptr: plan only
+
+    // Plan-only inputs (no device memory): order and symmetry of a factor.
+    int add_symbolic_input(int order, bool symmetric);
+    std::string dump() const;
+    struct Totals {
+        std::uint64_t gemms = 0, gemm_macs = 0, streams = 0, stream_entries = 0, fused = 0, symmetric = 0;
+    };
+    Totals totals() const;
+
+    int add_input(const Buf& real);
+    long long n() const { return n_; }
+    const SymBuf& buf(int id) const { return bufs_[static_cast<std::size_t>(id)]; }
+    const Config& config() const { return config_; }
+    bool sharing() const { return config_.device.share_subexpressions; }
+
+    View view_of(int buf, const IndexTuple& layout) const;
+
+    // Records out[out_ids] = sum_{sum} prod(factors). With `ext`, writes there
+    // (never shared) and returns -1; else returns the (possibly shared) buffer.
+    int stream(std::vector<View> factors, const std::vector<int>& out_ids, std::uint32_t sum, double* ext);
+    // Records a GEMM; returns the buffer and the caller-side layout (ids).
+    int gemm(std::vector<View> fa, std::vector<View> fb, const std::vector<int>& ra, const std::vector<int>& rb,
+             int e, std::vector<int>* layout);
+
+    struct Mark {
+        std::size_t ops = 0, bufs = 0, log = 0;
+    };
+    Mark mark() const { return {ops_.size(), bufs_.size(), memo_log_.size()}; }
+    void rollback(const Mark& m);
+    double cost_since(const Mark& m) const;
+
+    void keep(int buf) { keep_[buf] = true; }  // a result the caller takes after execute()
+    void optimize();  // epilogue fusion, symmetric tiles, dead ops, last uses
+    void execute();   // launches every live op in order
+    Buf take(int buf);  // result buffer (allocated during execute)
 
   private:
-    std::map<std::string, Buf> map_;
+    std::string desc(const View& v, const std::vector<int>& dims) const;
+    int new_buf(int order, bool symmetric);
+    void fuse_into_gemm(std::size_t s_idx);
+    void launch(Op& op);
+    void run_stream(const Op& op, double* out);
+    void run_gemm(const Op& op, double* out);
+    double* ptr(int buf) const;
+
+    Runtime* rt_;
+    long long n_;
+    const Config& config_;
+    DevStats* stats_;
+    std::vector<SymBuf> bufs_;
+    std::vector<Op> ops_;
+    std::unordered_map<std::string, int> memo_;
+    std::vector<std::string> memo_log_;
+    std::map<int, bool> keep_;
 };
 
+// Records one notation into a Program with the reference's elimination walk.
+// With `count`, also tallies the reference-rule counters and checks the
+// memory cap on the reference plan's intermediates.
 class Contractor {
   public:
-    Contractor(Runtime& rt, long long n, const Config& config, DevStats* stats,
-               ShareCache* cache = nullptr)
-        : rt_(rt), n_(n), config_(config), stats_(stats), cache_(cache) {}
+    Contractor(Program& prog, DevStats* count) : p_(prog), count_(count) {}
 
-    // Full einsum. Returns the output buffer (order |output|); when
-    // `scalar_out` is given and the output is a scalar, writes it there
-    // (device pointer) and returns null.
-    Buf run(const std::vector<Buf>& inputs, const EinsumNotation& notation,
-            const EliminationOrder& order, double* scalar_out = nullptr);
+    // Records the einsum; returns the result buffer (order |output|), or -1
+    // when `scalar_out` receives the scalar.
+    int run(const std::vector<int>& inputs, const EinsumNotation& notation, const EliminationOrder& order,
+            double* scalar_out);
+    int eliminate_single(const std::vector<int>& inputs, const std::vector<IndexTuple>& tuples, int index,
+                         IndexTuple* result_tuple);
 
-    // One elimination step in isolation (einsum.hpp:49-52); result ids ascending.
-    Buf eliminate_single(const std::vector<Buf>& inputs, const std::vector<IndexTuple>& tuples,
-                         int index, IndexTuple* result_tuple);
-
-    struct View {
-        Buf buf;
-        std::array<long long, kMaxIds> stride{};
-        std::uint32_t ids = 0;
-    };
     struct Slot {
         std::uint32_t ids = 0;
         std::vector<View> factors;
         bool owned = false;
-        IndexTuple tuple;  // the reference's tuple order (for counting only)
     };
 
   private:
-    View view_of(const Buf& b, const IndexTuple& tuple) const;
-    Slot slot_of(const Buf& b, const IndexTuple& tuple);
+    Slot slot_of(int buf, const IndexTuple& tuple);
     void eliminate_one(std::vector<Slot>& slots, int e);
     Slot marginalize(const Slot& s, std::uint32_t summed);
     Slot gemm_step(const Slot& a, const Slot& b, int e);
     Slot generic_step(const std::vector<Slot>& parts, int e);
-
-    // Kernel-level primitives
-    Buf stream_to_buffer(std::vector<View> factors, const std::vector<int>& out_ids,
-                         std::uint32_t sum_ids, double* out_ptr);
-    Buf gemm_to_buffer(std::vector<View> fa, std::vector<View> fb, const std::vector<int>& ra,
-                       const std::vector<int>& rb, int e);
-    std::vector<View> limit_factors(std::vector<View> fs, std::size_t limit);
-    View output_view(const Buf& b, const std::vector<int>& ids_in_layout) const;
-
-    void ref_count_alloc(int order);  // cap check on a reference-plan intermediate
-    void ref_owned(int order);        // peak bookkeeping (make_owned)
+    std::vector<View> formed(const Slot& s);  // factors with pending sums formed
+    void cap(int order);
+    void owned(int order);
     std::uint64_t pw(int e) const;
 
-    Runtime& rt_;
-    long long n_;
-    const Config& config_;
-    DevStats* stats_;
-    ShareCache* cache_;
+    Program& p_;
+    DevStats* count_;
 };
 
-// Device-side U/V statistic drivers over tensor inputs (host or device memory).
+// -------------------------------------------------------- statistic drivers
 struct StatisticResult {
     double value = 0.0;
-    std::vector<double> terms;          // mu * V per evaluated partition (enumeration order)
-    std::vector<std::vector<int>> rgs;  // the partitions
+    std::vector<double> terms;
+    std::vector<std::vector<int>> rgs;
     std::vector<long long> mu;
-    std::vector<double> v;              // raw V per partition (0 for terms owned by other ranks)
-    std::vector<int> owner;             // rank that evaluated each term
+    std::vector<double> v;
+    std::vector<int> owner;
     DevStats stats;
     std::uint64_t enumerated = 0;
     double upload_seconds = 0.0;
     double contract_seconds = 0.0;
+    double plan_seconds = 0.0;
 };
 
 enum class LatticeMode { Sparsified, Unsparsified };
 
-// Host-only planning of one statistic: the evaluated partitions in
-// enumeration order, their induced notations and elimination orders, and the
-// LPT assignment of terms to ranks (term sharding; no GPU needed).
 struct TermPlan {
     std::vector<std::vector<int>> rgs;
     std::vector<long long> mu;
     std::vector<EinsumNotation> notation;
     std::vector<EliminationOrder> order;
-    std::vector<double> cost;   // relative work estimate (n^(width+1) per term)
+    std::vector<double> cost;
     std::vector<int> owner;
     std::uint64_t enumerated = 0;
 };
 TermPlan plan_terms(const std::vector<IndexTuple>& zero_sig, int m, long long n, LatticeMode mode,
                     const Config& config);
 
-// `inputs[k]` points at factor k (row-major, n^|sig[k]| entries) in host memory
-// (inputs_on_device = false) or device memory. Aliased pointers are uploaded
-// and sparsified once.
 StatisticResult lattice_statistic(const std::vector<const double*>& inputs, bool inputs_on_device,
                                   const std::vector<IndexTuple>& zero_sig, int m, long long n,
                                   LatticeMode mode, const Config& config);
 
-// Single contraction (v_statistic / restricted_v / einsum) over host tensors.
-std::vector<double> contract_host(const std::vector<const double*>& inputs,
-                                  const std::vector<int>& orders, long long n,
-                                  const EinsumNotation& notation, const EliminationOrder* order,
+std::vector<double> contract_host(const std::vector<const double*>& inputs, const std::vector<int>& orders,
+                                  long long n, const EinsumNotation& notation, const EliminationOrder* order,
                                   const Config& config, DevStats* stats);
+
+std::vector<double> eliminate_host(const std::vector<const double*>& inputs, const std::vector<IndexTuple>& tuples,
+                                   long long n, int index, const Config& config, DevStats* stats,
+                                   IndexTuple* result_tuple);
+
+double combine_terms(const std::vector<double>& terms);
+
+// Plan-only view of a statistic (no GPU): the optimized Program's ops and totals.
+std::string plan_summary(const std::vector<IndexTuple>& zero_sig, int m, long long n, const Config& config,
+                         bool inputs_symmetric, Program::Totals* totals);
 
 }  // namespace ustats::dev

@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_f64_kernel(GemmArgs p) {
     }
 
     // ---------------------------------------------------------- epilogue
+    auto cpow = [&](double c) { return p.self_power == 2 ? c * c : c; };
     auto weight = [&](int rl, int cl) {
         double w = p.scale;
         for (int f = 0; f < p.w.nf; ++f) w *= __ldg(p.w.ptr[f] + sm.woff_r[f][rl] + sm.woff_c[f][cl]);
@@ -226,9 +227,9 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_f64_kernel(GemmArgs p) {
                 const int cl = wn * 32 + ni * 8 + 2 * t;
                 const long long c = c0 + cl;
                 double* dst = p.out + r * p.cols + c;
-                const double v0 = acc[mi][ni][0] * weight(rl, cl);
+                const double v0 = cpow(acc[mi][ni][0]) * weight(rl, cl);
                 if (c + 1 < p.cols) {
-                    const double v1 = acc[mi][ni][1] * weight(rl, cl + 1);
+                    const double v1 = cpow(acc[mi][ni][1]) * weight(rl, cl + 1);
                     if ((reinterpret_cast<unsigned long long>(dst) & 15) == 0)
                         *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
                     else {
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_f64_kernel(GemmArgs p) {
     auto val = [&](int mi, int ni, int h) {
         const int rl = wm * 64 + mi * 8 + g, cl = wn * 32 + ni * 8 + 2 * t + h;
         if (r0 + rl >= p.rows || c0 + cl >= p.cols) return 0.0;
-        return acc[mi][ni][h] * weight(rl, cl);
+        return cpow(acc[mi][ni][h]) * weight(rl, cl);
     };
 
     if (p.mode == kEpiSumAll) {
@@ -262,7 +263,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_f64_kernel(GemmArgs p) {
         if (threadIdx.x == 0) {
             double tot = 0.0;
             for (int w = 0; w < THREADS / 32; ++w) tot += sm.red[0][w];
-            p.partial[tm * tiles_n + tn] = tot;
+            p.partial[blockIdx.x] = tot;
         }
         return;
     }
@@ -353,10 +354,11 @@ std::size_t gemm_partial_entries(const GemmArgs& a) {
     }
 }
 
-int launch_gemm_tma(const GemmArgs& a, cudaStream_t s);  // gemm_tma.cu
+// gemm_tma.cu: returns the number of CTAs launched, or -1 when not eligible
+long long launch_gemm_tma(const GemmArgs& a, cudaStream_t s);
 
 int launch_gemm(const GemmArgs& a, cudaStream_t s) {
-    int launched = launch_gemm_tma(a, s);
+    const long long launched = launch_gemm_tma(a, s);
     if (launched > 0) {
         // shared finalize below
     } else if (a.a_kmajor) {
@@ -368,7 +370,8 @@ int launch_gemm(const GemmArgs& a, cudaStream_t s) {
     }
     const long long tm = (a.rows + BM - 1) / BM, tn = (a.cols + BN - 1) / BN;
     if (a.mode == kEpiSumAll) {
-        gemm_finalize_scalar<<<1, 1024, 0, s>>>(a.partial, tm * tn, a.out);
+        const long long blocks = launched > 0 ? launched : tm * tn;
+        gemm_finalize_scalar<<<1, 1024, 0, s>>>(a.partial, blocks, a.out);
     } else if (a.mode == kEpiSumCols) {
         gemm_finalize_vector<<<static_cast<unsigned>((a.rows + 255) / 256), 256, 0, s>>>(a.partial, tn, a.rows, a.out);
     } else if (a.mode == kEpiSumRows) {

@@ -123,11 +123,24 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     const long long tiles_m = (p.rows + BM - 1) / BM, tiles_n = (p.cols + BN - 1) / BN;
     const long long bid = blockIdx.x;
-    const long long width = GROUP_M * tiles_n;
-    const long long group = bid / width, first_m = group * GROUP_M;
-    const long long gsz = (tiles_m - first_m) < GROUP_M ? (tiles_m - first_m) : GROUP_M;
-    const long long tm = first_m + (bid % width) % gsz;
-    const long long tn = (bid % width) / gsz;
+    long long tm, tn;
+    if (p.symmetric_out) {
+        // upper-triangular tiles, row by row: row tm holds tiles tm..tiles_n-1
+        long long rest = bid;
+        tm = 0;
+        while (rest >= tiles_n - tm) {
+            rest -= tiles_n - tm;
+            ++tm;
+        }
+        tn = tm + rest;
+    } else {
+        const long long width = GROUP_M * tiles_n;
+        const long long group = bid / width, first_m = group * GROUP_M;
+        const long long gsz = (tiles_m - first_m) < GROUP_M ? (tiles_m - first_m) : GROUP_M;
+        tm = first_m + (bid % width) % gsz;
+        tn = (bid % width) / gsz;
+    }
+    const bool mirror = p.symmetric_out && tm != tn;
     const int r0 = static_cast<int>(tm * BM), c0 = static_cast<int>(tn * BN);
     const int KT = static_cast<int>((p.n + BK - 1) / BK);
 
@@ -226,6 +239,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     __syncthreads();  // epilogue offsets visible
 
+    auto cpow = [&](double c) { return p.self_power == 2 ? c * c : c; };
     auto weight = [&](int rl, int cl) {
         double w = p.scale;
         for (int f = 0; f < p.w.nf; ++f) w *= __ldg(p.w.ptr[f] + sm.woff_r[f][rl] + sm.woff_c[f][cl]);
@@ -243,17 +257,22 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int cl = wn * 32 + ni * 8 + 2 * t;
                 const long long c = c0 + cl;
                 double* dst = p.out + r * p.cols + c;
-                const double v0 = acc[mi][ni][0] * weight(rl, cl);
+                const double v0 = cpow(acc[mi][ni][0]) * weight(rl, cl);
                 if (c + 1 < p.cols) {
-                    const double v1 = acc[mi][ni][1] * weight(rl, cl + 1);
+                    const double v1 = cpow(acc[mi][ni][1]) * weight(rl, cl + 1);
                     if ((reinterpret_cast<unsigned long long>(dst) & 15) == 0)
                         *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
                     else {
                         dst[0] = v0;
                         dst[1] = v1;
                     }
+                    if (mirror) {
+                        p.out[c * p.cols + r] = v0;
+                        p.out[(c + 1) * p.cols + r] = v1;
+                    }
                 } else if (c < p.cols) {
                     dst[0] = v0;
+                    if (mirror) p.out[c * p.cols + r] = v0;
                 }
             }
         }
@@ -263,7 +282,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     auto val = [&](int mi, int ni, int h) {
         const int rl = wm * 64 + mi * 8 + g, cl = wn * 32 + ni * 8 + 2 * t + h;
         if (r0 + rl >= p.rows || c0 + cl >= p.cols) return 0.0;
-        return acc[mi][ni][h] * weight(rl, cl);
+        return cpow(acc[mi][ni][h]) * weight(rl, cl);
     };
 
     if (p.mode == kEpiSumAll) {
@@ -278,7 +297,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (tid == 0) {
             double tot = 0.0;
             for (int w = 0; w < THREADS / 32; ++w) tot += sm.red[0][w];
-            p.partial[tm * tiles_n + tn] = tot;
+            p.partial[blockIdx.x] = mirror ? 2.0 * tot : tot;
         }
         return;
     }
@@ -374,19 +393,24 @@ bool encode(CUtensorMap* map, const double* ptr, bool kmajor, long long rows, lo
 }
 
 template <bool AK, bool BKM>
-void launch_tma(const CUtensorMap& ma, const CUtensorMap& mb, const TmaArgs& args, cudaStream_t s) {
+long long launch_tma(const CUtensorMap& ma, const CUtensorMap& mb, const TmaArgs& args, cudaStream_t s) {
     static std::once_flag once;
     const int bytes = static_cast<int>(sizeof(TmaSmem)) + 1024;
     std::call_once(once, [&] {
         cudaFuncSetAttribute(gemm_tma_kernel<AK, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     });
-    const long long tiles = ((args.g.rows + BM - 1) / BM) * ((args.g.cols + BN - 1) / BN);
+    const long long tm = (args.g.rows + BM - 1) / BM, tn = (args.g.cols + BN - 1) / BN;
+    const long long tiles = args.g.symmetric_out ? tm * (tm + 1) / 2 : tm * tn;
     gemm_tma_kernel<AK, BKM><<<static_cast<unsigned>(tiles), THREADS, bytes, s>>>(ma, mb, args);
+    return tiles;
 }
 
 }  // namespace
 
-bool gemm_tma_eligible(const GemmArgs& a, int* a_kmajor, int* b_kmajor) {
+bool gemm_tma_eligible(const GemmArgs& a, int* a_kmajor_out, int* b_kmajor_out) {
+    int ak_local = 1, bk_local = 1;
+    int* a_kmajor = a_kmajor_out ? a_kmajor_out : &ak_local;
+    int* b_kmajor = b_kmajor_out ? b_kmajor_out : &bk_local;
     long long ars, aks, brs, bks;
     if (!plain(a.a, a.n, ars, aks) || !plain(a.b, a.n, brs, bks)) return false;
     if (a.rows >= (1ll << 31) || a.cols >= (1ll << 31) || a.n >= (1ll << 31)) return false;
@@ -405,9 +429,12 @@ bool gemm_tma_eligible(const GemmArgs& a, int* a_kmajor, int* b_kmajor) {
     return layout(a.a.ptr[0], ars, aks, a_kmajor) && layout(a.b.ptr[0], brs, bks, b_kmajor) && encoder() != nullptr;
 }
 
-int launch_gemm_tma(const GemmArgs& a, cudaStream_t s) {
+long long launch_gemm_tma(const GemmArgs& in, cudaStream_t s) {
     int ak = 1, bk = 1;
-    if (!gemm_tma_eligible(a, &ak, &bk)) return -1;
+    if (!gemm_tma_eligible(in, &ak, &bk)) return -1;
+    GemmArgs a = in;
+    // upper tiles only for symmetric store / full reductions with square output
+    if (a.symmetric_out && !(a.rows == a.cols && (a.mode == kEpiStore || a.mode == kEpiSumAll))) a.symmetric_out = 0;
     long long ars, aks, brs, bks;
     plain(a.a, a.n, ars, aks);
     plain(a.b, a.n, brs, bks);
@@ -415,14 +442,8 @@ int launch_gemm_tma(const GemmArgs& a, cudaStream_t s) {
     if (!encode(&ma, a.a.ptr[0], ak, a.rows, a.n, ars, aks) || !encode(&mb, a.b.ptr[0], bk, a.cols, a.n, brs, bks))
         return -1;
     TmaArgs args{a, ak, bk};
-    if (ak) {
-        if (bk) launch_tma<true, true>(ma, mb, args, s);
-        else launch_tma<true, false>(ma, mb, args, s);
-    } else {
-        if (bk) launch_tma<false, true>(ma, mb, args, s);
-        else launch_tma<false, false>(ma, mb, args, s);
-    }
-    return 1;
+    if (ak) return bk ? launch_tma<true, true>(ma, mb, args, s) : launch_tma<true, false>(ma, mb, args, s);
+    return bk ? launch_tma<false, true>(ma, mb, args, s) : launch_tma<false, false>(ma, mb, args, s);
 }
 
 }  // namespace ustats::dev

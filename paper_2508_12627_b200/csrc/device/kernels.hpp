@@ -40,8 +40,9 @@ struct GemmSide {
 };
 
 enum EpilogueMode : int {
-    kEpiStore = 0,      // out[r * cols + c] = scale * C * W
-    kEpiSumAll = 1,     // partial[tile] = sum_{r,c} C * W      (then finalize)
+    kEpiStore = 0,      // out[r * cols + c] = scale * C * W (symmetric_out: mirrored too)
+    kEpiSumAll = 1,     // partial[block] = sum_{r,c} C * W      (then finalize; symmetric_out:
+                        //   upper tiles only, off-diagonal tiles counted twice)
     kEpiSumCols = 2,    // partial[tile_n][r] = sum_c C * W     (then finalize -> out[r])
     kEpiSumRows = 3,    // partial[tile_m][c] = sum_r C * W     (then finalize -> out[c])
 };
@@ -68,6 +69,7 @@ struct GemmArgs {
     int a_kmajor = 1;           // loader orientation hints (coalescing)
     int b_kmajor = 1;
     int symmetric_out = 0;      // rows==cols and C symmetric: compute upper tiles only
+    int self_power = 1;         // epilogue value = C^self_power * W (2: the consumer read C twice)
 };
 
 // ------------------------------------------------------------- launchers

@@ -223,26 +223,13 @@ std::pair<DenseTensor, IndexTuple> eliminate_index(std::span<const DenseTensor> 
             if (id < 0 || id >= dev::kMaxIds)
                 fail(ErrorCode::InvalidArgument, "index outside the device executor's range");
     }
-    dev::Runtime& rt = dev::Runtime::get(config.device.device);
-    std::vector<dev::Buf> bufs;
-    for (const DenseTensor& t : tensors) {
-        dev::Buf b = rt.allocate(t.order, n);
-        dev::check_cuda(cudaMemcpyAsync(b->ptr, t.data.data(), t.data.size() * sizeof(double),
-                                        cudaMemcpyHostToDevice, rt.stream()),
-                        "upload");
-        bufs.push_back(b);
-    }
+    std::vector<const double*> ptrs;
+    for (const DenseTensor& t : tensors) ptrs.push_back(t.data.data());
     dev::DevStats ds;
-    dev::Contractor c(rt, n, config, &ds);
     IndexTuple tuple;
-    dev::Buf out = c.eliminate_single(bufs, tuples, index, &tuple);
+    std::vector<double> host = dev::eliminate_host(ptrs, tuples, n, index, config, &ds, &tuple);
     DenseTensor result(static_cast<int>(tuple.size()), n, config);
-    dev::check_cuda(cudaMemcpyAsync(result.data.data(), out->ptr, result.data.size() * sizeof(double),
-                                    cudaMemcpyDeviceToHost, rt.stream()),
-                    "D2H");
-    out.reset();
-    bufs.clear();
-    rt.sync();
+    result.data = std::move(host);
     if (stats) {
         stats->multiply_adds += ds.ref_madds;
         stats->peak_intermediate_entries = std::max(stats->peak_intermediate_entries, ds.ref_peak);
