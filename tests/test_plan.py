@@ -1,0 +1,57 @@
+"""Structure of the optimized device program (host only, no GPU).
+
+With sharing / reordering / fusion disabled the recorded program has exactly
+the reference executor's GEMM steps (C2 2, C3 7,
+C4 3 + 17 K-way, C5 241). With them enabled, the cross-term planner collapses
+them (C2's tr(A^4) becomes one symmetric GEMM whose epilogue squares and sums;
+C3's seven GEMMs are all B·B)."""
+import pytest
+
+import paper_2508_12627_b200 as us
+from paper_2508_12627_b200.workloads import CONFIGS
+
+PLAIN = dict(share=False, reorder=False, fuse_epilogues=False, symmetry=False)
+CAP = 2 ** 40
+
+
+def plan(name, **kw):
+    w = CONFIGS[name]
+    cfg = us.Config(memory_cap_entries=CAP, **kw)
+    return us.plan_summary([list(t) for t in w.signature], w.m, w.n, cfg)
+
+
+@pytest.mark.parametrize("name,gemms", [("C1", 0), ("C2", 2), ("C3", 7), ("C4", 20), ("C5", 241)])
+def test_reference_plan_gemm_counts(name, gemms):
+    _, tot = plan(name, **PLAIN)
+    assert tot["gemms"] == gemms
+
+
+def test_c2_single_symmetric_fused_gemm():
+    text, tot = plan("C2")
+    assert tot["gemms"] == 1 and tot["symmetric_gemms"] == 1 and tot["fused_epilogues"] == 1
+    n = CONFIGS["C2"].n
+    tiles = n // 128
+    assert tot["gemm_macs"] == n ** 3 // (tiles * tiles) * (tiles * (tiles + 1) // 2)
+    assert "epi=sum_all pow=2 SYM -> term" in text
+
+
+def test_sharing_never_increases_work():
+    for name in ("C2", "C3", "C4", "C5"):
+        _, base = plan(name, **PLAIN)
+        _, opt = plan(name)
+        assert opt["gemm_macs"] <= base["gemm_macs"]
+        assert opt["gemms"] <= base["gemms"]
+
+
+def test_c3_c5_collapse():
+    _, c3 = plan("C3")
+    assert c3["gemms"] == 1
+    _, c5 = plan("C5")
+    assert c5["gemms"] <= 10
+
+
+def test_plan_respects_memory_cap():
+    w = CONFIGS["C5"]
+    with pytest.raises(us.UStatsError) as e:
+        us.plan_summary([list(t) for t in w.signature], w.m, w.n, us.Config())
+    assert e.value.code == "MemoryCapExceeded"
