@@ -146,9 +146,9 @@ US_API int us_plan_terms(int32_t m, int32_t K, const int32_t* tuple_len, const i
 
 /* Plan inspection (host only): the optimized device program for the
  * sparsified lattice of a signature at extent n — one line per kernel
- * (GEMM / stream, operands, fused epilogue) into text[0..cap) — and totals[6]
+ * (GEMM / stream, operands, fused epilogue) into text[0..cap) — and totals[7]
  * = {gemms, gemm_macs, streams, stream_entries, fused_epilogues,
- * symmetric_gemms}. inputs_symmetric != 0 treats every order-2 factor as the
+ * symmetric_gemms, peak_entries (inputs + live intermediates over the schedule)}. inputs_symmetric != 0 treats every order-2 factor as the
  * same bitwise-symmetric matrix (the BASELINE configs). */
 US_API int us_plan_summary(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
                            int64_t n, const us_config* cfg, int32_t inputs_symmetric, char* text,

@@ -363,10 +363,11 @@ def plan_summary(signature, m: int, n: int, config: Config | None = None, inputs
     K, L, I = _signature(signature)
     cap = 1 << 22
     buf = C.create_string_buffer(cap)
-    tot = (N.u64 * 6)()
+    tot = (N.u64 * 7)()
     cfg = _cfg(config)
     _check(N.lib().us_plan_summary(m, K, L, I, n, C.byref(cfg), 1 if inputs_symmetric else 0, buf, cap, tot))
-    names = ["gemms", "gemm_macs", "streams", "stream_entries", "fused_epilogues", "symmetric_gemms"]
+    names = ["gemms", "gemm_macs", "streams", "stream_entries", "fused_epilogues", "symmetric_gemms",
+             "peak_entries"]
     return buf.value.decode(), dict(zip(names, list(tot)))
 
 

@@ -422,6 +422,7 @@ int us_plan_summary(int32_t m, int32_t K, const int32_t* tuple_len, const int32_
             totals[3] = t.stream_entries;
             totals[4] = t.fused;
             totals[5] = t.symmetric;
+            totals[6] = t.peak_entries;
         }
     });
 }

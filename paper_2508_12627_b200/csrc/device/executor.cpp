@@ -145,6 +145,16 @@ std::uint32_t ids_of_views(const std::vector<View>& vs) {
     for (const View& v : vs) m |= v.ids;
     return m;
 }
+
+// Every view an op reads (operands, stream factors, fused-epilogue weights).
+template <class F>
+void for_each_read(const Op& op, F&& f) {
+    for (const View& v : op.factors) f(v);
+    for (const View& v : op.fa) f(v);
+    for (const View& v : op.fb) f(v);
+    for (const Op::Epi& e : op.epis)
+        for (const View& v : e.w) f(v);
+}
 }  // namespace
 
 // ----------------------------------------------------------------- Program
@@ -179,19 +189,41 @@ Program::Totals Program::totals() const {
             ++t.gemms;
             const std::uint64_t tm = (ipow(n_, static_cast<int>(op.ra.size())) + 127) / 128;
             std::uint64_t macs = ipow(n_, static_cast<int>(op.ra.size() + op.rb.size()) + 1);
-            const bool tri = op.symmetric_out && (op.mode == kEpiStore || op.mode == kEpiSumAll) &&
-                             op.ra.size() == 1 && op.rb.size() == 1;
+            const bool tri = op.symmetric_out && op.ra.size() == 1 && op.rb.size() == 1;
             if (tri) {
                 macs = macs / (tm * tm) * (tm * (tm + 1) / 2);
                 ++t.symmetric;
             }
             t.gemm_macs += macs;
-            if (op.mode != kEpiStore || !op.w.empty() || op.self_power != 1) ++t.fused;
+            t.fused += op.epis.size();
         } else {
             ++t.streams;
             t.stream_entries += ipow(n_, static_cast<int>(op.out_ids.size()) + std::popcount(op.sum)) *
                                 static_cast<std::uint64_t>(op.factors.size());
         }
+    }
+    // live-set simulation: inputs always live; outputs from their op to last use
+    std::uint64_t live = 0;
+    for (const SymBuf& b : bufs_)
+        if (b.input) live += ipow(n_, b.order);
+    t.peak_entries = live;
+    for (std::size_t pos = 0; pos < schedule_.size(); ++pos) {
+        const Op& op = ops_[schedule_[pos]];
+        if (!op.ext && op.out >= 0 && (!op.gemm || op.store))
+            live += ipow(n_, bufs_[static_cast<std::size_t>(op.out)].order);
+        if (op.gemm)
+            for (const Op::Epi& e : op.epis)
+                if (!e.ext && e.out >= 0) live += ipow(n_, bufs_[static_cast<std::size_t>(e.out)].order);
+        t.peak_entries = std::max(t.peak_entries, live);
+        std::vector<int> done;
+        for_each_read(op, [&](const View& v) {
+            const SymBuf& b = bufs_[static_cast<std::size_t>(v.buf)];
+            if (!b.input && b.last_use == static_cast<int>(pos) &&
+                std::find(done.begin(), done.end(), v.buf) == done.end()) {
+                done.push_back(v.buf);
+                live -= ipow(n_, b.order);
+            }
+        });
     }
     return t;
 }
@@ -214,9 +246,11 @@ std::string Program::dump() const {
         std::string line = std::to_string(i) + ": ";
         if (op.gemm) {
             line += "GEMM rows=" + std::to_string(op.ra.size()) + " cols=" + std::to_string(op.rb.size()) + " e=" +
-                    std::to_string(op.e) + " A:" + vs(op.fa) + " B:" + vs(op.fb) + " epi=" + modes[op.mode] +
-                    " pow=" + std::to_string(op.self_power) + (op.symmetric_out ? " SYM" : "") +
-                    (op.w.empty() ? "" : " W:" + vs(op.w));
+                    std::to_string(op.e) + " A:" + vs(op.fa) + " B:" + vs(op.fb) + (op.symmetric_out ? " SYM" : "") +
+                    (op.store ? " store" : " nostore");
+            for (const Op::Epi& e : op.epis)
+                line += std::string(" | epi ") + modes[e.mode] + " pow=" + std::to_string(e.self_power) +
+                        (e.w.empty() ? "" : " W:" + vs(e.w)) + (e.ext ? " -> term" : " -> b" + std::to_string(e.out));
         } else {
             line += "STREAM out=[";
             for (int id : op.out_ids) line += std::to_string(id) + " ";
@@ -391,96 +425,190 @@ double Program::cost_since(const Mark& m) const {
     return c;
 }
 
-// A reduction whose only input from a GEMM output is that GEMM, and whose
-// iteration space is exactly the GEMM's (row, col) space, runs in the GEMM's
-// epilogue: its other factors become epilogue weights, a second read of the
-// GEMM output becomes self_power = 2, and its result (scalar, vector or an
-// elementwise product) is written straight from the accumulators.
-void Program::fuse_into_gemm(std::size_t s_idx) {
-    Op& s = ops_[s_idx];
-    std::vector<int> uses(bufs_.size(), 0);
-    for (const Op& op : ops_) {
-        if (op.dead) continue;
-        for (const auto* vs : {&op.factors, &op.fa, &op.fb, &op.w})
-            for (const View& v : *vs) ++uses[static_cast<std::size_t>(v.buf)];
-    }
-    for (std::size_t g_idx = 0; g_idx < s_idx; ++g_idx) {
-        Op& g = ops_[g_idx];
-        if (g.dead || !g.gemm || g.mode != kEpiStore || g.ext || g.w.size() || g.ra.size() != 1 || g.rb.size() != 1)
+// Host mirror of gemm_tma_eligible for one operand view: a single strided
+// matrix with a unit stride along rows or k and an even other stride.
+bool Program::tma_plain(const View& v, const std::vector<int>& rows, int e) const {
+    if (rows.size() != 1) return false;
+    const long long rs = v.stride[static_cast<std::size_t>(rows[0])], ks = v.stride[static_cast<std::size_t>(e)];
+    const bool sym = bufs_[static_cast<std::size_t>(v.buf)].symmetric;
+    auto ok = [](long long unit, long long other) { return unit == 1 && other > 0 && other % 2 == 0; };
+    return ok(ks, rs) || ok(rs, ks) || (sym && (ok(rs, ks) || ok(ks, rs)));
+}
+
+// Multi-consumer epilogue fusion. A stream op S that reads the output of a
+// GEMM G (once, or twice -> self_power 2), iterates exactly over G's
+// (row, col) space, and whose other factors do not depend on G, becomes an
+// epilogue of G: Hadamard with its weights, then a fixed-order reduction to a
+// scalar / row vector / column vector, or an elementwise store. G keeps
+// storing its product only if something else still reads it.
+void Program::fuse_epilogues() {
+    if (n_ % 2 != 0) return;  // TMA operands need even strides
+    const std::size_t N = ops_.size();
+    std::vector<int> producer(bufs_.size(), -1);
+    for (std::size_t i = 0; i < N; ++i)
+        if (!ops_[i].dead && !ops_[i].ext && ops_[i].out >= 0) producer[static_cast<std::size_t>(ops_[i].out)] = static_cast<int>(i);
+    const std::size_t words = (N + 63) / 64;
+    std::vector<std::uint64_t> deps(N * words, 0);
+    auto dep_has = [&](std::size_t i, std::size_t j) { return (deps[i * words + j / 64] >> (j % 64)) & 1; };
+    auto closure = [&] {
+        std::fill(deps.begin(), deps.end(), 0);
+        for (std::size_t i = 0; i < N; ++i) {
+            if (ops_[i].dead) continue;
+            for_each_read(ops_[i], [&](const View& v) {
+                const int p = producer[static_cast<std::size_t>(v.buf)];
+                if (p < 0) return;
+                const auto pp = static_cast<std::size_t>(p);
+                for (std::size_t w = 0; w < words; ++w) deps[i * words + w] |= deps[pp * words + w];
+                deps[i * words + pp / 64] |= std::uint64_t{1} << (pp % 64);
+            });
+        }
+    };
+    closure();
+    for (std::size_t gi = 0; gi < N; ++gi) {
+        Op& g = ops_[gi];
+        if (g.dead || !g.gemm || g.ra.size() != 1 || g.rb.size() != 1) continue;
+        if (g.fa.size() != 1 || g.fb.size() != 1 || !tma_plain(g.fa[0], g.ra, g.e) || !tma_plain(g.fb[0], g.rb, g.e))
             continue;
         const int gb = g.out;
-        std::vector<View> mine, rest;
-        for (const View& v : s.factors) (v.buf == gb ? mine : rest).push_back(v);
-        if (mine.empty() || mine.size() > 2 || uses[static_cast<std::size_t>(gb)] != static_cast<int>(mine.size()))
-            continue;
-        // the GEMM output's axes as seen by s: row -> x, col -> y
-        int x = -1, y = -1;
-        for (int id : ids_of(mine[0].ids)) {
-            if (mine[0].stride[static_cast<std::size_t>(id)] == n_) x = id;
-            if (mine[0].stride[static_cast<std::size_t>(id)] == 1) y = id;
+        // one descriptor slot stays free for the plain store of the product
+        for (std::size_t si = gi + 1; si < N && g.epis.size() + 1 < static_cast<std::size_t>(kMaxEpilogues); ++si) {
+            Op& s = ops_[si];
+            if (s.dead || s.gemm) continue;
+            std::vector<View> mine, rest;
+            for (const View& v : s.factors) (v.buf == gb ? mine : rest).push_back(v);
+            if (mine.empty() || mine.size() > 2 || rest.size() > static_cast<std::size_t>(kMaxEpiW)) continue;
+            // Epilogue weights are read while the SM's DMMA pipe idles (one CTA
+            // per SM): only vector / scalar weights are cheap enough there
+            // (measured: matrix weights cost more than the stream pass they save).
+            bool light = true;
+            for (const View& w : rest) light &= bufs_[static_cast<std::size_t>(w.buf)].order <= 1;
+            if (!light) continue;
+            int x = -1, y = -1;
+            for (int id : ids_of(mine[0].ids)) {
+                if (mine[0].stride[static_cast<std::size_t>(id)] == n_) x = id;
+                if (mine[0].stride[static_cast<std::size_t>(id)] == 1) y = id;
+            }
+            if (x < 0 || y < 0 || x == y || std::popcount(mine[0].ids) != 2) continue;
+            bool consistent = true;
+            for (const View& v : mine) {
+                const bool same = v.stride[static_cast<std::size_t>(x)] == n_ && v.stride[static_cast<std::size_t>(y)] == 1;
+                const bool flip = v.stride[static_cast<std::size_t>(x)] == 1 && v.stride[static_cast<std::size_t>(y)] == n_;
+                if (!(same || (flip && g.symmetric_out)) || std::popcount(v.ids) != 2) consistent = false;
+            }
+            if (!consistent) continue;
+            const std::uint32_t space = bit(x) | bit(y);
+            std::uint32_t iter = s.sum;
+            for (int id : s.out_ids) iter |= bit(id);
+            if (iter != space || (ids_of_views(rest) & ~space)) continue;
+            // the weights must exist before G runs and must not depend on G
+            bool acyclic = true;
+            for (const View& w : rest) {
+                const int p = producer[static_cast<std::size_t>(w.buf)];
+                if (w.buf == gb || (p >= 0 && (static_cast<std::size_t>(p) == gi || dep_has(static_cast<std::size_t>(p), gi))))
+                    acyclic = false;
+            }
+            if (!acyclic) continue;
+            Op::Epi e;
+            if (s.out_ids.empty()) e.mode = kEpiSumAll;
+            else if (s.out_ids.size() == 1 && s.out_ids[0] == x) e.mode = kEpiSumCols;
+            else if (s.out_ids.size() == 1 && s.out_ids[0] == y) e.mode = kEpiSumRows;
+            else if (s.out_ids.size() == 2 && s.out_ids[0] == x && s.out_ids[1] == y) e.mode = kEpiStore;
+            else if (s.out_ids.size() == 2 && s.out_ids[0] == y && s.out_ids[1] == x) {
+                e.mode = kEpiStore;
+                e.transpose = true;
+            } else continue;
+            e.w = rest;
+            e.self_power = static_cast<int>(mine.size());
+            e.row_id = x;
+            e.col_id = y;
+            e.out = s.out;
+            e.ext = s.ext;
+            g.epis.push_back(std::move(e));
+            s.dead = true;
+            if (!s.ext && s.out >= 0) producer[static_cast<std::size_t>(s.out)] = static_cast<int>(gi);
+            if (stats_) ++stats_->fused_epilogues;
+            closure();
         }
-        if (x < 0 || y < 0 || x == y || std::popcount(mine[0].ids) != 2) continue;
-        bool consistent = true;
-        for (const View& v : mine) {
-            const bool same = v.stride[static_cast<std::size_t>(x)] == n_ && v.stride[static_cast<std::size_t>(y)] == 1;
-            const bool flip = v.stride[static_cast<std::size_t>(x)] == 1 && v.stride[static_cast<std::size_t>(y)] == n_;
-            if (!(same || (flip && g.symmetric_out)) || std::popcount(v.ids) != 2) consistent = false;
+    }
+    // a GEMM stores its product only while something still reads it
+    std::vector<int> reads(bufs_.size(), 0);
+    for (const Op& op : ops_)
+        if (!op.dead) for_each_read(op, [&](const View& v) { ++reads[static_cast<std::size_t>(v.buf)]; });
+    for (Op& op : ops_) {
+        if (op.dead || !op.gemm) continue;
+        op.store = reads[static_cast<std::size_t>(op.out)] > 0 || keep_.count(op.out);
+        if (!op.store && op.epis.empty()) op.dead = true;
+    }
+}
+
+// Memory-aware list scheduling: among ops whose inputs exist, run the one
+// that grows the live set least (allocation minus buffers it frees), ties in
+// recording order. Keeps the working set of n^2 intermediates small when
+// sub-contractions are shared by V-terms far apart in enumeration order.
+void Program::make_schedule() {
+    const std::size_t N = ops_.size();
+    std::vector<int> producer(bufs_.size(), -1);
+    auto outputs = [&](std::size_t i, auto&& f) {
+        const Op& op = ops_[i];
+        if (!op.ext && op.out >= 0 && (!op.gemm || op.store)) f(op.out);
+        for (const Op::Epi& e : op.epis)
+            if (!e.ext && e.out >= 0) f(e.out);
+    };
+    for (std::size_t i = 0; i < N; ++i)
+        if (!ops_[i].dead) outputs(i, [&](int b) { producer[static_cast<std::size_t>(b)] = static_cast<int>(i); });
+    std::vector<std::vector<int>> reads(N);
+    std::vector<int> consumers(bufs_.size(), 0);
+    for (std::size_t i = 0; i < N; ++i) {
+        if (ops_[i].dead) continue;
+        std::vector<int>& r = reads[i];
+        for_each_read(ops_[i], [&](const View& v) {
+            if (std::find(r.begin(), r.end(), v.buf) == r.end()) r.push_back(v.buf);
+        });
+        for (int b : r) ++consumers[static_cast<std::size_t>(b)];
+    }
+    std::vector<char> done_buf(bufs_.size(), 0);
+    for (std::size_t b = 0; b < bufs_.size(); ++b)
+        if (bufs_[b].input || producer[b] < 0) done_buf[b] = 1;
+    std::vector<char> scheduled(N, 0);
+    schedule_.clear();
+    std::size_t live_ops = 0;
+    for (const Op& op : ops_) live_ops += !op.dead;
+    auto size = [&](int b) { return static_cast<double>(ipow(n_, bufs_[static_cast<std::size_t>(b)].order)); };
+    while (schedule_.size() < live_ops) {
+        long best = -1;
+        double best_delta = 0;
+        for (std::size_t i = 0; i < N; ++i) {
+            if (ops_[i].dead || scheduled[i]) continue;
+            bool ready = true;
+            for (int b : reads[i]) ready &= done_buf[static_cast<std::size_t>(b)] != 0;
+            if (!ready) continue;
+            double delta = 0.0;
+            outputs(i, [&](int b) { delta += size(b); });
+            for (int b : reads[i])
+                if (!bufs_[static_cast<std::size_t>(b)].input && consumers[static_cast<std::size_t>(b)] == 1 &&
+                    !keep_.count(b))
+                    delta -= size(b);
+            if (best < 0 || delta < best_delta) {
+                best = static_cast<long>(i);
+                best_delta = delta;
+            }
         }
-        if (!consistent) continue;
-        std::uint32_t space = bit(x) | bit(y);
-        std::uint32_t iter = s.sum;
-        for (int id : s.out_ids) iter |= bit(id);
-        if (iter != space || (ids_of_views(rest) & ~space)) continue;
-        int mode;
-        bool transpose = false;
-        if (s.out_ids.empty()) mode = kEpiSumAll;
-        else if (s.out_ids.size() == 1 && s.out_ids[0] == x) mode = kEpiSumCols;
-        else if (s.out_ids.size() == 1 && s.out_ids[0] == y) mode = kEpiSumRows;
-        else if (s.out_ids.size() == 2 && s.out_ids[0] == x && s.out_ids[1] == y) mode = kEpiStore;
-        else if (s.out_ids.size() == 2 && s.out_ids[0] == y && s.out_ids[1] == x) {
-            mode = kEpiStore;
-            transpose = true;  // compute the transposed product instead: swap the operands
-        } else continue;
-        bool sym_ok = g.symmetric_out && (mode == kEpiSumAll || mode == kEpiStore) && !transpose;
-        for (const View& w : rest) {
-            if (!bufs_[static_cast<std::size_t>(w.buf)].symmetric || w.ids != space) sym_ok = false;
-            else if (!((w.stride[static_cast<std::size_t>(x)] == n_ && w.stride[static_cast<std::size_t>(y)] == 1) ||
-                       (w.stride[static_cast<std::size_t>(x)] == 1 && w.stride[static_cast<std::size_t>(y)] == n_)))
-                sym_ok = false;
-        }
-        Op fused = g;
-        if (transpose) {
-            std::swap(fused.fa, fused.fb);
-            std::swap(fused.ra, fused.rb);
-            std::swap(x, y);
-        }
-        // epilogue factors in (row=x, col=y) terms: strides carried by id
-        fused.w = rest;
-        fused.self_power = static_cast<int>(mine.size());
-        fused.mode = mode;
-        fused.symmetric_out = sym_ok;
-        fused.out = s.out;
-        fused.ext = s.ext;
-        fused.epi_row = x;
-        fused.epi_col = y;
-        g.dead = true;
-        s = fused;
-        if (stats_) ++stats_->fused_epilogues;
-        return;
+        if (best < 0) fail(ErrorCode::InvalidArgument, "executor: dependency cycle in the device program");
+        const auto i = static_cast<std::size_t>(best);
+        scheduled[i] = 1;
+        schedule_.push_back(i);
+        for (int b : reads[i]) --consumers[static_cast<std::size_t>(b)];
+        outputs(i, [&](int b) { done_buf[static_cast<std::size_t>(b)] = 1; });
     }
 }
 
 void Program::optimize() {
-    if (config_.device.fuse_epilogues)
-        for (std::size_t i = 0; i < ops_.size(); ++i)
-            if (!ops_[i].dead && !ops_[i].gemm) fuse_into_gemm(i);
+    if (config_.device.fuse_epilogues) fuse_epilogues();
+    make_schedule();
     for (SymBuf& b : bufs_) b.last_use = -1;
-    for (std::size_t i = 0; i < ops_.size(); ++i) {
-        const Op& op = ops_[i];
-        if (op.dead) continue;
-        for (const auto* vs : {&op.factors, &op.fa, &op.fb, &op.w})
-            for (const View& v : *vs) bufs_[static_cast<std::size_t>(v.buf)].last_use = static_cast<int>(i);
-    }
+    for (std::size_t pos = 0; pos < schedule_.size(); ++pos)
+        for_each_read(ops_[schedule_[pos]],
+                      [&](const View& v) { bufs_[static_cast<std::size_t>(v.buf)].last_use = static_cast<int>(pos); });
 }
 
 double* Program::ptr(int buf) const {
@@ -596,28 +724,75 @@ void Program::run_gemm(const Op& op, double* out) {
     g.cols = static_cast<long long>(ipow(n_, static_cast<int>(op.rb.size())));
     g.a_kmajor = kmajor(fa, op.ra);
     g.b_kmajor = kmajor(fb, op.rb);
-    g.mode = op.mode;
-    g.self_power = op.self_power;
     g.symmetric_out = op.symmetric_out ? 1 : 0;
+    g.mode = kEpiStore;
     g.out = out;
-    // epilogue weights over (row, col) = the consumer's ids epi_row / epi_col
-    g.w.nf = static_cast<int>(op.w.size());
-    for (int f = 0; f < g.w.nf; ++f) {
-        const View& v = op.w[static_cast<std::size_t>(f)];
-        g.w.ptr[f] = ptr(v.buf);
-        g.w.rstride[f][0] = v.stride[static_cast<std::size_t>(op.epi_row)];
-        g.w.cstride[f][0] = v.stride[static_cast<std::size_t>(op.epi_col)];
+    int launched = -1;
+    double* scratch = nullptr;
+    if (!op.epis.empty() || (op.symmetric_out && gemm_tma_eligible(g, nullptr, nullptr))) {
+        EpiSet set;
+        std::size_t part_total = 0;
+        if (op.store) {
+            EpiDesc& d = set.d[set.count++];
+            d.mode = kEpiStore;
+            d.out = out;
+        }
+        if (op.epis.size() + (op.store ? 1 : 0) > static_cast<std::size_t>(kMaxEpilogues))
+            fail(ErrorCode::InvalidArgument, "executor: too many fused epilogues");
+        for (const Op::Epi& e : op.epis) {
+            EpiDesc& d = set.d[set.count++];
+            d.mode = e.mode;
+            d.self_power = e.self_power;
+            d.transpose = e.transpose ? 1 : 0;
+            d.nw = static_cast<int>(e.w.size());
+            for (int f = 0; f < d.nw; ++f) {
+                const View& v = e.w[static_cast<std::size_t>(f)];
+                d.wptr[f] = ptr(v.buf);
+                d.wr[f] = v.stride[static_cast<std::size_t>(e.row_id)];
+                d.wc[f] = v.stride[static_cast<std::size_t>(e.col_id)];
+                // a symmetric matrix reads the same transposed: make the column stride unit
+                if (bufs_[static_cast<std::size_t>(v.buf)].symmetric && d.wr[f] == 1 && d.wc[f] == n_) {
+                    d.wr[f] = n_;
+                    d.wc[f] = 1;
+                }
+            }
+            // weights with a unit row stride go first so the kernel picks row-fastest order
+            // only when no weight prefers columns
+            for (int f = 1; f < d.nw; ++f)
+                if (d.wc[f] == 1 && d.wc[0] != 1) {
+                    std::swap(d.wptr[0], d.wptr[f]);
+                    std::swap(d.wr[0], d.wr[f]);
+                    std::swap(d.wc[0], d.wc[f]);
+                }
+            if (e.ext) {
+                d.out = e.ext;
+            } else {
+                SymBuf& b = bufs_[static_cast<std::size_t>(e.out)];
+                if (!b.real) b.real = rt_->allocate(b.order, n_);
+                d.out = b.real->ptr;
+            }
+            part_total += gemm_epi_partial_entries(g, d.mode);
+        }
+        scratch = part_total ? rt_->scratch(part_total) : nullptr;
+        std::size_t at = 0;
+        for (int q = 0; q < set.count; ++q) {
+            set.d[q].partial = scratch + at;
+            at += gemm_epi_partial_entries(g, set.d[q].mode);
+        }
+        rt_->begin(Runtime::kGemm);
+        launched = launch_gemm_multi(g, set, rt_->stream());
+        rt_->end(Runtime::kGemm);
+        if (launched < 0) fail(ErrorCode::InvalidArgument, "executor: fused GEMM lost TMA eligibility");
+    } else {
+        g.symmetric_out = 0;
+        rt_->begin(Runtime::kGemm);
+        launched = launch_gemm(g, rt_->stream());
+        rt_->end(Runtime::kGemm);
     }
-    const std::size_t part_n = gemm_partial_entries(g);
-    g.partial = part_n ? rt_->scratch(part_n) : nullptr;
-    rt_->begin(Runtime::kGemm);
-    const int launched = launch_gemm(g, rt_->stream());
-    rt_->end(Runtime::kGemm);
     check_cuda(cudaGetLastError(), "gemm launch");
-    rt_->release(g.partial);
+    rt_->release(scratch);
     if (stats_) {
-        const bool tri = g.symmetric_out && g.rows == g.cols && (g.mode == kEpiStore || g.mode == kEpiSumAll) &&
-                         gemm_tma_eligible(g, nullptr, nullptr);
+        const bool tri = op.symmetric_out && g.rows == g.cols && gemm_tma_eligible(g, nullptr, nullptr);
         const long long tm = (g.rows + 127) / 128;
         const std::uint64_t full = static_cast<std::uint64_t>(g.rows) * static_cast<std::uint64_t>(g.cols) *
                                    static_cast<std::uint64_t>(n_);
@@ -632,7 +807,7 @@ void Program::run_gemm(const Op& op, double* out) {
 
 void Program::launch(Op& op) {
     double* out = op.ext;
-    if (!out) {
+    if (!out && (!op.gemm || op.store)) {
         SymBuf& b = bufs_[static_cast<std::size_t>(op.out)];
         if (!b.real) b.real = rt_->allocate(b.order, n_);
         b.real->symmetric = b.symmetric;
@@ -643,16 +818,15 @@ void Program::launch(Op& op) {
 }
 
 void Program::execute() {
-    for (std::size_t i = 0; i < ops_.size(); ++i) {
-        Op& op = ops_[i];
-        if (op.dead) continue;
+    for (std::size_t pos = 0; pos < schedule_.size(); ++pos) {
+        Op& op = ops_[schedule_[pos]];
         launch(op);
-        for (const auto* vs : {&op.factors, &op.fa, &op.fb, &op.w})
-            for (const View& v : *vs) {
-                SymBuf& b = bufs_[static_cast<std::size_t>(v.buf)];
-                if (!b.input && b.last_use == static_cast<int>(i) && b.real && b.real.use_count() == 1 && !keep_.count(v.buf))
-                    b.real.reset();
-            }
+        for_each_read(op, [&](const View& v) {
+            SymBuf& b = bufs_[static_cast<std::size_t>(v.buf)];
+            if (!b.input && b.last_use == static_cast<int>(pos) && b.real && b.real.use_count() == 1 &&
+                !keep_.count(v.buf))
+                b.real.reset();
+        });
     }
 }
 

@@ -136,11 +136,19 @@ struct Op {
     std::vector<View> fa, fb;
     std::vector<int> ra, rb;
     int e = -1;
-    int mode = kEpiStore;
-    std::vector<View> w;  // epilogue factors over ra ∪ rb
-    int self_power = 1;
+    // fused consumers of the product (multi-epilogue); `store` also writes it to `out`
+    struct Epi {
+        int mode = kEpiStore;
+        std::vector<View> w;     // weights over (row_id, col_id) of the consumer's ids
+        int self_power = 1;
+        int row_id = -1, col_id = -1;
+        bool transpose = false;  // Store: the consumer wants (col, row) layout
+        int out = -1;
+        double* ext = nullptr;
+    };
+    std::vector<Epi> epis;
+    bool store = true;
     bool symmetric_out = false;
-    int epi_row = -1, epi_col = -1;  // ids (in the weights' views) of the output row / column
     // destination: a program buffer, or an external device pointer
     int out = -1;
     double* ext = nullptr;
@@ -157,6 +165,7 @@ class Program {
     std::string dump() const;
     struct Totals {
         std::uint64_t gemms = 0, gemm_macs = 0, streams = 0, stream_entries = 0, fused = 0, symmetric = 0;
+        std::uint64_t peak_entries = 0;  // live intermediates + inputs, simulated over the schedule
     };
     Totals totals() const;
 
@@ -190,7 +199,8 @@ class Program {
   private:
     std::string desc(const View& v, const std::vector<int>& dims) const;
     int new_buf(int order, bool symmetric);
-    void fuse_into_gemm(std::size_t s_idx);
+    void fuse_epilogues();
+    bool tma_plain(const View& v, const std::vector<int>& rows, int e) const;
     void launch(Op& op);
     void run_stream(const Op& op, double* out);
     void run_gemm(const Op& op, double* out);
@@ -205,6 +215,8 @@ class Program {
     std::unordered_map<std::string, int> memo_;
     std::vector<std::string> memo_log_;
     std::map<int, bool> keep_;
+    std::vector<std::size_t> schedule_;  // execution order of live ops (memory-aware)
+    void make_schedule();
 };
 
 // Records one notation into a Program with the reference's elimination walk.

@@ -354,7 +354,7 @@ std::size_t gemm_partial_entries(const GemmArgs& a) {
     }
 }
 
-// gemm_tma.cu: returns the number of CTAs launched, or -1 when not eligible
+// gemm_tma.cu: plain-store TMA launch (1) or -1 when not eligible / a reduction
 long long launch_gemm_tma(const GemmArgs& a, cudaStream_t s);
 
 int launch_gemm(const GemmArgs& a, cudaStream_t s) {

@@ -32,15 +32,19 @@ constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4, THREADS = 256;
 constexpr int TILE_DOUBLES = BM * BK;              // 2048 doubles = 16 KiB
 constexpr unsigned STAGE_BYTES = 2u * TILE_DOUBLES * 8u;
 constexpr int GROUP_M = 8;
+constexpr int TP = BN + 1;                          // staged accumulator tile pitch (odd: conflict-free columns)
 
 struct alignas(1024) TmaSmem {
-    double a[STAGES][TILE_DOUBLES];
-    double b[STAGES][TILE_DOUBLES];
+    union {
+        struct {
+            double a[STAGES][TILE_DOUBLES];
+            double b[STAGES][TILE_DOUBLES];
+        } st;
+        double tile[BM * TP];
+    } u;
     unsigned long long full[STAGES];
     unsigned long long empty[STAGES];
-    long long woff_r[kMaxGemmFactors][BM];
-    long long woff_c[kMaxGemmFactors][BN];
-    double red[4][BM];
+    double red[THREADS / 32];
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -108,15 +112,15 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 struct TmaArgs {
-    GemmArgs g;
-    int a_kmajor, b_kmajor;
+    long long rows, cols, n;
+    int symmetric;
+    EpiSet epis;
 };
 
 template <bool AK, bool BKM>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                    TmaArgs args) {
-    const GemmArgs& p = args.g;
+                    const __grid_constant__ TmaArgs p) {
     extern __shared__ unsigned char smem_raw[];
     TmaSmem& sm = *reinterpret_cast<TmaSmem*>(
         (reinterpret_cast<unsigned long long>(smem_raw) + 1023ull) & ~1023ull);
@@ -124,7 +128,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const long long tiles_m = (p.rows + BM - 1) / BM, tiles_n = (p.cols + BN - 1) / BN;
     const long long bid = blockIdx.x;
     long long tm, tn;
-    if (p.symmetric_out) {
+    if (p.symmetric) {
         // upper-triangular tiles, row by row: row tm holds tiles tm..tiles_n-1
         long long rest = bid;
         tm = 0;
@@ -140,7 +144,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tm = first_m + (bid % width) % gsz;
         tn = (bid % width) / gsz;
     }
-    const bool mirror = p.symmetric_out && tm != tn;
+    const bool mirror = p.symmetric && tm != tn;
     const int r0 = static_cast<int>(tm * BM), c0 = static_cast<int>(tn * BN);
     const int KT = static_cast<int>((p.n + BK - 1) / BK);
 
@@ -158,16 +162,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_expect_tx(&sm.full[s], STAGE_BYTES);
         const int k0 = kt * BK;
         if (AK) {
-            tma_load_2d(sm.a[s], &map_a, k0, r0, &sm.full[s]);
+            tma_load_2d(sm.u.st.a[s], &map_a, k0, r0, &sm.full[s]);
         } else {
 #pragma unroll
-            for (int q = 0; q < BM / 16; ++q) tma_load_2d(sm.a[s] + q * 256, &map_a, r0 + 16 * q, k0, &sm.full[s]);
+            for (int q = 0; q < BM / 16; ++q) tma_load_2d(sm.u.st.a[s] + q * 256, &map_a, r0 + 16 * q, k0, &sm.full[s]);
         }
         if (BKM) {
-            tma_load_2d(sm.b[s], &map_b, k0, c0, &sm.full[s]);
+            tma_load_2d(sm.u.st.b[s], &map_b, k0, c0, &sm.full[s]);
         } else {
 #pragma unroll
-            for (int q = 0; q < BN / 16; ++q) tma_load_2d(sm.b[s] + q * 256, &map_b, c0 + 16 * q, k0, &sm.full[s]);
+            for (int q = 0; q < BN / 16; ++q) tma_load_2d(sm.u.st.b[s] + q * 256, &map_b, c0 + 16 * q, k0, &sm.full[s]);
         }
     };
 
@@ -175,31 +179,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&map_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&map_b)) : "memory");
         for (int kt = 0; kt < STAGES && kt < KT; ++kt) issue(kt, kt);
-    }
-    // epilogue offsets can be computed while the first stages land
-    if (p.w.nf) {
-        for (int i = tid; i < p.w.nf * BM; i += THREADS) {
-            const int f = i / BM, r = i % BM;
-            long long g = r0 + r, o = 0;
-            if (g < p.rows)
-                for (int d = p.a.nr - 1; d >= 0; --d) {
-                    const long long q = g / p.n;
-                    o += (g - q * p.n) * p.w.rstride[f][d];
-                    g = q;
-                }
-            sm.woff_r[f][r] = o;
-        }
-        for (int i = tid; i < p.w.nf * BN; i += THREADS) {
-            const int f = i / BN, c = i % BN;
-            long long g = c0 + c, o = 0;
-            if (g < p.cols)
-                for (int d = p.b.nr - 1; d >= 0; --d) {
-                    const long long q = g / p.n;
-                    o += (g - q * p.n) * p.w.cstride[f][d];
-                    g = q;
-                }
-            sm.woff_c[f][c] = o;
-        }
     }
 
     const int warp = tid >> 5, lane = tid & 31;
@@ -216,8 +195,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int s = kt % STAGES;
         const unsigned ph = static_cast<unsigned>((kt / STAGES) & 1);
         mbar_wait(&sm.full[s], ph);
-        const double* ta = sm.a[s];
-        const double* tb = sm.b[s];
+        const double* ta = sm.u.st.a[s];
+        const double* tb = sm.u.st.b[s];
 #pragma unroll
         for (int ks = 0; ks < BK / 4; ++ks) {
             double af[8], bf[4];
@@ -237,107 +216,104 @@ __global__ void __launch_bounds__(THREADS, 1)
             issue(kt + STAGES, s);
         }
     }
-    __syncthreads();  // epilogue offsets visible
+    __syncthreads();  // every stage consumed: the ring becomes the accumulator tile
 
-    auto cpow = [&](double c) { return p.self_power == 2 ? c * c : c; };
-    auto weight = [&](int rl, int cl) {
-        double w = p.scale;
-        for (int f = 0; f < p.w.nf; ++f) w *= __ldg(p.w.ptr[f] + sm.woff_r[f][rl] + sm.woff_c[f][cl]);
-        return w;
-    };
+    double* tile = sm.u.tile;
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+            const int r = wm * 64 + mi * 8 + g, c = wn * 32 + ni * 8 + 2 * t;
+            tile[r * TP + c] = acc[mi][ni][0];
+            tile[r * TP + c + 1] = acc[mi][ni][1];
+        }
+    __syncthreads();
 
-    if (p.mode == kEpiStore) {
-#pragma unroll
-        for (int mi = 0; mi < 8; ++mi) {
-            const int rl = wm * 64 + mi * 8 + g;
-            const long long r = r0 + rl;
-            if (r >= p.rows) continue;
-#pragma unroll
-            for (int ni = 0; ni < 4; ++ni) {
-                const int cl = wn * 32 + ni * 8 + 2 * t;
-                const long long c = c0 + cl;
-                double* dst = p.out + r * p.cols + c;
-                const double v0 = cpow(acc[mi][ni][0]) * weight(rl, cl);
-                if (c + 1 < p.cols) {
-                    const double v1 = cpow(acc[mi][ni][1]) * weight(rl, cl + 1);
-                    if ((reinterpret_cast<unsigned long long>(dst) & 15) == 0)
-                        *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
-                    else {
-                        dst[0] = v0;
-                        dst[1] = v1;
-                    }
-                    if (mirror) {
-                        p.out[c * p.cols + r] = v0;
-                        p.out[(c + 1) * p.cols + r] = v1;
-                    }
-                } else if (c < p.cols) {
-                    dst[0] = v0;
-                    if (mirror) p.out[c * p.cols + r] = v0;
+    const long long rows = p.rows, cols = p.cols;
+    for (int q = 0; q < p.epis.count; ++q) {
+        const EpiDesc& d = p.epis.d[q];
+        auto W = [&](long long R, long long C) {
+            double w = 1.0;
+            for (int f = 0; f < d.nw; ++f) w *= __ldg(d.wptr[f] + R * d.wr[f] + C * d.wc[f]);
+            return w;
+        };
+        auto P = [&](double x) { return d.self_power == 2 ? x * x : x; };
+        // element order: column-fastest unless the first weight is column-major
+        const bool cfast = !(d.nw > 0 && d.wr[0] == 1 && d.wc[0] != 1);
+        if (d.mode == kEpiStore || d.mode == kEpiSumAll) {
+            double s = 0.0;
+            for (int i = tid; i < BM * BN; i += THREADS) {
+                const int r = cfast ? (i >> 7) : (i & 127), c = cfast ? (i & 127) : (i >> 7);
+                const long long R = r0 + r, C = c0 + c;
+                if (R >= rows || C >= cols) continue;
+                const double v = P(tile[r * TP + c]) * W(R, C);
+                if (d.mode == kEpiStore) d.out[d.transpose ? C * rows + R : R * cols + C] = v;
+                else s += v;
+            }
+            if (mirror)  // the transposed tile (C, R): same values, weights at (C, R)
+                for (int i = tid; i < BM * BN; i += THREADS) {
+                    const int c = cfast ? (i >> 7) : (i & 127), r = cfast ? (i & 127) : (i >> 7);
+                    const long long R = r0 + r, C = c0 + c;
+                    if (R >= rows || C >= cols) continue;
+                    const double v = P(tile[r * TP + c]) * W(C, R);
+                    if (d.mode == kEpiStore) d.out[d.transpose ? R * rows + C : C * cols + R] = v;
+                    else s += v;
                 }
+            if (d.mode == kEpiSumAll) {
+                s = warp_sum(s);
+                if (lane == 0) sm.red[warp] = s;
+                __syncthreads();
+                if (tid == 0) {
+                    double tot = 0.0;
+                    for (int w = 0; w < THREADS / 32; ++w) tot += sm.red[w];
+                    d.partial[blockIdx.x] = tot;
+                }
+                __syncthreads();
+            }
+        } else if (d.mode == kEpiSumCols) {  // out[R] = sum_C
+            for (int r = warp; r < BM; r += THREADS / 32) {
+                const long long R = r0 + r;
+                double s = 0.0;
+                for (int c = lane; c < BN; c += 32) {
+                    const long long C = c0 + c;
+                    if (R < rows && C < cols) s += P(tile[r * TP + c]) * W(R, C);
+                }
+                s = warp_sum(s);
+                if (lane == 0 && R < rows) d.partial[tn * rows + R] = s;
+            }
+            if (mirror)
+                for (int c = warp; c < BN; c += THREADS / 32) {
+                    const long long C = c0 + c;
+                    double s = 0.0;
+                    for (int r = lane; r < BM; r += 32) {
+                        const long long R = r0 + r;
+                        if (R < rows && C < cols) s += P(tile[r * TP + c]) * W(C, R);
+                    }
+                    s = warp_sum(s);
+                    if (lane == 0 && C < rows) d.partial[tm * rows + C] = s;
+                }
+        } else {  // kEpiSumRows: out[C] = sum_R
+            if (tid < BN) {
+                const int c = tid;
+                const long long C = c0 + c;
+                double s = 0.0;
+                for (int r = 0; r < BM; ++r) {
+                    const long long R = r0 + r;
+                    if (R < rows && C < cols) s += P(tile[r * TP + c]) * W(R, C);
+                }
+                if (C < cols) d.partial[tm * cols + C] = s;
+            }
+            if (mirror && tid >= THREADS - BM) {
+                const int r = tid - (THREADS - BM);
+                const long long R = r0 + r;
+                double s = 0.0;
+                for (int c = 0; c < BN; ++c) {
+                    const long long C = c0 + c;
+                    if (R < rows && C < cols) s += P(tile[r * TP + c]) * W(C, R);
+                }
+                if (R < cols) d.partial[tn * cols + R] = s;
             }
         }
-        return;
-    }
-
-    auto val = [&](int mi, int ni, int h) {
-        const int rl = wm * 64 + mi * 8 + g, cl = wn * 32 + ni * 8 + 2 * t + h;
-        if (r0 + rl >= p.rows || c0 + cl >= p.cols) return 0.0;
-        return cpow(acc[mi][ni][h]) * weight(rl, cl);
-    };
-
-    if (p.mode == kEpiSumAll) {
-        double s = 0.0;
-#pragma unroll
-        for (int mi = 0; mi < 8; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < 4; ++ni) s += val(mi, ni, 0) + val(mi, ni, 1);
-        s = warp_sum(s);
-        if (lane == 0) sm.red[0][warp] = s;
-        __syncthreads();
-        if (tid == 0) {
-            double tot = 0.0;
-            for (int w = 0; w < THREADS / 32; ++w) tot += sm.red[0][w];
-            p.partial[blockIdx.x] = mirror ? 2.0 * tot : tot;
-        }
-        return;
-    }
-
-    if (p.mode == kEpiSumCols) {
-#pragma unroll
-        for (int mi = 0; mi < 8; ++mi) {
-            double s = 0.0;
-#pragma unroll
-            for (int ni = 0; ni < 4; ++ni) s += val(mi, ni, 0) + val(mi, ni, 1);
-            s += __shfl_xor_sync(0xffffffffu, s, 1);
-            s += __shfl_xor_sync(0xffffffffu, s, 2);
-            if (t == 0) sm.red[wn][wm * 64 + mi * 8 + g] = s;
-        }
-        __syncthreads();
-        for (int rl = tid; rl < BM; rl += THREADS) {
-            const long long r = r0 + rl;
-            if (r < p.rows)
-                p.partial[tn * p.rows + r] = ((sm.red[0][rl] + sm.red[1][rl]) + sm.red[2][rl]) + sm.red[3][rl];
-        }
-        return;
-    }
-
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            double s = 0.0;
-#pragma unroll
-            for (int mi = 0; mi < 8; ++mi) s += val(mi, ni, h);
-            s += __shfl_xor_sync(0xffffffffu, s, 4);
-            s += __shfl_xor_sync(0xffffffffu, s, 8);
-            s += __shfl_xor_sync(0xffffffffu, s, 16);
-            if (g == 0) sm.red[wm][wn * 32 + ni * 8 + 2 * t + h] = s;
-        }
-    }
-    __syncthreads();
-    for (int cl = tid; cl < BN; cl += THREADS) {
-        const long long c = c0 + cl;
-        if (c < p.cols) p.partial[tm * p.cols + c] = sm.red[0][cl] + sm.red[1][cl];
     }
 }
 
@@ -399,10 +375,32 @@ long long launch_tma(const CUtensorMap& ma, const CUtensorMap& mb, const TmaArgs
     std::call_once(once, [&] {
         cudaFuncSetAttribute(gemm_tma_kernel<AK, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     });
-    const long long tm = (args.g.rows + BM - 1) / BM, tn = (args.g.cols + BN - 1) / BN;
-    const long long tiles = args.g.symmetric_out ? tm * (tm + 1) / 2 : tm * tn;
+    const long long tm = (args.rows + BM - 1) / BM, tn = (args.cols + BN - 1) / BN;
+    const long long tiles = args.symmetric ? tm * (tm + 1) / 2 : tm * tn;
     gemm_tma_kernel<AK, BKM><<<static_cast<unsigned>(tiles), THREADS, bytes, s>>>(ma, mb, args);
     return tiles;
+}
+
+__global__ void epi_finalize_scalar(const double* partial, long long P, double* out) {
+    __shared__ double red[32];
+    double acc = 0.0;
+    for (long long i = threadIdx.x; i < P; i += blockDim.x) acc += partial[i];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) out[0] = v;
+    }
+}
+
+__global__ void epi_finalize_vector(const double* partial, long long P, long long len, double* out) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= len) return;
+    double acc = 0.0;
+    for (long long q = 0; q < P; ++q) acc += partial[q * len + i];
+    out[i] = acc;
 }
 
 }  // namespace
@@ -429,21 +427,75 @@ bool gemm_tma_eligible(const GemmArgs& a, int* a_kmajor_out, int* b_kmajor_out) 
     return layout(a.a.ptr[0], ars, aks, a_kmajor) && layout(a.b.ptr[0], brs, bks, b_kmajor) && encoder() != nullptr;
 }
 
-long long launch_gemm_tma(const GemmArgs& in, cudaStream_t s) {
+std::size_t gemm_epi_partial_entries(const GemmArgs& a, int mode) {
+    const long long tm = (a.rows + BM - 1) / BM, tn = (a.cols + BN - 1) / BN;
+    switch (mode) {
+        case kEpiSumAll: return static_cast<std::size_t>(tm * tn);
+        case kEpiSumCols: return static_cast<std::size_t>(tn * a.rows);
+        case kEpiSumRows: return static_cast<std::size_t>(tm * a.cols);
+        default: return 0;
+    }
+}
+
+int launch_gemm_multi(const GemmArgs& a, const EpiSet& epis, cudaStream_t s) {
     int ak = 1, bk = 1;
-    if (!gemm_tma_eligible(in, &ak, &bk)) return -1;
-    GemmArgs a = in;
-    // upper tiles only for symmetric store / full reductions with square output
-    if (a.symmetric_out && !(a.rows == a.cols && (a.mode == kEpiStore || a.mode == kEpiSumAll))) a.symmetric_out = 0;
+    if (!gemm_tma_eligible(a, &ak, &bk) || epis.count < 1 || epis.count > kMaxEpilogues) return -1;
     long long ars, aks, brs, bks;
     plain(a.a, a.n, ars, aks);
     plain(a.b, a.n, brs, bks);
     CUtensorMap ma, mb;
     if (!encode(&ma, a.a.ptr[0], ak, a.rows, a.n, ars, aks) || !encode(&mb, a.b.ptr[0], bk, a.cols, a.n, brs, bks))
         return -1;
-    TmaArgs args{a, ak, bk};
-    if (ak) return bk ? launch_tma<true, true>(ma, mb, args, s) : launch_tma<true, false>(ma, mb, args, s);
-    return bk ? launch_tma<false, true>(ma, mb, args, s) : launch_tma<false, false>(ma, mb, args, s);
+    TmaArgs args;
+    args.rows = a.rows;
+    args.cols = a.cols;
+    args.n = a.n;
+    args.symmetric = (a.symmetric_out && a.rows == a.cols) ? 1 : 0;
+    args.epis = epis;
+    long long blocks;
+    if (ak) blocks = bk ? launch_tma<true, true>(ma, mb, args, s) : launch_tma<true, false>(ma, mb, args, s);
+    else blocks = bk ? launch_tma<false, true>(ma, mb, args, s) : launch_tma<false, false>(ma, mb, args, s);
+    int launched = 1;
+    const long long tm = (a.rows + BM - 1) / BM, tn = (a.cols + BN - 1) / BN;
+    for (int q = 0; q < epis.count; ++q) {
+        const EpiDesc& d = epis.d[q];
+        if (d.mode == kEpiSumAll) {
+            epi_finalize_scalar<<<1, 1024, 0, s>>>(d.partial, blocks, d.out);
+        } else if (d.mode == kEpiSumCols) {
+            epi_finalize_vector<<<static_cast<unsigned>((a.rows + 255) / 256), 256, 0, s>>>(d.partial, tn, a.rows, d.out);
+        } else if (d.mode == kEpiSumRows) {
+            epi_finalize_vector<<<static_cast<unsigned>((a.cols + 255) / 256), 256, 0, s>>>(d.partial, tm, a.cols, d.out);
+        } else {
+            continue;
+        }
+        ++launched;
+    }
+    return launched;
+}
+
+// Single-epilogue entry used by launch_gemm: plain store, or one fused
+// epilogue whose weights fit the multi-epilogue form.
+long long launch_gemm_tma(const GemmArgs& in, cudaStream_t s) {
+    int ak = 1, bk = 1;
+    if (!gemm_tma_eligible(in, &ak, &bk)) return -1;
+    if (in.w.nf > kMaxEpiW || (in.w.nf > 0 && (in.a.nr != 1 || in.b.nr != 1))) return -1;
+    if (in.mode != kEpiStore) return -1;  // reductions go through launch_gemm_multi
+    EpiSet e;
+    e.count = 1;
+    EpiDesc& d = e.d[0];
+    d.mode = kEpiStore;
+    d.self_power = in.self_power;
+    d.nw = in.w.nf;
+    for (int f = 0; f < d.nw; ++f) {
+        d.wptr[f] = in.w.ptr[f];
+        d.wr[f] = in.w.rstride[f][0];
+        d.wc[f] = in.w.cstride[f][0];
+    }
+    d.out = in.out;
+    GemmArgs a = in;
+    if (a.symmetric_out && a.rows != a.cols) a.symmetric_out = 0;
+    const int k = launch_gemm_multi(a, e, s);
+    return k > 0 ? 1 : -1;
 }
 
 }  // namespace ustats::dev

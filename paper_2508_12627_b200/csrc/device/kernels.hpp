@@ -72,6 +72,27 @@ struct GemmArgs {
     int self_power = 1;         // epilogue value = C^self_power * W (2: the consumer read C twice)
 };
 
+// Multi-consumer epilogues of the TMA GEMM: every consumer of a GEMM output
+// that iterates exactly over its (row, col) space runs on the accumulator tile
+// staged in shared memory. Weights W(r,c) = prod_f wptr[f][r*wr[f] + c*wc[f]].
+constexpr int kMaxEpiW = 4;
+constexpr int kMaxEpilogues = 40;
+struct EpiDesc {
+    int mode = kEpiStore;
+    int self_power = 1;
+    int nw = 0;
+    int transpose = 0;          // Store: write out[C * rows + R] instead of out[R * cols + C]
+    const double* wptr[kMaxEpiW] = {};
+    long long wr[kMaxEpiW] = {};
+    long long wc[kMaxEpiW] = {};
+    double* out = nullptr;      // Store: rows x cols matrix; reductions: finalize target
+    double* partial = nullptr;  // reduction scratch (gemm_epi_partial_entries)
+};
+struct EpiSet {
+    int count = 0;
+    EpiDesc d[kMaxEpilogues];
+};
+
 // ------------------------------------------------------------- launchers
 // Launchers return the number of kernels they enqueued.
 int launch_stream(const StreamArgs& a, double* scratch, std::size_t scratch_entries,
@@ -82,6 +103,11 @@ std::size_t stream_scratch_entries(const StreamArgs& a, int sm_count);
 // (gemm_tma.cu), otherwise the lazy-product gather kernel (gemm_f64.cu).
 int launch_gemm(const GemmArgs& a, cudaStream_t s);
 bool gemm_tma_eligible(const GemmArgs& a, int* a_kmajor, int* b_kmajor);
+// Multi-epilogue TMA GEMM (a.mode/a.w/a.out ignored; symmetric_out computes
+// upper tiles and mirrors every epilogue). Returns kernels launched, or -1
+// if the operands are not TMA-eligible.
+int launch_gemm_multi(const GemmArgs& a, const EpiSet& epis, cudaStream_t s);
+std::size_t gemm_epi_partial_entries(const GemmArgs& a, int mode);
 std::size_t gemm_partial_entries(const GemmArgs& a);
 
 // Zero every entry of an order-`order` tensor whose multi-index repeats a

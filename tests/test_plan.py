@@ -32,7 +32,7 @@ def test_c2_single_symmetric_fused_gemm():
     n = CONFIGS["C2"].n
     tiles = n // 128
     assert tot["gemm_macs"] == n ** 3 // (tiles * tiles) * (tiles * (tiles + 1) // 2)
-    assert "epi=sum_all pow=2 SYM -> term" in text
+    assert "SYM nostore | epi sum_all pow=2 -> term" in text
 
 
 def test_sharing_never_increases_work():

@@ -1,6 +1,6 @@
 # iteration loop: GPU parity tests + quick bench lines
 cd $GRAFT_REPO_ROOT
-timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | grep -v "^  File" | tail -25
+timeout 1200 python -m pytest tests -m gpu -q -x -v 2>&1 | grep -v "^  File" | grep -v PASSED | tail -25
 for c in C2 C1 C3 C4; do
   timeout 600 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
   python -c "
