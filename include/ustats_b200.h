@@ -46,7 +46,8 @@ typedef struct us_config {
     int32_t device;              /* CUDA ordinal, -1 = current */
     int32_t rank;                /* term-sharding rank */
     int32_t world_size;          /* term-sharding world size (1 = all terms here) */
-    int32_t flags;               /* bit0 share, bit1 fuse epilogues, bit2 symmetry, bit3 reorder;
+    int32_t flags;               /* bit0 share, bit1 fuse epilogues, bit2 symmetry, bit3 reorder,
+                                    bit4 donate device inputs (sparsified in place, no copy);
                                     US_FLAGS_DEFAULT = 0xF */
 } us_config;
 

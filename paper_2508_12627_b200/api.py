@@ -55,6 +55,7 @@ class Config:
     fuse_epilogues: bool = True
     symmetry: bool = True
     reorder: bool = True
+    donate_inputs: bool = False  # device inputs sparsified in place (saves one copy)
 
     def native(self) -> N.UsConfig:
         c = N.UsConfig()
@@ -70,7 +71,7 @@ class Config:
         c.rank = self.rank
         c.world_size = self.world_size
         c.flags = (1 if self.share else 0) | (2 if self.fuse_epilogues else 0) | \
-                  (4 if self.symmetry else 0) | (8 if self.reorder else 0)
+                  (4 if self.symmetry else 0) | (8 if self.reorder else 0) | (16 if self.donate_inputs else 0)
         return c
 
 

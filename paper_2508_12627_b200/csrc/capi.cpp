@@ -58,6 +58,7 @@ ustats::Config to_config(const us_config* c) {
     cfg.device.fuse_epilogues = c->flags & 2;
     cfg.device.exploit_symmetry = c->flags & 4;
     cfg.device.reorder_for_sharing = c->flags & 8;
+    cfg.device.donate_inputs = c->flags & 16;
     return cfg;
 }
 

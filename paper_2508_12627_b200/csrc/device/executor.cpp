@@ -4,6 +4,8 @@
 #include <algorithm>
 #include <bit>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -20,7 +22,11 @@ void check_cuda(cudaError_t e, const char* what) {
 
 // ---------------------------------------------------------------- Runtime
 DeviceBuffer::~DeviceBuffer() {
-    if (ptr && !borrowed && rt) cudaFreeAsync(ptr, rt->stream());
+    if (ptr && !borrowed && rt) {
+        cudaFreeAsync(ptr, rt->stream());
+        if (std::getenv("USTATS_SCHED_DEBUG") && entries() * 8 > (1ull << 30))
+            std::fprintf(stderr, "[free] %.2f GiB\n", entries() * 8 / 1073741824.0);
+    }
 }
 
 std::uint64_t DeviceBuffer::entries() const {
@@ -59,8 +65,16 @@ Buf Runtime::allocate(int order, long long n) {
     b->n = n;
     b->rt = this;
     void* p = nullptr;
-    check_cuda(cudaMallocAsync(&p, std::max<std::uint64_t>(b->entries(), 1) * sizeof(double), stream_),
-               "cudaMallocAsync");
+    const std::size_t bytes = std::max<std::uint64_t>(b->entries(), 1) * sizeof(double);
+    const cudaError_t e = cudaMallocAsync(&p, bytes, stream_);
+    if (e != cudaSuccess || std::getenv("USTATS_SCHED_DEBUG")) {
+        std::size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        if (e != cudaSuccess || bytes > (1ull << 30))
+            std::fprintf(stderr, "[alloc] %.2f GiB -> %s (free %.2f / %.2f GiB)\n", bytes / 1073741824.0,
+                         cudaGetErrorString(e), fr / 1073741824.0, tot / 1073741824.0);
+    }
+    check_cuda(e, "cudaMallocAsync");
     b->ptr = static_cast<double*>(p);
     return b;
 }
@@ -183,6 +197,7 @@ int Program::add_symbolic_input(int order, bool symmetric) {
 
 Program::Totals Program::totals() const {
     Totals t;
+    t.peak_entries = static_cast<std::uint64_t>(sched_peak_ / 8.0);
     for (const Op& op : ops_) {
         if (op.dead) continue;
         if (op.gemm) {
@@ -201,29 +216,6 @@ Program::Totals Program::totals() const {
             t.stream_entries += ipow(n_, static_cast<int>(op.out_ids.size()) + std::popcount(op.sum)) *
                                 static_cast<std::uint64_t>(op.factors.size());
         }
-    }
-    // live-set simulation: inputs always live; outputs from their op to last use
-    std::uint64_t live = 0;
-    for (const SymBuf& b : bufs_)
-        if (b.input) live += ipow(n_, b.order);
-    t.peak_entries = live;
-    for (std::size_t pos = 0; pos < schedule_.size(); ++pos) {
-        const Op& op = ops_[schedule_[pos]];
-        if (!op.ext && op.out >= 0 && (!op.gemm || op.store))
-            live += ipow(n_, bufs_[static_cast<std::size_t>(op.out)].order);
-        if (op.gemm)
-            for (const Op::Epi& e : op.epis)
-                if (!e.ext && e.out >= 0) live += ipow(n_, bufs_[static_cast<std::size_t>(e.out)].order);
-        t.peak_entries = std::max(t.peak_entries, live);
-        std::vector<int> done;
-        for_each_read(op, [&](const View& v) {
-            const SymBuf& b = bufs_[static_cast<std::size_t>(v.buf)];
-            if (!b.input && b.last_use == static_cast<int>(pos) &&
-                std::find(done.begin(), done.end(), v.buf) == done.end()) {
-                done.push_back(v.buf);
-                live -= ipow(n_, b.order);
-            }
-        });
     }
     return t;
 }
@@ -541,70 +533,155 @@ void Program::fuse_epilogues() {
     }
 }
 
-// Memory-aware list scheduling: among ops whose inputs exist, run the one
-// that grows the live set least (allocation minus buffers it frees), ties in
-// recording order. Keeps the working set of n^2 intermediates small when
-// sub-contractions are shared by V-terms far apart in enumeration order.
-void Program::make_schedule() {
+// Memory-bounded scheduling. Ops that allocate no tensor of order >= 2 run
+// eagerly as soon as their inputs exist (they only free memory); the order in
+// which the "big" producers (GEMM products, materialized Hadamard operands)
+// run is searched depth-first, cheapest resulting live set first, pruning any
+// branch whose peak (inputs + live intermediates) exceeds the budget. Shared
+// sub-contractions make the naive recording order hold many n^2 products at
+// once (C5: 412 GB); the search finds orders that fit one B200.
+void Program::make_schedule(double budget) {
     const std::size_t N = ops_.size();
-    std::vector<int> producer(bufs_.size(), -1);
-    auto outputs = [&](std::size_t i, auto&& f) {
-        const Op& op = ops_[i];
-        if (!op.ext && op.out >= 0 && (!op.gemm || op.store)) f(op.out);
-        for (const Op::Epi& e : op.epis)
-            if (!e.ext && e.out >= 0) f(e.out);
-    };
-    for (std::size_t i = 0; i < N; ++i)
-        if (!ops_[i].dead) outputs(i, [&](int b) { producer[static_cast<std::size_t>(b)] = static_cast<int>(i); });
-    std::vector<std::vector<int>> reads(N);
+    std::vector<std::vector<int>> reads(N), outs(N);
     std::vector<int> consumers(bufs_.size(), 0);
     for (std::size_t i = 0; i < N; ++i) {
-        if (ops_[i].dead) continue;
-        std::vector<int>& r = reads[i];
-        for_each_read(ops_[i], [&](const View& v) {
-            if (std::find(r.begin(), r.end(), v.buf) == r.end()) r.push_back(v.buf);
+        const Op& op = ops_[i];
+        if (op.dead) continue;
+        for_each_read(op, [&](const View& v) {
+            if (std::find(reads[i].begin(), reads[i].end(), v.buf) == reads[i].end()) reads[i].push_back(v.buf);
         });
-        for (int b : r) ++consumers[static_cast<std::size_t>(b)];
+        for (int b : reads[i]) ++consumers[static_cast<std::size_t>(b)];
+        if (!op.ext && op.out >= 0 && (!op.gemm || op.store)) outs[i].push_back(op.out);
+        for (const Op::Epi& e : op.epis)
+            if (!e.ext && e.out >= 0) outs[i].push_back(e.out);
     }
-    std::vector<char> done_buf(bufs_.size(), 0);
+    auto size = [&](int b) { return 8.0 * static_cast<double>(ipow(n_, bufs_[static_cast<std::size_t>(b)].order)); };
+    std::vector<char> big(N, 0);
+    for (std::size_t i = 0; i < N; ++i)
+        for (int b : outs[i]) big[i] |= bufs_[static_cast<std::size_t>(b)].order >= 2;
+
+    struct State {
+        std::vector<char> exec, avail;
+        std::vector<int> left;
+        double live = 0, peak = 0;
+        std::vector<std::size_t> order;
+    };
+    State s0;
+    s0.exec.assign(N, 0);
+    s0.avail.assign(bufs_.size(), 0);
+    s0.left = consumers;
     for (std::size_t b = 0; b < bufs_.size(); ++b)
-        if (bufs_[b].input || producer[b] < 0) done_buf[b] = 1;
-    std::vector<char> scheduled(N, 0);
-    schedule_.clear();
+        if (bufs_[b].input) {
+            s0.avail[b] = 1;
+            s0.live += size(static_cast<int>(b));
+        }
+    s0.peak = s0.live;
     std::size_t live_ops = 0;
     for (const Op& op : ops_) live_ops += !op.dead;
-    auto size = [&](int b) { return static_cast<double>(ipow(n_, bufs_[static_cast<std::size_t>(b)].order)); };
-    while (schedule_.size() < live_ops) {
-        long best = -1;
-        double best_delta = 0;
-        for (std::size_t i = 0; i < N; ++i) {
-            if (ops_[i].dead || scheduled[i]) continue;
-            bool ready = true;
-            for (int b : reads[i]) ready &= done_buf[static_cast<std::size_t>(b)] != 0;
-            if (!ready) continue;
-            double delta = 0.0;
-            outputs(i, [&](int b) { delta += size(b); });
-            for (int b : reads[i])
-                if (!bufs_[static_cast<std::size_t>(b)].input && consumers[static_cast<std::size_t>(b)] == 1 &&
-                    !keep_.count(b))
-                    delta -= size(b);
-            if (best < 0 || delta < best_delta) {
-                best = static_cast<long>(i);
-                best_delta = delta;
-            }
+
+    auto ready = [&](const State& st, std::size_t i) {
+        if (ops_[i].dead || st.exec[i]) return false;
+        for (int b : reads[i])
+            if (!st.avail[static_cast<std::size_t>(b)]) return false;
+        return true;
+    };
+    auto run = [&](State& st, std::size_t i) {
+        st.exec[i] = 1;
+        st.order.push_back(i);
+        for (int b : outs[i]) {
+            st.avail[static_cast<std::size_t>(b)] = 1;
+            st.live += size(b);
         }
-        if (best < 0) fail(ErrorCode::InvalidArgument, "executor: dependency cycle in the device program");
-        const auto i = static_cast<std::size_t>(best);
-        scheduled[i] = 1;
-        schedule_.push_back(i);
-        for (int b : reads[i]) --consumers[static_cast<std::size_t>(b)];
-        outputs(i, [&](int b) { done_buf[static_cast<std::size_t>(b)] = 1; });
+        st.peak = std::max(st.peak, st.live);
+        for (int b : reads[i])
+            if (--st.left[static_cast<std::size_t>(b)] == 0 && !bufs_[static_cast<std::size_t>(b)].input && !keep_.count(b))
+                st.live -= size(b);
+    };
+    auto drain = [&](State& st) {  // every ready op that allocates nothing big
+        for (bool again = true; again;) {
+            again = false;
+            for (std::size_t i = 0; i < N; ++i)
+                if (!big[i] && ready(st, i)) {
+                    run(st, i);
+                    again = true;
+                }
+        }
+    };
+    std::size_t nodes = 0;
+    const std::size_t node_limit = 20000;
+    bool found = false;
+    State best;
+    auto dfs = [&](auto&& self, State st) -> void {
+        if (found || ++nodes > node_limit) return;
+        drain(st);
+        if (st.order.size() == live_ops) {
+            found = true;
+            best = std::move(st);
+            return;
+        }
+        std::vector<std::pair<double, State>> next, idle;
+        for (std::size_t i = 0; i < N; ++i) {
+            if (!big[i] || !ready(st, i)) continue;
+            State t = st;
+            run(t, i);
+            // a product read by exactly one other op (a materialized GEMM
+            // operand) is consumed at once: the pair is one scheduling step
+            for (int b : outs[i]) {
+                if (consumers[static_cast<std::size_t>(b)] != 1) continue;
+                for (std::size_t j = 0; j < N; ++j)
+                    if (std::find(reads[j].begin(), reads[j].end(), b) != reads[j].end() && ready(t, j)) run(t, j);
+            }
+            drain(t);
+            if (budget > 0 && t.peak > budget) continue;
+            // products nobody can consume yet only hold memory: try them last
+            bool useful = false;
+            for (int b : outs[i]) useful |= t.left[static_cast<std::size_t>(b)] < consumers[static_cast<std::size_t>(b)];
+            (useful ? next : idle).emplace_back(t.live, std::move(t));
+        }
+        std::stable_sort(idle.begin(), idle.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        std::stable_sort(next.begin(), next.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        for (auto& nx : idle) next.push_back(std::move(nx));
+        for (auto& nx : next) {
+            self(self, std::move(nx.second));
+            if (found) return;
+        }
+    };
+    dfs(dfs, s0);
+    if (std::getenv("USTATS_SCHED_DEBUG"))
+        std::fprintf(stderr, "[sched] ops=%zu nodes=%zu found=%d budget=%.1f GiB inputs=%.1f GiB\n", live_ops, nodes,
+                     found ? 1 : 0, budget / 1073741824.0, s0.live / 1073741824.0);
+    if (!found) {  // no order within budget: least-growth greedy (may exceed the budget)
+        State st = s0;
+        while (st.order.size() < live_ops) {
+            drain(st);
+            if (st.order.size() == live_ops) break;
+            long pick = -1;
+            double pick_live = 0;
+            for (std::size_t i = 0; i < N; ++i) {
+                if (!big[i] || !ready(st, i)) continue;
+                State t = st;
+                run(t, i);
+                drain(t);
+                if (pick < 0 || t.live < pick_live) {
+                    pick = static_cast<long>(i);
+                    pick_live = t.live;
+                }
+            }
+            if (pick < 0) fail(ErrorCode::InvalidArgument, "executor: dependency cycle in the device program");
+            run(st, static_cast<std::size_t>(pick));
+            if (std::getenv("USTATS_SCHED_DEBUG"))
+                std::fprintf(stderr, "[sched] greedy big op %ld live %.1f GiB peak %.1f GiB\n", pick, st.live / 1073741824.0,
+                             st.peak / 1073741824.0);
+        }
+        best = std::move(st);
     }
+    schedule_ = best.order;
+    sched_peak_ = best.peak;
 }
 
-void Program::optimize() {
+void Program::optimize(double budget_bytes) {
     if (config_.device.fuse_epilogues) fuse_epilogues();
-    make_schedule();
+    make_schedule(budget_bytes);
     for (SymBuf& b : bufs_) b.last_use = -1;
     for (std::size_t pos = 0; pos < schedule_.size(); ++pos)
         for_each_read(ops_[schedule_[pos]],
@@ -1222,10 +1299,16 @@ StatisticResult lattice_statistic(const std::vector<const double*>& inputs, bool
             tensors.push_back(hit->second);
             continue;
         }
-        Buf b = rt.allocate(order, n);
-        check_cuda(cudaMemcpyAsync(b->ptr, inputs[k], b->entries() * sizeof(double),
-                                   inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, rt.stream()),
-                   "upload");
+        Buf b;
+        if (inputs_on_device && config.device.donate_inputs) {
+            b = rt.borrow(inputs[k], order, n);  // sparsified in place: the caller donated it
+        } else {
+            b = rt.allocate(order, n);
+            check_cuda(cudaMemcpyAsync(b->ptr, inputs[k], b->entries() * sizeof(double),
+                                       inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                       rt.stream()),
+                       "upload");
+        }
         rt.begin(Runtime::kOther);
         if (mode == LatticeMode::Sparsified)
             res.stats.kernel_launches += static_cast<std::uint64_t>(launch_sparsify(b->ptr, order, n, rt.stream()));
@@ -1262,7 +1345,16 @@ StatisticResult lattice_statistic(const std::vector<const double*>& inputs, bool
         std::vector<int> ids;
         for (const Buf& b : tensors) ids.push_back(prog.add_input(b));
         record_terms(prog, plan, ids, config.device.rank, d_v, &res.stats);
-        prog.optimize();
+        double budget = static_cast<double>(config.device.memory_budget_bytes);
+        if (budget <= 0) {
+            std::size_t free_b = 0, total_b = 0;
+            check_cuda(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+            double inputs = 0;
+            for (const auto& kv : by_ptr) inputs += 8.0 * static_cast<double>(kv.second->entries());
+            // inputs are already resident: the program may use what is free, minus headroom
+            budget = inputs + 0.94 * static_cast<double>(free_b) - 2.0e9;
+        }
+        prog.optimize(budget);
         res.plan_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
         prog.execute();
     }
@@ -1364,25 +1456,24 @@ std::string plan_summary(const std::vector<IndexTuple>& zero_sig, int m, long lo
     TermPlan plan = plan_terms(zero_sig, m, n, LatticeMode::Sparsified, config);
     DevStats stats;
     Program prog(nullptr, n, config, &stats);
+    // Declared-symmetric inputs: every order-2 factor is the same matrix (the
+    // BASELINE configs alias one matrix); other factors are distinct.
     std::vector<int> ids;
-    std::map<std::pair<int, int>, int> same;  // identical (order) inputs alias only if the caller says so
-    for (const IndexTuple& t : zero_sig) ids.push_back(prog.add_symbolic_input(static_cast<int>(t.size()), inputs_symmetric));
-    // Treat all factors of equal order as the same tensor when symmetric inputs
-    // are declared (the BASELINE configs alias one matrix).
-    if (inputs_symmetric) {
-        std::map<int, int> first;
-        for (std::size_t k = 0; k < ids.size(); ++k) {
-            const int order = static_cast<int>(zero_sig[k].size());
-            if (order == 2) {
-                auto it = first.find(order);
-                if (it == first.end()) first[order] = ids[k];
-                else ids[k] = it->second;
-            }
+    int shared_matrix = -1;
+    for (const IndexTuple& t : zero_sig) {
+        const int order = static_cast<int>(t.size());
+        if (inputs_symmetric && order == 2) {
+            if (shared_matrix < 0) shared_matrix = prog.add_symbolic_input(2, true);
+            ids.push_back(shared_matrix);
+        } else {
+            ids.push_back(prog.add_symbolic_input(order, false));
         }
     }
     std::vector<double> dummy(plan.rgs.size() + 1);
     record_terms(prog, plan, ids, 0, dummy.data(), &stats);
-    prog.optimize();
+    const double budget = config.device.memory_budget_bytes ? static_cast<double>(config.device.memory_budget_bytes)
+                                                             : 179.0 * 1024 * 1024 * 1024;
+    prog.optimize(budget);
     if (totals) *totals = prog.totals();
     std::string head = "terms=" + std::to_string(plan.rgs.size()) + " shared_hits=" + std::to_string(stats.shared_hits) +
                        " ref_madds=" + std::to_string(stats.ref_madds) + "\n";

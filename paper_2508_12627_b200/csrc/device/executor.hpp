@@ -192,7 +192,8 @@ class Program {
     double cost_since(const Mark& m) const;
 
     void keep(int buf) { keep_[buf] = true; }  // a result the caller takes after execute()
-    void optimize();  // epilogue fusion, symmetric tiles, dead ops, last uses
+    void optimize(double budget_bytes = 0);  // fusion, memory-bounded schedule, last uses
+    double scheduled_peak_bytes() const { return sched_peak_; }
     void execute();   // launches every live op in order
     Buf take(int buf);  // result buffer (allocated during execute)
 
@@ -216,7 +217,8 @@ class Program {
     std::vector<std::string> memo_log_;
     std::map<int, bool> keep_;
     std::vector<std::size_t> schedule_;  // execution order of live ops (memory-aware)
-    void make_schedule();
+    double sched_peak_ = 0;
+    void make_schedule(double budget_bytes);
 };
 
 // Records one notation into a Program with the reference's elimination walk.
