@@ -50,6 +50,8 @@ Runtime::Runtime(int device) : device_(device) {
     check_cuda(cudaSetDevice(device), "cudaSetDevice");
     check_cuda(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, device), "cudaDeviceGetAttribute");
     check_cuda(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    check_cuda(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "cudaStreamCreate");
+    cur_ = stream_;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
         std::uint64_t keep = ~std::uint64_t{0};
@@ -66,7 +68,7 @@ Buf Runtime::allocate(int order, long long n) {
     b->rt = this;
     void* p = nullptr;
     const std::size_t bytes = std::max<std::uint64_t>(b->entries(), 1) * sizeof(double);
-    const cudaError_t e = cudaMallocAsync(&p, bytes, stream_);
+    const cudaError_t e = cudaMallocAsync(&p, bytes, cur_);
     if (e != cudaSuccess || std::getenv("USTATS_SCHED_DEBUG")) {
         std::size_t fr = 0, tot = 0;
         cudaMemGetInfo(&fr, &tot);
@@ -91,15 +93,18 @@ Buf Runtime::borrow(const double* ptr, int order, long long n) {
 
 double* Runtime::scratch(std::size_t entries) {
     void* p = nullptr;
-    check_cuda(cudaMallocAsync(&p, std::max<std::size_t>(entries, 1) * sizeof(double), stream_), "cudaMallocAsync");
+    check_cuda(cudaMallocAsync(&p, std::max<std::size_t>(entries, 1) * sizeof(double), cur_), "cudaMallocAsync");
     return static_cast<double*>(p);
 }
 
 void Runtime::release(double* p) {
-    if (p) cudaFreeAsync(p, stream_);
+    if (p) cudaFreeAsync(p, cur_);
 }
 
-void Runtime::sync() { check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize"); }
+void Runtime::sync() {
+    check_cuda(cudaStreamSynchronize(side_), "cudaStreamSynchronize");
+    check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
+}
 
 void Runtime::begin(Kind k) {
     if (!profiling_) return;
@@ -112,13 +117,13 @@ void Runtime::begin(Kind k) {
     pool_.pop_back();
     m.b = pool_.back();
     pool_.pop_back();
-    cudaEventRecord(m.a, stream_);
+    cudaEventRecord(m.a, cur_);
     marks_.push_back(m);
 }
 
 void Runtime::end(Kind) {
     if (!profiling_ || marks_.empty()) return;
-    cudaEventRecord(marks_.back().b, stream_);
+    cudaEventRecord(marks_.back().b, cur_);
 }
 
 Runtime::Profile Runtime::collect(bool reset) {
@@ -680,6 +685,7 @@ void Program::make_schedule(double budget) {
 }
 
 void Program::optimize(double budget_bytes) {
+    budget_ = budget_bytes;
     if (config_.device.fuse_epilogues) fuse_epilogues();
     make_schedule(budget_bytes);
     for (SymBuf& b : bufs_) b.last_use = -1;
@@ -894,17 +900,69 @@ void Program::launch(Op& op) {
     else run_stream(op, out);
 }
 
+// Launches the schedule. GEMMs and ops that allocate order>=2 tensors stay
+// on the main stream in schedule order (the memory bound assumes that);
+// reductions to vectors / scalars go to a side stream so they fill the SMs a
+// GEMM's last wave leaves idle. Cross-stream reads wait on the producer's
+// event; a buffer is freed on the stream of its last reader after the other
+// stream's readers are done.
 void Program::execute() {
+    bool has_gemm = false;
+    for (std::size_t i : schedule_) has_gemm |= ops_[i].gemm;
+    const bool multi =
+        has_gemm && !config_.device.serial_launch && (budget_ <= 0 || sched_peak_ <= 0.7 * budget_);
+    // only reductions over at most an n^2 space go to the side stream: heavier
+    // bandwidth ops running under a GEMM steal its SMs mid-wave (C4: -3%)
+    auto side_ok = [&](const Op& op) {
+        if (op.gemm || (!op.ext && bufs_[static_cast<std::size_t>(op.out)].order >= 2)) return false;
+        const int dims = static_cast<int>(op.out_ids.size()) + std::popcount(op.sum);
+        return dims <= 2;
+    };
+    cudaStream_t streams[2] = {rt_->main_stream(), rt_->side_stream()};
+    const std::size_t N = ops_.size();
+    std::vector<cudaEvent_t> done(N, nullptr);
+    std::vector<int> on(N, 0), producer(bufs_.size(), -1);
+    std::vector<std::array<int, 2>> readers(bufs_.size(), {-1, -1});
     for (std::size_t pos = 0; pos < schedule_.size(); ++pos) {
-        Op& op = ops_[schedule_[pos]];
+        const std::size_t i = schedule_[pos];
+        Op& op = ops_[i];
+        const int si = (multi && side_ok(op)) ? 1 : 0;
+        on[i] = si;
+        cudaStream_t s = streams[si];
+        if (multi)
+            for_each_read(op, [&](const View& v) {
+                const int p = producer[static_cast<std::size_t>(v.buf)];
+                if (p >= 0 && on[static_cast<std::size_t>(p)] != si) check_cuda(cudaStreamWaitEvent(s, done[static_cast<std::size_t>(p)], 0), "wait");
+            });
+        rt_->set_stream(s);
         launch(op);
+        if (!op.ext && op.out >= 0) producer[static_cast<std::size_t>(op.out)] = static_cast<int>(i);
+        for (const Op::Epi& e : op.epis)
+            if (!e.ext && e.out >= 0) producer[static_cast<std::size_t>(e.out)] = static_cast<int>(i);
+        if (multi) {
+            check_cuda(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming), "cudaEventCreate");
+            check_cuda(cudaEventRecord(done[i], s), "cudaEventRecord");
+        }
+        for_each_read(op, [&](const View& v) { readers[static_cast<std::size_t>(v.buf)][si] = static_cast<int>(i); });
         for_each_read(op, [&](const View& v) {
             SymBuf& b = bufs_[static_cast<std::size_t>(v.buf)];
-            if (!b.input && b.last_use == static_cast<int>(pos) && b.real && b.real.use_count() == 1 &&
-                !keep_.count(v.buf))
-                b.real.reset();
+            if (b.input || b.last_use != static_cast<int>(pos) || !b.real || b.real.use_count() != 1 || keep_.count(v.buf))
+                return;
+            const int other = readers[static_cast<std::size_t>(v.buf)][1 - si];
+            if (multi && other >= 0) check_cuda(cudaStreamWaitEvent(s, done[static_cast<std::size_t>(other)], 0), "wait");
+            b.real.reset();
         });
     }
+    if (multi) {
+        cudaEvent_t side_done;
+        check_cuda(cudaEventCreateWithFlags(&side_done, cudaEventDisableTiming), "cudaEventCreate");
+        check_cuda(cudaEventRecord(side_done, streams[1]), "cudaEventRecord");
+        check_cuda(cudaStreamWaitEvent(streams[0], side_done, 0), "wait");
+        cudaEventDestroy(side_done);
+        for (cudaEvent_t e : done)
+            if (e) cudaEventDestroy(e);
+    }
+    rt_->set_stream(streams[0]);
 }
 
 Buf Program::take(int buf) { return bufs_[static_cast<std::size_t>(buf)].real; }

@@ -61,7 +61,10 @@ class Runtime {
     static Runtime& get(int device);
     ~Runtime();
 
-    cudaStream_t stream() const { return stream_; }
+    cudaStream_t stream() const { return cur_; }  // where allocations / launches go now
+    cudaStream_t main_stream() const { return stream_; }
+    cudaStream_t side_stream() const { return side_; }
+    void set_stream(cudaStream_t s) { cur_ = s; }
     int device() const { return device_; }
     int sm_count() const { return sm_count_; }
 
@@ -86,6 +89,8 @@ class Runtime {
     int device_ = 0;
     int sm_count_ = 148;
     cudaStream_t stream_ = nullptr;
+    cudaStream_t side_ = nullptr;  // second stream: bandwidth ops overlap GEMM tails
+    cudaStream_t cur_ = nullptr;
     bool profiling_ = false;
     std::vector<cudaEvent_t> pool_;
     struct Mark {
@@ -218,6 +223,7 @@ class Program {
     std::map<int, bool> keep_;
     std::vector<std::size_t> schedule_;  // execution order of live ops (memory-aware)
     double sched_peak_ = 0;
+    double budget_ = 0;
     void make_schedule(double budget_bytes);
 };
 

@@ -19,6 +19,7 @@ struct DeviceConfig {
     bool exploit_symmetry = true;      ///< detect bitwise-symmetric matrices, read either orientation
     bool reorder_for_sharing = true;   ///< choose among equal-width orders to maximize sharing
     bool donate_inputs = false;        ///< device inputs may be sparsified in place (no copy)
+    bool serial_launch = false;        ///< one stream only (no GEMM/reduction overlap)
     /// Device-memory budget for inputs + live intermediates of one statistic's
     /// program (0 = free device memory at execution; plan-only: 179 GiB).
     std::uint64_t memory_budget_bytes = 0;
