@@ -51,7 +51,7 @@ def measured_peaks() -> dict:
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
@@ -75,7 +75,18 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 8:
+                parts.append(time.time())
                 self.rows.append(parts)
+
+    def wait_ready(self, timeout: float = 5.0):
+        """nvidia-smi's start-up (NVML init) perturbs the GPU: start the sampler
+        before the warm-up and wait for its first sample."""
+        t0 = time.time()
+        while self.proc and not self.rows and time.time() - t0 < timeout:
+            time.sleep(0.05)
+
+    def mark(self, start: float, end: float):
+        self.window = (start, end)
 
     def __exit__(self, *exc):
         if self.proc:
@@ -86,14 +97,19 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self) -> dict:
-        if not self.rows:
+        rows = self.rows
+        win = getattr(self, "window", None)
+        if win:
+            inside = [r for r in rows if win[0] - 0.25 <= r[-1] <= win[1] + 0.25]
+            rows = inside or rows[-2:]  # short regions: the samples bracketing them
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if str(r[4 + i]).lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows)}
 
 
 def dist_env():
@@ -198,8 +214,8 @@ def reference_madds(name, n):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--n", type=int, default=0, help="override the config's n (parity/debug only)")
@@ -246,30 +262,50 @@ def main():
             return us.combine_terms(r.mu, v.cpu().numpy()), r
         return r.value, r
 
+    # Inputs smaller than L2 (126 MB) would stay cached across steps: flush L2
+    # between steps (write a 512 MiB buffer) and time each step on its own.
+    flush = input_bytes(factors) < 126e6
+    scrub = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda") if flush else None
+
     def timed(fx, on_device, k):
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
         last = None
-        for _ in range(k):
-            last = step(fx, on_device)
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
+        if flush:
+            ms = 0.0
+            for _ in range(k):
+                scrub.fill_(1.0)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                last = step(fx, on_device)
+                e1.record()
+                torch.cuda.synchronize()
+                ms += e0.elapsed_time(e1)
+        else:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(k):
+                last = step(fx, on_device)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
         if world > 1:
             t = torch.tensor([ms], device="cuda")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             ms = float(t.item())
         return ms / k, last
 
-    for _ in range(args.warmup):
-        step(dfac, True)
-    us.profile(enable=True, reset=True, device=local)
     with ClockSampler(local) as clocks:
+        clocks.wait_ready()
+        for _ in range(args.warmup):
+            step(dfac, True)
+        us.profile(enable=True, reset=True, device=local)
+        t_start = time.time()
         ms_step, (u_val, r) = timed(dfac, True, args.steps)
-    prof = us.profile(enable=False, reset=True, device=local)
+        clocks.mark(t_start, time.time())
+        prof = us.profile(enable=False, reset=True, device=local)
     e2e = None
     if not args.no_e2e:
         step(hfac, False)
@@ -305,8 +341,8 @@ def main():
         "data": "synthetic (seeded, BASELINE.json construction)",
         "config": {"workload": name, "m": m, "n": n, "signature": sig, "terms": int(len(r.v)),
                    "parallelism": f"term-sharded x{world}" if world > 1 else "single GPU",
-                   "l2": "inputs larger than L2 (no flush needed)" if input_bytes(factors) > 126e6
-                   else "inputs L2-resident across steps (latency-bound config)"},
+                   "l2": "inputs larger than L2 (no flush needed)" if not flush
+                   else "L2 flushed (512 MiB write) before every timed step; steps timed individually"},
         "u": u_val,
         "roofline": roofline,
         "gpu_launches": int(st["kernel_launches"]) * args.steps,
