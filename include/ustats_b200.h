@@ -88,6 +88,15 @@ US_API int us_u_terms(int32_t m, int32_t K, const int32_t* tuple_len, const int3
                int32_t max_terms, int32_t* count, int32_t* rgs_out, int64_t* mu_out, double* v_out,
                int32_t* owner_out, double* u_out, us_stats* stats);
 
+/* Several U-statistics over factors of one extent n, evaluated as ONE device
+ * program (factors uploaded once, sub-contractions shared across statistics;
+ * e.g. hoif_tau's chain orders, hoif.cpp:74-100). Statistic s has arity m[s]
+ * and K[s] components; tuple_len / tuple_idx / factors are the per-statistic
+ * encodings concatenated in statistic order. u_out receives S values. */
+US_API int us_u_statistic_batch(int32_t S, const int32_t* m, const int32_t* K, const int32_t* tuple_len,
+                                const int32_t* tuple_idx, const double* const* factors, int64_t n,
+                                int32_t on_device, const us_config* cfg, double* u_out, us_stats* stats);
+
 /* u_statistic_unsparsified (engine.cpp:195-211): every lattice partition. */
 US_API int us_u_statistic_unsparsified(int32_t m, int32_t K, const int32_t* tuple_len,
                                 const int32_t* tuple_idx, const double* const* factors, int64_t n,

@@ -8,7 +8,8 @@ from .api import (  # noqa: F401
     Config, UStatsError, UTerms, bell_number, combine_terms, device_count, device_stream, einsum,
     profile,
     eliminate_index, kernel_tensors, optimize_order, plan_summary, plan_terms, restricted_v_tensors, survivors, treewidth,
-    u_statistic, u_statistic_tensors, u_statistic_unsparsified_tensors, u_terms, v_statistic,
+    u_statistic, u_statistic_batch, u_statistic_tensors, u_statistic_unsparsified_tensors, u_terms,
+    v_statistic, hoif_tau,
     v_statistic_tensors,
 )
 from ._native import LIB_PATH, lib  # noqa: F401

@@ -180,6 +180,58 @@ def u_terms(factors, signature, m: int | None = None, config: Config | None = No
     return UTerms(u.value, rgs[:T].copy(), mu[:T].copy(), v[:T].copy(), owner[:T].copy(), st.as_dict())
 
 
+def u_statistic_batch(problems, config: Config | None = None, with_stats: bool = False):
+    """Several U-statistics ``[(factors, signature, m), ...]`` over one extent,
+    evaluated as one device program (shared uploads and sub-contractions)."""
+    ms, Ks, lens, idx, allf = [], [], [], [], []
+    for factors, sig, m in problems:
+        ms.append(int(m))
+        Ks.append(len(sig))
+        for t in sig:
+            lens.append(len(t))
+            idx.extend(int(s) for s in t)
+        allf.extend(factors)
+    fx = _Factors(allf)
+    S = len(ms)
+    out = (N.f64 * S)()
+    st = N.UsStats()
+    cfg = _cfg(config)
+    _check(N.lib().us_u_statistic_batch(S, (N.i32 * S)(*ms), (N.i32 * S)(*Ks), (N.i32 * len(lens))(*lens),
+                                        (N.i32 * max(len(idx), 1))(*idx), fx.ptrs, fx.n, fx.on_device,
+                                        C.byref(cfg), out, C.byref(st)))
+    vals = [out[i] for i in range(S)]
+    return (vals, st.as_dict()) if with_stats else vals
+
+
+def hoif_tau(m: int, k: int, data, config: Config | None = None) -> float:
+    """hoif_tau (hoif.cpp:74-100): sum_{j=2..m} (-1)^j sum_{l=0..j-2} C(j-2,l)
+    (n-l)!/n! U(hoif:l+2:k), with every chain order evaluated in ONE program
+    (the reference makes m-1 separate u_statistic calls)."""
+    from math import comb
+    x = np.asarray(data, dtype=np.float64)
+    n = x.shape[0]
+    if m < 2:
+        raise UStatsError("InvalidArgument", "statistic order must be >= 2")
+    if n < m:
+        raise UStatsError("SampleTooSmall", f"need at least {m} observations, have {n}")
+    factors, _, _ = kernel_tensors(f"hoif:{m}:{k}", x)
+    middle, last = (factors[0] if m > 2 else None), factors[-1]
+    problems = []
+    for order in range(2, m + 1):
+        fs = [middle] * (order - 2) + [last]
+        problems.append((fs, [[i, i + 1] for i in range(order - 1)], order))
+    u = dict(zip(range(2, m + 1), u_statistic_batch(problems, config)))
+    tau = 0.0
+    for j in range(2, m + 1):
+        sign = 1.0 if j % 2 == 0 else -1.0
+        for l in range(j - 1):
+            w = 1.0
+            for i in range(l):
+                w /= (n - i)
+            tau += sign * comb(j - 2, l) * w * u[l + 2]
+    return tau
+
+
 def u_statistic_unsparsified_tensors(factors, signature, m: int | None = None, config: Config | None = None):
     m = m if m is not None else 1 + max(s for t in signature for s in t)
     K, L, I = _signature(signature)

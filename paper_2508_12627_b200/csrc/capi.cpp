@@ -208,6 +208,36 @@ int us_u_terms(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tu
     });
 }
 
+int us_u_statistic_batch(int32_t S, const int32_t* m, const int32_t* K, const int32_t* tuple_len,
+                         const int32_t* tuple_idx, const double* const* factors, int64_t n, int32_t on_device,
+                         const us_config* cfg, double* u_out, us_stats* stats) {
+    return guarded([&] {
+        ustats::Config config = to_config(cfg);
+        if (S < 1) ustats::fail(ustats::ErrorCode::InvalidArgument, "need at least one statistic");
+        if (n < 1) ustats::fail(ustats::ErrorCode::InvalidArgument, "sample is empty");
+        std::vector<ustats::dev::StatisticSpec> specs;
+        int comp = 0, idx = 0;
+        for (int s = 0; s < S; ++s) {
+            ustats::dev::StatisticSpec sp;
+            sp.m = m[s];
+            for (int k = 0; k < K[s]; ++k) {
+                sp.sig.emplace_back(tuple_idx + idx, tuple_idx + idx + tuple_len[comp]);
+                idx += tuple_len[comp];
+                sp.inputs.push_back(factors[comp]);
+                ++comp;
+            }
+            validate_signature(sp.m, sp.sig);
+            if (n < sp.m)
+                ustats::fail(ustats::ErrorCode::SampleTooSmall,
+                             "need at least " + std::to_string(sp.m) + " observations, have " + std::to_string(n));
+            specs.push_back(std::move(sp));
+        }
+        auto res = ustats::dev::lattice_batch(specs, on_device != 0, n, ustats::dev::LatticeMode::Sparsified, config);
+        for (int s = 0; s < S; ++s) u_out[s] = res[static_cast<std::size_t>(s)].value;
+        if (stats) export_dev(res[0], cfg ? cfg->rank : 0, stats);
+    });
+}
+
 int us_u_statistic_unsparsified(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
                                 const double* const* factors, int64_t n, int32_t on_device,
                                 const us_config* cfg, double* u_out, us_stats* stats) {

@@ -1335,49 +1335,56 @@ void record_terms(Program& prog, const TermPlan& plan, const std::vector<int>& i
     }
 }
 
-StatisticResult lattice_statistic(const std::vector<const double*>& inputs, bool inputs_on_device,
-                                  const std::vector<IndexTuple>& zero_sig, int m, long long n, LatticeMode mode,
-                                  const Config& config) {
-    StatisticResult res;
+std::vector<StatisticResult> lattice_batch(const std::vector<StatisticSpec>& specs, bool inputs_on_device,
+                                           long long n, LatticeMode mode, const Config& config) {
+    std::vector<StatisticResult> out(specs.size());
     Runtime& rt = Runtime::get(config.device.device);
     const auto t_up = Clock::now();
 
+    // Upload each distinct factor of every statistic once; sparsify on device
+    // (tensor.cpp:54-76) and probe matrices for bitwise symmetry.
     std::map<const double*, Buf> by_ptr;
-    std::vector<Buf> tensors;
+    std::vector<std::vector<Buf>> tensors(specs.size());
     std::vector<std::pair<Buf, int*>> probes;
+    std::size_t total_factors = 0;
+    for (const auto& sp : specs) total_factors += sp.sig.size();
     int* flags = nullptr;
+    DevStats upload_stats;
     if (config.device.exploit_symmetry)
-        check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&flags), sizeof(int) * zero_sig.size() + 4, rt.stream()),
+        check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&flags), sizeof(int) * total_factors + 4, rt.stream()),
                    "alloc flags");
-    for (std::size_t k = 0; k < zero_sig.size(); ++k) {
-        const int order = static_cast<int>(zero_sig[k].size());
-        checked_entry_count(order, static_cast<int>(n), config);
-        auto hit = by_ptr.find(inputs[k]);
-        if (hit != by_ptr.end() && hit->second->order == order) {
-            tensors.push_back(hit->second);
-            continue;
+    for (std::size_t q = 0; q < specs.size(); ++q) {
+        const StatisticSpec& sp = specs[q];
+        for (std::size_t k = 0; k < sp.sig.size(); ++k) {
+            const int order = static_cast<int>(sp.sig[k].size());
+            checked_entry_count(order, static_cast<int>(n), config);
+            auto hit = by_ptr.find(sp.inputs[k]);
+            if (hit != by_ptr.end() && hit->second->order == order) {
+                tensors[q].push_back(hit->second);
+                continue;
+            }
+            Buf b;
+            if (inputs_on_device && config.device.donate_inputs) {
+                b = rt.borrow(sp.inputs[k], order, n);  // sparsified in place: the caller donated it
+            } else {
+                b = rt.allocate(order, n);
+                check_cuda(cudaMemcpyAsync(b->ptr, sp.inputs[k], b->entries() * sizeof(double),
+                                           inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                           rt.stream()),
+                           "upload");
+            }
+            rt.begin(Runtime::kOther);
+            if (mode == LatticeMode::Sparsified)
+                upload_stats.kernel_launches += static_cast<std::uint64_t>(launch_sparsify(b->ptr, order, n, rt.stream()));
+            if (flags && order == 2) {
+                int* f = flags + probes.size();
+                upload_stats.kernel_launches += static_cast<std::uint64_t>(launch_symmetry_check(b->ptr, n, f, rt.stream()));
+                probes.emplace_back(b, f);
+            }
+            rt.end(Runtime::kOther);
+            by_ptr[sp.inputs[k]] = b;
+            tensors[q].push_back(b);
         }
-        Buf b;
-        if (inputs_on_device && config.device.donate_inputs) {
-            b = rt.borrow(inputs[k], order, n);  // sparsified in place: the caller donated it
-        } else {
-            b = rt.allocate(order, n);
-            check_cuda(cudaMemcpyAsync(b->ptr, inputs[k], b->entries() * sizeof(double),
-                                       inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                                       rt.stream()),
-                       "upload");
-        }
-        rt.begin(Runtime::kOther);
-        if (mode == LatticeMode::Sparsified)
-            res.stats.kernel_launches += static_cast<std::uint64_t>(launch_sparsify(b->ptr, order, n, rt.stream()));
-        if (flags && order == 2) {
-            int* f = flags + probes.size();
-            res.stats.kernel_launches += static_cast<std::uint64_t>(launch_symmetry_check(b->ptr, n, f, rt.stream()));
-            probes.emplace_back(b, f);
-        }
-        rt.end(Runtime::kOther);
-        by_ptr[inputs[k]] = b;
-        tensors.push_back(b);
     }
     if (!probes.empty()) {
         std::vector<int> host(probes.size());
@@ -1388,50 +1395,86 @@ StatisticResult lattice_statistic(const std::vector<const double*>& inputs, bool
     }
     if (flags) cudaFreeAsync(flags, rt.stream());
     rt.sync();
-    res.upload_seconds = std::chrono::duration<double>(Clock::now() - t_up).count();
+    const double upload_s = std::chrono::duration<double>(Clock::now() - t_up).count();
 
     const auto t0 = Clock::now();
-    TermPlan plan = plan_terms(zero_sig, m, n, mode, config);
-    const std::size_t T = plan.rgs.size();
-    res.enumerated = plan.enumerated;
-    res.owner = plan.owner;
-
+    std::vector<TermPlan> plans;
+    std::size_t T = 0;
+    for (const auto& sp : specs) {
+        plans.push_back(plan_terms(sp.sig, sp.m, n, mode, config));
+        T += plans.back().rgs.size();
+    }
     double* d_v = rt.scratch(std::max<std::size_t>(T, 1));
     check_cuda(cudaMemsetAsync(d_v, 0, sizeof(double) * std::max<std::size_t>(T, 1), rt.stream()), "memset");
+    DevStats shared;  // one program for every statistic: sub-contractions shared across them
+    double plan_s = 0;
     {
-        Program prog(&rt, n, config, &res.stats);
-        std::vector<int> ids;
-        for (const Buf& b : tensors) ids.push_back(prog.add_input(b));
-        record_terms(prog, plan, ids, config.device.rank, d_v, &res.stats);
+        Program prog(&rt, n, config, &shared);
+        std::size_t at = 0;
+        for (std::size_t q = 0; q < specs.size(); ++q) {
+            std::vector<int> ids;
+            for (const Buf& b : tensors[q]) ids.push_back(prog.add_input(b));
+            record_terms(prog, plans[q], ids, config.device.rank, d_v + at, &out[q].stats);
+            at += plans[q].rgs.size();
+        }
         double budget = static_cast<double>(config.device.memory_budget_bytes);
         if (budget <= 0) {
             std::size_t free_b = 0, total_b = 0;
             check_cuda(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-            double inputs = 0;
-            for (const auto& kv : by_ptr) inputs += 8.0 * static_cast<double>(kv.second->entries());
+            double in_bytes = 0;
+            for (const auto& kv : by_ptr) in_bytes += 8.0 * static_cast<double>(kv.second->entries());
             // inputs are already resident: the program may use what is free, minus headroom
-            budget = inputs + 0.94 * static_cast<double>(free_b) - 2.0e9;
+            budget = in_bytes + 0.94 * static_cast<double>(free_b) - 2.0e9;
         }
         prog.optimize(budget);
-        res.plan_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+        plan_s = std::chrono::duration<double>(Clock::now() - t0).count();
         prog.execute();
     }
-    res.v.assign(T, 0.0);
-    if (T)
-        check_cuda(cudaMemcpyAsync(res.v.data(), d_v, sizeof(double) * T, cudaMemcpyDeviceToHost, rt.stream()), "D2H");
+    std::vector<double> v(T, 0.0);
+    if (T) check_cuda(cudaMemcpyAsync(v.data(), d_v, sizeof(double) * T, cudaMemcpyDeviceToHost, rt.stream()), "D2H");
     rt.release(d_v);
     tensors.clear();
     by_ptr.clear();
     probes.clear();
     rt.sync();
-    res.contract_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+    const double contract_s = std::chrono::duration<double>(Clock::now() - t0).count();
 
-    res.terms.resize(T);
-    res.mu = plan.mu;
-    res.rgs = plan.rgs;
-    for (std::size_t t = 0; t < T; ++t) res.terms[t] = static_cast<double>(res.mu[t]) * res.v[t];
-    res.value = combine_terms(res.terms);
-    return res;
+    std::size_t at = 0;
+    for (std::size_t q = 0; q < specs.size(); ++q) {
+        StatisticResult& res = out[q];
+        const TermPlan& plan = plans[q];
+        const std::size_t Tq = plan.rgs.size();
+        res.enumerated = plan.enumerated;
+        res.owner = plan.owner;
+        res.mu = plan.mu;
+        res.rgs = plan.rgs;
+        res.v.assign(v.begin() + static_cast<std::ptrdiff_t>(at), v.begin() + static_cast<std::ptrdiff_t>(at + Tq));
+        res.terms.resize(Tq);
+        for (std::size_t t = 0; t < Tq; ++t) res.terms[t] = static_cast<double>(res.mu[t]) * res.v[t];
+        res.value = combine_terms(res.terms);
+        at += Tq;
+        // device work of the shared program is reported once, on the first statistic
+        if (q == 0) {
+            res.stats.gemm_macs = shared.gemm_macs;
+            res.stats.stream_entries = shared.stream_entries;
+            res.stats.gemm_launches = shared.gemm_launches;
+            res.stats.stream_launches = shared.stream_launches;
+            res.stats.shared_hits = shared.shared_hits;
+            res.stats.kernel_launches = shared.kernel_launches + upload_stats.kernel_launches;
+            res.stats.fused_epilogues = shared.fused_epilogues;
+            res.stats.symmetric_gemms = shared.symmetric_gemms;
+        }
+        res.upload_seconds = upload_s;
+        res.contract_seconds = contract_s;
+        res.plan_seconds = plan_s;
+    }
+    return out;
+}
+
+StatisticResult lattice_statistic(const std::vector<const double*>& inputs, bool inputs_on_device,
+                                  const std::vector<IndexTuple>& zero_sig, int m, long long n, LatticeMode mode,
+                                  const Config& config) {
+    return lattice_batch({StatisticSpec{inputs, zero_sig, m}}, inputs_on_device, n, mode, config)[0];
 }
 
 namespace {

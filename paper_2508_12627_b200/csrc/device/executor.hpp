@@ -291,6 +291,17 @@ struct TermPlan {
 TermPlan plan_terms(const std::vector<IndexTuple>& zero_sig, int m, long long n, LatticeMode mode,
                     const Config& config);
 
+// Several U-statistics over factors of one extent in ONE program: aliased
+// factor pointers are uploaded once and sub-contractions are shared across
+// the statistics (e.g. hoif_tau's chain orders 2..m, hoif.cpp:84-86).
+struct StatisticSpec {
+    std::vector<const double*> inputs;
+    std::vector<IndexTuple> sig;
+    int m = 0;
+};
+std::vector<StatisticResult> lattice_batch(const std::vector<StatisticSpec>& specs, bool inputs_on_device,
+                                           long long n, LatticeMode mode, const Config& config);
+
 StatisticResult lattice_statistic(const std::vector<const double*>& inputs, bool inputs_on_device,
                                   const std::vector<IndexTuple>& zero_sig, int m, long long n,
                                   LatticeMode mode, const Config& config);

@@ -210,3 +210,36 @@ def test_device_resident_inputs(engine):
         dfac.append(dev[id(f)])
     got = engine.u_statistic_tensors(dfac, sig, m)
     assert got == host
+
+
+def test_batch_equals_individual(engine):
+    from paper_2508_12627_b200.workloads import generate
+    probs = []
+    for name, n in (("C3", 160),):
+        factors, sig, m, _ = generate(name, n)
+        probs.append((factors, sig, m))
+        # the same chain without its end vector, sharing the matrix object
+        probs.append((factors[1:-1], [[i, i + 1] for i in range(m - 2)], m - 1))
+    vals = engine.u_statistic_batch(probs)
+    for (f, s, m), v in zip(probs, vals):
+        want = engine.u_statistic_tensors(f, s, m)
+        u_ref, rows = O.u_statistic(f, s, m)
+        scale = max(abs(r[2]) for r in rows)
+        assert abs(v - want) <= TOL * scale and abs(v - u_ref) <= TOL * scale
+
+
+def test_hoif_tau_closed_forms(engine):
+    # test_kernels.cpp:109-123: tau telescopes to closed forms in U_2..U_4
+    rng = np.random.default_rng(44)
+    n = 9
+    data = rng.normal(size=(n, 4))
+    u = {j: engine.u_statistic(f"hoif:{j}:2", data) for j in (2, 3, 4)}
+    for j in (2, 3, 4):
+        f, s, m = engine.kernel_tensors(f"hoif:{j}:2", data)
+        assert abs(u[j] - O.u_brute_force(f, s, m)) <= 1e-11 * max(1, abs(u[j]))
+    assert engine.hoif_tau(2, 2, data) == pytest.approx(u[2], rel=1e-12)
+    assert engine.hoif_tau(3, 2, data) == pytest.approx(-u[3] / n, rel=1e-12)
+    assert engine.hoif_tau(4, 2, data) == pytest.approx(u[2] + u[3] / n + u[4] / (n * (n - 1)), rel=1e-12)
+    with pytest.raises(engine.UStatsError) as e:
+        engine.hoif_tau(5, 1, rng.normal(size=(4, 3)))
+    assert e.value.code == "SampleTooSmall"
