@@ -221,6 +221,8 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override the config's n (parity/debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shard", default="rows", choices=["rows", "terms"],
+                    help="N>1: row-shard every op (NCCL inside the engine) or shard V-terms")
     args = ap.parse_args()
     world, rank, local = dist_env()
     name = args.config
@@ -236,10 +238,13 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.shard == "rows":
+            from paper_2508_12627_b200.distributed import init_row_sharding
+            init_row_sharding(local)
     w = CONFIGS[name]
     n = args.n or w.n
     factors, sig, m, _ = generate(name, n)
-    cfg = us.Config(device=local, rank=rank, world_size=world,
+    cfg = us.Config(device=local, rank=rank, world_size=world, shard_rows=(world > 1 and args.shard == "rows"),
                     memory_cap_entries=max(2 ** 31, n * n + 1, n ** 3 + 1 if name == "C4" else 0))
 
     # device-resident and pinned-host copies (aliases preserved)
@@ -255,7 +260,7 @@ def main():
 
     def step(fx, on_device):
         r = us.u_terms(fx, sig, m, cfg) if on_device else _host_terms(us, fx, sig, m, cfg)
-        if world > 1:
+        if world > 1 and not cfg.shard_rows:  # term sharding: one all-reduce of the V vector
             import torch.distributed as dist
             v = torch.from_numpy(r.v).cuda()
             dist.all_reduce(v)
@@ -340,7 +345,8 @@ def main():
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json construction)",
         "config": {"workload": name, "m": m, "n": n, "signature": sig, "terms": int(len(r.v)),
-                   "parallelism": f"term-sharded x{world}" if world > 1 else "single GPU",
+                   "parallelism": (f"row-sharded x{world}" if args.shard == "rows" else f"term-sharded x{world}")
+                   if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (no flush needed)" if not flush
                    else "L2 flushed (512 MiB write) before every timed step; steps timed individually"},
         "u": u_val,

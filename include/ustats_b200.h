@@ -47,8 +47,10 @@ typedef struct us_config {
     int32_t rank;                /* term-sharding rank */
     int32_t world_size;          /* term-sharding world size (1 = all terms here) */
     int32_t flags;               /* bit0 share, bit1 fuse epilogues, bit2 symmetry, bit3 reorder,
-                                    bit4 donate device inputs (sparsified in place, no copy);
-                                    US_FLAGS_DEFAULT = 0xF */
+                                    bit4 donate device inputs (sparsified in place, no copy),
+                                    bit5 row sharding across ranks (else V-term sharding),
+                                    bit6 serial launch (one stream); US_FLAGS_DEFAULT = 0xF */
+    int32_t emulate_world;       /* row sharding over this many virtual ranks on one device (tests) */
 } us_config;
 
 #define US_FLAGS_DEFAULT 0xF
@@ -163,6 +165,12 @@ US_API int us_plan_terms(int32_t m, int32_t K, const int32_t* tuple_len, const i
 US_API int us_plan_summary(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
                            int64_t n, const us_config* cfg, int32_t inputs_symmetric, char* text,
                            uint64_t cap, uint64_t* totals);
+
+/* Multi-GPU row sharding: rank 0 creates an NCCL unique id (128 bytes),
+ * the caller broadcasts it (e.g. torch.distributed), every rank calls
+ * us_nccl_init; then us_u_* with flags bit5 and cfg->rank/world_size. */
+US_API int us_nccl_unique_id(void* id_out);
+US_API int us_nccl_init(int32_t device, int32_t rank, int32_t world_size, const void* id);
 
 /* Device plumbing. */
 US_API int us_device_count(int32_t* count);

@@ -26,6 +26,7 @@ class UsConfig(C.Structure):
         ("rank", i32),
         ("world_size", i32),
         ("flags", i32),
+        ("emulate_world", i32),
     ]
 
 
@@ -76,6 +77,8 @@ SIGNATURES = {
     "us_treewidth": (C.c_int, [i32, i32, P(i32), P(i32), P(i32)]),
     "us_plan_terms": (C.c_int, [i32, i32, P(i32), P(i32), i64, i32, i32, P(i32), P(i32), P(f64)]),
     "us_plan_summary": (C.c_int, [i32, i32, P(i32), P(i32), i64, P(UsConfig), i32, C.c_char_p, u64, P(u64)]),
+    "us_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "us_nccl_init": (C.c_int, [i32, i32, i32, C.c_void_p]),
     "us_device_count": (C.c_int, [P(i32)]),
     "us_device_synchronize": (C.c_int, [i32]),
     "us_device_stream": (C.c_int, [i32, P(C.c_void_p)]),

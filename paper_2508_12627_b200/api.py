@@ -56,6 +56,9 @@ class Config:
     symmetry: bool = True
     reorder: bool = True
     donate_inputs: bool = False  # device inputs sparsified in place (saves one copy)
+    shard_rows: bool = False     # multi-GPU: row-shard every op (else V-term sharding)
+    serial_launch: bool = False  # one CUDA stream (no GEMM / reduction overlap)
+    emulate_world: int = 0       # row sharding over virtual ranks on one device (tests)
 
     def native(self) -> N.UsConfig:
         c = N.UsConfig()
@@ -71,7 +74,9 @@ class Config:
         c.rank = self.rank
         c.world_size = self.world_size
         c.flags = (1 if self.share else 0) | (2 if self.fuse_epilogues else 0) | \
-                  (4 if self.symmetry else 0) | (8 if self.reorder else 0) | (16 if self.donate_inputs else 0)
+                  (4 if self.symmetry else 0) | (8 if self.reorder else 0) | (16 if self.donate_inputs else 0) | \
+                  (32 if self.shard_rows else 0) | (64 if self.serial_launch else 0)
+        c.emulate_world = self.emulate_world
         return c
 
 
@@ -458,6 +463,18 @@ def profile(enable: bool = True, reset: bool = True, device: int = -1) -> dict:
     _check(N.lib().us_profile(device, 1 if enable else 0, 1 if reset else 0, ms, groups))
     return {"gemm_ms": ms[0], "stream_ms": ms[1], "other_ms": ms[2],
             "gemm_groups": groups[0], "stream_groups": groups[1], "other_groups": groups[2]}
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(N.lib().us_nccl_unique_id(buf))
+    return buf.raw
+
+
+def nccl_init(device: int, rank: int, world_size: int, uid: bytes) -> None:
+    """Creates the engine's NCCL communicator for row sharding on `device`."""
+    buf = C.create_string_buffer(bytes(uid), 128)
+    _check(N.lib().us_nccl_init(device, rank, world_size, buf))
 
 
 def device_count() -> int:

@@ -59,6 +59,9 @@ ustats::Config to_config(const us_config* c) {
     cfg.device.exploit_symmetry = c->flags & 4;
     cfg.device.reorder_for_sharing = c->flags & 8;
     cfg.device.donate_inputs = c->flags & 16;
+    cfg.device.shard_rows = c->flags & 32;
+    cfg.device.serial_launch = c->flags & 64;
+    cfg.device.emulate_world = c->emulate_world;
     return cfg;
 }
 
@@ -456,6 +459,14 @@ int us_plan_summary(int32_t m, int32_t K, const int32_t* tuple_len, const int32_
             totals[6] = t.peak_entries;
         }
     });
+}
+
+int us_nccl_unique_id(void* id_out) {
+    return guarded([&] { ustats::dev::Runtime::nccl_unique_id(id_out); });
+}
+
+int us_nccl_init(int32_t device, int32_t rank, int32_t world_size, const void* id) {
+    return guarded([&] { ustats::dev::Runtime::get(device).nccl_init(rank, world_size, id); });
 }
 
 int us_device_count(int32_t* count) {

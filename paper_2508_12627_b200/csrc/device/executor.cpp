@@ -1,6 +1,8 @@
 // Device executor (see executor.hpp).
 #include "executor.hpp"
 
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <bit>
 #include <chrono>
@@ -104,6 +106,60 @@ void Runtime::release(double* p) {
 void Runtime::sync() {
     check_cuda(cudaStreamSynchronize(side_), "cudaStreamSynchronize");
     check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
+}
+
+// ------------------------------------------------------------------- NCCL
+namespace {
+struct NcclApi {
+    using GetId = int (*)(void*);
+    using Init = int (*)(void**, int, std::array<char, 128>, int);
+    using AllReduce = int (*)(const void*, void*, std::size_t, int, int, void*, cudaStream_t);
+    using ErrStr = const char* (*)(int);
+    GetId get_id = nullptr;
+    Init init = nullptr;
+    AllReduce all_reduce = nullptr;
+    ErrStr err = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // the process's copy (torch) if loaded
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+        if (!h) return;
+        api.get_id = reinterpret_cast<NcclApi::GetId>(dlsym(h, "ncclGetUniqueId"));
+        api.init = reinterpret_cast<NcclApi::Init>(dlsym(h, "ncclCommInitRank"));
+        api.all_reduce = reinterpret_cast<NcclApi::AllReduce>(dlsym(h, "ncclAllReduce"));
+        api.err = reinterpret_cast<NcclApi::ErrStr>(dlsym(h, "ncclGetErrorString"));
+    });
+    if (!api.get_id || !api.init || !api.all_reduce) fail(ErrorCode::CollectiveError, "libnccl.so.2 not available");
+    return api;
+}
+
+void nccl_check(int r, const char* what) {
+    if (r != 0)
+        fail(ErrorCode::CollectiveError,
+             std::string(what) + ": " + (nccl().err ? nccl().err(r) : ("nccl error " + std::to_string(r)).c_str()));
+}
+}  // namespace
+
+void Runtime::nccl_unique_id(void* out128) { nccl_check(nccl().get_id(out128), "ncclGetUniqueId"); }
+
+void Runtime::nccl_init(int rank, int world, const void* unique_id) {
+    std::array<char, 128> id{};
+    std::memcpy(id.data(), unique_id, 128);
+    void* comm = nullptr;
+    check_cuda(cudaSetDevice(device_), "cudaSetDevice");
+    nccl_check(nccl().init(&comm, world, id, rank), "ncclCommInitRank");
+    comm_ = comm;
+    comm_world_ = world;
+}
+
+void Runtime::allreduce_sum(double* p, std::size_t count) {
+    if (!comm_ || comm_world_ <= 1 || count == 0) return;
+    constexpr int kNcclFloat64 = 8, kNcclSum = 0;  // nccl.h enum values
+    nccl_check(nccl().all_reduce(p, p, count, kNcclFloat64, kNcclSum, comm_, cur_), "ncclAllReduce");
 }
 
 void Runtime::begin(Kind k) {
@@ -757,6 +813,21 @@ void Program::run_stream(const Op& op, double* out) {
             a.stride[f][d] = factors[static_cast<std::size_t>(f)].stride[static_cast<std::size_t>(dims[d])];
     }
     a.out = out;
+    if (slice_world_ > 1) {
+        // row sharding: this rank covers [lo, hi) of iteration dim 0 (an output
+        // dim -> disjoint rows of the zeroed output; a summed dim -> a partial
+        // sum); every rank accumulates, the all-reduce / lockstep adds them up
+        a.accumulate = 1;
+        if (dims.empty()) {
+            if (slice_rank_ != 0) return;
+        } else {
+            const long long lo = n_ * slice_rank_ / slice_world_, hi = n_ * (slice_rank_ + 1) / slice_world_;
+            if (hi <= lo) return;
+            a.n0 = hi - lo;
+            for (int f = 0; f < a.nf; ++f) a.ptr[f] += lo * a.stride[f][0];
+            if (a.n_out >= 1) a.out += lo * static_cast<long long>(ipow(n_, a.n_out - 1));
+        }
+    }
     const std::size_t scratch_n = stream_scratch_entries(a, rt_->sm_count());
     double* scratch = scratch_n ? rt_->scratch(scratch_n) : nullptr;
     rt_->begin(Runtime::kStream);
@@ -812,7 +883,17 @@ void Program::run_gemm(const Op& op, double* out) {
     g.out = out;
     int launched = -1;
     double* scratch = nullptr;
-    if (!op.epis.empty() || (op.symmetric_out && gemm_tma_eligible(g, nullptr, nullptr))) {
+    const bool multi_path = !op.epis.empty() || (op.symmetric_out && gemm_tma_eligible(g, nullptr, nullptr));
+    if (slice_world_ > 1) {
+        // row sharding: a contiguous range of the tile list per rank
+        const bool tri = multi_path && op.symmetric_out && g.rows == g.cols;
+        const long long total = gemm_tile_total(g, tri);
+        g.tile_begin = total * slice_rank_ / slice_world_;
+        g.tile_count = total * (slice_rank_ + 1) / slice_world_ - g.tile_begin;
+        g.accumulate = 1;
+        if (g.tile_count <= 0) return;
+    }
+    if (multi_path) {
         EpiSet set;
         std::size_t part_total = 0;
         if (op.store) {
@@ -851,12 +932,19 @@ void Program::run_gemm(const Op& op, double* out) {
                 d.out = e.ext;
             } else {
                 SymBuf& b = bufs_[static_cast<std::size_t>(e.out)];
-                if (!b.real) b.real = rt_->allocate(b.order, n_);
+                if (!b.real) {
+                    b.real = rt_->allocate(b.order, n_);
+                    if (slice_world_ > 1)
+                        check_cuda(cudaMemsetAsync(b.real->ptr, 0, b.real->entries() * sizeof(double), rt_->stream()),
+                                   "memset");
+                }
                 d.out = b.real->ptr;
             }
             part_total += gemm_epi_partial_entries(g, d.mode);
         }
         scratch = part_total ? rt_->scratch(part_total) : nullptr;
+        if (scratch && slice_world_ > 1)  // tiles of other ranks leave their partial slots at zero
+            check_cuda(cudaMemsetAsync(scratch, 0, part_total * sizeof(double), rt_->stream()), "memset");
         std::size_t at = 0;
         for (int q = 0; q < set.count; ++q) {
             set.d[q].partial = scratch + at;
@@ -879,9 +967,15 @@ void Program::run_gemm(const Op& op, double* out) {
         const long long tm = (g.rows + 127) / 128;
         const std::uint64_t full = static_cast<std::uint64_t>(g.rows) * static_cast<std::uint64_t>(g.cols) *
                                    static_cast<std::uint64_t>(n_);
-        stats_->gemm_macs += tri ? full / static_cast<std::uint64_t>(tm * tm) *
+        std::uint64_t macs = tri ? full / static_cast<std::uint64_t>(tm * tm) *
                                        static_cast<std::uint64_t>(tm * (tm + 1) / 2)
                                  : full;
+        if (slice_world_ > 1 && g.tile_count >= 0) {
+            const long long total = gemm_tile_total(g, tri);
+            macs = static_cast<std::uint64_t>(static_cast<double>(macs) * static_cast<double>(g.tile_count) /
+                                              static_cast<double>(total));
+        }
+        stats_->gemm_macs += macs;
         ++stats_->gemm_launches;
         stats_->kernel_launches += static_cast<std::uint64_t>(launched);
         if (tri) ++stats_->symmetric_gemms;
@@ -892,7 +986,11 @@ void Program::launch(Op& op) {
     double* out = op.ext;
     if (!out && (!op.gemm || op.store)) {
         SymBuf& b = bufs_[static_cast<std::size_t>(op.out)];
-        if (!b.real) b.real = rt_->allocate(b.order, n_);
+        if (!b.real) {
+            b.real = rt_->allocate(b.order, n_);
+            if (slice_world_ > 1)
+                check_cuda(cudaMemsetAsync(b.real->ptr, 0, b.real->entries() * sizeof(double), rt_->stream()), "memset");
+        }
         b.real->symmetric = b.symmetric;
         out = b.real->ptr;
     }
@@ -907,6 +1005,43 @@ void Program::launch(Op& op) {
 // event; a buffer is freed on the stream of its last reader after the other
 // stream's readers are done.
 void Program::execute() {
+    const DeviceConfig& dc = config_.device;
+    const int emulate = dc.shard_rows && dc.emulate_world > 1 ? dc.emulate_world : 0;
+    const int world = emulate ? emulate : (dc.shard_rows ? std::max(1, dc.world_size) : 1);
+    if (world > 1) {
+        // Row sharding: each op runs as a slice per rank into zeroed outputs;
+        // with NCCL one all-reduce per materialized output completes it, in
+        // emulation the virtual ranks' slices accumulate on this device.
+        const bool collective = !emulate && rt_->has_comm();
+        if (!emulate && !collective) fail(ErrorCode::CollectiveError, "row sharding needs us_nccl_init first");
+        rt_->set_stream(rt_->main_stream());
+        slice_world_ = world;
+        for (std::size_t pos = 0; pos < schedule_.size(); ++pos) {
+            Op& op = ops_[schedule_[pos]];
+            for (int r = (emulate ? 0 : dc.rank); r < (emulate ? world : dc.rank + 1); ++r) {
+                slice_rank_ = r;
+                launch(op);
+            }
+            if (collective) {
+                auto reduce = [&](int b) {
+                    SymBuf& sb = bufs_[static_cast<std::size_t>(b)];
+                    if (sb.real) rt_->allreduce_sum(sb.real->ptr, sb.real->entries());
+                };
+                if (!op.ext && op.out >= 0 && (!op.gemm || op.store)) reduce(op.out);
+                for (const Op::Epi& e : op.epis)
+                    if (!e.ext && e.out >= 0) reduce(e.out);
+            }
+            for_each_read(op, [&](const View& v) {
+                SymBuf& b = bufs_[static_cast<std::size_t>(v.buf)];
+                if (!b.input && b.last_use == static_cast<int>(pos) && b.real && b.real.use_count() == 1 &&
+                    !keep_.count(v.buf))
+                    b.real.reset();
+            });
+        }
+        slice_world_ = 1;
+        slice_rank_ = 0;
+        return;
+    }
     bool has_gemm = false;
     for (std::size_t i : schedule_) has_gemm |= ops_[i].gemm;
     const bool multi =
@@ -1414,7 +1549,9 @@ std::vector<StatisticResult> lattice_batch(const std::vector<StatisticSpec>& spe
         for (std::size_t q = 0; q < specs.size(); ++q) {
             std::vector<int> ids;
             for (const Buf& b : tensors[q]) ids.push_back(prog.add_input(b));
-            record_terms(prog, plans[q], ids, config.device.rank, d_v + at, &out[q].stats);
+            if (config.device.shard_rows) plans[q].owner.assign(plans[q].owner.size(), 0);
+            record_terms(prog, plans[q], ids, config.device.shard_rows ? 0 : config.device.rank, d_v + at,
+                         &out[q].stats);
             at += plans[q].rgs.size();
         }
         double budget = static_cast<double>(config.device.memory_budget_bytes);
@@ -1430,6 +1567,8 @@ std::vector<StatisticResult> lattice_batch(const std::vector<StatisticSpec>& spe
         plan_s = std::chrono::duration<double>(Clock::now() - t0).count();
         prog.execute();
     }
+    // row sharding: every term value is a sum of per-rank partials
+    if (config.device.shard_rows && config.device.emulate_world <= 1 && rt.has_comm()) rt.allreduce_sum(d_v, T);
     std::vector<double> v(T, 0.0);
     if (T) check_cuda(cudaMemcpyAsync(v.data(), d_v, sizeof(double) * T, cudaMemcpyDeviceToHost, rt.stream()), "D2H");
     rt.release(d_v);

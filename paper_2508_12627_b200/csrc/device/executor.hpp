@@ -74,6 +74,14 @@ class Runtime {
     void release(double* p);
     void sync();
 
+    // NCCL communicator for row sharding (libnccl resolved at run time, so
+    // the library has no link-time NCCL dependency and shares the process's copy).
+    void nccl_init(int rank, int world, const void* unique_id);
+    static void nccl_unique_id(void* out128);
+    bool has_comm() const { return comm_ != nullptr; }
+    int comm_world() const { return comm_world_; }
+    void allreduce_sum(double* p, std::size_t count);
+
     enum Kind { kGemm = 0, kStream = 1, kOther = 2 };
     struct Profile {
         double ms[3] = {0, 0, 0};
@@ -91,6 +99,8 @@ class Runtime {
     cudaStream_t stream_ = nullptr;
     cudaStream_t side_ = nullptr;  // second stream: bandwidth ops overlap GEMM tails
     cudaStream_t cur_ = nullptr;
+    void* comm_ = nullptr;
+    int comm_world_ = 1;
     bool profiling_ = false;
     std::vector<cudaEvent_t> pool_;
     struct Mark {
@@ -222,6 +232,7 @@ class Program {
     std::vector<std::string> memo_log_;
     std::map<int, bool> keep_;
     std::vector<std::size_t> schedule_;  // execution order of live ops (memory-aware)
+    int slice_rank_ = 0, slice_world_ = 1;  // row sharding: the slice launch() computes
     double sched_peak_ = 0;
     double budget_ = 0;
     void make_schedule(double budget_bytes);

@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_f64_kernel(GemmArgs p) {
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
 
     const long long tiles_m = (p.rows + BM - 1) / BM, tiles_n = (p.cols + BN - 1) / BN;
-    const long long bid = blockIdx.x;
+    const long long bid = p.tile_begin + blockIdx.x;
     const long long width = GROUP_M * tiles_n;
     const long long group = bid / width, first_m = group * GROUP_M;
     const long long gsz = (tiles_m - first_m) < GROUP_M ? (tiles_m - first_m) : GROUP_M;
@@ -230,14 +230,17 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_f64_kernel(GemmArgs p) {
                 const double v0 = cpow(acc[mi][ni][0]) * weight(rl, cl);
                 if (c + 1 < p.cols) {
                     const double v1 = cpow(acc[mi][ni][1]) * weight(rl, cl + 1);
-                    if ((reinterpret_cast<unsigned long long>(dst) & 15) == 0)
+                    if (p.accumulate) {
+                        dst[0] += v0;
+                        dst[1] += v1;
+                    } else if ((reinterpret_cast<unsigned long long>(dst) & 15) == 0) {
                         *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
-                    else {
+                    } else {
                         dst[0] = v0;
                         dst[1] = v1;
                     }
                 } else if (c < p.cols) {
-                    dst[0] = v0;
+                    dst[0] = p.accumulate ? dst[0] + v0 : v0;
                 }
             }
         }
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_f64_kernel(GemmArgs p) {
     }
 }
 
-__global__ void gemm_finalize_scalar(const double* partial, long long P, double* out) {
+__global__ void gemm_finalize_scalar(const double* partial, long long P, double* out, int accumulate) {
     __shared__ double red[32];
     double acc = 0.0;
     for (long long i = threadIdx.x; i < P; i += blockDim.x) acc += partial[i];
@@ -318,16 +321,16 @@ __global__ void gemm_finalize_scalar(const double* partial, long long P, double*
     if (threadIdx.x < 32) {
         double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
         v = warp_sum(v);
-        if (threadIdx.x == 0) out[0] = v;
+        if (threadIdx.x == 0) out[0] = (accumulate ? out[0] : 0.0) + v;
     }
 }
 
-__global__ void gemm_finalize_vector(const double* partial, long long P, long long len, double* out) {
+__global__ void gemm_finalize_vector(const double* partial, long long P, long long len, double* out, int accumulate) {
     const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     if (i >= len) return;
     double acc = 0.0;
     for (long long q = 0; q < P; ++q) acc += partial[q * len + i];
-    out[i] = acc;
+    out[i] = (accumulate ? out[i] : 0.0) + acc;
 }
 
 template <bool AK, bool BK>
@@ -338,8 +341,9 @@ void launch_variant(const GemmArgs& a, cudaStream_t s) {
                              static_cast<int>(sizeof(Smem)));
         configured = true;
     }
-    const long long tiles = ((a.rows + BM - 1) / BM) * ((a.cols + BN - 1) / BN);
-    gemm_f64_kernel<AK, BK><<<static_cast<unsigned>(tiles), THREADS, sizeof(Smem), s>>>(a);
+    const long long total = ((a.rows + BM - 1) / BM) * ((a.cols + BN - 1) / BN);
+    const long long tiles = a.tile_count < 0 ? total - a.tile_begin : a.tile_count;
+    if (tiles > 0) gemm_f64_kernel<AK, BK><<<static_cast<unsigned>(tiles), THREADS, sizeof(Smem), s>>>(a);
 }
 
 }  // namespace
@@ -370,12 +374,14 @@ int launch_gemm(const GemmArgs& a, cudaStream_t s) {
     }
     const long long tm = (a.rows + BM - 1) / BM, tn = (a.cols + BN - 1) / BN;
     if (a.mode == kEpiSumAll) {
-        const long long blocks = launched > 0 ? launched : tm * tn;
-        gemm_finalize_scalar<<<1, 1024, 0, s>>>(a.partial, blocks, a.out);
+        const long long blocks = a.tile_count < 0 ? tm * tn - a.tile_begin : a.tile_count;
+        gemm_finalize_scalar<<<1, 1024, 0, s>>>(a.partial, blocks, a.out, a.accumulate);
     } else if (a.mode == kEpiSumCols) {
-        gemm_finalize_vector<<<static_cast<unsigned>((a.rows + 255) / 256), 256, 0, s>>>(a.partial, tn, a.rows, a.out);
+        gemm_finalize_vector<<<static_cast<unsigned>((a.rows + 255) / 256), 256, 0, s>>>(a.partial, tn, a.rows, a.out,
+                                                                                         a.accumulate);
     } else if (a.mode == kEpiSumRows) {
-        gemm_finalize_vector<<<static_cast<unsigned>((a.cols + 255) / 256), 256, 0, s>>>(a.partial, tm, a.cols, a.out);
+        gemm_finalize_vector<<<static_cast<unsigned>((a.cols + 255) / 256), 256, 0, s>>>(a.partial, tm, a.cols, a.out,
+                                                                                         a.accumulate);
     } else {
         return 1;
     }

@@ -113,7 +113,9 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 struct TmaArgs {
     long long rows, cols, n;
+    long long tile_begin;  // row sharding: first tile of this rank's range
     int symmetric;
+    int accumulate;        // outputs += (pre-zeroed)
     EpiSet epis;
 };
 
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         (reinterpret_cast<unsigned long long>(smem_raw) + 1023ull) & ~1023ull);
 
     const long long tiles_m = (p.rows + BM - 1) / BM, tiles_n = (p.cols + BN - 1) / BN;
-    const long long bid = blockIdx.x;
+    const long long bid = p.tile_begin + blockIdx.x;
     long long tm, tn;
     if (p.symmetric) {
         // upper-triangular tiles, row by row: row tm holds tiles tm..tiles_n-1
@@ -247,8 +249,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const long long R = r0 + r, C = c0 + c;
                 if (R >= rows || C >= cols) continue;
                 const double v = P(tile[r * TP + c]) * W(R, C);
-                if (d.mode == kEpiStore) d.out[d.transpose ? C * rows + R : R * cols + C] = v;
-                else s += v;
+                if (d.mode == kEpiStore) {
+                    double& o = d.out[d.transpose ? C * rows + R : R * cols + C];
+                    o = p.accumulate ? o + v : v;
+                } else {
+                    s += v;
+                }
             }
             if (mirror)  // the transposed tile (C, R): same values, weights at (C, R)
                 for (int i = tid; i < BM * BN; i += THREADS) {
@@ -256,8 +262,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                     const long long R = r0 + r, C = c0 + c;
                     if (R >= rows || C >= cols) continue;
                     const double v = P(tile[r * TP + c]) * W(C, R);
-                    if (d.mode == kEpiStore) d.out[d.transpose ? R * rows + C : C * cols + R] = v;
-                    else s += v;
+                    if (d.mode == kEpiStore) {
+                        double& o = d.out[d.transpose ? R * rows + C : C * cols + R];
+                        o = p.accumulate ? o + v : v;
+                    } else {
+                        s += v;
+                    }
                 }
             if (d.mode == kEpiSumAll) {
                 s = warp_sum(s);
@@ -369,19 +379,21 @@ bool encode(CUtensorMap* map, const double* ptr, bool kmajor, long long rows, lo
 }
 
 template <bool AK, bool BKM>
-long long launch_tma(const CUtensorMap& ma, const CUtensorMap& mb, const TmaArgs& args, cudaStream_t s) {
+long long launch_tma(const CUtensorMap& ma, const CUtensorMap& mb, const TmaArgs& args, long long count,
+                     cudaStream_t s) {
     static std::once_flag once;
     const int bytes = static_cast<int>(sizeof(TmaSmem)) + 1024;
     std::call_once(once, [&] {
         cudaFuncSetAttribute(gemm_tma_kernel<AK, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     });
     const long long tm = (args.rows + BM - 1) / BM, tn = (args.cols + BN - 1) / BN;
-    const long long tiles = args.symmetric ? tm * (tm + 1) / 2 : tm * tn;
-    gemm_tma_kernel<AK, BKM><<<static_cast<unsigned>(tiles), THREADS, bytes, s>>>(ma, mb, args);
+    const long long total = args.symmetric ? tm * (tm + 1) / 2 : tm * tn;
+    const long long tiles = count < 0 ? total - args.tile_begin : count;
+    if (tiles > 0) gemm_tma_kernel<AK, BKM><<<static_cast<unsigned>(tiles), THREADS, bytes, s>>>(ma, mb, args);
     return tiles;
 }
 
-__global__ void epi_finalize_scalar(const double* partial, long long P, double* out) {
+__global__ void epi_finalize_scalar(const double* partial, long long P, double* out, int accumulate) {
     __shared__ double red[32];
     double acc = 0.0;
     for (long long i = threadIdx.x; i < P; i += blockDim.x) acc += partial[i];
@@ -391,16 +403,16 @@ __global__ void epi_finalize_scalar(const double* partial, long long P, double* 
     if (threadIdx.x < 32) {
         double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
         v = warp_sum(v);
-        if (threadIdx.x == 0) out[0] = v;
+        if (threadIdx.x == 0) out[0] = (accumulate ? out[0] : 0.0) + v;
     }
 }
 
-__global__ void epi_finalize_vector(const double* partial, long long P, long long len, double* out) {
+__global__ void epi_finalize_vector(const double* partial, long long P, long long len, double* out, int accumulate) {
     const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     if (i >= len) return;
     double acc = 0.0;
     for (long long q = 0; q < P; ++q) acc += partial[q * len + i];
-    out[i] = acc;
+    out[i] = (accumulate ? out[i] : 0.0) + acc;
 }
 
 }  // namespace
@@ -450,21 +462,27 @@ int launch_gemm_multi(const GemmArgs& a, const EpiSet& epis, cudaStream_t s) {
     args.rows = a.rows;
     args.cols = a.cols;
     args.n = a.n;
+    args.tile_begin = a.tile_begin;
     args.symmetric = (a.symmetric_out && a.rows == a.cols) ? 1 : 0;
+    args.accumulate = a.accumulate;
     args.epis = epis;
     long long blocks;
-    if (ak) blocks = bk ? launch_tma<true, true>(ma, mb, args, s) : launch_tma<true, false>(ma, mb, args, s);
-    else blocks = bk ? launch_tma<false, true>(ma, mb, args, s) : launch_tma<false, false>(ma, mb, args, s);
+    const long long cnt = a.tile_count;
+    if (ak) blocks = bk ? launch_tma<true, true>(ma, mb, args, cnt, s) : launch_tma<true, false>(ma, mb, args, cnt, s);
+    else blocks = bk ? launch_tma<false, true>(ma, mb, args, cnt, s) : launch_tma<false, false>(ma, mb, args, cnt, s);
+    if (blocks <= 0) return 0;
     int launched = 1;
     const long long tm = (a.rows + BM - 1) / BM, tn = (a.cols + BN - 1) / BN;
     for (int q = 0; q < epis.count; ++q) {
         const EpiDesc& d = epis.d[q];
         if (d.mode == kEpiSumAll) {
-            epi_finalize_scalar<<<1, 1024, 0, s>>>(d.partial, blocks, d.out);
+            epi_finalize_scalar<<<1, 1024, 0, s>>>(d.partial, blocks, d.out, a.accumulate);
         } else if (d.mode == kEpiSumCols) {
-            epi_finalize_vector<<<static_cast<unsigned>((a.rows + 255) / 256), 256, 0, s>>>(d.partial, tn, a.rows, d.out);
+            epi_finalize_vector<<<static_cast<unsigned>((a.rows + 255) / 256), 256, 0, s>>>(d.partial, tn, a.rows, d.out,
+                                                                                          a.accumulate);
         } else if (d.mode == kEpiSumRows) {
-            epi_finalize_vector<<<static_cast<unsigned>((a.cols + 255) / 256), 256, 0, s>>>(d.partial, tm, a.cols, d.out);
+            epi_finalize_vector<<<static_cast<unsigned>((a.cols + 255) / 256), 256, 0, s>>>(d.partial, tm, a.cols, d.out,
+                                                                                          a.accumulate);
         } else {
             continue;
         }
@@ -495,7 +513,12 @@ long long launch_gemm_tma(const GemmArgs& in, cudaStream_t s) {
     GemmArgs a = in;
     if (a.symmetric_out && a.rows != a.cols) a.symmetric_out = 0;
     const int k = launch_gemm_multi(a, e, s);
-    return k > 0 ? 1 : -1;
+    return k >= 0 ? 1 : -1;
+}
+
+long long gemm_tile_total(const GemmArgs& a, bool tma_symmetric) {
+    const long long tm = (a.rows + BM - 1) / BM, tn = (a.cols + BN - 1) / BN;
+    return (tma_symmetric && a.rows == a.cols) ? tm * (tm + 1) / 2 : tm * tn;
 }
 
 }  // namespace ustats::dev

@@ -27,6 +27,8 @@ struct StreamArgs {
     long long stride[kMaxFactors][kMaxDims] = {};
     double* out = nullptr;
     double scale = 1.0;
+    long long n0 = 0;      // extent of iteration dim 0 (0 = n): a rank's slice in row sharding
+    int accumulate = 0;    // out += result (outputs pre-zeroed; slices of all ranks add up)
 };
 
 // One GEMM operand: value(r, k) = prod_f ptr_f[ off_f(r) + kstride_f * k ]
@@ -70,7 +72,13 @@ struct GemmArgs {
     int b_kmajor = 1;
     int symmetric_out = 0;      // rows==cols and C symmetric: compute upper tiles only
     int self_power = 1;         // epilogue value = C^self_power * W (2: the consumer read C twice)
+    long long tile_begin = 0;   // row sharding: this rank's contiguous range of the tile list
+    long long tile_count = -1;  // -1 = every tile
+    int accumulate = 0;         // outputs += (pre-zeroed), see StreamArgs::accumulate
 };
+
+// Number of CTA tiles of a GEMM launch (upper triangle when symmetric_out and square).
+long long gemm_tile_total(const GemmArgs& a, bool tma_symmetric);
 
 // Multi-consumer epilogues of the TMA GEMM: every consumer of a GEMM output
 // that iterates exactly over its (row, col) space runs on the accumulator tile

@@ -65,29 +65,34 @@ __device__ double block_sum(double v, double* red) {
     return t;  // valid in thread 0
 }
 
+__device__ __forceinline__ void put(const StreamArgs& a, unsigned long long o, double v) {
+    if (a.accumulate) a.out[o] += v;
+    else a.out[o] = v;
+}
+
 // No dims at all: product of scalar factors.
 __global__ void stream_product(StreamArgs a) {
     if (threadIdx.x != 0) return;
     double v = a.scale;
     for (int f = 0; f < a.nf; ++f) v *= a.ptr[f][0];
-    a.out[0] = v;
+    put(a, 0, v);
 }
 
 // Elementwise: n_sum == 0. Dims [0, n_out); inner = last output dim.
-__global__ void stream_elementwise(StreamArgs a, unsigned long long rows) {
+__global__ void stream_elementwise(StreamArgs a, unsigned long long rows, long long inner_n) {
     const int inner = a.n_out - 1;
     for (unsigned long long row = blockIdx.y; row < rows; row += gridDim.y) {
         long long off[kMaxFactors] = {};
         Digits::offsets(a, row, 0, a.n_out - 1, off);
-        for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < a.n;
+        for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < inner_n;
              i += static_cast<long long>(gridDim.x) * blockDim.x)
-            a.out[row * a.n + i] = a.scale * product_at(a, off, i, inner);
+            put(a, row * inner_n + i, a.scale * product_at(a, off, i, inner));
     }
 }
 
 // Full reduction: n_out == 0. `inner` chosen by the host (its dims order puts
 // it last). Block b reduces rows [b*rows/B, (b+1)*rows/B).
-__global__ void stream_reduce_all(StreamArgs a, unsigned long long rows, double* partial) {
+__global__ void stream_reduce_all(StreamArgs a, unsigned long long rows, long long inner_n, double* partial) {
     __shared__ double red[32];
     const int D = a.n_sum;
     const int inner = D - 1;
@@ -97,7 +102,7 @@ __global__ void stream_reduce_all(StreamArgs a, unsigned long long rows, double*
     for (unsigned long long row = lo; row < hi; ++row) {
         long long off[kMaxFactors] = {};
         Digits::offsets(a, row, 0, D - 1, off);
-        for (long long i = threadIdx.x; i < a.n; i += blockDim.x) acc += product_at(a, off, i, inner);
+        for (long long i = threadIdx.x; i < inner_n; i += blockDim.x) acc += product_at(a, off, i, inner);
     }
     const double t = block_sum(acc, red);
     if (threadIdx.x == 0) partial[blockIdx.x] = t;
@@ -124,7 +129,7 @@ __global__ void stream_reduce_warp(StreamArgs a, unsigned long long outputs,
         for (long long i = lane; i < a.n; i += 32) acc += product_at(a, off, i, inner);
     }
     acc = warp_sum(acc);
-    if (lane == 0) a.out[o] = a.scale * acc;
+    if (lane == 0) put(a, o, a.scale * acc);
 }
 
 // Output-dim-fast reduction: one thread per output (consecutive threads along
@@ -177,29 +182,29 @@ __global__ void stream_reduce_thread(StreamArgs a, unsigned long long outputs,
         }
     }
     if (S == 1)
-        a.out[o] = a.scale * acc;
+        put(a, o, a.scale * acc);
     else
         partial[blockIdx.y * outputs + o] = acc;
 }
 
 // out[o] = scale * sum_{p < P} partial[p * outputs + o], in p order.
 __global__ void finalize_columns(const double* partial, unsigned long long P,
-                                 unsigned long long outputs, double scale, double* out) {
+                                 unsigned long long outputs, double scale, double* out, int accumulate) {
     const unsigned long long o = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
     if (o >= outputs) return;
     double acc = 0.0;
     for (unsigned long long p = 0; p < P; ++p) acc += partial[p * outputs + o];
-    out[o] = scale * acc;
+    out[o] = (accumulate ? out[o] : 0.0) + scale * acc;
 }
 
 // out[0] = scale * sum of P partials: fixed strided split + fixed tree.
 __global__ void finalize_scalar(const double* partial, unsigned long long P, double scale,
-                                double* out) {
+                                double* out, int accumulate) {
     __shared__ double red[32];
     double acc = 0.0;
     for (unsigned long long p = threadIdx.x; p < P; p += blockDim.x) acc += partial[p];
     const double t = block_sum(acc, red);
-    if (threadIdx.x == 0) out[0] = scale * t;
+    if (threadIdx.x == 0) out[0] = (accumulate ? out[0] : 0.0) + scale * t;
 }
 
 unsigned long long ipow(long long n, int e) {
@@ -221,10 +226,22 @@ int blocks_for_all(unsigned long long rows, long long n, int sm_count) {
 
 }  // namespace
 
+// Extent of iteration dim 0 (a rank's slice under row sharding) and the
+// counts of the (row, inner) decompositions that include it.
+long long ext0(const StreamArgs& a) { return a.n0 > 0 ? a.n0 : a.n; }
+unsigned long long span(const StreamArgs& a, int dims) {  // dims [0, dims)
+    if (dims <= 0) return 1;
+    return static_cast<unsigned long long>(ext0(a)) * ipow(a.n, dims - 1);
+}
+
 std::size_t stream_scratch_entries(const StreamArgs& a, int sm_count) {
     if (a.n_sum == 0) return 0;
-    if (a.n_out == 0) return static_cast<std::size_t>(blocks_for_all(ipow(a.n, a.n_sum - 1), a.n, sm_count));
-    const unsigned long long outputs = ipow(a.n, a.n_out);
+    if (a.n_out == 0) {
+        const int D = a.n_sum;
+        const unsigned long long rows = span(a, D - 1);
+        return static_cast<std::size_t>(blocks_for_all(rows, D == 1 ? ext0(a) : a.n, sm_count));
+    }
+    const unsigned long long outputs = span(a, a.n_out);
     const unsigned long long sflat = ipow(a.n, a.n_sum);
     const unsigned long long threads_wanted = static_cast<unsigned long long>(sm_count) * 2048;
     unsigned long long slices = 1;
@@ -244,21 +261,25 @@ int launch_stream(const StreamArgs& a, double* scratch, std::size_t scratch_entr
         return 1;
     }
     if (a.n_sum == 0) {
-        const unsigned long long rows = ipow(a.n, a.n_out - 1);
-        const unsigned gx = static_cast<unsigned>((a.n + kThreads - 1) / kThreads);
+        const unsigned long long rows = a.n_out >= 2 ? span(a, a.n_out - 1) : 1;
+        const long long inner_n = a.n_out == 1 ? ext0(a) : a.n;
+        const unsigned gx = static_cast<unsigned>((inner_n + kThreads - 1) / kThreads);
         unsigned long long gy = rows;
         if (gy > 65535) gy = 65535;
-        stream_elementwise<<<dim3(gx, static_cast<unsigned>(gy)), kThreads, 0, s>>>(a, rows);
+        stream_elementwise<<<dim3(gx, static_cast<unsigned>(gy)), kThreads, 0, s>>>(a, rows, inner_n);
         return 1;
     }
     if (a.n_out == 0) {
-        const unsigned long long rows = ipow(a.n, a.n_sum - 1);
-        const int blocks = blocks_for_all(rows, a.n, sm_count);
-        stream_reduce_all<<<blocks, kThreads, 0, s>>>(a, rows, scratch);
-        finalize_scalar<<<1, 1024, 0, s>>>(scratch, static_cast<unsigned long long>(blocks), a.scale, a.out);
+        const int D = a.n_sum;
+        const unsigned long long rows = D >= 2 ? span(a, D - 1) : 1;
+        const long long inner_n = D == 1 ? ext0(a) : a.n;
+        const int blocks = blocks_for_all(rows, inner_n, sm_count);
+        stream_reduce_all<<<blocks, kThreads, 0, s>>>(a, rows, inner_n, scratch);
+        finalize_scalar<<<1, 1024, 0, s>>>(scratch, static_cast<unsigned long long>(blocks), a.scale, a.out,
+                                           a.accumulate);
         return 2;
     }
-    const unsigned long long outputs = ipow(a.n, a.n_out);
+    const unsigned long long outputs = span(a, a.n_out);
     const int last = a.n_out + a.n_sum - 1;
     const int out_last = a.n_out - 1;
     int unit_sum = 0, unit_out = 0;
@@ -282,7 +303,7 @@ int launch_stream(const StreamArgs& a, double* scratch, std::size_t scratch_entr
     stream_reduce_thread<<<dim3(gx, static_cast<unsigned>(slices)), kThreads, 0, s>>>(a, outputs, sflat,
                                                                                    scratch);
     if (slices > 1) {
-        finalize_columns<<<gx, kThreads, 0, s>>>(scratch, slices, outputs, a.scale, a.out);
+        finalize_columns<<<gx, kThreads, 0, s>>>(scratch, slices, outputs, a.scale, a.out, a.accumulate);
         return 2;
     }
     return 1;

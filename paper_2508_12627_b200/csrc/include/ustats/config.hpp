@@ -20,6 +20,13 @@ struct DeviceConfig {
     bool reorder_for_sharing = true;   ///< choose among equal-width orders to maximize sharing
     bool donate_inputs = false;        ///< device inputs may be sparsified in place (no copy)
     bool serial_launch = false;        ///< one stream only (no GEMM/reduction overlap)
+    /// Multi-GPU scheme: false = V-terms sharded over ranks (LPT, one all-reduce
+    /// of the term vector); true = every op row-sharded over ranks (GEMM tile
+    /// ranges / leading-index slices, one all-reduce per materialized output).
+    bool shard_rows = false;
+    /// Row sharding over `emulate_world` virtual ranks on this one device, op
+    /// by op in lockstep (tests the decomposition without NCCL). 0 = off.
+    int emulate_world = 0;
     /// Device-memory budget for inputs + live intermediates of one statistic's
     /// program (0 = free device memory at execution; plan-only: 179 GiB).
     std::uint64_t memory_budget_bytes = 0;

@@ -243,3 +243,28 @@ def test_hoif_tau_closed_forms(engine):
     with pytest.raises(engine.UStatsError) as e:
         engine.hoif_tau(5, 1, rng.normal(size=(4, 3)))
     assert e.value.code == "SampleTooSmall"
+
+
+@pytest.mark.parametrize("name,n,world", [("C2", 200, 3), ("C3", 130, 4), ("C4", 40, 3), ("C5", 130, 5),
+                                          ("C1", 101, 2)])
+def test_row_sharding_emulated(engine, name, n, world):
+    # every op split into `world` slices (GEMM tile ranges, leading-index
+    # ranges) accumulated on one device in lockstep == the unsharded result
+    from paper_2508_12627_b200.workloads import generate
+    factors, sig, m, _ = generate(name, n)
+    base = engine.u_terms(factors, sig, m)
+    cfg = engine.Config(shard_rows=True, emulate_world=world)
+    got = engine.u_terms(factors, sig, m, cfg)
+    scale = np.max(np.abs(base.v))
+    assert np.max(np.abs(got.v - base.v)) <= TOL * scale
+    assert abs(got.value - base.value) <= TOL * scale
+
+
+def test_row_sharding_single_rank_nccl(engine):
+    # the real NCCL path at world size 1 (the only size one GPU allows)
+    from paper_2508_12627_b200.workloads import generate
+    engine.nccl_init(0, 0, 1, engine.nccl_unique_id())
+    factors, sig, m, _ = generate("C2", 256)
+    base = engine.u_statistic_tensors(factors, sig, m)
+    got = engine.u_statistic_tensors(factors, sig, m, engine.Config(shard_rows=True, world_size=1))
+    assert got == base
