@@ -24,6 +24,7 @@ void check_cuda(cudaError_t e, const char* what) {
 
 // ---------------------------------------------------------------- Runtime
 DeviceBuffer::~DeviceBuffer() {
+    for (auto& r : ready) cudaEventDestroy(r.second);
     if (ptr && !borrowed && rt) {
         cudaFreeAsync(ptr, rt->stream());
         if (std::getenv("USTATS_SCHED_DEBUG") && entries() * 8 > (1ull << 30))
@@ -51,8 +52,13 @@ Runtime& Runtime::get(int device) {
 Runtime::Runtime(int device) : device_(device) {
     check_cuda(cudaSetDevice(device), "cudaSetDevice");
     check_cuda(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, device), "cudaDeviceGetAttribute");
-    check_cuda(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
-    check_cuda(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "cudaStreamCreate");
+    // the main stream (GEMMs) outranks the side stream (reductions filling
+    // the GEMM's tail): pending GEMM CTAs get freed SMs first
+    int lo_prio = 0, hi_prio = 0;
+    check_cuda(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio), "cudaDeviceGetStreamPriorityRange");
+    check_cuda(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, hi_prio), "cudaStreamCreate");
+    check_cuda(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, lo_prio), "cudaStreamCreate");
+    check_cuda(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking), "cudaStreamCreate");
     cur_ = stream_;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -104,6 +110,7 @@ void Runtime::release(double* p) {
 }
 
 void Runtime::sync() {
+    check_cuda(cudaStreamSynchronize(copy_), "cudaStreamSynchronize");
     check_cuda(cudaStreamSynchronize(side_), "cudaStreamSynchronize");
     check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
 }
@@ -950,8 +957,40 @@ void Program::run_gemm(const Op& op, double* out) {
             set.d[q].partial = scratch + at;
             at += gemm_epi_partial_entries(g, set.d[q].mode);
         }
+        // A symmetric product of an input still being uploaded in row panels:
+        // launch the column-ordered tile triangle in pieces, each as soon as
+        // the panels it reads have landed (upload/compute overlap).
+        const DeviceBuffer* src = bufs_[static_cast<std::size_t>(fa[0].buf)].real.get();
+        const bool chunked = slice_world_ == 1 && op.symmetric_out && g.rows == g.cols && fa[0].buf == fb[0].buf &&
+                             src && src->ready.size() > 1;
         rt_->begin(Runtime::kGemm);
-        launched = launch_gemm_multi(g, set, rt_->stream());
+        if (!chunked) {
+            launched = launch_gemm_multi(g, set, rt_->stream());
+        } else {
+            for (int q = 0; q < set.count; ++q)
+                if (set.d[q].mode == kEpiStore)
+                    check_cuda(cudaMemsetAsync(set.d[q].out, 0, static_cast<std::size_t>(g.rows * g.cols) * sizeof(double),
+                                               rt_->stream()),
+                               "memset");
+            const long long tiles_n = (g.rows + 127) / 128;
+            long long prev = 0;
+            launched = 0;
+            g.tri_colmajor = 1;
+            g.accumulate = 1;
+            for (const auto& [rows_ready, ev] : src->ready) {
+                const long long k = rows_ready >= g.rows ? tiles_n : rows_ready / 128;
+                if (k <= prev) continue;
+                check_cuda(cudaStreamWaitEvent(rt_->stream(), ev, 0), "wait panel");
+                if (scratch) check_cuda(cudaMemsetAsync(scratch, 0, part_total * sizeof(double), rt_->stream()), "memset");
+                g.tile_begin = prev * (prev + 1) / 2;
+                g.tile_count = k * (k + 1) / 2 - g.tile_begin;
+                const int l = launch_gemm_multi(g, set, rt_->stream());
+                if (l < 0) break;
+                launched += l;
+                prev = k;
+            }
+            if (prev < tiles_n) launched = -1;
+        }
         rt_->end(Runtime::kGemm);
         if (launched < 0) fail(ErrorCode::InvalidArgument, "executor: fused GEMM lost TMA eligibility");
     } else {
@@ -1015,6 +1054,9 @@ void Program::execute() {
         const bool collective = !emulate && rt_->has_comm();
         if (!emulate && !collective) fail(ErrorCode::CollectiveError, "row sharding needs us_nccl_init first");
         rt_->set_stream(rt_->main_stream());
+        for (const SymBuf& b : bufs_)
+            if (b.input && b.real && !b.real->ready.empty())
+                check_cuda(cudaStreamWaitEvent(rt_->main_stream(), b.real->ready.back().second, 0), "wait upload");
         slice_world_ = world;
         for (std::size_t pos = 0; pos < schedule_.size(); ++pos) {
             Op& op = ops_[schedule_[pos]];
@@ -1055,9 +1097,44 @@ void Program::execute() {
     };
     cudaStream_t streams[2] = {rt_->main_stream(), rt_->side_stream()};
     const std::size_t N = ops_.size();
+    if (multi) {
+        // Side-stream reductions are launched right after the next GEMM, so the
+        // GEMM takes the whole GPU first and they fill its last wave; a main-
+        // stream op that reads a deferred op's output flushes the queue first.
+        std::vector<std::size_t> order, deferred;
+        std::vector<char> pending_out(bufs_.size(), 0);
+        auto flush = [&] {
+            for (std::size_t d : deferred) {
+                order.push_back(d);
+                const Op& o = ops_[d];
+                if (!o.ext && o.out >= 0) pending_out[static_cast<std::size_t>(o.out)] = 0;
+            }
+            deferred.clear();
+        };
+        for (std::size_t i : schedule_) {
+            const Op& op = ops_[i];
+            if (side_ok(op)) {
+                deferred.push_back(i);
+                if (!op.ext && op.out >= 0) pending_out[static_cast<std::size_t>(op.out)] = 1;
+                continue;
+            }
+            bool needs = false;
+            for_each_read(op, [&](const View& v) { needs |= pending_out[static_cast<std::size_t>(v.buf)] != 0; });
+            if (needs) flush();
+            order.push_back(i);
+            if (op.gemm) flush();
+        }
+        flush();
+        schedule_ = order;
+        for (SymBuf& b : bufs_) b.last_use = -1;
+        for (std::size_t pos = 0; pos < schedule_.size(); ++pos)
+            for_each_read(ops_[schedule_[pos]],
+                          [&](const View& v) { bufs_[static_cast<std::size_t>(v.buf)].last_use = static_cast<int>(pos); });
+    }
     std::vector<cudaEvent_t> done(N, nullptr);
     std::vector<int> on(N, 0), producer(bufs_.size(), -1);
     std::vector<std::array<int, 2>> readers(bufs_.size(), {-1, -1});
+    std::vector<std::pair<int, int>> upload_waited;
     for (std::size_t pos = 0; pos < schedule_.size(); ++pos) {
         const std::size_t i = schedule_[pos];
         Op& op = ops_[i];
@@ -1069,6 +1146,19 @@ void Program::execute() {
                 const int p = producer[static_cast<std::size_t>(v.buf)];
                 if (p >= 0 && on[static_cast<std::size_t>(p)] != si) check_cuda(cudaStreamWaitEvent(s, done[static_cast<std::size_t>(p)], 0), "wait");
             });
+        // inputs still uploading in panels: every reader except the panel-aware
+        // symmetric GEMM waits for the whole upload (once per stream)
+        for_each_read(op, [&](const View& v) {
+            const SymBuf& b = bufs_[static_cast<std::size_t>(v.buf)];
+            if (!b.input || !b.real || b.real->ready.empty()) return;
+            const bool panel_aware = op.gemm && op.symmetric_out && op.fa.size() == 1 && op.fb.size() == 1 &&
+                                     op.fa[0].buf == op.fb[0].buf && (!op.epis.empty() || op.symmetric_out);
+            if (panel_aware) return;
+            const auto key = std::make_pair(v.buf, si);
+            if (std::find(upload_waited.begin(), upload_waited.end(), key) != upload_waited.end()) return;
+            upload_waited.push_back(key);
+            check_cuda(cudaStreamWaitEvent(s, b.real->ready.back().second, 0), "wait upload");
+        });
         rt_->set_stream(s);
         launch(op);
         if (!op.ext && op.out >= 0) producer[static_cast<std::size_t>(op.out)] = static_cast<int>(i);
@@ -1470,8 +1560,20 @@ void record_terms(Program& prog, const TermPlan& plan, const std::vector<int>& i
     }
 }
 
+namespace {
+// Host matrices at least this big are uploaded in row panels on the copy
+// stream so the first (symmetric) GEMM starts on the panels that landed.
+constexpr long long kChunkMinN = 2048;
+constexpr int kUploadPanels = 16;
+}  // namespace
+
 std::vector<StatisticResult> lattice_batch(const std::vector<StatisticSpec>& specs, bool inputs_on_device,
                                            long long n, LatticeMode mode, const Config& config) {
+    return lattice_batch_impl(specs, inputs_on_device, n, mode, config, true);
+}
+
+std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>& specs, bool inputs_on_device,
+                                                long long n, LatticeMode mode, const Config& config, bool speculate) {
     std::vector<StatisticResult> out(specs.size());
     Runtime& rt = Runtime::get(config.device.device);
     const auto t_up = Clock::now();
@@ -1481,6 +1583,8 @@ std::vector<StatisticResult> lattice_batch(const std::vector<StatisticSpec>& spe
     std::map<const double*, Buf> by_ptr;
     std::vector<std::vector<Buf>> tensors(specs.size());
     std::vector<std::pair<Buf, int*>> probes;
+    std::vector<std::tuple<Buf, int*, std::pair<const void*, long long>>> speculative;
+    std::vector<std::pair<std::pair<const void*, long long>, int>> probe_keys;
     std::size_t total_factors = 0;
     for (const auto& sp : specs) total_factors += sp.sig.size();
     int* flags = nullptr;
@@ -1499,8 +1603,32 @@ std::vector<StatisticResult> lattice_batch(const std::vector<StatisticSpec>& spe
                 continue;
             }
             Buf b;
+            const bool panels = !inputs_on_device && order == 2 && n >= kChunkMinN;
             if (inputs_on_device && config.device.donate_inputs) {
                 b = rt.borrow(sp.inputs[k], order, n);  // sparsified in place: the caller donated it
+            } else if (panels) {
+                // row panels on the copy stream, each sparsified as it lands
+                b = rt.allocate(order, n);
+                cudaEvent_t allocated;
+                check_cuda(cudaEventCreateWithFlags(&allocated, cudaEventDisableTiming), "event");
+                check_cuda(cudaEventRecord(allocated, rt.main_stream()), "event");
+                check_cuda(cudaStreamWaitEvent(rt.copy_stream(), allocated, 0), "wait");
+                cudaEventDestroy(allocated);
+                const long long step = ((n + kUploadPanels - 1) / kUploadPanels + 127) / 128 * 128;
+                for (long long r0 = 0; r0 < n; r0 += step) {
+                    const long long r1 = std::min(n, r0 + step);
+                    check_cuda(cudaMemcpyAsync(b->ptr + r0 * n, sp.inputs[k] + r0 * n,
+                                               static_cast<std::size_t>((r1 - r0) * n) * sizeof(double),
+                                               cudaMemcpyHostToDevice, rt.copy_stream()),
+                               "upload panel");
+                    if (mode == LatticeMode::Sparsified)
+                        upload_stats.kernel_launches +=
+                            static_cast<std::uint64_t>(launch_zero_diagonal_rows(b->ptr, n, r0, r1, rt.copy_stream()));
+                    cudaEvent_t ev;
+                    check_cuda(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+                    check_cuda(cudaEventRecord(ev, rt.copy_stream()), "event");
+                    b->ready.emplace_back(r1, ev);
+                }
             } else {
                 b = rt.allocate(order, n);
                 check_cuda(cudaMemcpyAsync(b->ptr, sp.inputs[k], b->entries() * sizeof(double),
@@ -1509,12 +1637,26 @@ std::vector<StatisticResult> lattice_batch(const std::vector<StatisticSpec>& spe
                            "upload");
             }
             rt.begin(Runtime::kOther);
-            if (mode == LatticeMode::Sparsified)
+            if (mode == LatticeMode::Sparsified && !panels)
                 upload_stats.kernel_launches += static_cast<std::uint64_t>(launch_sparsify(b->ptr, order, n, rt.stream()));
             if (flags && order == 2) {
                 int* f = flags + probes.size();
-                upload_stats.kernel_launches += static_cast<std::uint64_t>(launch_symmetry_check(b->ptr, n, f, rt.stream()));
-                probes.emplace_back(b, f);
+                const auto key = std::make_pair(static_cast<const void*>(sp.inputs[k]), n);
+                auto seen = rt.symmetry_seen.find(key);
+                if (panels && speculate && seen != rt.symmetry_seen.end() && seen->second) {
+                    // speculate (the same host matrix was symmetric last time):
+                    // plan now, verify with a probe queued behind the upload
+                    b->symmetric = true;
+                    upload_stats.kernel_launches +=
+                        static_cast<std::uint64_t>(launch_symmetry_check(b->ptr, n, f, rt.copy_stream()));
+                    speculative.emplace_back(b, f, key);
+                } else {
+                    if (panels) check_cuda(cudaStreamWaitEvent(rt.stream(), b->ready.back().second, 0), "wait upload");
+                    upload_stats.kernel_launches +=
+                        static_cast<std::uint64_t>(launch_symmetry_check(b->ptr, n, f, rt.stream()));
+                    probes.emplace_back(b, f);
+                    if (!inputs_on_device) probe_keys.emplace_back(key, static_cast<int>(probes.size()) - 1);
+                }
             }
             rt.end(Runtime::kOther);
             by_ptr[sp.inputs[k]] = b;
@@ -1525,11 +1667,11 @@ std::vector<StatisticResult> lattice_batch(const std::vector<StatisticSpec>& spe
         std::vector<int> host(probes.size());
         check_cuda(cudaMemcpyAsync(host.data(), flags, sizeof(int) * probes.size(), cudaMemcpyDeviceToHost, rt.stream()),
                    "flags");
-        rt.sync();
+        check_cuda(cudaStreamSynchronize(rt.main_stream()), "sync");
         for (std::size_t i = 0; i < probes.size(); ++i) probes[i].first->symmetric = host[i] == 0;
+        for (const auto& [key, idx] : probe_keys) rt.symmetry_seen[key] = host[static_cast<std::size_t>(idx)] == 0;
     }
-    if (flags) cudaFreeAsync(flags, rt.stream());
-    rt.sync();
+    check_cuda(cudaStreamSynchronize(rt.main_stream()), "sync");
     const double upload_s = std::chrono::duration<double>(Clock::now() - t_up).count();
 
     const auto t0 = Clock::now();
@@ -1572,10 +1714,27 @@ std::vector<StatisticResult> lattice_batch(const std::vector<StatisticSpec>& spe
     std::vector<double> v(T, 0.0);
     if (T) check_cuda(cudaMemcpyAsync(v.data(), d_v, sizeof(double) * T, cudaMemcpyDeviceToHost, rt.stream()), "D2H");
     rt.release(d_v);
+    std::vector<int> spec_flags(speculative.size(), 0);
+    for (std::size_t i = 0; i < speculative.size(); ++i) {
+        check_cuda(cudaStreamWaitEvent(rt.main_stream(), std::get<0>(speculative[i])->ready.back().second, 0), "wait");
+        check_cuda(cudaMemcpyAsync(&spec_flags[i], std::get<1>(speculative[i]), sizeof(int), cudaMemcpyDeviceToHost,
+                                   rt.main_stream()),
+                   "D2H flag");
+    }
+    if (flags) cudaFreeAsync(flags, rt.main_stream());
     tensors.clear();
     by_ptr.clear();
     probes.clear();
     rt.sync();
+    bool mispredicted = false;
+    for (std::size_t i = 0; i < speculative.size(); ++i)
+        if (spec_flags[i] != 0) {
+            rt.symmetry_seen[std::get<2>(speculative[i])] = false;
+            mispredicted = true;
+        }
+    speculative.clear();
+    if (mispredicted)  // the host matrix changed and is no longer symmetric: redo without speculation
+        return lattice_batch_impl(specs, inputs_on_device, n, mode, config, false);
     const double contract_s = std::chrono::duration<double>(Clock::now() - t0).count();
 
     std::size_t at = 0;

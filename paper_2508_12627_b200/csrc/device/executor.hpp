@@ -51,6 +51,8 @@ struct DeviceBuffer {
     bool symmetric = false;
     bool borrowed = false;
     Runtime* rt = nullptr;
+    // chunked upload in flight: rows [0, first) are usable once `second` completes
+    std::vector<std::pair<long long, cudaEvent_t>> ready;
     ~DeviceBuffer();
     std::uint64_t entries() const;
 };
@@ -64,6 +66,9 @@ class Runtime {
     cudaStream_t stream() const { return cur_; }  // where allocations / launches go now
     cudaStream_t main_stream() const { return stream_; }
     cudaStream_t side_stream() const { return side_; }
+    cudaStream_t copy_stream() const { return copy_; }
+    // bitwise-symmetry results of host inputs seen before (speculation key)
+    std::map<std::pair<const void*, long long>, bool> symmetry_seen;
     void set_stream(cudaStream_t s) { cur_ = s; }
     int device() const { return device_; }
     int sm_count() const { return sm_count_; }
@@ -98,6 +103,7 @@ class Runtime {
     int sm_count_ = 148;
     cudaStream_t stream_ = nullptr;
     cudaStream_t side_ = nullptr;  // second stream: bandwidth ops overlap GEMM tails
+    cudaStream_t copy_ = nullptr;  // chunked host->device uploads
     cudaStream_t cur_ = nullptr;
     void* comm_ = nullptr;
     int comm_world_ = 1;
@@ -312,6 +318,8 @@ struct StatisticSpec {
 };
 std::vector<StatisticResult> lattice_batch(const std::vector<StatisticSpec>& specs, bool inputs_on_device,
                                            long long n, LatticeMode mode, const Config& config);
+std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>& specs, bool inputs_on_device,
+                                                long long n, LatticeMode mode, const Config& config, bool speculate);
 
 StatisticResult lattice_statistic(const std::vector<const double*>& inputs, bool inputs_on_device,
                                   const std::vector<IndexTuple>& zero_sig, int m, long long n,

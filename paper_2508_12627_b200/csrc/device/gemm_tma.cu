@@ -115,6 +115,7 @@ struct TmaArgs {
     long long rows, cols, n;
     long long tile_begin;  // row sharding: first tile of this rank's range
     int symmetric;
+    int colmajor;          // symmetric list ordered by column: tile (tm <= tn) at tn(tn+1)/2 + tm
     int accumulate;        // outputs += (pre-zeroed)
     EpiSet epis;
 };
@@ -130,7 +131,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     const long long tiles_m = (p.rows + BM - 1) / BM, tiles_n = (p.cols + BN - 1) / BN;
     const long long bid = p.tile_begin + blockIdx.x;
     long long tm, tn;
-    if (p.symmetric) {
+    if (p.symmetric && p.colmajor) {
+        // column by column: column tn holds tiles 0..tn (panels <= tn)
+        tn = static_cast<long long>((sqrt(8.0 * static_cast<double>(bid) + 1.0) - 1.0) * 0.5);
+        while (tn * (tn + 1) / 2 > bid) --tn;
+        while ((tn + 1) * (tn + 2) / 2 <= bid) ++tn;
+        tm = bid - tn * (tn + 1) / 2;
+    } else if (p.symmetric) {
         // upper-triangular tiles, row by row: row tm holds tiles tm..tiles_n-1
         long long rest = bid;
         tm = 0;
@@ -464,6 +471,7 @@ int launch_gemm_multi(const GemmArgs& a, const EpiSet& epis, cudaStream_t s) {
     args.n = a.n;
     args.tile_begin = a.tile_begin;
     args.symmetric = (a.symmetric_out && a.rows == a.cols) ? 1 : 0;
+    args.colmajor = a.tri_colmajor;
     args.accumulate = a.accumulate;
     args.epis = epis;
     long long blocks;

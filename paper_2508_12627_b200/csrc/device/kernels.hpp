@@ -72,6 +72,7 @@ struct GemmArgs {
     int b_kmajor = 1;
     int symmetric_out = 0;      // rows==cols and C symmetric: compute upper tiles only
     int self_power = 1;         // epilogue value = C^self_power * W (2: the consumer read C twice)
+    int tri_colmajor = 0;       // symmetric tile list ordered by column (tiles of row panels <= tn first)
     long long tile_begin = 0;   // row sharding: this rank's contiguous range of the tile list
     long long tile_count = -1;  // -1 = every tile
     int accumulate = 0;         // outputs += (pre-zeroed), see StreamArgs::accumulate
@@ -121,6 +122,9 @@ std::size_t gemm_partial_entries(const GemmArgs& a);
 // Zero every entry of an order-`order` tensor whose multi-index repeats a
 // coordinate (tensor.cpp:54-76), in place.
 int launch_sparsify(double* data, int order, long long n, cudaStream_t s);
+// Zeroes the diagonal entries of rows [r0, r1) of an n x n matrix (a panel
+// of a chunked upload).
+int launch_zero_diagonal_rows(double* data, long long n, long long r0, long long r1, cudaStream_t s);
 // flag[0] = 0 if the n x n matrix is bitwise symmetric, else 1.
 int launch_symmetry_check(const double* data, long long n, int* flag, cudaStream_t s);
 

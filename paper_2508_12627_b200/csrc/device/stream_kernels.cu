@@ -317,6 +317,12 @@ __global__ void zero_diagonal(double* d, long long n) {
         d[i * n + i] = 0.0;
 }
 
+__global__ void zero_diagonal_rows(double* d, long long n, long long r0, long long r1) {
+    for (long long i = r0 + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < r1;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        d[i * n + i] = 0.0;
+}
+
 __global__ void zero_repeated(double* d, int order, long long n, unsigned long long total) {
     for (unsigned long long flat = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
          flat < total; flat += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
@@ -358,6 +364,13 @@ int launch_sparsify(double* data, int order, long long n, cudaStream_t s) {
     unsigned long long blocks = (total + 255) / 256;
     if (blocks > 148ull * 32) blocks = 148ull * 32;
     zero_repeated<<<static_cast<unsigned>(blocks), 256, 0, s>>>(data, order, n, total);
+    return 1;
+}
+
+int launch_zero_diagonal_rows(double* data, long long n, long long r0, long long r1, cudaStream_t s) {
+    if (r1 <= r0) return 0;
+    const long long blocks = (r1 - r0 + 255) / 256;
+    zero_diagonal_rows<<<static_cast<unsigned>(blocks < 1024 ? blocks : 1024), 256, 0, s>>>(data, n, r0, r1);
     return 1;
 }
 

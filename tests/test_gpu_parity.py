@@ -268,3 +268,22 @@ def test_row_sharding_single_rank_nccl(engine):
     base = engine.u_statistic_tensors(factors, sig, m)
     got = engine.u_statistic_tensors(factors, sig, m, engine.Config(shard_rows=True, world_size=1))
     assert got == base
+
+
+def test_panel_upload_speculation(engine):
+    # host matrices >= 2048 upload in row panels overlapped with the first
+    # symmetric GEMM; the second call with the same host buffer speculates on
+    # symmetry, and a buffer that stopped being symmetric is caught and redone
+    from paper_2508_12627_b200.workloads import generate
+    factors, sig, m, _ = generate("C2", 2304)
+    first = engine.u_terms(factors, sig, m)
+    again = engine.u_terms(factors, sig, m)      # speculative path
+    assert np.array_equal(first.v, again.v)
+    a = factors[0]
+    a[5, 7] += 1.0                               # same pointer, now asymmetric
+    fresh = engine.u_terms([a.copy()] * 4, sig, m)  # new pointer: probed before planning
+    spec = engine.u_terms(factors, sig, m)       # stale cache: mispredicts, recomputes
+    scale = np.max(np.abs(fresh.v))
+    assert np.max(np.abs(spec.v - fresh.v)) <= TOL * scale
+    _, rows = O.u_statistic([a] * 4, sig, m)
+    assert abs(spec.value - O.combine([r[1] for r in rows], [r[2] for r in rows])) <= TOL * scale
