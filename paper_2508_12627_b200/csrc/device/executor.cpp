@@ -59,6 +59,8 @@ Runtime::Runtime(int device) : device_(device) {
     check_cuda(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, hi_prio), "cudaStreamCreate");
     check_cuda(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, lo_prio), "cudaStreamCreate");
     check_cuda(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking), "cudaStreamCreate");
+    check_cuda(cudaStreamCreateWithPriority(&prep_, cudaStreamNonBlocking, hi_prio), "cudaStreamCreate");
+    for (auto& c : chunk_) check_cuda(cudaStreamCreateWithPriority(&c, cudaStreamNonBlocking, hi_prio), "cudaStreamCreate");
     cur_ = stream_;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -110,7 +112,9 @@ void Runtime::release(double* p) {
 }
 
 void Runtime::sync() {
+    for (auto& c : chunk_) check_cuda(cudaStreamSynchronize(c), "cudaStreamSynchronize");
     check_cuda(cudaStreamSynchronize(copy_), "cudaStreamSynchronize");
+    check_cuda(cudaStreamSynchronize(prep_), "cudaStreamSynchronize");
     check_cuda(cudaStreamSynchronize(side_), "cudaStreamSynchronize");
     check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
 }
@@ -967,29 +971,89 @@ void Program::run_gemm(const Op& op, double* out) {
         if (!chunked) {
             launched = launch_gemm_multi(g, set, rt_->stream());
         } else {
+            // Pieces run concurrently on the chunk streams (a piece smaller than
+            // one wave must not serialize the next); reductions land in
+            // per-piece slots combined in piece order afterwards; stores are
+            // disjoint tiles accumulated into the zeroed output.
+            cudaStream_t main = rt_->stream();
             for (int q = 0; q < set.count; ++q)
                 if (set.d[q].mode == kEpiStore)
                     check_cuda(cudaMemsetAsync(set.d[q].out, 0, static_cast<std::size_t>(g.rows * g.cols) * sizeof(double),
-                                               rt_->stream()),
+                                               main),
                                "memset");
             const long long tiles_n = (g.rows + 127) / 128;
+            std::vector<std::pair<long long, cudaEvent_t>> pieces;
             long long prev = 0;
-            launched = 0;
-            g.tri_colmajor = 1;
-            g.accumulate = 1;
             for (const auto& [rows_ready, ev] : src->ready) {
                 const long long k = rows_ready >= g.rows ? tiles_n : rows_ready / 128;
-                if (k <= prev) continue;
-                check_cuda(cudaStreamWaitEvent(rt_->stream(), ev, 0), "wait panel");
-                if (scratch) check_cuda(cudaMemsetAsync(scratch, 0, part_total * sizeof(double), rt_->stream()), "memset");
-                g.tile_begin = prev * (prev + 1) / 2;
-                g.tile_count = k * (k + 1) / 2 - g.tile_begin;
-                const int l = launch_gemm_multi(g, set, rt_->stream());
-                if (l < 0) break;
-                launched += l;
-                prev = k;
+                if (k > prev) {
+                    pieces.emplace_back(k, ev);
+                    prev = k;
+                }
             }
-            if (prev < tiles_n) launched = -1;
+            const int C = static_cast<int>(pieces.size());
+            auto out_len = [&](int mode) -> long long {
+                return mode == kEpiSumAll ? 1 : mode == kEpiSumCols ? g.rows : mode == kEpiSumRows ? g.cols : 0;
+            };
+            // slots of epilogue q: [q][piece][len_q]
+            std::vector<std::size_t> base(static_cast<std::size_t>(set.count) + 1, 0);
+            for (int q = 0; q < set.count; ++q)
+                base[static_cast<std::size_t>(q) + 1] =
+                    base[static_cast<std::size_t>(q)] + static_cast<std::size_t>(out_len(set.d[q].mode)) * C;
+            const std::size_t slot_total = base.back();
+            double* slots = slot_total ? rt_->scratch(slot_total) : nullptr;
+            double* parts = part_total ? rt_->scratch(part_total * static_cast<std::size_t>(C)) : nullptr;
+            if (slots) check_cuda(cudaMemsetAsync(slots, 0, slot_total * sizeof(double), main), "memset");
+            if (parts) check_cuda(cudaMemsetAsync(parts, 0, part_total * C * sizeof(double), main), "memset");
+            cudaEvent_t start;
+            check_cuda(cudaEventCreateWithFlags(&start, cudaEventDisableTiming), "event");
+            check_cuda(cudaEventRecord(start, main), "event");
+            std::vector<cudaEvent_t> finished;
+            long long lo = 0;
+            launched = 0;
+            for (int c = 0; c < C; ++c) {
+                cudaStream_t cs = rt_->chunk_stream(c);
+                check_cuda(cudaStreamWaitEvent(cs, start, 0), "wait");
+                check_cuda(cudaStreamWaitEvent(cs, pieces[static_cast<std::size_t>(c)].second, 0), "wait panel");
+                EpiSet piece = set;
+                std::size_t po = 0;
+                for (int q = 0; q < piece.count; ++q) {
+                    EpiDesc& d = piece.d[q];
+                    const long long len = out_len(d.mode);
+                    if (len > 0) d.out = slots + base[static_cast<std::size_t>(q)] + static_cast<std::size_t>(c * len);
+                    d.partial = parts ? parts + static_cast<std::size_t>(c) * part_total + po : nullptr;
+                    po += gemm_epi_partial_entries(g, d.mode);
+                }
+                const long long k = pieces[static_cast<std::size_t>(c)].first;
+                GemmArgs gc = g;
+                gc.tri_colmajor = 1;
+                gc.tile_begin = lo * (lo + 1) / 2;
+                gc.tile_count = k * (k + 1) / 2 - gc.tile_begin;
+                gc.accumulate = 1;  // stores: disjoint tiles into the zeroed output; slots are zeroed
+                const int l = launch_gemm_multi(gc, piece, cs);
+                if (l < 0) {
+                    launched = -1;
+                    break;
+                }
+                launched += l;
+                cudaEvent_t done;
+                check_cuda(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "event");
+                check_cuda(cudaEventRecord(done, cs), "event");
+                finished.push_back(done);
+                lo = k;
+            }
+            for (cudaEvent_t e : finished) {
+                check_cuda(cudaStreamWaitEvent(main, e, 0), "wait piece");
+                cudaEventDestroy(e);
+            }
+            cudaEventDestroy(start);
+            for (int q = 0; q < set.count && launched >= 0; ++q) {
+                const long long len = out_len(set.d[q].mode);
+                if (len > 0)
+                    launched += launch_sum_slices(slots + base[static_cast<std::size_t>(q)], C, len, set.d[q].out, 0, main);
+            }
+            rt_->release(slots);
+            rt_->release(parts);
         }
         rt_->end(Runtime::kGemm);
         if (launched < 0) fail(ErrorCode::InvalidArgument, "executor: fused GEMM lost TMA eligibility");
@@ -1592,14 +1656,22 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
     if (config.device.exploit_symmetry)
         check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&flags), sizeof(int) * total_factors + 4, rt.stream()),
                    "alloc flags");
+    for (std::size_t q = 0; q < specs.size(); ++q) tensors[q].assign(specs[q].sig.size(), nullptr);
+    // Small host inputs go first: H2D copies share the copy engines in issue
+    // order, so a vector queued behind a matrix's panels would hold the
+    // main stream until the whole matrix landed.
+    for (int pass = 0; pass < 2; ++pass)
     for (std::size_t q = 0; q < specs.size(); ++q) {
         const StatisticSpec& sp = specs[q];
         for (std::size_t k = 0; k < sp.sig.size(); ++k) {
             const int order = static_cast<int>(sp.sig[k].size());
+            const bool big = !inputs_on_device && order == 2 && n >= kChunkMinN;
+            if (pass == 0 && big) continue;
+            if (pass == 1 && !big) continue;
             checked_entry_count(order, static_cast<int>(n), config);
             auto hit = by_ptr.find(sp.inputs[k]);
             if (hit != by_ptr.end() && hit->second->order == order) {
-                tensors[q].push_back(hit->second);
+                tensors[q][k] = hit->second;
                 continue;
             }
             Buf b;
@@ -1621,12 +1693,19 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
                                                static_cast<std::size_t>((r1 - r0) * n) * sizeof(double),
                                                cudaMemcpyHostToDevice, rt.copy_stream()),
                                "upload panel");
+                    // the copy stream carries copies only (a kernel there would wait
+                    // for an SM held by the GEMM and stall the next copy); the panel
+                    // is sparsified on the high-priority prep stream
+                    cudaEvent_t landed, ev;
+                    check_cuda(cudaEventCreateWithFlags(&landed, cudaEventDisableTiming), "event");
+                    check_cuda(cudaEventRecord(landed, rt.copy_stream()), "event");
+                    check_cuda(cudaStreamWaitEvent(rt.prep_stream(), landed, 0), "wait");
+                    cudaEventDestroy(landed);
                     if (mode == LatticeMode::Sparsified)
                         upload_stats.kernel_launches +=
-                            static_cast<std::uint64_t>(launch_zero_diagonal_rows(b->ptr, n, r0, r1, rt.copy_stream()));
-                    cudaEvent_t ev;
+                            static_cast<std::uint64_t>(launch_zero_diagonal_rows(b->ptr, n, r0, r1, rt.prep_stream()));
                     check_cuda(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
-                    check_cuda(cudaEventRecord(ev, rt.copy_stream()), "event");
+                    check_cuda(cudaEventRecord(ev, rt.prep_stream()), "event");
                     b->ready.emplace_back(r1, ev);
                 }
             } else {
@@ -1643,12 +1722,16 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
                 int* f = flags + probes.size();
                 const auto key = std::make_pair(static_cast<const void*>(sp.inputs[k]), n);
                 auto seen = rt.symmetry_seen.find(key);
+                if (std::getenv("USTATS_TRACE"))
+                    std::fprintf(stderr, "[trace] input %p n=%lld panels=%d seen=%d sym=%d\n", static_cast<const void*>(sp.inputs[k]),
+                                 n, panels ? 1 : 0, seen != rt.symmetry_seen.end() ? 1 : 0,
+                                 seen != rt.symmetry_seen.end() && seen->second ? 1 : 0);
                 if (panels && speculate && seen != rt.symmetry_seen.end() && seen->second) {
                     // speculate (the same host matrix was symmetric last time):
                     // plan now, verify with a probe queued behind the upload
                     b->symmetric = true;
                     upload_stats.kernel_launches +=
-                        static_cast<std::uint64_t>(launch_symmetry_check(b->ptr, n, f, rt.copy_stream()));
+                        static_cast<std::uint64_t>(launch_symmetry_check(b->ptr, n, f, rt.prep_stream()));
                     speculative.emplace_back(b, f, key);
                 } else {
                     if (panels) check_cuda(cudaStreamWaitEvent(rt.stream(), b->ready.back().second, 0), "wait upload");
@@ -1660,7 +1743,7 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
             }
             rt.end(Runtime::kOther);
             by_ptr[sp.inputs[k]] = b;
-            tensors[q].push_back(b);
+            tensors[q][k] = b;
         }
     }
     if (!probes.empty()) {
@@ -1671,8 +1754,10 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
         for (std::size_t i = 0; i < probes.size(); ++i) probes[i].first->symmetric = host[i] == 0;
         for (const auto& [key, idx] : probe_keys) rt.symmetry_seen[key] = host[static_cast<std::size_t>(idx)] == 0;
     }
+    const double enqueue_s = std::chrono::duration<double>(Clock::now() - t_up).count();
     check_cuda(cudaStreamSynchronize(rt.main_stream()), "sync");
     const double upload_s = std::chrono::duration<double>(Clock::now() - t_up).count();
+    const bool trace = std::getenv("USTATS_TRACE") != nullptr;
 
     const auto t0 = Clock::now();
     std::vector<TermPlan> plans;
@@ -1708,6 +1793,10 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
         prog.optimize(budget);
         plan_s = std::chrono::duration<double>(Clock::now() - t0).count();
         prog.execute();
+        if (trace)
+            std::fprintf(stderr, "[trace] upload-enqueue %.3f ms, upload-sync %.3f ms, plan %.3f ms, launch done %.3f ms\n",
+                         enqueue_s * 1e3, upload_s * 1e3, plan_s * 1e3,
+                         std::chrono::duration<double>(Clock::now() - t0).count() * 1e3);
     }
     // row sharding: every term value is a sum of per-rank partials
     if (config.device.shard_rows && config.device.emulate_world <= 1 && rt.has_comm()) rt.allreduce_sum(d_v, T);
@@ -1715,13 +1804,18 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
     if (T) check_cuda(cudaMemcpyAsync(v.data(), d_v, sizeof(double) * T, cudaMemcpyDeviceToHost, rt.stream()), "D2H");
     rt.release(d_v);
     std::vector<int> spec_flags(speculative.size(), 0);
-    for (std::size_t i = 0; i < speculative.size(); ++i) {
-        check_cuda(cudaStreamWaitEvent(rt.main_stream(), std::get<0>(speculative[i])->ready.back().second, 0), "wait");
+    for (std::size_t i = 0; i < speculative.size(); ++i)  // in prep-stream order: after the probe itself
         check_cuda(cudaMemcpyAsync(&spec_flags[i], std::get<1>(speculative[i]), sizeof(int), cudaMemcpyDeviceToHost,
-                                   rt.main_stream()),
+                                   rt.prep_stream()),
                    "D2H flag");
+    if (flags) {
+        cudaEvent_t probed;
+        check_cuda(cudaEventCreateWithFlags(&probed, cudaEventDisableTiming), "event");
+        check_cuda(cudaEventRecord(probed, rt.prep_stream()), "event");
+        check_cuda(cudaStreamWaitEvent(rt.main_stream(), probed, 0), "wait");
+        cudaEventDestroy(probed);
+        cudaFreeAsync(flags, rt.main_stream());
     }
-    if (flags) cudaFreeAsync(flags, rt.main_stream());
     tensors.clear();
     by_ptr.clear();
     probes.clear();
@@ -1736,6 +1830,7 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
     if (mispredicted)  // the host matrix changed and is no longer symmetric: redo without speculation
         return lattice_batch_impl(specs, inputs_on_device, n, mode, config, false);
     const double contract_s = std::chrono::duration<double>(Clock::now() - t0).count();
+    if (trace) std::fprintf(stderr, "[trace] contract total %.3f ms\n", contract_s * 1e3);
 
     std::size_t at = 0;
     for (std::size_t q = 0; q < specs.size(); ++q) {

@@ -67,6 +67,9 @@ class Runtime {
     cudaStream_t main_stream() const { return stream_; }
     cudaStream_t side_stream() const { return side_; }
     cudaStream_t copy_stream() const { return copy_; }
+    cudaStream_t prep_stream() const { return prep_; }
+    static constexpr int kChunkStreams = 4;
+    cudaStream_t chunk_stream(int i) const { return chunk_[i % kChunkStreams]; }
     // bitwise-symmetry results of host inputs seen before (speculation key)
     std::map<std::pair<const void*, long long>, bool> symmetry_seen;
     void set_stream(cudaStream_t s) { cur_ = s; }
@@ -103,7 +106,9 @@ class Runtime {
     int sm_count_ = 148;
     cudaStream_t stream_ = nullptr;
     cudaStream_t side_ = nullptr;  // second stream: bandwidth ops overlap GEMM tails
-    cudaStream_t copy_ = nullptr;  // chunked host->device uploads
+    cudaStream_t copy_ = nullptr;  // chunked host->device uploads (copies only: never waits for an SM)
+    cudaStream_t prep_ = nullptr;  // per-panel sparsify / probe kernels behind the copies (high priority)
+    cudaStream_t chunk_[kChunkStreams] = {};  // concurrent per-panel GEMM pieces
     cudaStream_t cur_ = nullptr;
     void* comm_ = nullptr;
     int comm_world_ = 1;

@@ -122,6 +122,9 @@ std::size_t gemm_partial_entries(const GemmArgs& a);
 // Zero every entry of an order-`order` tensor whose multi-index repeats a
 // coordinate (tensor.cpp:54-76), in place.
 int launch_sparsify(double* data, int order, long long n, cudaStream_t s);
+// out[i] (+)= sum_{c < C} slices[c * len + i], c in order (deterministic
+// combine of per-chunk reductions).
+int launch_sum_slices(const double* slices, int C, long long len, double* out, int accumulate, cudaStream_t s);
 // Zeroes the diagonal entries of rows [r0, r1) of an n x n matrix (a panel
 // of a chunked upload).
 int launch_zero_diagonal_rows(double* data, long long n, long long r0, long long r1, cudaStream_t s);

@@ -367,6 +367,22 @@ int launch_sparsify(double* data, int order, long long n, cudaStream_t s) {
     return 1;
 }
 
+namespace {
+__global__ void sum_slices(const double* slices, int C, long long len, double* out, int accumulate) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= len) return;
+    double acc = 0.0;
+    for (int c = 0; c < C; ++c) acc += slices[c * len + i];
+    out[i] = (accumulate ? out[i] : 0.0) + acc;
+}
+}  // namespace
+
+int launch_sum_slices(const double* slices, int C, long long len, double* out, int accumulate, cudaStream_t s) {
+    if (len <= 0) return 0;
+    sum_slices<<<static_cast<unsigned>((len + 255) / 256), 256, 0, s>>>(slices, C, len, out, accumulate);
+    return 1;
+}
+
 int launch_zero_diagonal_rows(double* data, long long n, long long r0, long long r1, cudaStream_t s) {
     if (r1 <= r0) return 0;
     const long long blocks = (r1 - r0 + 255) / 256;
