@@ -1783,12 +1783,19 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
         }
         double budget = static_cast<double>(config.device.memory_budget_bytes);
         if (budget <= 0) {
-            std::size_t free_b = 0, total_b = 0;
-            check_cuda(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+            // cudaMemGetInfo stalls for milliseconds at times (measured: up to
+            // 69 ms): query only for programs whose footprint could matter
             double in_bytes = 0;
             for (const auto& kv : by_ptr) in_bytes += 8.0 * static_cast<double>(kv.second->entries());
-            // inputs are already resident: the program may use what is free, minus headroom
-            budget = in_bytes + 0.94 * static_cast<double>(free_b) - 2.0e9;
+            const double n2 = 8.0 * static_cast<double>(n) * static_cast<double>(n);
+            if (n2 * 8 + in_bytes < 16.0e9) {
+                budget = 0;  // unbounded: far below any B200's memory
+            } else {
+                std::size_t free_b = 0, total_b = 0;
+                check_cuda(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+                // inputs are already resident: the program may use what is free, minus headroom
+                budget = in_bytes + 0.94 * static_cast<double>(free_b) - 2.0e9;
+            }
         }
         prog.optimize(budget);
         plan_s = std::chrono::duration<double>(Clock::now() - t0).count();
