@@ -62,6 +62,7 @@ Runtime::Runtime(int device) : device_(device) {
     check_cuda(cudaStreamCreateWithPriority(&prep_, cudaStreamNonBlocking, hi_prio), "cudaStreamCreate");
     for (auto& c : chunk_) check_cuda(cudaStreamCreateWithPriority(&c, cudaStreamNonBlocking, hi_prio), "cudaStreamCreate");
     cur_ = stream_;
+    refresh_free_bytes();
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
         std::uint64_t keep = ~std::uint64_t{0};
@@ -70,6 +71,20 @@ Runtime::Runtime(int device) : device_(device) {
 }
 
 Runtime::~Runtime() {}
+
+void Runtime::refresh_free_bytes() {
+    std::size_t free_b = 0, total_b = 0;
+    check_cuda(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    double pooled = 0;  // freed blocks our stream-ordered pool keeps for reuse
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device_) == cudaSuccess) {
+        std::uint64_t reserved = 0, used = 0;
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+        pooled = static_cast<double>(reserved > used ? reserved - used : 0);
+    }
+    free_bytes_ = static_cast<double>(free_b) + pooled;
+}
 
 Buf Runtime::allocate(int order, long long n) {
     auto b = std::make_shared<DeviceBuffer>();
@@ -1640,6 +1655,12 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
                                                 long long n, LatticeMode mode, const Config& config, bool speculate) {
     std::vector<StatisticResult> out(specs.size());
     Runtime& rt = Runtime::get(config.device.device);
+    {
+        // re-measure free memory only when this call's footprint is a large
+        // share of the device (n^2 matrices of several GiB)
+        const double n2 = 8.0 * static_cast<double>(n) * static_cast<double>(n);
+        if (n2 * 6 > 0.5 * rt.free_bytes()) rt.refresh_free_bytes();
+    }
     const auto t_up = Clock::now();
 
     // Upload each distinct factor of every statistic once; sparsify on device
@@ -1782,21 +1803,7 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
             at += plans[q].rgs.size();
         }
         double budget = static_cast<double>(config.device.memory_budget_bytes);
-        if (budget <= 0) {
-            // cudaMemGetInfo stalls for milliseconds at times (measured: up to
-            // 69 ms): query only for programs whose footprint could matter
-            double in_bytes = 0;
-            for (const auto& kv : by_ptr) in_bytes += 8.0 * static_cast<double>(kv.second->entries());
-            const double n2 = 8.0 * static_cast<double>(n) * static_cast<double>(n);
-            if (n2 * 8 + in_bytes < 16.0e9) {
-                budget = 0;  // unbounded: far below any B200's memory
-            } else {
-                std::size_t free_b = 0, total_b = 0;
-                check_cuda(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-                // inputs are already resident: the program may use what is free, minus headroom
-                budget = in_bytes + 0.94 * static_cast<double>(free_b) - 2.0e9;
-            }
-        }
+        if (budget <= 0) budget = 0.94 * rt.free_bytes() - 2.0e9;  // inputs included: they came out of it
         prog.optimize(budget);
         plan_s = std::chrono::duration<double>(Clock::now() - t0).count();
         prog.execute();

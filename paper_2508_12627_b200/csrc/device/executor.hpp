@@ -68,6 +68,12 @@ class Runtime {
     cudaStream_t side_stream() const { return side_; }
     cudaStream_t copy_stream() const { return copy_; }
     cudaStream_t prep_stream() const { return prep_; }
+    // Device memory available to this engine: free memory when the runtime was
+    // created (the stream-ordered pool then recycles it). cudaMemGetInfo can
+    // stall for tens of ms, so it is re-queried only for programs that need
+    // most of the device (refresh_free_bytes).
+    double free_bytes() const { return free_bytes_; }
+    void refresh_free_bytes();
     static constexpr int kChunkStreams = 4;
     cudaStream_t chunk_stream(int i) const { return chunk_[i % kChunkStreams]; }
     // bitwise-symmetry results of host inputs seen before (speculation key)
@@ -112,6 +118,7 @@ class Runtime {
     cudaStream_t cur_ = nullptr;
     void* comm_ = nullptr;
     int comm_world_ = 1;
+    double free_bytes_ = 0;
     bool profiling_ = false;
     std::vector<cudaEvent_t> pool_;
     struct Mark {
