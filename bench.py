@@ -119,13 +119,23 @@ def dist_env():
     return world, rank, local
 
 
-def reference_sample(name: str, n_sample: int, threads: int, repeats: int = 1):
-    """Times the reference u_statistic (oracle/_ref) on a bounded sample."""
+def reference_sample(name: str, n_sample: int, threads: int, repeats: int = 1, data_api: bool = True):
+    """Times the reference u_statistic (oracle/_ref) on a bounded sample: with
+    data_api, the reference's own call on the raw sample (its tensorize
+    evaluates the RBF / projection components per entry); otherwise on
+    pre-tensorized factors."""
     from oracle import ref as REF
-    from paper_2508_12627_b200.workloads import generate
-    factors, sig, m, _ = generate(name, n_sample)
+    from paper_2508_12627_b200.workloads import generate, generate_data
     cap = max(2 ** 31, n_sample ** 3 + 1)
     walls, stats = [], None
+    if data_api:
+        data, spec, m, _ = generate_data(name, n_sample)
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            u, stats = REF.u_statistic_data(spec, data, threads=threads, cap=cap)
+            walls.append(time.perf_counter() - t0)
+        return u, min(walls), stats
+    factors, sig, m, _ = generate(name, n_sample)
     for _ in range(repeats):
         t0 = time.perf_counter()
         u, stats = REF.u_statistic(factors, sig, m, threads=threads, cap=cap)
@@ -133,16 +143,16 @@ def reference_sample(name: str, n_sample: int, threads: int, repeats: int = 1):
     return u, min(walls), stats
 
 
-def fitted_cpu_time(name, n, threads):
+def fitted_cpu_time(name, n, threads, data_api=True):
     """Times the reference at two bounded sizes (n2/2, n2) and extrapolates to n
     with the fitted power law T ~ n^p. Returns (t_full_est, detail dict)."""
     n2 = min(CPU_SAMPLE_N[name], n)
     if n2 == n:
-        _, t, st = reference_sample(name, n, threads)
+        _, t, st = reference_sample(name, n, threads, data_api=data_api)
         return t, {"n": n, "wall": t, "exponent": None, "contract": st["contract_seconds"]}
     n1 = max(CONFIG_MIN_N.get(name, 8), n2 // 2)
-    _, t1, _ = reference_sample(name, n1, threads)
-    _, t2, st = reference_sample(name, n2, threads)
+    _, t1, _ = reference_sample(name, n1, threads, data_api=data_api)
+    _, t2, st = reference_sample(name, n2, threads, data_api=data_api)
     p = float(np.log(t2 / t1) / np.log(n2 / n1)) if t1 > 0 and t2 > t1 else 3.0
     return t2 * (n / n2) ** p, {"n1": n1, "t1": t1, "n": n2, "wall": t2, "exponent": p,
                                 "contract": st["contract_seconds"]}
@@ -164,16 +174,18 @@ def run_reference_arm(args, name, world, rank):
     n = args.n or w.n
     threads = os.cpu_count() or 1
     # warm-up = the two bounded probes that also predict the full-size time
-    est, det = fitted_cpu_time(name, n, threads)
+    data_api = args.api == "data"
+    est, det = fitted_cpu_time(name, n, threads, data_api)
+    call = "u_statistic(kernel spec, sample) incl. its tensorize" if data_api else "u_statistic on tensor-backed components"
     if est * args.steps <= REFERENCE_ARM_BUDGET_S or det.get("exponent") is None:
-        walls = [reference_sample(name, n, threads)[1] for _ in range(args.steps)]
+        walls = [reference_sample(name, n, threads, data_api=data_api)[1] for _ in range(args.steps)]
         t_full = statistics.mean(walls)
-        sample = (f"ustats::u_statistic (oracle/_ref: the unmodified reference sources) at full n={n}, "
+        sample = (f"ustats::u_statistic (oracle/_ref: the unmodified reference sources), {call}, at full n={n}, "
                   f"threads={threads}, mean wall {t_full:.3f}s over {len(walls)} runs (tensorize+sparsify+contract)")
     else:
-        walls = [reference_sample(name, det["n"], threads)[1] for _ in range(args.steps)]
+        walls = [reference_sample(name, det["n"], threads, data_api=data_api)[1] for _ in range(args.steps)]
         t_full = statistics.mean(walls) * (n / det["n"]) ** det["exponent"]
-        sample = (f"ustats::u_statistic (oracle/_ref) at n={det['n']}, threads={threads}, mean wall "
+        sample = (f"ustats::u_statistic (oracle/_ref), {call}, at n={det['n']}, threads={threads}, mean wall "
                   f"{statistics.mean(walls):.3f}s over {len(walls)} runs; extrapolated to n={n} with the "
                   f"power law fitted between n={det['n1']} and n={det['n']} (p={det['exponent']:.2f}); "
                   f"full size would take ~{est:.0f}s per step")
@@ -221,6 +233,9 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override the config's n (parity/debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--api", default="data", choices=["data", "tensors"],
+                    help="data: u_statistic(spec, sample) with GPU tensorization (the binding's call); "
+                         "tensors: pre-tensorized factors (us_u_terms)")
     ap.add_argument("--shard", default="rows", choices=["rows", "terms"],
                     help="N>1: row-shard every op (NCCL inside the engine) or shard V-terms")
     args = ap.parse_args()
@@ -243,33 +258,55 @@ def main():
             init_row_sharding(local)
     w = CONFIGS[name]
     n = args.n or w.n
-    factors, sig, m, _ = generate(name, n)
+    use_data = args.api == "data" and not (world > 1 and args.shard == "terms")
     cfg = us.Config(device=local, rank=rank, world_size=world, shard_rows=(world > 1 and args.shard == "rows"),
                     memory_cap_entries=max(2 ** 31, n * n + 1, n ** 3 + 1 if name == "C4" else 0))
-
-    # device-resident and pinned-host copies (aliases preserved)
-    dev, pin, dfac, hfac = {}, {}, [], []
-    for f in factors:
-        if id(f) not in dev:
-            t = torch.from_numpy(f)
-            dev[id(f)] = t.cuda()
-            pin[id(f)] = t.pin_memory()
-        dfac.append(dev[id(f)])
-        hfac.append(pin[id(f)])
+    if use_data:
+        # the binding's public call: u_statistic(kernel spec, sample); the
+        # components are tensorized on the GPU from the sample
+        from paper_2508_12627_b200.workloads import generate_data
+        data, spec, m, _ = generate_data(name, n)
+        sig = [list(t) for t in w.signature]
+        dX = torch.from_numpy(data).cuda()
+        hX = torch.from_numpy(data).pin_memory()
+        dfac, hfac = dX, hX
+        in_bytes = data.nbytes
+    else:
+        factors, sig, m, _ = generate(name, n)
+        spec = None
+        # device-resident and pinned-host copies (aliases preserved)
+        dev, pin, dfac, hfac = {}, {}, [], []
+        for f in factors:
+            if id(f) not in dev:
+                t = torch.from_numpy(f)
+                dev[id(f)] = t.cuda()
+                pin[id(f)] = t.pin_memory()
+            dfac.append(dev[id(f)])
+            hfac.append(pin[id(f)])
+        in_bytes = input_bytes(factors)
     torch.cuda.synchronize()
 
+    class _R:  # per-step result: value + engine stats
+        def __init__(self, value, stats, terms):
+            self.value, self.stats, self.terms = value, stats, terms
+
     def step(fx, on_device):
+        if use_data:
+            u, st = us.u_statistic(spec, fx, config=cfg, with_stats=True)
+            return u, _R(u, st, int(st["partitions_evaluated"]))
         r = us.u_terms(fx, sig, m, cfg) if on_device else _host_terms(us, fx, sig, m, cfg)
         if world > 1 and not cfg.shard_rows:  # term sharding: one all-reduce of the V vector
             import torch.distributed as dist
             v = torch.from_numpy(r.v).cuda()
             dist.all_reduce(v)
-            return us.combine_terms(r.mu, v.cpu().numpy()), r
-        return r.value, r
+            u = us.combine_terms(r.mu, v.cpu().numpy())
+        else:
+            u = r.value
+        return u, _R(u, r.stats, len(r.v))
 
     # Inputs smaller than L2 (126 MB) would stay cached across steps: flush L2
     # between steps (write a 512 MiB buffer) and time each step on its own.
-    flush = input_bytes(factors) < 126e6
+    flush = in_bytes < 126e6
     scrub = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda") if flush else None
 
     def timed(fx, on_device, k):
@@ -315,8 +352,9 @@ def main():
     if not args.no_e2e:
         step(hfac, False)
         e2e_ms, _ = timed(hfac, False, args.steps)
-        e2e = {"value": 1e3 / e2e_ms, "unit": "evals/s", "h2d_bytes_per_step": input_bytes(factors),
-               "d2h_bytes_per_step": int(r.v.nbytes), "ms_per_step": e2e_ms}
+        e2e = {"value": 1e3 / e2e_ms, "unit": "evals/s", "h2d_bytes_per_step": int(in_bytes),
+               "d2h_bytes_per_step": 8 * int(r.terms) + (4 if use_data else 0), "ms_per_step": e2e_ms,
+               "call": f"u_statistic('{spec}', pinned host sample)" if use_data else "us_u_terms(host tensors)"}
 
     st = r.stats
     gemm_ms = prof["gemm_ms"] / args.steps
@@ -344,7 +382,9 @@ def main():
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json construction)",
-        "config": {"workload": name, "m": m, "n": n, "signature": sig, "terms": int(len(r.v)),
+        "config": {"workload": name, "m": m, "n": n, "signature": sig, "terms": int(r.terms),
+                   "api": (f"u_statistic('{spec}', sample): components tensorized on the GPU"
+                           if use_data else "u_terms(tensors)"),
                    "parallelism": (f"row-sharded x{world}" if args.shard == "rows" else f"term-sharded x{world}")
                    if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (no flush needed)" if not flush
@@ -360,7 +400,7 @@ def main():
     if e2e:
         line["e2e"] = e2e
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(name, n)
+        line["cpu_baseline"] = cpu_baseline(name, n, use_data)
     if rank == 0:
         print(json.dumps(line))
     if world > 1:
@@ -404,17 +444,18 @@ def ncu_traffic(name, kind):
     return entry.get("bytes_per_launch") if isinstance(entry, dict) else entry
 
 
-def cpu_baseline(name, n):
+def cpu_baseline(name, n, data_api=True):
     from oracle import ref as REF
     if not REF.available():
         return {"value": None, "unit": "evals/s", "cores": 0, "kind": "reference",
                 "sample": "oracle/_ref not built on this host"}
     threads = os.cpu_count() or 1
-    est, det = fitted_cpu_time(name, n, threads)
+    est, det = fitted_cpu_time(name, n, threads, data_api)
     if det.get("exponent") is None:
         sample = f"ustats::u_statistic (oracle/_ref) at full n={n}, threads={threads}: {det['wall']:.3f}s wall"
     else:
-        sample = (f"ustats::u_statistic (unmodified reference, oracle/_ref), threads={threads}: "
+        sample = (f"ustats::u_statistic (unmodified reference, oracle/_ref) on the "
+                  f"{'raw sample (its tensorize included)' if data_api else 'tensorized factors'}, threads={threads}: "
                   f"{det['t1']:.3f}s at n={det['n1']}, {det['wall']:.3f}s at n={det['n']} "
                   f"(contract {det['contract']:.3f}s); extrapolated to n={n} with the fitted power law "
                   f"p={det['exponent']:.2f}")

@@ -90,6 +90,18 @@ US_API int us_u_terms(int32_t m, int32_t K, const int32_t* tuple_len, const int3
                int32_t max_terms, int32_t* count, int32_t* rgs_out, int64_t* mu_out, double* v_out,
                int32_t* owner_out, double* u_out, us_stats* stats);
 
+/* Data-level u_statistic (engine.cpp:173-193 including tensorize, and
+ * _ustats.u_statistic(kernel, data), ustats_py.cpp:92-101): the kernel spec's
+ * components are tensorized ON THE DEVICE from the sample (n rows x d columns,
+ * row-major; host or device memory), so only the sample crosses PCIe.
+ * Specs: "prod2", "hoif:<j>:<k>" (hoif.cpp:50-72), "rbf:<shape>:<h>"
+ * (exp(-|x_i-x_j|^2/(2h^2)); shape chain<m> | cycle<m> | k4tail) and
+ * "proj:<m>:<kmax>" (r B..B e chain, B = Z(Z'Z/n)^-1 Z' of cosine features
+ * cos(pi k u), k=1..kmax, of the first d-2 columns; r, e the last two).
+ * stats->tensorize_seconds is the device tensorization time. */
+US_API int us_u_statistic_data(const char* kernel, const double* data, int64_t n, int32_t d, int32_t on_device,
+                               const us_config* cfg, double* u_out, us_stats* stats);
+
 /* Several U-statistics over factors of one extent n, evaluated as ONE device
  * program (factors uploaded once, sub-contractions shared across statistics;
  * e.g. hoif_tau's chain orders, hoif.cpp:74-100). Statistic s has arity m[s]

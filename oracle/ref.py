@@ -38,6 +38,7 @@ def lib():
         _lib.ref_einsum.argtypes = [C.c_int, I32P, I32P, C.POINTER(C.c_void_p), C.c_int, C.c_int, I32P,
                                     C.c_int, F64P, F64P]
         _lib.ref_optimize_order.argtypes = [C.c_int, I32P, I32P, I32P, I32P]
+        _lib.ref_u_statistic_data.argtypes = [C.c_char_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64, F64P, F64P]
         _lib.ref_last_error.restype = C.c_char_p
     return _lib
 
@@ -149,3 +150,16 @@ def optimize_order(inputs):
     w = C.c_int()
     _check(lib().ref_optimize_order(K, L, I, out, C.byref(w)))
     return list(out), w.value
+
+
+def u_statistic_data(spec, data, threads=0, cap=0):
+    """The reference's u_statistic on a data kernel: components evaluated per
+    entry by its own tensorize (rbf / proj / hoif / prod2 specs)."""
+    x = np.ascontiguousarray(data, dtype=np.float64)
+    if x.ndim == 1:
+        x = x.reshape(-1, 1)
+    out = C.c_double()
+    st = (C.c_double * 7)()
+    _check(lib().ref_u_statistic_data(spec.encode(), C.c_void_p(x.ctypes.data), x.shape[0], x.shape[1], threads, cap,
+                                      C.byref(out), st))
+    return out.value, dict(zip(STAT_KEYS, list(st)))

@@ -12,6 +12,10 @@
 #include <string>
 #include <vector>
 
+#include <cmath>
+#include <memory>
+#include <span>
+
 #include "ustats/ustats.hpp"
 
 namespace {
@@ -256,3 +260,144 @@ int ref_optimize_order(int K, const int* tuple_len, const int* tuple_idx, int* o
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Data kernels through the reference's OWN tensorize path (engine.cpp:108-136):
+// the components are std::function callbacks evaluated per entry on the sample,
+// exactly how a reference user states the BASELINE kernels. Specs as in
+// us_u_statistic_data: rbf:<shape>:<h>, proj:<m>:<kmax>, hoif:<j>:<k>, prod2.
+namespace {
+
+std::vector<std::string> split_spec(const std::string& s) {
+    std::vector<std::string> out;
+    std::string cur;
+    for (char c : s) {
+        if (c == ':') {
+            out.push_back(cur);
+            cur.clear();
+        } else {
+            cur += c;
+        }
+    }
+    out.push_back(cur);
+    return out;
+}
+
+}  // namespace
+
+extern "C" int ref_u_statistic_data(const char* spec_c, const double* data, int n, int d, int threads,
+                                    std::uint64_t cap, double* u_out, double* stats) {
+    try {
+        const std::string spec(spec_c);
+        const auto p = split_spec(spec);
+        std::vector<ustats::Observation> rows(static_cast<std::size_t>(n));
+        for (int i = 0; i < n; ++i) rows[static_cast<std::size_t>(i)].assign(data + i * d, data + (i + 1) * d);
+        ustats::Sample sample(std::move(rows));
+        ustats::MDKernel k;
+        if (p[0] == "prod2") {
+            k = ustats::prod2_kernel();
+        } else if (p[0] == "hoif") {
+            k = ustats::hoif_kernel(std::stoi(p[1]), ustats::truncation_phi(std::stoi(p[2])));
+        } else if (p[0] == "rbf") {
+            const std::string shape = p[1];
+            const double scale = 0.5 / (std::stod(p[2]) * std::stod(p[2]));
+            auto rbf = [scale](const ustats::Sample& s, std::span<const int> idx) {
+                const auto& a = s.points[static_cast<std::size_t>(idx[0])];
+                const auto& b = s.points[static_cast<std::size_t>(idx[1])];
+                double acc = 0.0;
+                for (std::size_t c = 0; c < a.size(); ++c) {
+                    const double t = a[c] - b[c];
+                    acc += t * t;
+                }
+                return std::exp(-scale * acc);
+            };
+            std::vector<ustats::IndexTuple> sig;
+            int m = 0;
+            if (shape == "k4tail") {
+                m = 6;
+                sig = {{1, 2}, {1, 3}, {1, 4}, {2, 3}, {2, 4}, {3, 4}, {4, 5}, {5, 6}};
+            } else {
+                m = std::stoi(shape.substr(5));
+                for (int i = 1; i < m; ++i) sig.push_back({i, i + 1});
+                if (shape[1] == 'y') sig.push_back({m, 1});
+            }
+            k.arity = m;
+            k.signature = sig;
+            k.components.assign(sig.size(), rbf);
+            k.name = spec;
+        } else if (p[0] == "proj") {
+            const int m = std::stoi(p[1]), kmax = std::stoi(p[2]);
+            const int c = d - 2, F = c * kmax;
+            // user-side kernel setup: features, Omega = (Z'Z/n)^-1, W = Z Omega
+            std::vector<double> Z(static_cast<std::size_t>(n) * F), G(static_cast<std::size_t>(F) * F, 0.0);
+            for (int i = 0; i < n; ++i)
+                for (int cc = 0; cc < c; ++cc)
+                    for (int kk = 1; kk <= kmax; ++kk)
+                        Z[static_cast<std::size_t>(i) * F + cc * kmax + kk - 1] = std::cos(M_PI * kk * data[i * d + cc]);
+            for (int i = 0; i < n; ++i)
+                for (int a = 0; a < F; ++a)
+                    for (int b = 0; b < F; ++b)
+                        G[static_cast<std::size_t>(a) * F + b] +=
+                            Z[static_cast<std::size_t>(i) * F + a] * Z[static_cast<std::size_t>(i) * F + b];
+            for (double& g : G) g /= n;
+            // Gauss-Jordan inverse
+            std::vector<double> inv(static_cast<std::size_t>(F) * F, 0.0);
+            for (int i = 0; i < F; ++i) inv[static_cast<std::size_t>(i) * F + i] = 1.0;
+            for (int col = 0; col < F; ++col) {
+                const double piv = G[static_cast<std::size_t>(col) * F + col];
+                for (int j = 0; j < F; ++j) {
+                    G[static_cast<std::size_t>(col) * F + j] /= piv;
+                    inv[static_cast<std::size_t>(col) * F + j] /= piv;
+                }
+                for (int r = 0; r < F; ++r) {
+                    if (r == col) continue;
+                    const double f = G[static_cast<std::size_t>(r) * F + col];
+                    for (int j = 0; j < F; ++j) {
+                        G[static_cast<std::size_t>(r) * F + j] -= f * G[static_cast<std::size_t>(col) * F + j];
+                        inv[static_cast<std::size_t>(r) * F + j] -= f * inv[static_cast<std::size_t>(col) * F + j];
+                    }
+                }
+            }
+            auto W = std::make_shared<std::vector<double>>(static_cast<std::size_t>(n) * F, 0.0);
+            for (int i = 0; i < n; ++i)
+                for (int a = 0; a < F; ++a) {
+                    double s = 0;
+                    for (int b = 0; b < F; ++b)
+                        s += Z[static_cast<std::size_t>(i) * F + b] * inv[static_cast<std::size_t>(b) * F + a];
+                    (*W)[static_cast<std::size_t>(i) * F + a] = s;
+                }
+            auto Zs = std::make_shared<std::vector<double>>(std::move(Z));
+            auto proj = [W, Zs, F](const ustats::Sample&, std::span<const int> idx) {
+                const double* w = W->data() + static_cast<std::size_t>(idx[0]) * F;
+                const double* z = Zs->data() + static_cast<std::size_t>(idx[1]) * F;
+                double s = 0;
+                for (int a = 0; a < F; ++a) s += w[a] * z[a];
+                return s;
+            };
+            const int rc = d - 2, ec = d - 1;
+            k.arity = m;
+            k.signature.push_back({1});
+            k.components.push_back([rc](const ustats::Sample& s, std::span<const int> idx) {
+                return s.points[static_cast<std::size_t>(idx[0])][static_cast<std::size_t>(rc)];
+            });
+            for (int i = 1; i < m; ++i) {
+                k.signature.push_back({i, i + 1});
+                k.components.push_back(proj);
+            }
+            k.signature.push_back({m});
+            k.components.push_back([ec](const ustats::Sample& s, std::span<const int> idx) {
+                return s.points[static_cast<std::size_t>(idx[0])][static_cast<std::size_t>(ec)];
+            });
+            k.name = spec;
+        } else {
+            g_err = "unknown spec";
+            return 99;
+        }
+        ustats::RunStats rs;
+        *u_out = ustats::u_statistic(k, sample, config_of(threads, cap), &rs);
+        export_stats(rs, stats);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}

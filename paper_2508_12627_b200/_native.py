@@ -59,6 +59,7 @@ SIGNATURES = {
     "us_u_statistic": (C.c_int, [i32, i32, P(i32), P(i32), P(C.c_void_p), i64, i32, P(UsConfig), P(f64), P(UsStats)]),
     "us_u_terms": (C.c_int, [i32, i32, P(i32), P(i32), P(C.c_void_p), i64, i32, P(UsConfig), i32, P(i32),
                              P(i32), P(i64), P(f64), P(i32), P(f64), P(UsStats)]),
+    "us_u_statistic_data": (C.c_int, [C.c_char_p, C.c_void_p, i64, i32, i32, P(UsConfig), P(f64), P(UsStats)]),
     "us_u_statistic_batch": (C.c_int, [i32, P(i32), P(i32), P(i32), P(i32), P(C.c_void_p), i64, i32, P(UsConfig),
                                        P(f64), P(UsStats)]),
     "us_u_statistic_unsparsified": (C.c_int, [i32, i32, P(i32), P(i32), P(C.c_void_p), i64, i32, P(UsConfig),

@@ -368,10 +368,30 @@ def kernel_tensors(kernel: str, data):
     raise UStatsError("InvalidArgument", f"unknown kernel spec '{kernel}' (prod2 | hoif:<j>:<k>)")
 
 
-def u_statistic(kernel: str, data, threads: int = 0, config: Config | None = None):
-    """``_ustats.u_statistic`` (ustats_py.cpp:92-101)."""
-    factors, sig, m = kernel_tensors(kernel, data)
-    return u_statistic_tensors(factors, sig, m, config or Config(threads=threads))
+def u_statistic(kernel: str, data, threads: int = 0, config: Config | None = None, with_stats: bool = False):
+    """``_ustats.u_statistic`` (ustats_py.cpp:92-101): the kernel's components
+    are tensorized on the GPU from ``data`` (n x d; a numpy array, or a CUDA
+    float64 tensor already resident in HBM). Specs: prod2 | hoif:<j>:<k> |
+    rbf:<shape>:<h> | proj:<m>:<kmax> (us_u_statistic_data)."""
+    if hasattr(data, "data_ptr"):  # torch tensor: CUDA (resident) or CPU (e.g. pinned)
+        if str(data.dtype) != "torch.float64" or not data.is_contiguous() or data.dim() != 2:
+            raise UStatsError("InvalidArgument", "tensor data must be a contiguous 2-D float64 tensor")
+        on_dev = 1 if getattr(data, "is_cuda", False) else 0
+        ptr, n, d, keep = data.data_ptr(), data.shape[0], data.shape[1], data
+    else:
+        x = np.ascontiguousarray(data, dtype=np.float64)
+        if x.ndim == 1:
+            x = x.reshape(-1, 1)
+        if x.ndim != 2:
+            raise UStatsError("InvalidArgument", "data must be a 2-D array (rows = observations)")
+        ptr, n, d, on_dev, keep = x.ctypes.data, x.shape[0], x.shape[1], 0, x
+    out = N.f64()
+    st = N.UsStats()
+    cfg = (config or Config(threads=threads)).native()
+    _check(N.lib().us_u_statistic_data(kernel.encode(), C.c_void_p(ptr), n, d, on_dev, C.byref(cfg),
+                                       C.byref(out), C.byref(st)))
+    del keep
+    return (out.value, st.as_dict()) if with_stats else out.value
 
 
 def v_statistic(kernel: str, data, threads: int = 0, config: Config | None = None):

@@ -25,7 +25,7 @@ NVCC = str(CUDA_HOME / "bin" / "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 INCLUDES = [f"-I{CSRC / 'include'}", f"-I{CSRC}", f"-I{CSRC / 'device'}", f"-I{REPO / 'include'}"]
 
-CXX_SOURCES = sorted((CSRC / "host").glob("*.cpp")) + [CSRC / "device" / "executor.cpp", CSRC / "capi.cpp"]
+CXX_SOURCES = sorted((CSRC / "host").glob("*.cpp")) + sorted((CSRC / "device").glob("*.cpp")) + [CSRC / "capi.cpp"]
 CU_SOURCES = sorted((CSRC / "device").glob("*.cu"))
 
 
@@ -65,7 +65,7 @@ def build(verbose: bool = False) -> Path:
     newest = max(o.stat().st_mtime for o in objs)
     if LIB.exists() and LIB.stat().st_mtime >= newest:
         return LIB
-    cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lpthread",
+    cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lpthread", "-Xlinker", "--no-undefined",
            "-Xlinker", "-Bsymbolic"]
     if verbose:
         print(" ".join(cmd), flush=True)

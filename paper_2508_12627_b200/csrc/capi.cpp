@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include "device/executor.hpp"
+#include "device/tensorize.hpp"
 #include "ustats/ustats.hpp"
 
 namespace ustats::dev {
@@ -208,6 +209,20 @@ int us_u_terms(int32_t m, int32_t K, const int32_t* tuple_len, const int32_t* tu
         }
         if (u_out) *u_out = r.value;
         export_dev(r, cfg ? cfg->rank : 0, stats);
+    });
+}
+
+int us_u_statistic_data(const char* kernel, const double* data, int64_t n, int32_t d, int32_t on_device,
+                        const us_config* cfg, double* u_out, us_stats* stats) {
+    return guarded([&] {
+        ustats::Config config = to_config(cfg);
+        if (!kernel) ustats::fail(ustats::ErrorCode::InvalidArgument, "null kernel spec");
+        if (n < 1 || d < 1) ustats::fail(ustats::ErrorCode::InvalidArgument, "data must be a non-empty n x d array");
+        double tz = 0;
+        auto r = ustats::dev::u_statistic_data(kernel, data, n, d, on_device != 0, config, &tz);
+        *u_out = r.value;
+        export_dev(r, cfg ? cfg->rank : 0, stats);
+        if (stats) stats->tensorize_seconds = tz;
     });
 }
 

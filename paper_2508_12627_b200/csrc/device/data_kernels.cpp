@@ -1,0 +1,244 @@
+// Data-level entry: parse a kernel spec, tensorize its components on the
+// device from the raw sample, evaluate the U-statistic (engine.cpp:173-193
+// with tensorize, engine.cpp:108-136, moved to the GPU).
+#include <chrono>
+#include <cmath>
+#include <map>
+#include <string>
+
+#include "executor.hpp"
+#include "kernels.hpp"
+#include "tensorize.hpp"
+#include "ustats/errors.hpp"
+#include "ustats/tensor.hpp"
+
+namespace ustats::dev {
+
+namespace {
+
+std::vector<std::string> split(const std::string& s, char sep) {
+    std::vector<std::string> out;
+    std::string cur;
+    for (char ch : s) {
+        if (ch == sep) {
+            out.push_back(cur);
+            cur.clear();
+        } else {
+            cur += ch;
+        }
+    }
+    out.push_back(cur);
+    return out;
+}
+
+int to_int(const std::string& s, const std::string& spec) {
+    try {
+        std::size_t used = 0;
+        const int v = std::stoi(s, &used);
+        if (used != s.size()) throw std::invalid_argument(s);
+        return v;
+    } catch (const std::exception&) {
+        fail(ErrorCode::InvalidArgument, "bad number '" + s + "' in kernel spec '" + spec + "'");
+    }
+}
+
+double to_double(const std::string& s, const std::string& spec) {
+    try {
+        std::size_t used = 0;
+        const double v = std::stod(s, &used);
+        if (used != s.size()) throw std::invalid_argument(s);
+        return v;
+    } catch (const std::exception&) {
+        fail(ErrorCode::InvalidArgument, "bad number '" + s + "' in kernel spec '" + spec + "'");
+    }
+}
+
+// Cholesky G = R R^T (lower R) and M = R^{-T}, so Z G^{-1} Z^T = (Z M)(Z M)^T.
+std::vector<double> inverse_cholesky_transpose(const std::vector<double>& G, int F) {
+    std::vector<double> R(static_cast<std::size_t>(F * F), 0.0);
+    for (int i = 0; i < F; ++i)
+        for (int j = 0; j <= i; ++j) {
+            long double s = G[static_cast<std::size_t>(i * F + j)];
+            for (int k = 0; k < j; ++k) s -= static_cast<long double>(R[static_cast<std::size_t>(i * F + k)]) * R[static_cast<std::size_t>(j * F + k)];
+            if (i == j) {
+                if (s <= 0) fail(ErrorCode::InvalidArgument, "feature Gram matrix is not positive definite");
+                R[static_cast<std::size_t>(i * F + i)] = static_cast<double>(std::sqrt(s));
+            } else {
+                R[static_cast<std::size_t>(i * F + j)] = static_cast<double>(s / R[static_cast<std::size_t>(j * F + j)]);
+            }
+        }
+    // Rinv (lower) by forward substitution; M = Rinv^T
+    std::vector<double> Rinv(static_cast<std::size_t>(F * F), 0.0);
+    for (int c = 0; c < F; ++c)
+        for (int i = c; i < F; ++i) {
+            long double s = (i == c) ? 1.0L : 0.0L;
+            for (int k = c; k < i; ++k) s -= static_cast<long double>(R[static_cast<std::size_t>(i * F + k)]) * Rinv[static_cast<std::size_t>(k * F + c)];
+            Rinv[static_cast<std::size_t>(i * F + c)] = static_cast<double>(s / R[static_cast<std::size_t>(i * F + i)]);
+        }
+    std::vector<double> M(static_cast<std::size_t>(F * F), 0.0);
+    for (int i = 0; i < F; ++i)
+        for (int j = 0; j < F; ++j) M[static_cast<std::size_t>(i * F + j)] = Rinv[static_cast<std::size_t>(j * F + i)];
+    return M;
+}
+
+}  // namespace
+
+DataKernel parse_data_kernel(const std::string& spec, int d) {
+    DataKernel k;
+    const auto parts = split(spec, ':');
+    const std::string& kind = parts[0];
+    if (kind == "prod2" && parts.size() == 1) {
+        if (d < 1) fail(ErrorCode::InvalidArgument, "prod2 needs at least one coordinate");
+        k.m = 2;
+        k.sig = {{0}, {1}};
+        k.recipe = {"col:0", "col:0"};
+        return k;
+    }
+    if (kind == "hoif" && parts.size() == 3) {  // hoif.cpp:50-72
+        const int j = to_int(parts[1], spec), kk = to_int(parts[2], spec);
+        if (j < 2) fail(ErrorCode::InvalidArgument, "sequential kernel needs order >= 2");
+        if (kk < 1) fail(ErrorCode::InvalidArgument, "basis size must be >= 1");
+        if (d < 2 + kk) fail(ErrorCode::InvalidArgument, "covariate block shorter than the basis");
+        k.m = j;
+        for (int i = 0; i + 1 < j; ++i) {
+            k.sig.push_back({i, i + 1});
+            k.recipe.push_back(i + 2 < j ? "gram:0:0:2:" + std::to_string(kk) : "gram:0:1:2:" + std::to_string(kk));
+        }
+        return k;
+    }
+    if (kind == "rbf" && parts.size() == 3) {
+        const std::string& shape = parts[1];
+        const double h = to_double(parts[2], spec);
+        if (!(h > 0)) fail(ErrorCode::InvalidArgument, "RBF bandwidth must be positive");
+        const std::string rec = "rbf:" + parts[2];
+        if (shape.rfind("chain", 0) == 0 || shape.rfind("cycle", 0) == 0) {
+            const int m = to_int(shape.substr(5), spec);
+            if (m < 2) fail(ErrorCode::InvalidArgument, "shape needs m >= 2");
+            k.m = m;
+            for (int i = 0; i + 1 < m; ++i) k.sig.push_back({i, i + 1});
+            if (shape[1] == 'y') k.sig.push_back({m - 1, 0});
+        } else if (shape == "k4tail") {  // BASELINE C4
+            k.m = 6;
+            k.sig = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}, {3, 4}, {4, 5}};
+        } else {
+            fail(ErrorCode::InvalidArgument, "unknown RBF shape '" + shape + "' (chain<m> | cycle<m> | k4tail)");
+        }
+        k.recipe.assign(k.sig.size(), rec);
+        return k;
+    }
+    if (kind == "proj" && parts.size() == 3) {  // BASELINE C3 / C5: r B ... B e
+        const int m = to_int(parts[1], spec), kmax = to_int(parts[2], spec);
+        if (m < 2 || kmax < 1) fail(ErrorCode::InvalidArgument, "proj needs m >= 2 and kmax >= 1");
+        if (d < 3) fail(ErrorCode::InvalidArgument, "proj needs data columns [u_1..u_c, r, e] with c >= 1");
+        k.m = m;
+        k.sig.push_back({0});
+        k.recipe.push_back("col:" + std::to_string(d - 2));
+        for (int i = 0; i + 1 < m; ++i) {
+            k.sig.push_back({i, i + 1});
+            k.recipe.push_back("proj:" + std::to_string(d - 2) + ":" + std::to_string(kmax));
+        }
+        k.sig.push_back({m - 1});
+        k.recipe.push_back("col:" + std::to_string(d - 1));
+        return k;
+    }
+    fail(ErrorCode::InvalidArgument,
+         "unknown kernel spec '" + spec + "' (prod2 | hoif:<j>:<k> | rbf:<shape>:<h> | proj:<m>:<kmax>)");
+}
+
+StatisticResult u_statistic_data(const std::string& spec, const double* data, long long n, int d, bool on_device,
+                                 const Config& config, double* tensorize_seconds) {
+    const DataKernel k = parse_data_kernel(spec, d);
+    if (n < k.m)
+        fail(ErrorCode::SampleTooSmall,
+             "need at least " + std::to_string(k.m) + " observations, have " + std::to_string(n));
+    for (std::size_t c = 0; c < k.sig.size(); ++c)
+        checked_entry_count(static_cast<int>(k.sig[c].size()), static_cast<int>(n), config);
+    Runtime& rt = Runtime::get(config.device.device);
+    cudaStream_t s = rt.main_stream();
+    rt.set_stream(s);
+    const auto t0 = std::chrono::steady_clock::now();
+
+    // the sample on the device (n x d doubles: the only H2D of the call)
+    Buf sample;
+    const double* x = data;
+    if (!on_device) {
+        sample = rt.allocate(1, n * d);
+        check_cuda(cudaMemcpyAsync(sample->ptr, data, static_cast<std::size_t>(n * d) * sizeof(double),
+                                   cudaMemcpyHostToDevice, s),
+                   "upload sample");
+        x = sample->ptr;
+    }
+    std::map<std::string, Buf> built;
+    std::uint64_t launches = 0;
+    for (const std::string& rec : k.recipe) {
+        if (built.count(rec)) continue;
+        const auto p = split(rec, ':');
+        Buf b;
+        if (p[0] == "col") {
+            b = rt.allocate(1, n);
+            launch_column(x, n, d, std::stoi(p[1]), b->ptr, s);
+            ++launches;
+        } else if (p[0] == "gram") {
+            b = rt.allocate(2, n);
+            launch_scaled_gram(x, n, d, std::stoi(p[1]), std::stoi(p[2]), std::stoi(p[3]), std::stoi(p[4]), b->ptr, s);
+            ++launches;
+        } else if (p[0] == "rbf") {
+            b = rt.allocate(2, n);
+            launch_rbf(x, n, d, std::stod(p[1]), b->ptr, s);
+            ++launches;
+        } else {  // proj: B = Z (Z^T Z / n)^{-1} Z^T as the symmetric product (Z M)(Z M)^T
+            const int ncols = std::stoi(p[1]), kmax = std::stoi(p[2]);
+            const int F = ncols * kmax;
+            Buf z = rt.allocate(1, n * F), y = rt.allocate(1, n * F), g = rt.allocate(1, static_cast<long long>(F) * F);
+            launch_cosine_features(x, n, d, ncols, kmax, z->ptr, s);
+            launch_thin_gram(z->ptr, n, F, g->ptr, s);
+            std::vector<double> G(static_cast<std::size_t>(F * F));
+            check_cuda(cudaMemcpyAsync(G.data(), g->ptr, G.size() * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+            check_cuda(cudaStreamSynchronize(s), "sync");
+            const std::vector<double> M = inverse_cholesky_transpose(G, F);
+            check_cuda(cudaMemcpyAsync(g->ptr, M.data(), M.size() * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+            launch_times_small(z->ptr, n, F, g->ptr, y->ptr, s);
+            b = rt.allocate(2, n);
+            GemmArgs a;
+            a.a.nf = a.b.nf = 1;
+            a.a.nr = a.b.nr = 1;
+            a.a.ptr[0] = a.b.ptr[0] = y->ptr;
+            a.a.rstride[0][0] = a.b.rstride[0][0] = F;
+            a.a.kstride[0] = a.b.kstride[0] = 1;
+            a.n = F;
+            a.rows = a.cols = n;
+            a.symmetric_out = 1;
+            EpiSet e;
+            e.count = 1;
+            e.d[0].mode = kEpiStore;
+            e.d[0].out = b->ptr;
+            launches += 3;  // features, thin Gram, Z M
+            const int gl = launch_gemm_multi(a, e, s);
+            launches += gl > 0 ? static_cast<std::uint64_t>(gl) : 1;
+            if (gl < 0) {  // operands not TMA-eligible (odd F): plain product
+                a.symmetric_out = 0;
+                a.mode = kEpiStore;
+                a.out = b->ptr;
+                launch_gemm(a, s);
+            }
+            check_cuda(cudaStreamSynchronize(s), "sync");  // z, y, g freed at scope exit
+        }
+        check_cuda(cudaGetLastError(), "tensorize");
+        built[rec] = b;
+    }
+    check_cuda(cudaStreamSynchronize(s), "sync");
+    if (tensorize_seconds)
+        *tensorize_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+
+    StatisticSpec spec_in;
+    spec_in.m = k.m;
+    spec_in.sig = k.sig;
+    for (const std::string& rec : k.recipe) spec_in.inputs.push_back(built[rec]->ptr);
+    Config cfg = config;
+    cfg.device.donate_inputs = true;  // our own tensors: sparsify in place
+    auto res = lattice_batch({spec_in}, true, n, LatticeMode::Sparsified, cfg);
+    res[0].stats.kernel_launches += launches;
+    return res[0];
+}
+
+}  // namespace ustats::dev

@@ -1,0 +1,119 @@
+// Device-side tensorization: the kernel components of the
+// BASELINE workloads and of the binding's kernel specs are materialized on
+// the GPU from the raw sample (n x d, row-major) instead of n^|A_k|
+// std::function calls on the host (engine.cpp:108-136, tensor.cpp:42-52).
+#include <cmath>
+
+#include "kernels.hpp"
+#include "tensorize.hpp"
+
+namespace ustats::dev {
+
+namespace {
+
+// A_ij = exp(-scale * sum_c (x_ic - x_jc)^2). The squared differences are
+// summed in coordinate order, so A is bitwise symmetric.
+__global__ void rbf(const double* __restrict__ x, long long n, int d, double scale, double* __restrict__ out) {
+    const long long j = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    const long long i = blockIdx.y;
+    if (j >= n) return;
+    const double* xi = x + i * d;
+    const double* xj = x + j * d;
+    double s = 0.0;
+    for (int c = 0; c < d; ++c) {
+        const double t = xi[c] - xj[c];
+        s += t * t;
+    }
+    out[i * n + j] = exp(-scale * s);
+}
+
+// out_ij = left_i * (sum_c z_ic z_jc) * right_j   (hoif.cpp:50-72 components)
+__global__ void scaled_gram(const double* __restrict__ x, long long n, int d, int col_left, int col_right, int z0,
+                            int k, double* __restrict__ out) {
+    const long long j = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    const long long i = blockIdx.y;
+    if (j >= n) return;
+    const double* xi = x + i * d;
+    const double* xj = x + j * d;
+    double dot = 0.0;
+    for (int c = 0; c < k; ++c) dot += xi[z0 + c] * xj[z0 + c];
+    const double l = col_left >= 0 ? xi[col_left] : 1.0;
+    const double r = col_right >= 0 ? xj[col_right] : 1.0;
+    out[i * n + j] = (l * dot) * r;
+}
+
+__global__ void column(const double* __restrict__ x, long long n, int d, int c, double* __restrict__ out) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i < n) out[i] = x[i * d + c];
+}
+
+// Z_i,(c*kmax + k-1) = cos(pi * k * u_ic), k = 1..kmax, for columns c < ncols.
+__global__ void cosine_features(const double* __restrict__ x, long long n, int d, int ncols, int kmax,
+                                double* __restrict__ z) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const int F = ncols * kmax;
+    for (int c = 0; c < ncols; ++c) {
+        const double u = x[i * d + c];
+        for (int k = 1; k <= kmax; ++k) z[i * F + c * kmax + (k - 1)] = cos(M_PI * k * u);
+    }
+}
+
+// G = Z^T Z / n for a thin Z (n x F, F <= 128): one block per (f, g) pair,
+// fixed-order strided sums + tree (deterministic).
+__global__ void thin_gram(const double* __restrict__ z, long long n, int F, double* __restrict__ g) {
+    __shared__ double red[256];
+    const int f = blockIdx.x, h = blockIdx.y;
+    double s = 0.0;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) s += z[i * F + f] * z[i * F + h];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) g[f * F + h] = red[0] / static_cast<double>(n);
+}
+
+// Y = Z M (n x F times a small dense F x F).
+__global__ void times_small(const double* __restrict__ z, long long n, int F, const double* __restrict__ M,
+                            double* __restrict__ y) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    for (int c = 0; c < F; ++c) {
+        double s = 0.0;
+        for (int r = 0; r < F; ++r) s += z[i * F + r] * M[r * F + c];
+        y[i * F + c] = s;
+    }
+}
+
+}  // namespace
+
+void launch_rbf(const double* x, long long n, int d, double bandwidth, double* out, cudaStream_t s) {
+    rbf<<<dim3(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(n)), 256, 0, s>>>(
+        x, n, d, 0.5 / (bandwidth * bandwidth), out);
+}
+
+void launch_scaled_gram(const double* x, long long n, int d, int col_left, int col_right, int z0, int k, double* out,
+                        cudaStream_t s) {
+    scaled_gram<<<dim3(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(n)), 256, 0, s>>>(
+        x, n, d, col_left, col_right, z0, k, out);
+}
+
+void launch_column(const double* x, long long n, int d, int c, double* out, cudaStream_t s) {
+    column<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(x, n, d, c, out);
+}
+
+void launch_cosine_features(const double* x, long long n, int d, int ncols, int kmax, double* z, cudaStream_t s) {
+    cosine_features<<<static_cast<unsigned>((n + 127) / 128), 128, 0, s>>>(x, n, d, ncols, kmax, z);
+}
+
+void launch_thin_gram(const double* z, long long n, int F, double* g, cudaStream_t s) {
+    thin_gram<<<dim3(static_cast<unsigned>(F), static_cast<unsigned>(F)), 256, 0, s>>>(z, n, F, g);
+}
+
+void launch_times_small(const double* z, long long n, int F, const double* M, double* y, cudaStream_t s) {
+    times_small<<<static_cast<unsigned>((n + 127) / 128), 128, 0, s>>>(z, n, F, M, y);
+}
+
+}  // namespace ustats::dev

@@ -1,0 +1,42 @@
+// Device tensorization kernels (tensorize.cu) and the data-kernel front end
+// (data_kernels.cpp).
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "ustats/config.hpp"
+#include "ustats/notation.hpp"
+
+namespace ustats::dev {
+
+void launch_rbf(const double* x, long long n, int d, double bandwidth, double* out, cudaStream_t s);
+void launch_scaled_gram(const double* x, long long n, int d, int col_left, int col_right, int z0, int k, double* out,
+                        cudaStream_t s);
+void launch_column(const double* x, long long n, int d, int c, double* out, cudaStream_t s);
+void launch_cosine_features(const double* x, long long n, int d, int ncols, int kmax, double* z, cudaStream_t s);
+void launch_thin_gram(const double* z, long long n, int F, double* g, cudaStream_t s);
+void launch_times_small(const double* z, long long n, int F, const double* M, double* y, cudaStream_t s);
+
+struct StatisticResult;
+
+// Parsed data kernel: component k reads slots sig[k] and is built by recipe[k].
+struct DataKernel {
+    int m = 0;
+    std::vector<IndexTuple> sig;   // 0-based
+    std::vector<std::string> recipe;  // canonical component recipe (equal strings = same tensor)
+};
+
+// Kernel specs (the binding's prod2 / hoif:<j>:<k>, plus the BASELINE
+// workloads): "prod2", "hoif:<j>:<k>", "rbf:<shape>:<bandwidth>" with shape
+// chain<m> | cycle<m> | k4tail, "proj:<m>:<kmax>" (cosine-feature projection
+// chain r B..B e over data columns [u_1..u_c, r, e]).
+DataKernel parse_data_kernel(const std::string& spec, int d);
+
+// Tensorizes on the device from the sample and evaluates the U-statistic.
+StatisticResult u_statistic_data(const std::string& spec, const double* data, long long n, int d, bool on_device,
+                                 const Config& config, double* tensorize_seconds);
+
+}  // namespace ustats::dev

@@ -110,3 +110,23 @@ def input_bytes(factors) -> int:
             seen.add(id(f))
             total += f.nbytes
     return total
+
+
+# Data-level form of each workload: the raw sample and the kernel spec that
+# the engine tensorizes on the device (us_u_statistic_data).
+SPECS = {"C1": "rbf:chain3:1", "C2": "rbf:cycle4:1", "C3": "proj:5:16", "C4": "rbf:k4tail:1", "C5": "proj:7:16"}
+
+
+def generate_data(name: str, n: int | None = None):
+    """Returns (data n x d, spec, m, workload): the same draws as generate()."""
+    w = CONFIGS[name]
+    n = w.n if n is None else int(n)
+    rng = np.random.default_rng(w.seed)
+    if w.kind == "rbf":
+        x = rng.standard_normal((n, w.dim))
+    else:
+        u = rng.uniform(size=(n, 4))
+        r = rng.standard_normal(n)
+        e = rng.standard_normal(n)
+        x = np.concatenate([u, r[:, None], e[:, None]], axis=1)
+    return np.ascontiguousarray(x), SPECS[name], w.m, w

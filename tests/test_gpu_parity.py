@@ -287,3 +287,32 @@ def test_panel_upload_speculation(engine):
     assert np.max(np.abs(spec.v - fresh.v)) <= TOL * scale
     _, rows = O.u_statistic([a] * 4, sig, m)
     assert abs(spec.value - O.combine([r[1] for r in rows], [r[2] for r in rows])) <= TOL * scale
+
+
+@pytest.mark.parametrize("name,n", [("C1", 300), ("C2", 256), ("C3", 200), ("C4", 40), ("C5", 160)])
+def test_device_tensorization_matches_host(engine, name, n):
+    # components tensorized on the GPU from the raw sample == the reference
+    # computed from host-tensorized factors (RBF / cosine-feature projection)
+    from paper_2508_12627_b200.workloads import generate, generate_data
+    data, spec, m, _ = generate_data(name, n)
+    factors, sig, _, _ = generate(name, n)
+    got, stats = engine.u_statistic(spec, data, config=engine.Config(memory_cap_entries=2 ** 31), with_stats=True)
+    u_ref, rows = O.u_statistic(factors, sig, m)
+    scale = max(abs(r[2]) for r in rows)
+    assert abs(got - u_ref) <= TOL * scale, (got, u_ref)
+    assert stats["tensorize_seconds"] > 0
+    if REF.available() and name in ("C1", "C2", "C4"):
+        u_ref2, _ = REF.u_statistic_data(spec, data)
+        assert abs(got - u_ref2) <= TOL * scale
+
+
+def test_device_tensorization_resident_sample(engine):
+    import torch
+    from paper_2508_12627_b200.workloads import generate_data
+    data, spec, m, _ = generate_data("C2", 300)
+    host = engine.u_statistic(spec, data)
+    dev = engine.u_statistic(spec, torch.from_numpy(data).cuda())
+    assert dev == host
+    with pytest.raises(engine.UStatsError) as e:
+        engine.u_statistic("rbf:blob3:1", data)
+    assert e.value.code == "InvalidArgument"
