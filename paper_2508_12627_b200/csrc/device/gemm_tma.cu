@@ -117,6 +117,13 @@ struct TmaArgs {
     int symmetric;
     int colmajor;          // symmetric list ordered by column: tile (tm <= tn) at tn(tn+1)/2 + tm
     int accumulate;        // outputs += (pre-zeroed)
+    // Split-K tail (the last, partial wave): phase 1 computes K-slices of the
+    // leftover tiles into kpart, phase 2 sums the slices in order and runs the
+    // epilogues; phase 0 is the ordinary full-K tile.
+    int phase;
+    int ksplit;
+    long long slot_base;   // reduction-partial slot of this launch's first tile
+    double* kpart;
     EpiSet epis;
 };
 
@@ -129,7 +136,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         (reinterpret_cast<unsigned long long>(smem_raw) + 1023ull) & ~1023ull);
 
     const long long tiles_m = (p.rows + BM - 1) / BM, tiles_n = (p.cols + BN - 1) / BN;
-    const long long bid = p.tile_begin + blockIdx.x;
+    const long long local = p.phase == 1 ? blockIdx.x / p.ksplit : blockIdx.x;
+    const int slice = p.phase == 1 ? static_cast<int>(blockIdx.x % p.ksplit) : 0;
+    const long long bid = p.tile_begin + local;
     long long tm, tn;
     if (p.symmetric && p.colmajor) {
         // column by column: column tn holds tiles 0..tn (panels <= tn)
@@ -156,87 +165,111 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool mirror = p.symmetric && tm != tn;
     const int r0 = static_cast<int>(tm * BM), c0 = static_cast<int>(tn * BN);
     const int KT = static_cast<int>((p.n + BK - 1) / BK);
-
+    const int kt0 = p.phase == 1 ? static_cast<int>(static_cast<long long>(KT) * slice / p.ksplit) : 0;
+    const int kt1 = p.phase == 1 ? static_cast<int>(static_cast<long long>(KT) * (slice + 1) / p.ksplit) : KT;
     const int tid = threadIdx.x;
-    if (tid == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&sm.full[s], 1);
-            mbar_init(&sm.empty[s], THREADS / 32);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    auto issue = [&](int kt, int s) {
-        mbar_expect_tx(&sm.full[s], STAGE_BYTES);
-        const int k0 = kt * BK;
-        if (AK) {
-            tma_load_2d(sm.u.st.a[s], &map_a, k0, r0, &sm.full[s]);
-        } else {
-#pragma unroll
-            for (int q = 0; q < BM / 16; ++q) tma_load_2d(sm.u.st.a[s] + q * 256, &map_a, r0 + 16 * q, k0, &sm.full[s]);
-        }
-        if (BKM) {
-            tma_load_2d(sm.u.st.b[s], &map_b, k0, c0, &sm.full[s]);
-        } else {
-#pragma unroll
-            for (int q = 0; q < BN / 16; ++q) tma_load_2d(sm.u.st.b[s] + q * 256, &map_b, c0 + 16 * q, k0, &sm.full[s]);
-        }
-    };
-
-    if (tid == 0) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&map_a)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&map_b)) : "memory");
-        for (int kt = 0; kt < STAGES && kt < KT; ++kt) issue(kt, kt);
-    }
-
     const int warp = tid >> 5, lane = tid & 31;
-    const int wm = warp >> 2, wn = warp & 3;
-    const int g = lane >> 2, t = lane & 3;
+    double* tile = sm.u.tile;
 
-    double acc[8][4][2];
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    if (p.phase != 2) {
+        if (tid == 0) {
+            for (int s = 0; s < STAGES; ++s) {
+                mbar_init(&sm.full[s], 1);
+                mbar_init(&sm.empty[s], THREADS / 32);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
 
-    for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % STAGES;
-        const unsigned ph = static_cast<unsigned>((kt / STAGES) & 1);
-        mbar_wait(&sm.full[s], ph);
-        const double* ta = sm.u.st.a[s];
-        const double* tb = sm.u.st.b[s];
+        auto issue = [&](int kt, int s) {
+            mbar_expect_tx(&sm.full[s], STAGE_BYTES);
+            const int k0 = kt * BK;
+            if (AK) {
+                tma_load_2d(sm.u.st.a[s], &map_a, k0, r0, &sm.full[s]);
+            } else {
 #pragma unroll
-        for (int ks = 0; ks < BK / 4; ++ks) {
-            double af[8], bf[4];
+                for (int q = 0; q < BM / 16; ++q) tma_load_2d(sm.u.st.a[s] + q * 256, &map_a, r0 + 16 * q, k0, &sm.full[s]);
+            }
+            if (BKM) {
+                tma_load_2d(sm.u.st.b[s], &map_b, k0, c0, &sm.full[s]);
+            } else {
 #pragma unroll
-            for (int mi = 0; mi < 8; ++mi) af[mi] = tile_at<AK>(ta, wm * 64 + mi * 8 + g, ks * 4 + t);
+                for (int q = 0; q < BN / 16; ++q) tma_load_2d(sm.u.st.b[s] + q * 256, &map_b, c0 + 16 * q, k0, &sm.full[s]);
+            }
+        };
+
+        if (tid == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&map_a)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&map_b)) : "memory");
+            for (int j = 0; j < STAGES && kt0 + j < kt1; ++j) issue(kt0 + j, j);
+        }
+
+        const int wm = warp >> 2, wn = warp & 3;
+        const int g = lane >> 2, t = lane & 3;
+
+        double acc[8][4][2];
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) bf[ni] = tile_at<BKM>(tb, wn * 32 + ni * 8 + g, ks * 4 + t);
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+        for (int j = 0; j < kt1 - kt0; ++j) {
+            const int s = j % STAGES;
+            const unsigned ph = static_cast<unsigned>((j / STAGES) & 1);
+            mbar_wait(&sm.full[s], ph);
+            const double* ta = sm.u.st.a[s];
+            const double* tb = sm.u.st.b[s];
+#pragma unroll
+            for (int ks = 0; ks < BK / 4; ++ks) {
+                double af[8], bf[4];
+#pragma unroll
+                for (int mi = 0; mi < 8; ++mi) af[mi] = tile_at<AK>(ta, wm * 64 + mi * 8 + g, ks * 4 + t);
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) bf[ni] = tile_at<BKM>(tb, wn * 32 + ni * 8 + g, ks * 4 + t);
+#pragma unroll
+                for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+                    for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.empty[s]);
+            if (tid == 0 && kt0 + j + STAGES < kt1) {
+                mbar_wait(&sm.empty[s], ph);
+                issue(kt0 + j + STAGES, s);
+            }
+        }
+
+        if (p.phase == 1) {  // a K-slice of a tail tile: raw accumulators out, no epilogue
+            double* dst = p.kpart + static_cast<long long>(blockIdx.x) * (BM * BN);
 #pragma unroll
             for (int mi = 0; mi < 8; ++mi)
 #pragma unroll
-                for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+                for (int ni = 0; ni < 4; ++ni) {
+                    const int r = wm * 64 + mi * 8 + g, c = wn * 32 + ni * 8 + 2 * t;
+                    *reinterpret_cast<double2*>(dst + r * BN + c) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+                }
+            return;
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.empty[s]);
-        if (tid == 0 && kt + STAGES < KT) {
-            mbar_wait(&sm.empty[s], ph);
-            issue(kt + STAGES, s);
+        __syncthreads();  // every stage consumed: the ring becomes the accumulator tile
+#pragma unroll
+        for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {
+                const int r = wm * 64 + mi * 8 + g, c = wn * 32 + ni * 8 + 2 * t;
+                tile[r * TP + c] = acc[mi][ni][0];
+                tile[r * TP + c + 1] = acc[mi][ni][1];
+            }
+    } else {
+        // phase 2: the tile is the in-order sum of its K-slices
+        const double* src = p.kpart + static_cast<long long>(blockIdx.x) * p.ksplit * (BM * BN);
+        for (int i = tid; i < BM * BN; i += THREADS) {
+            double v = 0.0;
+            for (int sl = 0; sl < p.ksplit; ++sl) v += src[static_cast<long long>(sl) * (BM * BN) + i];
+            tile[(i >> 7) * TP + (i & 127)] = v;
         }
     }
-    __syncthreads();  // every stage consumed: the ring becomes the accumulator tile
-
-    double* tile = sm.u.tile;
-#pragma unroll
-    for (int mi = 0; mi < 8; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-            const int r = wm * 64 + mi * 8 + g, c = wn * 32 + ni * 8 + 2 * t;
-            tile[r * TP + c] = acc[mi][ni][0];
-            tile[r * TP + c + 1] = acc[mi][ni][1];
-        }
     __syncthreads();
+    const long long slot = p.slot_base + blockIdx.x;
 
     const long long rows = p.rows, cols = p.cols;
     for (int q = 0; q < p.epis.count; ++q) {
@@ -283,7 +316,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (tid == 0) {
                     double tot = 0.0;
                     for (int w = 0; w < THREADS / 32; ++w) tot += sm.red[w];
-                    d.partial[blockIdx.x] = tot;
+                    d.partial[slot] = tot;
                 }
                 __syncthreads();
             }
@@ -386,18 +419,25 @@ bool encode(CUtensorMap* map, const double* ptr, bool kmajor, long long rows, lo
 }
 
 template <bool AK, bool BKM>
-long long launch_tma(const CUtensorMap& ma, const CUtensorMap& mb, const TmaArgs& args, long long count,
-                     cudaStream_t s) {
+void launch_tma(const CUtensorMap& ma, const CUtensorMap& mb, const TmaArgs& args, long long grid, cudaStream_t s) {
     static std::once_flag once;
     const int bytes = static_cast<int>(sizeof(TmaSmem)) + 1024;
     std::call_once(once, [&] {
         cudaFuncSetAttribute(gemm_tma_kernel<AK, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     });
-    const long long tm = (args.rows + BM - 1) / BM, tn = (args.cols + BN - 1) / BN;
-    const long long total = args.symmetric ? tm * (tm + 1) / 2 : tm * tn;
-    const long long tiles = count < 0 ? total - args.tile_begin : count;
-    if (tiles > 0) gemm_tma_kernel<AK, BKM><<<static_cast<unsigned>(tiles), THREADS, bytes, s>>>(ma, mb, args);
-    return tiles;
+    if (grid > 0) gemm_tma_kernel<AK, BKM><<<static_cast<unsigned>(grid), THREADS, bytes, s>>>(ma, mb, args);
+}
+
+int sm_count_cached() {
+    static int sms = 0;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    });
+    return sms;
 }
 
 __global__ void epi_finalize_scalar(const double* partial, long long P, double* out, int accumulate) {
@@ -473,14 +513,56 @@ int launch_gemm_multi(const GemmArgs& a, const EpiSet& epis, cudaStream_t s) {
     args.symmetric = (a.symmetric_out && a.rows == a.cols) ? 1 : 0;
     args.colmajor = a.tri_colmajor;
     args.accumulate = a.accumulate;
+    args.phase = 0;
+    args.ksplit = 1;
+    args.slot_base = 0;
+    args.kpart = nullptr;
     args.epis = epis;
-    long long blocks;
-    const long long cnt = a.tile_count;
-    if (ak) blocks = bk ? launch_tma<true, true>(ma, mb, args, cnt, s) : launch_tma<true, false>(ma, mb, args, cnt, s);
-    else blocks = bk ? launch_tma<false, true>(ma, mb, args, cnt, s) : launch_tma<false, false>(ma, mb, args, cnt, s);
+    const long long tm_ = (a.rows + BM - 1) / BM, tn_ = (a.cols + BN - 1) / BN;
+    const long long total = args.symmetric ? tm_ * (tm_ + 1) / 2 : tm_ * tn_;
+    const long long blocks = a.tile_count < 0 ? total - a.tile_begin : a.tile_count;
     if (blocks <= 0) return 0;
-    int launched = 1;
-    const long long tm = (a.rows + BM - 1) / BM, tn = (a.cols + BN - 1) / BN;
+    auto go = [&](const TmaArgs& t, long long grid) {
+        if (ak) {
+            if (bk) launch_tma<true, true>(ma, mb, t, grid, s);
+            else launch_tma<true, false>(ma, mb, t, grid, s);
+        } else {
+            if (bk) launch_tma<false, true>(ma, mb, t, grid, s);
+            else launch_tma<false, false>(ma, mb, t, grid, s);
+        }
+    };
+    // The last wave of a multi-wave grid is partial (C2: 2080 tiles = 14.05
+    // waves of 148): its tiles are split along K over the idle SMs and
+    // re-assembled, so the tail costs ~1/S of a tile instead of a whole tile.
+    const int sms = sm_count_cached();
+    const long long waves = blocks / sms, tail = blocks % sms;
+    const int KT = static_cast<int>((a.n + BK - 1) / BK);
+    int S = tail > 0 ? static_cast<int>(sms / tail) : 1;
+    if (S > KT / 4) S = KT / 4;
+    int launched_kernels = 0;
+    if (waves >= 1 && tail > 0 && S >= 2) {
+        go(args, blocks - tail);
+        double* kpart = nullptr;
+        const std::size_t kbytes = static_cast<std::size_t>(tail) * S * BM * BN * sizeof(double);
+        if (cudaMallocAsync(reinterpret_cast<void**>(&kpart), kbytes, s) != cudaSuccess) return -1;
+        TmaArgs t1 = args;
+        t1.tile_begin = a.tile_begin + blocks - tail;
+        t1.phase = 1;
+        t1.ksplit = S;
+        t1.kpart = kpart;
+        go(t1, tail * S);
+        TmaArgs t2 = t1;
+        t2.phase = 2;
+        t2.slot_base = blocks - tail;
+        go(t2, tail);
+        cudaFreeAsync(kpart, s);
+        launched_kernels = 3;
+    } else {
+        go(args, blocks);
+        launched_kernels = 1;
+    }
+    int launched = launched_kernels;
+    const long long tm = tm_, tn = tn_;
     for (int q = 0; q < epis.count; ++q) {
         const EpiDesc& d = epis.d[q];
         if (d.mode == kEpiSumAll) {
