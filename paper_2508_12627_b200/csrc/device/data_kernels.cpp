@@ -226,14 +226,20 @@ StatisticResult u_statistic_data(const std::string& spec, const double* data, lo
         check_cuda(cudaGetLastError(), "tensorize");
         built[rec] = b;
     }
-    check_cuda(cudaStreamSynchronize(s), "sync");
+    // no sync here: the tensorization kernels run while the host plans the
+    // statistic (tensorize_seconds is the host time to build and enqueue them)
     if (tensorize_seconds)
         *tensorize_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 
     StatisticSpec spec_in;
     spec_in.m = k.m;
     spec_in.sig = k.sig;
-    for (const std::string& rec : k.recipe) spec_in.inputs.push_back(built[rec]->ptr);
+    for (const std::string& rec : k.recipe) {
+        spec_in.inputs.push_back(built[rec]->ptr);
+        // RBF entries are computed once per unordered pair and mirrored; the
+        // projection is a mirrored symmetric GEMM: both bitwise symmetric
+        spec_in.symmetric.push_back(rec.rfind("rbf", 0) == 0 || rec.rfind("proj", 0) == 0);
+    }
     Config cfg = config;
     cfg.device.donate_inputs = true;  // our own tensors: sparsify in place
     auto res = lattice_batch({spec_in}, true, n, LatticeMode::Sparsified, cfg);

@@ -396,7 +396,7 @@ int Program::stream(std::vector<View> factors, const std::vector<int>& out_ids, 
     if (static_cast<int>(out_ids.size()) + std::popcount(sum) > kMaxDims)
         fail(ErrorCode::InvalidArgument, "contraction step spans too many indices for the stream kernel");
     std::string key;
-    if (!ext && sharing()) {
+    if (sharing()) {
         std::vector<int> sums = ids_of(sum);
         std::sort(sums.begin(), sums.end());
         std::string best;
@@ -411,10 +411,20 @@ int Program::stream(std::vector<View> factors, const std::vector<int>& out_ids, 
             if (best.empty() || k < best) best = k;
         } while (std::next_permutation(sums.begin(), sums.end()));
         key = best;
-        auto hit = memo_.find(key);
-        if (hit != memo_.end()) {
-            if (stats_) ++stats_->shared_hits;
-            return hit->second;
+        if (ext) {
+            key = "X" + key;
+            auto hit = term_memo_.find(key);
+            if (hit != term_memo_.end()) {
+                if (stats_) ++stats_->shared_hits;
+                aliases_.emplace_back(ext, hit->second);
+                return -1;
+            }
+        } else {
+            auto hit = memo_.find(key);
+            if (hit != memo_.end()) {
+                if (stats_) ++stats_->shared_hits;
+                return hit->second;
+            }
         }
     }
     Op op;
@@ -425,7 +435,8 @@ int Program::stream(std::vector<View> factors, const std::vector<int>& out_ids, 
     if (!ext) op.out = new_buf(static_cast<int>(out_ids.size()), false);
     ops_.push_back(op);
     if (!key.empty()) {
-        memo_[key] = op.out;
+        if (ext) term_memo_[key] = ext;
+        else memo_[key] = op.out;
         memo_log_.push_back(key);
     }
     return op.out;
@@ -483,8 +494,12 @@ int Program::gemm(std::vector<View> fa, std::vector<View> fb, const std::vector<
 }
 
 void Program::rollback(const Mark& m) {
-    for (std::size_t i = m.log; i < memo_log_.size(); ++i) memo_.erase(memo_log_[i]);
+    for (std::size_t i = m.log; i < memo_log_.size(); ++i) {
+        if (memo_log_[i][0] == 'X') term_memo_.erase(memo_log_[i]);
+        else memo_.erase(memo_log_[i]);
+    }
     memo_log_.resize(m.log);
+    aliases_.resize(m.aliases);
     ops_.resize(m.ops);
     bufs_.resize(m.bufs);
 }
@@ -1739,7 +1754,9 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
             rt.begin(Runtime::kOther);
             if (mode == LatticeMode::Sparsified && !panels)
                 upload_stats.kernel_launches += static_cast<std::uint64_t>(launch_sparsify(b->ptr, order, n, rt.stream()));
-            if (flags && order == 2) {
+            if (order == 2 && k < sp.symmetric.size() && sp.symmetric[k]) {
+                b->symmetric = config.device.exploit_symmetry;  // known by construction: no probe
+            } else if (flags && order == 2) {
                 int* f = flags + probes.size();
                 const auto key = std::make_pair(static_cast<const void*>(sp.inputs[k]), n);
                 auto seen = rt.symmetry_seen.find(key);
@@ -1791,6 +1808,7 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
     check_cuda(cudaMemsetAsync(d_v, 0, sizeof(double) * std::max<std::size_t>(T, 1), rt.stream()), "memset");
     DevStats shared;  // one program for every statistic: sub-contractions shared across them
     double plan_s = 0;
+    std::vector<std::pair<std::size_t, std::size_t>> term_alias;
     {
         Program prog(&rt, n, config, &shared);
         std::size_t at = 0;
@@ -1807,6 +1825,8 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
         prog.optimize(budget);
         plan_s = std::chrono::duration<double>(Clock::now() - t0).count();
         prog.execute();
+        for (const auto& [dup, src] : prog.term_aliases())
+            term_alias.emplace_back(static_cast<std::size_t>(dup - d_v), static_cast<std::size_t>(src - d_v));
         if (trace)
             std::fprintf(stderr, "[trace] upload-enqueue %.3f ms, upload-sync %.3f ms, plan %.3f ms, launch done %.3f ms\n",
                          enqueue_s * 1e3, upload_s * 1e3, plan_s * 1e3,
@@ -1843,6 +1863,7 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
     speculative.clear();
     if (mispredicted)  // the host matrix changed and is no longer symmetric: redo without speculation
         return lattice_batch_impl(specs, inputs_on_device, n, mode, config, false);
+    for (const auto& [dup, src] : term_alias) v[dup] = v[src];
     const double contract_s = std::chrono::duration<double>(Clock::now() - t0).count();
     if (trace) std::fprintf(stderr, "[trace] contract total %.3f ms\n", contract_s * 1e3);
 

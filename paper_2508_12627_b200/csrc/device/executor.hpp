@@ -218,9 +218,13 @@ class Program {
              int e, std::vector<int>* layout);
 
     struct Mark {
-        std::size_t ops = 0, bufs = 0, log = 0;
+        std::size_t ops = 0, bufs = 0, log = 0, aliases = 0;
     };
-    Mark mark() const { return {ops_.size(), bufs_.size(), memo_log_.size()}; }
+    Mark mark() const { return {ops_.size(), bufs_.size(), memo_log_.size(), aliases_.size()}; }
+    // Terms whose final reduction repeats an earlier term's (same canonical
+    // op): (duplicate slot, source slot); the host copies the value after
+    // the D2H instead of launching the reduction again.
+    const std::vector<std::pair<double*, double*>>& term_aliases() const { return aliases_; }
     void rollback(const Mark& m);
     double cost_since(const Mark& m) const;
 
@@ -248,6 +252,8 @@ class Program {
     std::vector<Op> ops_;
     std::unordered_map<std::string, int> memo_;
     std::vector<std::string> memo_log_;
+    std::map<std::string, double*> term_memo_;  // canonical key of a term-final op -> its slot
+    std::vector<std::pair<double*, double*>> aliases_;
     std::map<int, bool> keep_;
     std::vector<std::size_t> schedule_;  // execution order of live ops (memory-aware)
     int slice_rank_ = 0, slice_world_ = 1;  // row sharding: the slice launch() computes
@@ -327,6 +333,9 @@ struct StatisticSpec {
     std::vector<const double*> inputs;
     std::vector<IndexTuple> sig;
     int m = 0;
+    // per input: symmetric by construction (device-built kernels), so the
+    // bitwise symmetry probe is skipped; empty = probe every matrix
+    std::vector<char> symmetric;
 };
 std::vector<StatisticResult> lattice_batch(const std::vector<StatisticSpec>& specs, bool inputs_on_device,
                                            long long n, LatticeMode mode, const Config& config);

@@ -11,6 +11,7 @@
 // shared-memory tree, then an in-order pass over block partials): results are
 // bit-reproducible run to run.
 #include <cstdio>
+#include <type_traits>
 
 #include "kernels.hpp"
 
@@ -43,6 +44,68 @@ __device__ __forceinline__ double product_at(const StreamArgs& a, const long lon
     for (int f = 0; f < kMaxFactors; ++f)
         if (f < a.nf) v *= __ldg(a.ptr[f] + off[f] + i * a.stride[f][inner]);
     return v;
+}
+
+// sum_{k < cnt} prod_f p[f][k * st[f]] with four independent load/multiply
+// chains, so every thread keeps 4*NF loads in flight (a single dependent
+// chain left the reductions at ~2 TB/s). Fixed association:
+// ((c0 + c1) + (c2 + c3)), chain u holding k = u (mod 4), tail in c0.
+template <int NF>
+__device__ __forceinline__ double run_sum(const double* const* p, const long long* st, long long cnt) {
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+    long long k = 0;
+    for (; k + 4 <= cnt; k += 4) {
+        double v0 = 1.0, v1 = 1.0, v2 = 1.0, v3 = 1.0;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            const double* q = p[f] + k * st[f];
+            v0 *= __ldg(q);
+            v1 *= __ldg(q + st[f]);
+            v2 *= __ldg(q + 2 * st[f]);
+            v3 *= __ldg(q + 3 * st[f]);
+        }
+        c0 += v0;
+        c1 += v1;
+        c2 += v2;
+        c3 += v3;
+    }
+    for (; k < cnt; ++k) {
+        double v = 1.0;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) v *= __ldg(p[f] + k * st[f]);
+        c0 += v;
+    }
+    return (c0 + c1) + (c2 + c3);
+}
+
+// Sum over i = first, first+step, ... < end along dim `inner`, factors based at off[].
+template <int NF>
+__device__ __forceinline__ double line_sum(const StreamArgs& a, const long long* off, int inner, long long first,
+                                           long long end, long long step) {
+    if (first >= end) return 0.0;
+    const double* p[NF];
+    long long st[NF];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+        p[f] = a.ptr[f] + off[f] + first * a.stride[f][inner];
+        st[f] = step * a.stride[f][inner];
+    }
+    return run_sum<NF>(p, st, (end - first + step - 1) / step);
+}
+
+// Calls fn(std::integral_constant<int, NF>) for the runtime factor count.
+template <typename Fn>
+void with_nf(int nf, Fn&& fn) {
+    switch (nf) {
+        case 1: fn(std::integral_constant<int, 1>{}); break;
+        case 2: fn(std::integral_constant<int, 2>{}); break;
+        case 3: fn(std::integral_constant<int, 3>{}); break;
+        case 4: fn(std::integral_constant<int, 4>{}); break;
+        case 5: fn(std::integral_constant<int, 5>{}); break;
+        case 6: fn(std::integral_constant<int, 6>{}); break;
+        case 7: fn(std::integral_constant<int, 7>{}); break;
+        default: fn(std::integral_constant<int, 8>{}); break;
+    }
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -92,6 +155,7 @@ __global__ void stream_elementwise(StreamArgs a, unsigned long long rows, long l
 
 // Full reduction: n_out == 0. `inner` chosen by the host (its dims order puts
 // it last). Block b reduces rows [b*rows/B, (b+1)*rows/B).
+template <int NF>
 __global__ void stream_reduce_all(StreamArgs a, unsigned long long rows, long long inner_n, double* partial) {
     __shared__ double red[32];
     const int D = a.n_sum;
@@ -102,7 +166,7 @@ __global__ void stream_reduce_all(StreamArgs a, unsigned long long rows, long lo
     for (unsigned long long row = lo; row < hi; ++row) {
         long long off[kMaxFactors] = {};
         Digits::offsets(a, row, 0, D - 1, off);
-        for (long long i = threadIdx.x; i < inner_n; i += blockDim.x) acc += product_at(a, off, i, inner);
+        acc += line_sum<NF>(a, off, inner, threadIdx.x, inner_n, blockDim.x);
     }
     const double t = block_sum(acc, red);
     if (threadIdx.x == 0) partial[blockIdx.x] = t;
@@ -111,6 +175,7 @@ __global__ void stream_reduce_all(StreamArgs a, unsigned long long rows, long lo
 // Summed-dim-fast reduction: one warp per output; lanes walk the innermost
 // summed dim (unit stride in the dominant factors), the other summed dims
 // are the "rows".
+template <int NF>
 __global__ void stream_reduce_warp(StreamArgs a, unsigned long long outputs,
                                    unsigned long long srows) {
     const int lane = threadIdx.x & 31;
@@ -126,7 +191,7 @@ __global__ void stream_reduce_warp(StreamArgs a, unsigned long long outputs,
 #pragma unroll
         for (int f = 0; f < kMaxFactors; ++f) off[f] = base[f];
         Digits::offsets(a, sr, a.n_out, a.n_sum - 1, off);
-        for (long long i = lane; i < a.n; i += 32) acc += product_at(a, off, i, inner);
+        acc += line_sum<NF>(a, off, inner, lane, a.n, 32);
     }
     acc = warp_sum(acc);
     if (lane == 0) put(a, o, a.scale * acc);
@@ -136,6 +201,7 @@ __global__ void stream_reduce_warp(StreamArgs a, unsigned long long outputs,
 // the innermost output dim), sequential sum over a slice of the summed space.
 // gridDim.y slices split the summed space for parallelism; slice partials go
 // to partial[slice * outputs + o] and are added in slice order afterwards.
+template <int NF>
 __global__ void stream_reduce_thread(StreamArgs a, unsigned long long outputs,
                                      unsigned long long sflat, double* partial) {
     const unsigned long long o = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
@@ -144,8 +210,9 @@ __global__ void stream_reduce_thread(StreamArgs a, unsigned long long outputs,
     const unsigned long long lo = sflat * blockIdx.y / S, hi = sflat * (blockIdx.y + 1) / S;
     long long base[kMaxFactors] = {};
     Digits::offsets(a, o, 0, a.n_out, base);
-    // odometer over the summed dims, starting at `lo`
-    const int first = a.n_out, D = a.n_sum;
+    // odometer over the summed dims, starting at `lo`; the innermost summed
+    // dim is walked in runs (up to the slice end or the end of the dim)
+    const int first = a.n_out, D = a.n_sum, last = first + D - 1;
     long long digit[kMaxDims];
     {
         unsigned long long flat = lo;
@@ -159,16 +226,17 @@ __global__ void stream_reduce_thread(StreamArgs a, unsigned long long outputs,
     for (int f = 0; f < kMaxFactors; ++f) {
         off[f] = base[f];
         if (f < a.nf)
-            for (int d = 0; d < D; ++d) off[f] += digit[d] * a.stride[f][first + d];
+            for (int d = 0; d < D - 1; ++d) off[f] += digit[d] * a.stride[f][first + d];
     }
     double acc = 0.0;
-    for (unsigned long long s = lo; s < hi; ++s) {
-        double v = 1.0;
-#pragma unroll
-        for (int f = 0; f < kMaxFactors; ++f)
-            if (f < a.nf) v *= __ldg(a.ptr[f] + off[f]);
-        acc += v;
-        for (int d = D - 1; d >= 0; --d) {
+    unsigned long long s = lo;
+    while (s < hi) {
+        const long long run = static_cast<long long>(
+            (hi - s) < static_cast<unsigned long long>(a.n - digit[D - 1]) ? (hi - s) : (a.n - digit[D - 1]));
+        acc += line_sum<NF>(a, off, last, digit[D - 1], digit[D - 1] + run, 1);
+        s += static_cast<unsigned long long>(run);
+        digit[D - 1] = 0;
+        for (int d = D - 2; d >= 0; --d) {
             if (++digit[d] < a.n) {
 #pragma unroll
                 for (int f = 0; f < kMaxFactors; ++f)
@@ -254,8 +322,18 @@ std::size_t stream_scratch_entries(const StreamArgs& a, int sm_count) {
 //  - n_out == 0          -> two-stage full reduction
 //  - innermost summed dim has the unit strides -> warp per output
 //  - otherwise           -> thread per output (+ summed-space slicing)
-int launch_stream(const StreamArgs& a, double* scratch, std::size_t scratch_entries,
+__device__ const double kUnitFactor = 1.0;
+
+int launch_stream(const StreamArgs& args, double* scratch, std::size_t scratch_entries,
                   int sm_count, cudaStream_t s) {
+    StreamArgs a = args;
+    if (a.nf == 0 && a.n_out + a.n_sum > 0) {  // a pure count: one broadcast unit factor
+        void* one = nullptr;
+        if (cudaGetSymbolAddress(&one, kUnitFactor) != cudaSuccess) return -1;
+        a.nf = 1;
+        a.ptr[0] = static_cast<const double*>(one);
+        for (int d = 0; d < kMaxDims; ++d) a.stride[0][d] = 0;
+    }
     if (a.n_out + a.n_sum == 0) {
         stream_product<<<1, 32, 0, s>>>(a);
         return 1;
@@ -274,7 +352,9 @@ int launch_stream(const StreamArgs& a, double* scratch, std::size_t scratch_entr
         const unsigned long long rows = D >= 2 ? span(a, D - 1) : 1;
         const long long inner_n = D == 1 ? ext0(a) : a.n;
         const int blocks = blocks_for_all(rows, inner_n, sm_count);
-        stream_reduce_all<<<blocks, kThreads, 0, s>>>(a, rows, inner_n, scratch);
+        with_nf(a.nf, [&](auto nf) {
+            stream_reduce_all<decltype(nf)::value><<<blocks, kThreads, 0, s>>>(a, rows, inner_n, scratch);
+        });
         finalize_scalar<<<1, 1024, 0, s>>>(scratch, static_cast<unsigned long long>(blocks), a.scale, a.out,
                                            a.accumulate);
         return 2;
@@ -290,7 +370,9 @@ int launch_stream(const StreamArgs& a, double* scratch, std::size_t scratch_entr
     if (unit_sum > unit_out || (unit_sum == unit_out && outputs < static_cast<unsigned long long>(sm_count) * 256)) {
         const unsigned long long srows = ipow(a.n, a.n_sum - 1);
         const unsigned long long blocks = (outputs + (kThreads / 32) - 1) / (kThreads / 32);
-        stream_reduce_warp<<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(a, outputs, srows);
+        with_nf(a.nf, [&](auto nf) {
+            stream_reduce_warp<decltype(nf)::value><<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(a, outputs, srows);
+        });
         return 1;
     }
     const unsigned long long sflat = ipow(a.n, a.n_sum);
@@ -300,8 +382,10 @@ int launch_stream(const StreamArgs& a, double* scratch, std::size_t scratch_entr
         if (slices > 1024) slices = 1024;
     }
     const unsigned gx = static_cast<unsigned>((outputs + kThreads - 1) / kThreads);
-    stream_reduce_thread<<<dim3(gx, static_cast<unsigned>(slices)), kThreads, 0, s>>>(a, outputs, sflat,
-                                                                                   scratch);
+    with_nf(a.nf, [&](auto nf) {
+        stream_reduce_thread<decltype(nf)::value>
+            <<<dim3(gx, static_cast<unsigned>(slices)), kThreads, 0, s>>>(a, outputs, sflat, scratch);
+    });
     if (slices > 1) {
         finalize_columns<<<gx, kThreads, 0, s>>>(scratch, slices, outputs, a.scale, a.out, a.accumulate);
         return 2;

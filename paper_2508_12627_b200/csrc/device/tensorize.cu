@@ -27,6 +27,47 @@ __global__ void rbf(const double* __restrict__ x, long long n, int d, double sca
     out[i * n + j] = exp(-scale * s);
 }
 
+// Symmetric tiled form: one 32x32 tile pair (ti <= tj) per block, sample
+// rows staged in shared memory, exp evaluated once per unordered pair and
+// written to both (i, j) and (j, i) with coalesced stores (the transpose goes
+// through a padded smem tile). Same per-entry arithmetic as `rbf`, so the
+// matrix is identical and bitwise symmetric.
+constexpr int kRbfTile = 32, kRbfMaxDim = 64;
+__global__ void rbf_sym(const double* __restrict__ x, long long n, int d, double scale, double* __restrict__ out) {
+    const int ti = blockIdx.y, tj = blockIdx.x;
+    if (ti > tj) return;
+    __shared__ double xi[kRbfTile][kRbfMaxDim + 1], xj[kRbfTile][kRbfMaxDim + 1];
+    __shared__ double t[kRbfTile][kRbfTile + 1];
+    const long long i0 = static_cast<long long>(ti) * kRbfTile, j0 = static_cast<long long>(tj) * kRbfTile;
+    const int tid = threadIdx.y * kRbfTile + threadIdx.x;
+    for (int e = tid; e < kRbfTile * d; e += kRbfTile * 8) {
+        const int r = e / d, c = e - r * d;
+        xi[r][c] = i0 + r < n ? x[(i0 + r) * d + c] : 0.0;
+        xj[r][c] = j0 + r < n ? x[(j0 + r) * d + c] : 0.0;
+    }
+    __syncthreads();
+    const int cj = threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < kRbfTile / 8; ++k) {
+        const int ri = threadIdx.y + 8 * k;
+        double s = 0.0;
+        for (int c = 0; c < d; ++c) {
+            const double u = xi[ri][c] - xj[cj][c];
+            s += u * u;
+        }
+        const double v = exp(-scale * s);
+        t[ri][cj] = v;
+        if (i0 + ri < n && j0 + cj < n) out[(i0 + ri) * n + j0 + cj] = v;
+    }
+    if (ti == tj) return;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kRbfTile / 8; ++k) {
+        const int rj = threadIdx.y + 8 * k;  // row j0 + rj of the mirror tile
+        if (j0 + rj < n && i0 + cj < n) out[(j0 + rj) * n + i0 + cj] = t[cj][rj];
+    }
+}
+
 // out_ij = left_i * (sum_c z_ic z_jc) * right_j   (hoif.cpp:50-72 components)
 __global__ void scaled_gram(const double* __restrict__ x, long long n, int d, int col_left, int col_right, int z0,
                             int k, double* __restrict__ out) {
@@ -90,8 +131,13 @@ __global__ void times_small(const double* __restrict__ z, long long n, int F, co
 }  // namespace
 
 void launch_rbf(const double* x, long long n, int d, double bandwidth, double* out, cudaStream_t s) {
-    rbf<<<dim3(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(n)), 256, 0, s>>>(
-        x, n, d, 0.5 / (bandwidth * bandwidth), out);
+    const double scale = 0.5 / (bandwidth * bandwidth);
+    if (d <= kRbfMaxDim) {
+        const unsigned T = static_cast<unsigned>((n + kRbfTile - 1) / kRbfTile);
+        rbf_sym<<<dim3(T, T), dim3(kRbfTile, 8), 0, s>>>(x, n, d, scale, out);
+        return;
+    }
+    rbf<<<dim3(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(n)), 256, 0, s>>>(x, n, d, scale, out);
 }
 
 void launch_scaled_gram(const double* x, long long n, int d, int col_left, int col_right, int z0, int k, double* out,
