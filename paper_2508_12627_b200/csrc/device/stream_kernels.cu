@@ -11,6 +11,8 @@
 // shared-memory tree, then an in-order pass over block partials): results are
 // bit-reproducible run to run.
 #include <cstdio>
+#include <map>
+#include <mutex>
 #include <type_traits>
 
 #include "kernels.hpp"
@@ -107,6 +109,73 @@ void with_nf(int nf, Fn&& fn) {
         default: fn(std::integral_constant<int, 8>{}); break;
     }
 }
+
+// ------------------------------------------------ paired (16-byte) fast path
+// When every factor walks the inner dim with stride 1 (loaded as double2) or
+// 0 (a per-line constant), lines are streamed as aligned pairs: 16-byte
+// loads, four independent chains per thread. The host checks alignment.
+
+template <int NF>
+__device__ __forceinline__ void line_offsets(const StreamArgs& a, unsigned long long flat, int first, int count,
+                                             long long* off) {
+#pragma unroll
+    for (int f = 0; f < NF; ++f) off[f] = 0;
+    for (int d = first + count - 1; d >= first; --d) {
+        const unsigned long long q = flat / static_cast<unsigned long long>(a.n);
+        const long long digit = static_cast<long long>(flat - q * static_cast<unsigned long long>(a.n));
+        flat = q;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) off[f] += digit * a.stride[f][d];
+    }
+}
+
+template <int NF>
+struct PairLine {
+    const double2* p[NF];
+    double c[NF];
+    bool unit[NF];
+    __device__ __forceinline__ void setup(const StreamArgs& a, const long long* off, int inner) {
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            const double* q = a.ptr[f] + off[f];
+            unit[f] = a.stride[f][inner] != 0;
+            p[f] = reinterpret_cast<const double2*>(q);
+            c[f] = unit[f] ? 0.0 : __ldg(q);
+        }
+    }
+    __device__ __forceinline__ double2 at(long long q) const {
+        double2 v = make_double2(1.0, 1.0);
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            if (unit[f]) {
+                const double2 x = __ldg(p[f] + q);
+                v.x *= x.x;
+                v.y *= x.y;
+            } else {
+                v.x *= c[f];
+                v.y *= c[f];
+            }
+        }
+        return v;
+    }
+    // sum over pairs q = first, first+step, ... < end
+    __device__ __forceinline__ double sum(long long first, long long end, long long step) const {
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+        long long q = first;
+        for (; q + 3 * step < end; q += 4 * step) {
+            const double2 v0 = at(q), v1 = at(q + step), v2 = at(q + 2 * step), v3 = at(q + 3 * step);
+            c0 += v0.x + v0.y;
+            c1 += v1.x + v1.y;
+            c2 += v2.x + v2.y;
+            c3 += v3.x + v3.y;
+        }
+        for (; q < end; q += step) {
+            const double2 v = at(q);
+            c0 += v.x + v.y;
+        }
+        return (c0 + c1) + (c2 + c3);
+    }
+};
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -255,6 +324,94 @@ __global__ void stream_reduce_thread(StreamArgs a, unsigned long long outputs,
         partial[blockIdx.y * outputs + o] = acc;
 }
 
+// Paired variants of the three kernels above (inner extent even, every
+// factor's inner stride 0 or 1, 16-byte aligned lines).
+template <int NF>
+__global__ void __launch_bounds__(256) stream_elementwise_pairs(StreamArgs a, unsigned long long rows,
+                                                                long long inner_n) {
+    const int inner = a.n_out - 1, rdim = a.n_out - 2;
+    const unsigned long long B = gridDim.x;
+    const unsigned long long lo = rows * blockIdx.x / B, hi = rows * (blockIdx.x + 1) / B;
+    const long long pairs = inner_n >> 1;
+    long long off[NF], rs[NF];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) rs[f] = rdim >= 0 ? a.stride[f][rdim] : 0;
+    long long digit = 0;
+    bool fresh = true;
+    for (unsigned long long row = lo; row < hi; ++row) {
+        if (fresh) {
+            line_offsets<NF>(a, row, 0, a.n_out - 1, off);
+            digit = rdim > 0 ? static_cast<long long>(row % static_cast<unsigned long long>(a.n)) : 0;
+            fresh = false;
+        }
+        PairLine<NF> L;
+        L.setup(a, off, inner);
+        double2* out = reinterpret_cast<double2*>(a.out + row * inner_n);
+        for (long long q = threadIdx.x; q < pairs; q += blockDim.x) {
+            double2 v = L.at(q);
+            v.x *= a.scale;
+            v.y *= a.scale;
+            if (a.accumulate) {
+                const double2 o = out[q];
+                v.x += o.x;
+                v.y += o.y;
+            }
+            out[q] = v;
+        }
+        ++digit;
+        if (rdim == 0 || digit < a.n) {
+#pragma unroll
+            for (int f = 0; f < NF; ++f) off[f] += rs[f];
+        } else {
+            fresh = true;
+        }
+    }
+}
+
+template <int NF>
+__global__ void __launch_bounds__(256) stream_reduce_all_pairs(StreamArgs a, unsigned long long rows,
+                                                               long long inner_n, double* partial) {
+    __shared__ double red[32];
+    const int D = a.n_sum;
+    const int inner = D - 1;
+    const unsigned long long B = gridDim.x;
+    const unsigned long long lo = rows * blockIdx.x / B, hi = rows * (blockIdx.x + 1) / B;
+    double acc = 0.0;
+    for (unsigned long long row = lo; row < hi; ++row) {
+        long long off[NF];
+        line_offsets<NF>(a, row, 0, D - 1, off);
+        PairLine<NF> L;
+        L.setup(a, off, inner);
+        acc += L.sum(threadIdx.x, inner_n >> 1, blockDim.x);
+    }
+    const double t = block_sum(acc, red);
+    if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+template <int NF>
+__global__ void __launch_bounds__(256) stream_reduce_warp_pairs(StreamArgs a, unsigned long long outputs,
+                                                                unsigned long long srows) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long o =
+        blockIdx.x * static_cast<unsigned long long>(blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (o >= outputs) return;
+    const int inner = a.n_out + a.n_sum - 1;
+    long long base[NF];
+    line_offsets<NF>(a, o, 0, a.n_out, base);
+    double acc = 0.0;
+    for (unsigned long long sr = 0; sr < srows; ++sr) {
+        long long off[NF];
+        line_offsets<NF>(a, sr, a.n_out, a.n_sum - 1, off);
+#pragma unroll
+        for (int f = 0; f < NF; ++f) off[f] += base[f];
+        PairLine<NF> L;
+        L.setup(a, off, inner);
+        acc += L.sum(lane, a.n >> 1, 32);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) put(a, o, a.scale * acc);
+}
+
 // out[o] = scale * sum_{p < P} partial[p * outputs + o], in p order.
 __global__ void finalize_columns(const double* partial, unsigned long long P,
                                  unsigned long long outputs, double scale, double* out, int accumulate) {
@@ -324,6 +481,38 @@ std::size_t stream_scratch_entries(const StreamArgs& a, int sm_count) {
 //  - otherwise           -> thread per output (+ summed-space slicing)
 __device__ const double kUnitFactor = 1.0;
 
+namespace {
+// Resident blocks per SM of a kernel at kThreads (cached per kernel).
+template <typename K>
+int resident_blocks(K kernel) {
+    static std::mutex mu;
+    static std::map<const void*, int> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    const void* key = reinterpret_cast<const void*>(kernel);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0) != cudaSuccess || b < 1) b = 1;
+    cache[key] = b;
+    return b;
+}
+
+// The paired fast path applies when the inner extent is even and every factor
+// walks the inner dim with stride 0 or 1 from 16-byte aligned line starts.
+bool pairs_ok(const StreamArgs& a, int inner, long long inner_n, int dims) {
+    if ((inner_n & 1) != 0) return false;
+    for (int f = 0; f < a.nf; ++f) {
+        const long long si = a.stride[f][inner];
+        if (si != 0 && si != 1) return false;
+        if (si == 0) continue;
+        if ((reinterpret_cast<unsigned long long>(a.ptr[f]) & 15) != 0) return false;
+        for (int d = 0; d < dims; ++d)
+            if (d != inner && (a.stride[f][d] & 1) != 0) return false;
+    }
+    return true;
+}
+}  // namespace
+
 int launch_stream(const StreamArgs& args, double* scratch, std::size_t scratch_entries,
                   int sm_count, cudaStream_t s) {
     StreamArgs a = args;
@@ -341,6 +530,15 @@ int launch_stream(const StreamArgs& args, double* scratch, std::size_t scratch_e
     if (a.n_sum == 0) {
         const unsigned long long rows = a.n_out >= 2 ? span(a, a.n_out - 1) : 1;
         const long long inner_n = a.n_out == 1 ? ext0(a) : a.n;
+        if (pairs_ok(a, a.n_out - 1, inner_n, a.n_out) && (reinterpret_cast<unsigned long long>(a.out) & 15) == 0) {
+            with_nf(a.nf, [&](auto nf) {
+                auto k = stream_elementwise_pairs<decltype(nf)::value>;
+                unsigned long long blocks = static_cast<unsigned long long>(sm_count) * resident_blocks(k);
+                if (blocks > rows) blocks = rows;
+                k<<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(a, rows, inner_n);
+            });
+            return 1;
+        }
         const unsigned gx = static_cast<unsigned>((inner_n + kThreads - 1) / kThreads);
         unsigned long long gy = rows;
         if (gy > 65535) gy = 65535;
@@ -351,9 +549,14 @@ int launch_stream(const StreamArgs& args, double* scratch, std::size_t scratch_e
         const int D = a.n_sum;
         const unsigned long long rows = D >= 2 ? span(a, D - 1) : 1;
         const long long inner_n = D == 1 ? ext0(a) : a.n;
-        const int blocks = blocks_for_all(rows, inner_n, sm_count);
+        // one full wave of resident blocks (never more than the scratch holds)
+        int blocks = blocks_for_all(rows, inner_n, sm_count);
+        const bool pairs = pairs_ok(a, D - 1, inner_n, D);
         with_nf(a.nf, [&](auto nf) {
-            stream_reduce_all<decltype(nf)::value><<<blocks, kThreads, 0, s>>>(a, rows, inner_n, scratch);
+            auto k = pairs ? stream_reduce_all_pairs<decltype(nf)::value> : stream_reduce_all<decltype(nf)::value>;
+            const int wave = sm_count * resident_blocks(k);
+            if (blocks > wave) blocks = wave;
+            k<<<blocks, kThreads, 0, s>>>(a, rows, inner_n, scratch);
         });
         finalize_scalar<<<1, 1024, 0, s>>>(scratch, static_cast<unsigned long long>(blocks), a.scale, a.out,
                                            a.accumulate);
@@ -370,8 +573,14 @@ int launch_stream(const StreamArgs& args, double* scratch, std::size_t scratch_e
     if (unit_sum > unit_out || (unit_sum == unit_out && outputs < static_cast<unsigned long long>(sm_count) * 256)) {
         const unsigned long long srows = ipow(a.n, a.n_sum - 1);
         const unsigned long long blocks = (outputs + (kThreads / 32) - 1) / (kThreads / 32);
+        const bool pairs = pairs_ok(a, last, a.n, last + 1);
         with_nf(a.nf, [&](auto nf) {
-            stream_reduce_warp<decltype(nf)::value><<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(a, outputs, srows);
+            if (pairs)
+                stream_reduce_warp_pairs<decltype(nf)::value>
+                    <<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(a, outputs, srows);
+            else
+                stream_reduce_warp<decltype(nf)::value>
+                    <<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(a, outputs, srows);
         });
         return 1;
     }
