@@ -161,6 +161,22 @@ US_API int us_optimize_order(int32_t K, const int32_t* tuple_len, const int32_t*
 US_API int us_treewidth(int32_t n, int32_t edge_count, const int32_t* edges, int32_t* width_out,
                  int32_t* order_out);
 
+/* complexity_report (proj/include/ustats/complexity.hpp:46-47, host only):
+ * lattice sizes, the survivors' exact quotient-treewidth histogram and the
+ * exact decimal FLOP estimate K * sum_w count_w * n^(w+1) (into flops[0..cap),
+ * NUL-terminated). Tuples may be 0- or 1-based (canonicalized as
+ * validate_notation does). treewidth_exact is -1 when m exceeds
+ * cfg->exact_treewidth_bound. */
+typedef struct us_complexity {
+    int32_t index_count, extent, graph_vertices, graph_edges;
+    int32_t treewidth_lower, treewidth_upper, treewidth_exact, max_quotient_width;
+    uint64_t bell_count, sparsified_count;
+    uint64_t count_by_width[16]; /* [w] = survivors whose quotient has treewidth w */
+} us_complexity;
+US_API int us_complexity_report(int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx,
+                                int32_t extent, const us_config* cfg, us_complexity* out,
+                                char* flops, int32_t cap);
+
 /* Term sharding plan (host only): for the sparsified lattice of the
  * signature at extent n over world_size ranks, owner_out[t] receives the rank
  * that evaluates survivor t (LPT on n^(width+1)), cost_out[t] its estimate. */

@@ -39,6 +39,8 @@ def lib():
                                     C.c_int, F64P, F64P]
         _lib.ref_optimize_order.argtypes = [C.c_int, I32P, I32P, I32P, I32P]
         _lib.ref_u_statistic_data.argtypes = [C.c_char_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64, F64P, F64P]
+        _lib.ref_complexity_report.argtypes = [C.c_int, I32P, I32P, C.c_int, I32P, C.POINTER(C.c_uint64),
+                                               C.POINTER(C.c_uint64), C.c_char_p, C.c_int]
         _lib.ref_last_error.restype = C.c_char_p
     return _lib
 
@@ -163,3 +165,18 @@ def u_statistic_data(spec, data, threads=0, cap=0):
     _check(lib().ref_u_statistic_data(spec.encode(), C.c_void_p(x.ctypes.data), x.shape[0], x.shape[1], threads, cap,
                                       C.byref(out), st))
     return out.value, dict(zip(STAT_KEYS, list(st)))
+
+
+def complexity_report(signature, extent):
+    """The reference's complexity_report as a dict (same keys as the engine's)."""
+    K, L, I = _enc(signature)
+    ints = (C.c_int * 8)()
+    counts = (C.c_uint64 * 2)()
+    hist = (C.c_uint64 * 16)()
+    buf = C.create_string_buffer(512)
+    _check(lib().ref_complexity_report(K, L, I, int(extent), ints, counts, hist, buf, 512))
+    return {"index_count": ints[0], "extent": ints[1], "graph_vertices": ints[2], "graph_edges": ints[3],
+            "treewidth_lower": ints[4], "treewidth_upper": ints[5],
+            "treewidth_exact": None if ints[6] < 0 else ints[6], "max_quotient_width": ints[7],
+            "bell_count": counts[0], "sparsified_count": counts[1],
+            "count_by_width": {w: int(c) for w, c in enumerate(hist) if c}, "flops_estimate": buf.value.decode()}

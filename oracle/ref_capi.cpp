@@ -7,6 +7,7 @@
 // einsum.hpp:41-43, bruteforce.hpp:20-36) over caller-owned row-major f64
 // tensors, so Python can drive the reference exactly as a user would.
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -16,6 +17,7 @@
 #include <memory>
 #include <span>
 
+#include "ustats/complexity.hpp"
 #include "ustats/ustats.hpp"
 
 namespace {
@@ -254,6 +256,40 @@ int ref_optimize_order(int K, const int* tuple_len, const int* tuple_idx, int* o
         for (std::size_t i = 0; i < o.order.size(); ++i) order_out[i] = o.order[i];
         *width_out = o.predicted_width;
         return static_cast<int>(o.order.size()) >= 0 ? 0 : 1;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+// complexity_report (complexity.cpp:73-127): ints[8] = index_count, extent,
+// graph_vertices, graph_edges, treewidth_lower, treewidth_upper,
+// treewidth_exact (-1 absent), max_quotient_width; counts[2] = bell,
+// sparsified; hist[16] by width; flops decimal into buf[cap].
+int ref_complexity_report(int K, const int* tuple_len, const int* tuple_idx, int extent, int* ints,
+                          std::uint64_t* counts, std::uint64_t* hist, char* buf, int cap) {
+    try {
+        std::vector<ustats::IndexTuple> raw;
+        int off = 0;
+        for (int k = 0; k < K; ++k) {
+            raw.emplace_back(tuple_idx + off, tuple_idx + off + tuple_len[k]);
+            off += tuple_len[k];
+        }
+        auto r = ustats::complexity_report(raw, extent);
+        ints[0] = r.index_count;
+        ints[1] = r.extent;
+        ints[2] = r.graph_vertices;
+        ints[3] = r.graph_edges;
+        ints[4] = r.treewidth_lower;
+        ints[5] = r.treewidth_upper;
+        ints[6] = r.treewidth_exact ? *r.treewidth_exact : -1;
+        ints[7] = r.max_quotient_width;
+        counts[0] = r.bell_count;
+        counts[1] = r.sparsified_count;
+        for (int w = 0; w < 16; ++w) hist[w] = 0;
+        for (const auto& [w, c] : r.count_by_width)
+            if (w >= 0 && w < 16) hist[w] = c;
+        std::snprintf(buf, static_cast<std::size_t>(cap), "%s", r.flops_estimate.c_str());
+        return 0;
     } catch (const std::exception& e) {
         return status_of(e);
     }

@@ -51,6 +51,22 @@ class UsStats(C.Structure):
         return {name: getattr(self, name) for name, _ in self._fields_}
 
 
+class UsComplexity(C.Structure):
+    _fields_ = [
+        ("index_count", i32),
+        ("extent", i32),
+        ("graph_vertices", i32),
+        ("graph_edges", i32),
+        ("treewidth_lower", i32),
+        ("treewidth_upper", i32),
+        ("treewidth_exact", i32),
+        ("max_quotient_width", i32),
+        ("bell_count", u64),
+        ("sparsified_count", u64),
+        ("count_by_width", u64 * 16),
+    ]
+
+
 # name -> (restype, argtypes); exactly the declarations of include/ustats_b200.h
 SIGNATURES = {
     "us_version": (C.c_char_p, []),
@@ -76,6 +92,7 @@ SIGNATURES = {
     "us_survivors": (C.c_int, [i32, i32, P(i32), P(i32), i32, P(i32), P(i32), P(i64), P(u64)]),
     "us_optimize_order": (C.c_int, [i32, P(i32), P(i32), i32, P(i32), P(i32), P(i32)]),
     "us_treewidth": (C.c_int, [i32, i32, P(i32), P(i32), P(i32)]),
+    "us_complexity_report": (C.c_int, [i32, P(i32), P(i32), i32, P(UsConfig), P(UsComplexity), C.c_char_p, i32]),
     "us_plan_terms": (C.c_int, [i32, i32, P(i32), P(i32), i64, i32, i32, P(i32), P(i32), P(f64)]),
     "us_plan_summary": (C.c_int, [i32, i32, P(i32), P(i32), i64, P(UsConfig), i32, C.c_char_p, u64, P(u64)]),
     "us_nccl_unique_id": (C.c_int, [C.c_void_p]),

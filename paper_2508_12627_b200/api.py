@@ -468,6 +468,47 @@ def treewidth(n: int, edges):
     return w.value, [order[i] for i in range(n)]
 
 
+@dataclass
+class ComplexityReport:
+    """``ustats::ComplexityReport`` (complexity.hpp:19-44)."""
+    index_count: int
+    extent: int
+    graph_vertices: int
+    graph_edges: int
+    treewidth_lower: int
+    treewidth_upper: int
+    treewidth_exact: int | None
+    bell_count: int
+    sparsified_count: int
+    count_by_width: dict
+    max_quotient_width: int
+    flops_estimate: str
+
+
+def complexity_report(signature, extent: int, config: Config | None = None) -> ComplexityReport:
+    """``complexity_report`` (complexity.hpp:46-47): lattice sizes, the
+    survivors' exact quotient-treewidth histogram and the exact FLOP estimate.
+    Tuples may be 0- or 1-based."""
+    K, L, I = _signature(signature)
+    out = N.UsComplexity()
+    buf = C.create_string_buffer(512)
+    _check(N.lib().us_complexity_report(K, L, I, int(extent), C.byref(_cfg(config)), C.byref(out), buf, 512))
+    return ComplexityReport(
+        index_count=out.index_count, extent=out.extent, graph_vertices=out.graph_vertices,
+        graph_edges=out.graph_edges, treewidth_lower=out.treewidth_lower, treewidth_upper=out.treewidth_upper,
+        treewidth_exact=None if out.treewidth_exact < 0 else out.treewidth_exact,
+        bell_count=out.bell_count, sparsified_count=out.sparsified_count,
+        count_by_width={w: int(c) for w, c in enumerate(out.count_by_width) if c},
+        max_quotient_width=out.max_quotient_width, flops_estimate=buf.value.decode())
+
+
+def chain_signature(m: int):
+    """``chain_signature`` (complexity.hpp:51): ((1,2),...,(m-1,m)), 1-based."""
+    if m < 2:
+        raise UStatsError("InvalidArgument", "chain signature needs order >= 2")
+    return [(i, i + 1) for i in range(1, m)]
+
+
 def device_stream(device: int = -1) -> int:
     """The engine's cudaStream_t on `device` (as an int handle)."""
     h = C.c_void_p()

@@ -12,6 +12,7 @@
 #include "device/executor.hpp"
 #include "device/tensorize.hpp"
 #include "ustats/ustats.hpp"
+#include "ustats/complexity.hpp"
 
 namespace ustats::dev {
 double combine_terms(const std::vector<double>& terms);
@@ -417,6 +418,41 @@ int us_optimize_order(int32_t K, const int32_t* tuple_len, const int32_t* tuple_
         for (std::size_t i = 0; i < o.order.size(); ++i) order_out[i] = o.order[i];
         *index_count = notation.index_count;
         *width_out = o.predicted_width;
+    });
+}
+
+int us_complexity_report(int32_t K, const int32_t* tuple_len, const int32_t* tuple_idx, int32_t extent,
+                         const us_config* cfg, us_complexity* out, char* flops, int32_t cap) {
+    return guarded([&] {
+        if (K < 0 || (K > 0 && (!tuple_len || !tuple_idx)) || !out)
+            ustats::fail(ustats::ErrorCode::InvalidArgument, "null argument");
+        std::vector<ustats::IndexTuple> raw;
+        int off = 0;
+        for (int k = 0; k < K; ++k) {
+            raw.emplace_back(tuple_idx + off, tuple_idx + off + tuple_len[k]);
+            off += tuple_len[k];
+        }
+        const auto r = ustats::complexity_report(raw, extent, to_config(cfg));
+        us_complexity c{};
+        c.index_count = r.index_count;
+        c.extent = r.extent;
+        c.graph_vertices = r.graph_vertices;
+        c.graph_edges = r.graph_edges;
+        c.treewidth_lower = r.treewidth_lower;
+        c.treewidth_upper = r.treewidth_upper;
+        c.treewidth_exact = r.treewidth_exact ? *r.treewidth_exact : -1;
+        c.max_quotient_width = r.max_quotient_width;
+        c.bell_count = r.bell_count;
+        c.sparsified_count = r.sparsified_count;
+        for (const auto& [w, count] : r.count_by_width)
+            if (w >= 0 && w < 16) c.count_by_width[w] = count;
+        *out = c;
+        if (flops && cap > 0) {
+            if (static_cast<int32_t>(r.flops_estimate.size()) >= cap)
+                ustats::fail(ustats::ErrorCode::InvalidArgument, "flops buffer too small");
+            std::copy(r.flops_estimate.begin(), r.flops_estimate.end(), flops);
+            flops[r.flops_estimate.size()] = '\0';
+        }
     });
 }
 

@@ -383,6 +383,34 @@ std::string Program::desc(const View& v, const std::vector<int>& dims) const {
     return out + "]";
 }
 
+// Canonical content key of a stream op: factor descriptors over (out dims,
+// summed dims), minimised over the order of the summed dims.
+std::string Program::stream_key(const std::vector<View>& factors, const std::vector<int>& out_ids,
+                                std::uint32_t sum) const {
+    std::vector<int> sums = ids_of(sum);
+    std::sort(sums.begin(), sums.end());
+    std::string best;
+    do {
+        std::vector<int> dims = out_ids;
+        dims.insert(dims.end(), sums.begin(), sums.end());
+        std::vector<std::string> ds;
+        for (const View& v : factors) ds.push_back(desc(v, dims));
+        std::sort(ds.begin(), ds.end());
+        std::string k = "S" + std::to_string(out_ids.size()) + ":";
+        for (auto& d : ds) k += d;
+        if (best.empty() || k < best) best = k;
+    } while (std::next_permutation(sums.begin(), sums.end()));
+    return best;
+}
+
+int Program::lookup_stream(const std::vector<View>& factors, const std::vector<int>& out_ids,
+                           std::uint32_t sum) const {
+    if (!sharing() || factors.size() > static_cast<std::size_t>(kMaxFactors)) return -1;
+    if (static_cast<int>(out_ids.size()) + std::popcount(sum) > kMaxDims) return -1;
+    auto hit = memo_.find(stream_key(factors, out_ids, sum));
+    return hit == memo_.end() ? -1 : hit->second;
+}
+
 int Program::stream(std::vector<View> factors, const std::vector<int>& out_ids, std::uint32_t sum, double* ext) {
     // keep within the kernel's factor budget: form the product of the leading
     // factors over their own ids first
@@ -397,20 +425,7 @@ int Program::stream(std::vector<View> factors, const std::vector<int>& out_ids, 
         fail(ErrorCode::InvalidArgument, "contraction step spans too many indices for the stream kernel");
     std::string key;
     if (sharing()) {
-        std::vector<int> sums = ids_of(sum);
-        std::sort(sums.begin(), sums.end());
-        std::string best;
-        do {
-            std::vector<int> dims = out_ids;
-            dims.insert(dims.end(), sums.begin(), sums.end());
-            std::vector<std::string> ds;
-            for (const View& v : factors) ds.push_back(desc(v, dims));
-            std::sort(ds.begin(), ds.end());
-            std::string k = "S" + std::to_string(out_ids.size()) + ":";
-            for (auto& d : ds) k += d;
-            if (best.empty() || k < best) best = k;
-        } while (std::next_permutation(sums.begin(), sums.end()));
-        key = best;
+        key = stream_key(factors, out_ids, sum);
         if (ext) {
             key = "X" + key;
             auto hit = term_memo_.find(key);
@@ -1323,6 +1338,15 @@ std::vector<View> Contractor::formed(const Slot& s) {
     return {p_.view_of(b, layout)};
 }
 
+void Contractor::settle(Slot& s) {
+    const std::uint32_t pend = ids_of_views(s.factors) & ~s.ids;
+    if (!pend) return;
+    std::vector<int> layout = ids_of(s.ids);
+    const int b = p_.lookup_stream(s.factors, layout, pend);
+    if (b < 0) return;
+    s.factors = {p_.view_of(b, layout)};
+}
+
 Contractor::Slot Contractor::marginalize(const Slot& s, std::uint32_t summed) {
     const int kept = std::popcount(s.ids & ~summed);
     cap(kept);
@@ -1424,6 +1448,7 @@ void Contractor::eliminate_one(std::vector<Slot>& slots, int e) {
     }
     if (parts.empty()) return;
     if (count_) ++count_->steps;
+    for (Slot& p : parts) settle(p);
 
     for (bool folded = true; folded && parts.size() > 1;) {
         folded = false;
@@ -1438,6 +1463,7 @@ void Contractor::eliminate_one(std::vector<Slot>& slots, int e) {
                 }
                 if (count_) count_->ref_madds += pw(std::popcount(parts[j].ids));
                 std::vector<View> src = formed(parts[i]);  // a pending sum must not leak into the target
+                settle(parts[j]);  // the target's own pending sum may be the op just formed
                 parts[j].factors.insert(parts[j].factors.end(), src.begin(), src.end());
                 parts.erase(parts.begin() + static_cast<std::ptrdiff_t>(i));
                 folded = true;
@@ -1490,6 +1516,7 @@ int Contractor::run(const std::vector<int>& inputs, const EinsumNotation& notati
     const int out_order = static_cast<int>(notation.output.size());
     cap(out_order);
     if (count_) count_->ref_madds += pw(out_order) * slots.size();
+    for (Slot& s : slots) settle(s);
     std::size_t widest = 0;
     auto pend = [&](const Slot& s) { return ids_of_views(s.factors) & ~s.ids; };
     for (std::size_t i = 0; i < slots.size(); ++i)
@@ -1636,6 +1663,11 @@ void record_terms(Program& prog, const TermPlan& plan, const std::vector<int>& i
                 o.order = cand;
                 Contractor(prog, nullptr).run(inputs, nt, o, d_v + t);
                 const double c = prog.cost_since(mk);
+                if (std::getenv("USTATS_ORDER_DEBUG")) {
+                    std::fprintf(stderr, "[order] term %zu cand", t);
+                    for (int id : cand) std::fprintf(stderr, " %d", id);
+                    std::fprintf(stderr, " cost %.4g\n", c);
+                }
                 prog.rollback(mk);
                 if (best_cost < 0 || c < best_cost * (1 - 1e-12)) {
                     best_cost = c;

@@ -211,8 +211,11 @@ class Program {
     View view_of(int buf, const IndexTuple& layout) const;
 
     // Records out[out_ids] = sum_{sum} prod(factors). With `ext`, writes there
-    // (never shared) and returns -1; else returns the (possibly shared) buffer.
+    // and returns -1 (a repeat of an earlier term's op becomes a term alias);
+    // else returns the (possibly shared) buffer.
     int stream(std::vector<View> factors, const std::vector<int>& out_ids, std::uint32_t sum, double* ext);
+    // The buffer an identical earlier stream op produced, or -1 (records nothing).
+    int lookup_stream(const std::vector<View>& factors, const std::vector<int>& out_ids, std::uint32_t sum) const;
     // Records a GEMM; returns the buffer and the caller-side layout (ids).
     int gemm(std::vector<View> fa, std::vector<View> fb, const std::vector<int>& ra, const std::vector<int>& rb,
              int e, std::vector<int>* layout);
@@ -252,6 +255,7 @@ class Program {
     std::vector<Op> ops_;
     std::unordered_map<std::string, int> memo_;
     std::vector<std::string> memo_log_;
+    std::string stream_key(const std::vector<View>& factors, const std::vector<int>& out_ids, std::uint32_t sum) const;
     std::map<std::string, double*> term_memo_;  // canonical key of a term-final op -> its slot
     std::vector<std::pair<double*, double*>> aliases_;
     std::map<int, bool> keep_;
@@ -289,6 +293,7 @@ class Contractor {
     Slot gemm_step(const Slot& a, const Slot& b, int e);
     Slot generic_step(const std::vector<Slot>& parts, int e);
     std::vector<View> formed(const Slot& s);  // factors with pending sums formed
+    void settle(Slot& s);                     // pending sums an earlier op already formed
     void cap(int order);
     void owned(int order);
     std::uint64_t pw(int e) const;
