@@ -107,6 +107,19 @@ US_API int us_u_statistic_data(const char* kernel, const double* data, int64_t n
  * e.g. hoif_tau's chain orders, hoif.cpp:74-100). Statistic s has arity m[s]
  * and K[s] components; tuple_len / tuple_idx / factors are the per-statistic
  * encodings concatenated in statistic order. u_out receives S values. */
+/* Callers of the path (SURVEY 8b "callers to keep working"), evaluated on the
+ * device end to end:
+ * us_dcov_squared: dcov_squared (dcov.hpp:22-23) of paired samples x (n x dx)
+ *   and y (n x dy), row-major, host or device; the four U-statistics share one
+ *   program. SampleTooSmall below 4 pairs.
+ * us_motif_count: motif_count (motifs.hpp:47-48) of motif id "r1".."r8" in the
+ *   graph on vertices 0..n-1 given by edge_count (u, v) pairs (host int32);
+ *   NonIntegerResult when the scaled count is not integral. */
+US_API int us_dcov_squared(const double* x, int32_t dx, const double* y, int32_t dy, int64_t n,
+                           int32_t on_device, const us_config* cfg, double* out, us_stats* stats);
+US_API int us_motif_count(int64_t n, int64_t edge_count, const int32_t* edges, const char* motif_id,
+                          const us_config* cfg, int64_t* count, us_stats* stats);
+
 US_API int us_u_statistic_batch(int32_t S, const int32_t* m, const int32_t* K, const int32_t* tuple_len,
                                 const int32_t* tuple_idx, const double* const* factors, int64_t n,
                                 int32_t on_device, const us_config* cfg, double* u_out, us_stats* stats);

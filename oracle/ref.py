@@ -41,6 +41,8 @@ def lib():
         _lib.ref_u_statistic_data.argtypes = [C.c_char_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64, F64P, F64P]
         _lib.ref_complexity_report.argtypes = [C.c_int, I32P, I32P, C.c_int, I32P, C.POINTER(C.c_uint64),
                                                C.POINTER(C.c_uint64), C.c_char_p, C.c_int]
+        _lib.ref_dcov_squared.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, F64P]
+        _lib.ref_motif_count.argtypes = [C.c_int, C.c_int, I32P, C.c_char_p, C.c_int, C.POINTER(C.c_longlong)]
         _lib.ref_last_error.restype = C.c_char_p
     return _lib
 
@@ -180,3 +182,24 @@ def complexity_report(signature, extent):
             "treewidth_exact": None if ints[6] < 0 else ints[6], "max_quotient_width": ints[7],
             "bell_count": counts[0], "sparsified_count": counts[1],
             "count_by_width": {w: int(c) for w, c in enumerate(hist) if c}, "flops_estimate": buf.value.decode()}
+
+
+def dcov_squared(x, y, threads=0):
+    """The reference's dcov_squared on paired samples (rows = observations)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    x = x.reshape(x.shape[0], -1)
+    y = y.reshape(y.shape[0], -1)
+    out = C.c_double()
+    _check(lib().ref_dcov_squared(x.ctypes.data, x.shape[1], y.ctypes.data, y.shape[1], x.shape[0], threads,
+                                  C.byref(out)))
+    return out.value
+
+
+def motif_count(n, edges, motif_id, threads=0):
+    """The reference's motif_count on the graph over vertices 0..n-1."""
+    e = np.ascontiguousarray(np.asarray(edges, dtype=np.int32).reshape(-1, 2))
+    out = C.c_longlong()
+    _check(lib().ref_motif_count(int(n), e.shape[0], e.ctypes.data_as(C.POINTER(C.c_int)), motif_id.encode(),
+                                 threads, C.byref(out)))
+    return out.value

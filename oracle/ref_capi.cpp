@@ -18,6 +18,8 @@
 #include <span>
 
 #include "ustats/complexity.hpp"
+#include "ustats/dcov.hpp"
+#include "ustats/motifs.hpp"
 #include "ustats/ustats.hpp"
 
 namespace {
@@ -289,6 +291,35 @@ int ref_complexity_report(int K, const int* tuple_len, const int* tuple_idx, int
         for (const auto& [w, c] : r.count_by_width)
             if (w >= 0 && w < 16) hist[w] = c;
         std::snprintf(buf, static_cast<std::size_t>(cap), "%s", r.flops_estimate.c_str());
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+// dcov_squared (dcov.cpp:35-87) on row-major paired samples.
+int ref_dcov_squared(const double* x, int dx, const double* y, int dy, int n, int threads, double* out) {
+    try {
+        std::vector<ustats::Observation> xs(static_cast<std::size_t>(n)), ys(static_cast<std::size_t>(n));
+        for (int i = 0; i < n; ++i) {
+            xs[static_cast<std::size_t>(i)].assign(x + static_cast<std::size_t>(i) * dx, x + static_cast<std::size_t>(i + 1) * dx);
+            ys[static_cast<std::size_t>(i)].assign(y + static_cast<std::size_t>(i) * dy, y + static_cast<std::size_t>(i + 1) * dy);
+        }
+        ustats::Sample sx(std::move(xs)), sy(std::move(ys));
+        *out = ustats::dcov_squared(sx, sy, config_of(threads, 0));
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+// motif_count (motifs.cpp:53-69) on the graph over vertices 0..n-1.
+int ref_motif_count(int n, int edge_count, const int* edges, const char* id, int threads, long long* out) {
+    try {
+        ustats::SimpleGraph g;
+        for (int v = 0; v < n; ++v) g.add_vertex(v);
+        for (int e = 0; e < edge_count; ++e) g.add_edge(edges[2 * e], edges[2 * e + 1]);
+        *out = ustats::motif_count(g, ustats::motif_by_id(id), config_of(threads, 0));
         return 0;
     } catch (const std::exception& e) {
         return status_of(e);

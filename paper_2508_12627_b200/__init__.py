@@ -10,7 +10,7 @@ from .api import (  # noqa: F401
     eliminate_index, kernel_tensors, optimize_order, plan_summary, plan_terms, restricted_v_tensors, survivors, treewidth,
     ComplexityReport, chain_signature, complexity_report,
     u_statistic, u_statistic_batch, u_statistic_tensors, u_statistic_unsparsified_tensors, u_terms,
-    v_statistic, hoif_tau,
+    v_statistic, hoif_tau, dcov_squared, motif_count, MOTIF_IDS,
     v_statistic_tensors,
 )
 from ._native import LIB_PATH, lib  # noqa: F401

@@ -394,6 +394,53 @@ def u_statistic(kernel: str, data, threads: int = 0, config: Config | None = Non
     return (out.value, st.as_dict()) if with_stats else out.value
 
 
+def _sample_arg(data, label):
+    """(ptr, n, d, on_device, keepalive) of an n x d float64 sample."""
+    if hasattr(data, "data_ptr"):
+        if str(data.dtype) != "torch.float64" or not data.is_contiguous() or data.dim() not in (1, 2):
+            raise UStatsError("InvalidArgument", f"{label} must be a contiguous float64 tensor")
+        d = data.shape[1] if data.dim() == 2 else 1
+        return data.data_ptr(), data.shape[0], d, 1 if getattr(data, "is_cuda", False) else 0, data
+    x = np.ascontiguousarray(data, dtype=np.float64)
+    if x.ndim == 1:
+        x = x.reshape(-1, 1)
+    if x.ndim != 2:
+        raise UStatsError("InvalidArgument", f"{label} must be a 2-D array (rows = observations)")
+    return x.ctypes.data, x.shape[0], x.shape[1], 0, x
+
+
+def dcov_squared(x, y, config: Config | None = None, with_stats: bool = False):
+    """``dcov_squared`` (dcov.hpp:22-23): unbiased squared distance covariance
+    of paired samples (rows = observations), from four U-statistics over the
+    Euclidean distance matrices, built and evaluated on the GPU."""
+    px, nx, dx, ox, kx = _sample_arg(x, "x")
+    py, ny, dy, oy, ky = _sample_arg(y, "y")
+    if nx != ny:
+        raise UStatsError("InvalidArgument", "paired samples must have equal sizes")
+    if ox != oy:
+        raise UStatsError("InvalidArgument", "x and y must both be host or both be device arrays")
+    out = N.f64()
+    st = N.UsStats()
+    _check(N.lib().us_dcov_squared(C.c_void_p(px), dx, C.c_void_p(py), dy, nx, ox,
+                                   C.byref((config or Config()).native()), C.byref(out), C.byref(st)))
+    del kx, ky
+    return (out.value, st.as_dict()) if with_stats else out.value
+
+
+MOTIF_IDS = ("r1", "r2", "r3", "r4", "r5", "r6", "r7", "r8")
+
+
+def motif_count(n: int, edges, motif_id: str, config: Config | None = None, with_stats: bool = False):
+    """``motif_count`` (motifs.hpp:47-48): induced copies of motif r1..r8 in the
+    graph on vertices 0..n-1 with the given (u, v) edges."""
+    e = np.ascontiguousarray(np.asarray(edges, dtype=np.int32).reshape(-1, 2))
+    out = N.i64()
+    st = N.UsStats()
+    _check(N.lib().us_motif_count(int(n), e.shape[0], e.ctypes.data_as(C.POINTER(N.i32)), motif_id.encode(),
+                                  C.byref((config or Config()).native()), C.byref(out), C.byref(st)))
+    return (out.value, st.as_dict()) if with_stats else out.value
+
+
 def v_statistic(kernel: str, data, threads: int = 0, config: Config | None = None):
     """``_ustats.v_statistic`` (ustats_py.cpp:104-113)."""
     factors, sig, m = kernel_tensors(kernel, data)

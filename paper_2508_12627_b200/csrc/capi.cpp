@@ -227,6 +227,28 @@ int us_u_statistic_data(const char* kernel, const double* data, int64_t n, int32
     });
 }
 
+int us_dcov_squared(const double* x, int32_t dx, const double* y, int32_t dy, int64_t n, int32_t on_device,
+                    const us_config* cfg, double* out, us_stats* stats) {
+    return guarded([&] {
+        if (!x || !y || !out) ustats::fail(ustats::ErrorCode::InvalidArgument, "null argument");
+        auto r = ustats::dev::dcov_squared(x, dx, y, dy, n, on_device != 0, to_config(cfg));
+        *out = r.value;
+        export_dev(r, cfg ? cfg->rank : 0, stats);
+    });
+}
+
+int us_motif_count(int64_t n, int64_t edge_count, const int32_t* edges, const char* motif_id, const us_config* cfg,
+                   int64_t* count, us_stats* stats) {
+    return guarded([&] {
+        if (!motif_id || !count || (edge_count > 0 && !edges) || edge_count < 0)
+            ustats::fail(ustats::ErrorCode::InvalidArgument, "null argument");
+        long long c = 0;
+        auto r = ustats::dev::motif_count(n, edges, edge_count, motif_id, to_config(cfg), &c);
+        *count = c;
+        export_dev(r, cfg ? cfg->rank : 0, stats);
+    });
+}
+
 int us_u_statistic_batch(int32_t S, const int32_t* m, const int32_t* K, const int32_t* tuple_len,
                          const int32_t* tuple_idx, const double* const* factors, int64_t n, int32_t on_device,
                          const us_config* cfg, double* u_out, us_stats* stats) {

@@ -1,6 +1,7 @@
 // Data-level entry: parse a kernel spec, tensorize its components on the
 // device from the raw sample, evaluate the U-statistic (engine.cpp:173-193
 // with tensorize, engine.cpp:108-136, moved to the GPU).
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <map>
@@ -245,6 +246,151 @@ StatisticResult u_statistic_data(const std::string& spec, const double* data, lo
     auto res = lattice_batch({spec_in}, true, n, LatticeMode::Sparsified, cfg);
     res[0].stats.kernel_launches += launches;
     return res[0];
+}
+
+}  // namespace ustats::dev
+
+// ------------------------------------------------------------ drivers
+namespace ustats::dev {
+
+namespace {
+
+// Folds the per-statistic results of one shared batch into one report: the
+// device work is the batch's (carried by the first), lattice counters add up.
+StatisticResult merged(std::vector<StatisticResult>& parts, double value) {
+    StatisticResult r = parts[0];
+    r.value = value;
+    for (std::size_t q = 1; q < parts.size(); ++q) {
+        r.enumerated += parts[q].enumerated;
+        r.owner.insert(r.owner.end(), parts[q].owner.begin(), parts[q].owner.end());
+        r.stats.ref_madds += parts[q].stats.ref_madds;
+        r.stats.ref_peak = std::max(r.stats.ref_peak, parts[q].stats.ref_peak);
+    }
+    return r;
+}
+
+}  // namespace
+
+StatisticResult dcov_squared(const double* x, int dx, const double* y, int dy, long long n, bool on_device,
+                             const Config& config) {
+    if (dx < 1 || dy < 1) fail(ErrorCode::InvalidArgument, "observations need at least one coordinate");
+    if (n < 4) fail(ErrorCode::SampleTooSmall, "need at least 4 paired observations, have " + std::to_string(n));
+    checked_entry_count(2, static_cast<int>(n), config);
+    Runtime& rt = Runtime::get(config.device.device);
+    cudaStream_t s = rt.main_stream();
+    rt.set_stream(s);
+    Buf xs, ys;
+    const double* xd = x;
+    const double* yd = y;
+    if (!on_device) {
+        xs = rt.allocate(1, n * dx);
+        ys = rt.allocate(1, n * dy);
+        check_cuda(cudaMemcpyAsync(xs->ptr, x, static_cast<std::size_t>(n * dx) * sizeof(double),
+                                   cudaMemcpyHostToDevice, s), "upload x");
+        check_cuda(cudaMemcpyAsync(ys->ptr, y, static_cast<std::size_t>(n * dy) * sizeof(double),
+                                   cudaMemcpyHostToDevice, s), "upload y");
+        xd = xs->ptr;
+        yd = ys->ptr;
+    }
+    Buf d1 = rt.allocate(2, n), d2 = rt.allocate(2, n);
+    launch_distance(xd, n, dx, 0, dx, d1->ptr, s);
+    launch_distance(yd, n, dy, 0, dy, d2->ptr, s);
+    check_cuda(cudaGetLastError(), "distance");
+    // dcov.cpp:74-77: ((1,2),(3,4)), ((1,2),(1,2)), ((1,2),(1,3)), ((1,2),(2,3)), components (d1, d2)
+    const std::vector<std::pair<int, std::vector<IndexTuple>>> shapes = {
+        {4, {{0, 1}, {2, 3}}}, {2, {{0, 1}, {0, 1}}}, {3, {{0, 1}, {0, 2}}}, {3, {{0, 1}, {1, 2}}}};
+    std::vector<StatisticSpec> specs;
+    for (const auto& [m, sig] : shapes) {
+        StatisticSpec sp;
+        sp.m = m;
+        sp.sig = sig;
+        sp.inputs = {d1->ptr, d2->ptr};
+        sp.symmetric = {1, 1};
+        specs.push_back(std::move(sp));
+    }
+    Config cfg = config;
+    cfg.device.donate_inputs = true;
+    auto res = lattice_batch(specs, true, n, LatticeMode::Sparsified, cfg);
+    // dcov.cpp:79-85, in long double
+    const long double nn = static_cast<long double>(n);
+    long double c = static_cast<long double>(res[0].value) + (nn - 2) * (nn - 3) * static_cast<long double>(res[1].value) -
+                    (nn - 3) * static_cast<long double>(res[2].value) - (nn - 3) * static_cast<long double>(res[3].value);
+    c /= nn * (nn - 1) * (nn - 2) * (nn - 3);
+    StatisticResult r = merged(res, static_cast<double>(c));
+    r.stats.kernel_launches += 2;
+    return r;
+}
+
+const std::vector<MotifSpec>& motif_catalog() {
+    // induced patterns on 3-4 vertices (motifs.hpp:33-36): edges that must be
+    // present / absent, automorphism counts
+    static const std::vector<MotifSpec> cat = {
+        {"r1", 3, 2, {{1, 2}, {2, 3}}, {{1, 3}}},                                  // path P3
+        {"r2", 3, 6, {{1, 2}, {1, 3}, {2, 3}}, {}},                                // triangle
+        {"r3", 4, 6, {{1, 2}, {1, 3}, {1, 4}}, {{2, 3}, {2, 4}, {3, 4}}},          // 3-star
+        {"r4", 4, 2, {{1, 2}, {2, 3}, {3, 4}}, {{1, 3}, {1, 4}, {2, 4}}},          // path P4
+        {"r5", 4, 2, {{1, 2}, {1, 3}, {2, 3}, {3, 4}}, {{1, 4}, {2, 4}}},          // tailed triangle
+        {"r6", 4, 8, {{1, 2}, {2, 3}, {3, 4}, {1, 4}}, {{1, 3}, {2, 4}}},          // 4-cycle
+        {"r7", 4, 4, {{1, 2}, {1, 3}, {1, 4}, {2, 3}, {2, 4}}, {{3, 4}}},          // diamond
+        {"r8", 4, 24, {{1, 2}, {1, 3}, {1, 4}, {2, 3}, {2, 4}, {3, 4}}, {}},       // K4
+    };
+    return cat;
+}
+
+StatisticResult motif_count(long long n, const int* edges, long long edge_count, const std::string& id,
+                            const Config& config, long long* count) {
+    const MotifSpec* spec = nullptr;
+    for (const MotifSpec& m : motif_catalog())
+        if (id == m.id) spec = &m;
+    if (!spec) fail(ErrorCode::InvalidArgument, "unknown motif id '" + id + "' (expected r1..r8)");
+    if (n < 0) fail(ErrorCode::InvalidArgument, "vertex count must be non-negative");
+    for (long long e = 0; e < edge_count; ++e) {
+        const int u = edges[2 * e], v = edges[2 * e + 1];
+        if (u < 0 || v < 0 || u >= n || v >= n)
+            fail(ErrorCode::InvalidArgument, "graph vertex ids must be contiguous 0..n-1");
+        if (u == v) fail(ErrorCode::InvalidArgument, "self-loop on vertex " + std::to_string(u));
+    }
+    StatisticResult r;
+    *count = 0;
+    if (n < spec->order) return r;  // motifs.cpp:59
+    checked_entry_count(2, static_cast<int>(n), config);
+    Runtime& rt = Runtime::get(config.device.device);
+    cudaStream_t s = rt.main_stream();
+    rt.set_stream(s);
+    int* de = nullptr;
+    if (edge_count > 0) {
+        check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&de), static_cast<std::size_t>(edge_count) * 2 * sizeof(int), s),
+                   "alloc edges");
+        check_cuda(cudaMemcpyAsync(de, edges, static_cast<std::size_t>(edge_count) * 2 * sizeof(int),
+                                   cudaMemcpyHostToDevice, s), "upload edges");
+    }
+    Buf a = rt.allocate(2, n), b = rt.allocate(2, n);
+    launch_adjacency(de, edge_count, n, a->ptr, b->ptr, s);
+    check_cuda(cudaGetLastError(), "adjacency");
+    if (de) cudaFreeAsync(de, s);
+    StatisticSpec sp;
+    sp.m = spec->order;
+    for (const auto& [u, v] : spec->present) {
+        sp.sig.push_back({u - 1, v - 1});
+        sp.inputs.push_back(a->ptr);
+        sp.symmetric.push_back(1);
+    }
+    for (const auto& [u, v] : spec->absent) {
+        sp.sig.push_back({u - 1, v - 1});
+        sp.inputs.push_back(b->ptr);
+        sp.symmetric.push_back(1);
+    }
+    Config cfg = config;
+    cfg.device.donate_inputs = true;
+    auto res = lattice_batch({sp}, true, n, LatticeMode::Sparsified, cfg);
+    r = res[0];
+    r.stats.kernel_launches += edge_count > 0 ? 2 : 1;
+    const double scaled = r.value / static_cast<double>(spec->automorphisms);
+    const double rounded = std::nearbyint(scaled);
+    if (std::abs(scaled - rounded) > 1e-6)
+        fail(ErrorCode::NonIntegerResult, "count " + std::to_string(scaled) + " is not an integer");
+    *count = static_cast<long long>(rounded);
+    return r;
 }
 
 }  // namespace ustats::dev

@@ -27,44 +27,82 @@ __global__ void rbf(const double* __restrict__ x, long long n, int d, double sca
     out[i * n + j] = exp(-scale * s);
 }
 
-// Symmetric tiled form: one 32x32 tile pair (ti <= tj) per block, sample
-// rows staged in shared memory, exp evaluated once per unordered pair and
-// written to both (i, j) and (j, i) with coalesced stores (the transpose goes
-// through a padded smem tile). Same per-entry arithmetic as `rbf`, so the
-// matrix is identical and bitwise symmetric.
-constexpr int kRbfTile = 32, kRbfMaxDim = 64;
-__global__ void rbf_sym(const double* __restrict__ x, long long n, int d, double scale, double* __restrict__ out) {
+// Symmetric tiled pair kernels: one 32x32 tile pair (ti <= tj) per block,
+// sample rows staged in shared memory, the entry evaluated once per
+// unordered pair and written to both (i, j) and (j, i) with coalesced stores
+// (the transpose goes through a padded smem tile). The squared distance is
+// summed per coordinate in order, as the reference's per-entry callbacks do,
+// so the matrix is bitwise symmetric.
+//   kind 0: exp(-scale * s)   (RBF)
+//   kind 1: sqrt(s)           (Euclidean distance, dcov.cpp:24-31)
+constexpr int kPairTile = 32, kPairMaxDim = 64;
+template <int KIND>
+__global__ void pair_sym(const double* __restrict__ x, long long n, int d, int c0, int dc, double scale,
+                         double* __restrict__ out) {
     const int ti = blockIdx.y, tj = blockIdx.x;
     if (ti > tj) return;
-    __shared__ double xi[kRbfTile][kRbfMaxDim + 1], xj[kRbfTile][kRbfMaxDim + 1];
-    __shared__ double t[kRbfTile][kRbfTile + 1];
-    const long long i0 = static_cast<long long>(ti) * kRbfTile, j0 = static_cast<long long>(tj) * kRbfTile;
-    const int tid = threadIdx.y * kRbfTile + threadIdx.x;
-    for (int e = tid; e < kRbfTile * d; e += kRbfTile * 8) {
-        const int r = e / d, c = e - r * d;
-        xi[r][c] = i0 + r < n ? x[(i0 + r) * d + c] : 0.0;
-        xj[r][c] = j0 + r < n ? x[(j0 + r) * d + c] : 0.0;
+    __shared__ double xi[kPairTile][kPairMaxDim + 1], xj[kPairTile][kPairMaxDim + 1];
+    __shared__ double t[kPairTile][kPairTile + 1];
+    const long long i0 = static_cast<long long>(ti) * kPairTile, j0 = static_cast<long long>(tj) * kPairTile;
+    const int tid = threadIdx.y * kPairTile + threadIdx.x;
+    for (int e = tid; e < kPairTile * dc; e += kPairTile * 8) {
+        const int r = e / dc, c = e - r * dc;
+        xi[r][c] = i0 + r < n ? x[(i0 + r) * d + c0 + c] : 0.0;
+        xj[r][c] = j0 + r < n ? x[(j0 + r) * d + c0 + c] : 0.0;
     }
     __syncthreads();
     const int cj = threadIdx.x;
 #pragma unroll
-    for (int k = 0; k < kRbfTile / 8; ++k) {
+    for (int k = 0; k < kPairTile / 8; ++k) {
         const int ri = threadIdx.y + 8 * k;
         double s = 0.0;
-        for (int c = 0; c < d; ++c) {
+        for (int c = 0; c < dc; ++c) {
             const double u = xi[ri][c] - xj[cj][c];
             s += u * u;
         }
-        const double v = exp(-scale * s);
+        const double v = KIND == 0 ? exp(-scale * s) : sqrt(s);
         t[ri][cj] = v;
         if (i0 + ri < n && j0 + cj < n) out[(i0 + ri) * n + j0 + cj] = v;
     }
     if (ti == tj) return;
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < kRbfTile / 8; ++k) {
+    for (int k = 0; k < kPairTile / 8; ++k) {
         const int rj = threadIdx.y + 8 * k;  // row j0 + rj of the mirror tile
         if (j0 + rj < n && i0 + cj < n) out[(j0 + rj) * n + i0 + cj] = t[cj][rj];
+    }
+}
+
+// Euclidean distances over columns [c0, c0 + dc) (fallback for wide samples).
+__global__ void distance(const double* __restrict__ x, long long n, int d, int c0, int dc, double* __restrict__ out) {
+    const long long j = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    const long long i = blockIdx.y;
+    if (j >= n) return;
+    double s = 0.0;
+    for (int c = 0; c < dc; ++c) {
+        const double u = x[i * d + c0 + c] - x[j * d + c0 + c];
+        s += u * u;
+    }
+    out[i * n + j] = sqrt(s);
+}
+
+// Graph indicators (motifs.cpp:11-31): A[u][v] = A[v][u] = 1 per edge over a
+// zeroed matrix; the co-indicator B = 1 - A off the diagonal, 0 on it.
+__global__ void scatter_edges(const int* __restrict__ edges, long long count, long long n, double* __restrict__ a) {
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < count;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long u = edges[2 * e], v = edges[2 * e + 1];
+        a[u * n + v] = 1.0;
+        a[v * n + u] = 1.0;
+    }
+}
+
+__global__ void co_indicator(const double* __restrict__ a, long long n, double* __restrict__ b) {
+    const long long total = n * n;
+    for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < total;
+         q += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = q / n, j = q - i * n;
+        b[q] = i == j ? 0.0 : 1.0 - a[q];
     }
 }
 
@@ -132,12 +170,34 @@ __global__ void times_small(const double* __restrict__ z, long long n, int F, co
 
 void launch_rbf(const double* x, long long n, int d, double bandwidth, double* out, cudaStream_t s) {
     const double scale = 0.5 / (bandwidth * bandwidth);
-    if (d <= kRbfMaxDim) {
-        const unsigned T = static_cast<unsigned>((n + kRbfTile - 1) / kRbfTile);
-        rbf_sym<<<dim3(T, T), dim3(kRbfTile, 8), 0, s>>>(x, n, d, scale, out);
+    if (d <= kPairMaxDim) {
+        const unsigned T = static_cast<unsigned>((n + kPairTile - 1) / kPairTile);
+        pair_sym<0><<<dim3(T, T), dim3(kPairTile, 8), 0, s>>>(x, n, d, 0, d, scale, out);
         return;
     }
     rbf<<<dim3(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(n)), 256, 0, s>>>(x, n, d, scale, out);
+}
+
+void launch_distance(const double* x, long long n, int d, int c0, int dc, double* out, cudaStream_t s) {
+    if (dc <= kPairMaxDim) {
+        const unsigned T = static_cast<unsigned>((n + kPairTile - 1) / kPairTile);
+        pair_sym<1><<<dim3(T, T), dim3(kPairTile, 8), 0, s>>>(x, n, d, c0, dc, 0.0, out);
+        return;
+    }
+    distance<<<dim3(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(n)), 256, 0, s>>>(x, n, d, c0, dc,
+                                                                                                  out);
+}
+
+void launch_adjacency(const int* edges, long long count, long long n, double* a, double* b, cudaStream_t s) {
+    cudaMemsetAsync(a, 0, static_cast<std::size_t>(n * n) * sizeof(double), s);
+    if (count > 0) {
+        long long blocks = (count + 255) / 256;
+        if (blocks > 148 * 16) blocks = 148 * 16;
+        scatter_edges<<<static_cast<unsigned>(blocks), 256, 0, s>>>(edges, count, n, a);
+    }
+    long long blocks = (n * n + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    co_indicator<<<static_cast<unsigned>(blocks), 256, 0, s>>>(a, n, b);
 }
 
 void launch_scaled_gram(const double* x, long long n, int d, int col_left, int col_right, int z0, int k, double* out,
