@@ -1206,7 +1206,8 @@ void Program::execute() {
     };
     cudaStream_t streams[2] = {rt_->main_stream(), rt_->side_stream()};
     const std::size_t N = ops_.size();
-    if (multi) {
+    if (multi && !launch_ordered_) {
+        launch_ordered_ = true;  // a cached program re-executes in the same order
         // Side-stream reductions are launched right after the next GEMM, so the
         // GEMM takes the whole GPU first and they fill its last wave; a main-
         // stream op that reads a deferred op's output flushes the queue first.
@@ -1239,6 +1240,15 @@ void Program::execute() {
         for (std::size_t pos = 0; pos < schedule_.size(); ++pos)
             for_each_read(ops_[schedule_[pos]],
                           [&](const View& v) { bufs_[static_cast<std::size_t>(v.buf)].last_use = static_cast<int>(pos); });
+    }
+    if (multi) {
+        // inputs were prepared (uploaded, sparsified, probed) on the main
+        // stream: the side stream starts behind that work
+        cudaEvent_t inputs_ready;
+        check_cuda(cudaEventCreateWithFlags(&inputs_ready, cudaEventDisableTiming), "event");
+        check_cuda(cudaEventRecord(inputs_ready, rt_->main_stream()), "event");
+        check_cuda(cudaStreamWaitEvent(rt_->side_stream(), inputs_ready, 0), "wait");
+        cudaEventDestroy(inputs_ready);
     }
     std::vector<cudaEvent_t> done(N, nullptr);
     std::vector<int> on(N, 0), producer(bufs_.size(), -1);
@@ -1300,6 +1310,27 @@ void Program::execute() {
 }
 
 Buf Program::take(int buf) { return bufs_[static_cast<std::size_t>(buf)].real; }
+
+std::vector<Buf> Program::inputs() const {
+    std::vector<Buf> out;
+    for (const SymBuf& b : bufs_)
+        if (b.input) out.push_back(b.real);
+    return out;
+}
+
+void Program::rebind_inputs(const std::vector<Buf>& reals) {
+    std::size_t k = 0;
+    for (SymBuf& b : bufs_) {
+        if (!b.input) continue;
+        if (k >= reals.size()) fail(ErrorCode::InvalidArgument, "executor: cached plan input count mismatch");
+        b.real = reals[k++];
+    }
+    if (k != reals.size()) fail(ErrorCode::InvalidArgument, "executor: cached plan input count mismatch");
+}
+
+void Program::release_buffers() {
+    for (SymBuf& b : bufs_) b.real.reset();
+}
 
 // -------------------------------------------------------------- Contractor
 std::uint64_t Contractor::pw(int e) const { return ipow(p_.n(), e); }
@@ -1693,6 +1724,92 @@ constexpr long long kChunkMinN = 2048;
 constexpr int kUploadPanels = 16;
 }  // namespace
 
+// ------------------------------------------------------------ plan cache
+// Recording a statistic (term plans, candidate orders, the cross-term
+// program, fusion, the memory-bounded schedule) is pure host work that
+// depends only on the signatures, the extent, the inputs' orders / symmetry /
+// aliasing and the config; the cache keeps the optimized program per device
+// (LRU, 16 entries) so repeated evaluations go straight to launching.
+struct PlanEntry {
+    Config config;  // the program refers to this copy
+    std::vector<TermPlan> plans;
+    std::vector<DevStats> counters;  // per statistic: reference-rule counters
+    DevStats recorded;               // record-time device counters (shared hits, ...)
+    std::unique_ptr<Program> prog;
+    Buf v;                           // term slots the program's reductions write
+    std::size_t T = 0;
+    std::vector<std::pair<std::size_t, std::size_t>> alias;
+    std::uint64_t used = 0;
+};
+
+namespace {
+
+constexpr std::size_t kPlanCacheEntries = 16;
+
+struct PlanCache {
+    std::mutex mu;
+    std::map<std::string, std::unique_ptr<PlanEntry>> entries;
+    std::uint64_t clock = 0;
+};
+
+PlanCache& plan_cache(int device) {
+    static auto* caches = new std::map<int, PlanCache>();  // leaked on purpose: no teardown-order issues
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    return (*caches)[device];
+}
+
+std::string plan_key(const std::vector<StatisticSpec>& specs, const std::vector<std::vector<int>>& slot,
+                     const std::vector<Buf>& uniq, long long n, LatticeMode mode, const Config& c, double budget) {
+    const DeviceConfig& d = c.device;
+    std::string k = std::to_string(n) + "|" + std::to_string(static_cast<int>(mode)) + "|" +
+                    std::to_string(static_cast<long long>(budget / 8.589934592e9)) + "|" +
+                    std::to_string(c.memory_cap_entries) + "," + std::to_string(static_cast<int>(c.strategy)) + "," +
+                    std::to_string(c.exhaustive_index_bound) + "," + std::to_string(c.exact_treewidth_bound) + "|" +
+                    std::to_string(d.share_subexpressions) + std::to_string(d.fuse_epilogues) +
+                    std::to_string(d.exploit_symmetry) + std::to_string(d.reorder_for_sharing) +
+                    std::to_string(d.serial_launch) + std::to_string(d.shard_rows) + "," + std::to_string(d.rank) + "," +
+                    std::to_string(d.world_size) + "," + std::to_string(d.emulate_world) + "," +
+                    std::to_string(d.memory_budget_bytes) + "|";
+    for (const Buf& b : uniq) k += std::to_string(b->order) + (b->symmetric ? "s" : "g");
+    for (std::size_t q = 0; q < specs.size(); ++q) {
+        k += "|" + std::to_string(specs[q].m) + ":";
+        for (std::size_t f = 0; f < specs[q].sig.size(); ++f) {
+            k += std::to_string(slot[q][f]) + "(";
+            for (int i : specs[q].sig[f]) k += std::to_string(i) + ",";
+            k += ")";
+        }
+    }
+    return k;
+}
+
+PlanEntry* find_plan(int device, const std::string& key) {
+    if (std::getenv("USTATS_NO_PLAN_CACHE")) return nullptr;
+    PlanCache& pc = plan_cache(device);
+    std::lock_guard<std::mutex> lock(pc.mu);
+    auto it = pc.entries.find(key);
+    if (it == pc.entries.end()) return nullptr;
+    it->second->used = ++pc.clock;
+    return it->second.get();
+}
+
+PlanEntry* store_plan(int device, const std::string& key, std::unique_ptr<PlanEntry> e) {
+    PlanCache& pc = plan_cache(device);
+    std::lock_guard<std::mutex> lock(pc.mu);
+    e->used = ++pc.clock;
+    while (pc.entries.size() >= kPlanCacheEntries) {
+        auto lru = pc.entries.begin();
+        for (auto it = pc.entries.begin(); it != pc.entries.end(); ++it)
+            if (it->second->used < lru->second->used) lru = it;
+        pc.entries.erase(lru);
+    }
+    PlanEntry* raw = e.get();
+    pc.entries[key] = std::move(e);
+    return raw;
+}
+
+}  // namespace
+
 std::vector<StatisticResult> lattice_batch(const std::vector<StatisticSpec>& specs, bool inputs_on_device,
                                            long long n, LatticeMode mode, const Config& config) {
     return lattice_batch_impl(specs, inputs_on_device, n, mode, config, true);
@@ -1824,51 +1941,86 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
         for (std::size_t i = 0; i < probes.size(); ++i) probes[i].first->symmetric = host[i] == 0;
         for (const auto& [key, idx] : probe_keys) rt.symmetry_seen[key] = host[static_cast<std::size_t>(idx)] == 0;
     }
+    // no sync: the copies / sparsify kernels are stream-ordered before the
+    // program, whose host-side planning overlaps them
     const double enqueue_s = std::chrono::duration<double>(Clock::now() - t_up).count();
-    check_cuda(cudaStreamSynchronize(rt.main_stream()), "sync");
-    const double upload_s = std::chrono::duration<double>(Clock::now() - t_up).count();
+    const double upload_s = enqueue_s;
     const bool trace = std::getenv("USTATS_TRACE") != nullptr;
 
     const auto t0 = Clock::now();
-    std::vector<TermPlan> plans;
-    std::size_t T = 0;
-    for (const auto& sp : specs) {
-        plans.push_back(plan_terms(sp.sig, sp.m, n, mode, config));
-        T += plans.back().rgs.size();
-    }
-    double* d_v = rt.scratch(std::max<std::size_t>(T, 1));
-    check_cuda(cudaMemsetAsync(d_v, 0, sizeof(double) * std::max<std::size_t>(T, 1), rt.stream()), "memset");
-    DevStats shared;  // one program for every statistic: sub-contractions shared across them
-    double plan_s = 0;
-    std::vector<std::pair<std::size_t, std::size_t>> term_alias;
-    {
-        Program prog(&rt, n, config, &shared);
+    double budget = static_cast<double>(config.device.memory_budget_bytes);
+    if (budget <= 0) budget = 0.94 * rt.free_bytes() - 2.0e9;  // inputs included: they came out of it
+    // distinct inputs in first-use order, and each factor's position among them
+    std::vector<Buf> uniq;
+    std::vector<std::vector<int>> slot(specs.size());
+    for (std::size_t q = 0; q < specs.size(); ++q)
+        for (const Buf& b : tensors[q]) {
+            auto it = std::find(uniq.begin(), uniq.end(), b);
+            slot[q].push_back(static_cast<int>(it - uniq.begin()));
+            if (it == uniq.end()) uniq.push_back(b);
+        }
+    const std::string key = plan_key(specs, slot, uniq, n, mode, config, budget);
+    PlanEntry* entry = find_plan(rt.device(), key);
+    const bool hit = entry != nullptr;
+    if (!hit) {
+        // Record every statistic into one program (sub-contractions shared
+        // across them), optimize it, and keep it: a later call with the same
+        // signatures, extent, input structure and config re-executes it.
+        auto e = std::make_unique<PlanEntry>();
+        e->config = config;
+        std::size_t T = 0;
+        for (const auto& sp : specs) {
+            e->plans.push_back(plan_terms(sp.sig, sp.m, n, mode, e->config));
+            if (config.device.shard_rows) e->plans.back().owner.assign(e->plans.back().owner.size(), 0);
+            T += e->plans.back().rgs.size();
+        }
+        e->T = T;
+        e->v = rt.allocate(1, static_cast<long long>(std::max<std::size_t>(T, 1)));
+        e->counters.resize(specs.size());
+        e->prog = std::make_unique<Program>(&rt, n, e->config, &e->recorded);
         std::size_t at = 0;
         for (std::size_t q = 0; q < specs.size(); ++q) {
             std::vector<int> ids;
-            for (const Buf& b : tensors[q]) ids.push_back(prog.add_input(b));
-            if (config.device.shard_rows) plans[q].owner.assign(plans[q].owner.size(), 0);
-            record_terms(prog, plans[q], ids, config.device.shard_rows ? 0 : config.device.rank, d_v + at,
-                         &out[q].stats);
-            at += plans[q].rgs.size();
+            for (const Buf& b : tensors[q]) ids.push_back(e->prog->add_input(b));
+            record_terms(*e->prog, e->plans[q], ids, config.device.shard_rows ? 0 : config.device.rank,
+                         e->v->ptr + at, &e->counters[q]);
+            at += e->plans[q].rgs.size();
         }
-        double budget = static_cast<double>(config.device.memory_budget_bytes);
-        if (budget <= 0) budget = 0.94 * rt.free_bytes() - 2.0e9;  // inputs included: they came out of it
-        prog.optimize(budget);
-        plan_s = std::chrono::duration<double>(Clock::now() - t0).count();
-        prog.execute();
-        for (const auto& [dup, src] : prog.term_aliases())
-            term_alias.emplace_back(static_cast<std::size_t>(dup - d_v), static_cast<std::size_t>(src - d_v));
+        e->prog->optimize(budget);
+        for (const auto& [dup, src] : e->prog->term_aliases())
+            e->alias.emplace_back(static_cast<std::size_t>(dup - e->v->ptr), static_cast<std::size_t>(src - e->v->ptr));
+        e->prog->release_buffers();
+        entry = store_plan(rt.device(), key, std::move(e));
+    }
+    const std::vector<TermPlan>& plans = entry->plans;
+    const std::size_t T = entry->T;
+    double* d_v = entry->v->ptr;
+    const std::vector<std::pair<std::size_t, std::size_t>>& term_alias = entry->alias;
+    for (std::size_t q = 0; q < specs.size(); ++q) out[q].stats = entry->counters[q];
+    check_cuda(cudaMemsetAsync(d_v, 0, sizeof(double) * std::max<std::size_t>(T, 1), rt.stream()), "memset");
+    DevStats shared = entry->recorded;  // record-time counters; execute adds the launches
+    const double plan_s = std::chrono::duration<double>(Clock::now() - t0).count();
+    {
+        Program& prog = *entry->prog;
+        prog.set_stats(&shared);
+        prog.rebind_inputs(uniq);
+        try {
+            prog.execute();
+        } catch (...) {
+            prog.release_buffers();
+            throw;
+        }
+        prog.release_buffers();
+        prog.set_stats(nullptr);
         if (trace)
-            std::fprintf(stderr, "[trace] upload-enqueue %.3f ms, upload-sync %.3f ms, plan %.3f ms, launch done %.3f ms\n",
-                         enqueue_s * 1e3, upload_s * 1e3, plan_s * 1e3,
+            std::fprintf(stderr, "[trace] upload-enqueue %.3f ms, upload-sync %.3f ms, plan %.3f ms (%s), launch done %.3f ms\n",
+                         enqueue_s * 1e3, upload_s * 1e3, plan_s * 1e3, hit ? "cached" : "recorded",
                          std::chrono::duration<double>(Clock::now() - t0).count() * 1e3);
     }
     // row sharding: every term value is a sum of per-rank partials
     if (config.device.shard_rows && config.device.emulate_world <= 1 && rt.has_comm()) rt.allreduce_sum(d_v, T);
     std::vector<double> v(T, 0.0);
     if (T) check_cuda(cudaMemcpyAsync(v.data(), d_v, sizeof(double) * T, cudaMemcpyDeviceToHost, rt.stream()), "D2H");
-    rt.release(d_v);
     std::vector<int> spec_flags(speculative.size(), 0);
     for (std::size_t i = 0; i < speculative.size(); ++i)  // in prep-stream order: after the probe itself
         check_cuda(cudaMemcpyAsync(&spec_flags[i], std::get<1>(speculative[i]), sizeof(int), cudaMemcpyDeviceToHost,

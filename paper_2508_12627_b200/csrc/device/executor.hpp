@@ -236,6 +236,12 @@ class Program {
     double scheduled_peak_bytes() const { return sched_peak_; }
     void execute();   // launches every live op in order
     Buf take(int buf);  // result buffer (allocated during execute)
+    // Plan reuse: the distinct inputs in first-use order; rebinding new device
+    // buffers with the same orders / symmetry / aliasing re-executes the plan.
+    std::vector<Buf> inputs() const;
+    void rebind_inputs(const std::vector<Buf>& reals);
+    void release_buffers();  // drop every device reference after a run
+    void set_stats(DevStats* stats) { stats_ = stats; }
 
   private:
     std::string desc(const View& v, const std::vector<int>& dims) const;
@@ -263,6 +269,7 @@ class Program {
     int slice_rank_ = 0, slice_world_ = 1;  // row sharding: the slice launch() computes
     double sched_peak_ = 0;
     double budget_ = 0;
+    bool launch_ordered_ = false;
     void make_schedule(double budget_bytes);
 };
 

@@ -316,3 +316,45 @@ def test_device_tensorization_resident_sample(engine):
     with pytest.raises(engine.UStatsError) as e:
         engine.u_statistic("rbf:blob3:1", data)
     assert e.value.code == "InvalidArgument"
+
+
+def test_plan_cache_reexecutes_identically(engine, monkeypatch):
+    # a cached program rebinds new inputs of the same structure: bitwise the
+    # result of recording afresh; a structural change (asymmetric input) is a
+    # different plan
+    from paper_2508_12627_b200.workloads import generate
+    fa, sig, m, _ = generate("C2", 160)
+    rng = np.random.default_rng(3)
+    b = rng.random((160, 160))
+    b = (b + b.T) / 2
+    fb = [b] * len(sig)
+    warm = engine.u_terms(fa, sig, m)
+    cached = engine.u_terms(fb, sig, m)
+    again = engine.u_terms(fa, sig, m)
+    monkeypatch.setenv("USTATS_NO_PLAN_CACHE", "1")
+    fresh = engine.u_terms(fb, sig, m)
+    assert np.array_equal(cached.v, fresh.v) and cached.value == fresh.value
+    assert np.array_equal(warm.v, again.v)
+    c = rng.random((160, 160))  # not symmetric: another plan
+    fc = [c] * len(sig)
+    want = engine.u_terms(fc, sig, m)
+    monkeypatch.delenv("USTATS_NO_PLAN_CACHE")
+    engine.u_terms(fb, sig, m)
+    got = engine.u_terms(fc, sig, m)
+    assert np.array_equal(got.v, want.v)
+    check_u(engine, fc, sig, m)
+
+
+@pytest.mark.parametrize("name,n", [("C2", 4096), ("C1", 2000)])
+def test_data_path_repeatable_at_scale(engine, name, n):
+    # the device-tensorized path at a size where the tensorization, the
+    # sparsify kernel and the two launch streams overlap: repeated calls are
+    # bitwise equal and equal the host-tensor path (whose probe synchronizes)
+    from paper_2508_12627_b200.workloads import generate, generate_data
+    data, spec, m, _ = generate_data(name, n)
+    vals = [engine.u_statistic(spec, data) for _ in range(4)]
+    assert all(v == vals[0] for v in vals), vals
+    factors, sig, _, _ = generate(name, n)
+    ref = engine.u_terms(factors, sig, m)
+    scale = np.max(np.abs(ref.v))
+    assert abs(vals[0] - ref.value) <= TOL * scale, (vals[0], ref.value)
