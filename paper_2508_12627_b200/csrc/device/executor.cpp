@@ -122,6 +122,20 @@ double* Runtime::scratch(std::size_t entries) {
     return static_cast<double*>(p);
 }
 
+const double* Runtime::ones(long long n) {
+    if (n > ones_n_) {
+        // grown buffers stay allocated (in-flight kernels may still read them)
+        const long long len = std::max<long long>(n, 1 << 16);
+        void* p = nullptr;
+        check_cuda(cudaMalloc(&p, static_cast<std::size_t>(len) * sizeof(double)), "cudaMalloc");
+        const std::vector<double> host(static_cast<std::size_t>(len), 1.0);
+        check_cuda(cudaMemcpy(p, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice), "ones");
+        ones_.push_back(static_cast<double*>(p));
+        ones_n_ = len;
+    }
+    return ones_.back();
+}
+
 void Runtime::release(double* p) {
     if (p) cudaFreeAsync(p, cur_);
 }
@@ -298,6 +312,10 @@ Program::Totals Program::totals() const {
             }
             t.gemm_macs += macs;
             t.fused += op.epis.size();
+        } else if (op.sweep) {
+            ++t.streams;
+            t.stream_entries += ipow(n_, 2);
+            t.fused += op.epis.size();
         } else {
             ++t.streams;
             t.stream_entries += ipow(n_, static_cast<int>(op.out_ids.size()) + std::popcount(op.sum)) *
@@ -330,6 +348,13 @@ std::string Program::dump() const {
             for (const Op::Epi& e : op.epis)
                 line += std::string(" | epi ") + modes[e.mode] + " pow=" + std::to_string(e.self_power) +
                         (e.w.empty() ? "" : " W:" + vs(e.w)) + (e.ext ? " -> term" : " -> b" + std::to_string(e.out));
+        } else if (op.sweep) {
+            line += "SWEEP X:" + vs(op.factors);
+            for (const Op::Epi& e : op.epis)
+                line += std::string(" | ") + modes[e.mode] + " pow=" + std::to_string(e.self_power) +
+                        (e.w.empty() ? "" : " W:" + vs(e.w)) + (e.ext ? " -> term" : " -> b" + std::to_string(e.out));
+            out += line + "\n";
+            continue;
         } else {
             line += "STREAM out=[";
             for (int id : op.out_ids) line += std::to_string(id) + " ";
@@ -650,6 +675,238 @@ void Program::fuse_epilogues() {
     }
 }
 
+// Sweep fusion. Reductions over a 2-index space that each stream the same
+// n x n matrix X (C3: B~ is read by ~15 reductions across the lattice) are
+// merged into one pass over X, one consumer per reduction: X read
+// row-major (a symmetric X in either orientation), its power, up to four
+// weights over the same two indices, and a scalar / row-vector / matrix
+// output. Only mutually independent consumers share a sweep.
+void Program::fuse_sweeps() {
+    struct Cand {
+        std::size_t op;
+        Op::Epi epi;
+    };
+    // candidates: live stream ops over two indices reading an order-2 buffer X
+    auto candidates = [&] {
+        std::map<int, std::vector<Cand>> by_x;
+        for (std::size_t i = 0; i < ops_.size(); ++i) {
+            const Op& s = ops_[i];
+            if (s.dead || s.gemm || s.sweep) continue;
+            std::uint32_t space = s.sum;
+            for (int id : s.out_ids) space |= bit(id);
+            if (std::popcount(space) != 2) continue;
+            const int a = std::countr_zero(space), b = 31 - std::countl_zero(space);
+            std::map<int, int> count;  // X: the order-2 buffer over exactly {a, b} read most often
+            for (const View& v : s.factors)
+                if (v.ids == space && bufs_[static_cast<std::size_t>(v.buf)].order == 2) ++count[v.buf];
+            int xb = -1, best = 0;
+            for (const auto& [buf, c] : count)
+                if (c > best) {
+                    best = c;
+                    xb = buf;
+                }
+            if (xb < 0 || best > 4) continue;
+            const bool xsym = bufs_[static_cast<std::size_t>(xb)].symmetric;
+            const View* x0 = nullptr;
+            for (const View& v : s.factors)
+                if (v.buf == xb && v.ids == space) {
+                    x0 = &v;
+                    break;
+                }
+            // the sweep's row index: the output index of a row reduction, the
+            // first output index of a store, else X's leading index
+            int R, mode;
+            if (s.out_ids.empty()) {
+                mode = kEpiSumAll;
+                R = x0->stride[static_cast<std::size_t>(a)] == n_ ? a : b;
+            } else if (s.out_ids.size() == 1) {
+                mode = kEpiSumCols;
+                R = s.out_ids[0];
+            } else {
+                continue;  // elementwise outputs stay stream ops
+            }
+            const int Cc = R == a ? b : a;
+            bool ok = true;
+            int power = 0;
+            std::vector<View> w;
+            for (const View& v : s.factors) {
+                if (v.buf == xb && v.ids == space) {
+                    const long long sr = v.stride[static_cast<std::size_t>(R)], sc = v.stride[static_cast<std::size_t>(Cc)];
+                    if (!((sr == n_ && sc == 1) || (xsym && sr == 1 && sc == n_))) ok = false;
+                    ++power;
+                } else {
+                    if (v.ids & ~space) ok = false;
+                    w.push_back(v);
+                }
+            }
+            int nrow = 0, ncol = 0;
+            for (const View& v : w) {
+                if (!ok) break;
+                const auto [wr, wc] = sweep_strides(v, R, Cc);
+                if (wc != 0 && wc != 1) ok = false;
+                nrow += wc == 0;
+                ncol += wc == 1;
+            }
+            if (!ok || nrow > 4 || ncol > 0) continue;  // row weights only: consumers share the power sums
+            Op::Epi e;
+            e.mode = mode;
+            e.w = std::move(w);
+            e.self_power = power;
+            e.row_id = R;
+            e.col_id = Cc;
+            e.out = s.out;
+            e.ext = s.ext;
+            by_x[xb].push_back({i, std::move(e)});
+        }
+        return by_x;
+    };
+    for (bool merged = true; merged;) {
+        merged = false;
+        // transitive producers over the current (possibly already swept) program
+        const std::size_t N = ops_.size();
+        std::vector<int> producer(bufs_.size(), -1);
+        for (std::size_t i = 0; i < N; ++i) {
+            const Op& op = ops_[i];
+            if (op.dead) continue;
+            if (!op.ext && op.out >= 0 && (!op.gemm || op.store)) producer[static_cast<std::size_t>(op.out)] = static_cast<int>(i);
+            for (const Op::Epi& e : op.epis)
+                if (!e.ext && e.out >= 0) producer[static_cast<std::size_t>(e.out)] = static_cast<int>(i);
+        }
+        const std::size_t words = (N + 63) / 64;
+        std::vector<std::uint64_t> deps(N * words, 0);
+        std::vector<char> state(N, 0);
+        auto close = [&](auto&& self, std::size_t i) -> void {
+            if (state[i] == 2) return;
+            state[i] = 1;
+            for_each_read(ops_[i], [&](const View& v) {
+                const int p = producer[static_cast<std::size_t>(v.buf)];
+                if (p < 0 || static_cast<std::size_t>(p) == i) return;
+                const auto pp = static_cast<std::size_t>(p);
+                if (state[pp] != 2) self(self, pp);
+                for (std::size_t w = 0; w < words; ++w) deps[i * words + w] |= deps[pp * words + w];
+                deps[i * words + pp / 64] |= std::uint64_t{1} << (pp % 64);
+            });
+            state[i] = 2;
+        };
+        for (std::size_t i = 0; i < N; ++i)
+            if (!ops_[i].dead) close(close, i);
+        auto depends = [&](std::size_t i, std::size_t j) { return (deps[i * words + j / 64] >> (j % 64)) & 1; };
+        // Matrix weights tie their buffers' lifetimes to the sweep: allowed
+        // only while X plus every such weight stays a small share of the
+        // memory budget (C3: 2 GiB matrices yes; C5: 32 GiB ones no)
+        const double mat = 8.0 * static_cast<double>(n_) * static_cast<double>(n_);
+        const double room = budget_ > 0 ? 0.25 * budget_ : 0.25 * 179.0 * 1073741824.0;
+        for (auto& [xb, cands] : candidates()) {
+            if (cands.size() < 2) continue;
+            std::vector<Cand> group;
+            std::vector<int> mats;
+
+            for (Cand& c : cands) {
+                if (group.size() >= static_cast<std::size_t>(kMaxSweep)) break;
+                bool indep = true;
+                for (const Cand& g : group)
+                    if (depends(c.op, g.op) || depends(g.op, c.op)) indep = false;
+                if (!indep) continue;
+                std::vector<int> m2 = mats;
+                for (const View& v : c.epi.w)
+                    if (bufs_[static_cast<std::size_t>(v.buf)].order >= 2 &&
+                        std::find(m2.begin(), m2.end(), v.buf) == m2.end())
+                        m2.push_back(v.buf);
+                if (!m2.empty() && mat * static_cast<double>(m2.size() + 1) > room) continue;
+                mats = std::move(m2);
+                group.push_back(std::move(c));
+            }
+            if (group.size() < 2) continue;
+            Op sw;
+            sw.sweep = true;
+            View xv;
+            xv.buf = xb;
+            xv.ids = bit(0) | bit(1);  // positional: 0 = row, 1 = column
+            xv.stride[0] = n_;
+            xv.stride[1] = 1;
+            sw.factors = {xv};
+            for (Cand& c : group) {
+                sw.epis.push_back(std::move(c.epi));
+                ops_[c.op].dead = true;
+            }
+            if (stats_) stats_->fused_epilogues += group.size();
+            ops_.push_back(std::move(sw));
+            merged = true;
+            break;  // recompute dependencies with the new sweep in place
+        }
+    }
+}
+
+// (row stride, column stride) of a sweep weight; a symmetric matrix read
+// column-major is read row-major instead. Column stride 0 = a row weight,
+// 1 = a column stream; anything else cannot join a sweep.
+std::pair<long long, long long> Program::sweep_strides(const View& v, int row_id, int col_id) const {
+    long long wr = v.ids & bit(row_id) ? v.stride[static_cast<std::size_t>(row_id)] : 0;
+    long long wc = v.ids & bit(col_id) ? v.stride[static_cast<std::size_t>(col_id)] : 0;
+    if (bufs_[static_cast<std::size_t>(v.buf)].symmetric && wr == 1 && wc == n_) {
+        wr = n_;
+        wc = 1;
+    }
+    return {wr, wc};
+}
+
+void Program::run_sweep(const Op& op) {
+    SweepArgs a;
+    a.x = ptr(op.factors[0].buf);
+    a.xr = n_;
+    a.cols = n_;
+    a.r0 = 0;
+    a.r1 = n_;
+    if (slice_world_ > 1) {
+        a.r0 = n_ * slice_rank_ / slice_world_;
+        a.r1 = n_ * (slice_rank_ + 1) / slice_world_;
+        a.accumulate = 1;
+        if (a.r1 <= a.r0) return;
+    }
+    const int blocks = sweep_blocks(a.r1 - a.r0, rt_->sm_count());
+    std::size_t scalars = 0;
+    for (const Op::Epi& e : op.epis) scalars += e.mode == kEpiSumAll;
+    double* scratch = scalars ? rt_->scratch(scalars * static_cast<std::size_t>(blocks)) : nullptr;
+    std::size_t at = 0;
+    for (const Op::Epi& e : op.epis) {
+        SweepOut& o = a.o[a.count++];
+        o.mode = e.mode == kEpiSumAll ? kSweepAll : kSweepRow;
+        o.power = e.self_power;
+        for (const View& v : e.w) {
+            const auto [wr, wc] = sweep_strides(v, e.row_id, e.col_id);
+            if (wc != 0 || o.nrow >= 4) fail(ErrorCode::InvalidArgument, "executor: sweep weight is not a row weight");
+            o.rowv[o.nrow] = ptr(v.buf);
+            o.rows_stride[o.nrow++] = wr;
+        }
+        if (e.ext) {
+            o.out = e.ext;
+        } else {
+            SymBuf& b = bufs_[static_cast<std::size_t>(e.out)];
+            if (!b.real) {
+                b.real = rt_->allocate(b.order, n_);
+                if (slice_world_ > 1)
+                    check_cuda(cudaMemsetAsync(b.real->ptr, 0, b.real->entries() * sizeof(double), rt_->stream()),
+                               "memset");
+            }
+            o.out = b.real->ptr;
+        }
+        if (o.mode == kSweepAll) {
+            o.partial = scratch + at;
+            at += static_cast<std::size_t>(blocks);
+        }
+    }
+    rt_->begin(Runtime::kStream);
+    const int launched = launch_sweep(a, rt_->sm_count(), rt_->stream());
+    rt_->end(Runtime::kStream);
+    check_cuda(cudaGetLastError(), "sweep launch");
+    rt_->release(scratch);
+    if (stats_) {
+        stats_->stream_entries += ipow(n_, 2);
+        ++stats_->stream_launches;
+        stats_->kernel_launches += static_cast<std::uint64_t>(launched);
+    }
+}
+
 // Memory-bounded scheduling. Ops that allocate no tensor of order >= 2 run
 // eagerly as soon as their inputs exist (they only free memory); the order in
 // which the "big" producers (GEMM products, materialized Hadamard operands)
@@ -800,15 +1057,49 @@ void Program::optimize(double budget_bytes) {
     budget_ = budget_bytes;
     if (config_.device.fuse_epilogues) fuse_epilogues();
     make_schedule(budget_bytes);
+    if (config_.device.fuse_epilogues) {
+        // sweeps tie their consumers' operands together; keep them only if
+        // the memory-bounded schedule stays well inside the budget or does
+        // not get a higher peak (C5 at n = 65536 reverts, C3/C4 keep them)
+        const std::vector<Op> before = ops_;
+        const std::vector<std::size_t> sched = schedule_;
+        const double peak = sched_peak_;
+        const std::uint64_t fused = stats_ ? stats_->fused_epilogues : 0;
+        fuse_sweeps();
+        if (ops_.size() != before.size()) {
+            make_schedule(budget_bytes);
+            const double roomy = 0.6 * (budget_bytes > 0 ? budget_bytes : 179.0 * 1073741824.0);
+            if (sched_peak_ > std::max(peak * 1.0001 + 1.0, roomy)) {
+                ops_ = before;
+                schedule_ = sched;
+                sched_peak_ = peak;
+                if (stats_) stats_->fused_epilogues = fused;
+            }
+        }
+    }
     for (SymBuf& b : bufs_) b.last_use = -1;
     for (std::size_t pos = 0; pos < schedule_.size(); ++pos)
         for_each_read(ops_[schedule_[pos]],
                       [&](const View& v) { bufs_[static_cast<std::size_t>(v.buf)].last_use = static_cast<int>(pos); });
+    // every operand is an input or produced earlier in the schedule
+    std::vector<char> have(bufs_.size(), 0);
+    for (std::size_t b = 0; b < bufs_.size(); ++b) have[b] = bufs_[b].input;
+    for (std::size_t i : schedule_) {
+        const Op& op = ops_[i];
+        for_each_read(op, [&](const View& v) {
+            if (!have[static_cast<std::size_t>(v.buf)])
+                fail(ErrorCode::InvalidArgument, "executor: op " + std::to_string(i) + " reads b" + std::to_string(v.buf) +
+                                                     " before it is produced");
+        });
+        if (!op.ext && op.out >= 0 && (!op.gemm || op.store)) have[static_cast<std::size_t>(op.out)] = 1;
+        for (const Op::Epi& e : op.epis)
+            if (!e.ext && e.out >= 0) have[static_cast<std::size_t>(e.out)] = 1;
+    }
 }
 
 double* Program::ptr(int buf) const {
     const SymBuf& b = bufs_[static_cast<std::size_t>(buf)];
-    if (!b.real) fail(ErrorCode::InvalidArgument, "executor: operand buffer not materialized");
+    if (!b.real) fail(ErrorCode::InvalidArgument, "executor: operand buffer b" + std::to_string(buf) + " not materialized");
     return b.real->ptr;
 }
 
@@ -1131,6 +1422,10 @@ void Program::run_gemm(const Op& op, double* out) {
 }
 
 void Program::launch(Op& op) {
+    if (op.sweep) {
+        run_sweep(op);
+        return;
+    }
     double* out = op.ext;
     if (!out && (!op.gemm || op.store)) {
         SymBuf& b = bufs_[static_cast<std::size_t>(op.out)];
@@ -1200,6 +1495,11 @@ void Program::execute() {
     // only reductions over at most an n^2 space go to the side stream: heavier
     // bandwidth ops running under a GEMM steal its SMs mid-wave (C4: -3%)
     auto side_ok = [&](const Op& op) {
+        if (op.sweep) {
+            for (const Op::Epi& e : op.epis)
+                if (e.mode == kEpiStore) return false;
+            return true;
+        }
         if (op.gemm || (!op.ext && bufs_[static_cast<std::size_t>(op.out)].order >= 2)) return false;
         const int dims = static_cast<int>(op.out_ids.size()) + std::popcount(op.sum);
         return dims <= 2;
@@ -1218,6 +1518,8 @@ void Program::execute() {
                 order.push_back(d);
                 const Op& o = ops_[d];
                 if (!o.ext && o.out >= 0) pending_out[static_cast<std::size_t>(o.out)] = 0;
+                for (const Op::Epi& e : o.epis)
+                    if (!e.ext && e.out >= 0) pending_out[static_cast<std::size_t>(e.out)] = 0;
             }
             deferred.clear();
         };
@@ -1226,6 +1528,8 @@ void Program::execute() {
             if (side_ok(op)) {
                 deferred.push_back(i);
                 if (!op.ext && op.out >= 0) pending_out[static_cast<std::size_t>(op.out)] = 1;
+                for (const Op::Epi& e : op.epis)
+                    if (!e.ext && e.out >= 0) pending_out[static_cast<std::size_t>(e.out)] = 1;
                 continue;
             }
             bool needs = false;

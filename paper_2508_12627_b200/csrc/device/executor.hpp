@@ -85,6 +85,7 @@ class Runtime {
     Buf allocate(int order, long long n);
     Buf borrow(const double* ptr, int order, long long n);
     double* scratch(std::size_t entries);
+    const double* ones(long long n);  // a persistent device vector of at least n ones
     void release(double* p);
     void sync();
 
@@ -120,6 +121,8 @@ class Runtime {
     int comm_world_ = 1;
     double free_bytes_ = 0;
     bool profiling_ = false;
+    std::vector<double*> ones_;
+    long long ones_n_ = 0;
     std::vector<cudaEvent_t> pool_;
     struct Mark {
         Kind kind;
@@ -182,6 +185,9 @@ struct Op {
     std::vector<Epi> epis;
     bool store = true;
     bool symmetric_out = false;
+    // sweep: one pass over the matrix factors[0] (row-major view) feeding the
+    // consumers in `epis` (row_id = the matrix's row index)
+    bool sweep = false;
     // destination: a program buffer, or an external device pointer
     int out = -1;
     double* ext = nullptr;
@@ -247,6 +253,9 @@ class Program {
     std::string desc(const View& v, const std::vector<int>& dims) const;
     int new_buf(int order, bool symmetric);
     void fuse_epilogues();
+    void fuse_sweeps();
+    void run_sweep(const Op& op);
+    std::pair<long long, long long> sweep_strides(const View& v, int row_id, int col_id) const;
     bool tma_plain(const View& v, const std::vector<int>& rows, int e) const;
     void launch(Op& op);
     void run_stream(const Op& op, double* out);

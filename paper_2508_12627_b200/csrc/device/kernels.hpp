@@ -14,6 +14,37 @@ constexpr int kMaxFactors = 8;       // factors multiplied inside one kernel
 constexpr int kMaxGemmFactors = 6;   // factors per GEMM operand (prologue product)
 constexpr int kMaxRowDims = 3;       // ids folded into one GEMM row / column index
 
+// Multi-consumer matrix sweep: ONE pass over a matrix X (row-major view,
+// X(R, C) = x[R * xr + C]) feeding several reductions that would each have
+// streamed X again. Per row the kernel forms the power sums
+// S_p(R) = sum_C X(R,C)^p (p = 1..4); consumer q scales S_{power_q} by its
+// row weights f_q(R) = prod_i rowv_i[R * rs_i]:
+//   kSweepAll: out[0] (+)= sum_R f_q(R) S_p(R)   (block partials, then in order)
+//   kSweepRow: out[R] (+)= f_q(R) S_p(R)
+constexpr int kMaxSweep = 16;
+enum SweepMode : int { kSweepAll = 0, kSweepRow = 1 };
+struct SweepOut {
+    int mode = kSweepAll;
+    int power = 1;
+    int nrow = 0;
+    const double* rowv[4] = {};
+    long long rows_stride[4] = {};
+    double* out = nullptr;
+    double* partial = nullptr;  // kSweepAll: one slot per block
+};
+struct SweepArgs {
+    const double* x = nullptr;
+    long long xr = 0;           // row stride of X (column stride 1)
+    long long cols = 0;
+    long long r0 = 0, r1 = 0;   // rows [r0, r1) (a rank's slice under row sharding)
+    int accumulate = 0;
+    int count = 0;
+    SweepOut o[kMaxSweep];
+};
+// Blocks a sweep over `rows` rows launches (= partial slots per kSweepAll consumer).
+int sweep_blocks(long long rows, int sm_count);
+int launch_sweep(const SweepArgs& a, int sm_count, cudaStream_t s);
+
 // Broadcast-product-reduce ("stream") kernel:
 //   out[o] = scale * sum_{s} prod_f F_f[ sum_d digit_d * stride[f][d] ]
 // iteration dims [0, n_out) are the output (row-major, last fastest),

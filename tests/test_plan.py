@@ -28,11 +28,13 @@ def test_reference_plan_gemm_counts(name, gemms):
 
 def test_c2_single_symmetric_fused_gemm():
     text, tot = plan("C2")
-    assert tot["gemms"] == 1 and tot["symmetric_gemms"] == 1 and tot["fused_epilogues"] == 1
+    assert tot["gemms"] == 1 and tot["symmetric_gemms"] == 1 and tot["fused_epilogues"] >= 1
     n = CONFIGS["C2"].n
     tiles = n // 128
     assert tot["gemm_macs"] == n ** 3 // (tiles * tiles) * (tiles * (tiles + 1) // 2)
     assert "SYM nostore | epi sum_all pow=2 -> term" in text
+    # the two remaining n^2 passes over A (sum A^4, row sums of A^2) share one sweep
+    assert "SWEEP" in text and tot["streams"] == 2
 
 
 def test_sharing_never_increases_work():
