@@ -1126,8 +1126,38 @@ void Program::run_stream(const Op& op, double* out) {
         sums.erase(std::find(sums.begin(), sums.end(), best));
         sums.push_back(best);
     }
+    // The output dim along which the big non-symmetric operand is contiguous
+    // may not be the layout's last (C4: b9{1:1024 2:1 3:n^2} summed over 1
+    // into (2,3)): iterate it fastest, one thread per output, writing through
+    // output strides, instead of reading that operand with a stride of n.
+    std::vector<int> ord = out_ids;
+    int moved = -1;
+    if (!sums.empty() && out_ids.size() >= 2 && slice_world_ == 1) {
+        auto weight = [&](const View& v, int id) -> long long {
+            const SymBuf& b = bufs_[static_cast<std::size_t>(v.buf)];
+            if (b.symmetric || !(v.ids & bit(id)) || v.stride[static_cast<std::size_t>(id)] != 1) return 0;
+            return b.order >= 3 ? 16 : b.order == 2 ? 4 : 1;
+        };
+        long long on_sum = 0, best = 0;
+        for (const View& v : factors) on_sum += weight(v, sums.back());
+        for (int id : out_ids) {
+            long long w = 0;
+            for (const View& v : factors) w += weight(v, id);
+            if (w > best) {
+                best = w;
+                moved = id;
+            }
+        }
+        if (moved == out_ids.back() || best <= on_sum) moved = -1;
+        if (moved >= 0) {
+            ord.erase(std::find(ord.begin(), ord.end(), moved));
+            ord.push_back(moved);
+        }
+    }
     int fast = -1;
-    if (!sums.empty()) {
+    if (moved >= 0) {
+        fast = moved;
+    } else if (!sums.empty()) {
         int cs = 0, co = 0;
         for (const View& v : factors) {
             if (bufs_[static_cast<std::size_t>(v.buf)].symmetric) continue;
@@ -1152,7 +1182,7 @@ void Program::run_stream(const Op& op, double* out) {
     a.n_out = static_cast<int>(out_ids.size());
     a.n_sum = static_cast<int>(sums.size());
     a.n = n_;
-    std::vector<int> dims = out_ids;
+    std::vector<int> dims = ord;
     dims.insert(dims.end(), sums.begin(), sums.end());
     for (int f = 0; f < a.nf; ++f) {
         a.ptr[f] = ptr(factors[static_cast<std::size_t>(f)].buf);
@@ -1160,6 +1190,13 @@ void Program::run_stream(const Op& op, double* out) {
             a.stride[f][d] = factors[static_cast<std::size_t>(f)].stride[static_cast<std::size_t>(dims[d])];
     }
     a.out = out;
+    if (moved >= 0) {
+        a.permuted_out = 1;
+        for (std::size_t d = 0; d < ord.size(); ++d) {
+            const auto k = static_cast<std::size_t>(std::find(out_ids.begin(), out_ids.end(), ord[d]) - out_ids.begin());
+            a.ostride[d] = static_cast<long long>(ipow(n_, static_cast<int>(out_ids.size() - 1 - k)));
+        }
+    }
     if (slice_world_ > 1) {
         // row sharding: this rank covers [lo, hi) of iteration dim 0 (an output
         // dim -> disjoint rows of the zeroed output; a summed dim -> a partial

@@ -60,6 +60,10 @@ struct StreamArgs {
     double scale = 1.0;
     long long n0 = 0;      // extent of iteration dim 0 (0 = n): a rank's slice in row sharding
     int accumulate = 0;    // out += result (outputs pre-zeroed; slices of all ranks add up)
+    // permuted outputs: the output dims are iterated in an order other than
+    // the buffer's layout; output dim d sits at out[sum_d digit_d * ostride[d]]
+    int permuted_out = 0;
+    long long ostride[kMaxDims] = {};
 };
 
 // One GEMM operand: value(r, k) = prod_f ptr_f[ off_f(r) + kstride_f * k ]

@@ -318,10 +318,20 @@ __global__ void stream_reduce_thread(StreamArgs a, unsigned long long outputs,
                 if (f < a.nf) off[f] -= (a.n - 1) * a.stride[f][first + d];
         }
     }
-    if (S == 1)
+    if (a.permuted_out) {
+        unsigned long long flat = o;
+        long long dst = 0;
+        for (int d = a.n_out - 1; d >= 0; --d) {
+            const unsigned long long q = flat / static_cast<unsigned long long>(a.n);
+            dst += static_cast<long long>(flat - q * static_cast<unsigned long long>(a.n)) * a.ostride[d];
+            flat = q;
+        }
+        put(a, static_cast<unsigned long long>(dst), a.scale * acc);
+    } else if (S == 1) {
         put(a, o, a.scale * acc);
-    else
+    } else {
         partial[blockIdx.y * outputs + o] = acc;
+    }
 }
 
 // Paired variants of the three kernels above (inner extent even, every
@@ -368,9 +378,10 @@ __global__ void __launch_bounds__(256) stream_elementwise_pairs(StreamArgs a, un
     }
 }
 
+// Long rows: the block's threads share each row (C3: 8192 pairs per row).
 template <int NF>
-__global__ void __launch_bounds__(256) stream_reduce_all_pairs(StreamArgs a, unsigned long long rows,
-                                                               long long inner_n, double* partial) {
+__global__ void __launch_bounds__(256) stream_reduce_all_pairs_block(StreamArgs a, unsigned long long rows,
+                                                                     long long inner_n, double* partial) {
     __shared__ double red[32];
     const int D = a.n_sum;
     const int inner = D - 1;
@@ -383,6 +394,47 @@ __global__ void __launch_bounds__(256) stream_reduce_all_pairs(StreamArgs a, uns
         PairLine<NF> L;
         L.setup(a, off, inner);
         acc += L.sum(threadIdx.x, inner_n >> 1, blockDim.x);
+    }
+    const double t = block_sum(acc, red);
+    if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+// Each warp takes a contiguous range of rows and walks them with an
+// odometer on the last row dim (one division per wrap, not per row), lanes
+// over the row's pairs: short rows (C4: n = 1024) no longer pay the row
+// setup per few loads.
+template <int NF>
+__global__ void __launch_bounds__(256) stream_reduce_all_pairs(StreamArgs a, unsigned long long rows,
+                                                               long long inner_n, double* partial) {
+    __shared__ double red[32];
+    const int D = a.n_sum;
+    const int inner = D - 1, rdim = D - 2;
+    const int lane = threadIdx.x & 31;
+    const unsigned long long W = static_cast<unsigned long long>(gridDim.x) * (blockDim.x >> 5);
+    const unsigned long long w = static_cast<unsigned long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const unsigned long long lo = rows * w / W, hi = rows * (w + 1) / W;
+    long long off[NF], rs[NF];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) rs[f] = rdim >= 0 ? a.stride[f][rdim] : 0;
+    long long digit = 0;
+    bool fresh = true;
+    double acc = 0.0;
+    for (unsigned long long row = lo; row < hi; ++row) {
+        if (fresh) {
+            line_offsets<NF>(a, row, 0, D - 1, off);
+            digit = rdim > 0 ? static_cast<long long>(row % static_cast<unsigned long long>(a.n)) : 0;
+            fresh = false;
+        }
+        PairLine<NF> L;
+        L.setup(a, off, inner);
+        acc += L.sum(lane, inner_n >> 1, 32);
+        ++digit;
+        if (rdim <= 0 || digit < a.n) {
+#pragma unroll
+            for (int f = 0; f < NF; ++f) off[f] += rs[f];
+        } else {
+            fresh = true;
+        }
     }
     const double t = block_sum(acc, red);
     if (threadIdx.x == 0) partial[blockIdx.x] = t;
@@ -553,7 +605,11 @@ int launch_stream(const StreamArgs& args, double* scratch, std::size_t scratch_e
         int blocks = blocks_for_all(rows, inner_n, sm_count);
         const bool pairs = pairs_ok(a, D - 1, inner_n, D);
         with_nf(a.nf, [&](auto nf) {
-            auto k = pairs ? stream_reduce_all_pairs<decltype(nf)::value> : stream_reduce_all<decltype(nf)::value>;
+            constexpr int NF = decltype(nf)::value;
+            auto k = pairs ? stream_reduce_all_pairs<NF> : stream_reduce_all<NF>;
+            // many short rows: a warp per row range; few long rows: blocks share rows
+            if (pairs && (inner_n > 4096 || rows < 4ull * static_cast<unsigned long long>(sm_count) * 64))
+                k = stream_reduce_all_pairs_block<NF>;
             const int wave = sm_count * resident_blocks(k);
             if (blocks > wave) blocks = wave;
             k<<<blocks, kThreads, 0, s>>>(a, rows, inner_n, scratch);
@@ -570,7 +626,8 @@ int launch_stream(const StreamArgs& args, double* scratch, std::size_t scratch_e
         unit_sum += a.stride[f][last] == 1;
         unit_out += a.stride[f][out_last] == 1;
     }
-    if (unit_sum > unit_out || (unit_sum == unit_out && outputs < static_cast<unsigned long long>(sm_count) * 256)) {
+    if (!a.permuted_out &&
+        (unit_sum > unit_out || (unit_sum == unit_out && outputs < static_cast<unsigned long long>(sm_count) * 256))) {
         const unsigned long long srows = ipow(a.n, a.n_sum - 1);
         const unsigned long long blocks = (outputs + (kThreads / 32) - 1) / (kThreads / 32);
         const bool pairs = pairs_ok(a, last, a.n, last + 1);
@@ -586,7 +643,7 @@ int launch_stream(const StreamArgs& args, double* scratch, std::size_t scratch_e
     }
     const unsigned long long sflat = ipow(a.n, a.n_sum);
     unsigned long long slices = 1;
-    if (scratch_entries >= 2 * outputs) {
+    if (!a.permuted_out && scratch_entries >= 2 * outputs) {
         slices = scratch_entries / outputs;
         if (slices > 1024) slices = 1024;
     }
