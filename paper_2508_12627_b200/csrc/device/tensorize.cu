@@ -73,6 +73,78 @@ __global__ void pair_sym(const double* __restrict__ x, long long n, int d, int c
     }
 }
 
+// Register-blocked form for narrow samples (dc <= 32): 64x64 tile pairs
+// (ti <= tj), each thread a 4x4 block (4 + 4 shared loads per coordinate for
+// 16 entries), the entry written to (i, j) and — for off-diagonal tiles — to
+// (j, i), each as 32-byte row segments. Same per-entry arithmetic (squared
+// differences summed per coordinate in order), so the matrix is identical to
+// pair_sym's and bitwise symmetric.
+constexpr int kBlkTile = 64, kBlkDim = 32;
+template <int KIND>
+__global__ void __launch_bounds__(256) pair_sym_blocked(const double* __restrict__ x, long long n, int d, int c0,
+                                                        int dc, double scale, double* __restrict__ out) {
+    const int ti = blockIdx.y, tj = blockIdx.x;
+    if (ti > tj) return;
+    __shared__ double xi[kBlkDim][kBlkTile + 1], xj[kBlkDim][kBlkTile + 1];  // coordinate-major
+    const long long i0 = static_cast<long long>(ti) * kBlkTile, j0 = static_cast<long long>(tj) * kBlkTile;
+    const int tid = threadIdx.x;
+    for (int e = tid; e < kBlkTile * dc; e += 256) {
+        const int r = e / dc, c = e - r * dc;
+        xi[c][r] = i0 + r < n ? x[(i0 + r) * d + c0 + c] : 0.0;
+        xj[c][r] = j0 + r < n ? x[(j0 + r) * d + c0 + c] : 0.0;
+    }
+    __syncthreads();
+    const int ty = tid >> 4, tx = tid & 15;
+    double s[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) s[a][b] = 0.0;
+    for (int c = 0; c < dc; ++c) {
+        double u[4], v[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) u[a] = xi[c][ty * 4 + a];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) v[b] = xj[c][tx * 4 + b];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const double t = u[a] - v[b];
+                s[a][b] += t * t;
+            }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) s[a][b] = KIND == 0 ? exp(-scale * s[a][b]) : sqrt(s[a][b]);
+    const long long ib = i0 + ty * 4, jb = j0 + tx * 4;
+    const bool full = i0 + kBlkTile <= n && j0 + kBlkTile <= n && (n & 1) == 0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        if (full) {
+            double2* o = reinterpret_cast<double2*>(out + (ib + a) * n + jb);
+            o[0] = make_double2(s[a][0], s[a][1]);
+            o[1] = make_double2(s[a][2], s[a][3]);
+        } else if (ib + a < n) {
+            for (int b = 0; b < 4; ++b)
+                if (jb + b < n) out[(ib + a) * n + jb + b] = s[a][b];
+        }
+    }
+    if (ti == tj) return;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        if (full) {
+            double2* o = reinterpret_cast<double2*>(out + (jb + b) * n + ib);
+            o[0] = make_double2(s[0][b], s[1][b]);
+            o[1] = make_double2(s[2][b], s[3][b]);
+        } else if (jb + b < n) {
+            for (int a = 0; a < 4; ++a)
+                if (ib + a < n) out[(jb + b) * n + ib + a] = s[a][b];
+        }
+    }
+}
+
 // Euclidean distances over columns [c0, c0 + dc) (fallback for wide samples).
 __global__ void distance(const double* __restrict__ x, long long n, int d, int c0, int dc, double* __restrict__ out) {
     const long long j = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
@@ -170,6 +242,11 @@ __global__ void times_small(const double* __restrict__ z, long long n, int F, co
 
 void launch_rbf(const double* x, long long n, int d, double bandwidth, double* out, cudaStream_t s) {
     const double scale = 0.5 / (bandwidth * bandwidth);
+    if (d <= kBlkDim) {
+        const unsigned T = static_cast<unsigned>((n + kBlkTile - 1) / kBlkTile);
+        pair_sym_blocked<0><<<dim3(T, T), 256, 0, s>>>(x, n, d, 0, d, scale, out);
+        return;
+    }
     if (d <= kPairMaxDim) {
         const unsigned T = static_cast<unsigned>((n + kPairTile - 1) / kPairTile);
         pair_sym<0><<<dim3(T, T), dim3(kPairTile, 8), 0, s>>>(x, n, d, 0, d, scale, out);
@@ -179,6 +256,11 @@ void launch_rbf(const double* x, long long n, int d, double bandwidth, double* o
 }
 
 void launch_distance(const double* x, long long n, int d, int c0, int dc, double* out, cudaStream_t s) {
+    if (dc <= kBlkDim) {
+        const unsigned T = static_cast<unsigned>((n + kBlkTile - 1) / kBlkTile);
+        pair_sym_blocked<1><<<dim3(T, T), 256, 0, s>>>(x, n, d, c0, dc, 0.0, out);
+        return;
+    }
     if (dc <= kPairMaxDim) {
         const unsigned T = static_cast<unsigned>((n + kPairTile - 1) / kPairTile);
         pair_sym<1><<<dim3(T, T), dim3(kPairTile, 8), 0, s>>>(x, n, d, c0, dc, 0.0, out);
