@@ -84,6 +84,7 @@ void Runtime::refresh_free_bytes() {
         pooled = static_cast<double>(reserved > used ? reserved - used : 0);
     }
     free_bytes_ = static_cast<double>(free_b) + pooled;
+    agree_free_bytes();
 }
 
 Buf Runtime::allocate(int order, long long n) {
@@ -194,6 +195,22 @@ void Runtime::nccl_init(int rank, int world, const void* unique_id) {
     nccl_check(nccl().init(&comm, world, id, rank), "ncclCommInitRank");
     comm_ = comm;
     comm_world_ = world;
+    agree_free_bytes();
+}
+
+// Row-sharded ranks must record identical programs (the same collectives in
+// the same order), and the memory-bounded schedule depends on the budget:
+// every rank plans with the smallest free memory of the communicator.
+void Runtime::agree_free_bytes() {
+    if (!comm_ || comm_world_ <= 1) return;
+    constexpr int kNcclFloat64 = 8, kNcclMin = 3;  // nccl.h enum values
+    double* d = nullptr;
+    check_cuda(cudaMalloc(reinterpret_cast<void**>(&d), sizeof(double)), "cudaMalloc");
+    check_cuda(cudaMemcpy(d, &free_bytes_, sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    nccl_check(nccl().all_reduce(d, d, 1, kNcclFloat64, kNcclMin, comm_, stream_), "ncclAllReduce(min)");
+    check_cuda(cudaStreamSynchronize(stream_), "sync");
+    check_cuda(cudaMemcpy(&free_bytes_, d, sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    cudaFree(d);
 }
 
 void Runtime::allreduce_sum(double* p, std::size_t count) {

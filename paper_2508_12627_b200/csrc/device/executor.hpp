@@ -74,6 +74,7 @@ class Runtime {
     // most of the device (refresh_free_bytes).
     double free_bytes() const { return free_bytes_; }
     void refresh_free_bytes();
+    void agree_free_bytes();  // row sharding: every rank plans with the communicator's minimum
     static constexpr int kChunkStreams = 4;
     cudaStream_t chunk_stream(int i) const { return chunk_[i % kChunkStreams]; }
     // bitwise-symmetry results of host inputs seen before (speculation key)
