@@ -123,20 +123,6 @@ double* Runtime::scratch(std::size_t entries) {
     return static_cast<double*>(p);
 }
 
-const double* Runtime::ones(long long n) {
-    if (n > ones_n_) {
-        // grown buffers stay allocated (in-flight kernels may still read them)
-        const long long len = std::max<long long>(n, 1 << 16);
-        void* p = nullptr;
-        check_cuda(cudaMalloc(&p, static_cast<std::size_t>(len) * sizeof(double)), "cudaMalloc");
-        const std::vector<double> host(static_cast<std::size_t>(len), 1.0);
-        check_cuda(cudaMemcpy(p, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice), "ones");
-        ones_.push_back(static_cast<double*>(p));
-        ones_n_ = len;
-    }
-    return ones_.back();
-}
-
 void Runtime::release(double* p) {
     if (p) cudaFreeAsync(p, cur_);
 }
@@ -693,11 +679,12 @@ void Program::fuse_epilogues() {
 }
 
 // Sweep fusion. Reductions over a 2-index space that each stream the same
-// n x n matrix X (C3: B~ is read by ~15 reductions across the lattice) are
-// merged into one pass over X, one consumer per reduction: X read
-// row-major (a symmetric X in either orientation), its power, up to four
-// weights over the same two indices, and a scalar / row-vector / matrix
-// output. Only mutually independent consumers share a sweep.
+// n x n matrix X and otherwise read only row weights (vectors or scalars
+// indexed by X's row) are merged into one pass over X that forms the row
+// power sums S_p = sum_C X^p (p <= 4); each reduction becomes a consumer
+// scaling S_p by its row weights into a scalar or a row vector (C2: sum A^4
+// and the row sums of A^2). X is read row-major (a symmetric X in either
+// orientation). Only mutually independent consumers share a sweep.
 void Program::fuse_sweeps() {
     struct Cand {
         std::size_t op;

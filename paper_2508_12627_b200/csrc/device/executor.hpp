@@ -86,7 +86,6 @@ class Runtime {
     Buf allocate(int order, long long n);
     Buf borrow(const double* ptr, int order, long long n);
     double* scratch(std::size_t entries);
-    const double* ones(long long n);  // a persistent device vector of at least n ones
     void release(double* p);
     void sync();
 
@@ -122,8 +121,6 @@ class Runtime {
     int comm_world_ = 1;
     double free_bytes_ = 0;
     bool profiling_ = false;
-    std::vector<double*> ones_;
-    long long ones_n_ = 0;
     std::vector<cudaEvent_t> pool_;
     struct Mark {
         Kind kind;
