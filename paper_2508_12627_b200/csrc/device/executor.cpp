@@ -518,7 +518,28 @@ int Program::gemm(std::vector<View> fa, std::vector<View> fb, const std::vector<
             return hit->second;
         }
     }
-    const bool sym = ka == kb && ra.size() == 1 && rb.size() == 1 && config_.device.exploit_symmetry;
+    bool sym = ka == kb && ra.size() == 1 && rb.size() == 1 && config_.device.exploit_symmetry;
+    // B^p * B^q = B^(p+q) for a symmetric B: symmetric although the operands
+    // differ (C5: B * B^2), so only its upper tiles are computed
+    int out_base = -1, out_power = 0;
+    auto power_of = [&](const View& v, int* base, int* pw) {
+        const SymBuf& b = bufs_[static_cast<std::size_t>(v.buf)];
+        if (b.order != 2 || !b.symmetric || std::popcount(v.ids) != 2) return false;
+        const int i = std::countr_zero(v.ids), j = 31 - std::countl_zero(v.ids);
+        const long long si = v.stride[static_cast<std::size_t>(i)], sj = v.stride[static_cast<std::size_t>(j)];
+        if (!((si == 1 && sj == n_) || (si == n_ && sj == 1))) return false;
+        *base = b.power_base >= 0 ? b.power_base : b.content;
+        *pw = b.power_base >= 0 ? b.power : 1;
+        return true;
+    };
+    if (ra.size() == 1 && rb.size() == 1 && fa.size() == 1 && fb.size() == 1 && config_.device.exploit_symmetry) {
+        int ba = -1, pa = 0, bb = -1, pb = 0;
+        if (power_of(fa[0], &ba, &pa) && power_of(fb[0], &bb, &pb) && ba == bb) {
+            sym = true;
+            out_base = ba;
+            out_power = pa + pb;
+        }
+    }
     Op op;
     op.gemm = true;
     op.fa = std::move(fa);
@@ -528,6 +549,8 @@ int Program::gemm(std::vector<View> fa, std::vector<View> fb, const std::vector<
     op.e = e;
     op.symmetric_out = sym;
     op.out = new_buf(static_cast<int>(ra.size() + rb.size()), sym);
+    bufs_[static_cast<std::size_t>(op.out)].power_base = out_base;
+    bufs_[static_cast<std::size_t>(op.out)].power = out_power;
     ops_.push_back(op);
     if (sharing()) {
         memo_[key] = op.out;

@@ -154,6 +154,10 @@ struct View {
 struct SymBuf {
     int order = 0;
     bool symmetric = false;
+    // a known power of a symmetric matrix: base content id (-1 = none) and
+    // exponent; products of powers of one base commute, so they are symmetric
+    int power_base = -1;
+    int power = 0;
     bool input = false;
     Buf real;
     int content = -1;

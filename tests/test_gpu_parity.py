@@ -46,7 +46,7 @@ def test_prod2_golden(engine):
 
 
 @pytest.mark.parametrize("name,n", [("C1", 64), ("C1", 257), ("C2", 96), ("C2", 130), ("C3", 96),
-                                    ("C3", 129), ("C4", 24), ("C4", 33), ("C5", 96), ("C5", 130)])
+                                    ("C3", 129), ("C4", 24), ("C4", 33), ("C5", 96), ("C5", 97), ("C5", 130)])
 def test_configs_small(engine, name, n):
     from paper_2508_12627_b200.workloads import generate
     factors, sig, m, _ = generate(name, n)
