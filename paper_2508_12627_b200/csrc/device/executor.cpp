@@ -431,6 +431,19 @@ std::string Program::stream_key(const std::vector<View>& factors, const std::vec
     return best;
 }
 
+// A full-matrix view of a symmetric matrix that is a known power B^p of a
+// symmetric base (a symmetric input is its own base, p = 1).
+bool Program::power_of(const View& v, int* base, int* pw) const {
+    const SymBuf& b = bufs_[static_cast<std::size_t>(v.buf)];
+    if (b.order != 2 || !b.symmetric || std::popcount(v.ids) != 2) return false;
+    const int i = std::countr_zero(v.ids), j = 31 - std::countl_zero(v.ids);
+    const long long si = v.stride[static_cast<std::size_t>(i)], sj = v.stride[static_cast<std::size_t>(j)];
+    if (!((si == 1 && sj == n_) || (si == n_ && sj == 1))) return false;
+    *base = b.power_base >= 0 ? b.power_base : b.content;
+    *pw = b.power_base >= 0 ? b.power : 1;
+    return true;
+}
+
 int Program::lookup_stream(const std::vector<View>& factors, const std::vector<int>& out_ids,
                            std::uint32_t sum) const {
     if (!sharing() || factors.size() > static_cast<std::size_t>(kMaxFactors)) return -1;
@@ -470,12 +483,46 @@ int Program::stream(std::vector<View> factors, const std::vector<int>& out_ids, 
             }
         }
     }
+    // B^p scaled along one axis by a vector: remember it (see SymBuf)
+    int sc_base = -1, sc_pow = 0, sc_w = -1, sc_axis = -1;
+    if (!ext && sum == 0 && out_ids.size() == 2 && factors.size() >= 2) {
+        // one matrix factor B^p and vectors that all run along one output index
+        int mats = 0, b = -1, p = 0, wid = -1;
+        bool ok = true;
+        for (const View& v : factors) {
+            int vb = -1, vp = 0;
+            if (power_of(v, &vb, &vp)) {
+                ++mats;
+                b = vb;
+                p = vp;
+            } else if (bufs_[static_cast<std::size_t>(v.buf)].order == 1 && std::popcount(v.ids) == 1 &&
+                       (wid < 0 || wid == std::countr_zero(v.ids))) {
+                wid = std::countr_zero(v.ids);
+            } else {
+                ok = false;
+            }
+        }
+        const auto pos = wid >= 0 ? std::find(out_ids.begin(), out_ids.end(), wid) - out_ids.begin() : 2;
+        if (ok && mats == 1 && pos <= 1) {
+            sc_base = b;
+            sc_pow = p;
+            sc_w = wid;
+            sc_axis = static_cast<int>(pos);
+        }
+    }
     Op op;
     op.factors = std::move(factors);
     op.out_ids = out_ids;
     op.sum = sum;
     op.ext = ext;
-    if (!ext) op.out = new_buf(static_cast<int>(out_ids.size()), false);
+    if (!ext) {
+        op.out = new_buf(static_cast<int>(out_ids.size()), false);
+        SymBuf& ob = bufs_[static_cast<std::size_t>(op.out)];
+        ob.scaled_base = sc_base;
+        ob.scaled_power = sc_pow;
+        ob.scaled_w = sc_w;
+        ob.scaled_axis = sc_axis;
+    }
     ops_.push_back(op);
     if (!key.empty()) {
         if (ext) term_memo_[key] = ext;
@@ -522,14 +569,13 @@ int Program::gemm(std::vector<View> fa, std::vector<View> fb, const std::vector<
     // B^p * B^q = B^(p+q) for a symmetric B: symmetric although the operands
     // differ (C5: B * B^2), so only its upper tiles are computed
     int out_base = -1, out_power = 0;
-    auto power_of = [&](const View& v, int* base, int* pw) {
+    // B^p D_w with w on the contracted index: A * (B^p D_w)^T = B^p D_w B^p
+    auto scaled_on_e = [&](const View& v, int* base, int* pw) {
         const SymBuf& b = bufs_[static_cast<std::size_t>(v.buf)];
-        if (b.order != 2 || !b.symmetric || std::popcount(v.ids) != 2) return false;
-        const int i = std::countr_zero(v.ids), j = 31 - std::countl_zero(v.ids);
-        const long long si = v.stride[static_cast<std::size_t>(i)], sj = v.stride[static_cast<std::size_t>(j)];
-        if (!((si == 1 && sj == n_) || (si == n_ && sj == 1))) return false;
-        *base = b.power_base >= 0 ? b.power_base : b.content;
-        *pw = b.power_base >= 0 ? b.power : 1;
+        if (b.scaled_base < 0 || std::popcount(v.ids) != 2 || !(v.ids & bit(e))) return false;
+        if (v.stride[static_cast<std::size_t>(e)] != (b.scaled_axis == 0 ? n_ : 1)) return false;
+        *base = b.scaled_base;
+        *pw = b.scaled_power;
         return true;
     };
     if (ra.size() == 1 && rb.size() == 1 && fa.size() == 1 && fb.size() == 1 && config_.device.exploit_symmetry) {
@@ -538,6 +584,9 @@ int Program::gemm(std::vector<View> fa, std::vector<View> fb, const std::vector<
             sym = true;
             out_base = ba;
             out_power = pa + pb;
+        } else if ((power_of(fa[0], &ba, &pa) && scaled_on_e(fb[0], &bb, &pb) && ba == bb && pa == pb) ||
+                   (scaled_on_e(fa[0], &ba, &pa) && power_of(fb[0], &bb, &pb) && ba == bb && pa == pb)) {
+            sym = true;  // B^p D B^p
         }
     }
     Op op;

@@ -158,6 +158,9 @@ struct SymBuf {
     // exponent; products of powers of one base commute, so they are symmetric
     int power_base = -1;
     int power = 0;
+    // B^p scaled by vectors along one axis (row or column), i.e. B^p D or
+    // D B^p for a diagonal D: B^p D B^p is symmetric
+    int scaled_base = -1, scaled_power = 0, scaled_w = -1, scaled_axis = -1;
     bool input = false;
     Buf real;
     int content = -1;
@@ -253,6 +256,7 @@ class Program {
 
   private:
     std::string desc(const View& v, const std::vector<int>& dims) const;
+    bool power_of(const View& v, int* base, int* pw) const;
     int new_buf(int order, bool symmetric);
     void fuse_epilogues();
     void fuse_sweeps();
