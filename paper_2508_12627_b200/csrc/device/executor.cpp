@@ -535,6 +535,31 @@ int Program::stream(std::vector<View> factors, const std::vector<int>& out_ids, 
 int Program::gemm(std::vector<View> fa, std::vector<View> fb, const std::vector<int>& ra_in,
                   const std::vector<int>& rb_in, int e, std::vector<int>* layout) {
     std::vector<int> ra = ra_in, rb = rb_in;
+    // A diagonal weight (factors over the contracted index alone) can sit on
+    // either operand; put it on a canonical side so that X D Y and (Y D X)^T
+    // lower to the same operands and share one GEMM (C5: B D (B o B) and
+    // (B o B) D B).
+    {
+        std::vector<View> diag, ka0, kb0;
+        for (const View& v : fa) (v.ids == bit(e) ? diag : ka0).push_back(v);
+        for (const View& v : fb) (v.ids == bit(e) ? diag : kb0).push_back(v);
+        if (!diag.empty() && !ka0.empty() && !kb0.empty()) {
+            auto side_key = [&](const std::vector<View>& fs, const std::vector<int>& rows) {
+                std::vector<int> d = rows;
+                d.push_back(e);
+                std::vector<std::string> ks;
+                for (const View& v : fs) ks.push_back(desc(v, d));
+                std::sort(ks.begin(), ks.end());
+                std::string k;
+                for (const auto& x : ks) k += x + ";";
+                return k;
+            };
+            const bool to_b = side_key(kb0, rb) > side_key(ka0, ra);
+            (to_b ? kb0 : ka0).insert((to_b ? kb0 : ka0).end(), diag.begin(), diag.end());
+            fa = std::move(ka0);
+            fb = std::move(kb0);
+        }
+    }
     // Multi-factor (Hadamard / scaled / Khatri-Rao) operands are formed once,
     // k-major (rows..., e): O(rows*n) traffic against O(rows*cols*n) DMMA work.
     auto lower = [&](std::vector<View>& fs, const std::vector<int>& rows) {
@@ -625,7 +650,9 @@ double Program::cost_since(const Mark& m) const {
     for (std::size_t i = m.ops; i < ops_.size(); ++i) {
         const Op& op = ops_[i];
         if (op.gemm) {
-            c += static_cast<double>(ipow(n_, static_cast<int>(op.ra.size() + op.rb.size()) + 1));
+            // a symmetric product computes only its upper tiles
+            c += static_cast<double>(ipow(n_, static_cast<int>(op.ra.size() + op.rb.size()) + 1)) *
+                 (op.symmetric_out ? 0.5 : 1.0);
         } else {
             const int dims = static_cast<int>(op.out_ids.size()) + std::popcount(op.sum);
             c += 23.0 * static_cast<double>(ipow(n_, dims)) * static_cast<double>(op.factors.size());
