@@ -57,3 +57,31 @@ def test_plan_respects_memory_cap():
     with pytest.raises(us.UStatsError) as e:
         us.plan_summary([list(t) for t in w.signature], w.m, w.n, us.Config())
     assert e.value.code == "MemoryCapExceeded"
+
+
+def test_c5_symmetric_products():
+    # B, B^2, B^3 = B*B^2, B^4, B D B and its shared transpose: 6 of the 8
+    # GEMMs are symmetric (upper tiles only) and the MAC count reflects it
+    text, c5 = plan("C5")
+    assert c5["gemms"] == 8 and c5["symmetric_gemms"] >= 6
+    n = CONFIGS["C5"].n
+    assert c5["gemm_macs"] < 8 * n ** 3 * 0.65
+    assert text.count(" SYM ") == c5["symmetric_gemms"]
+
+
+def test_power_and_diagonal_symmetry_rules():
+    # chain r B B B e (m = 5 HOIF chain, C3 shape): B*B symmetric; with the
+    # symmetric flag off nothing is symmetric
+    w = CONFIGS["C3"]
+    sig = [list(t) for t in w.signature]
+    _, sym = us.plan_summary(sig, w.m, 512, us.Config(memory_cap_entries=CAP), inputs_symmetric=True)
+    _, nos = us.plan_summary(sig, w.m, 512, us.Config(memory_cap_entries=CAP, symmetry=False), inputs_symmetric=True)
+    assert sym["symmetric_gemms"] >= 1 and nos["symmetric_gemms"] == 0
+    assert sym["gemm_macs"] < nos["gemm_macs"]
+
+
+def test_c2_row_power_sweep():
+    text, c2 = plan("C2")
+    sweep = [l for l in text.splitlines() if "SWEEP" in l]
+    assert len(sweep) == 1
+    assert "sum_all pow=4" in sweep[0] and "sum_cols pow=2" in sweep[0]
