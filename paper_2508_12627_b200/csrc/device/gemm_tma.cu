@@ -20,6 +20,7 @@
 //     fixed-order reductions).
 #include <cuda.h>
 
+#include <cmath>
 #include <mutex>
 
 #include "kernels.hpp"
@@ -535,12 +536,27 @@ int launch_gemm_multi(const GemmArgs& a, const EpiSet& epis, cudaStream_t s) {
     // waves of 148): its tiles are split along K over the idle SMs and
     // re-assembled, so the tail costs ~1/S of a tile instead of a whole tile.
     const int sms = sm_count_cached();
-    const long long waves = blocks / sms, tail = blocks % sms;
+    const long long tail = blocks % sms;
     const int KT = static_cast<int>((a.n + BK - 1) / BK);
-    int S = tail > 0 ? static_cast<int>(sms / tail) : 1;
-    if (S > KT / 4) S = KT / 4;
+    // K-split factor of the tail: the one that finishes it soonest, in units
+    // of a full tile (ceil(tail*S / sms) / S), with at least 4 k-tiles per
+    // slice and at most 256 MiB of slice partials; used only if it beats
+    // running the tail unsplit (row-sharded C2 on 8 GPUs: 260 tiles per rank
+    // = 148 + 112, S = 5 -> 1.8 instead of 2 tile times)
+    int S = 1;
+    if (tail > 0) {
+        double best = 1.0;
+        for (int c = 2; c <= KT / 4 && c <= 64; ++c) {
+            if (static_cast<double>(tail) * c * BM * BN * 8.0 > 268435456.0) break;
+            const double t = std::ceil(static_cast<double>(tail) * c / sms) / c;
+            if (t < best * 0.95) {
+                best = t;
+                S = c;
+            }
+        }
+    }
     int launched_kernels = 0;
-    if (waves >= 1 && tail > 0 && S >= 2) {
+    if (tail > 0 && S >= 2) {
         go(args, blocks - tail);
         double* kpart = nullptr;
         const std::size_t kbytes = static_cast<std::size_t>(tail) * S * BM * BN * sizeof(double);
