@@ -1,0 +1,250 @@
+// Device runtime (executor.hpp): streams, stream-ordered allocation, the
+// NCCL communicator for row sharding, event profiling.
+#include "executor.hpp"
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <bit>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <numeric>
+#include <string>
+
+#include "executor_util.hpp"
+#include "ustats/errors.hpp"
+#include "ustats/partition.hpp"
+#include "ustats/tensor.hpp"
+
+namespace ustats::dev {
+
+void check_cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(ErrorCode::CudaError, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------- Runtime
+DeviceBuffer::~DeviceBuffer() {
+    for (auto& r : ready) cudaEventDestroy(r.second);
+    if (ptr && !borrowed && rt) {
+        cudaFreeAsync(ptr, rt->stream());
+        if (std::getenv("USTATS_SCHED_DEBUG") && entries() * 8 > (1ull << 30))
+            std::fprintf(stderr, "[free] %.2f GiB\n", entries() * 8 / 1073741824.0);
+    }
+}
+
+std::uint64_t DeviceBuffer::entries() const {
+    std::uint64_t e = 1;
+    for (int i = 0; i < order; ++i) e *= static_cast<std::uint64_t>(n);
+    return e;
+}
+
+Runtime& Runtime::get(int device) {
+    static std::mutex mu;
+    static std::map<int, std::unique_ptr<Runtime>> all;
+    std::lock_guard<std::mutex> lock(mu);
+    if (device < 0) check_cuda(cudaGetDevice(&device), "cudaGetDevice");
+    auto& slot = all[device];
+    if (!slot) slot.reset(new Runtime(device));
+    check_cuda(cudaSetDevice(device), "cudaSetDevice");
+    return *slot;
+}
+
+Runtime::Runtime(int device) : device_(device) {
+    check_cuda(cudaSetDevice(device), "cudaSetDevice");
+    check_cuda(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, device), "cudaDeviceGetAttribute");
+    // the main stream (GEMMs) outranks the side stream (reductions filling
+    // the GEMM's tail): pending GEMM CTAs get freed SMs first
+    int lo_prio = 0, hi_prio = 0;
+    check_cuda(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio), "cudaDeviceGetStreamPriorityRange");
+    check_cuda(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, hi_prio), "cudaStreamCreate");
+    check_cuda(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, lo_prio), "cudaStreamCreate");
+    check_cuda(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking), "cudaStreamCreate");
+    check_cuda(cudaStreamCreateWithPriority(&prep_, cudaStreamNonBlocking, hi_prio), "cudaStreamCreate");
+    for (auto& c : chunk_) check_cuda(cudaStreamCreateWithPriority(&c, cudaStreamNonBlocking, hi_prio), "cudaStreamCreate");
+    cur_ = stream_;
+    refresh_free_bytes();
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        std::uint64_t keep = ~std::uint64_t{0};
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+}
+
+Runtime::~Runtime() {}
+
+void Runtime::refresh_free_bytes() {
+    std::size_t free_b = 0, total_b = 0;
+    check_cuda(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    double pooled = 0;  // freed blocks our stream-ordered pool keeps for reuse
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device_) == cudaSuccess) {
+        std::uint64_t reserved = 0, used = 0;
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+        pooled = static_cast<double>(reserved > used ? reserved - used : 0);
+    }
+    free_bytes_ = static_cast<double>(free_b) + pooled;
+    agree_free_bytes();
+}
+
+Buf Runtime::allocate(int order, long long n) {
+    auto b = std::make_shared<DeviceBuffer>();
+    b->order = order;
+    b->n = n;
+    b->rt = this;
+    void* p = nullptr;
+    const std::size_t bytes = std::max<std::uint64_t>(b->entries(), 1) * sizeof(double);
+    const cudaError_t e = cudaMallocAsync(&p, bytes, cur_);
+    if (e != cudaSuccess || std::getenv("USTATS_SCHED_DEBUG")) {
+        std::size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        if (e != cudaSuccess || bytes > (1ull << 30))
+            std::fprintf(stderr, "[alloc] %.2f GiB -> %s (free %.2f / %.2f GiB)\n", bytes / 1073741824.0,
+                         cudaGetErrorString(e), fr / 1073741824.0, tot / 1073741824.0);
+    }
+    check_cuda(e, "cudaMallocAsync");
+    b->ptr = static_cast<double*>(p);
+    return b;
+}
+
+Buf Runtime::borrow(const double* ptr, int order, long long n) {
+    auto b = std::make_shared<DeviceBuffer>();
+    b->ptr = const_cast<double*>(ptr);
+    b->order = order;
+    b->n = n;
+    b->borrowed = true;
+    b->rt = this;
+    return b;
+}
+
+double* Runtime::scratch(std::size_t entries) {
+    void* p = nullptr;
+    check_cuda(cudaMallocAsync(&p, std::max<std::size_t>(entries, 1) * sizeof(double), cur_), "cudaMallocAsync");
+    return static_cast<double*>(p);
+}
+
+void Runtime::release(double* p) {
+    if (p) cudaFreeAsync(p, cur_);
+}
+
+void Runtime::sync() {
+    for (auto& c : chunk_) check_cuda(cudaStreamSynchronize(c), "cudaStreamSynchronize");
+    check_cuda(cudaStreamSynchronize(copy_), "cudaStreamSynchronize");
+    check_cuda(cudaStreamSynchronize(prep_), "cudaStreamSynchronize");
+    check_cuda(cudaStreamSynchronize(side_), "cudaStreamSynchronize");
+    check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
+}
+
+// ------------------------------------------------------------------- NCCL
+namespace {
+struct NcclApi {
+    using GetId = int (*)(void*);
+    using Init = int (*)(void**, int, std::array<char, 128>, int);
+    using AllReduce = int (*)(const void*, void*, std::size_t, int, int, void*, cudaStream_t);
+    using ErrStr = const char* (*)(int);
+    GetId get_id = nullptr;
+    Init init = nullptr;
+    AllReduce all_reduce = nullptr;
+    ErrStr err = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // the process's copy (torch) if loaded
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+        if (!h) return;
+        api.get_id = reinterpret_cast<NcclApi::GetId>(dlsym(h, "ncclGetUniqueId"));
+        api.init = reinterpret_cast<NcclApi::Init>(dlsym(h, "ncclCommInitRank"));
+        api.all_reduce = reinterpret_cast<NcclApi::AllReduce>(dlsym(h, "ncclAllReduce"));
+        api.err = reinterpret_cast<NcclApi::ErrStr>(dlsym(h, "ncclGetErrorString"));
+    });
+    if (!api.get_id || !api.init || !api.all_reduce) fail(ErrorCode::CollectiveError, "libnccl.so.2 not available");
+    return api;
+}
+
+void nccl_check(int r, const char* what) {
+    if (r != 0)
+        fail(ErrorCode::CollectiveError,
+             std::string(what) + ": " + (nccl().err ? nccl().err(r) : ("nccl error " + std::to_string(r)).c_str()));
+}
+}  // namespace
+
+void Runtime::nccl_unique_id(void* out128) { nccl_check(nccl().get_id(out128), "ncclGetUniqueId"); }
+
+void Runtime::nccl_init(int rank, int world, const void* unique_id) {
+    std::array<char, 128> id{};
+    std::memcpy(id.data(), unique_id, 128);
+    void* comm = nullptr;
+    check_cuda(cudaSetDevice(device_), "cudaSetDevice");
+    nccl_check(nccl().init(&comm, world, id, rank), "ncclCommInitRank");
+    comm_ = comm;
+    comm_world_ = world;
+    agree_free_bytes();
+}
+
+// Row-sharded ranks must record identical programs (the same collectives in
+// the same order), and the memory-bounded schedule depends on the budget:
+// every rank plans with the smallest free memory of the communicator.
+void Runtime::agree_free_bytes() {
+    if (!comm_ || comm_world_ <= 1) return;
+    constexpr int kNcclFloat64 = 8, kNcclMin = 3;  // nccl.h enum values
+    double* d = nullptr;
+    check_cuda(cudaMalloc(reinterpret_cast<void**>(&d), sizeof(double)), "cudaMalloc");
+    check_cuda(cudaMemcpy(d, &free_bytes_, sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    nccl_check(nccl().all_reduce(d, d, 1, kNcclFloat64, kNcclMin, comm_, stream_), "ncclAllReduce(min)");
+    check_cuda(cudaStreamSynchronize(stream_), "sync");
+    check_cuda(cudaMemcpy(&free_bytes_, d, sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    cudaFree(d);
+}
+
+void Runtime::allreduce_sum(double* p, std::size_t count) {
+    if (!comm_ || comm_world_ <= 1 || count == 0) return;
+    constexpr int kNcclFloat64 = 8, kNcclSum = 0;  // nccl.h enum values
+    nccl_check(nccl().all_reduce(p, p, count, kNcclFloat64, kNcclSum, comm_, cur_), "ncclAllReduce");
+}
+
+void Runtime::begin(Kind k) {
+    if (!profiling_) return;
+    while (pool_.size() < 2) {
+        cudaEvent_t e;
+        check_cuda(cudaEventCreate(&e), "cudaEventCreate");
+        pool_.push_back(e);
+    }
+    Mark m{k, pool_.back(), nullptr};
+    pool_.pop_back();
+    m.b = pool_.back();
+    pool_.pop_back();
+    cudaEventRecord(m.a, cur_);
+    marks_.push_back(m);
+}
+
+void Runtime::end(Kind) {
+    if (!profiling_ || marks_.empty()) return;
+    cudaEventRecord(marks_.back().b, cur_);
+}
+
+Runtime::Profile Runtime::collect(bool reset) {
+    sync();
+    for (const Mark& m : marks_) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, m.a, m.b) == cudaSuccess) {
+            totals_.ms[m.kind] += ms;
+            totals_.groups[m.kind] += 1;
+        }
+        pool_.push_back(m.a);
+        pool_.push_back(m.b);
+    }
+    marks_.clear();
+    Profile p = totals_;
+    if (reset) totals_ = Profile{};
+    return p;
+}
+
+}  // namespace ustats::dev
