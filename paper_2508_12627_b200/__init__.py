@@ -8,7 +8,7 @@ from .api import (  # noqa: F401
     Config, UStatsError, UTerms, bell_number, combine_terms, device_count, device_stream, einsum,
     profile, nccl_init, nccl_unique_id,
     eliminate_index, kernel_tensors, optimize_order, plan_summary, plan_terms, restricted_v_tensors, survivors, treewidth,
-    ComplexityReport, chain_signature, complexity_report,
+    ComplexityReport, chain_signature, complexity_report, dgemm,
     u_statistic, u_statistic_batch, u_statistic_tensors, u_statistic_unsparsified_tensors, u_terms,
     v_statistic, hoif_tau, dcov_squared, motif_count, MOTIF_IDS,
     v_statistic_tensors,

@@ -556,6 +556,20 @@ def chain_signature(m: int):
     return [(i, i + 1) for i in range(1, m)]
 
 
+def dgemm(a, b, method: str = "ozaki", slices: int = 7, symmetric: bool = False, with_time: bool = False):
+    """C = A B^T in FP64 on the device: method "dmma" (mma.sync f64) or
+    "ozaki" (7-bit digit splitting on the INT8 tcgen05 tensor cores)."""
+    A = np.ascontiguousarray(a, dtype=np.float64)
+    B = np.ascontiguousarray(b, dtype=np.float64)
+    if A.ndim != 2 or B.ndim != 2 or A.shape[1] != B.shape[1]:
+        raise UStatsError("InvalidArgument", "dgemm needs A (m x k) and B (n x k)")
+    Cm = np.empty((A.shape[0], B.shape[0]))
+    ms = N.f64()
+    _check(N.lib().us_dgemm(1 if method == "ozaki" else 0, slices, 1 if symmetric else 0, A.shape[0], B.shape[0],
+                            A.shape[1], A.ctypes.data, B.ctypes.data, Cm.ctypes.data, C.byref(ms)))
+    return (Cm, ms.value) if with_time else Cm
+
+
 def device_stream(device: int = -1) -> int:
     """The engine's cudaStream_t on `device` (as an int handle)."""
     h = C.c_void_p()

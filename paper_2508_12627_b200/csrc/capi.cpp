@@ -554,6 +554,93 @@ int us_device_synchronize(int32_t device) {
     return guarded([&] { ustats::dev::Runtime::get(device).sync(); });
 }
 
+int us_dgemm(int32_t method, int32_t slices, int32_t symmetric, int64_t m, int64_t n, int64_t k, const double* a,
+             const double* b, double* c, double* ms_out) {
+    return guarded([&] {
+        using namespace ustats::dev;
+        if (m < 1 || n < 1 || k < 1 || !a || !b || !c) ustats::fail(ustats::ErrorCode::InvalidArgument, "bad GEMM shape");
+        if (symmetric && m != n) ustats::fail(ustats::ErrorCode::InvalidArgument, "symmetric GEMM needs m = n");
+        Runtime& rt = Runtime::get(-1);
+        cudaStream_t s = rt.main_stream();
+        rt.set_stream(s);
+        Buf da = rt.allocate(1, m * k), db = rt.allocate(1, n * k), dc = rt.allocate(1, m * n);
+        check_cuda(cudaMemcpyAsync(da->ptr, a, sizeof(double) * m * k, cudaMemcpyHostToDevice, s), "H2D");
+        check_cuda(cudaMemcpyAsync(db->ptr, b, sizeof(double) * n * k, cudaMemcpyHostToDevice, s), "H2D");
+        check_cuda(cudaMemsetAsync(dc->ptr, 0, sizeof(double) * m * n, s), "memset");
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        int8_t *sa = nullptr, *sb = nullptr;
+        int *ea = nullptr, *eb = nullptr;
+        if (method == 1) {
+            if (slices < 1 || slices > kOzMaxSlices) ustats::fail(ustats::ErrorCode::InvalidArgument, "slices must be 1..7");
+            const std::size_t abytes = ozaki_slice_bytes(m, k, 128), bbytes = ozaki_slice_bytes(n, k, 64);
+            check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&sa), abytes * slices, s), "alloc");
+            check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&sb), bbytes * slices, s), "alloc");
+            check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&ea), sizeof(int) * m, s), "alloc");
+            check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&eb), sizeof(int) * n, s), "alloc");
+            cudaEventRecord(e0, s);
+            ozaki_split(da->ptr, m, k, k, 1, 128, slices, sa, ea, s);
+            ozaki_split(db->ptr, n, k, k, 1, 64, slices, sb, eb, s);
+            OzakiArgs p;
+            p.a = sa;
+            p.b = sb;
+            p.a_slice = static_cast<long long>(abytes);
+            p.b_slice = static_cast<long long>(bbytes);
+            p.a_exp = ea;
+            p.b_exp = eb;
+            p.m = m;
+            p.n = n;
+            p.mpad = (m + 127) / 128 * 128;
+            p.npad = (n + 63) / 64 * 64;
+            p.kpad = (k + 63) / 64 * 64;
+            p.slices = slices;
+            p.symmetric = symmetric ? 1 : 0;
+            p.c = dc->ptr;
+            p.ldc = n;
+            launch_ozaki_gemm(p, s);
+            cudaEventRecord(e1, s);
+        } else {
+            GemmArgs g;
+            g.a.nf = g.b.nf = 1;
+            g.a.nr = g.b.nr = 1;
+            g.a.ptr[0] = da->ptr;
+            g.b.ptr[0] = db->ptr;
+            g.a.rstride[0][0] = k;
+            g.b.rstride[0][0] = k;
+            g.a.kstride[0] = g.b.kstride[0] = 1;
+            g.n = k;
+            g.rows = m;
+            g.cols = n;
+            g.symmetric_out = symmetric ? 1 : 0;
+            EpiSet e;
+            e.count = 1;
+            e.d[0].mode = kEpiStore;
+            e.d[0].out = dc->ptr;
+            cudaEventRecord(e0, s);
+            if (launch_gemm_multi(g, e, s) < 0) {
+                g.symmetric_out = 0;
+                g.mode = kEpiStore;
+                g.out = dc->ptr;
+                launch_gemm(g, s);
+            }
+            cudaEventRecord(e1, s);
+        }
+        check_cuda(cudaGetLastError(), "dgemm launch");
+        check_cuda(cudaMemcpyAsync(c, dc->ptr, sizeof(double) * m * n, cudaMemcpyDeviceToHost, s), "D2H");
+        check_cuda(cudaStreamSynchronize(s), "sync");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms_out) *ms_out = ms;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (sa) cudaFree(sa);
+        if (sb) cudaFree(sb);
+        if (ea) cudaFree(ea);
+        if (eb) cudaFree(eb);
+    });
+}
+
 int us_device_stream(int32_t device, void** stream_out) {
     return guarded([&] { *stream_out = static_cast<void*>(ustats::dev::Runtime::get(device).stream()); });
 }

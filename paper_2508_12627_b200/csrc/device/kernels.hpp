@@ -14,6 +14,28 @@ constexpr int kMaxFactors = 8;       // factors multiplied inside one kernel
 constexpr int kMaxGemmFactors = 6;   // factors per GEMM operand (prologue product)
 constexpr int kMaxRowDims = 3;       // ids folded into one GEMM row / column index
 
+// FP64 GEMM by Ozaki splitting on the INT8 tensor cores (gemm_ozaki.cu):
+// C (m x n, row stride ldc) = A B^T with A m x k and B n x k given as
+// pre-split digit slices (ozaki_split: tiled K-major int8, row exponents).
+constexpr int kOzMaxSlices = 7;
+struct OzakiArgs {
+    const int8_t* a = nullptr;   // slices of A: tiles of 128 rows x 64 bytes
+    const int8_t* b = nullptr;   // slices of B: tiles of 64 rows x 64 bytes
+    long long a_slice = 0, b_slice = 0;  // bytes between consecutive slices
+    const int* a_exp = nullptr;
+    const int* b_exp = nullptr;
+    long long m = 0, n = 0, mpad = 0, npad = 0, kpad = 0;
+    int slices = 7;
+    int symmetric = 0;           // B = A: upper tiles only, mirrored stores
+    double* c = nullptr;
+    long long ldc = 0;
+};
+std::size_t ozaki_slice_bytes(long long rows, long long k, int tile_rows);
+int ozaki_split(const double* x, long long rows, long long k, long long rs, long long ks, int tile_rows, int slices,
+                int8_t* out, int* exps, cudaStream_t s);
+long long ozaki_tile_count(const OzakiArgs& p);
+int launch_ozaki_gemm(const OzakiArgs& p, cudaStream_t s);
+
 // Multi-consumer matrix sweep: ONE pass over a matrix X (row-major view,
 // X(R, C) = x[R * xr + C]) feeding several reductions that would each have
 // streamed X again. Per row the kernel forms the power sums
