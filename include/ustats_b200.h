@@ -49,7 +49,9 @@ typedef struct us_config {
     int32_t flags;               /* bit0 share, bit1 fuse epilogues, bit2 symmetry, bit3 reorder,
                                     bit4 donate device inputs (sparsified in place, no copy),
                                     bit5 row sharding across ranks (else V-term sharding),
-                                    bit6 serial launch (one stream); US_FLAGS_DEFAULT = 0xF */
+                                    bit6 serial launch (one stream),
+                                    bit7 exact DMMA only (no INT8 tensor-core emulation of
+                                    large FP64 GEMMs); US_FLAGS_DEFAULT = 0xF */
     int32_t emulate_world;       /* row sharding over this many virtual ranks on one device (tests) */
 } us_config;
 

@@ -58,6 +58,7 @@ class Config:
     donate_inputs: bool = False  # device inputs sparsified in place (saves one copy)
     shard_rows: bool = False     # multi-GPU: row-shard every op (else V-term sharding)
     serial_launch: bool = False  # one CUDA stream (no GEMM / reduction overlap)
+    fp64_emulation: bool = True  # large FP64 GEMMs on the INT8 tensor cores (Ozaki digits); False = DMMA only
     emulate_world: int = 0       # row sharding over virtual ranks on one device (tests)
 
     def native(self) -> N.UsConfig:
@@ -75,7 +76,8 @@ class Config:
         c.world_size = self.world_size
         c.flags = (1 if self.share else 0) | (2 if self.fuse_epilogues else 0) | \
                   (4 if self.symmetry else 0) | (8 if self.reorder else 0) | (16 if self.donate_inputs else 0) | \
-                  (32 if self.shard_rows else 0) | (64 if self.serial_launch else 0)
+                  (32 if self.shard_rows else 0) | (64 if self.serial_launch else 0) | \
+                  (0 if self.fp64_emulation else 128)
         c.emulate_world = self.emulate_world
         return c
 

@@ -63,6 +63,7 @@ ustats::Config to_config(const us_config* c) {
     cfg.device.donate_inputs = c->flags & 16;
     cfg.device.shard_rows = c->flags & 32;
     cfg.device.serial_launch = c->flags & 64;
+    cfg.device.fp64_emulation = !(c->flags & 128);
     cfg.device.emulate_world = c->emulate_world;
     return cfg;
 }

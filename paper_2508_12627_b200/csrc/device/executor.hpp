@@ -261,6 +261,8 @@ class Program {
     void fuse_epilogues();
     void fuse_sweeps();
     void run_sweep(const Op& op);
+    bool emulated_eligible(const GemmArgs& g) const;
+    int run_emulated(const GemmArgs& g, const EpiSet& set);
     std::pair<long long, long long> sweep_strides(const View& v, int row_id, int col_id) const;
     bool tma_plain(const View& v, const std::vector<int>& rows, int e) const;
     void launch(Op& op);

@@ -121,10 +121,12 @@ struct TmaArgs {
     // Split-K tail (the last, partial wave): phase 1 computes K-slices of the
     // leftover tiles into kpart, phase 2 sums the slices in order and runs the
     // epilogues; phase 0 is the ordinary full-K tile.
-    int phase;
+    int phase;             // 3: the product already exists in `prod` (an emulated GEMM): epilogues only
     int ksplit;
     long long slot_base;   // reduction-partial slot of this launch's first tile
     double* kpart;
+    const double* prod;    // phase 3: row-major product, row stride ldp
+    long long ldp;
     EpiSet epis;
 };
 
@@ -172,7 +174,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int warp = tid >> 5, lane = tid & 31;
     double* tile = sm.u.tile;
 
-    if (p.phase != 2) {
+    if (p.phase == 3) {
+        // the product tile from global memory (coalesced rows)
+        for (int i = tid; i < BM * BN; i += THREADS) {
+            const int r = i >> 7, c = i & 127;
+            const long long R = r0 + r, C = c0 + c;
+            tile[r * TP + c] = (R < p.rows && C < p.cols) ? p.prod[R * p.ldp + C] : 0.0;
+        }
+    } else if (p.phase != 2) {
         if (tid == 0) {
             for (int s = 0; s < STAGES; ++s) {
                 mbar_init(&sm.full[s], 1);
@@ -518,6 +527,8 @@ int launch_gemm_multi(const GemmArgs& a, const EpiSet& epis, cudaStream_t s) {
     args.ksplit = 1;
     args.slot_base = 0;
     args.kpart = nullptr;
+    args.prod = nullptr;
+    args.ldp = 0;
     args.epis = epis;
     const long long tm_ = (a.rows + BM - 1) / BM, tn_ = (a.cols + BN - 1) / BN;
     const long long total = args.symmetric ? tm_ * (tm_ + 1) / 2 : tm_ * tn_;
@@ -579,6 +590,51 @@ int launch_gemm_multi(const GemmArgs& a, const EpiSet& epis, cudaStream_t s) {
     }
     int launched = launched_kernels;
     const long long tm = tm_, tn = tn_;
+    for (int q = 0; q < epis.count; ++q) {
+        const EpiDesc& d = epis.d[q];
+        if (d.mode == kEpiSumAll) {
+            epi_finalize_scalar<<<1, 1024, 0, s>>>(d.partial, blocks, d.out, a.accumulate);
+        } else if (d.mode == kEpiSumCols) {
+            epi_finalize_vector<<<static_cast<unsigned>((a.rows + 255) / 256), 256, 0, s>>>(d.partial, tn, a.rows, d.out,
+                                                                                          a.accumulate);
+        } else if (d.mode == kEpiSumRows) {
+            epi_finalize_vector<<<static_cast<unsigned>((a.cols + 255) / 256), 256, 0, s>>>(d.partial, tm, a.cols, d.out,
+                                                                                          a.accumulate);
+        } else {
+            continue;
+        }
+        ++launched;
+    }
+    return launched;
+}
+
+// Fused epilogues over a product that already exists (the Ozaki-emulated
+// GEMM wrote it row-major into `prod`): the same tile list, the same
+// epilogue code and partial-slot layout as launch_gemm_multi, no MMA.
+int launch_epilogue_pass(const GemmArgs& a, const EpiSet& epis, const double* prod, long long ldp, cudaStream_t s) {
+    if (epis.count < 1 || epis.count > kMaxEpilogues) return -1;
+    TmaArgs args;
+    args.rows = a.rows;
+    args.cols = a.cols;
+    args.n = a.n;
+    args.tile_begin = a.tile_begin;
+    args.symmetric = (a.symmetric_out && a.rows == a.cols) ? 1 : 0;
+    args.colmajor = a.tri_colmajor;
+    args.accumulate = a.accumulate;
+    args.phase = 3;
+    args.ksplit = 1;
+    args.slot_base = 0;
+    args.kpart = nullptr;
+    args.prod = prod;
+    args.ldp = ldp;
+    args.epis = epis;
+    const long long tm = (a.rows + BM - 1) / BM, tn = (a.cols + BN - 1) / BN;
+    const long long total = args.symmetric ? tm * (tm + 1) / 2 : tm * tn;
+    const long long blocks = a.tile_count < 0 ? total - a.tile_begin : a.tile_count;
+    if (blocks <= 0) return 0;
+    CUtensorMap none{};
+    launch_tma<true, true>(none, none, args, blocks, s);
+    int launched = 1;
     for (int q = 0; q < epis.count; ++q) {
         const EpiDesc& d = epis.d[q];
         if (d.mode == kEpiSumAll) {

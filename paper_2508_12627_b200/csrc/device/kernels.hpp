@@ -173,6 +173,8 @@ bool gemm_tma_eligible(const GemmArgs& a, int* a_kmajor, int* b_kmajor);
 // upper tiles and mirrors every epilogue). Returns kernels launched, or -1
 // if the operands are not TMA-eligible.
 int launch_gemm_multi(const GemmArgs& a, const EpiSet& epis, cudaStream_t s);
+// The fused epilogues of `epis` over an existing row-major product (row stride ldp).
+int launch_epilogue_pass(const GemmArgs& a, const EpiSet& epis, const double* prod, long long ldp, cudaStream_t s);
 std::size_t gemm_epi_partial_entries(const GemmArgs& a, int mode);
 std::size_t gemm_partial_entries(const GemmArgs& a);
 

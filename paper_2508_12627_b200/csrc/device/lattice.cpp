@@ -213,7 +213,8 @@ std::string plan_key(const std::vector<StatisticSpec>& specs, const std::vector<
                     std::to_string(c.exhaustive_index_bound) + "," + std::to_string(c.exact_treewidth_bound) + "|" +
                     std::to_string(d.share_subexpressions) + std::to_string(d.fuse_epilogues) +
                     std::to_string(d.exploit_symmetry) + std::to_string(d.reorder_for_sharing) +
-                    std::to_string(d.serial_launch) + std::to_string(d.shard_rows) + "," + std::to_string(d.rank) + "," +
+                    std::to_string(d.serial_launch) + std::to_string(d.shard_rows) + std::to_string(d.fp64_emulation) +
+                    "," + std::to_string(d.rank) + "," +
                     std::to_string(d.world_size) + "," + std::to_string(d.emulate_world) + "," +
                     std::to_string(d.memory_budget_bytes) + "|";
     for (const Buf& b : uniq) k += std::to_string(b->order) + (b->symmetric ? "s" : "g");

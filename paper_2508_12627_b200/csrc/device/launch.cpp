@@ -209,6 +209,66 @@ void Program::run_stream(const Op& op, double* out) {
     }
 }
 
+// FP64 emulation on the INT8 tensor cores (gemm_ozaki.cu) for large plain
+// products whose K keeps every digit diagonal exact in int32.
+constexpr int kOzSlices = 7;
+constexpr long long kOzMaxK = 19000;    // 7 products of K * 127^2 per diagonal < 2^31
+constexpr long long kOzMinDim = 1024;   // below, DMMA is as fast and needs no digit pass
+
+bool Program::emulated_eligible(const GemmArgs& g) const {
+    if (!config_.device.fp64_emulation || slice_world_ > 1 || g.tile_count >= 0) return false;
+    if (g.n > kOzMaxK || g.rows < kOzMinDim || g.cols < kOzMinDim) return false;
+    if (g.a.nf != 1 || g.b.nf != 1 || g.a.nr != 1 || g.b.nr != 1) return false;
+    return true;
+}
+
+// Digits of both operands, the product (straight into a plain store's output,
+// else into scratch), then the fused epilogues over the stored product.
+int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
+    cudaStream_t s = rt_->stream();
+    const std::size_t abytes = ozaki_slice_bytes(g.rows, g.n, 128), bbytes = ozaki_slice_bytes(g.cols, g.n, 64);
+    int8_t* da = reinterpret_cast<int8_t*>(rt_->scratch((abytes * kOzSlices + 7) / 8));
+    int8_t* db = reinterpret_cast<int8_t*>(rt_->scratch((bbytes * kOzSlices + 7) / 8));
+    int* ea = reinterpret_cast<int*>(rt_->scratch(static_cast<std::size_t>(g.rows + 1) / 2 + 1));
+    int* eb = reinterpret_cast<int*>(rt_->scratch(static_cast<std::size_t>(g.cols + 1) / 2 + 1));
+    int launched = ozaki_split(g.a.ptr[0], g.rows, g.n, g.a.rstride[0][0], g.a.kstride[0], 128, kOzSlices, da, ea, s);
+    launched += ozaki_split(g.b.ptr[0], g.cols, g.n, g.b.rstride[0][0], g.b.kstride[0], 64, kOzSlices, db, eb, s);
+    const bool sym = g.symmetric_out && g.rows == g.cols;
+    // a lone plain store takes the product directly
+    const bool direct = set.count == 1 && set.d[0].mode == kEpiStore && set.d[0].nw == 0 && set.d[0].self_power == 1 &&
+                        !set.d[0].transpose && !g.accumulate;
+    double* prod = direct ? set.d[0].out : rt_->scratch(static_cast<std::size_t>(g.rows * g.cols));
+    OzakiArgs p;
+    p.a = da;
+    p.b = db;
+    p.a_slice = static_cast<long long>(abytes);
+    p.b_slice = static_cast<long long>(bbytes);
+    p.a_exp = ea;
+    p.b_exp = eb;
+    p.m = g.rows;
+    p.n = g.cols;
+    p.mpad = (g.rows + 127) / 128 * 128;
+    p.npad = (g.cols + 63) / 64 * 64;
+    p.kpad = (g.n + 63) / 64 * 64;
+    p.slices = kOzSlices;
+    p.symmetric = sym ? 1 : 0;
+    p.c = prod;
+    p.ldc = g.cols;
+    if (launch_ozaki_gemm(p, s) < 0) fail(ErrorCode::InvalidArgument, "executor: emulated GEMM launch failed");
+    ++launched;
+    if (!direct) {
+        const int l = launch_epilogue_pass(g, set, prod, g.cols, s);
+        if (l < 0) fail(ErrorCode::InvalidArgument, "executor: epilogue pass failed");
+        launched += l;
+        rt_->release(prod);
+    }
+    rt_->release(reinterpret_cast<double*>(da));
+    rt_->release(reinterpret_cast<double*>(db));
+    rt_->release(reinterpret_cast<double*>(ea));
+    rt_->release(reinterpret_cast<double*>(eb));
+    return launched;
+}
+
 void Program::run_gemm(const Op& op, double* out) {
     std::vector<View> fa = op.fa, fb = op.fb;
     const int e = op.e;
@@ -324,7 +384,9 @@ void Program::run_gemm(const Op& op, double* out) {
         const bool chunked = slice_world_ == 1 && op.symmetric_out && g.rows == g.cols && fa[0].buf == fb[0].buf &&
                              src && src->ready.size() > 1;
         rt_->begin(Runtime::kGemm);
-        if (!chunked) {
+        if (!chunked && emulated_eligible(g)) {
+            launched = run_emulated(g, set);
+        } else if (!chunked) {
             launched = launch_gemm_multi(g, set, rt_->stream());
         } else {
             // Pieces run concurrently on the chunk streams (a piece smaller than

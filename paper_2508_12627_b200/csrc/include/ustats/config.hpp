@@ -20,6 +20,10 @@ struct DeviceConfig {
     bool reorder_for_sharing = true;   ///< choose among equal-width orders to maximize sharing
     bool donate_inputs = false;        ///< device inputs may be sparsified in place (no copy)
     bool serial_launch = false;        ///< one stream only (no GEMM/reduction overlap)
+    /// Large FP64 GEMMs (K <= 19000) run as Ozaki digit splitting on the INT8
+    /// tcgen05 tensor cores (7 digits: ~1e-12 relative to the row-scale
+    /// product) instead of DMMA; false = DMMA everywhere.
+    bool fp64_emulation = true;
     /// Multi-GPU scheme: false = V-terms sharded over ranks (LPT, one all-reduce
     /// of the term vector); true = every op row-sharded over ranks (GEMM tile
     /// ranges / leading-index slices, one all-reduce per materialized output).
