@@ -574,15 +574,15 @@ int us_dgemm(int32_t method, int32_t slices, int32_t symmetric, int64_t m, int64
         int8_t *sa = nullptr, *sb = nullptr;
         int *ea = nullptr, *eb = nullptr;
         if (method == 1) {
-            if (slices < 1 || slices > kOzMaxSlices) ustats::fail(ustats::ErrorCode::InvalidArgument, "slices must be 1..7");
-            const std::size_t abytes = ozaki_slice_bytes(m, k, 128), bbytes = ozaki_slice_bytes(n, k, 64);
+            if (slices < 4 || slices > kOzMaxSlices) ustats::fail(ustats::ErrorCode::InvalidArgument, "slices must be 4..7");
+            const std::size_t abytes = ozaki_slice_bytes(m, k, 128), bbytes = ozaki_slice_bytes(n, k, 128);
             check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&sa), abytes * slices, s), "alloc");
             check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&sb), bbytes * slices, s), "alloc");
             check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&ea), sizeof(int) * m, s), "alloc");
             check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&eb), sizeof(int) * n, s), "alloc");
             cudaEventRecord(e0, s);
             ozaki_split(da->ptr, m, k, k, 1, 128, slices, sa, ea, s);
-            ozaki_split(db->ptr, n, k, k, 1, 64, slices, sb, eb, s);
+            ozaki_split(db->ptr, n, k, k, 1, 128, slices, sb, eb, s);
             OzakiArgs p;
             p.a = sa;
             p.b = sb;
@@ -593,7 +593,7 @@ int us_dgemm(int32_t method, int32_t slices, int32_t symmetric, int64_t m, int64
             p.m = m;
             p.n = n;
             p.mpad = (m + 127) / 128 * 128;
-            p.npad = (n + 63) / 64 * 64;
+            p.npad = (n + 127) / 128 * 128;
             p.kpad = (k + 63) / 64 * 64;
             p.slices = slices;
             p.symmetric = symmetric ? 1 : 0;

@@ -27,9 +27,12 @@ namespace ustats::dev {
 
 namespace {
 
-constexpr int OZ_BM = 128, OZ_BN = 64, OZ_BK = 64;  // tile rows, tile cols, K bytes per stage
-constexpr int OZ_STAGES = 2;
-constexpr int OZ_THREADS = 128;
+constexpr int OZ_BM = 128, OZ_BN = 128;   // output tile
+constexpr int OZ_BK = 64;                  // K bytes per tile of the global digit layout
+constexpr int OZ_SK = 32;                  // K bytes per pipeline stage (one MMA k-step)
+constexpr int OZ_STAGES = 4;
+constexpr int OZ_THREADS = 192;            // warps 0-3 epilogue, 4 producer, 5 MMA issuer
+constexpr int OZ_TILE_STAGE = OZ_BM * OZ_SK;  // 4 KiB per operand slice per stage
 
 __device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 
@@ -48,6 +51,9 @@ __device__ __forceinline__ void bar_init(unsigned long long* b, unsigned count) 
 __device__ __forceinline__ void bar_expect(unsigned long long* b, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void bar_arrive(unsigned long long* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
 __device__ __forceinline__ void bar_wait(unsigned long long* b, unsigned parity) {
     asm volatile(
         "{\n.reg .pred p;\nOZW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra OZW_%=;\n}\n" ::"r"(
@@ -61,30 +67,60 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
         "l"(reinterpret_cast<unsigned long long>(src)), "r"(bytes), "r"(su32(bar))
         : "memory");
 }
+__device__ __forceinline__ void tmem_ld16(unsigned addr, unsigned* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+}
 
 struct OzSmem {
-    int8_t a[OZ_STAGES][kOzMaxSlices][OZ_BM * OZ_BK];  // 8 KiB per slice
-    int8_t b[OZ_STAGES][kOzMaxSlices][OZ_BN * OZ_BK];  // 4 KiB per slice
-    unsigned long long full[OZ_STAGES], empty[OZ_STAGES], done;
+    int8_t a[OZ_STAGES][kOzMaxSlices][OZ_TILE_STAGE];
+    int8_t b[OZ_STAGES][kOzMaxSlices][OZ_TILE_STAGE];
+    unsigned long long full[OZ_STAGES], empty[OZ_STAGES], done[2], drained;
     unsigned tmem;
 };
 
-// One 128 x 64 output tile per CTA. Warp 0 lane 0 streams the digit tiles,
-// warp 1 lane 0 issues the MMAs, all four warps assemble the FP64 tile.
+// One 128 x 128 output tile per CTA, in two passes over K so that the digit
+// diagonals fit TMEM at N = 128 (the full-rate MMA shape): pass 0 sums the
+// high diagonals d = 4..S-1 (slices 0..S-1), pass 1 the low ones d = 0..3
+// (slices 0..3), each into <= 4 int32 accumulators of 128 columns. Between
+// the passes the epilogue warps drain pass 0 into the output tile (FP64,
+// before the row/column exponents); pass 1 adds to it.
+template <int S, int D0, int D1>
+__device__ __forceinline__ void oz_issue_stage(unsigned tmem, const unsigned long long* da, const unsigned long long* db,
+                                               unsigned idesc, bool first) {
+    // diagonals [D0, D1) of the digit products, accumulators at (d - D0) * 128 columns
+#pragma unroll
+    for (int d = D0; d < D1; ++d)
+#pragma unroll
+        for (int t = 0; t <= d; ++t) {
+            const int u = d - t;
+            if (t >= S || u >= S) continue;
+            const unsigned acc = tmem + static_cast<unsigned>((d - D0) * OZ_BN);
+            const unsigned accumulate = (first && t == 0) ? 0u : 1u;
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(acc),
+                "l"(da[t]), "l"(db[u]), "r"(idesc), "r"(accumulate));
+        }
+}
+
+template <int S>
 __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) {
     extern __shared__ unsigned char oz_raw[];
     OzSmem& sm = *reinterpret_cast<OzSmem*>((reinterpret_cast<unsigned long long>(oz_raw) + 1023) & ~1023ull);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int S = p.slices;
+    constexpr int split = S > 4 ? 4 : S;  // diagonals of pass 1: [0, split); pass 0: [split, S)
     const long long tiles_n = p.npad / OZ_BN;
     long long tm, tn;
-    if (p.symmetric) {  // upper tiles (by 128-row blocks) in column order
-        // tile t of the column-ordered list of (tm, tn) with 128 tm < 64 (tn + 1)
+    if (p.symmetric) {  // upper tiles, column by column
         long long t = blockIdx.x, col = 0;
-        for (;; ++col) {
-            const long long h = (64 * (col + 1) + OZ_BM - 1) / OZ_BM;  // row tiles touching the upper part
-            if (t < h) break;
-            t -= h;
+        while (t > col) {
+            t -= col + 1;
+            ++col;
         }
         tm = t;
         tn = col;
@@ -92,20 +128,23 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
         tm = blockIdx.x / tiles_n;
         tn = blockIdx.x % tiles_n;
     }
-    const long long kt_count = p.kpad / OZ_BK;
-    const int8_t* abase = p.a + tm * kt_count * (OZ_BM * OZ_BK);
-    const int8_t* bbase = p.b + tn * kt_count * (OZ_BN * OZ_BK);
+    const long long ksteps = p.kpad / OZ_SK;
+    const long long tile_bytes = OZ_BM * OZ_BK;  // one 128-row x 64-byte tile of the global layout
+    const int8_t* abase = p.a + tm * (p.kpad / OZ_BK) * tile_bytes;
+    const int8_t* bbase = p.b + tn * (p.kpad / OZ_BK) * tile_bytes;
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&sm.tmem)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (tid == 32) {
+    if (tid == 128) {
         for (int s = 0; s < OZ_STAGES; ++s) {
             bar_init(&sm.full[s], 1);
             bar_init(&sm.empty[s], 1);
         }
-        bar_init(&sm.done, 1);
+        bar_init(&sm.done[0], 1);
+        bar_init(&sm.done[1], 1);
+        bar_init(&sm.drained, 4);
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -113,79 +152,122 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
     asm volatile("tcgen05.fence::after_thread_sync;");
     const unsigned tmem = sm.tmem;
 
-    if (tid == 0) {  // producer
-        const unsigned bytes = static_cast<unsigned>(S) * (OZ_BM + OZ_BN) * OZ_BK;
-        for (long long kt = 0; kt < kt_count; ++kt) {
-            const int s = static_cast<int>(kt % OZ_STAGES);
-            if (kt >= OZ_STAGES) bar_wait(&sm.empty[s], static_cast<unsigned>(((kt / OZ_STAGES) - 1) & 1));
-            bar_expect(&sm.full[s], bytes);
-            for (int t = 0; t < S; ++t) {
-                bulk_load(sm.a[s][t], abase + t * p.a_slice + kt * (OZ_BM * OZ_BK), OZ_BM * OZ_BK, &sm.full[s]);
-                bulk_load(sm.b[s][t], bbase + t * p.b_slice + kt * (OZ_BN * OZ_BK), OZ_BN * OZ_BK, &sm.full[s]);
+    if (tid == 128) {  // producer: pass 0 then pass 1 through one stage ring
+        long long it = 0;
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+            const int ns = pass == 0 ? S : split;
+            if (pass == 0 && split >= S) continue;
+#pragma unroll 1
+            for (long long k = 0; k < ksteps; ++k, ++it) {
+                const int s = static_cast<int>(it % OZ_STAGES);
+                if (it >= OZ_STAGES) bar_wait(&sm.empty[s], static_cast<unsigned>(((it / OZ_STAGES) - 1) & 1));
+                bar_expect(&sm.full[s], static_cast<unsigned>(2 * ns * OZ_TILE_STAGE));
+                // stage k = half (k % 2) of global k-tile k / 2: its two 16-byte chunks are contiguous
+                const long long off = (k >> 1) * tile_bytes + (k & 1) * OZ_TILE_STAGE;
+                for (int t = 0; t < ns; ++t) {
+                    bulk_load(sm.a[s][t], abase + t * p.a_slice + off, OZ_TILE_STAGE, &sm.full[s]);
+                    bulk_load(sm.b[s][t], bbase + t * p.b_slice + off, OZ_TILE_STAGE, &sm.full[s]);
+                }
             }
         }
-    } else if (tid == 32) {  // MMA issuer
-        // kind::i8, int32 accumulate, signed A and B, both K-major, N = 64, M = 128
+    } else if (tid == 160) {  // MMA issuer: descriptors precomputed per stage, products unrolled
+        // kind::i8, int32 accumulate, signed A and B, both K-major, N = 128, M = 128
         const unsigned idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((OZ_BN >> 3) << 17) | ((OZ_BM >> 4) << 24);
-        for (long long kt = 0; kt < kt_count; ++kt) {
-            const int s = static_cast<int>(kt % OZ_STAGES);
-            bar_wait(&sm.full[s], static_cast<unsigned>((kt / OZ_STAGES) & 1));
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            for (int t = 0; t < S; ++t)
-                for (int u = 0; t + u < S; ++u) {
-                    const unsigned acc = tmem + static_cast<unsigned>((t + u) * OZ_BN);
-                    for (int ks = 0; ks < OZ_BK / 32; ++ks) {
-                        // 32 K bytes = two 16-byte chunks: chunk stride = rows x 16 B
-                        const unsigned long long da =
-                            umma_desc(su32(sm.a[s][t]) + ks * 2 * OZ_BM * 16, OZ_BM * 16, 128);
-                        const unsigned long long db =
-                            umma_desc(su32(sm.b[s][u]) + ks * 2 * OZ_BN * 16, OZ_BN * 16, 128);
-                        const unsigned accumulate = (kt > 0 || ks > 0 || t > 0) ? 1u : 0u;  // first product of diagonal t+u: t = 0
-                        asm volatile(
-                            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(acc),
-                            "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
-                    }
+        unsigned long long da[OZ_STAGES][S], db[OZ_STAGES][S];
+#pragma unroll
+        for (int s = 0; s < OZ_STAGES; ++s)
+#pragma unroll
+            for (int t = 0; t < S; ++t) {
+                da[s][t] = umma_desc(su32(sm.a[s][t]), OZ_BM * 16, 128);
+                db[s][t] = umma_desc(su32(sm.b[s][t]), OZ_BN * 16, 128);
+            }
+        long long it = 0;
+        if (split < S) {
+#pragma unroll 1
+            for (long long k = 0; k < ksteps; ++k, ++it) {
+                const int s = static_cast<int>(it % OZ_STAGES);
+                bar_wait(&sm.full[s], static_cast<unsigned>((it / OZ_STAGES) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                switch (s) {
+#pragma unroll
+                    case 0: oz_issue_stage<S, split, S>(tmem, da[0], db[0], idesc, k == 0); break;
+                    case 1: oz_issue_stage<S, split, S>(tmem, da[1], db[1], idesc, k == 0); break;
+                    case 2: oz_issue_stage<S, split, S>(tmem, da[2], db[2], idesc, k == 0); break;
+                    default: oz_issue_stage<S, split, S>(tmem, da[3], db[3], idesc, k == 0); break;
                 }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                    su32(&sm.empty[s])));
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                su32(&sm.done[0])));
+            bar_wait(&sm.drained, 0);  // pass 0 read out of TMEM
+            asm volatile("tcgen05.fence::after_thread_sync;");
+        }
+#pragma unroll 1
+        for (long long k = 0; k < ksteps; ++k, ++it) {
+            const int s = static_cast<int>(it % OZ_STAGES);
+            bar_wait(&sm.full[s], static_cast<unsigned>((it / OZ_STAGES) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            switch (s) {
+                case 0: oz_issue_stage<S, 0, split>(tmem, da[0], db[0], idesc, k == 0); break;
+                case 1: oz_issue_stage<S, 0, split>(tmem, da[1], db[1], idesc, k == 0); break;
+                case 2: oz_issue_stage<S, 0, split>(tmem, da[2], db[2], idesc, k == 0); break;
+                default: oz_issue_stage<S, 0, split>(tmem, da[3], db[3], idesc, k == 0); break;
+            }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                 su32(&sm.empty[s])));
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&sm.done)));
-    }
-    __syncwarp();
-    bar_wait(&sm.done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;");
-
-    // epilogue: thread = one row of the tile (TMEM lane), 16 columns at a time
-    const long long row = tm * OZ_BM + warp * 32 + lane;
-    const bool row_ok = row < p.m;
-    const int ea = row_ok ? p.a_exp[row] : 0;
-    for (int c0 = 0; c0 < OZ_BN; c0 += 16) {
-        double v[16];
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            su32(&sm.done[1])));
+    } else if (warp < 4) {  // epilogue warps: thread = one row of the tile (TMEM lane)
+        const long long row = tm * OZ_BM + warp * 32 + lane;
+        const bool row_ok = row < p.m;
+        for (int pass = 0; pass < 2; ++pass) {
+            if (pass == 0 && split >= S) continue;
+            const int d0 = pass == 0 ? split : 0, d1 = pass == 0 ? S : split;
+            bar_wait(&sm.done[pass], 0);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const int ea = row_ok ? p.a_exp[row] : 0;
+            for (int c0 = 0; c0 < OZ_BN; c0 += 16) {
+                double v[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0.0;
-        for (int d = S - 1; d >= 0; --d) {  // smallest contributions first
-            unsigned r[16];
-            const unsigned addr = tmem + (static_cast<unsigned>(warp * 32) << 16) + static_cast<unsigned>(d * OZ_BN + c0);
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-                : "r"(addr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;");
-            const double scale = ldexp(1.0, -7 * (d + 2));
+                for (int j = 0; j < 16; ++j) v[j] = 0.0;
+                if (pass == 1 && split < S && row_ok) {  // the high diagonals, already assembled
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] += static_cast<double>(static_cast<int>(r[j])) * scale;
-        }
-        if (!row_ok) continue;
+                    for (int j = 0; j < 16; ++j) {
+                        const long long col = tn * OZ_BN + c0 + j;
+                        if (col < p.n) v[j] = p.c[row * p.ldc + col];
+                    }
+                }
+                for (int d = d1 - 1; d >= d0; --d) {  // smallest contributions first
+                    unsigned r[16];
+                    tmem_ld16(tmem + (static_cast<unsigned>(warp * 32) << 16) + static_cast<unsigned>((d - d0) * OZ_BN + c0),
+                              r);
+                    const double scale = ldexp(1.0, -7 * (d + 2));
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const long long col = tn * OZ_BN + c0 + j;
-            if (col >= p.n) continue;
-            const double x = ldexp(v[j], ea + p.b_exp[col]);
-            if (p.symmetric && col < row) continue;  // lower part: written by the mirror of (col, row)
-            p.c[row * p.ldc + col] = x;
-            if (p.symmetric && col != row) p.c[col * p.ldc + row] = x;
+                    for (int j = 0; j < 16; ++j) v[j] += static_cast<double>(static_cast<int>(r[j])) * scale;
+                }
+                if (!row_ok) continue;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const long long col = tn * OZ_BN + c0 + j;
+                    if (col >= p.n) continue;
+                    if (pass == 0) {  // partial: the tile itself, no exponents yet
+                        p.c[row * p.ldc + col] = v[j];
+                        continue;
+                    }
+                    if (p.symmetric && col < row) continue;  // lower part: the mirror of (col, row)
+                    const double x = ldexp(v[j], ea + p.b_exp[col]);
+                    p.c[row * p.ldc + col] = x;
+                    if (p.symmetric && col != row) p.c[col * p.ldc + row] = x;
+                }
+            }
+            if (pass == 0) {
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) bar_arrive(&sm.drained);
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -262,24 +344,32 @@ int ozaki_split(const double* x, long long rows, long long k, long long rs, long
 }
 
 long long ozaki_tile_count(const OzakiArgs& p) {
-    const long long tiles_n = p.npad / 64;
-    if (!p.symmetric) return (p.mpad / 128) * tiles_n;
-    long long total = 0;
-    for (long long col = 0; col < tiles_n; ++col) total += (64 * (col + 1) + 127) / 128;
-    return total;
+    const long long tiles_m = p.mpad / OZ_BM, tiles_n = p.npad / OZ_BN;
+    return p.symmetric ? tiles_n * (tiles_n + 1) / 2 : tiles_m * tiles_n;
 }
 
-int launch_ozaki_gemm(const OzakiArgs& p, cudaStream_t s) {
-    if (p.slices < 1 || p.slices > kOzMaxSlices || p.kpad % OZ_BK != 0) return -1;
+template <int S>
+void launch_oz(const OzakiArgs& p, long long tiles, cudaStream_t s) {
     const int bytes = static_cast<int>(sizeof(OzSmem)) + 1024;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(ozaki_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        cudaFuncSetAttribute(ozaki_gemm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         configured = true;
     }
+    ozaki_gemm_kernel<S><<<static_cast<unsigned>(tiles), OZ_THREADS, bytes, s>>>(p);
+}
+
+int launch_ozaki_gemm(const OzakiArgs& p, cudaStream_t s) {
+    if (p.kpad % OZ_BK != 0) return -1;
     const long long tiles = ozaki_tile_count(p);
     if (tiles <= 0) return 0;
-    ozaki_gemm_kernel<<<static_cast<unsigned>(tiles), OZ_THREADS, bytes, s>>>(p);
+    switch (p.slices) {
+        case 4: launch_oz<4>(p, tiles, s); break;
+        case 5: launch_oz<5>(p, tiles, s); break;
+        case 6: launch_oz<6>(p, tiles, s); break;
+        case 7: launch_oz<7>(p, tiles, s); break;
+        default: return -1;
+    }
     return 1;
 }
 

@@ -20,7 +20,7 @@ constexpr int kMaxRowDims = 3;       // ids folded into one GEMM row / column in
 constexpr int kOzMaxSlices = 7;
 struct OzakiArgs {
     const int8_t* a = nullptr;   // slices of A: tiles of 128 rows x 64 bytes
-    const int8_t* b = nullptr;   // slices of B: tiles of 64 rows x 64 bytes
+    const int8_t* b = nullptr;   // slices of B: tiles of 128 rows x 64 bytes (may alias A)
     long long a_slice = 0, b_slice = 0;  // bytes between consecutive slices
     const int* a_exp = nullptr;
     const int* b_exp = nullptr;

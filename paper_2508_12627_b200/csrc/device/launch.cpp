@@ -226,13 +226,17 @@ bool Program::emulated_eligible(const GemmArgs& g) const {
 // else into scratch), then the fused epilogues over the stored product.
 int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
     cudaStream_t s = rt_->stream();
-    const std::size_t abytes = ozaki_slice_bytes(g.rows, g.n, 128), bbytes = ozaki_slice_bytes(g.cols, g.n, 64);
+    const std::size_t abytes = ozaki_slice_bytes(g.rows, g.n, 128), bbytes = ozaki_slice_bytes(g.cols, g.n, 128);
+    // one set of digits when both operands are the same matrix view (A A^T)
+    const bool same = g.a.ptr[0] == g.b.ptr[0] && g.rows == g.cols && g.a.rstride[0][0] == g.b.rstride[0][0] &&
+                      g.a.kstride[0] == g.b.kstride[0];
     int8_t* da = reinterpret_cast<int8_t*>(rt_->scratch((abytes * kOzSlices + 7) / 8));
-    int8_t* db = reinterpret_cast<int8_t*>(rt_->scratch((bbytes * kOzSlices + 7) / 8));
     int* ea = reinterpret_cast<int*>(rt_->scratch(static_cast<std::size_t>(g.rows + 1) / 2 + 1));
-    int* eb = reinterpret_cast<int*>(rt_->scratch(static_cast<std::size_t>(g.cols + 1) / 2 + 1));
+    int8_t* db = same ? da : reinterpret_cast<int8_t*>(rt_->scratch((bbytes * kOzSlices + 7) / 8));
+    int* eb = same ? ea : reinterpret_cast<int*>(rt_->scratch(static_cast<std::size_t>(g.cols + 1) / 2 + 1));
     int launched = ozaki_split(g.a.ptr[0], g.rows, g.n, g.a.rstride[0][0], g.a.kstride[0], 128, kOzSlices, da, ea, s);
-    launched += ozaki_split(g.b.ptr[0], g.cols, g.n, g.b.rstride[0][0], g.b.kstride[0], 64, kOzSlices, db, eb, s);
+    if (!same)
+        launched += ozaki_split(g.b.ptr[0], g.cols, g.n, g.b.rstride[0][0], g.b.kstride[0], 128, kOzSlices, db, eb, s);
     const bool sym = g.symmetric_out && g.rows == g.cols;
     // a lone plain store takes the product directly
     const bool direct = set.count == 1 && set.d[0].mode == kEpiStore && set.d[0].nw == 0 && set.d[0].self_power == 1 &&
@@ -248,7 +252,7 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
     p.m = g.rows;
     p.n = g.cols;
     p.mpad = (g.rows + 127) / 128 * 128;
-    p.npad = (g.cols + 63) / 64 * 64;
+    p.npad = (g.cols + 127) / 128 * 128;
     p.kpad = (g.n + 63) / 64 * 64;
     p.slices = kOzSlices;
     p.symmetric = sym ? 1 : 0;
@@ -263,9 +267,11 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
         rt_->release(prod);
     }
     rt_->release(reinterpret_cast<double*>(da));
-    rt_->release(reinterpret_cast<double*>(db));
     rt_->release(reinterpret_cast<double*>(ea));
-    rt_->release(reinterpret_cast<double*>(eb));
+    if (!same) {
+        rt_->release(reinterpret_cast<double*>(db));
+        rt_->release(reinterpret_cast<double*>(eb));
+    }
     return launched;
 }
 
