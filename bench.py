@@ -38,6 +38,7 @@ sys.path.insert(0, str(ROOT))
 
 FP64_PEAK_TFLOPS = 37.17      # measured: mma.sync f64 issue-rate probe, profiles/r01_fp64_peak_probe.log
 FP64_CUBLAS_TFLOPS = 36.17    # measured: cuBLAS DGEMM 16384^3 on this pool (same log)
+INT8_PEAK_TOPS = 4568.7       # measured: tcgen05.mma kind::i8 issue-rate probe, profiles/r01_int8_peak_probe.log
 CPU_SAMPLE_N = {"C1": 2000, "C2": 4096, "C3": 4096, "C4": 160, "C5": 1024}
 
 
@@ -360,7 +361,21 @@ def main():
     gemm_ms = prof["gemm_ms"] / args.steps
     stream_ms = prof["stream_ms"] / args.steps
     peaks = measured_peaks()
-    if st["executed_gemm_macs"] > 0:
+    if st.get("int8_tensor_ops", 0) > 0 and st.get("emulated_gemm_macs", 0) * 2 > st["executed_gemm_macs"]:
+        # FP64 GEMMs emulated on the INT8 tensor cores (Ozaki digits): the
+        # dominant kernel's roofline is the INT8 tcgen05 rate
+        achieved = st["int8_tensor_ops"] / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": INT8_PEAK_TOPS, "unit": "TOPS (int8)",
+                    "frac": achieved / INT8_PEAK_TOPS if achieved else None,
+                    "kernel": "ozaki_gemm_kernel (tcgen05.mma kind::i8, TMEM accumulators) + digit split + epilogue pass",
+                    "kernel_ms_per_step": gemm_ms, "kernel_share_of_step": gemm_ms / ms_step,
+                    "fp64_equivalent_tflops": 2.0 * st["executed_gemm_macs"] / (gemm_ms * 1e-3) / 1e12
+                    if gemm_ms > 0 else None,
+                    "fp64_dmma_peak_tflops": FP64_PEAK_TFLOPS,
+                    "peak_source": f"measured INT8 tcgen05 issue-rate probe {INT8_PEAK_TOPS} TOPS (M128 N256 K32, "
+                                   f"148 SMs); MEASURED_PEAKS.json has no INT8 entry",
+                    "traffic": ncu_traffic(name, "gemm")}
+    elif st["executed_gemm_macs"] > 0:
         achieved = 2.0 * st["executed_gemm_macs"] / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
         roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                     "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
@@ -385,6 +400,9 @@ def main():
         "config": {"workload": name, "m": m, "n": n, "signature": sig, "terms": int(r.terms),
                    "api": (f"u_statistic('{spec}', sample): components tensorized on the GPU"
                            if use_data else "u_terms(tensors)"),
+                   "gemm": ("FP64 via Ozaki splitting on the INT8 tensor cores (7 signed 7-bit digits per value, "
+                            "exact int32 digit products, FP64 assembly; ~1e-12 relative) where K <= 19000, "
+                            "else FP64 DMMA") if cfg.fp64_emulation else "FP64 DMMA (mma.sync f64)",
                    "parallelism": (f"row-sharded x{world}" if args.shard == "rows" else f"term-sharded x{world}")
                    if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (no flush needed)" if not flush
@@ -394,7 +412,8 @@ def main():
         "gpu_launches": int(st["kernel_launches"]) * args.steps,
         "clocks": clocks.summary(),
         "stats_per_step": {k: st[k] for k in ("multiply_adds", "executed_gemm_macs", "executed_stream_entries",
-                                               "gemm_launches", "stream_launches", "shared_hits")},
+                                               "gemm_launches", "stream_launches", "shared_hits",
+                                               "emulated_gemm_macs", "int8_tensor_ops")},
         "stream_ms_per_step": stream_ms,
     }
     if e2e:

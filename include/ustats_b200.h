@@ -72,6 +72,8 @@ typedef struct us_stats {
     uint64_t stream_launches;
     uint64_t shared_hits;
     uint64_t kernel_launches;       /* every kernel this call enqueued */
+    uint64_t emulated_gemm_macs;    /* FP64 multiply-adds done on the INT8 tensor cores (Ozaki) */
+    uint64_t int8_tensor_ops;       /* INT8 tensor-core operations those issued (2 per MAC) */
 } us_stats;
 
 US_API const char* us_version(void);

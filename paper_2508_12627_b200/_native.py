@@ -45,6 +45,8 @@ class UsStats(C.Structure):
         ("stream_launches", u64),
         ("shared_hits", u64),
         ("kernel_launches", u64),
+        ("emulated_gemm_macs", u64),
+        ("int8_tensor_ops", u64),
     ]
 
     def as_dict(self) -> dict:

@@ -118,6 +118,8 @@ void export_stats(const ustats::RunStats& rs, us_stats* s) {
     s->stream_launches = rs.stream_launches;
     s->shared_hits = rs.shared_hits;
     s->kernel_launches = 0;
+    s->emulated_gemm_macs = 0;
+    s->int8_tensor_ops = 0;
 }
 
 void export_dev(const ustats::dev::StatisticResult& r, int rank, us_stats* s) {
@@ -139,6 +141,8 @@ void export_dev(const ustats::dev::StatisticResult& r, int rank, us_stats* s) {
     rs.shared_hits = r.stats.shared_hits;
     export_stats(rs, s);
     s->kernel_launches = r.stats.kernel_launches;
+    s->emulated_gemm_macs = r.stats.emulated_macs;
+    s->int8_tensor_ops = r.stats.int8_ops;
 }
 
 ustats::dev::StatisticResult run_lattice(int32_t m, int32_t K, const int32_t* tuple_len,
@@ -597,9 +601,16 @@ int us_dgemm(int32_t method, int32_t slices, int32_t symmetric, int64_t m, int64
             p.kpad = (k + 63) / 64 * 64;
             p.slices = slices;
             p.symmetric = symmetric ? 1 : 0;
-            p.c = dc->ptr;
-            p.ldc = n;
+            p.epis.count = 1;
+            p.epis.d[0].mode = kEpiStore;
+            p.epis.d[0].out = dc->ptr;
+            double* work = nullptr;
+            check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&work),
+                                       static_cast<std::size_t>(ozaki_tile_count(p)) * 128 * 128 * sizeof(double), s),
+                       "alloc");
+            p.work = work;
             launch_ozaki_gemm(p, s);
+            cudaFreeAsync(work, s);
             cudaEventRecord(e1, s);
         } else {
             GemmArgs g;

@@ -140,6 +140,8 @@ struct DevStats {
     std::uint64_t stream_launches = 0;
     std::uint64_t shared_hits = 0;
     std::uint64_t kernel_launches = 0;
+    std::uint64_t emulated_macs = 0;  // FP64 MACs of GEMMs run on the INT8 tensor cores
+    std::uint64_t int8_ops = 0;       // INT8 tensor-core ops those issued
     std::uint64_t fused_epilogues = 0;
     std::uint64_t symmetric_gemms = 0;
 };

@@ -21,6 +21,7 @@
 #include <cstdint>
 #include <cstdio>
 
+#include "epilogue.cuh"
 #include "kernels.hpp"
 
 namespace ustats::dev {
@@ -77,9 +78,15 @@ __device__ __forceinline__ void tmem_ld16(unsigned addr, unsigned* r) {
 }
 
 struct OzSmem {
-    int8_t a[OZ_STAGES][kOzMaxSlices][OZ_TILE_STAGE];
-    int8_t b[OZ_STAGES][kOzMaxSlices][OZ_TILE_STAGE];
+    union {
+        struct {
+            int8_t a[OZ_STAGES][kOzMaxSlices][OZ_TILE_STAGE];
+            int8_t b[OZ_STAGES][kOzMaxSlices][OZ_TILE_STAGE];
+        } st;
+        double tile[epi::BM * epi::TP];  // the FP64 product tile once every MMA has read its operands
+    } u;
     unsigned long long full[OZ_STAGES], empty[OZ_STAGES], done[2], drained;
+    double red[4];
     unsigned tmem;
 };
 
@@ -166,8 +173,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
                 // stage k = half (k % 2) of global k-tile k / 2: its two 16-byte chunks are contiguous
                 const long long off = (k >> 1) * tile_bytes + (k & 1) * OZ_TILE_STAGE;
                 for (int t = 0; t < ns; ++t) {
-                    bulk_load(sm.a[s][t], abase + t * p.a_slice + off, OZ_TILE_STAGE, &sm.full[s]);
-                    bulk_load(sm.b[s][t], bbase + t * p.b_slice + off, OZ_TILE_STAGE, &sm.full[s]);
+                    bulk_load(sm.u.st.a[s][t], abase + t * p.a_slice + off, OZ_TILE_STAGE, &sm.full[s]);
+                    bulk_load(sm.u.st.b[s][t], bbase + t * p.b_slice + off, OZ_TILE_STAGE, &sm.full[s]);
                 }
             }
         }
@@ -179,8 +186,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
         for (int s = 0; s < OZ_STAGES; ++s)
 #pragma unroll
             for (int t = 0; t < S; ++t) {
-                da[s][t] = umma_desc(su32(sm.a[s][t]), OZ_BM * 16, 128);
-                db[s][t] = umma_desc(su32(sm.b[s][t]), OZ_BN * 16, 128);
+                da[s][t] = umma_desc(su32(sm.u.st.a[s][t]), OZ_BM * 16, 128);
+                db[s][t] = umma_desc(su32(sm.u.st.b[s][t]), OZ_BN * 16, 128);
             }
         long long it = 0;
         if (split < S) {
@@ -223,6 +230,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
     } else if (warp < 4) {  // epilogue warps: thread = one row of the tile (TMEM lane)
         const long long row = tm * OZ_BM + warp * 32 + lane;
         const bool row_ok = row < p.m;
+        double* work = p.work + static_cast<long long>(blockIdx.x) * (OZ_BM * OZ_BN) + (warp * 32 + lane) * OZ_BN;
         for (int pass = 0; pass < 2; ++pass) {
             if (pass == 0 && split >= S) continue;
             const int d0 = pass == 0 ? split : 0, d1 = pass == 0 ? S : split;
@@ -232,14 +240,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
             for (int c0 = 0; c0 < OZ_BN; c0 += 16) {
                 double v[16];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = 0.0;
-                if (pass == 1 && split < S && row_ok) {  // the high diagonals, already assembled
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const long long col = tn * OZ_BN + c0 + j;
-                        if (col < p.n) v[j] = p.c[row * p.ldc + col];
-                    }
-                }
+                for (int j = 0; j < 16; ++j) v[j] = (pass == 1 && split < S) ? work[c0 + j] : 0.0;  // high diagonals
                 for (int d = d1 - 1; d >= d0; --d) {  // smallest contributions first
                     unsigned r[16];
                     tmem_ld16(tmem + (static_cast<unsigned>(warp * 32) << 16) + static_cast<unsigned>((d - d0) * OZ_BN + c0),
@@ -248,19 +249,17 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
 #pragma unroll
                     for (int j = 0; j < 16; ++j) v[j] += static_cast<double>(static_cast<int>(r[j])) * scale;
                 }
-                if (!row_ok) continue;
+                if (pass == 0) {  // partial, no exponents yet (L2-resident scratch of this tile)
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) work[c0 + j] = v[j];
+                    continue;
+                }
+                // the product tile in shared memory (every MMA has completed: the ring is free)
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
                     const long long col = tn * OZ_BN + c0 + j;
-                    if (col >= p.n) continue;
-                    if (pass == 0) {  // partial: the tile itself, no exponents yet
-                        p.c[row * p.ldc + col] = v[j];
-                        continue;
-                    }
-                    if (p.symmetric && col < row) continue;  // lower part: the mirror of (col, row)
-                    const double x = ldexp(v[j], ea + p.b_exp[col]);
-                    p.c[row * p.ldc + col] = x;
-                    if (p.symmetric && col != row) p.c[col * p.ldc + row] = x;
+                    sm.u.tile[(warp * 32 + lane) * epi::TP + c0 + j] =
+                        (row_ok && col < p.n) ? ldexp(v[j], ea + p.b_exp[col]) : 0.0;
                 }
             }
             if (pass == 0) {
@@ -269,6 +268,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
                 if (lane == 0) bar_arrive(&sm.drained);
             }
         }
+        // the fused consumers of the tile (plain store, Hadamard + reductions), as in the DMMA kernel
+        auto sync128 = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
+        sync128();
+        epi::apply<128>(p.epis, p.m, p.n, p.accumulate, sm.u.tile, tm * OZ_BM, tn * OZ_BN, tm, tn,
+                        p.symmetric && tm != tn, static_cast<long long>(blockIdx.x), sm.red, tid, sync128);
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -370,7 +374,7 @@ int launch_ozaki_gemm(const OzakiArgs& p, cudaStream_t s) {
         case 7: launch_oz<7>(p, tiles, s); break;
         default: return -1;
     }
-    return 1;
+    return 1 + launch_epilogue_finalize(p.m, p.n, p.epis, tiles, p.accumulate, s);
 }
 
 }  // namespace ustats::dev

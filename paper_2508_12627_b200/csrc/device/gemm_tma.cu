@@ -23,6 +23,7 @@
 #include <cmath>
 #include <mutex>
 
+#include "epilogue.cuh"
 #include "kernels.hpp"
 
 namespace ustats::dev {
@@ -121,12 +122,10 @@ struct TmaArgs {
     // Split-K tail (the last, partial wave): phase 1 computes K-slices of the
     // leftover tiles into kpart, phase 2 sums the slices in order and runs the
     // epilogues; phase 0 is the ordinary full-K tile.
-    int phase;             // 3: the product already exists in `prod` (an emulated GEMM): epilogues only
+    int phase;
     int ksplit;
     long long slot_base;   // reduction-partial slot of this launch's first tile
     double* kpart;
-    const double* prod;    // phase 3: row-major product, row stride ldp
-    long long ldp;
     EpiSet epis;
 };
 
@@ -174,14 +173,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int warp = tid >> 5, lane = tid & 31;
     double* tile = sm.u.tile;
 
-    if (p.phase == 3) {
-        // the product tile from global memory (coalesced rows)
-        for (int i = tid; i < BM * BN; i += THREADS) {
-            const int r = i >> 7, c = i & 127;
-            const long long R = r0 + r, C = c0 + c;
-            tile[r * TP + c] = (R < p.rows && C < p.cols) ? p.prod[R * p.ldp + C] : 0.0;
-        }
-    } else if (p.phase != 2) {
+    if (p.phase != 2) {
         if (tid == 0) {
             for (int s = 0; s < STAGES; ++s) {
                 mbar_init(&sm.full[s], 1);
@@ -281,100 +273,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
     const long long slot = p.slot_base + blockIdx.x;
 
-    const long long rows = p.rows, cols = p.cols;
-    for (int q = 0; q < p.epis.count; ++q) {
-        const EpiDesc& d = p.epis.d[q];
-        auto W = [&](long long R, long long C) {
-            double w = 1.0;
-            for (int f = 0; f < d.nw; ++f) w *= __ldg(d.wptr[f] + R * d.wr[f] + C * d.wc[f]);
-            return w;
-        };
-        auto P = [&](double x) { return d.self_power == 2 ? x * x : x; };
-        // element order: column-fastest unless the first weight is column-major
-        const bool cfast = !(d.nw > 0 && d.wr[0] == 1 && d.wc[0] != 1);
-        if (d.mode == kEpiStore || d.mode == kEpiSumAll) {
-            double s = 0.0;
-            for (int i = tid; i < BM * BN; i += THREADS) {
-                const int r = cfast ? (i >> 7) : (i & 127), c = cfast ? (i & 127) : (i >> 7);
-                const long long R = r0 + r, C = c0 + c;
-                if (R >= rows || C >= cols) continue;
-                const double v = P(tile[r * TP + c]) * W(R, C);
-                if (d.mode == kEpiStore) {
-                    double& o = d.out[d.transpose ? C * rows + R : R * cols + C];
-                    o = p.accumulate ? o + v : v;
-                } else {
-                    s += v;
-                }
-            }
-            if (mirror)  // the transposed tile (C, R): same values, weights at (C, R)
-                for (int i = tid; i < BM * BN; i += THREADS) {
-                    const int c = cfast ? (i >> 7) : (i & 127), r = cfast ? (i & 127) : (i >> 7);
-                    const long long R = r0 + r, C = c0 + c;
-                    if (R >= rows || C >= cols) continue;
-                    const double v = P(tile[r * TP + c]) * W(C, R);
-                    if (d.mode == kEpiStore) {
-                        double& o = d.out[d.transpose ? R * rows + C : C * cols + R];
-                        o = p.accumulate ? o + v : v;
-                    } else {
-                        s += v;
-                    }
-                }
-            if (d.mode == kEpiSumAll) {
-                s = warp_sum(s);
-                if (lane == 0) sm.red[warp] = s;
-                __syncthreads();
-                if (tid == 0) {
-                    double tot = 0.0;
-                    for (int w = 0; w < THREADS / 32; ++w) tot += sm.red[w];
-                    d.partial[slot] = tot;
-                }
-                __syncthreads();
-            }
-        } else if (d.mode == kEpiSumCols) {  // out[R] = sum_C
-            for (int r = warp; r < BM; r += THREADS / 32) {
-                const long long R = r0 + r;
-                double s = 0.0;
-                for (int c = lane; c < BN; c += 32) {
-                    const long long C = c0 + c;
-                    if (R < rows && C < cols) s += P(tile[r * TP + c]) * W(R, C);
-                }
-                s = warp_sum(s);
-                if (lane == 0 && R < rows) d.partial[tn * rows + R] = s;
-            }
-            if (mirror)
-                for (int c = warp; c < BN; c += THREADS / 32) {
-                    const long long C = c0 + c;
-                    double s = 0.0;
-                    for (int r = lane; r < BM; r += 32) {
-                        const long long R = r0 + r;
-                        if (R < rows && C < cols) s += P(tile[r * TP + c]) * W(C, R);
-                    }
-                    s = warp_sum(s);
-                    if (lane == 0 && C < rows) d.partial[tm * rows + C] = s;
-                }
-        } else {  // kEpiSumRows: out[C] = sum_R
-            if (tid < BN) {
-                const int c = tid;
-                const long long C = c0 + c;
-                double s = 0.0;
-                for (int r = 0; r < BM; ++r) {
-                    const long long R = r0 + r;
-                    if (R < rows && C < cols) s += P(tile[r * TP + c]) * W(R, C);
-                }
-                if (C < cols) d.partial[tm * cols + C] = s;
-            }
-            if (mirror && tid >= THREADS - BM) {
-                const int r = tid - (THREADS - BM);
-                const long long R = r0 + r;
-                double s = 0.0;
-                for (int c = 0; c < BN; ++c) {
-                    const long long C = c0 + c;
-                    if (R < rows && C < cols) s += P(tile[r * TP + c]) * W(C, R);
-                }
-                if (R < cols) d.partial[tn * cols + R] = s;
-            }
-        }
-    }
+    epi::apply<THREADS>(p.epis, p.rows, p.cols, p.accumulate, tile, r0, c0, tm, tn, mirror, slot, sm.red, tid,
+                        [] { __syncthreads(); });
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -527,8 +427,6 @@ int launch_gemm_multi(const GemmArgs& a, const EpiSet& epis, cudaStream_t s) {
     args.ksplit = 1;
     args.slot_base = 0;
     args.kpart = nullptr;
-    args.prod = nullptr;
-    args.ldp = 0;
     args.epis = epis;
     const long long tm_ = (a.rows + BM - 1) / BM, tn_ = (a.cols + BN - 1) / BN;
     const long long total = args.symmetric ? tm_ * (tm_ + 1) / 2 : tm_ * tn_;
@@ -588,63 +486,24 @@ int launch_gemm_multi(const GemmArgs& a, const EpiSet& epis, cudaStream_t s) {
         go(args, blocks);
         launched_kernels = 1;
     }
-    int launched = launched_kernels;
-    const long long tm = tm_, tn = tn_;
-    for (int q = 0; q < epis.count; ++q) {
-        const EpiDesc& d = epis.d[q];
-        if (d.mode == kEpiSumAll) {
-            epi_finalize_scalar<<<1, 1024, 0, s>>>(d.partial, blocks, d.out, a.accumulate);
-        } else if (d.mode == kEpiSumCols) {
-            epi_finalize_vector<<<static_cast<unsigned>((a.rows + 255) / 256), 256, 0, s>>>(d.partial, tn, a.rows, d.out,
-                                                                                          a.accumulate);
-        } else if (d.mode == kEpiSumRows) {
-            epi_finalize_vector<<<static_cast<unsigned>((a.cols + 255) / 256), 256, 0, s>>>(d.partial, tm, a.cols, d.out,
-                                                                                          a.accumulate);
-        } else {
-            continue;
-        }
-        ++launched;
-    }
+    int launched = launched_kernels + launch_epilogue_finalize(a.rows, a.cols, epis, blocks, a.accumulate, s);
     return launched;
 }
 
-// Fused epilogues over a product that already exists (the Ozaki-emulated
-// GEMM wrote it row-major into `prod`): the same tile list, the same
-// epilogue code and partial-slot layout as launch_gemm_multi, no MMA.
-int launch_epilogue_pass(const GemmArgs& a, const EpiSet& epis, const double* prod, long long ldp, cudaStream_t s) {
-    if (epis.count < 1 || epis.count > kMaxEpilogues) return -1;
-    TmaArgs args;
-    args.rows = a.rows;
-    args.cols = a.cols;
-    args.n = a.n;
-    args.tile_begin = a.tile_begin;
-    args.symmetric = (a.symmetric_out && a.rows == a.cols) ? 1 : 0;
-    args.colmajor = a.tri_colmajor;
-    args.accumulate = a.accumulate;
-    args.phase = 3;
-    args.ksplit = 1;
-    args.slot_base = 0;
-    args.kpart = nullptr;
-    args.prod = prod;
-    args.ldp = ldp;
-    args.epis = epis;
-    const long long tm = (a.rows + BM - 1) / BM, tn = (a.cols + BN - 1) / BN;
-    const long long total = args.symmetric ? tm * (tm + 1) / 2 : tm * tn;
-    const long long blocks = a.tile_count < 0 ? total - a.tile_begin : a.tile_count;
-    if (blocks <= 0) return 0;
-    CUtensorMap none{};
-    launch_tma<true, true>(none, none, args, blocks, s);
-    int launched = 1;
+int launch_epilogue_finalize(long long rows, long long cols, const EpiSet& epis, long long blocks, int accumulate,
+                             cudaStream_t s) {
+    const long long tm = (rows + BM - 1) / BM, tn = (cols + BN - 1) / BN;
+    int launched = 0;
     for (int q = 0; q < epis.count; ++q) {
         const EpiDesc& d = epis.d[q];
         if (d.mode == kEpiSumAll) {
-            epi_finalize_scalar<<<1, 1024, 0, s>>>(d.partial, blocks, d.out, a.accumulate);
+            epi_finalize_scalar<<<1, 1024, 0, s>>>(d.partial, blocks, d.out, accumulate);
         } else if (d.mode == kEpiSumCols) {
-            epi_finalize_vector<<<static_cast<unsigned>((a.rows + 255) / 256), 256, 0, s>>>(d.partial, tn, a.rows, d.out,
-                                                                                          a.accumulate);
+            epi_finalize_vector<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, s>>>(d.partial, tn, rows, d.out,
+                                                                                        accumulate);
         } else if (d.mode == kEpiSumRows) {
-            epi_finalize_vector<<<static_cast<unsigned>((a.cols + 255) / 256), 256, 0, s>>>(d.partial, tm, a.cols, d.out,
-                                                                                          a.accumulate);
+            epi_finalize_vector<<<static_cast<unsigned>((cols + 255) / 256), 256, 0, s>>>(d.partial, tm, cols, d.out,
+                                                                                        accumulate);
         } else {
             continue;
         }

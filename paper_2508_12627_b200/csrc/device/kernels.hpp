@@ -14,28 +14,6 @@ constexpr int kMaxFactors = 8;       // factors multiplied inside one kernel
 constexpr int kMaxGemmFactors = 6;   // factors per GEMM operand (prologue product)
 constexpr int kMaxRowDims = 3;       // ids folded into one GEMM row / column index
 
-// FP64 GEMM by Ozaki splitting on the INT8 tensor cores (gemm_ozaki.cu):
-// C (m x n, row stride ldc) = A B^T with A m x k and B n x k given as
-// pre-split digit slices (ozaki_split: tiled K-major int8, row exponents).
-constexpr int kOzMaxSlices = 7;
-struct OzakiArgs {
-    const int8_t* a = nullptr;   // slices of A: tiles of 128 rows x 64 bytes
-    const int8_t* b = nullptr;   // slices of B: tiles of 128 rows x 64 bytes (may alias A)
-    long long a_slice = 0, b_slice = 0;  // bytes between consecutive slices
-    const int* a_exp = nullptr;
-    const int* b_exp = nullptr;
-    long long m = 0, n = 0, mpad = 0, npad = 0, kpad = 0;
-    int slices = 7;
-    int symmetric = 0;           // B = A: upper tiles only, mirrored stores
-    double* c = nullptr;
-    long long ldc = 0;
-};
-std::size_t ozaki_slice_bytes(long long rows, long long k, int tile_rows);
-int ozaki_split(const double* x, long long rows, long long k, long long rs, long long ks, int tile_rows, int slices,
-                int8_t* out, int* exps, cudaStream_t s);
-long long ozaki_tile_count(const OzakiArgs& p);
-int launch_ozaki_gemm(const OzakiArgs& p, cudaStream_t s);
-
 // Multi-consumer matrix sweep: ONE pass over a matrix X (row-major view,
 // X(R, C) = x[R * xr + C]) feeding several reductions that would each have
 // streamed X again. Per row the kernel forms the power sums
@@ -173,8 +151,10 @@ bool gemm_tma_eligible(const GemmArgs& a, int* a_kmajor, int* b_kmajor);
 // upper tiles and mirrors every epilogue). Returns kernels launched, or -1
 // if the operands are not TMA-eligible.
 int launch_gemm_multi(const GemmArgs& a, const EpiSet& epis, cudaStream_t s);
-// The fused epilogues of `epis` over an existing row-major product (row stride ldp).
-int launch_epilogue_pass(const GemmArgs& a, const EpiSet& epis, const double* prod, long long ldp, cudaStream_t s);
+// The fixed-order finalizers of the reduction epilogues of `epis` after a
+// launch of `blocks` 128 x 128 tiles over a rows x cols product.
+int launch_epilogue_finalize(long long rows, long long cols, const EpiSet& epis, long long blocks, int accumulate,
+                             cudaStream_t s);
 std::size_t gemm_epi_partial_entries(const GemmArgs& a, int mode);
 std::size_t gemm_partial_entries(const GemmArgs& a);
 
@@ -189,5 +169,29 @@ int launch_sum_slices(const double* slices, int C, long long len, double* out, i
 int launch_zero_diagonal_rows(double* data, long long n, long long r0, long long r1, cudaStream_t s);
 // flag[0] = 0 if the n x n matrix is bitwise symmetric, else 1.
 int launch_symmetry_check(const double* data, long long n, int* flag, cudaStream_t s);
+
+// FP64 GEMM by Ozaki splitting on the INT8 tensor cores (gemm_ozaki.cu):
+// C (m x n, row stride ldc) = A B^T with A m x k and B n x k given as
+// pre-split digit slices (ozaki_split: tiled K-major int8, row exponents).
+constexpr int kOzMaxSlices = 7;
+struct OzakiArgs {
+    const int8_t* a = nullptr;   // slices of A: tiles of 128 rows x 64 bytes
+    const int8_t* b = nullptr;   // slices of B: tiles of 128 rows x 64 bytes (may alias A)
+    long long a_slice = 0, b_slice = 0;  // bytes between consecutive slices
+    const int* a_exp = nullptr;
+    const int* b_exp = nullptr;
+    long long m = 0, n = 0, mpad = 0, npad = 0, kpad = 0;
+    int slices = 7;
+    int symmetric = 0;           // B = A: upper tiles only, mirrored epilogues
+    int accumulate = 0;          // epilogue outputs += (pre-zeroed)
+    double* work = nullptr;      // 128 x 128 doubles per tile: the high-diagonal partial between the passes
+    EpiSet epis;                 // fused consumers of the product tile (a plain store is one of them)
+};
+std::size_t ozaki_slice_bytes(long long rows, long long k, int tile_rows);
+int ozaki_split(const double* x, long long rows, long long k, long long rs, long long ks, int tile_rows, int slices,
+                int8_t* out, int* exps, cudaStream_t s);
+long long ozaki_tile_count(const OzakiArgs& p);
+// Launches the emulated GEMM with its fused epilogues and their finalizers.
+int launch_ozaki_gemm(const OzakiArgs& p, cudaStream_t s);
 
 }  // namespace ustats::dev

@@ -521,6 +521,8 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
             res.stats.kernel_launches = shared.kernel_launches + upload_stats.kernel_launches;
             res.stats.fused_epilogues = shared.fused_epilogues;
             res.stats.symmetric_gemms = shared.symmetric_gemms;
+            res.stats.emulated_macs = shared.emulated_macs;
+            res.stats.int8_ops = shared.int8_ops;
         }
         res.upload_seconds = upload_s;
         res.contract_seconds = contract_s;

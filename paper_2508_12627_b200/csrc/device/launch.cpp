@@ -238,10 +238,6 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
     if (!same)
         launched += ozaki_split(g.b.ptr[0], g.cols, g.n, g.b.rstride[0][0], g.b.kstride[0], 128, kOzSlices, db, eb, s);
     const bool sym = g.symmetric_out && g.rows == g.cols;
-    // a lone plain store takes the product directly
-    const bool direct = set.count == 1 && set.d[0].mode == kEpiStore && set.d[0].nw == 0 && set.d[0].self_power == 1 &&
-                        !set.d[0].transpose && !g.accumulate;
-    double* prod = direct ? set.d[0].out : rt_->scratch(static_cast<std::size_t>(g.rows * g.cols));
     OzakiArgs p;
     p.a = da;
     p.b = db;
@@ -256,15 +252,22 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
     p.kpad = (g.n + 63) / 64 * 64;
     p.slices = kOzSlices;
     p.symmetric = sym ? 1 : 0;
-    p.c = prod;
-    p.ldc = g.cols;
-    if (launch_ozaki_gemm(p, s) < 0) fail(ErrorCode::InvalidArgument, "executor: emulated GEMM launch failed");
-    ++launched;
-    if (!direct) {
-        const int l = launch_epilogue_pass(g, set, prod, g.cols, s);
-        if (l < 0) fail(ErrorCode::InvalidArgument, "executor: epilogue pass failed");
-        launched += l;
-        rt_->release(prod);
+    p.accumulate = g.accumulate;
+    p.epis = set;  // the same fused consumers (and partial slots) as the DMMA kernel's
+    double* work = rt_->scratch(static_cast<std::size_t>(ozaki_tile_count(p)) * 128 * 128);
+    p.work = work;
+    const int l = launch_ozaki_gemm(p, s);
+    if (l < 0) fail(ErrorCode::InvalidArgument, "executor: emulated GEMM launch failed");
+    launched += l;
+    rt_->release(work);
+    if (stats_) {
+        const std::uint64_t tile = 128ull * 128ull * static_cast<std::uint64_t>(p.kpad);
+        const std::uint64_t products = static_cast<std::uint64_t>(kOzSlices * (kOzSlices + 1) / 2);
+        stats_->int8_ops += 2 * static_cast<std::uint64_t>(ozaki_tile_count(p)) * tile * products;
+        const std::uint64_t full = static_cast<std::uint64_t>(g.rows) * static_cast<std::uint64_t>(g.cols) *
+                                   static_cast<std::uint64_t>(g.n);
+        const std::uint64_t tm = static_cast<std::uint64_t>((g.rows + 127) / 128);
+        stats_->emulated_macs += sym ? full / (tm * tm) * (tm * (tm + 1) / 2) : full;  // as gemm_macs counts it
     }
     rt_->release(reinterpret_cast<double*>(da));
     rt_->release(reinterpret_cast<double*>(ea));
