@@ -96,6 +96,36 @@ struct OzSmem {
 // (slices 0..3), each into <= 4 int32 accumulators of 128 columns. Between
 // the passes the epilogue warps drain pass 0 into the output tile (FP64,
 // before the row/column exponents); pass 1 adds to it.
+// Tile order: square groups of OZ_GROUP x OZ_GROUP tiles (upper groups only
+// when symmetric), column-major inside a group, so one wave of CTAs streams
+// about OZ_GROUP A panels and OZ_GROUP B panels (~130 MB of digits at
+// K = 8192) that stay L2-resident across the wave.
+constexpr long long OZ_GROUP = 12;
+__device__ __forceinline__ void oz_tile_of(const OzakiArgs& p, long long bid, long long* tm, long long* tn) {
+    const long long T_m = p.mpad / OZ_BM, T_n = p.npad / OZ_BN;
+    const long long gm = (T_m + OZ_GROUP - 1) / OZ_GROUP, gn = (T_n + OZ_GROUP - 1) / OZ_GROUP;
+    for (long long J = 0; J < gn; ++J)
+        for (long long I = 0; I < gm; ++I) {
+            if (p.symmetric && I > J) break;
+            const long long m0 = I * OZ_GROUP, m1 = (m0 + OZ_GROUP < T_m) ? m0 + OZ_GROUP : T_m;
+            const long long n0 = J * OZ_GROUP, n1 = (n0 + OZ_GROUP < T_n) ? n0 + OZ_GROUP : T_n;
+            long long count = 0;
+            for (long long c = n0; c < n1; ++c) {
+                const long long top = (p.symmetric && I == J) ? ((c + 1 < m1) ? c + 1 : m1) : m1;  // rows m0..top-1
+                const long long h = top > m0 ? top - m0 : 0;
+                if (bid < count + h) {
+                    *tm = m0 + (bid - count);
+                    *tn = c;
+                    return;
+                }
+                count += h;
+            }
+            bid -= count;
+        }
+    *tm = 0;
+    *tn = 0;
+}
+
 template <int S, int D0, int D1>
 __device__ __forceinline__ void oz_issue_stage(unsigned tmem, const unsigned long long* da, const unsigned long long* db,
                                                unsigned idesc, bool first) {
@@ -121,20 +151,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
     OzSmem& sm = *reinterpret_cast<OzSmem*>((reinterpret_cast<unsigned long long>(oz_raw) + 1023) & ~1023ull);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr int split = S > 4 ? 4 : S;  // diagonals of pass 1: [0, split); pass 0: [split, S)
-    const long long tiles_n = p.npad / OZ_BN;
     long long tm, tn;
-    if (p.symmetric) {  // upper tiles, column by column
-        long long t = blockIdx.x, col = 0;
-        while (t > col) {
-            t -= col + 1;
-            ++col;
-        }
-        tm = t;
-        tn = col;
-    } else {
-        tm = blockIdx.x / tiles_n;
-        tn = blockIdx.x % tiles_n;
-    }
+    oz_tile_of(p, p.tile_begin + blockIdx.x, &tm, &tn);
     const long long ksteps = p.kpad / OZ_SK;
     const long long tile_bytes = OZ_BM * OZ_BK;  // one 128-row x 64-byte tile of the global layout
     const int8_t* abase = p.a + tm * (p.kpad / OZ_BK) * tile_bytes;
@@ -365,7 +383,8 @@ void launch_oz(const OzakiArgs& p, long long tiles, cudaStream_t s) {
 
 int launch_ozaki_gemm(const OzakiArgs& p, cudaStream_t s) {
     if (p.kpad % OZ_BK != 0) return -1;
-    const long long tiles = ozaki_tile_count(p);
+    const long long total = ozaki_tile_count(p);
+    const long long tiles = p.tile_count < 0 ? total - p.tile_begin : p.tile_count;
     if (tiles <= 0) return 0;
     switch (p.slices) {
         case 4: launch_oz<4>(p, tiles, s); break;

@@ -184,6 +184,8 @@ struct OzakiArgs {
     int slices = 7;
     int symmetric = 0;           // B = A: upper tiles only, mirrored epilogues
     int accumulate = 0;          // epilogue outputs += (pre-zeroed)
+    long long tile_begin = 0;    // row sharding: this launch covers tiles [tile_begin, tile_begin + tile_count)
+    long long tile_count = -1;   // -1: to the end of the tile list
     double* work = nullptr;      // 128 x 128 doubles per tile: the high-diagonal partial between the passes
     EpiSet epis;                 // fused consumers of the product tile (a plain store is one of them)
 };

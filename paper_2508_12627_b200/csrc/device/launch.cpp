@@ -216,7 +216,7 @@ constexpr long long kOzMaxK = 19000;    // 7 products of K * 127^2 per diagonal 
 constexpr long long kOzMinDim = 1024;   // below, DMMA is as fast and needs no digit pass
 
 bool Program::emulated_eligible(const GemmArgs& g) const {
-    if (!config_.device.fp64_emulation || slice_world_ > 1 || g.tile_count >= 0) return false;
+    if (!config_.device.fp64_emulation) return false;
     if (g.n > kOzMaxK || g.rows < kOzMinDim || g.cols < kOzMinDim) return false;
     if (g.a.nf != 1 || g.b.nf != 1 || g.a.nr != 1 || g.b.nr != 1) return false;
     return true;
@@ -254,7 +254,12 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
     p.symmetric = sym ? 1 : 0;
     p.accumulate = g.accumulate;
     p.epis = set;  // the same fused consumers (and partial slots) as the DMMA kernel's
-    double* work = rt_->scratch(static_cast<std::size_t>(ozaki_tile_count(p)) * 128 * 128);
+    if (g.tile_count >= 0) {  // row sharding: this rank's range of the (same) tile list
+        p.tile_begin = g.tile_begin;
+        p.tile_count = g.tile_count;
+    }
+    const long long tiles = p.tile_count >= 0 ? p.tile_count : ozaki_tile_count(p);
+    double* work = rt_->scratch(static_cast<std::size_t>(tiles) * 128 * 128);
     p.work = work;
     const int l = launch_ozaki_gemm(p, s);
     if (l < 0) fail(ErrorCode::InvalidArgument, "executor: emulated GEMM launch failed");
@@ -263,7 +268,7 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
     if (stats_) {
         const std::uint64_t tile = 128ull * 128ull * static_cast<std::uint64_t>(p.kpad);
         const std::uint64_t products = static_cast<std::uint64_t>(kOzSlices * (kOzSlices + 1) / 2);
-        stats_->int8_ops += 2 * static_cast<std::uint64_t>(ozaki_tile_count(p)) * tile * products;
+        stats_->int8_ops += 2 * static_cast<std::uint64_t>(tiles) * tile * products;
         const std::uint64_t full = static_cast<std::uint64_t>(g.rows) * static_cast<std::uint64_t>(g.cols) *
                                    static_cast<std::uint64_t>(g.n);
         const std::uint64_t tm = static_cast<std::uint64_t>((g.rows + 127) / 128);

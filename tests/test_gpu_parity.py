@@ -358,3 +358,19 @@ def test_data_path_repeatable_at_scale(engine, name, n):
     ref = engine.u_terms(factors, sig, m)
     scale = np.max(np.abs(ref.v))
     assert abs(vals[0] - ref.value) <= TOL * scale, (vals[0], ref.value)
+
+
+@pytest.mark.parametrize("name,n,world", [("C2", 1536, 3), ("C3", 1280, 2)])
+def test_emulated_gemm_row_sharding(engine, name, n, world):
+    # the INT8-emulated GEMM (n >= 1024) over virtual ranks' tile ranges == unsharded;
+    # both within the north-star tolerance of the DMMA path
+    from paper_2508_12627_b200.workloads import generate
+    factors, sig, m, _ = generate(name, n)
+    base = engine.u_terms(factors, sig, m)
+    assert base.stats["int8_tensor_ops"] > 0
+    sharded = engine.u_terms(factors, sig, m, engine.Config(shard_rows=True, emulate_world=world))
+    exact = engine.u_terms(factors, sig, m, engine.Config(fp64_emulation=False))
+    assert exact.stats["int8_tensor_ops"] == 0
+    scale = np.max(np.abs(exact.v))
+    assert np.max(np.abs(sharded.v - base.v)) <= 1e-12 * scale
+    assert np.max(np.abs(base.v - exact.v)) <= TOL * scale
