@@ -313,35 +313,63 @@ __global__ void oz_row_exponents(const double* __restrict__ x, long long rows, l
     }
 }
 
-// Digits into the tiled core-matrix layout: thread = (row, 16-byte K chunk).
-__global__ void oz_split(const double* __restrict__ x, long long rows, long long k, long long rs, long long ks,
-                         const int* __restrict__ exps, int th, long long rows_pad, long long kpad, int slices,
-                         long long slice_bytes, int8_t* __restrict__ out) {
-    const long long chunks = kpad / 16;
-    const long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    if (g >= rows_pad * chunks) return;
-    const long long r = g % rows_pad, ch = g / rows_pad;  // consecutive threads: consecutive rows
-    const long long kt = ch / (OZ_BK / 16), cin = ch % (OZ_BK / 16);
-    const long long rt = r / th, rin = r % th;
-    const long long off = (rt * (kpad / OZ_BK) + kt) * (th * OZ_BK) + cin * (th * 16) + rin * 16;
-    double v[16];
-    const int e = r < rows ? exps[r] : 0;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        const long long c = ch * 16 + j;
-        v[j] = (r < rows && c < k) ? ldexp(x[r * rs + c * ks], -e) : 0.0;
+// Digits into the tiled core-matrix layout, one (th x 64) tile per block:
+// the FP64 tile is staged in shared memory with coalesced row reads, each
+// thread turns one (row, 16-element chunk) into S 16-byte digit words, and
+// every slice tile (th x 64 bytes, contiguous) is written coalesced.
+// |x| 2^-e < 1, so m = trunc(|x| 2^{7S-e}) < 2^{7S} holds the first S base-128
+// digits of |x| 2^-e exactly (the digits the exact FP64 peeling
+// x -> 128 x - trunc(128 x) yields); the sign is applied to every digit.
+constexpr int OZ_SPLIT_THREADS = 256;
+__global__ void __launch_bounds__(OZ_SPLIT_THREADS) oz_split(const double* __restrict__ x, long long rows, long long k,
+                                                            long long rs, long long ks, const int* __restrict__ exps,
+                                                            int th, long long kpad, int slices, long long slice_bytes,
+                                                            int8_t* __restrict__ out) {
+    extern __shared__ double tilebuf[];  // th x (OZ_BK + 1) doubles
+    const long long kt_count = kpad / OZ_BK;
+    const long long rt = blockIdx.x / kt_count, kt = blockIdx.x % kt_count;
+    const long long r0 = rt * th, k0 = kt * OZ_BK;
+    const int tid = threadIdx.x;
+    constexpr int P = OZ_BK + 1;
+    if (ks == 1) {  // k-contiguous rows: lanes along k
+        for (int i = tid; i < th * OZ_BK; i += OZ_SPLIT_THREADS) {
+            const int rr = i / OZ_BK, cc = i % OZ_BK;
+            const long long R = r0 + rr, C = k0 + cc;
+            tilebuf[rr * P + cc] = (R < rows && C < k) ? x[R * rs + C] : 0.0;
+        }
+    } else {  // row-contiguous (m-major) operand: lanes along rows
+        for (int i = tid; i < th * OZ_BK; i += OZ_SPLIT_THREADS) {
+            const int cc = i / th, rr = i % th;
+            const long long R = r0 + rr, C = k0 + cc;
+            tilebuf[rr * P + cc] = (R < rows && C < k) ? x[R * rs + C * ks] : 0.0;
+        }
     }
-    for (int t = 0; t < slices; ++t) {
-        unsigned w[4] = {0, 0, 0, 0};
+    __syncthreads();
+    const long long tile_off = (rt * kt_count + kt) * (static_cast<long long>(th) * OZ_BK);
+    for (int item = tid; item < th * (OZ_BK / 16); item += OZ_SPLIT_THREADS) {
+        const int rr = item % th, cin = item / th;  // consecutive threads: consecutive rows of one chunk
+        const long long R = r0 + rr;
+        const int e = R < rows ? exps[R] : 0;
+        unsigned long long mag[16];
+        bool neg[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-            const double y = v[j] * 128.0;       // exact (power of two)
-            const double dgt = trunc(y);         // in [-127, 127]
-            v[j] = y - dgt;                      // exact
-            const unsigned byte = static_cast<unsigned>(static_cast<int>(dgt)) & 0xFFu;
-            w[j >> 2] |= byte << ((j & 3) * 8);
+            const double xv = tilebuf[rr * P + cin * 16 + j];
+            neg[j] = xv < 0.0;
+            mag[j] = static_cast<unsigned long long>(ldexp(fabs(xv), 7 * slices - e));
         }
-        *reinterpret_cast<uint4*>(out + t * slice_bytes + off) = make_uint4(w[0], w[1], w[2], w[3]);
+        const long long off = tile_off + cin * (th * 16) + rr * 16;
+        for (int t = 0; t < slices; ++t) {
+            const int shift = 7 * (slices - 1 - t);
+            unsigned w[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int dg = static_cast<int>((mag[j] >> shift) & 127u);
+                const unsigned byte = static_cast<unsigned>(neg[j] ? -dg : dg) & 0xFFu;
+                w[j >> 2] |= byte << ((j & 3) * 8);
+            }
+            *reinterpret_cast<uint4*>(out + t * slice_bytes + off) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
     }
 }
 
@@ -359,9 +387,14 @@ int ozaki_split(const double* x, long long rows, long long k, long long rs, long
     const long long rp = (rows + tile_rows - 1) / tile_rows * tile_rows;
     const long long kp = (k + OZ_BK - 1) / OZ_BK * OZ_BK;
     oz_row_exponents<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(x, rows, k, rs, ks, exps);
-    const long long threads = rp * (kp / 16);
-    oz_split<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(x, rows, k, rs, ks, exps, tile_rows, rp, kp,
-                                                                        slices, rp * kp, out);
+    const int smem = tile_rows * (OZ_BK + 1) * static_cast<int>(sizeof(double));
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(oz_split, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        configured = true;
+    }
+    oz_split<<<static_cast<unsigned>((rp / tile_rows) * (kp / OZ_BK)), OZ_SPLIT_THREADS, smem, s>>>(
+        x, rows, k, rs, ks, exps, tile_rows, kp, slices, rp * kp, out);
     return 2;
 }
 
