@@ -605,9 +605,7 @@ int us_dgemm(int32_t method, int32_t slices, int32_t symmetric, int64_t m, int64
             p.epis.d[0].mode = kEpiStore;
             p.epis.d[0].out = dc->ptr;
             double* work = nullptr;
-            check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&work),
-                                       static_cast<std::size_t>(ozaki_tile_count(p)) * 128 * 128 * sizeof(double), s),
-                       "alloc");
+            check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&work), ozaki_work_entries() * sizeof(double), s), "alloc");
             p.work = work;
             launch_ozaki_gemm(p, s);
             cudaFreeAsync(work, s);

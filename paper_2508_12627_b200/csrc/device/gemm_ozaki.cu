@@ -248,7 +248,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
     } else if (warp < 4) {  // epilogue warps: thread = one row of the tile (TMEM lane)
         const long long row = tm * OZ_BM + warp * 32 + lane;
         const bool row_ok = row < p.m;
-        double* work = p.work + static_cast<long long>(blockIdx.x) * (OZ_BM * OZ_BN) + (warp * 32 + lane) * OZ_BN;
+        // one CTA per SM at a time (shared memory and TMEM say so): the scratch
+        // of the high-diagonal partial is per SM, L2-resident
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        double* work = p.work + static_cast<long long>(smid) * (OZ_BM * OZ_BN) + (warp * 32 + lane) * OZ_BN;
         for (int pass = 0; pass < 2; ++pass) {
             if (pass == 0 && split >= S) continue;
             const int d0 = pass == 0 ? split : 0, d1 = pass == 0 ? S : split;
@@ -396,6 +400,18 @@ int ozaki_split(const double* x, long long rows, long long k, long long rs, long
     oz_split<<<static_cast<unsigned>((rp / tile_rows) * (kp / OZ_BK)), OZ_SPLIT_THREADS, smem, s>>>(
         x, rows, k, rs, ks, exps, tile_rows, kp, slices, rp * kp, out);
     return 2;
+}
+
+std::size_t ozaki_work_entries() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        sms = v > 0 ? v : 148;
+    }
+    return static_cast<std::size_t>(sms + 8) * OZ_BM * OZ_BN;  // %smid < SM count (slack for safety)
 }
 
 long long ozaki_tile_count(const OzakiArgs& p) {

@@ -186,13 +186,14 @@ struct OzakiArgs {
     int accumulate = 0;          // epilogue outputs += (pre-zeroed)
     long long tile_begin = 0;    // row sharding: this launch covers tiles [tile_begin, tile_begin + tile_count)
     long long tile_count = -1;   // -1: to the end of the tile list
-    double* work = nullptr;      // 128 x 128 doubles per tile: the high-diagonal partial between the passes
+    double* work = nullptr;      // 128 x 128 doubles per SM (ozaki_work_entries): the high-diagonal partial
     EpiSet epis;                 // fused consumers of the product tile (a plain store is one of them)
 };
 std::size_t ozaki_slice_bytes(long long rows, long long k, int tile_rows);
 int ozaki_split(const double* x, long long rows, long long k, long long rs, long long ks, int tile_rows, int slices,
                 int8_t* out, int* exps, cudaStream_t s);
 long long ozaki_tile_count(const OzakiArgs& p);
+std::size_t ozaki_work_entries();  // doubles of OzakiArgs::work
 // Launches the emulated GEMM with its fused epilogues and their finalizers.
 int launch_ozaki_gemm(const OzakiArgs& p, cudaStream_t s);
 

@@ -214,12 +214,22 @@ void Program::run_stream(const Op& op, double* out) {
 constexpr int kOzSlices = 7;
 constexpr long long kOzMaxK = 19000;    // 7 products of K * 127^2 per diagonal < 2^31
 constexpr long long kOzMinDim = 1024;   // below, DMMA is as fast and needs no digit pass
+constexpr long long kOzMinK = 2048;     // shorter K: per-tile drains and digit passes outweigh the MMA savings
+                                        // (C4's Khatri-Rao GEMMs, K = 1024, measured 1.5x slower emulated)
+
+// A single-factor operand whose row digits flatten to one stride (a
+// materialized Khatri-Rao operand of n^2 rows is one): its row stride, or -1.
+long long flat_row_stride(const GemmSide& s, long long n) {
+    if (s.nf != 1) return -1;
+    for (int d = s.nr - 1; d > 0; --d)
+        if (s.rstride[0][d - 1] != s.rstride[0][d] * n) return -1;
+    return s.rstride[0][s.nr - 1];
+}
 
 bool Program::emulated_eligible(const GemmArgs& g) const {
     if (!config_.device.fp64_emulation) return false;
-    if (g.n > kOzMaxK || g.rows < kOzMinDim || g.cols < kOzMinDim) return false;
-    if (g.a.nf != 1 || g.b.nf != 1 || g.a.nr != 1 || g.b.nr != 1) return false;
-    return true;
+    if (g.n > kOzMaxK || g.n < kOzMinK || g.rows < kOzMinDim || g.cols < kOzMinDim) return false;
+    return flat_row_stride(g.a, n_) >= 0 && flat_row_stride(g.b, n_) >= 0;
 }
 
 // Digits of both operands, the product (straight into a plain store's output,
@@ -228,15 +238,14 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
     cudaStream_t s = rt_->stream();
     const std::size_t abytes = ozaki_slice_bytes(g.rows, g.n, 128), bbytes = ozaki_slice_bytes(g.cols, g.n, 128);
     // one set of digits when both operands are the same matrix view (A A^T)
-    const bool same = g.a.ptr[0] == g.b.ptr[0] && g.rows == g.cols && g.a.rstride[0][0] == g.b.rstride[0][0] &&
-                      g.a.kstride[0] == g.b.kstride[0];
+    const long long ars = flat_row_stride(g.a, n_), brs = flat_row_stride(g.b, n_);
+    const bool same = g.a.ptr[0] == g.b.ptr[0] && g.rows == g.cols && ars == brs && g.a.kstride[0] == g.b.kstride[0];
     int8_t* da = reinterpret_cast<int8_t*>(rt_->scratch((abytes * kOzSlices + 7) / 8));
     int* ea = reinterpret_cast<int*>(rt_->scratch(static_cast<std::size_t>(g.rows + 1) / 2 + 1));
     int8_t* db = same ? da : reinterpret_cast<int8_t*>(rt_->scratch((bbytes * kOzSlices + 7) / 8));
     int* eb = same ? ea : reinterpret_cast<int*>(rt_->scratch(static_cast<std::size_t>(g.cols + 1) / 2 + 1));
-    int launched = ozaki_split(g.a.ptr[0], g.rows, g.n, g.a.rstride[0][0], g.a.kstride[0], 128, kOzSlices, da, ea, s);
-    if (!same)
-        launched += ozaki_split(g.b.ptr[0], g.cols, g.n, g.b.rstride[0][0], g.b.kstride[0], 128, kOzSlices, db, eb, s);
+    int launched = ozaki_split(g.a.ptr[0], g.rows, g.n, ars, g.a.kstride[0], 128, kOzSlices, da, ea, s);
+    if (!same) launched += ozaki_split(g.b.ptr[0], g.cols, g.n, brs, g.b.kstride[0], 128, kOzSlices, db, eb, s);
     const bool sym = g.symmetric_out && g.rows == g.cols;
     OzakiArgs p;
     p.a = da;
@@ -259,7 +268,7 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
         p.tile_count = g.tile_count;
     }
     const long long tiles = p.tile_count >= 0 ? p.tile_count : ozaki_tile_count(p);
-    double* work = rt_->scratch(static_cast<std::size_t>(tiles) * 128 * 128);
+    double* work = rt_->scratch(ozaki_work_entries());
     p.work = work;
     const int l = launch_ozaki_gemm(p, s);
     if (l < 0) fail(ErrorCode::InvalidArgument, "executor: emulated GEMM launch failed");
@@ -489,6 +498,15 @@ void Program::run_gemm(const Op& op, double* out) {
         }
         rt_->end(Runtime::kGemm);
         if (launched < 0) fail(ErrorCode::InvalidArgument, "executor: fused GEMM lost TMA eligibility");
+    } else if (emulated_eligible(g)) {  // a plain product (e.g. a Khatri-Rao GEMM) on the INT8 tensor cores
+        EpiSet set;
+        set.count = 1;
+        set.d[0].mode = kEpiStore;
+        set.d[0].out = out;
+        g.symmetric_out = 0;
+        rt_->begin(Runtime::kGemm);
+        launched = run_emulated(g, set);
+        rt_->end(Runtime::kGemm);
     } else {
         g.symmetric_out = 0;
         rt_->begin(Runtime::kGemm);
