@@ -407,7 +407,10 @@ void Program::run_gemm(const Op& op, double* out) {
         const bool chunked = slice_world_ == 1 && op.symmetric_out && g.rows == g.cols && fa[0].buf == fb[0].buf &&
                              src && src->ready.size() > 1;
         rt_->begin(Runtime::kGemm);
-        if (!chunked && emulated_eligible(g)) {
+        if (emulated_eligible(g)) {
+            // the emulated GEMM digitizes whole operands: an input still arriving
+            // in panels is waited for (its upload then overlaps only the split)
+            if (chunked) check_cuda(cudaStreamWaitEvent(rt_->stream(), src->ready.back().second, 0), "wait upload");
             launched = run_emulated(g, set);
         } else if (!chunked) {
             launched = launch_gemm_multi(g, set, rt_->stream());
