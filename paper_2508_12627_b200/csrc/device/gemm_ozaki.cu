@@ -30,10 +30,10 @@ namespace {
 
 constexpr int OZ_BM = 128, OZ_BN = 128;   // output tile
 constexpr int OZ_BK = 64;                  // K bytes per tile of the global digit layout
-constexpr int OZ_SK = 32;                  // K bytes per pipeline stage (one MMA k-step)
-constexpr int OZ_STAGES = 4;
+constexpr int OZ_SK = 64;                  // K bytes per pipeline stage (two MMA k-steps)
+constexpr int OZ_STAGES = 2;
 constexpr int OZ_THREADS = 192;            // warps 0-3 epilogue, 4 producer, 5 MMA issuer
-constexpr int OZ_TILE_STAGE = OZ_BM * OZ_SK;  // 4 KiB per operand slice per stage
+constexpr int OZ_TILE_STAGE = OZ_BM * OZ_SK;  // 8 KiB per operand slice per stage
 
 __device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 
@@ -127,9 +127,19 @@ __device__ __forceinline__ void oz_tile_of(const OzakiArgs& p, long long bid, lo
 }
 
 template <int S, int D0, int D1>
-__device__ __forceinline__ void oz_issue_stage(unsigned tmem, const unsigned long long* da, const unsigned long long* db,
-                                               unsigned idesc, bool first) {
-    // diagonals [D0, D1) of the digit products, accumulators at (d - D0) * 128 columns
+__device__ __forceinline__ void oz_issue_stage(unsigned tmem, const unsigned long long* da0, const unsigned long long* db0,
+                                               unsigned idesc, bool first0) {
+    // diagonals [D0, D1) of the digit products, accumulators at (d - D0) * 128 columns;
+    // two 32-byte k-steps per stage: the second starts two 16-byte chunks (2 x 2048 B) further
+#pragma unroll
+    for (int ks = 0; ks < OZ_SK / 32; ++ks) {
+    unsigned long long da[S], db[S];
+#pragma unroll
+    for (int t = 0; t < S; ++t) {
+        da[t] = da0[t] + static_cast<unsigned long long>(ks * 2 * OZ_BM * 16 >> 4);
+        db[t] = db0[t] + static_cast<unsigned long long>(ks * 2 * OZ_BN * 16 >> 4);
+    }
+    const bool first = first0 && ks == 0;
 #pragma unroll
     for (int d = D0; d < D1; ++d)
 #pragma unroll
@@ -143,6 +153,7 @@ __device__ __forceinline__ void oz_issue_stage(unsigned tmem, const unsigned lon
                 "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(acc),
                 "l"(da[t]), "l"(db[u]), "r"(idesc), "r"(accumulate));
         }
+    }
 }
 
 template <int S>
@@ -188,8 +199,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
                 const int s = static_cast<int>(it % OZ_STAGES);
                 if (it >= OZ_STAGES) bar_wait(&sm.empty[s], static_cast<unsigned>(((it / OZ_STAGES) - 1) & 1));
                 bar_expect(&sm.full[s], static_cast<unsigned>(2 * ns * OZ_TILE_STAGE));
-                // stage k = half (k % 2) of global k-tile k / 2: its two 16-byte chunks are contiguous
-                const long long off = (k >> 1) * tile_bytes + (k & 1) * OZ_TILE_STAGE;
+                // stage k = global k-tile k (four 16-byte chunks, contiguous)
+                const long long off = k * tile_bytes;
                 for (int t = 0; t < ns; ++t) {
                     bulk_load(sm.u.st.a[s][t], abase + t * p.a_slice + off, OZ_TILE_STAGE, &sm.full[s]);
                     bulk_load(sm.u.st.b[s][t], bbase + t * p.b_slice + off, OZ_TILE_STAGE, &sm.full[s]);
@@ -214,13 +225,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
                 const int s = static_cast<int>(it % OZ_STAGES);
                 bar_wait(&sm.full[s], static_cast<unsigned>((it / OZ_STAGES) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                switch (s) {
-#pragma unroll
-                    case 0: oz_issue_stage<S, split, S>(tmem, da[0], db[0], idesc, k == 0); break;
-                    case 1: oz_issue_stage<S, split, S>(tmem, da[1], db[1], idesc, k == 0); break;
-                    case 2: oz_issue_stage<S, split, S>(tmem, da[2], db[2], idesc, k == 0); break;
-                    default: oz_issue_stage<S, split, S>(tmem, da[3], db[3], idesc, k == 0); break;
-                }
+                if (s == 0) oz_issue_stage<S, split, S>(tmem, da[0], db[0], idesc, k == 0);
+                else oz_issue_stage<S, split, S>(tmem, da[1], db[1], idesc, k == 0);
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                     su32(&sm.empty[s])));
             }
@@ -234,12 +240,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
             const int s = static_cast<int>(it % OZ_STAGES);
             bar_wait(&sm.full[s], static_cast<unsigned>((it / OZ_STAGES) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
-            switch (s) {
-                case 0: oz_issue_stage<S, 0, split>(tmem, da[0], db[0], idesc, k == 0); break;
-                case 1: oz_issue_stage<S, 0, split>(tmem, da[1], db[1], idesc, k == 0); break;
-                case 2: oz_issue_stage<S, 0, split>(tmem, da[2], db[2], idesc, k == 0); break;
-                default: oz_issue_stage<S, 0, split>(tmem, da[3], db[3], idesc, k == 0); break;
-            }
+            if (s == 0) oz_issue_stage<S, 0, split>(tmem, da[0], db[0], idesc, k == 0);
+            else oz_issue_stage<S, 0, split>(tmem, da[1], db[1], idesc, k == 0);
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                 su32(&sm.empty[s])));
         }
