@@ -205,6 +205,20 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
                     bulk_load(sm.u.st.a[s][t], abase + t * p.a_slice + off, OZ_TILE_STAGE, &sm.full[s]);
                     bulk_load(sm.u.st.b[s][t], bbase + t * p.b_slice + off, OZ_TILE_STAGE, &sm.full[s]);
                 }
+                // warm L2 a few k-tiles ahead: the ring is only two stages deep
+                if (p.prefetch > 0 && k + p.prefetch < ksteps) {
+                    const long long poff = off + p.prefetch * tile_bytes;
+                    for (int t = 0; t < ns; ++t) {
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                         reinterpret_cast<unsigned long long>(abase + t * p.a_slice + poff)),
+                                     "r"(static_cast<unsigned>(OZ_TILE_STAGE))
+                                     : "memory");
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                         reinterpret_cast<unsigned long long>(bbase + t * p.b_slice + poff)),
+                                     "r"(static_cast<unsigned>(OZ_TILE_STAGE))
+                                     : "memory");
+                    }
+                }
             }
         }
     } else if (tid == 160) {  // MMA issuer: descriptors precomputed per stage, products unrolled
@@ -432,8 +446,12 @@ void launch_oz(const OzakiArgs& p, long long tiles, cudaStream_t s) {
     ozaki_gemm_kernel<S><<<static_cast<unsigned>(tiles), OZ_THREADS, bytes, s>>>(p);
 }
 
-int launch_ozaki_gemm(const OzakiArgs& p, cudaStream_t s) {
-    if (p.kpad % OZ_BK != 0) return -1;
+int launch_ozaki_gemm(const OzakiArgs& in, cudaStream_t s) {
+    if (in.kpad % OZ_BK != 0) return -1;
+    OzakiArgs p = in;
+    // warming L2 two k-tiles ahead pays while a wave's digit panels fit L2
+    // (C2, K = 8192: +2%); at K = 16384 it evicts them (C3: -9%)
+    p.prefetch = p.kpad <= 8192 ? 2 : 0;
     const long long total = ozaki_tile_count(p);
     const long long tiles = p.tile_count < 0 ? total - p.tile_begin : p.tile_count;
     if (tiles <= 0) return 0;

@@ -186,6 +186,7 @@ struct OzakiArgs {
     int accumulate = 0;          // epilogue outputs += (pre-zeroed)
     long long tile_begin = 0;    // row sharding: this launch covers tiles [tile_begin, tile_begin + tile_count)
     long long tile_count = -1;   // -1: to the end of the tile list
+    int prefetch = 0;            // k-tiles ahead the producer warms L2 (set by launch_ozaki_gemm)
     double* work = nullptr;      // 128 x 128 doubles per SM (ozaki_work_entries): the high-diagonal partial
     EpiSet epis;                 // fused consumers of the product tile (a plain store is one of them)
 };
