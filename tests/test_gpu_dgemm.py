@@ -1,0 +1,46 @@
+"""The two FP64 GEMM engines behind the executor (us_dgemm): DMMA (mma.sync
+f64) and Ozaki splitting on the INT8 tcgen05 tensor cores, against numpy."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 128, 64), (300, 200, 257), (1000, 130, 2049), (129, 1100, 640)])
+def test_ozaki_matches_numpy(engine, m, n, k):
+    rng = np.random.default_rng(m + n + k)
+    a, b = rng.normal(size=(m, k)), rng.normal(size=(n, k))
+    ref = a @ b.T
+    got = engine.dgemm(a, b, "ozaki", 7)
+    # 7 digits of 7 bits: ~2^-49 K max|a| max|b| per entry
+    assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
+    dm = engine.dgemm(a, b, "dmma")
+    assert np.max(np.abs(dm - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+def test_ozaki_symmetric_is_bitwise_symmetric(engine):
+    rng = np.random.default_rng(1)
+    a = rng.normal(size=(700, 333))
+    c = engine.dgemm(a, a, "ozaki", 7, symmetric=True)
+    assert np.array_equal(c, c.T)
+    assert np.max(np.abs(c - a @ a.T)) <= 1e-12 * np.max(np.abs(a @ a.T))
+
+
+def test_ozaki_precision_grows_with_digits(engine):
+    rng = np.random.default_rng(2)
+    a, b = rng.uniform(0, 1, size=(256, 512)), rng.uniform(0, 1, size=(256, 512))
+    ref = a @ b.T
+    errs = [np.max(np.abs(engine.dgemm(a, b, "ozaki", s) - ref)) / np.max(ref) for s in (4, 5, 6, 7)]
+    assert all(e2 < e1 for e1, e2 in zip(errs, errs[1:]))
+    assert errs[-1] < 1e-12
+
+
+def test_ozaki_wide_dynamic_range_rows(engine):
+    # row scaling: rows of very different magnitudes keep their relative accuracy
+    rng = np.random.default_rng(3)
+    a = rng.normal(size=(256, 256)) * np.logspace(-150, 150, 256)[:, None]
+    b = rng.normal(size=(256, 256))
+    ref = a @ b.T
+    got = engine.dgemm(a, b, "ozaki", 7)
+    row_scale = np.max(np.abs(a), axis=1)[:, None] * np.max(np.abs(b)) * 256
+    assert np.all(np.abs(got - ref) <= 1e-12 * row_scale)
