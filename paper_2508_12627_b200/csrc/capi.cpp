@@ -622,18 +622,17 @@ int us_dgemm(int32_t method, int32_t slices, int32_t symmetric, int64_t m, int64
             g.n = k;
             g.rows = m;
             g.cols = n;
+            g.a_kmajor = g.b_kmajor = 1;
             g.symmetric_out = symmetric ? 1 : 0;
             EpiSet e;
             e.count = 1;
             e.d[0].mode = kEpiStore;
             e.d[0].out = dc->ptr;
             cudaEventRecord(e0, s);
-            if (launch_gemm_multi(g, e, s) < 0) {
-                g.symmetric_out = 0;
-                g.mode = kEpiStore;
-                g.out = dc->ptr;
-                launch_gemm(g, s);
-            }
+            // the TMA-fed DMMA kernel (the executor's gather fallback assumes every
+            // extent equals n, as in a U-statistic; it is not exposed here)
+            if (launch_gemm_multi(g, e, s) < 0)
+                ustats::fail(ustats::ErrorCode::InvalidArgument, "dmma test GEMM needs an even k (16-byte aligned rows)");
             cudaEventRecord(e1, s);
         }
         check_cuda(cudaGetLastError(), "dgemm launch");
