@@ -240,10 +240,27 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
     // one set of digits when both operands are the same matrix view (A A^T)
     const long long ars = flat_row_stride(g.a, n_), brs = flat_row_stride(g.b, n_);
     const bool same = g.a.ptr[0] == g.b.ptr[0] && g.rows == g.cols && ars == brs && g.a.kstride[0] == g.b.kstride[0];
-    int8_t* da = reinterpret_cast<int8_t*>(rt_->scratch((abytes * kOzSlices + 7) / 8));
-    int* ea = reinterpret_cast<int*>(rt_->scratch(static_cast<std::size_t>(g.rows + 1) / 2 + 1));
-    int8_t* db = same ? da : reinterpret_cast<int8_t*>(rt_->scratch((bbytes * kOzSlices + 7) / 8));
-    int* eb = same ? ea : reinterpret_cast<int*>(rt_->scratch(static_cast<std::size_t>(g.cols + 1) / 2 + 1));
+    // the digits are scratch the memory-bounded schedule did not plan for: if
+    // they do not fit now, the GEMM runs on DMMA instead (caller's fallback)
+    std::vector<void*> got;
+    auto grab = [&](std::size_t bytes) -> void* {
+        void* q = nullptr;
+        if (cudaMallocAsync(&q, bytes, s) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        got.push_back(q);
+        return q;
+    };
+    int8_t* da = static_cast<int8_t*>(grab(abytes * kOzSlices));
+    int* ea = static_cast<int*>(grab(sizeof(int) * static_cast<std::size_t>(g.rows)));
+    int8_t* db = same ? da : static_cast<int8_t*>(grab(bbytes * kOzSlices));
+    int* eb = same ? ea : static_cast<int*>(grab(sizeof(int) * static_cast<std::size_t>(g.cols)));
+    double* work = static_cast<double*>(grab(ozaki_work_entries() * sizeof(double)));
+    if (!da || !ea || !db || !eb || !work) {
+        for (void* q : got) cudaFreeAsync(q, s);
+        return -1;
+    }
     int launched = ozaki_split(g.a.ptr[0], g.rows, g.n, ars, g.a.kstride[0], 128, kOzSlices, da, ea, s);
     if (!same) launched += ozaki_split(g.b.ptr[0], g.cols, g.n, brs, g.b.kstride[0], 128, kOzSlices, db, eb, s);
     const bool sym = g.symmetric_out && g.rows == g.cols;
@@ -268,12 +285,10 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
         p.tile_count = g.tile_count;
     }
     const long long tiles = p.tile_count >= 0 ? p.tile_count : ozaki_tile_count(p);
-    double* work = rt_->scratch(ozaki_work_entries());
     p.work = work;
     const int l = launch_ozaki_gemm(p, s);
     if (l < 0) fail(ErrorCode::InvalidArgument, "executor: emulated GEMM launch failed");
     launched += l;
-    rt_->release(work);
     if (stats_) {
         const std::uint64_t tile = 128ull * 128ull * static_cast<std::uint64_t>(p.kpad);
         const std::uint64_t products = static_cast<std::uint64_t>(kOzSlices * (kOzSlices + 1) / 2);
@@ -283,12 +298,7 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
         const std::uint64_t tm = static_cast<std::uint64_t>((g.rows + 127) / 128);
         stats_->emulated_macs += sym ? full / (tm * tm) * (tm * (tm + 1) / 2) : full;  // as gemm_macs counts it
     }
-    rt_->release(reinterpret_cast<double*>(da));
-    rt_->release(reinterpret_cast<double*>(ea));
-    if (!same) {
-        rt_->release(reinterpret_cast<double*>(db));
-        rt_->release(reinterpret_cast<double*>(eb));
-    }
+    for (void* q : got) cudaFreeAsync(q, s);
     return launched;
 }
 
@@ -412,6 +422,7 @@ void Program::run_gemm(const Op& op, double* out) {
             // in panels is waited for (its upload then overlaps only the split)
             if (chunked) check_cuda(cudaStreamWaitEvent(rt_->stream(), src->ready.back().second, 0), "wait upload");
             launched = run_emulated(g, set);
+            if (launched < 0) launched = launch_gemm_multi(g, set, rt_->stream());
         } else if (!chunked) {
             launched = launch_gemm_multi(g, set, rt_->stream());
         } else {
@@ -509,6 +520,7 @@ void Program::run_gemm(const Op& op, double* out) {
         g.symmetric_out = 0;
         rt_->begin(Runtime::kGemm);
         launched = run_emulated(g, set);
+        if (launched < 0) launched = launch_gemm(g, rt_->stream());
         rt_->end(Runtime::kGemm);
     } else {
         g.symmetric_out = 0;
