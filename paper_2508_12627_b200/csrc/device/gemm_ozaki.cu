@@ -20,6 +20,7 @@
 // each TH rows x 16 B), so each stage is a handful of 1-D bulk copies.
 #include <cstdint>
 #include <cstdio>
+#include <vector>
 
 #include "epilogue.cuh"
 #include "kernels.hpp"
@@ -101,7 +102,7 @@ struct OzSmem {
 // about OZ_GROUP A panels and OZ_GROUP B panels (~130 MB of digits at
 // K = 8192) that stay L2-resident across the wave.
 constexpr long long OZ_GROUP = 12;
-__device__ __forceinline__ void oz_tile_of(const OzakiArgs& p, long long bid, long long* tm, long long* tn) {
+__host__ __device__ __forceinline__ void oz_tile_of(const OzakiArgs& p, long long bid, long long* tm, long long* tn) {
     const long long T_m = p.mpad / OZ_BM, T_n = p.npad / OZ_BN;
     const long long gm = (T_m + OZ_GROUP - 1) / OZ_GROUP, gn = (T_n + OZ_GROUP - 1) / OZ_GROUP;
     for (long long J = 0; J < gn; ++J)
@@ -319,8 +320,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
 
 // Row exponents: e_i with max_k |x_ik| < 2^e_i (0 for an all-zero row).
 __global__ void oz_row_exponents(const double* __restrict__ x, long long rows, long long k, long long rs, long long ks,
-                                 int* __restrict__ exps) {
-    const long long r = blockIdx.x * static_cast<long long>(blockDim.x / 32) + (threadIdx.x >> 5);
+                                 int* __restrict__ exps, const int* __restrict__ panels) {
+    long long r = blockIdx.x * static_cast<long long>(blockDim.x / 32) + (threadIdx.x >> 5);
+    if (panels) r = static_cast<long long>(panels[r / OZ_BM]) * OZ_BM + r % OZ_BM;  // rows of the listed panels
     const int lane = threadIdx.x & 31;
     if (r >= rows) return;
     double mx = 0.0;
@@ -344,10 +346,11 @@ constexpr int OZ_SPLIT_THREADS = 256;
 __global__ void __launch_bounds__(OZ_SPLIT_THREADS) oz_split(const double* __restrict__ x, long long rows, long long k,
                                                             long long rs, long long ks, const int* __restrict__ exps,
                                                             int th, long long kpad, int slices, long long slice_bytes,
-                                                            int8_t* __restrict__ out) {
+                                                            int8_t* __restrict__ out, const int* __restrict__ panels) {
     extern __shared__ double tilebuf[];  // th x (OZ_BK + 1) doubles
     const long long kt_count = kpad / OZ_BK;
-    const long long rt = blockIdx.x / kt_count, kt = blockIdx.x % kt_count;
+    const long long pi = blockIdx.x / kt_count, kt = blockIdx.x % kt_count;
+    const long long rt = panels ? panels[pi] : pi;
     const long long r0 = rt * th, k0 = kt * OZ_BK;
     const int tid = threadIdx.x;
     constexpr int P = OZ_BK + 1;
@@ -402,20 +405,48 @@ std::size_t ozaki_slice_bytes(long long rows, long long k, int tile_rows) {
 }
 
 int ozaki_split(const double* x, long long rows, long long k, long long rs, long long ks, int tile_rows, int slices,
-                int8_t* out, int* exps, cudaStream_t s) {
-    if (slices < 1 || slices > kOzMaxSlices) return -1;
+                int8_t* out, int* exps, cudaStream_t s, const std::vector<int>* panels) {
+    if (slices < 1 || slices > kOzMaxSlices || tile_rows != OZ_BM) return -1;
     const long long rp = (rows + tile_rows - 1) / tile_rows * tile_rows;
     const long long kp = (k + OZ_BK - 1) / OZ_BK * OZ_BK;
-    oz_row_exponents<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(x, rows, k, rs, ks, exps);
+    int* dpanels = nullptr;
+    long long npanels = rp / tile_rows;
+    if (panels) {  // only these 128-row panels (a row-sharded rank's tiles read no others)
+        npanels = static_cast<long long>(panels->size());
+        if (npanels == 0) return 0;
+        if (cudaMallocAsync(reinterpret_cast<void**>(&dpanels), sizeof(int) * panels->size(), s) != cudaSuccess) return -1;
+        cudaMemcpyAsync(dpanels, panels->data(), sizeof(int) * panels->size(), cudaMemcpyHostToDevice, s);
+    }
+    const long long exp_rows = panels ? npanels * tile_rows : rows;
+    oz_row_exponents<<<static_cast<unsigned>((exp_rows + 7) / 8), 256, 0, s>>>(x, rows, k, rs, ks, exps, dpanels);
     const int smem = tile_rows * (OZ_BK + 1) * static_cast<int>(sizeof(double));
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(oz_split, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         configured = true;
     }
-    oz_split<<<static_cast<unsigned>((rp / tile_rows) * (kp / OZ_BK)), OZ_SPLIT_THREADS, smem, s>>>(
-        x, rows, k, rs, ks, exps, tile_rows, kp, slices, rp * kp, out);
+    oz_split<<<static_cast<unsigned>(npanels * (kp / OZ_BK)), OZ_SPLIT_THREADS, smem, s>>>(
+        x, rows, k, rs, ks, exps, tile_rows, kp, slices, rp * kp, out, dpanels);
+    if (dpanels) cudaFreeAsync(dpanels, s);
     return 2;
+}
+
+void ozaki_tile_panels(const OzakiArgs& p, std::vector<int>* a_panels, std::vector<int>* b_panels) {
+    const long long total = ozaki_tile_count(p);
+    const long long end = p.tile_count < 0 ? total : p.tile_begin + p.tile_count;
+    std::vector<char> ma(static_cast<std::size_t>(p.mpad / OZ_BM), 0), mb(static_cast<std::size_t>(p.npad / OZ_BN), 0);
+    for (long long b = p.tile_begin; b < end; ++b) {
+        long long tm = 0, tn = 0;
+        oz_tile_of(p, b, &tm, &tn);
+        ma[static_cast<std::size_t>(tm)] = 1;
+        mb[static_cast<std::size_t>(tn)] = 1;
+    }
+    a_panels->clear();
+    b_panels->clear();
+    for (std::size_t i = 0; i < ma.size(); ++i)
+        if (ma[i]) a_panels->push_back(static_cast<int>(i));
+    for (std::size_t i = 0; i < mb.size(); ++i)
+        if (mb[i]) b_panels->push_back(static_cast<int>(i));
 }
 
 std::size_t ozaki_work_entries() {

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -191,9 +192,13 @@ struct OzakiArgs {
     EpiSet epis;                 // fused consumers of the product tile (a plain store is one of them)
 };
 std::size_t ozaki_slice_bytes(long long rows, long long k, int tile_rows);
+// Digits of a rows x k operand (row stride rs, k stride ks) for tile_rows = 128;
+// with `panels`, only those 128-row panels are written.
 int ozaki_split(const double* x, long long rows, long long k, long long rs, long long ks, int tile_rows, int slices,
-                int8_t* out, int* exps, cudaStream_t s);
+                int8_t* out, int* exps, cudaStream_t s, const std::vector<int>* panels = nullptr);
 long long ozaki_tile_count(const OzakiArgs& p);
+// The 128-row panels of A and of B that the tiles [tile_begin, tile_begin + tile_count) read.
+void ozaki_tile_panels(const OzakiArgs& p, std::vector<int>* a_panels, std::vector<int>* b_panels);
 std::size_t ozaki_work_entries();  // doubles of OzakiArgs::work
 // Launches the emulated GEMM with its fused epilogues and their finalizers.
 int launch_ozaki_gemm(const OzakiArgs& p, cudaStream_t s);

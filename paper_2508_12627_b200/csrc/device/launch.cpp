@@ -261,8 +261,6 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
         for (void* q : got) cudaFreeAsync(q, s);
         return -1;
     }
-    int launched = ozaki_split(g.a.ptr[0], g.rows, g.n, ars, g.a.kstride[0], 128, kOzSlices, da, ea, s);
-    if (!same) launched += ozaki_split(g.b.ptr[0], g.cols, g.n, brs, g.b.kstride[0], 128, kOzSlices, db, eb, s);
     const bool sym = g.symmetric_out && g.rows == g.cols;
     OzakiArgs p;
     p.a = da;
@@ -286,6 +284,25 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
     }
     const long long tiles = p.tile_count >= 0 ? p.tile_count : ozaki_tile_count(p);
     p.work = work;
+    // digits: all panels, or under row sharding only the panels this rank's tiles read
+    int launched = 0;
+    if (g.tile_count >= 0) {
+        std::vector<int> pa, pb;
+        ozaki_tile_panels(p, &pa, &pb);
+        if (same) {
+            std::vector<int> u(pa);
+            u.insert(u.end(), pb.begin(), pb.end());
+            std::sort(u.begin(), u.end());
+            u.erase(std::unique(u.begin(), u.end()), u.end());
+            launched += ozaki_split(g.a.ptr[0], g.rows, g.n, ars, g.a.kstride[0], 128, kOzSlices, da, ea, s, &u);
+        } else {
+            launched += ozaki_split(g.a.ptr[0], g.rows, g.n, ars, g.a.kstride[0], 128, kOzSlices, da, ea, s, &pa);
+            launched += ozaki_split(g.b.ptr[0], g.cols, g.n, brs, g.b.kstride[0], 128, kOzSlices, db, eb, s, &pb);
+        }
+    } else {
+        launched += ozaki_split(g.a.ptr[0], g.rows, g.n, ars, g.a.kstride[0], 128, kOzSlices, da, ea, s);
+        if (!same) launched += ozaki_split(g.b.ptr[0], g.cols, g.n, brs, g.b.kstride[0], 128, kOzSlices, db, eb, s);
+    }
     const int l = launch_ozaki_gemm(p, s);
     if (l < 0) fail(ErrorCode::InvalidArgument, "executor: emulated GEMM launch failed");
     launched += l;
