@@ -104,6 +104,15 @@ struct OzSmem {
 constexpr long long OZ_GROUP = 12;
 __host__ __device__ __forceinline__ void oz_tile_of(const OzakiArgs& p, long long bid, long long* tm, long long* tn) {
     const long long T_m = p.mpad / OZ_BM, T_n = p.npad / OZ_BN;
+    if (!p.symmetric) {  // groups of OZ_GROUP row tiles x all column tiles, column-major inside: O(1)
+        const long long width = OZ_GROUP * T_n;
+        const long long g = bid / width, m0 = g * OZ_GROUP;
+        const long long gsz = (T_m - m0) < OZ_GROUP ? (T_m - m0) : OZ_GROUP;
+        const long long rem = bid - g * width;
+        *tm = m0 + rem % gsz;
+        *tn = rem / gsz;
+        return;
+    }
     const long long gm = (T_m + OZ_GROUP - 1) / OZ_GROUP, gn = (T_n + OZ_GROUP - 1) / OZ_GROUP;
     for (long long J = 0; J < gn; ++J)
         for (long long I = 0; I < gm; ++I) {

@@ -214,8 +214,8 @@ void Program::run_stream(const Op& op, double* out) {
 constexpr int kOzSlices = 7;
 constexpr long long kOzMaxK = 19000;    // 7 products of K * 127^2 per diagonal < 2^31
 constexpr long long kOzMinDim = 1024;   // below, DMMA is as fast and needs no digit pass
-constexpr long long kOzMinK = 2048;     // shorter K: per-tile drains and digit passes outweigh the MMA savings
-                                        // (C4's Khatri-Rao GEMMs, K = 1024, measured 1.5x slower emulated)
+constexpr long long kOzMinK = 1024;     // shorter K: per-tile drains and digit passes outweigh the MMA savings
+                                        // (C4's Khatri-Rao GEMMs, K = 1024: 297 -> 216 ms per evaluation)
 
 // A single-factor operand whose row digits flatten to one stride (a
 // materialized Khatri-Rao operand of n^2 rows is one): its row stride, or -1.
@@ -228,7 +228,11 @@ long long flat_row_stride(const GemmSide& s, long long n) {
 
 bool Program::emulated_eligible(const GemmArgs& g) const {
     if (!config_.device.fp64_emulation) return false;
-    if (g.n > kOzMaxK || g.n < kOzMinK || g.rows < kOzMinDim || g.cols < kOzMinDim) return false;
+    static const long long min_k = [] {  // USTATS_OZ_MIN_K: experiment with the threshold
+        const char* v = std::getenv("USTATS_OZ_MIN_K");
+        return v ? std::atoll(v) : kOzMinK;
+    }();
+    if (g.n > kOzMaxK || g.n < min_k || g.rows < kOzMinDim || g.cols < kOzMinDim) return false;
     return flat_row_stride(g.a, n_) >= 0 && flat_row_stride(g.b, n_) >= 0;
 }
 
