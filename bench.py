@@ -400,8 +400,8 @@ def main():
         "config": {"workload": name, "m": m, "n": n, "signature": sig, "terms": int(r.terms),
                    "api": (f"u_statistic('{spec}', sample): components tensorized on the GPU"
                            if use_data else "u_terms(tensors)"),
-                   "gemm": ("FP64 via Ozaki splitting on the INT8 tensor cores (7 signed 7-bit digits per value, "
-                            "exact int32 digit products, FP64 assembly; ~1e-12 relative) where 1024 <= K <= 19000, "
+                   "gemm": ("FP64 via Ozaki splitting on the INT8 tensor cores (6 balanced 8-bit digits per value, "
+                            "exact int32 digit products, FP64 assembly; ~1e-11 relative) where 1024 <= K <= 21000, "
                             "else FP64 DMMA") if cfg.fp64_emulation else "FP64 DMMA (mma.sync f64)",
                    "parallelism": (f"row-sharded x{world}" if args.shard == "rows" else f"term-sharded x{world}")
                    if world > 1 else "single GPU",

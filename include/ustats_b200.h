@@ -222,8 +222,8 @@ US_API int us_device_count(int32_t* count);
 US_API int us_device_synchronize(int32_t device);
 /* FP64 GEMM C = A B^T (A m x k, B n x k, C m x n; row-major host buffers)
  * on the device: method 0 = DMMA (mma.sync f64, TMA-fed), 1 = Ozaki
- * splitting on the INT8 tcgen05 tensor cores with `slices` 7-bit digits
- * (4..7; method 0 needs an even k); symmetric != 0 asserts B = A (upper
+ * splitting on the INT8 tcgen05 tensor cores with `slices` balanced 8-bit
+ * digits (4..7, slices * k * 128^2 < 2^31; method 0 needs an even k); symmetric != 0 asserts B = A (upper
  * tiles, mirrored). ms_out
  * (optional) receives the device time of the GEMM itself. */
 US_API int us_dgemm(int32_t method, int32_t slices, int32_t symmetric, int64_t m, int64_t n, int64_t k,

@@ -560,7 +560,7 @@ def chain_signature(m: int):
 
 def dgemm(a, b, method: str = "ozaki", slices: int = 7, symmetric: bool = False, with_time: bool = False):
     """C = A B^T in FP64 on the device: method "dmma" (mma.sync f64) or
-    "ozaki" (7-bit digit splitting on the INT8 tcgen05 tensor cores)."""
+    "ozaki" (balanced 8-bit digit splitting on the INT8 tcgen05 tensor cores)."""
     A = np.ascontiguousarray(a, dtype=np.float64)
     B = np.ascontiguousarray(b, dtype=np.float64)
     if A.ndim != 2 or B.ndim != 2 or A.shape[1] != B.shape[1]:

@@ -607,8 +607,10 @@ int us_dgemm(int32_t method, int32_t slices, int32_t symmetric, int64_t m, int64
             double* work = nullptr;
             check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&work), ozaki_work_entries() * sizeof(double), s), "alloc");
             p.work = work;
-            launch_ozaki_gemm(p, s);
+            const int launched = launch_ozaki_gemm(p, s);
             cudaFreeAsync(work, s);
+            if (launched < 0)
+                ustats::fail(ustats::ErrorCode::InvalidArgument, "Ozaki GEMM: slices * k * 128^2 must stay below 2^31");
             cudaEventRecord(e1, s);
         } else {
             GemmArgs g;

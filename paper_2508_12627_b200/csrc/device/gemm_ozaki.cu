@@ -2,18 +2,19 @@
 // kind::i8, accumulators in TMEM) — the Ozaki splitting scheme:
 //
 //   every row x of an operand is scaled by a power of two 2^-e (e = the
-//   exponent of the row's largest |x|, so |x 2^-e| < 1) and cut into S signed
-//   7-bit digits, x 2^-e = sum_{t<S} 2^{-7(t+1)} x_t, x_t in [-127, 127]
-//   (each digit is an exact subtraction: no rounding);
-//   C = A B^T = 2^{eA_i + eB_j} sum_{t+u<S} 2^{-7(t+u+2)} (A_t B_u^T)
+//   exponent of the row's largest |x|, so |x 2^-e| < 1), truncated to the
+//   integer m = trunc(x 2^{8S-2-e}) (|m| < 2^{8S-2}) and written in balanced
+//   base 256: m = sum_{t<S} 256^{S-1-t} x_t, x_t in [-128, 127] (every digit
+//   exact: the signed int8 range is used in full, 8 bits per slice);
+//   C = A B^T = 2^{eA_i + eB_j} sum_{t+u<S} 2^{-8(t+u)-12} (A_t B_u^T)
 //
 // Each digit product A_t B_u^T is an exact int8 x int8 -> int32 tensor-core
 // GEMM; products of one diagonal d = t+u share a TMEM accumulator (exact while
-// (d+1) K 127^2 < 2^31). The dropped products (t+u >= S) bound the error by
-// ~2^{-7S} K max|A_i| max|B_j| per entry: S = 7 keeps it below 1e-14 of the
-// row-scale product. The FP64 result is assembled from the S int32 diagonals
-// in a fixed order, so it is deterministic (and bitwise symmetric for A B^T
-// with B = A).
+// S K 128^2 < 2^31). Truncation and the dropped products (t+u >= S) bound the
+// error by ~(S + 2) 2^{2-8S} K max|A_i| max|B_j| per entry: S = 6 (21 products,
+// 46 bits) keeps it near 1e-13 of the row-scale product. The FP64 result is
+// assembled from the S int32 diagonals in a fixed order, so it is
+// deterministic (and bitwise symmetric for A B^T with B = A).
 //
 // Operand digits live in global memory pre-tiled in the tensor core's K-major
 // "core matrix" layout (tiles of TH rows x 64 bytes: four 16-byte K chunks,
@@ -93,8 +94,9 @@ struct OzSmem {
 
 // One 128 x 128 output tile per CTA, in two passes over K so that the digit
 // diagonals fit TMEM at N = 128 (the full-rate MMA shape): pass 0 sums the
-// high diagonals d = 4..S-1 (slices 0..S-1), pass 1 the low ones d = 0..3
-// (slices 0..3), each into <= 4 int32 accumulators of 128 columns. Between
+// high diagonals d = P..S-1 (slices 0..S-1), pass 1 the low ones d = 0..P-1
+// (slices 0..P-1, P = oz_pass_split(S)), each into <= 4 int32 accumulators of
+// 128 columns. Between
 // the passes the epilogue warps drain pass 0 into the output tile (FP64,
 // before the row/column exponents); pass 1 adds to it.
 // Tile order: square groups of OZ_GROUP x OZ_GROUP tiles (upper groups only
@@ -136,6 +138,15 @@ __host__ __device__ __forceinline__ void oz_tile_of(const OzakiArgs& p, long lon
     *tn = 0;
 }
 
+// Diagonals of pass 1 (the rest, at most 4, go to pass 0). Pass 0 loads all S
+// slices, pass 1 only P: the fewer accumulators pass 0 takes, the fewer bytes
+// per k, the more MMAs per staged byte in pass 0.
+#ifndef OZ_PASS0_ACC
+#define OZ_PASS0_ACC 3
+#endif
+__host__ __device__ constexpr int oz_pass_split(int S) { return S <= 4 ? S : S - OZ_PASS0_ACC; }
+static_assert(oz_pass_split(7) <= 4 && 7 - oz_pass_split(7) <= 4, "TMEM holds 4 accumulators of 128 columns");
+
 template <int S, int D0, int D1>
 __device__ __forceinline__ void oz_issue_stage(unsigned tmem, const unsigned long long* da0, const unsigned long long* db0,
                                                unsigned idesc, bool first0) {
@@ -171,7 +182,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
     extern __shared__ unsigned char oz_raw[];
     OzSmem& sm = *reinterpret_cast<OzSmem*>((reinterpret_cast<unsigned long long>(oz_raw) + 1023) & ~1023ull);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    constexpr int split = S > 4 ? 4 : S;  // diagonals of pass 1: [0, split); pass 0: [split, S)
+    constexpr int split = oz_pass_split(S);  // diagonals of pass 1: [0, split); pass 0: [split, S)
     long long tm, tn;
     oz_tile_of(p, p.tile_begin + blockIdx.x, &tm, &tn);
     const long long ksteps = p.kpad / OZ_SK;
@@ -293,7 +304,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
                     unsigned r[16];
                     tmem_ld16(tmem + (static_cast<unsigned>(warp * 32) << 16) + static_cast<unsigned>((d - d0) * OZ_BN + c0),
                               r);
-                    const double scale = ldexp(1.0, -7 * (d + 2));
+                    const double scale = ldexp(1.0, -8 * d - 12);
 #pragma unroll
                     for (int j = 0; j < 16; ++j) v[j] += static_cast<double>(static_cast<int>(r[j])) * scale;
                 }
@@ -348,9 +359,9 @@ __global__ void oz_row_exponents(const double* __restrict__ x, long long rows, l
 // the FP64 tile is staged in shared memory with coalesced row reads, each
 // thread turns one (row, 16-element chunk) into S 16-byte digit words, and
 // every slice tile (th x 64 bytes, contiguous) is written coalesced.
-// |x| 2^-e < 1, so m = trunc(|x| 2^{7S-e}) < 2^{7S} holds the first S base-128
-// digits of |x| 2^-e exactly (the digits the exact FP64 peeling
-// x -> 128 x - trunc(128 x) yields); the sign is applied to every digit.
+// |x| 2^-e < 1, so m = trunc(x 2^{8S-2-e}) satisfies |m| < 2^{8S-2}: its S
+// balanced base-256 digits (low byte as a signed int8, subtract, shift) fit
+// int8, the top one in [-64, 64].
 constexpr int OZ_SPLIT_THREADS = 256;
 __global__ void __launch_bounds__(OZ_SPLIT_THREADS) oz_split(const double* __restrict__ x, long long rows, long long k,
                                                             long long rs, long long ks, const int* __restrict__ exps,
@@ -382,23 +393,17 @@ __global__ void __launch_bounds__(OZ_SPLIT_THREADS) oz_split(const double* __res
         const int rr = item % th, cin = item / th;  // consecutive threads: consecutive rows of one chunk
         const long long R = r0 + rr;
         const int e = R < rows ? exps[R] : 0;
-        unsigned long long mag[16];
-        bool neg[16];
+        long long m[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const double xv = tilebuf[rr * P + cin * 16 + j];
-            neg[j] = xv < 0.0;
-            mag[j] = static_cast<unsigned long long>(ldexp(fabs(xv), 7 * slices - e));
-        }
+        for (int j = 0; j < 16; ++j) m[j] = static_cast<long long>(ldexp(tilebuf[rr * P + cin * 16 + j], 8 * slices - 2 - e));
         const long long off = tile_off + cin * (th * 16) + rr * 16;
-        for (int t = 0; t < slices; ++t) {
-            const int shift = 7 * (slices - 1 - t);
+        for (int t = slices - 1; t >= 0; --t) {  // least significant digit first
             unsigned w[4] = {0, 0, 0, 0};
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-                const int dg = static_cast<int>((mag[j] >> shift) & 127u);
-                const unsigned byte = static_cast<unsigned>(neg[j] ? -dg : dg) & 0xFFu;
-                w[j >> 2] |= byte << ((j & 3) * 8);
+                const int dg = static_cast<int>(static_cast<signed char>(m[j] & 0xFF));  // in [-128, 127]
+                m[j] = (m[j] - dg) >> 8;                                                  // exact
+                w[j >> 2] |= (static_cast<unsigned>(dg) & 0xFFu) << ((j & 3) * 8);
             }
             *reinterpret_cast<uint4*>(out + t * slice_bytes + off) = make_uint4(w[0], w[1], w[2], w[3]);
         }
@@ -488,6 +493,7 @@ void launch_oz(const OzakiArgs& p, long long tiles, cudaStream_t s) {
 
 int launch_ozaki_gemm(const OzakiArgs& in, cudaStream_t s) {
     if (in.kpad % OZ_BK != 0) return -1;
+    if (static_cast<long long>(in.slices) * in.kpad * 128 * 128 >= (1ll << 31)) return -1;  // int32 diagonals exact
     OzakiArgs p = in;
     // warming L2 two k-tiles ahead pays while a wave's digit panels fit L2
     // (C2, K = 8192: +2%); at K = 16384 it evicts them (C3: -9%)

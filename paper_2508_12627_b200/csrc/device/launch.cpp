@@ -211,8 +211,8 @@ void Program::run_stream(const Op& op, double* out) {
 
 // FP64 emulation on the INT8 tensor cores (gemm_ozaki.cu) for large plain
 // products whose K keeps every digit diagonal exact in int32.
-constexpr int kOzSlices = 7;
-constexpr long long kOzMaxK = 19000;    // 7 products of K * 127^2 per diagonal < 2^31
+constexpr int kOzSlices = 6;           // 8-bit balanced digits: 46 bits, 21 digit products
+constexpr long long kOzMaxK = 21000;    // 6 products of K * 128^2 per diagonal < 2^31
 constexpr long long kOzMinDim = 1024;   // below, DMMA is as fast and needs no digit pass
 constexpr long long kOzMinK = 1024;     // shorter K: per-tile drains and digit passes outweigh the MMA savings
                                         // (C4's Khatri-Rao GEMMs, K = 1024: 297 -> 216 ms per evaluation)

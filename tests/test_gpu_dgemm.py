@@ -12,7 +12,7 @@ def test_ozaki_matches_numpy(engine, m, n, k):
     a, b = rng.normal(size=(m, k)), rng.normal(size=(n, k))
     ref = a @ b.T
     got = engine.dgemm(a, b, "ozaki", 7)
-    # 7 digits of 7 bits: ~2^-49 K max|a| max|b| per entry
+    # 7 balanced 8-bit digits: ~2^-54 K max|a| max|b| per entry
     assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
     if k % 2 == 0:  # the TMA-fed DMMA kernel needs 16-byte aligned rows
         dm = engine.dgemm(a, b, "dmma")
