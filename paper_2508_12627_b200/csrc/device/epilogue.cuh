@@ -33,7 +33,31 @@ __device__ __forceinline__ void apply(const EpiSet& epis, long long rows, long l
         auto P = [&](double x) { return d.self_power == 2 ? x * x : x; };
         // element order: column-fastest unless the first weight is column-major
         const bool cfast = !(d.nw > 0 && d.wr[0] == 1 && d.wc[0] != 1);
-        if (d.mode == kEpiStore || d.mode == kEpiSumAll) {
+        if (d.mode == kEpiStore && d.nw == 0 && !d.transpose) {  // plain store: a warp per row, lanes along it
+            for (int r = warp; r < BM; r += NT / 32) {
+                const long long R = r0 + r;
+                if (R >= rows) break;
+                double* o = d.out + R * cols + c0;
+#pragma unroll 4
+                for (int c = lane; c < BN; c += 32)
+                    if (c0 + c < cols) {
+                        const double v = P(tile[r * TP + c]);
+                        o[c] = accumulate ? o[c] + v : v;
+                    }
+            }
+            if (mirror)  // out[C][R] = tile[R][C]: a warp per tile column, lanes down it
+                for (int c = warp; c < BN; c += NT / 32) {
+                    const long long C = c0 + c;
+                    if (C >= cols) break;
+                    double* o = d.out + C * cols + r0;
+#pragma unroll 4
+                    for (int r = lane; r < BM; r += 32)
+                        if (r0 + r < rows) {
+                            const double v = P(tile[r * TP + c]);
+                            o[r] = accumulate ? o[r] + v : v;
+                        }
+                }
+        } else if (d.mode == kEpiStore || d.mode == kEpiSumAll) {
             double s = 0.0;
             for (int i = tid; i < BM * BN; i += NT) {
                 const int r = cfast ? (i >> 7) : (i & 127), c = cfast ? (i & 127) : (i >> 7);

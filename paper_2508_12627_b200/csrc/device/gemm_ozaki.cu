@@ -70,13 +70,22 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
         "l"(reinterpret_cast<unsigned long long>(src)), "r"(bytes), "r"(su32(bar))
         : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(unsigned addr, unsigned* r) {
+// Asynchronous TMEM load (no wait): pair with tmem_wait_ld, which also pins
+// the loaded registers after the wait.
+__device__ __forceinline__ void tmem_ld16_async(unsigned addr, unsigned* r) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
           "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(addr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;");
+}
+template <int N>
+__device__ __forceinline__ void tmem_wait_ld(unsigned (&r)[N][16]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) asm volatile("" : "+r"(r[i][j]));
 }
 
 struct OzSmem {
@@ -89,6 +98,7 @@ struct OzSmem {
     } u;
     unsigned long long full[OZ_STAGES], empty[OZ_STAGES], done[2], drained;
     double red[4];
+    int bexp[OZ_BN];  // column exponents of the tile
     unsigned tmem;
 };
 
@@ -147,40 +157,74 @@ __host__ __device__ __forceinline__ void oz_tile_of(const OzakiArgs& p, long lon
 __host__ __device__ constexpr int oz_pass_split(int S) { return S <= 4 ? S : S - OZ_PASS0_ACC; }
 static_assert(oz_pass_split(7) <= 4 && 7 - oz_pass_split(7) <= 4, "TMEM holds 4 accumulators of 128 columns");
 
-template <int S, int D0, int D1>
-__device__ __forceinline__ void oz_issue_stage(unsigned tmem, const unsigned long long* da0, const unsigned long long* db0,
-                                               unsigned idesc, bool first0) {
+// Issued by the whole MMA warp: every operand is warp-uniform (one base
+// descriptor plus compile-time offsets), so the descriptors stay in uniform
+// registers and each MMA is one elected UTCIMMA (no per-MMA waterfall loop).
+template <int S, int D0, int D1, int STAGE>
+__device__ __forceinline__ void oz_issue_stage(unsigned tmem, unsigned long long desc0, unsigned idesc, bool first0) {
     // diagonals [D0, D1) of the digit products, accumulators at (d - D0) * 128 columns;
     // two 32-byte k-steps per stage: the second starts two 16-byte chunks (2 x 2048 B) further
+    constexpr unsigned b_off = OZ_STAGES * kOzMaxSlices * OZ_TILE_STAGE;  // sm.u.st.b after sm.u.st.a
 #pragma unroll
     for (int ks = 0; ks < OZ_SK / 32; ++ks) {
-    unsigned long long da[S], db[S];
+        const bool first = first0 && ks == 0;
 #pragma unroll
-    for (int t = 0; t < S; ++t) {
-        da[t] = da0[t] + static_cast<unsigned long long>(ks * 2 * OZ_BM * 16 >> 4);
-        db[t] = db0[t] + static_cast<unsigned long long>(ks * 2 * OZ_BN * 16 >> 4);
+        for (int d = D0; d < D1; ++d)
+#pragma unroll
+            for (int t = 0; t <= d; ++t) {
+                const int u = d - t;
+                if (t >= S || u >= S) continue;
+                const unsigned a_off = (STAGE * kOzMaxSlices + t) * OZ_TILE_STAGE + ks * 2 * OZ_BM * 16;
+                const unsigned bo = b_off + (STAGE * kOzMaxSlices + u) * OZ_TILE_STAGE + ks * 2 * OZ_BN * 16;
+                const unsigned acc = tmem + static_cast<unsigned>((d - D0) * OZ_BN);
+                const unsigned accumulate = (first && t == 0) ? 0u : 1u;
+                asm volatile(
+                    "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+                    "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(acc),
+                    "l"(desc0 + (a_off >> 4)), "l"(desc0 + (bo >> 4)), "r"(idesc), "r"(accumulate));
+            }
     }
-    const bool first = first0 && ks == 0;
+}
+
+__device__ __forceinline__ void oz_commit(unsigned long long* bar) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(su32(bar)));
+}
+
+constexpr int kOzNoColumn = 1 << 30;  // padding column of the tile
+
+// v 2^e: one exact multiply while 2^e is a normal double (ldexp otherwise)
+__device__ __forceinline__ double oz_scale(double v, int e) {
+    if (e >= -1022 && e <= 1023) return v * __longlong_as_double(static_cast<long long>(e + 1023) << 52);
+    return ldexp(v, e);
+}
+
+// Adds the diagonals [D0, D1) of columns c0..c0+15 (this thread's TMEM lane) to
+// v, smallest contributions first: all loads in flight, one wait.
+template <int D0, int D1>
+__device__ __forceinline__ void oz_drain(unsigned lane_base, int c0, double (&v)[16], bool add) {
+    unsigned r[D1 - D0][16];
 #pragma unroll
-    for (int d = D0; d < D1; ++d)
+    for (int d = D0; d < D1; ++d) tmem_ld16_async(lane_base + static_cast<unsigned>((d - D0) * OZ_BN + c0), r[d - D0]);
+    tmem_wait_ld(r);
+    if (!add)
 #pragma unroll
-        for (int t = 0; t <= d; ++t) {
-            const int u = d - t;
-            if (t >= S || u >= S) continue;
-            const unsigned acc = tmem + static_cast<unsigned>((d - D0) * OZ_BN);
-            const unsigned accumulate = (first && t == 0) ? 0u : 1u;
-            asm volatile(
-                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(acc),
-                "l"(da[t]), "l"(db[u]), "r"(idesc), "r"(accumulate));
-        }
+        for (int j = 0; j < 16; ++j) v[j] = 0.0;
+#pragma unroll
+    for (int d = D1 - 1; d >= D0; --d) {
+        const double scale = __longlong_as_double(static_cast<long long>(1023 - 8 * d - 12) << 52);  // 2^{-8d-12}
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] += static_cast<double>(static_cast<int>(r[d - D0][j])) * scale;
     }
 }
 
 template <int S>
 __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) {
-    extern __shared__ unsigned char oz_raw[];
-    OzSmem& sm = *reinterpret_cast<OzSmem*>((reinterpret_cast<unsigned long long>(oz_raw) + 1023) & ~1023ull);
+    // no swizzle: 16-byte alignment is all the descriptors and bulk copies need, and
+    // addressing the struct straight off the shared array keeps every access in .shared
+    extern __shared__ __align__(128) unsigned char oz_raw[];
+    OzSmem& sm = *reinterpret_cast<OzSmem*>(oz_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr int split = oz_pass_split(S);  // diagonals of pass 1: [0, split); pass 0: [split, S)
     long long tm, tn;
@@ -242,17 +286,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
                 }
             }
         }
-    } else if (tid == 160) {  // MMA issuer: descriptors precomputed per stage, products unrolled
+    } else if (warp == 5) {  // MMA warp: the loop runs warp-wide, one elected lane issues
         // kind::i8, int32 accumulate, signed A and B, both K-major, N = 128, M = 128
         const unsigned idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((OZ_BN >> 3) << 17) | ((OZ_BM >> 4) << 24);
-        unsigned long long da[OZ_STAGES][S], db[OZ_STAGES][S];
-#pragma unroll
-        for (int s = 0; s < OZ_STAGES; ++s)
-#pragma unroll
-            for (int t = 0; t < S; ++t) {
-                da[s][t] = umma_desc(su32(sm.u.st.a[s][t]), OZ_BM * 16, 128);
-                db[s][t] = umma_desc(su32(sm.u.st.b[s][t]), OZ_BN * 16, 128);
-            }
+        // a[0][0]; every other slice / stage / operand tile at a constant offset (K-major core matrices:
+        // leading-byte offset = one 16-byte K chunk of 128 rows, stride-byte offset = 8 rows x 16 B)
+        const unsigned long long desc0 = umma_desc(su32(sm.u.st.a[0][0]), OZ_BM * 16, 128);
+        static_assert(OZ_BM == OZ_BN, "one descriptor template for both operands");
         long long it = 0;
         if (split < S) {
 #pragma unroll 1
@@ -260,13 +300,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
                 const int s = static_cast<int>(it % OZ_STAGES);
                 bar_wait(&sm.full[s], static_cast<unsigned>((it / OZ_STAGES) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                if (s == 0) oz_issue_stage<S, split, S>(tmem, da[0], db[0], idesc, k == 0);
-                else oz_issue_stage<S, split, S>(tmem, da[1], db[1], idesc, k == 0);
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                    su32(&sm.empty[s])));
+                if (s == 0) oz_issue_stage<S, split, S, 0>(tmem, desc0, idesc, k == 0);
+                else oz_issue_stage<S, split, S, 1>(tmem, desc0, idesc, k == 0);
+                oz_commit(&sm.empty[s]);
             }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                su32(&sm.done[0])));
+            oz_commit(&sm.done[0]);
             bar_wait(&sm.drained, 0);  // pass 0 read out of TMEM
             asm volatile("tcgen05.fence::after_thread_sync;");
         }
@@ -275,56 +313,55 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
             const int s = static_cast<int>(it % OZ_STAGES);
             bar_wait(&sm.full[s], static_cast<unsigned>((it / OZ_STAGES) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
-            if (s == 0) oz_issue_stage<S, 0, split>(tmem, da[0], db[0], idesc, k == 0);
-            else oz_issue_stage<S, 0, split>(tmem, da[1], db[1], idesc, k == 0);
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                su32(&sm.empty[s])));
+            if (s == 0) oz_issue_stage<S, 0, split, 0>(tmem, desc0, idesc, k == 0);
+            else oz_issue_stage<S, 0, split, 1>(tmem, desc0, idesc, k == 0);
+            oz_commit(&sm.empty[s]);
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-            su32(&sm.done[1])));
+        oz_commit(&sm.done[1]);
     } else if (warp < 4) {  // epilogue warps: thread = one row of the tile (TMEM lane)
-        const long long row = tm * OZ_BM + warp * 32 + lane;
+        const int rt = warp * 32 + lane;  // row inside the tile
+        const long long row = tm * OZ_BM + rt;
         const bool row_ok = row < p.m;
+        if (rt < OZ_BN) {
+            const long long col = tn * OZ_BN + rt;
+            sm.bexp[rt] = col < p.n ? p.b_exp[col] : kOzNoColumn;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int ea = row_ok ? p.a_exp[row] : 0;
         // one CTA per SM at a time (shared memory and TMEM say so): the scratch
-        // of the high-diagonal partial is per SM, L2-resident
+        // of the high-diagonal partial is per SM, L2-resident, column-major so a
+        // warp's 32 rows of one column are one coalesced 256-byte access
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        double* work = p.work + static_cast<long long>(smid) * (OZ_BM * OZ_BN) + (warp * 32 + lane) * OZ_BN;
-        for (int pass = 0; pass < 2; ++pass) {
-            if (pass == 0 && split >= S) continue;
-            const int d0 = pass == 0 ? split : 0, d1 = pass == 0 ? S : split;
-            bar_wait(&sm.done[pass], 0);
+        double* work = p.work + static_cast<long long>(smid) * (OZ_BM * OZ_BN) + rt;
+        const unsigned lane_base = tmem + (static_cast<unsigned>(warp * 32) << 16);
+        if constexpr (split < S) {  // pass 0: high diagonals into the scratch
+            bar_wait(&sm.done[0], 0);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            const int ea = row_ok ? p.a_exp[row] : 0;
+#pragma unroll 1
             for (int c0 = 0; c0 < OZ_BN; c0 += 16) {
                 double v[16];
+                oz_drain<split, S>(lane_base, c0, v, false);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = (pass == 1 && split < S) ? work[c0 + j] : 0.0;  // high diagonals
-                for (int d = d1 - 1; d >= d0; --d) {  // smallest contributions first
-                    unsigned r[16];
-                    tmem_ld16(tmem + (static_cast<unsigned>(warp * 32) << 16) + static_cast<unsigned>((d - d0) * OZ_BN + c0),
-                              r);
-                    const double scale = ldexp(1.0, -8 * d - 12);
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] += static_cast<double>(static_cast<int>(r[j])) * scale;
-                }
-                if (pass == 0) {  // partial, no exponents yet (L2-resident scratch of this tile)
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) work[c0 + j] = v[j];
-                    continue;
-                }
-                // the product tile in shared memory (every MMA has completed: the ring is free)
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const long long col = tn * OZ_BN + c0 + j;
-                    sm.u.tile[(warp * 32 + lane) * epi::TP + c0 + j] =
-                        (row_ok && col < p.n) ? ldexp(v[j], ea + p.b_exp[col]) : 0.0;
-                }
+                for (int j = 0; j < 16; ++j) work[(c0 + j) * OZ_BM] = v[j];
             }
-            if (pass == 0) {
-                asm volatile("tcgen05.fence::before_thread_sync;");
-                __syncwarp();
-                if (lane == 0) bar_arrive(&sm.drained);
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) bar_arrive(&sm.drained);
+        }
+        bar_wait(&sm.done[1], 0);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+        for (int c0 = 0; c0 < OZ_BN; c0 += 16) {
+            double v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = split < S ? work[(c0 + j) * OZ_BM] : 0.0;  // high diagonals
+            oz_drain<0, split>(lane_base, c0, v, true);
+            // the product tile in shared memory (every MMA has completed: the ring is free)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int eb = sm.bexp[c0 + j];
+                sm.u.tile[rt * epi::TP + c0 + j] = (row_ok && eb != kOzNoColumn) ? oz_scale(v[j], ea + eb) : 0.0;
             }
         }
         // the fused consumers of the tile (plain store, Hadamard + reductions), as in the DMMA kernel
@@ -362,6 +399,63 @@ __global__ void oz_row_exponents(const double* __restrict__ x, long long rows, l
 // |x| 2^-e < 1, so m = trunc(x 2^{8S-2-e}) satisfies |m| < 2^{8S-2}: its S
 // balanced base-256 digits (low byte as a signed int8, subtract, shift) fit
 // int8, the top one in [-64, 64].
+// x 2^sh as two exact power-of-two multiplies (each factor a normal double)
+__device__ __forceinline__ double oz_pow2_mul(double x, int sh) {
+    const int a = sh / 2, b = sh - a;
+    return x * __longlong_as_double(static_cast<long long>(a + 1023) << 52) *
+           __longlong_as_double(static_cast<long long>(b + 1023) << 52);
+}
+
+// The S digit words of 16 consecutive values of one row (exponent e) to
+// out[t * slice_bytes], t = 0 (most significant) .. S-1.
+__device__ __forceinline__ void oz_digits16(const double (&xv)[16], int e, int slices, long long slice_bytes,
+                                            int8_t* __restrict__ out) {
+    long long m[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) m[j] = static_cast<long long>(oz_pow2_mul(xv[j], 8 * slices - 2 - e));
+    for (int t = slices - 1; t >= 0; --t) {  // least significant digit first
+        unsigned w[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int dg = static_cast<int>(static_cast<signed char>(m[j] & 0xFF));  // in [-128, 127]
+            m[j] = (m[j] - dg) >> 8;                                                  // exact
+            w[j >> 2] |= (static_cast<unsigned>(dg) & 0xFFu) << ((j & 3) * 8);
+        }
+        *reinterpret_cast<uint4*>(out + t * slice_bytes) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+// k-contiguous rows with 16-byte aligned starts: a thread per (row, 16-value
+// chunk) reads its 128 bytes straight from global memory (8 vector loads in
+// flight), lanes along rows so every slice word store of a warp is 512
+// contiguous bytes. Block: 128 rows x 2 chunks; grid (panels, kpad / 32).
+__global__ void __launch_bounds__(256) oz_split_rows(const double* __restrict__ x, long long rows, long long k,
+                                                     long long rs, const int* __restrict__ exps, long long kpad,
+                                                     int slices, long long slice_bytes, int8_t* __restrict__ out,
+                                                     const int* __restrict__ panels) {
+    const int rr = threadIdx.x & 127;
+    const long long rt = panels ? panels[blockIdx.x] : blockIdx.x;
+    const long long R = rt * OZ_BM + rr;
+    const long long c0 = (static_cast<long long>(blockIdx.y) * 2 + (threadIdx.x >> 7)) * 16;
+    double xv[16];
+    if (R < rows && c0 + 16 <= k) {
+        const double2* src = reinterpret_cast<const double2*>(x + R * rs + c0);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const double2 v = __ldg(src + j);
+            xv[2 * j] = v.x;
+            xv[2 * j + 1] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) xv[j] = (R < rows && c0 + j < k) ? x[R * rs + c0 + j] : 0.0;
+    }
+    const int e = R < rows ? exps[R] : 0;
+    const long long kt = c0 / OZ_BK, cin = (c0 % OZ_BK) / 16;
+    const long long off = (rt * (kpad / OZ_BK) + kt) * (OZ_BM * OZ_BK) + cin * (OZ_BM * 16) + rr * 16;
+    oz_digits16(xv, e, slices, slice_bytes, out + off);
+}
+
 constexpr int OZ_SPLIT_THREADS = 256;
 __global__ void __launch_bounds__(OZ_SPLIT_THREADS) oz_split(const double* __restrict__ x, long long rows, long long k,
                                                             long long rs, long long ks, const int* __restrict__ exps,
@@ -393,20 +487,10 @@ __global__ void __launch_bounds__(OZ_SPLIT_THREADS) oz_split(const double* __res
         const int rr = item % th, cin = item / th;  // consecutive threads: consecutive rows of one chunk
         const long long R = r0 + rr;
         const int e = R < rows ? exps[R] : 0;
-        long long m[16];
+        double xv[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) m[j] = static_cast<long long>(ldexp(tilebuf[rr * P + cin * 16 + j], 8 * slices - 2 - e));
-        const long long off = tile_off + cin * (th * 16) + rr * 16;
-        for (int t = slices - 1; t >= 0; --t) {  // least significant digit first
-            unsigned w[4] = {0, 0, 0, 0};
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int dg = static_cast<int>(static_cast<signed char>(m[j] & 0xFF));  // in [-128, 127]
-                m[j] = (m[j] - dg) >> 8;                                                  // exact
-                w[j >> 2] |= (static_cast<unsigned>(dg) & 0xFFu) << ((j & 3) * 8);
-            }
-            *reinterpret_cast<uint4*>(out + t * slice_bytes + off) = make_uint4(w[0], w[1], w[2], w[3]);
-        }
+        for (int j = 0; j < 16; ++j) xv[j] = tilebuf[rr * P + cin * 16 + j];
+        oz_digits16(xv, e, slices, slice_bytes, out + tile_off + cin * (th * 16) + rr * 16);
     }
 }
 
@@ -439,8 +523,12 @@ int ozaki_split(const double* x, long long rows, long long k, long long rs, long
         cudaFuncSetAttribute(oz_split, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         configured = true;
     }
-    oz_split<<<static_cast<unsigned>(npanels * (kp / OZ_BK)), OZ_SPLIT_THREADS, smem, s>>>(
-        x, rows, k, rs, ks, exps, tile_rows, kp, slices, rp * kp, out, dpanels);
+    if (ks == 1 && rs % 2 == 0 && reinterpret_cast<std::uintptr_t>(x) % 16 == 0)
+        oz_split_rows<<<dim3(static_cast<unsigned>(npanels), static_cast<unsigned>(kp / 32)), 256, 0, s>>>(
+            x, rows, k, rs, exps, kp, slices, rp * kp, out, dpanels);
+    else
+        oz_split<<<static_cast<unsigned>(npanels * (kp / OZ_BK)), OZ_SPLIT_THREADS, smem, s>>>(
+            x, rows, k, rs, ks, exps, tile_rows, kp, slices, rp * kp, out, dpanels);
     if (dpanels) cudaFreeAsync(dpanels, s);
     return 2;
 }
@@ -482,7 +570,7 @@ long long ozaki_tile_count(const OzakiArgs& p) {
 
 template <int S>
 void launch_oz(const OzakiArgs& p, long long tiles, cudaStream_t s) {
-    const int bytes = static_cast<int>(sizeof(OzSmem)) + 1024;
+    const int bytes = static_cast<int>(sizeof(OzSmem));
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(ozaki_gemm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
