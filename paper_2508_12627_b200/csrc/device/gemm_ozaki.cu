@@ -97,6 +97,7 @@ struct OzSmem {
         double tile[epi::BM * epi::TP];  // the FP64 product tile once every MMA has read its operands
     } u;
     unsigned long long full[OZ_STAGES], empty[OZ_STAGES], done[2], drained;
+    unsigned long long full1[8], empty1[8];  // pass 1's deeper ring (oz_p1_stages)
     double red[4];
     int bexp[OZ_BN];  // column exponents of the tile
     unsigned tmem;
@@ -160,7 +161,7 @@ static_assert(oz_pass_split(7) <= 4 && 7 - oz_pass_split(7) <= 4, "TMEM holds 4 
 // Issued by the whole MMA warp: every operand is warp-uniform (one base
 // descriptor plus compile-time offsets), so the descriptors stay in uniform
 // registers and each MMA is one elected UTCIMMA (no per-MMA waterfall loop).
-template <int S, int D0, int D1, int STAGE>
+template <int S, int D0, int D1, int SLOT0>
 __device__ __forceinline__ void oz_issue_stage(unsigned tmem, unsigned long long desc0, unsigned idesc, bool first0) {
     // diagonals [D0, D1) of the digit products, accumulators at (d - D0) * 128 columns;
     // two 32-byte k-steps per stage: the second starts two 16-byte chunks (2 x 2048 B) further
@@ -174,8 +175,8 @@ __device__ __forceinline__ void oz_issue_stage(unsigned tmem, unsigned long long
             for (int t = 0; t <= d; ++t) {
                 const int u = d - t;
                 if (t >= S || u >= S) continue;
-                const unsigned a_off = (STAGE * kOzMaxSlices + t) * OZ_TILE_STAGE + ks * 2 * OZ_BM * 16;
-                const unsigned bo = b_off + (STAGE * kOzMaxSlices + u) * OZ_TILE_STAGE + ks * 2 * OZ_BN * 16;
+                const unsigned a_off = (SLOT0 + t) * OZ_TILE_STAGE + ks * 2 * OZ_BM * 16;
+                const unsigned bo = b_off + (SLOT0 + u) * OZ_TILE_STAGE + ks * 2 * OZ_BN * 16;
                 const unsigned acc = tmem + static_cast<unsigned>((d - D0) * OZ_BN);
                 const unsigned accumulate = (first && t == 0) ? 0u : 1u;
                 asm volatile(
@@ -184,6 +185,22 @@ __device__ __forceinline__ void oz_issue_stage(unsigned tmem, unsigned long long
                     "l"(desc0 + (a_off >> 4)), "l"(desc0 + (bo >> 4)), "r"(idesc), "r"(accumulate));
             }
     }
+}
+
+// Pass 1 stages only `split` slices, so its ring reuses the slot array as
+// OZ_STAGES x (kOzMaxSlices / split) smaller stages: stage q starts at slot
+// oz_p1_slot(q). Deeper lookahead where pass 1 has the fewest MMAs per byte.
+__host__ __device__ constexpr int oz_p1_groups(int split) { return kOzMaxSlices / split; }
+__host__ __device__ constexpr int oz_p1_stages(int split) {
+    return OZ_STAGES * oz_p1_groups(split) < 8 ? OZ_STAGES * oz_p1_groups(split) : 8;
+}
+__host__ __device__ constexpr int oz_p1_slot(int split, int q) {
+    return (q / oz_p1_groups(split)) * kOzMaxSlices + (q % oz_p1_groups(split)) * split;
+}
+template <int S, int SPLIT, int Q = 0>
+__device__ __forceinline__ void oz_issue_p1(int q, unsigned tmem, unsigned long long desc0, unsigned idesc, bool first) {
+    if (q == Q) oz_issue_stage<S, 0, SPLIT, oz_p1_slot(SPLIT, Q)>(tmem, desc0, idesc, first);
+    else if constexpr (Q + 1 < oz_p1_stages(SPLIT)) oz_issue_p1<S, SPLIT, Q + 1>(q, tmem, desc0, idesc, first);
 }
 
 __device__ __forceinline__ void oz_commit(unsigned long long* bar) {
@@ -243,6 +260,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
             bar_init(&sm.full[s], 1);
             bar_init(&sm.empty[s], 1);
         }
+        for (int q = 0; q < oz_p1_stages(split); ++q) {
+            bar_init(&sm.full1[q], 1);
+            bar_init(&sm.empty1[q], 1);
+        }
         bar_init(&sm.done[0], 1);
         bar_init(&sm.done[1], 1);
         bar_init(&sm.drained, 4);
@@ -253,38 +274,45 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
     asm volatile("tcgen05.fence::after_thread_sync;");
     const unsigned tmem = sm.tmem;
 
-    if (tid == 128) {  // producer: pass 0 then pass 1 through one stage ring
-        long long it = 0;
-#pragma unroll 1
-        for (int pass = 0; pass < 2; ++pass) {
-            const int ns = pass == 0 ? S : split;
-            if (pass == 0 && split >= S) continue;
-#pragma unroll 1
-            for (long long k = 0; k < ksteps; ++k, ++it) {
-                const int s = static_cast<int>(it % OZ_STAGES);
-                if (it >= OZ_STAGES) bar_wait(&sm.empty[s], static_cast<unsigned>(((it / OZ_STAGES) - 1) & 1));
-                bar_expect(&sm.full[s], static_cast<unsigned>(2 * ns * OZ_TILE_STAGE));
-                // stage k = global k-tile k (four 16-byte chunks, contiguous)
-                const long long off = k * tile_bytes;
+    if (tid == 128) {  // producer: pass 0 through the 2-stage ring, then pass 1 through its deeper one
+        auto load_stage = [&](long long k, int ns, int slot0, unsigned long long* bar) {
+            bar_expect(bar, static_cast<unsigned>(2 * ns * OZ_TILE_STAGE));
+            // stage k = global k-tile k (four 16-byte chunks, contiguous)
+            const long long off = k * tile_bytes;
+            for (int t = 0; t < ns; ++t) {
+                bulk_load(sm.u.st.a[0][0] + (slot0 + t) * OZ_TILE_STAGE, abase + t * p.a_slice + off, OZ_TILE_STAGE, bar);
+                bulk_load(sm.u.st.b[0][0] + (slot0 + t) * OZ_TILE_STAGE, bbase + t * p.b_slice + off, OZ_TILE_STAGE, bar);
+            }
+            // warm L2 a few k-tiles ahead
+            if (p.prefetch > 0 && k + p.prefetch < ksteps) {
+                const long long poff = off + p.prefetch * tile_bytes;
                 for (int t = 0; t < ns; ++t) {
-                    bulk_load(sm.u.st.a[s][t], abase + t * p.a_slice + off, OZ_TILE_STAGE, &sm.full[s]);
-                    bulk_load(sm.u.st.b[s][t], bbase + t * p.b_slice + off, OZ_TILE_STAGE, &sm.full[s]);
-                }
-                // warm L2 a few k-tiles ahead: the ring is only two stages deep
-                if (p.prefetch > 0 && k + p.prefetch < ksteps) {
-                    const long long poff = off + p.prefetch * tile_bytes;
-                    for (int t = 0; t < ns; ++t) {
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                                         reinterpret_cast<unsigned long long>(abase + t * p.a_slice + poff)),
-                                     "r"(static_cast<unsigned>(OZ_TILE_STAGE))
-                                     : "memory");
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                                         reinterpret_cast<unsigned long long>(bbase + t * p.b_slice + poff)),
-                                     "r"(static_cast<unsigned>(OZ_TILE_STAGE))
-                                     : "memory");
-                    }
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                     reinterpret_cast<unsigned long long>(abase + t * p.a_slice + poff)),
+                                 "r"(static_cast<unsigned>(OZ_TILE_STAGE))
+                                 : "memory");
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                     reinterpret_cast<unsigned long long>(bbase + t * p.b_slice + poff)),
+                                 "r"(static_cast<unsigned>(OZ_TILE_STAGE))
+                                 : "memory");
                 }
             }
+        };
+        if constexpr (split < S) {
+#pragma unroll 1
+            for (long long k = 0; k < ksteps; ++k) {
+                const int s = static_cast<int>(k % OZ_STAGES);
+                if (k >= OZ_STAGES) bar_wait(&sm.empty[s], static_cast<unsigned>(((k / OZ_STAGES) - 1) & 1));
+                load_stage(k, S, s * kOzMaxSlices, &sm.full[s]);
+            }
+            bar_wait(&sm.done[0], 0);  // every pass-0 MMA has read its operands: the slots are free
+        }
+        constexpr int P1 = oz_p1_stages(split);
+#pragma unroll 1
+        for (long long k = 0; k < ksteps; ++k) {
+            const int q = static_cast<int>(k % P1);
+            if (k >= P1) bar_wait(&sm.empty1[q], static_cast<unsigned>(((k / P1) - 1) & 1));
+            load_stage(k, split, oz_p1_slot(split, q), &sm.full1[q]);
         }
     } else if (warp == 5) {  // MMA warp: the loop runs warp-wide, one elected lane issues
         // kind::i8, int32 accumulate, signed A and B, both K-major, N = 128, M = 128
@@ -293,29 +321,28 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
         // leading-byte offset = one 16-byte K chunk of 128 rows, stride-byte offset = 8 rows x 16 B)
         const unsigned long long desc0 = umma_desc(su32(sm.u.st.a[0][0]), OZ_BM * 16, 128);
         static_assert(OZ_BM == OZ_BN, "one descriptor template for both operands");
-        long long it = 0;
-        if (split < S) {
+        if constexpr (split < S) {
 #pragma unroll 1
-            for (long long k = 0; k < ksteps; ++k, ++it) {
-                const int s = static_cast<int>(it % OZ_STAGES);
-                bar_wait(&sm.full[s], static_cast<unsigned>((it / OZ_STAGES) & 1));
+            for (long long k = 0; k < ksteps; ++k) {
+                const int s = static_cast<int>(k % OZ_STAGES);
+                bar_wait(&sm.full[s], static_cast<unsigned>((k / OZ_STAGES) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 if (s == 0) oz_issue_stage<S, split, S, 0>(tmem, desc0, idesc, k == 0);
-                else oz_issue_stage<S, split, S, 1>(tmem, desc0, idesc, k == 0);
+                else oz_issue_stage<S, split, S, kOzMaxSlices>(tmem, desc0, idesc, k == 0);
                 oz_commit(&sm.empty[s]);
             }
             oz_commit(&sm.done[0]);
             bar_wait(&sm.drained, 0);  // pass 0 read out of TMEM
             asm volatile("tcgen05.fence::after_thread_sync;");
         }
+        constexpr int P1 = oz_p1_stages(split);
 #pragma unroll 1
-        for (long long k = 0; k < ksteps; ++k, ++it) {
-            const int s = static_cast<int>(it % OZ_STAGES);
-            bar_wait(&sm.full[s], static_cast<unsigned>((it / OZ_STAGES) & 1));
+        for (long long k = 0; k < ksteps; ++k) {
+            const int q = static_cast<int>(k % P1);
+            bar_wait(&sm.full1[q], static_cast<unsigned>((k / P1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
-            if (s == 0) oz_issue_stage<S, 0, split, 0>(tmem, desc0, idesc, k == 0);
-            else oz_issue_stage<S, 0, split, 1>(tmem, desc0, idesc, k == 0);
-            oz_commit(&sm.empty[s]);
+            oz_issue_p1<S, split>(q, tmem, desc0, idesc, k == 0);
+            oz_commit(&sm.empty1[q]);
         }
         oz_commit(&sm.done[1]);
     } else if (warp < 4) {  // epilogue warps: thread = one row of the tile (TMEM lane)
