@@ -99,7 +99,9 @@ struct OzSmem {
     unsigned long long full[OZ_STAGES], empty[OZ_STAGES], done[2], drained;
     unsigned long long full1[8], empty1[8];  // pass 1's deeper ring (oz_p1_stages)
     double red[4];
-    int bexp[OZ_BN];  // column exponents of the tile
+    int bexp[OZ_BN];       // column exponents of the tile
+    double bscale[OZ_BN];  // 2^bexp (0 for padding columns) while every |bexp| <= 511
+    int bwide;             // some column exponent outside [-511, 511]
     unsigned tmem;
 };
 
@@ -211,10 +213,12 @@ __device__ __forceinline__ void oz_commit(unsigned long long* bar) {
 
 constexpr int kOzNoColumn = 1 << 30;  // padding column of the tile
 
-// v 2^e: one exact multiply while 2^e is a normal double (ldexp otherwise)
+// v 2^e: one exact multiply while 2^e is a normal double; ldexp (out of line:
+// inlined, its range handling costs ~60 instructions per value) otherwise
+__device__ __noinline__ double oz_scale_slow(double v, int e) { return ldexp(v, e); }
 __device__ __forceinline__ double oz_scale(double v, int e) {
     if (e >= -1022 && e <= 1023) return v * __longlong_as_double(static_cast<long long>(e + 1023) << 52);
-    return ldexp(v, e);
+    return oz_scale_slow(v, e);
 }
 
 // Adds the diagonals [D0, D1) of columns c0..c0+15 (this thread's TMEM lane) to
@@ -349,12 +353,20 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
         const int rt = warp * 32 + lane;  // row inside the tile
         const long long row = tm * OZ_BM + rt;
         const bool row_ok = row < p.m;
+        if (rt == 0) sm.bwide = 0;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
         if (rt < OZ_BN) {
             const long long col = tn * OZ_BN + rt;
-            sm.bexp[rt] = col < p.n ? p.b_exp[col] : kOzNoColumn;
+            const int eb = col < p.n ? p.b_exp[col] : kOzNoColumn;
+            sm.bexp[rt] = eb;
+            const bool pad = eb == kOzNoColumn, narrow = eb >= -511 && eb <= 511;
+            sm.bscale[rt] = (pad || !narrow) ? 0.0 : __longlong_as_double(static_cast<long long>(eb + 1023) << 52);
+            if (!pad && !narrow) sm.bwide = 1;
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
         const int ea = row_ok ? p.a_exp[row] : 0;
+        const bool narrow = !sm.bwide && ea >= -511 && ea <= 511;
+        const double sa = row_ok ? __longlong_as_double(static_cast<long long>(ea + 1023) << 52) : 0.0;
         // one CTA per SM at a time (shared memory and TMEM say so): the scratch
         // of the high-diagonal partial is per SM, L2-resident, column-major so a
         // warp's 32 rows of one column are one coalesced 256-byte access
@@ -376,20 +388,36 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
             __syncwarp();
             if (lane == 0) bar_arrive(&sm.drained);
         }
+        // the high-diagonal partial comes back from L2 two 16-column chunks ahead
+        // of its use (the first two while pass 1 still runs: this thread wrote them)
+        double h0[16], h1[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            h0[j] = split < S ? work[j * OZ_BM] : 0.0;
+            h1[j] = split < S ? work[(16 + j) * OZ_BM] : 0.0;
+        }
         bar_wait(&sm.done[1], 0);
         asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll 1
         for (int c0 = 0; c0 < OZ_BN; c0 += 16) {
             double v[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = split < S ? work[(c0 + j) * OZ_BM] : 0.0;  // high diagonals
-            oz_drain<0, split>(lane_base, c0, v, true);
-            // the product tile in shared memory (every MMA has completed: the ring is free)
-#pragma unroll
             for (int j = 0; j < 16; ++j) {
-                const int eb = sm.bexp[c0 + j];
-                sm.u.tile[rt * epi::TP + c0 + j] = (row_ok && eb != kOzNoColumn) ? oz_scale(v[j], ea + eb) : 0.0;
+                v[j] = h0[j];
+                h0[j] = h1[j];
+                if (c0 + 32 < OZ_BN) h1[j] = split < S ? work[(c0 + 32 + j) * OZ_BM] : 0.0;
             }
+            oz_drain<0, split>(lane_base, c0, v, true);
+            // the product tile in shared memory (every MMA has completed: the ring is free);
+            // exact power-of-two scaling: (v 2^ea) 2^eb, branch-free while both |e| <= 511
+            if (narrow)
+#pragma unroll
+                for (int j = 0; j < 16; ++j) sm.u.tile[rt * epi::TP + c0 + j] = (v[j] * sa) * sm.bscale[c0 + j];
+            else
+                for (int j = 0; j < 16; ++j) {
+                    const int eb = sm.bexp[c0 + j];
+                    sm.u.tile[rt * epi::TP + c0 + j] = (row_ok && eb != kOzNoColumn) ? oz_scale(v[j], ea + eb) : 0.0;
+                }
         }
         // the fused consumers of the tile (plain store, Hadamard + reductions), as in the DMMA kernel
         auto sync128 = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
