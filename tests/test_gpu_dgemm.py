@@ -45,3 +45,19 @@ def test_ozaki_wide_dynamic_range_rows(engine):
     got = engine.dgemm(a, b, "ozaki", 7)
     row_scale = np.max(np.abs(a), axis=1)[:, None] * np.max(np.abs(b)) * 256
     assert np.all(np.abs(got - ref) <= 1e-12 * row_scale)
+
+
+def test_ozaki_exponents_beyond_the_fast_scaling_range(engine):
+    # rows / columns scaled past 2^511 take the out-of-line exponent path of
+    # the epilogue; the rest of the tile stays on the branch-free one
+    rng = np.random.default_rng(4)
+    a = rng.normal(size=(300, 256))
+    b = rng.normal(size=(260, 256))
+    a[::7] *= 1e200
+    b[::11] *= 1e-200
+    ref = a @ b.T
+    got = engine.dgemm(a, b, "ozaki", 7)
+    scale = np.max(np.abs(a), axis=1)[:, None] * np.max(np.abs(b), axis=1)[None, :] * 256
+    assert np.all(np.abs(got - ref) <= 1e-12 * scale)
+    c = engine.dgemm(a, a, "ozaki", 7, symmetric=True)
+    assert np.array_equal(c, c.T)
