@@ -19,6 +19,7 @@
 // Operand digits live in global memory pre-tiled in the tensor core's K-major
 // "core matrix" layout (tiles of TH rows x 64 bytes: four 16-byte K chunks,
 // each TH rows x 16 B), so each stage is a handful of 1-D bulk copies.
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <vector>
@@ -102,6 +103,7 @@ struct OzSmem {
     int bexp[OZ_BN];       // column exponents of the tile
     double bscale[OZ_BN];  // 2^bexp (0 for padding columns) while every |bexp| <= 511
     int bwide;             // some column exponent outside [-511, 511]
+    int last;              // K-split tail tile: this CTA sums the partials
     unsigned tmem;
 };
 
@@ -212,6 +214,9 @@ __device__ __forceinline__ void oz_commit(unsigned long long* bar) {
 }
 
 constexpr int kOzNoColumn = 1 << 30;  // padding column of the tile
+// K-split of the last partial wave: more chunks shorten it but lengthen the
+// summing of the partial tiles that follows
+constexpr int kOzMaxTailSplit = 8;
 
 // v 2^e: one exact multiply while 2^e is a normal double; ldexp (out of line:
 // inlined, its range handling costs ~60 instructions per value) otherwise
@@ -248,12 +253,21 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
     OzSmem& sm = *reinterpret_cast<OzSmem*>(oz_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr int split = oz_pass_split(S);  // diagonals of pass 1: [0, split); pass 0: [split, S)
-    long long tm, tn;
-    oz_tile_of(p, p.tile_begin + blockIdx.x, &tm, &tn);
-    const long long ksteps = p.kpad / OZ_SK;
+    long long rel = blockIdx.x, tm, tn;  // tile index inside this launch
+    int chunk = 0;
+    const bool tail = p.tail_split > 1 && rel >= p.tail_from;
+    if (tail) {  // one K range of a tile of the last partial wave
+        const long long q = rel - p.tail_from;
+        rel = p.tail_from + q / p.tail_split;
+        chunk = static_cast<int>(q % p.tail_split);
+    }
+    oz_tile_of(p, p.tile_begin + rel, &tm, &tn);
+    const long long ktiles = p.kpad / OZ_BK;
+    const long long kb = tail ? chunk * ktiles / p.tail_split : 0;
+    const long long ksteps = (tail ? (chunk + 1) * ktiles / p.tail_split : ktiles) - kb;  // OZ_SK == OZ_BK
     const long long tile_bytes = OZ_BM * OZ_BK;  // one 128-row x 64-byte tile of the global layout
-    const int8_t* abase = p.a + tm * (p.kpad / OZ_BK) * tile_bytes;
-    const int8_t* bbase = p.b + tn * (p.kpad / OZ_BK) * tile_bytes;
+    const int8_t* abase = p.a + (tm * ktiles + kb) * tile_bytes;
+    const int8_t* bbase = p.b + (tn * ktiles + kb) * tile_bytes;
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&sm.tmem)));
@@ -422,8 +436,52 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
         // the fused consumers of the tile (plain store, Hadamard + reductions), as in the DMMA kernel
         auto sync128 = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
         sync128();
-        epi::apply<128>(p.epis, p.m, p.n, p.accumulate, sm.u.tile, tm * OZ_BM, tn * OZ_BN, tm, tn,
-                        p.symmetric && tm != tn, static_cast<long long>(blockIdx.x), sm.red, tid, sync128);
+        bool apply = true;
+        if (tail) {  // partial tile out; the last of the tile's chunks sums them in chunk order
+            const long long t = rel - p.tail_from;
+            double* part = p.tail_part + (t * p.tail_split + chunk) * (OZ_BM * OZ_BN);
+            for (int i = tid; i < OZ_BM * OZ_BN; i += 128) part[i] = sm.u.tile[(i >> 7) * epi::TP + (i & 127)];
+            __threadfence();
+            sync128();
+            if (tid == 0) {
+                const unsigned done_before = atomicAdd(&p.tail_count[t], 1u);
+                sm.last = done_before == static_cast<unsigned>(p.tail_split - 1);
+            }
+            sync128();
+            apply = sm.last;
+            if (apply) {
+                __threadfence();
+                // 16-byte loads, 4 x kOzMaxTailSplit of them in flight per thread
+                const double2* p0 = reinterpret_cast<const double2*>(p.tail_part + t * p.tail_split * (OZ_BM * OZ_BN));
+                constexpr int H = OZ_BM * OZ_BN / 2;  // double2 per partial tile
+#pragma unroll 1
+                for (int i0 = tid; i0 < H; i0 += 4 * 128) {
+                    double2 acc[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) acc[u] = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int c = 0; c < kOzMaxTailSplit; ++c)
+                        if (c < p.tail_split)
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const double2 v = __ldcg(p0 + c * H + i0 + u * 128);
+                                acc[u].x += v.x;
+                                acc[u].y += v.y;
+                            }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int i = 2 * (i0 + u * 128);
+                        sm.u.tile[(i >> 7) * epi::TP + (i & 127)] = acc[u].x;
+                        sm.u.tile[((i + 1) >> 7) * epi::TP + ((i + 1) & 127)] = acc[u].y;
+                    }
+                }
+                if (tid == 0) p.tail_count[t] = 0;  // reusable counters
+                sync128();
+            }
+        }
+        if (apply)
+            epi::apply<128>(p.epis, p.m, p.n, p.accumulate, sm.u.tile, tm * OZ_BM, tn * OZ_BN, tm, tn,
+                            p.symmetric && tm != tn, rel, sm.red, tid, sync128);
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -644,12 +702,39 @@ int launch_ozaki_gemm(const OzakiArgs& in, cudaStream_t s) {
     const long long total = ozaki_tile_count(p);
     const long long tiles = p.tile_count < 0 ? total - p.tile_begin : p.tile_count;
     if (tiles <= 0) return 0;
+    // one CTA per SM: a last wave at most half full runs its tiles split along K
+    // over the SMs the full waves leave idle (C2: 2080 tiles = 14 x 148 + 8)
+    const long long sms = static_cast<long long>(ozaki_work_entries() / (OZ_BM * OZ_BN)) - 8;
+    const long long rem = tiles % sms, ktiles = p.kpad / OZ_BK;
+    long long grid = tiles;
+    p.tail_split = 1;
+    if (rem > 0 && 2 * rem <= sms) {
+        const long long split = std::min({sms / rem, ktiles / 4, static_cast<long long>(kOzMaxTailSplit)});
+        if (split >= 2) {
+            const std::size_t part = static_cast<std::size_t>(rem * split) * OZ_BM * OZ_BN * sizeof(double);
+            if (cudaMallocAsync(reinterpret_cast<void**>(&p.tail_part), part, s) == cudaSuccess &&
+                cudaMallocAsync(reinterpret_cast<void**>(&p.tail_count), sizeof(unsigned) * rem, s) == cudaSuccess) {
+                cudaMemsetAsync(p.tail_count, 0, sizeof(unsigned) * rem, s);
+                p.tail_split = static_cast<int>(split);
+                p.tail_from = tiles - rem;
+                grid = p.tail_from + rem * split;
+            } else {
+                cudaGetLastError();
+                if (p.tail_part) cudaFreeAsync(p.tail_part, s);
+                p.tail_part = nullptr;
+            }
+        }
+    }
     switch (p.slices) {
-        case 4: launch_oz<4>(p, tiles, s); break;
-        case 5: launch_oz<5>(p, tiles, s); break;
-        case 6: launch_oz<6>(p, tiles, s); break;
-        case 7: launch_oz<7>(p, tiles, s); break;
+        case 4: launch_oz<4>(p, grid, s); break;
+        case 5: launch_oz<5>(p, grid, s); break;
+        case 6: launch_oz<6>(p, grid, s); break;
+        case 7: launch_oz<7>(p, grid, s); break;
         default: return -1;
+    }
+    if (p.tail_split > 1) {
+        cudaFreeAsync(p.tail_part, s);
+        cudaFreeAsync(p.tail_count, s);
     }
     return 1 + launch_epilogue_finalize(p.m, p.n, p.epis, tiles, p.accumulate, s);
 }

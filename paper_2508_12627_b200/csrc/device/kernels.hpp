@@ -189,6 +189,13 @@ struct OzakiArgs {
     long long tile_count = -1;   // -1: to the end of the tile list
     int prefetch = 0;            // k-tiles ahead the producer warms L2 (set by launch_ozaki_gemm)
     double* work = nullptr;      // 128 x 128 doubles per SM (ozaki_work_entries): the high-diagonal partial
+    // last partial wave split along K (set by launch_ozaki_gemm): launch-relative
+    // tiles >= tail_from run as tail_split CTAs each over a K range; the last
+    // one to finish sums the partial tiles (in chunk order) and runs the epilogues
+    long long tail_from = 0;
+    int tail_split = 1;
+    double* tail_part = nullptr;
+    unsigned* tail_count = nullptr;
     EpiSet epis;                 // fused consumers of the product tile (a plain store is one of them)
 };
 std::size_t ozaki_slice_bytes(long long rows, long long k, int tile_rows);
