@@ -85,7 +85,11 @@ __global__ void __launch_bounds__(256) pair_sym_blocked(const double* __restrict
                                                         int dc, double scale, double* __restrict__ out) {
     const int ti = blockIdx.y, tj = blockIdx.x;
     if (ti > tj) return;
-    __shared__ double xi[kBlkDim][kBlkTile + 1], xj[kBlkDim][kBlkTile + 1];  // coordinate-major
+    // coordinate-major point blocks; reused afterwards as the transposed 64 x 64 tile
+    __shared__ double buf[2 * kBlkDim * (kBlkTile + 1)];
+    static_assert(2 * kBlkDim >= kBlkTile, "the transposed tile fits the point blocks");
+    auto xi = reinterpret_cast<double(*)[kBlkTile + 1]>(buf);
+    auto xj = reinterpret_cast<double(*)[kBlkTile + 1]>(buf + kBlkDim * (kBlkTile + 1));
     const long long i0 = static_cast<long long>(ti) * kBlkTile, j0 = static_cast<long long>(tj) * kBlkTile;
     const int tid = threadIdx.x;
     for (int e = tid; e < kBlkTile * dc; e += 256) {
@@ -132,17 +136,25 @@ __global__ void __launch_bounds__(256) pair_sym_blocked(const double* __restrict
         }
     }
     if (ti == tj) return;
+    if (full) {  // the mirrored block through shared memory: a warp writes 512 contiguous bytes of a row
+        __syncthreads();  // every thread is done with the point blocks
+        auto tr = reinterpret_cast<double(*)[kBlkTile + 1]>(buf);  // tr[j][i]
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-        if (full) {
-            double2* o = reinterpret_cast<double2*>(out + (jb + b) * n + ib);
-            o[0] = make_double2(s[0][b], s[1][b]);
-            o[1] = make_double2(s[2][b], s[3][b]);
-        } else if (jb + b < n) {
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) tr[tx * 4 + b][ty * 4 + a] = s[a][b];
+        __syncthreads();
+        for (int e = tid; e < kBlkTile * kBlkTile / 2; e += 256) {
+            const int j = e / (kBlkTile / 2), i = 2 * (e % (kBlkTile / 2));
+            *reinterpret_cast<double2*>(out + (j0 + j) * n + i0 + i) = make_double2(tr[j][i], tr[j][i + 1]);
+        }
+        return;
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+        if (jb + b < n)
             for (int a = 0; a < 4; ++a)
                 if (ib + a < n) out[(jb + b) * n + ib + a] = s[a][b];
-        }
-    }
 }
 
 // Euclidean distances over columns [c0, c0 + dc) (fallback for wide samples).
