@@ -57,6 +57,44 @@ __device__ __forceinline__ void apply(const EpiSet& epis, long long rows, long l
                             o[r] = accumulate ? o[r] + v : v;
                         }
                 }
+        } else if (d.mode == kEpiSumAll) {
+            // a warp per line of the tile, lanes along it (columns when the first weight is
+            // row-major, else rows, so weight loads coalesce); per-line weight bases hoisted
+            double s = 0.0;
+            auto lines = [&](bool transposed) {  // transposed: the mirror tile, weights at (C, R)
+                for (int l = warp; l < BM; l += NT / 32) {
+                    // line l: a tile row (cfast) or a tile column; position q along it
+                    const double* base[kMaxEpiW];
+                    long long step[kMaxEpiW];
+                    const long long L = (cfast ? r0 : c0) + l;
+                    if (L >= (cfast ? rows : cols)) break;
+                    for (int f = 0; f < d.nw; ++f) {
+                        // weight index (R, C) or, mirrored, (C, R)
+                        const long long sl = transposed ? (cfast ? d.wc[f] : d.wr[f]) : (cfast ? d.wr[f] : d.wc[f]);
+                        const long long sq = transposed ? (cfast ? d.wr[f] : d.wc[f]) : (cfast ? d.wc[f] : d.wr[f]);
+                        base[f] = d.wptr[f] + L * sl + (cfast ? c0 : r0) * sq;
+                        step[f] = sq;
+                    }
+                    const long long qn = (cfast ? cols - c0 : rows - r0) < BN ? (cfast ? cols - c0 : rows - r0) : BN;
+                    for (int q = lane; q < qn; q += 32) {
+                        const int r = cfast ? l : q, c = cfast ? q : l;
+                        double w = P(tile[r * TP + c]);
+                        for (int f = 0; f < d.nw; ++f) w *= __ldg(base[f] + q * step[f]);
+                        s += w;
+                    }
+                }
+            };
+            lines(false);
+            if (mirror) lines(true);
+            s = warp_sum(s);
+            if (lane == 0) red[warp] = s;
+            sync();
+            if (tid == 0) {
+                double tot = 0.0;
+                for (int w = 0; w < NT / 32; ++w) tot += red[w];
+                d.partial[slot] = tot;
+            }
+            sync();
         } else if (d.mode == kEpiStore || d.mode == kEpiSumAll) {
             double s = 0.0;
             for (int i = tid; i < BM * BN; i += NT) {
