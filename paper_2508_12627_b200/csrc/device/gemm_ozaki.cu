@@ -191,16 +191,15 @@ __device__ __forceinline__ void oz_issue_stage(unsigned tmem, unsigned long long
     }
 }
 
-// Pass 1 stages only `split` slices, so its ring reuses the slot array as
-// OZ_STAGES x (kOzMaxSlices / split) smaller stages: stage q starts at slot
-// oz_p1_slot(q). Deeper lookahead where pass 1 has the fewest MMAs per byte.
-__host__ __device__ constexpr int oz_p1_groups(int split) { return kOzMaxSlices / split; }
+// Pass 1 stages only `split` slices, so its ring reuses the flat slot array
+// (OZ_STAGES x kOzMaxSlices slots per operand) as OZ_STAGES x kOzMaxSlices /
+// split smaller stages: stage q starts at slot q * split. Deeper lookahead
+// where pass 1 has the fewest MMAs per byte (measured: split 3 of S = 6 beats
+// 2 and 4).
 __host__ __device__ constexpr int oz_p1_stages(int split) {
-    return OZ_STAGES * oz_p1_groups(split) < 8 ? OZ_STAGES * oz_p1_groups(split) : 8;
+    return OZ_STAGES * kOzMaxSlices / split < 8 ? OZ_STAGES * kOzMaxSlices / split : 8;
 }
-__host__ __device__ constexpr int oz_p1_slot(int split, int q) {
-    return (q / oz_p1_groups(split)) * kOzMaxSlices + (q % oz_p1_groups(split)) * split;
-}
+__host__ __device__ constexpr int oz_p1_slot(int split, int q) { return q * split; }
 template <int S, int SPLIT, int Q = 0>
 __device__ __forceinline__ void oz_issue_p1(int q, unsigned tmem, unsigned long long desc0, unsigned idesc, bool first) {
     if (q == Q) oz_issue_stage<S, 0, SPLIT, oz_p1_slot(SPLIT, Q)>(tmem, desc0, idesc, first);
