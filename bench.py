@@ -326,6 +326,8 @@ def main():
                 e1.record()
                 torch.cuda.synchronize()
                 ms += e0.elapsed_time(e1)
+                if os.environ.get("BENCH_STEP_TIMES"):
+                    print(f"step {e0.elapsed_time(e1):.3f} ms", file=sys.stderr)
         else:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
