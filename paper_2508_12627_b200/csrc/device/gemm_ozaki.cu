@@ -35,7 +35,8 @@ constexpr int OZ_BM = 128, OZ_BN = 128;   // output tile
 constexpr int OZ_BK = 64;                  // K bytes per tile of the global digit layout
 constexpr int OZ_SK = 64;                  // K bytes per pipeline stage (two MMA k-steps)
 constexpr int OZ_STAGES = 2;
-constexpr int OZ_THREADS = 192;            // warps 0-3 epilogue, 4 producer, 5 MMA issuer
+constexpr int OZ_THREADS = 320;            // warps 0-3 and 6-9 epilogue, 4 producer, 5 MMA issuer
+constexpr int OZ_EPI = 256;                // epilogue threads: two per tile row (TMEM lane), 64 columns each
 constexpr int OZ_TILE_STAGE = OZ_BM * OZ_SK;  // 8 KiB per operand slice per stage
 
 __device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
@@ -99,7 +100,7 @@ struct OzSmem {
     } u;
     unsigned long long full[OZ_STAGES], empty[OZ_STAGES], done[2], drained;
     unsigned long long full1[8], empty1[8];  // pass 1's deeper ring (oz_p1_stages)
-    double red[4];
+    double red[OZ_EPI / 32];
     int bexp[OZ_BN];       // column exponents of the tile
     double bscale[OZ_BN];  // 2^bexp (0 for padding columns) while every |bexp| <= 511
     int bwide;             // some column exponent outside [-511, 511]
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
         }
         bar_init(&sm.done[0], 1);
         bar_init(&sm.done[1], 1);
-        bar_init(&sm.drained, 4);
+        bar_init(&sm.drained, OZ_EPI / 32);
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -362,13 +363,21 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
             oz_commit(&sm.empty1[q]);
         }
         oz_commit(&sm.done[1]);
-    } else if (warp < 4) {  // epilogue warps: thread = one row of the tile (TMEM lane)
-        const int rt = warp * 32 + lane;  // row inside the tile
+    } else if (warp < 4 || warp >= 6) {  // epilogue warps: thread = one row of the tile (TMEM lane), half its columns
+        // a warp reaches only the TMEM lanes 32 (warp % 4) .. +31: warps 0-3 take columns 0-63 of
+        // their lanes, warps 6-9 (lane quarters 2, 3, 0, 1) columns 64-127
+        const int quarter = warp & 3, half = warp >= 6 ? 1 : 0;
+        const int et = half * 128 + quarter * 32 + lane;  // epilogue thread index, warp-aligned
+        const int rt = quarter * 32 + lane;               // row inside the tile
+        const int cb = half * (OZ_BN / 2);                // first column of this thread's half
         const long long row = tm * OZ_BM + rt;
         const bool row_ok = row < p.m;
-        if (rt == 0) sm.bwide = 0;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (rt < OZ_BN) {
+        auto sync_epi = [] { asm volatile("bar.sync 1, 256;" ::: "memory"); };
+        static_assert(OZ_EPI == 256, "named barrier count");
+        if (et == 0) sm.bwide = 0;
+        sync_epi();
+        if (et < OZ_BN) {
+            const int rt = et;
             const long long col = tn * OZ_BN + rt;
             const int eb = col < p.n ? p.b_exp[col] : kOzNoColumn;
             sm.bexp[rt] = eb;
@@ -376,7 +385,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
             sm.bscale[rt] = (pad || !narrow) ? 0.0 : __longlong_as_double(static_cast<long long>(eb + 1023) << 52);
             if (!pad && !narrow) sm.bwide = 1;
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        sync_epi();
         const int ea = row_ok ? p.a_exp[row] : 0;
         const bool narrow = !sm.bwide && ea >= -511 && ea <= 511;
         const double sa = row_ok ? __longlong_as_double(static_cast<long long>(ea + 1023) << 52) : 0.0;
@@ -386,12 +395,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         double* work = p.work + static_cast<long long>(smid) * (OZ_BM * OZ_BN) + rt;
-        const unsigned lane_base = tmem + (static_cast<unsigned>(warp * 32) << 16);
+        const unsigned lane_base = tmem + (static_cast<unsigned>(quarter * 32) << 16);
         if constexpr (split < S) {  // pass 0: high diagonals into the scratch
             bar_wait(&sm.done[0], 0);
             asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll 1
-            for (int c0 = 0; c0 < OZ_BN; c0 += 16) {
+            for (int c0 = cb; c0 < cb + OZ_BN / 2; c0 += 16) {
                 double v[16];
                 oz_drain<split, S>(lane_base, c0, v, false);
 #pragma unroll
@@ -406,19 +415,19 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
         double h0[16], h1[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-            h0[j] = split < S ? work[j * OZ_BM] : 0.0;
-            h1[j] = split < S ? work[(16 + j) * OZ_BM] : 0.0;
+            h0[j] = split < S ? work[(cb + j) * OZ_BM] : 0.0;
+            h1[j] = split < S ? work[(cb + 16 + j) * OZ_BM] : 0.0;
         }
         bar_wait(&sm.done[1], 0);
         asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll 1
-        for (int c0 = 0; c0 < OZ_BN; c0 += 16) {
+        for (int c0 = cb; c0 < cb + OZ_BN / 2; c0 += 16) {
             double v[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
                 v[j] = h0[j];
                 h0[j] = h1[j];
-                if (c0 + 32 < OZ_BN) h1[j] = split < S ? work[(c0 + 32 + j) * OZ_BM] : 0.0;
+                if (c0 + 32 < cb + OZ_BN / 2) h1[j] = split < S ? work[(c0 + 32 + j) * OZ_BM] : 0.0;
             }
             oz_drain<0, split>(lane_base, c0, v, true);
             // the product tile in shared memory (every MMA has completed: the ring is free);
@@ -433,20 +442,19 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
                 }
         }
         // the fused consumers of the tile (plain store, Hadamard + reductions), as in the DMMA kernel
-        auto sync128 = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
-        sync128();
+        sync_epi();
         bool apply = true;
         if (tail) {  // partial tile out; the last of the tile's chunks sums them in chunk order
             const long long t = rel - p.tail_from;
             double* part = p.tail_part + (t * p.tail_split + chunk) * (OZ_BM * OZ_BN);
-            for (int i = tid; i < OZ_BM * OZ_BN; i += 128) part[i] = sm.u.tile[(i >> 7) * epi::TP + (i & 127)];
+            for (int i = et; i < OZ_BM * OZ_BN; i += OZ_EPI) part[i] = sm.u.tile[(i >> 7) * epi::TP + (i & 127)];
             __threadfence();
-            sync128();
-            if (tid == 0) {
+            sync_epi();
+            if (et == 0) {
                 const unsigned done_before = atomicAdd(&p.tail_count[t], 1u);
                 sm.last = done_before == static_cast<unsigned>(p.tail_split - 1);
             }
-            sync128();
+            sync_epi();
             apply = sm.last;
             if (apply) {
                 __threadfence();
@@ -454,7 +462,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
                 const double2* p0 = reinterpret_cast<const double2*>(p.tail_part + t * p.tail_split * (OZ_BM * OZ_BN));
                 constexpr int H = OZ_BM * OZ_BN / 2;  // double2 per partial tile
 #pragma unroll 1
-                for (int i0 = tid; i0 < H; i0 += 4 * 128) {
+                for (int i0 = et; i0 < H; i0 += 4 * OZ_EPI) {
                     double2 acc[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) acc[u] = make_double2(0.0, 0.0);
@@ -463,24 +471,24 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
                         if (c < p.tail_split)
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
-                                const double2 v = __ldcg(p0 + c * H + i0 + u * 128);
+                                const double2 v = __ldcg(p0 + c * H + i0 + u * OZ_EPI);
                                 acc[u].x += v.x;
                                 acc[u].y += v.y;
                             }
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        const int i = 2 * (i0 + u * 128);
+                        const int i = 2 * (i0 + u * OZ_EPI);
                         sm.u.tile[(i >> 7) * epi::TP + (i & 127)] = acc[u].x;
                         sm.u.tile[((i + 1) >> 7) * epi::TP + ((i + 1) & 127)] = acc[u].y;
                     }
                 }
-                if (tid == 0) p.tail_count[t] = 0;  // reusable counters
-                sync128();
+                if (et == 0) p.tail_count[t] = 0;  // reusable counters
+                sync_epi();
             }
         }
         if (apply)
-            epi::apply<128>(p.epis, p.m, p.n, p.accumulate, sm.u.tile, tm * OZ_BM, tn * OZ_BN, tm, tn,
-                            p.symmetric && tm != tn, rel, sm.red, tid, sync128);
+            epi::apply<OZ_EPI>(p.epis, p.m, p.n, p.accumulate, sm.u.tile, tm * OZ_BM, tn * OZ_BN, tm, tn,
+                               p.symmetric && tm != tn, rel, sm.red, et, sync_epi);
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
