@@ -116,10 +116,10 @@ struct OzSmem {
 // the passes the epilogue warps drain pass 0 into the output tile (FP64,
 // before the row/column exponents); pass 1 adds to it.
 // Tile order: square groups of OZ_GROUP x OZ_GROUP tiles (upper groups only
-// when symmetric), column-major inside a group, so one wave of CTAs streams
-// about OZ_GROUP A panels and OZ_GROUP B panels (~130 MB of digits at
-// K = 8192) that stay L2-resident across the wave.
-constexpr long long OZ_GROUP = 12;
+// when symmetric), column-major inside a group, so one wave of CTAs streams a
+// bounded set of A and B panels that mostly stay L2-resident across the wave
+// (measured on C2: 16 > 12, 20, 24 > 8, 32).
+constexpr long long OZ_GROUP = 16;
 __host__ __device__ __forceinline__ void oz_tile_of(const OzakiArgs& p, long long bid, long long* tm, long long* tn) {
     const long long T_m = p.mpad / OZ_BM, T_n = p.npad / OZ_BN;
     if (!p.symmetric) {  // groups of OZ_GROUP row tiles x all column tiles, column-major inside: O(1)
