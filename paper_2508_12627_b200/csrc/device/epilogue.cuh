@@ -1,7 +1,7 @@
 // The fused GEMM epilogues (EpiDesc / EpiSet, kernels.hpp) over a 128 x 128
 // FP64 product tile staged in shared memory (pitch TP), shared by the DMMA
 // TMA kernel (gemm_tma.cu, 256 threads) and the INT8-emulated kernel
-// (gemm_ozaki.cu, 128 threads). NT threads of the calling group take part;
+// (gemm_ozaki.cu, 256 epilogue threads). NT threads of the calling group take part;
 // `sync()` must synchronize exactly them. Fixed-order reductions: every
 // scalar partial is a warp tree then an in-order sum over the NT/32 warps.
 #pragma once
