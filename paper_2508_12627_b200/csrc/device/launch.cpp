@@ -228,11 +228,7 @@ long long flat_row_stride(const GemmSide& s, long long n) {
 
 bool Program::emulated_eligible(const GemmArgs& g) const {
     if (!config_.device.fp64_emulation) return false;
-    static const long long min_k = [] {  // USTATS_OZ_MIN_K: experiment with the threshold
-        const char* v = std::getenv("USTATS_OZ_MIN_K");
-        return v ? std::atoll(v) : kOzMinK;
-    }();
-    if (g.n > kOzMaxK || g.n < min_k || g.rows < kOzMinDim || g.cols < kOzMinDim) return false;
+    if (g.n > kOzMaxK || g.n < kOzMinK || g.rows < kOzMinDim || g.cols < kOzMinDim) return false;
     return flat_row_stride(g.a, n_) >= 0 && flat_row_stride(g.b, n_) >= 0;
 }
 
