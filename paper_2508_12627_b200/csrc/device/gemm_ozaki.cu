@@ -703,9 +703,10 @@ int launch_ozaki_gemm(const OzakiArgs& in, cudaStream_t s) {
     if (in.kpad % OZ_BK != 0) return -1;
     if (static_cast<long long>(in.slices) * in.kpad * 128 * 128 >= (1ll << 31)) return -1;  // int32 diagonals exact
     OzakiArgs p = in;
-    // warming L2 two k-tiles ahead pays while a wave's digit panels fit L2
-    // (C2, K = 8192: +2%); at K = 16384 it evicts them (C3: -9%)
-    p.prefetch = p.kpad <= 8192 ? 2 : 0;
+    // warming L2 k-tiles ahead of the bulk copies (p.prefetch > 0) paid with the
+    // 2-stage ring of the first version (C2 +2%); with pass 1 on its deeper ring
+    // it no longer does (C2 -0.5%, C3 -9%), so it is off
+    p.prefetch = 0;
     const long long total = ozaki_tile_count(p);
     const long long tiles = p.tile_count < 0 ? total - p.tile_begin : p.tile_count;
     if (tiles <= 0) return 0;
