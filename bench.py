@@ -403,8 +403,8 @@ def main():
                    "api": (f"u_statistic('{spec}', sample): components tensorized on the GPU"
                            if use_data else "u_terms(tensors)"),
                    "gemm": ("FP64 via Ozaki splitting on the INT8 tensor cores (6 balanced 8-bit digits per value, "
-                            "exact int32 digit products, FP64 assembly; ~1e-11 relative) where 1024 <= K <= 21000, "
-                            "else FP64 DMMA") if cfg.fp64_emulation else "FP64 DMMA (mma.sync f64)",
+                            "exact int32 digit products, FP64 assembly; ~1e-11 relative) where K >= 1024 (K > 21000 in K chunks "
+                            "summed in FP64; consumers of C^2 then stay on DMMA), else FP64 DMMA") if cfg.fp64_emulation else "FP64 DMMA (mma.sync f64)",
                    "parallelism": (f"row-sharded x{world}" if args.shard == "rows" else f"term-sharded x{world}")
                    if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (no flush needed)" if not flush

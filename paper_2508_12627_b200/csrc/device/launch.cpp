@@ -212,7 +212,8 @@ void Program::run_stream(const Op& op, double* out) {
 // FP64 emulation on the INT8 tensor cores (gemm_ozaki.cu) for large plain
 // products whose K keeps every digit diagonal exact in int32.
 constexpr int kOzSlices = 6;           // 8-bit balanced digits: 46 bits, 21 digit products
-constexpr long long kOzMaxK = 21000;    // 6 products of K * 128^2 per diagonal < 2^31
+constexpr long long kOzMaxK = 21000;    // 6 products of K * 128^2 per diagonal < 2^31; longer K runs
+                                        // as a sequence of K chunks accumulated in FP64 (all epilogues are linear in C)
 constexpr long long kOzMinDim = 1024;   // below, DMMA is as fast and needs no digit pass
 constexpr long long kOzMinK = 1024;     // shorter K: per-tile drains and digit passes outweigh the MMA savings
                                         // (C4's Khatri-Rao GEMMs, K = 1024: 297 -> 216 ms per evaluation)
@@ -228,15 +229,23 @@ long long flat_row_stride(const GemmSide& s, long long n) {
 
 bool Program::emulated_eligible(const GemmArgs& g) const {
     if (!config_.device.fp64_emulation) return false;
-    if (g.n > kOzMaxK || g.n < kOzMinK || g.rows < kOzMinDim || g.cols < kOzMinDim) return false;
+    if (g.n < kOzMinK || g.rows < kOzMinDim || g.cols < kOzMinDim) return false;
     return flat_row_stride(g.a, n_) >= 0 && flat_row_stride(g.b, n_) >= 0;
 }
 
 // Digits of both operands, the product (straight into a plain store's output,
 // else into scratch), then the fused epilogues over the stored product.
+// K beyond the exact int32 bound (C5: K = 65536) runs as equal K chunks of at
+// most kOzMaxK, each digitized on its own (per-chunk row exponents) and
+// accumulated into the outputs in chunk order: every epilogue is linear in C.
 int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
     cudaStream_t s = rt_->stream();
-    const std::size_t abytes = ozaki_slice_bytes(g.rows, g.n, 128), bbytes = ozaki_slice_bytes(g.cols, g.n, 128);
+    const long long nchunks = (g.n + kOzMaxK - 1) / kOzMaxK;  // fewest chunks: each costs a full epilogue pass
+    const long long kc = ((g.n + nchunks - 1) / nchunks + 63) / 64 * 64;  // chunk starts stay 512-byte aligned
+    if (nchunks > 1)  // a consumer of C^2 is not linear in C: the caller runs it on DMMA
+        for (int q = 0; q < set.count; ++q)
+            if (set.d[q].self_power != 1) return -1;
+    const std::size_t abytes = ozaki_slice_bytes(g.rows, kc, 128), bbytes = ozaki_slice_bytes(g.cols, kc, 128);
     // one set of digits when both operands are the same matrix view (A A^T)
     const long long ars = flat_row_stride(g.a, n_), brs = flat_row_stride(g.b, n_);
     const bool same = g.a.ptr[0] == g.b.ptr[0] && g.rows == g.cols && ars == brs && g.a.kstride[0] == g.b.kstride[0];
@@ -262,52 +271,58 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
         return -1;
     }
     const bool sym = g.symmetric_out && g.rows == g.cols;
-    OzakiArgs p;
-    p.a = da;
-    p.b = db;
-    p.a_slice = static_cast<long long>(abytes);
-    p.b_slice = static_cast<long long>(bbytes);
-    p.a_exp = ea;
-    p.b_exp = eb;
-    p.m = g.rows;
-    p.n = g.cols;
-    p.mpad = (g.rows + 127) / 128 * 128;
-    p.npad = (g.cols + 127) / 128 * 128;
-    p.kpad = (g.n + 63) / 64 * 64;
-    p.slices = kOzSlices;
-    p.symmetric = sym ? 1 : 0;
-    p.accumulate = g.accumulate;
-    p.epis = set;  // the same fused consumers (and partial slots) as the DMMA kernel's
-    if (g.tile_count >= 0) {  // row sharding: this rank's range of the (same) tile list
-        p.tile_begin = g.tile_begin;
-        p.tile_count = g.tile_count;
-    }
-    const long long tiles = p.tile_count >= 0 ? p.tile_count : ozaki_tile_count(p);
-    p.work = work;
-    // digits: all panels, or under row sharding only the panels this rank's tiles read
     int launched = 0;
-    if (g.tile_count >= 0) {
-        std::vector<int> pa, pb;
-        ozaki_tile_panels(p, &pa, &pb);
-        if (same) {
-            std::vector<int> u(pa);
-            u.insert(u.end(), pb.begin(), pb.end());
-            std::sort(u.begin(), u.end());
-            u.erase(std::unique(u.begin(), u.end()), u.end());
-            launched += ozaki_split(g.a.ptr[0], g.rows, g.n, ars, g.a.kstride[0], 128, kOzSlices, da, ea, s, &u);
-        } else {
-            launched += ozaki_split(g.a.ptr[0], g.rows, g.n, ars, g.a.kstride[0], 128, kOzSlices, da, ea, s, &pa);
-            launched += ozaki_split(g.b.ptr[0], g.cols, g.n, brs, g.b.kstride[0], 128, kOzSlices, db, eb, s, &pb);
+    long long tiles = 0;
+    for (long long k0 = 0; k0 < g.n; k0 += kc) {
+        const long long k = std::min(kc, g.n - k0);
+        const double* xa = g.a.ptr[0] + k0 * g.a.kstride[0];
+        const double* xb = g.b.ptr[0] + k0 * g.b.kstride[0];
+        OzakiArgs p;
+        p.a = da;
+        p.b = db;
+        p.a_slice = static_cast<long long>(abytes);
+        p.b_slice = static_cast<long long>(bbytes);
+        p.a_exp = ea;
+        p.b_exp = eb;
+        p.m = g.rows;
+        p.n = g.cols;
+        p.mpad = (g.rows + 127) / 128 * 128;
+        p.npad = (g.cols + 127) / 128 * 128;
+        p.kpad = (k + 63) / 64 * 64;
+        p.slices = kOzSlices;
+        p.symmetric = sym ? 1 : 0;
+        p.accumulate = k0 == 0 ? g.accumulate : 1;
+        p.epis = set;  // the same fused consumers (and partial slots) as the DMMA kernel's
+        if (g.tile_count >= 0) {  // row sharding: this rank's range of the (same) tile list
+            p.tile_begin = g.tile_begin;
+            p.tile_count = g.tile_count;
         }
-    } else {
-        launched += ozaki_split(g.a.ptr[0], g.rows, g.n, ars, g.a.kstride[0], 128, kOzSlices, da, ea, s);
-        if (!same) launched += ozaki_split(g.b.ptr[0], g.cols, g.n, brs, g.b.kstride[0], 128, kOzSlices, db, eb, s);
+        tiles = p.tile_count >= 0 ? p.tile_count : ozaki_tile_count(p);
+        p.work = work;
+        // digits: all panels, or under row sharding only the panels this rank's tiles read
+        if (g.tile_count >= 0) {
+            std::vector<int> pa, pb;
+            ozaki_tile_panels(p, &pa, &pb);
+            if (same) {
+                std::vector<int> u(pa);
+                u.insert(u.end(), pb.begin(), pb.end());
+                std::sort(u.begin(), u.end());
+                u.erase(std::unique(u.begin(), u.end()), u.end());
+                launched += ozaki_split(xa, g.rows, k, ars, g.a.kstride[0], 128, kOzSlices, da, ea, s, &u);
+            } else {
+                launched += ozaki_split(xa, g.rows, k, ars, g.a.kstride[0], 128, kOzSlices, da, ea, s, &pa);
+                launched += ozaki_split(xb, g.cols, k, brs, g.b.kstride[0], 128, kOzSlices, db, eb, s, &pb);
+            }
+        } else {
+            launched += ozaki_split(xa, g.rows, k, ars, g.a.kstride[0], 128, kOzSlices, da, ea, s);
+            if (!same) launched += ozaki_split(xb, g.cols, k, brs, g.b.kstride[0], 128, kOzSlices, db, eb, s);
+        }
+        const int l = launch_ozaki_gemm(p, s);
+        if (l < 0) fail(ErrorCode::InvalidArgument, "executor: emulated GEMM launch failed");
+        launched += l;
     }
-    const int l = launch_ozaki_gemm(p, s);
-    if (l < 0) fail(ErrorCode::InvalidArgument, "executor: emulated GEMM launch failed");
-    launched += l;
     if (stats_) {
-        const std::uint64_t tile = 128ull * 128ull * static_cast<std::uint64_t>(p.kpad);
+        const std::uint64_t tile = 128ull * 128ull * static_cast<std::uint64_t>((g.n + 63) / 64 * 64);
         const std::uint64_t products = static_cast<std::uint64_t>(kOzSlices * (kOzSlices + 1) / 2);
         stats_->int8_ops += 2 * static_cast<std::uint64_t>(tiles) * tile * products;
         const std::uint64_t full = static_cast<std::uint64_t>(g.rows) * static_cast<std::uint64_t>(g.cols) *

@@ -374,3 +374,20 @@ def test_emulated_gemm_row_sharding(engine, name, n, world):
     scale = np.max(np.abs(exact.v))
     assert np.max(np.abs(sharded.v - base.v)) <= 1e-12 * scale
     assert np.max(np.abs(base.v - exact.v)) <= TOL * scale
+
+
+@pytest.mark.parametrize("name,n", [("C5", 22528)])
+def test_emulated_gemm_k_chunks(engine, name, n):
+    # K = n beyond the exact int32 bound of the digit products (21000): the
+    # emulated GEMM runs as K chunks accumulated in FP64 (C5's chain GEMMs
+    # have linear consumers only; C2/C3's C^2 consumers stay on DMMA); within
+    # the north-star tolerance of the DMMA path, per V-term
+    from paper_2508_12627_b200.workloads import generate
+    factors, sig, m, _ = generate(name, n)
+    base = engine.u_terms(factors, sig, m)
+    assert base.stats["int8_tensor_ops"] > 0
+    exact = engine.u_terms(factors, sig, m, engine.Config(fp64_emulation=False))
+    assert exact.stats["int8_tensor_ops"] == 0
+    scale = np.max(np.abs(exact.v))
+    assert np.max(np.abs(base.v - exact.v)) <= TOL * scale
+    assert abs(base.value - exact.value) <= TOL * scale
