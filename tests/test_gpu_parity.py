@@ -376,12 +376,13 @@ def test_emulated_gemm_row_sharding(engine, name, n, world):
     assert np.max(np.abs(base.v - exact.v)) <= TOL * scale
 
 
-@pytest.mark.parametrize("name,n", [("C5", 22528)])
+@pytest.mark.parametrize("name,n", [("C5", 22528), ("C5", 21056)])
 def test_emulated_gemm_k_chunks(engine, name, n):
     # K = n beyond the exact int32 bound of the digit products (21000): the
     # emulated GEMM runs as K chunks accumulated in FP64 (C5's chain GEMMs
     # have linear consumers only; C2/C3's C^2 consumers stay on DMMA); within
-    # the north-star tolerance of the DMMA path, per V-term
+    # the north-star tolerance of the DMMA path, per V-term. n = 21056: a
+    # last chunk one 64-wide K step shorter than the first (its own digit layout)
     from paper_2508_12627_b200.workloads import generate
     factors, sig, m, _ = generate(name, n)
     base = engine.u_terms(factors, sig, m)
