@@ -392,3 +392,16 @@ def test_emulated_gemm_k_chunks(engine, name, n):
     scale = np.max(np.abs(exact.v))
     assert np.max(np.abs(base.v - exact.v)) <= TOL * scale
     assert abs(base.value - exact.value) <= TOL * scale
+
+
+def test_emulated_gemm_k_chunks_row_sharded(engine):
+    # the multi-GPU decomposition of C5 (row sharding: each rank a range of every
+    # GEMM's tile list, digitizing only its panels, per K chunk), on virtual
+    # ranks in lockstep: equal to the unsharded K-chunked evaluation
+    from paper_2508_12627_b200.workloads import generate
+    factors, sig, m, _ = generate("C5", 21056)
+    base = engine.u_terms(factors, sig, m)
+    sharded = engine.u_terms(factors, sig, m, engine.Config(shard_rows=True, emulate_world=3))
+    assert sharded.stats["int8_tensor_ops"] > 0
+    scale = np.max(np.abs(base.v))
+    assert np.max(np.abs(sharded.v - base.v)) <= 1e-12 * scale
