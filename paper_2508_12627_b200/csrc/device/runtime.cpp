@@ -99,7 +99,17 @@ Buf Runtime::allocate(int order, long long n) {
     b->rt = this;
     void* p = nullptr;
     const std::size_t bytes = std::max<std::uint64_t>(b->entries(), 1) * sizeof(double);
-    const cudaError_t e = cudaMallocAsync(&p, bytes, cur_);
+    cudaError_t e = cudaMallocAsync(&p, bytes, cur_);
+    if (e == cudaErrorMemoryAllocation) {
+        // the pool keeps freed blocks (release threshold = inf); a large request
+        // that no freed block fits (e.g. after the emulated GEMM's digit
+        // scratch) needs them handed back first: drain, trim, retry once
+        cudaGetLastError();
+        cudaDeviceSynchronize();
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device_) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+        e = cudaMallocAsync(&p, bytes, cur_);
+    }
     if (e != cudaSuccess || std::getenv("USTATS_SCHED_DEBUG")) {
         std::size_t fr = 0, tot = 0;
         cudaMemGetInfo(&fr, &tot);
