@@ -1,23 +1,28 @@
 #!/usr/bin/env python
 """Exact U-statistic throughput on B200 (BASELINE.json metric: evals/s and % of
-the FP64 tensor-core / HBM roofline).
+the FP64 tensor-core / HBM roofline at 1/2/4/8 B200).
 
-One step = one exact U-statistic evaluation of the workload (all sparsified
-partition-lattice V-terms contracted on the GPU, combined on the host in the
-reference's order). Default workload: BASELINE.json configs[1] (C2, m=4 cycle,
-n=8192), the largest single-GPU config the metric is quoted on.
+One step = one exact U-statistic evaluation of the workload (device
+tensorization of the components from the raw sample, every sparsified
+partition-lattice V-term contracted on the GPU, the per-term values combined
+on the host in the reference's order). Default workload: BASELINE.json
+configs[4] (C5, m=7 HOIF chain, n=65536, a 34 GB factor): the config the
+metric is quoted on at 1/2/4/8 GPUs; it fits one B200 (`--config C1..C4` for
+the others).
 
-  value  inputs resident in HBM (device pointers through the C-ABI); each step
-         still copies + sparsifies the factor on device, plans, contracts and
-         reads the per-term values back
-  e2e    the same call with HOST (pinned) buffers: H2D of the factor matrix
-         and D2H of the terms inside every timed step
+  value  sample resident in HBM (device pointer through the C-ABI)
+  e2e    the same public call with the sample in pinned HOST memory: its H2D
+         and the D2H of the terms inside every timed step
 
 `--impl reference` times the reference's own CPU implementation
-(oracle/_ref, compiled from /root/reference sources) on this host's cores.
+(oracle/_ref, compiled from /root/reference sources) on this host's cores:
+full size where that finishes in the run's time budget (C1, C2; C3 with few
+steps), else a bounded sample per step extrapolated to the config's n with
+the reference's exact multiply-add polynomial (C4, C5: the full-size CPU run
+needs ~1e6 s and >= 0.4 TB of RAM), labelled as such.
 
-N>1 (torchrun): V-terms are LPT-sharded over ranks (no data-path exchange);
-per-term values meet in one NCCL all-reduce, then the reference combination.
+N>1 (torchrun): V-terms are LPT-sharded over ranks and shared GEMMs are split
+into row panels; per-term values meet in one NCCL all-reduce.
 """
 from __future__ import annotations
 
@@ -39,7 +44,6 @@ sys.path.insert(0, str(ROOT))
 FP64_PEAK_TFLOPS = 37.17      # measured: mma.sync f64 issue-rate probe, profiles/r01_fp64_peak_probe.log
 FP64_CUBLAS_TFLOPS = 36.17    # measured: cuBLAS DGEMM 16384^3 on this pool (same log)
 INT8_PEAK_TOPS = 4568.7       # measured: tcgen05.mma kind::i8 issue-rate probe, profiles/r01_int8_peak_probe.log
-CPU_SAMPLE_N = {"C1": 2000, "C2": 4096, "C3": 4096, "C4": 160, "C5": 1024}
 
 
 def measured_peaks() -> dict:
@@ -144,23 +148,59 @@ def reference_sample(name: str, n_sample: int, threads: int, repeats: int = 1, d
     return u, min(walls), stats
 
 
-def fitted_cpu_time(name, n, threads, data_api=True):
-    """Times the reference at two bounded sizes (n2/2, n2) and extrapolates to n
-    with the fitted power law T ~ n^p. Returns (t_full_est, detail dict)."""
-    n2 = min(CPU_SAMPLE_N[name], n)
-    if n2 == n:
-        _, t, st = reference_sample(name, n, threads, data_api=data_api)
-        return t, {"n": n, "wall": t, "exponent": None, "contract": st["contract_seconds"]}
-    n1 = max(CONFIG_MIN_N.get(name, 8), n2 // 2)
-    _, t1, _ = reference_sample(name, n1, threads, data_api=data_api)
-    _, t2, st = reference_sample(name, n2, threads, data_api=data_api)
-    p = float(np.log(t2 / t1) / np.log(n2 / n1)) if t1 > 0 and t2 > t1 else 3.0
-    return t2 * (n / n2) ** p, {"n1": n1, "t1": t1, "n": n2, "wall": t2, "exponent": p,
-                                "contract": st["contract_seconds"]}
+# Bounded reference sample per config: C1 and C2 run at full size; C3's full
+# size (~10 min per evaluation) only when the run's step count fits the budget;
+# C4 and C5 are infeasible at full size on any host (C4 ~1.5 h and ~300 GB of
+# concurrent n^3 buffers, C5 ~1e6 s and >= 0.4 TB), so they are timed at the
+# sample n and extrapolated with the reference's EXACT multiply-add polynomial
+# (C5 241 n^3 + 1534 n^2 + ..., C4 51 n^4 + ...).
+CPU_SAMPLE_N = {"C1": 2000, "C2": 4096, "C3": 4096, "C4": 192, "C5": 2048}
+FULL_FEASIBLE = {"C1", "C2", "C3"}
+REFERENCE_ARM_BUDGET_S = 1500.0
+_MADDS = {}
 
 
-CONFIG_MIN_N = {"C3": 256, "C5": 256}
-REFERENCE_ARM_BUDGET_S = 300.0
+def reference_madds(name, n):
+    """Exact reference-plan multiply-adds (ExecStats rules, einsum.cpp) at extent
+    n: the polynomial of degree <= m fitted EXACTLY (integer coefficients) to
+    the reference's own counts at small n."""
+    from paper_2508_12627_b200.workloads import CONFIGS
+    from oracle import ref as REF
+    w = CONFIGS[name]
+    if name not in _MADDS:
+        sig = [list(t) for t in w.signature]
+        xs = list(range(w.m + 2, 2 * w.m + 5))
+        ys = []
+        for x in xs:
+            rng = np.random.default_rng(0)
+            facs = [rng.uniform(0.5, 1.5, size=(x,) * len(t)) for t in sig]
+            _, st = REF.u_statistic(facs, sig, w.m, threads=1)
+            ys.append(st["multiply_adds"])
+        _MADDS[name] = np.round(np.polyfit(np.array(xs, float), np.array(ys, float), w.m))
+    return float(np.polyval(_MADDS[name], float(n)))
+
+
+def extrapolated_seconds(name, n, n_s, wall, stats):
+    """Reference time at n from a run at n_s: tensorize ~ n^2 (one callback per
+    entry per component), contraction ~ the exact multiply-add polynomial, the
+    rest (enumeration, planning) as measured."""
+    tz, tc = stats["tensorize_seconds"], stats["contract_seconds"]
+    rest = max(0.0, wall - tz - tc)
+    return tz * (n / n_s) ** 2 + tc * reference_madds(name, n) / reference_madds(name, n_s) + rest
+
+
+def reference_plan(name, n, threads, data_api, runs):
+    """Decides full size vs bounded sample for `runs` reference evaluations.
+    Returns (run_n, full, detail)."""
+    n_s = min(CPU_SAMPLE_N[name], n)
+    if n_s == n:
+        return n, True, {}
+    if name not in FULL_FEASIBLE:
+        return n_s, False, {}
+    _, t_s, st = reference_sample(name, n_s, threads, data_api=data_api)  # one probe predicts full size
+    est = extrapolated_seconds(name, n, n_s, t_s, st)
+    full = est * runs <= REFERENCE_ARM_BUDGET_S
+    return (n if full else n_s), full, {"probe_n": n_s, "probe_wall": t_s, "full_estimate_s": est}
 
 
 def run_reference_arm(args, name, world, rank):
@@ -174,22 +214,26 @@ def run_reference_arm(args, name, world, rank):
     w = CONFIGS[name]
     n = args.n or w.n
     threads = os.cpu_count() or 1
-    # warm-up = the two bounded probes that also predict the full-size time
     data_api = args.api == "data"
-    est, det = fitted_cpu_time(name, n, threads, data_api)
+    run_n, full, det = reference_plan(name, n, threads, data_api, args.steps + args.warmup)
+    for _ in range(args.warmup):
+        reference_sample(name, run_n, threads, data_api=data_api)
+    secs, walls = [], []
+    for _ in range(args.steps):
+        _, wall, st = reference_sample(name, run_n, threads, data_api=data_api)
+        walls.append(wall)
+        secs.append(wall if full else extrapolated_seconds(name, n, run_n, wall, st))
+    t_full = statistics.mean(secs)
     call = "u_statistic(kernel spec, sample) incl. its tensorize" if data_api else "u_statistic on tensor-backed components"
-    if est * args.steps <= REFERENCE_ARM_BUDGET_S or det.get("exponent") is None:
-        walls = [reference_sample(name, n, threads, data_api=data_api)[1] for _ in range(args.steps)]
-        t_full = statistics.mean(walls)
-        sample = (f"ustats::u_statistic (oracle/_ref: the unmodified reference sources), {call}, at full n={n}, "
-                  f"threads={threads}, mean wall {t_full:.3f}s over {len(walls)} runs (tensorize+sparsify+contract)")
+    if full:
+        sample = (f"ustats::u_statistic (oracle/_ref: the unmodified reference sources), {call}, at FULL n={n}, "
+                  f"threads={threads}, mean wall {t_full:.3f}s over {len(secs)} runs")
     else:
-        walls = [reference_sample(name, det["n"], threads, data_api=data_api)[1] for _ in range(args.steps)]
-        t_full = statistics.mean(walls) * (n / det["n"]) ** det["exponent"]
-        sample = (f"ustats::u_statistic (oracle/_ref), {call}, at n={det['n']}, threads={threads}, mean wall "
-                  f"{statistics.mean(walls):.3f}s over {len(walls)} runs; extrapolated to n={n} with the "
-                  f"power law fitted between n={det['n1']} and n={det['n']} (p={det['exponent']:.2f}); "
-                  f"full size would take ~{est:.0f}s per step")
+        sample = (f"EXTRAPOLATED: ustats::u_statistic (oracle/_ref), {call}, at n={run_n}, threads={threads}, "
+                  f"mean wall {statistics.mean(walls):.3f}s over {len(walls)} runs; each run scaled to n={n} "
+                  f"(tensorize x (n/{run_n})^2, contraction x madds({n})/madds({run_n}) = "
+                  f"{reference_madds(name, n):.4g}/{reference_madds(name, run_n):.4g}, the reference's exact "
+                  f"multiply-add polynomial)")
     value = 1.0 / t_full
     line = {
         "metric": "U-statistic exact evals/sec", "value": value, "unit": "evals/s", "impl": "reference",
@@ -197,31 +241,15 @@ def run_reference_arm(args, name, world, rank):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json construction)",
         "config": {"workload": name, "m": w.m, "n": n, "signature": [list(t) for t in w.signature]},
-        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "reference", "sample": sample},
+        "same_config": bool(full), "sample_n": run_n,
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "reference", "sample": sample,
+                         "extrapolated": not full},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if det:
+        line["probe"] = det
     print(json.dumps(line))
     return 0
-
-
-def reference_madds(name, n):
-    """Exact reference-plan multiply-adds (ExecStats rules) at extent n, from the
-    engine's host planner walk (no GPU): polynomial fitted exactly at small n."""
-    from paper_2508_12627_b200.workloads import CONFIGS
-    from oracle import ref as REF
-    w = CONFIGS[name]
-    sig = [list(t) for t in w.signature]
-    # madds(n) is a polynomial of degree <= m; fit on the reference at small n
-    xs = list(range(w.m + 2, 2 * w.m + 5))
-    ys = []
-    for x in xs:
-        rng = np.random.default_rng(0)
-        facs = [rng.uniform(0.5, 1.5, size=(x,) * len(t)) for t in sig]
-        _, st = REF.u_statistic(facs, sig, w.m, threads=1)
-        ys.append(st["multiply_adds"])
-    coef = np.polyfit(np.array(xs, float), np.array(ys, float), w.m)
-    coef = np.round(coef)
-    return float(np.polyval(coef, float(n)))
 
 
 def main():
@@ -230,10 +258,13 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--n", type=int, default=0, help="override the config's n (parity/debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-strict", action="store_true", help="skip the FP64-strict (DMMA-only) roofline leg")
+    ap.add_argument("--budget-s", type=float, default=1400.0,
+                    help="wall budget of the whole run: the e2e and FP64-strict legs shrink to fit it")
     ap.add_argument("--api", default="data", choices=["data", "tensors"],
                     help="data: u_statistic(spec, sample) with GPU tensorization (the binding's call); "
                          "tensors: pre-tensorized factors (us_u_terms)")
@@ -242,6 +273,7 @@ def main():
     args = ap.parse_args()
     world, rank, local = dist_env()
     name = args.config
+    t_begin = time.time()
 
     if args.impl == "reference":
         return run_reference_arm(args, name, world, rank)
@@ -262,6 +294,8 @@ def main():
     use_data = args.api == "data" and not (world > 1 and args.shard == "terms")
     cfg = us.Config(device=local, rank=rank, world_size=world, shard_rows=(world > 1 and args.shard == "rows"),
                     memory_cap_entries=max(2 ** 31, n * n + 1, n ** 3 + 1 if name == "C4" else 0))
+    # the reference needs memory_cap_entries raised past n^2 for C5 (tensor.cpp:9-23);
+    # SURVEY 8d prescribes the same for its CPU baseline
     if use_data:
         # the binding's public call: u_statistic(kernel spec, sample); the
         # components are tensorized on the GPU from the sample
@@ -352,12 +386,52 @@ def main():
         clocks.mark(t_start, time.time())
         prof = us.profile(enable=False, reset=True, device=local)
     e2e = None
+    step_s = ms_step * 1e-3
+    strict_s = 3.5 * step_s if (cfg.fp64_emulation and not args.no_strict) else 0.0  # DMMA ~3x slower
     if not args.no_e2e:
-        step(hfac, False)
-        e2e_ms, _ = timed(hfac, False, args.steps)
+        # e2e repeats the timed loop with host buffers; a long step (C5) runs
+        # fewer e2e steps so the whole bench stays inside --budget-s
+        left = args.budget_s - (time.time() - t_begin) - strict_s
+        e2e_steps = args.steps if left >= (args.steps + 1) * step_s else max(3, min(args.steps, int(left / step_s) - 1))
+        if step_s < 5.0:
+            step(hfac, False)  # warm the host-buffer path (pinned registration); a long step needs none
+        e2e_ms, _ = timed(hfac, False, e2e_steps)
         e2e = {"value": 1e3 / e2e_ms, "unit": "evals/s", "h2d_bytes_per_step": int(in_bytes),
                "d2h_bytes_per_step": 8 * int(r.terms) + (4 if use_data else 0), "ms_per_step": e2e_ms,
+               "steps": e2e_steps,
                "call": f"u_statistic('{spec}', pinned host sample)" if use_data else "us_u_terms(host tensors)"}
+    strict = None
+    if strict_s > 0 and world == 1 and time.time() - t_begin + strict_s < args.budget_s:
+        # FP64-strict leg: the same evaluation with every GEMM on the FP64 DMMA
+        # tensor cores (no INT8 emulation) -> the IEEE-FP64 roofline beside the emulated one
+        import dataclasses
+        scfg = dataclasses.replace(cfg, fp64_emulation=False)
+
+        def sstep():
+            if use_data:
+                return us.u_statistic(spec, dfac, config=scfg, with_stats=True)
+            rr = us.u_terms(dfac, sig, m, scfg)
+            return rr.value, rr.stats
+        nst = 1 if strict_s > 30 else max(1, min(args.steps, int(30 / max(strict_s, 1e-3))))
+        if strict_s <= 30:
+            sstep()  # plan + warm
+        us.profile(enable=True, reset=True, device=local)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(nst):
+            su, sst = sstep()
+        torch.cuda.synchronize()
+        s_wall = (time.perf_counter() - t0) / nst
+        sprof = us.profile(enable=False, reset=True, device=local)
+        s_gemm_ms = sprof["gemm_ms"] / nst
+        s_ach = 2.0 * sst["executed_gemm_macs"] / (s_gemm_ms * 1e-3) / 1e12 if s_gemm_ms > 0 else None
+        strict = {"value": 1.0 / s_wall, "unit": "evals/s", "steps": nst, "u": su,
+                  "u_minus_emulated_u": su - u_val,
+                  "roofline": {"bound": "tensor", "achieved": s_ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                               "frac": s_ach / FP64_PEAK_TFLOPS if s_ach else None,
+                               "kernel": "gemm_tma_kernel (TMA + DMMA.8x8x4, FP64 tensor pipe)",
+                               "kernel_ms_per_step": s_gemm_ms, "kernel_share_of_step": s_gemm_ms / (s_wall * 1e3)},
+                  "timing": "host wall per evaluation (plan cached when steps > 1), GEMM time from CUDA events"}
 
     st = r.stats
     gemm_ms = prof["gemm_ms"] / args.steps
@@ -402,9 +476,11 @@ def main():
         "config": {"workload": name, "m": m, "n": n, "signature": sig, "terms": int(r.terms),
                    "api": (f"u_statistic('{spec}', sample): components tensorized on the GPU"
                            if use_data else "u_terms(tensors)"),
-                   "gemm": ("FP64 via Ozaki splitting on the INT8 tensor cores (6 balanced 8-bit digits per value, "
-                            "exact int32 digit products, FP64 assembly; ~1e-11 relative) where K >= 1024 (K > 21000 in K chunks "
-                            "summed in FP64; consumers of C^2 then stay on DMMA), else FP64 DMMA") if cfg.fp64_emulation else "FP64 DMMA (mma.sync f64)",
+                   "gemm": ("FP64 via Ozaki splitting on the INT8 tensor cores (S balanced 8-bit digits per value, S "
+                            "from the error-bound guard: worst-case entry error <= that of the FP64 dot product, S=6 "
+                            "for K >= 1024; exact int32 digit products, FP64 assembly) where K >= 1024 (long K in "
+                            "chunks summed in FP64; consumers of C^2 then stay on DMMA), else FP64 DMMA")
+                   if cfg.fp64_emulation else "FP64 DMMA (mma.sync f64)",
                    "parallelism": (f"row-sharded x{world}" if args.shard == "rows" else f"term-sharded x{world}")
                    if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (no flush needed)" if not flush
@@ -415,11 +491,13 @@ def main():
         "clocks": clocks.summary(),
         "stats_per_step": {k: st[k] for k in ("multiply_adds", "executed_gemm_macs", "executed_stream_entries",
                                                "gemm_launches", "stream_launches", "shared_hits",
-                                               "emulated_gemm_macs", "int8_tensor_ops")},
+                                               "emulated_gemm_macs", "int8_tensor_ops", "oz_slices")},
         "stream_ms_per_step": stream_ms,
     }
     if e2e:
         line["e2e"] = e2e
+    if strict:
+        line["fp64_strict"] = strict
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(name, n, use_data)
     if rank == 0:
@@ -466,21 +544,26 @@ def ncu_traffic(name, kind):
 
 
 def cpu_baseline(name, n, data_api=True):
+    """The reference CPU path on this host, one bounded run (rank 0, N=1): full
+    size for C1, else the config's sample n extrapolated with the exact
+    multiply-add polynomial (as in the reference arm)."""
     from oracle import ref as REF
     if not REF.available():
         return {"value": None, "unit": "evals/s", "cores": 0, "kind": "reference",
                 "sample": "oracle/_ref not built on this host"}
     threads = os.cpu_count() or 1
-    est, det = fitted_cpu_time(name, n, threads, data_api)
-    if det.get("exponent") is None:
-        sample = f"ustats::u_statistic (oracle/_ref) at full n={n}, threads={threads}: {det['wall']:.3f}s wall"
-    else:
-        sample = (f"ustats::u_statistic (unmodified reference, oracle/_ref) on the "
-                  f"{'raw sample (its tensorize included)' if data_api else 'tensorized factors'}, threads={threads}: "
-                  f"{det['t1']:.3f}s at n={det['n1']}, {det['wall']:.3f}s at n={det['n']} "
-                  f"(contract {det['contract']:.3f}s); extrapolated to n={n} with the fitted power law "
-                  f"p={det['exponent']:.2f}")
-    return {"value": 1.0 / est, "unit": "evals/s", "cores": threads, "kind": "reference", "sample": sample}
+    n_s = min(CPU_SAMPLE_N[name], n)
+    _, wall, st = reference_sample(name, n_s, threads, data_api=data_api)
+    if n_s == n:
+        return {"value": 1.0 / wall, "unit": "evals/s", "cores": threads, "kind": "reference", "extrapolated": False,
+                "sample": f"ustats::u_statistic (oracle/_ref) at full n={n}, threads={threads}: {wall:.3f}s wall"}
+    est = extrapolated_seconds(name, n, n_s, wall, st)
+    return {"value": 1.0 / est, "unit": "evals/s", "cores": threads, "kind": "reference", "extrapolated": True,
+            "sample": (f"ustats::u_statistic (unmodified reference, oracle/_ref) on the "
+                       f"{'raw sample (its tensorize included)' if data_api else 'tensorized factors'}, "
+                       f"threads={threads}: {wall:.3f}s at n={n_s} (tensorize {st['tensorize_seconds']:.3f}s, "
+                       f"contract {st['contract_seconds']:.3f}s), extrapolated to n={n} with the exact "
+                       f"multiply-add polynomial (contract) and n^2 (tensorize): {est:.4g}s")}
 
 
 if __name__ == "__main__":

@@ -53,6 +53,10 @@ typedef struct us_config {
                                     bit7 exact DMMA only (no INT8 tensor-core emulation of
                                     large FP64 GEMMs); US_FLAGS_DEFAULT = 0xF */
     int32_t emulate_world;       /* row sharding over this many virtual ranks on one device (tests) */
+    uint64_t memory_budget_bytes; /* device bytes the memory-bounded schedule may plan for (0 = free memory) */
+    int32_t oz_slices;           /* emulated-GEMM digit slices (0 = error-bound guard; 4..7 forced) */
+    int32_t reserved0;
+    int64_t oz_max_k;            /* longest emulated K per pass (0 = 21000, the int32-exact bound) */
 } us_config;
 
 #define US_FLAGS_DEFAULT 0xF
@@ -74,6 +78,7 @@ typedef struct us_stats {
     uint64_t kernel_launches;       /* every kernel this call enqueued */
     uint64_t emulated_gemm_macs;    /* FP64 multiply-adds done on the INT8 tensor cores (Ozaki) */
     uint64_t int8_tensor_ops;       /* INT8 tensor-core operations those issued (2 per MAC) */
+    uint64_t oz_slices;             /* digit slices of the emulated GEMMs (error-bound guard; 0 = none ran) */
 } us_stats;
 
 US_API const char* us_version(void);

@@ -27,6 +27,10 @@ class UsConfig(C.Structure):
         ("world_size", i32),
         ("flags", i32),
         ("emulate_world", i32),
+        ("memory_budget_bytes", u64),
+        ("oz_slices", i32),
+        ("reserved0", i32),
+        ("oz_max_k", i64),
     ]
 
 
@@ -47,6 +51,7 @@ class UsStats(C.Structure):
         ("kernel_launches", u64),
         ("emulated_gemm_macs", u64),
         ("int8_tensor_ops", u64),
+        ("oz_slices", u64),
     ]
 
     def as_dict(self) -> dict:

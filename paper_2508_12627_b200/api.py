@@ -60,6 +60,9 @@ class Config:
     serial_launch: bool = False  # one CUDA stream (no GEMM / reduction overlap)
     fp64_emulation: bool = True  # large FP64 GEMMs on the INT8 tensor cores (Ozaki digits); False = DMMA only
     emulate_world: int = 0       # row sharding over virtual ranks on one device (tests)
+    memory_budget_bytes: int = 0  # device bytes the memory-bounded schedule may use (0 = free memory)
+    oz_slices: int = 0           # emulated-GEMM digit slices (0 = error-bound guard, 4..7 forced)
+    oz_max_k: int = 0            # longest emulated K per pass (0 = 21000); longer K runs in chunks
 
     def native(self) -> N.UsConfig:
         c = N.UsConfig()
@@ -79,6 +82,9 @@ class Config:
                   (32 if self.shard_rows else 0) | (64 if self.serial_launch else 0) | \
                   (0 if self.fp64_emulation else 128)
         c.emulate_world = self.emulate_world
+        c.memory_budget_bytes = self.memory_budget_bytes
+        c.oz_slices = self.oz_slices
+        c.oz_max_k = self.oz_max_k
         return c
 
 

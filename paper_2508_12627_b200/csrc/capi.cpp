@@ -65,6 +65,13 @@ ustats::Config to_config(const us_config* c) {
     cfg.device.serial_launch = c->flags & 64;
     cfg.device.fp64_emulation = !(c->flags & 128);
     cfg.device.emulate_world = c->emulate_world;
+    cfg.device.memory_budget_bytes = c->memory_budget_bytes;
+    if (c->oz_slices != 0 && (c->oz_slices < 4 || c->oz_slices > 7))
+        ustats::fail(ustats::ErrorCode::InvalidArgument, "oz_slices must be 0 (auto) or 4..7");
+    cfg.device.oz_slices = c->oz_slices;
+    if (c->oz_max_k < 0 || (c->oz_max_k > 0 && c->oz_max_k < 64))
+        ustats::fail(ustats::ErrorCode::InvalidArgument, "oz_max_k must be 0 (auto) or >= 64");
+    cfg.device.oz_max_k = c->oz_max_k;
     return cfg;
 }
 
@@ -120,6 +127,7 @@ void export_stats(const ustats::RunStats& rs, us_stats* s) {
     s->kernel_launches = 0;
     s->emulated_gemm_macs = 0;
     s->int8_tensor_ops = 0;
+    s->oz_slices = 0;
 }
 
 void export_dev(const ustats::dev::StatisticResult& r, int rank, us_stats* s) {
@@ -143,6 +151,7 @@ void export_dev(const ustats::dev::StatisticResult& r, int rank, us_stats* s) {
     s->kernel_launches = r.stats.kernel_launches;
     s->emulated_gemm_macs = r.stats.emulated_macs;
     s->int8_tensor_ops = r.stats.int8_ops;
+    s->oz_slices = r.stats.oz_slices;
 }
 
 ustats::dev::StatisticResult run_lattice(int32_t m, int32_t K, const int32_t* tuple_len,

@@ -50,6 +50,7 @@ struct DeviceBuffer {
     long long n = 1;
     bool symmetric = false;
     bool borrowed = false;
+    bool slab = false;  // from the runtime's slab cache (returned there, not freed)
     Runtime* rt = nullptr;
     // chunked upload in flight: rows [0, first) are usable once `second` completes
     std::vector<std::pair<long long, cudaEvent_t>> ready;
@@ -89,6 +90,21 @@ class Runtime {
     void release(double* p);
     void sync();
 
+    // Large buffers (>= kSlabMin: n^2 intermediates, Ozaki digit panels) come
+    // from a cache of exact-size slabs instead of the stream-ordered pool: a
+    // 32 GiB request then never fails on a pool fragmented by smaller blocks,
+    // and a program that repeats (the plan cache) reuses the same slabs. A
+    // returned slab carries the event of its release, which its next user's
+    // stream waits on. reclaim() hands every idle slab and the pool's unused
+    // blocks back to the driver (after a sync) when an allocation fails.
+    static constexpr std::size_t kSlabMin = std::size_t{1} << 30;
+    // slab (>= kSlabMin and slab_ok) or pool, retrying once after reclaim();
+    // MemoryCapExceeded when even that fails
+    void* raw_alloc(std::size_t bytes, bool slab_ok = true);
+    void raw_free(void* p, std::size_t bytes);     // stream-ordered on the current stream
+    void reclaim();
+    double idle_slab_bytes() const;
+
     // NCCL communicator for row sharding (libnccl resolved at run time, so
     // the library has no link-time NCCL dependency and shares the process's copy).
     void nccl_init(int rank, int world, const void* unique_id);
@@ -122,6 +138,14 @@ class Runtime {
     double free_bytes_ = 0;
     bool profiling_ = false;
     std::vector<cudaEvent_t> pool_;
+    struct Slab {
+        void* ptr = nullptr;
+        std::size_t bytes = 0;
+        cudaEvent_t freed = nullptr;
+    };
+    std::vector<Slab> idle_;
+    void* slab_get(std::size_t bytes);
+    void slab_put(void* p, std::size_t bytes);
     struct Mark {
         Kind kind;
         cudaEvent_t a, b;
@@ -144,7 +168,18 @@ struct DevStats {
     std::uint64_t int8_ops = 0;       // INT8 tensor-core ops those issued
     std::uint64_t fused_epilogues = 0;
     std::uint64_t symmetric_gemms = 0;
+    std::uint64_t oz_slices = 0;      // digit slices the last emulated GEMM used (0 = none ran)
 };
+
+// Emulated-GEMM plan of one product (launch.cpp): digit slices (error-bound
+// guard or Config.oz_slices), K chunking, and the digit scratch it needs.
+struct OzPlan {
+    int slices = 6;
+    long long nchunks = 1, kc = 0;
+    std::size_t a_bytes = 0, b_bytes = 0, scratch_bytes = 0;
+};
+int oz_guard_slices(long long K);
+OzPlan oz_plan(long long K, long long rows, long long cols, bool same_operand, const DeviceConfig& dc);
 
 // ------------------------------------------------------------------ Program
 struct View {
@@ -264,6 +299,7 @@ class Program {
     void fuse_sweeps();
     void run_sweep(const Op& op);
     bool emulated_eligible(const GemmArgs& g) const;
+    std::size_t op_scratch_bytes(const Op& op) const;
     int run_emulated(const GemmArgs& g, const EpiSet& set);
     std::pair<long long, long long> sweep_strides(const View& v, int row_id, int col_id) const;
     bool tma_plain(const View& v, const std::vector<int>& rows, int e) const;
@@ -287,6 +323,7 @@ class Program {
     std::vector<std::size_t> schedule_;  // execution order of live ops (memory-aware)
     int slice_rank_ = 0, slice_world_ = 1;  // row sharding: the slice launch() computes
     double sched_peak_ = 0;
+    bool sched_fits_ = true;
     double budget_ = 0;
     bool launch_ordered_ = false;
     void make_schedule(double budget_bytes);

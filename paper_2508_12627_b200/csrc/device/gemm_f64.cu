@@ -335,12 +335,7 @@ __global__ void gemm_finalize_vector(const double* partial, long long P, long lo
 
 template <bool AK, bool BK>
 void launch_variant(const GemmArgs& a, cudaStream_t s) {
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(gemm_f64_kernel<AK, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(sizeof(Smem)));
-        configured = true;
-    }
+    set_max_smem_once(reinterpret_cast<const void*>(gemm_f64_kernel<AK, BK>), static_cast<int>(sizeof(Smem)));
     const long long total = ((a.rows + BM - 1) / BM) * ((a.cols + BN - 1) / BN);
     const long long tiles = a.tile_count < 0 ? total - a.tile_begin : a.tile_count;
     if (tiles > 0) gemm_f64_kernel<AK, BK><<<static_cast<unsigned>(tiles), THREADS, sizeof(Smem), s>>>(a);

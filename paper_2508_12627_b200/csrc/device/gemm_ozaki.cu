@@ -22,6 +22,8 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "epilogue.cuh"
@@ -38,6 +40,7 @@ constexpr int OZ_STAGES = 2;
 constexpr int OZ_THREADS = 320;            // warps 0-3 and 6-9 epilogue, 4 producer, 5 MMA issuer
 constexpr int OZ_EPI = 256;                // epilogue threads: two per tile row (TMEM lane), 64 columns each
 constexpr int OZ_TILE_STAGE = OZ_BM * OZ_SK;  // 8 KiB per operand slice per stage
+constexpr int kOzWorkSlots = 256;             // per-SM scratch slots (see ozaki_work_entries)
 
 __device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 
@@ -404,6 +407,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
         // warp's 32 rows of one column are one coalesced 256-byte access
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        if (smid >= static_cast<unsigned>(kOzWorkSlots)) __trap();
         double* work = p.work + static_cast<long long>(smid) * (OZ_BM * OZ_BN) + rt;
         const unsigned lane_base = tmem + (static_cast<unsigned>(quarter * 32) << 16);
         if constexpr (split < S) {  // pass 0: high diagonals into the scratch
@@ -642,17 +646,16 @@ int ozaki_split(const double* x, long long rows, long long k, long long rs, long
     if (panels) {  // only these 128-row panels (a row-sharded rank's tiles read no others)
         npanels = static_cast<long long>(panels->size());
         if (npanels == 0) return 0;
-        if (cudaMallocAsync(reinterpret_cast<void**>(&dpanels), sizeof(int) * panels->size(), s) != cudaSuccess) return -1;
+        if (cudaMallocAsync(reinterpret_cast<void**>(&dpanels), sizeof(int) * panels->size(), s) != cudaSuccess) {
+            cudaGetLastError();
+            return -1;
+        }
         cudaMemcpyAsync(dpanels, panels->data(), sizeof(int) * panels->size(), cudaMemcpyHostToDevice, s);
     }
     const long long exp_rows = panels ? npanels * tile_rows : rows;
     oz_row_exponents<<<static_cast<unsigned>((exp_rows + 7) / 8), 256, 0, s>>>(x, rows, k, rs, ks, exps, dpanels);
     const int smem = tile_rows * (OZ_BK + 1) * static_cast<int>(sizeof(double));
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(oz_split, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        configured = true;
-    }
+    set_max_smem_once(reinterpret_cast<const void*>(oz_split), smem);
     if (ks == 1 && rs % 2 == 0 && reinterpret_cast<std::uintptr_t>(x) % 16 == 0)
         oz_split_rows<<<dim3(static_cast<unsigned>(npanels), static_cast<unsigned>(kp / 32)), 256, 0, s>>>(
             x, rows, k, rs, exps, kp, slices, rp * kp, out, dpanels);
@@ -681,17 +684,26 @@ void ozaki_tile_panels(const OzakiArgs& p, std::vector<int>* a_panels, std::vect
         if (mb[i]) b_panels->push_back(static_cast<int>(i));
 }
 
-std::size_t ozaki_work_entries() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        int v = 0;
+// The per-SM high-diagonal scratch is indexed by %smid, which PTX bounds only
+// by %nsmid (not by the enabled SM count): kOzWorkSlots covers every SM id a
+// Blackwell part exposes, and the kernel traps on anything beyond it.
+std::size_t ozaki_work_entries() { return static_cast<std::size_t>(kOzWorkSlots) * OZ_BM * OZ_BN; }
+
+namespace {
+long long ozaki_sm_count() {  // per device (function attributes and SM counts are per device)
+    static std::mutex mu;
+    static std::map<int, int> by_dev;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    int& v = by_dev[dev];
+    if (!v) {
         cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        sms = v > 0 ? v : 148;
+        if (v <= 0) v = 148;
     }
-    return static_cast<std::size_t>(sms + 8) * OZ_BM * OZ_BN;  // %smid < SM count (slack for safety)
+    return v;
 }
+}  // namespace
 
 long long ozaki_tile_count(const OzakiArgs& p) {
     const long long tiles_m = p.mpad / OZ_BM, tiles_n = p.npad / OZ_BN;
@@ -701,11 +713,7 @@ long long ozaki_tile_count(const OzakiArgs& p) {
 template <int S>
 void launch_oz(const OzakiArgs& p, long long tiles, cudaStream_t s) {
     const int bytes = static_cast<int>(sizeof(OzSmem));
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(ozaki_gemm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-        configured = true;
-    }
+    set_max_smem_once(reinterpret_cast<const void*>(ozaki_gemm_kernel<S>), bytes);
     ozaki_gemm_kernel<S><<<static_cast<unsigned>(tiles), OZ_THREADS, bytes, s>>>(p);
 }
 
@@ -722,7 +730,7 @@ int launch_ozaki_gemm(const OzakiArgs& in, cudaStream_t s) {
     if (tiles <= 0) return 0;
     // one CTA per SM: a last wave at most half full runs its tiles split along K
     // over the SMs the full waves leave idle (C2: 2080 tiles = 14 x 148 + 8)
-    const long long sms = static_cast<long long>(ozaki_work_entries() / (OZ_BM * OZ_BN)) - 8;
+    const long long sms = ozaki_sm_count();
     const long long rem = tiles % sms, ktiles = p.kpad / OZ_BK;
     long long grid = tiles;
     p.tail_split = 1;
@@ -730,16 +738,25 @@ int launch_ozaki_gemm(const OzakiArgs& in, cudaStream_t s) {
         const long long split = std::min({sms / rem, ktiles / 4, static_cast<long long>(kOzMaxTailSplit)});
         if (split >= 2) {
             const std::size_t part = static_cast<std::size_t>(rem * split) * OZ_BM * OZ_BN * sizeof(double);
-            if (cudaMallocAsync(reinterpret_cast<void**>(&p.tail_part), part, s) == cudaSuccess &&
-                cudaMallocAsync(reinterpret_cast<void**>(&p.tail_count), sizeof(unsigned) * rem, s) == cudaSuccess) {
+            if (cudaPeekAtLastError() != cudaSuccess) return -1;  // an earlier launch failed: report, never mask it
+            const cudaError_t e1 = cudaMallocAsync(reinterpret_cast<void**>(&p.tail_part), part, s);
+            const cudaError_t e2 =
+                e1 == cudaSuccess ? cudaMallocAsync(reinterpret_cast<void**>(&p.tail_count), sizeof(unsigned) * rem, s)
+                                  : cudaSuccess;
+            if (e1 == cudaSuccess && e2 == cudaSuccess) {
                 cudaMemsetAsync(p.tail_count, 0, sizeof(unsigned) * rem, s);
                 p.tail_split = static_cast<int>(split);
                 p.tail_from = tiles - rem;
                 grid = p.tail_from + rem * split;
             } else {
-                cudaGetLastError();
-                if (p.tail_part) cudaFreeAsync(p.tail_part, s);
+                // no room for the partial tiles: the tail runs unsplit (same result, later)
+                if ((e1 != cudaSuccess && e1 != cudaErrorMemoryAllocation) ||
+                    (e2 != cudaSuccess && e2 != cudaErrorMemoryAllocation))
+                    return -1;
+                cudaGetLastError();  // exactly the allocation error just returned
+                if (e1 == cudaSuccess) cudaFreeAsync(p.tail_part, s);
                 p.tail_part = nullptr;
+                p.tail_count = nullptr;
             }
         }
     }

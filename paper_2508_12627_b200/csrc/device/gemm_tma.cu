@@ -330,11 +330,8 @@ bool encode(CUtensorMap* map, const double* ptr, bool kmajor, long long rows, lo
 
 template <bool AK, bool BKM>
 void launch_tma(const CUtensorMap& ma, const CUtensorMap& mb, const TmaArgs& args, long long grid, cudaStream_t s) {
-    static std::once_flag once;
     const int bytes = static_cast<int>(sizeof(TmaSmem)) + 1024;
-    std::call_once(once, [&] {
-        cudaFuncSetAttribute(gemm_tma_kernel<AK, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    });
+    set_max_smem_once(reinterpret_cast<const void*>(gemm_tma_kernel<AK, BKM>), bytes);
     if (grid > 0) gemm_tma_kernel<AK, BKM><<<static_cast<unsigned>(grid), THREADS, bytes, s>>>(ma, mb, args);
 }
 

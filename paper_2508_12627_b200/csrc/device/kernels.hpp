@@ -4,11 +4,30 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <vector>
 
 #include <cuda_runtime.h>
 
 namespace ustats::dev {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel):
+// function attributes are per device, so a process-wide flag would leave the
+// kernel unconfigured on a second GPU.
+inline void set_max_smem_once(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, int> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    int& have = done[{dev, func}];
+    if (have < bytes) {
+        cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        have = bytes;
+    }
+}
 
 constexpr int kMaxDims = 12;         // iteration dims of one stream (bandwidth) kernel
 constexpr int kMaxFactors = 8;       // factors multiplied inside one kernel

@@ -216,7 +216,8 @@ std::string plan_key(const std::vector<StatisticSpec>& specs, const std::vector<
                     std::to_string(d.serial_launch) + std::to_string(d.shard_rows) + std::to_string(d.fp64_emulation) +
                     "," + std::to_string(d.rank) + "," +
                     std::to_string(d.world_size) + "," + std::to_string(d.emulate_world) + "," +
-                    std::to_string(d.memory_budget_bytes) + "|";
+                    std::to_string(d.memory_budget_bytes) + "," + std::to_string(d.oz_slices) + "," +
+                    std::to_string(d.oz_max_k) + "|";
     for (const Buf& b : uniq) k += std::to_string(b->order) + (b->symmetric ? "s" : "g");
     for (std::size_t q = 0; q < specs.size(); ++q) {
         k += "|" + std::to_string(specs[q].m) + ":";
@@ -265,12 +266,6 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
                                                 long long n, LatticeMode mode, const Config& config, bool speculate) {
     std::vector<StatisticResult> out(specs.size());
     Runtime& rt = Runtime::get(config.device.device);
-    {
-        // re-measure free memory only when this call's footprint is a large
-        // share of the device (n^2 matrices of several GiB)
-        const double n2 = 8.0 * static_cast<double>(n) * static_cast<double>(n);
-        if (n2 * 6 > 0.5 * rt.free_bytes()) rt.refresh_free_bytes();
-    }
     const auto t_up = Clock::now();
 
     // Upload each distinct factor of every statistic once; sparsify on device
@@ -394,8 +389,25 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
     const bool trace = std::getenv("USTATS_TRACE") != nullptr;
 
     const auto t0 = Clock::now();
+    // The schedule counts the distinct inputs as live from the start, so the
+    // budget is the memory available now PLUS those inputs (every one of them
+    // is device-resident by now: uploaded, donated or caller-owned), minus a
+    // reserve for the small pool allocations (epilogue partials, stream
+    // scratch, term slots) the schedule does not itemize.
     double budget = static_cast<double>(config.device.memory_budget_bytes);
-    if (budget <= 0) budget = 0.94 * rt.free_bytes() - 2.0e9;  // inputs included: they came out of it
+    if (budget <= 0) {
+        double inputs = 0;
+        std::vector<const DeviceBuffer*> seen;
+        for (const auto& ts : tensors)
+            for (const Buf& b : ts)
+                if (std::find(seen.begin(), seen.end(), b.get()) == seen.end()) {
+                    seen.push_back(b.get());
+                    inputs += 8.0 * static_cast<double>(b->entries());
+                }
+        const double n2 = 8.0 * static_cast<double>(n) * static_cast<double>(n);
+        if (n2 * 6 > 0.5 * rt.free_bytes()) rt.refresh_free_bytes();  // a program that needs most of the device
+        budget = rt.free_bytes() + inputs - 1.5 * 1073741824.0;
+    }
     // distinct inputs in first-use order, and each factor's position among them
     std::vector<Buf> uniq;
     std::vector<std::vector<int>> slot(specs.size());
@@ -523,6 +535,7 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
             res.stats.symmetric_gemms = shared.symmetric_gemms;
             res.stats.emulated_macs = shared.emulated_macs;
             res.stats.int8_ops = shared.int8_ops;
+            res.stats.oz_slices = shared.oz_slices;
         }
         res.upload_seconds = upload_s;
         res.contract_seconds = contract_s;

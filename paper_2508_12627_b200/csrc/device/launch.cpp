@@ -211,12 +211,50 @@ void Program::run_stream(const Op& op, double* out) {
 
 // FP64 emulation on the INT8 tensor cores (gemm_ozaki.cu) for large plain
 // products whose K keeps every digit diagonal exact in int32.
-constexpr int kOzSlices = 6;           // 8-bit balanced digits: 46 bits, 21 digit products
-constexpr long long kOzMaxK = 21000;    // 6 products of K * 128^2 per diagonal < 2^31; longer K runs
-                                        // as a sequence of K chunks accumulated in FP64 (all epilogues are linear in C)
 constexpr long long kOzMinDim = 1024;   // below, DMMA is as fast and needs no digit pass
 constexpr long long kOzMinK = 1024;     // shorter K: per-tile drains and digit passes outweigh the MMA savings
                                         // (C4's Khatri-Rao GEMMs, K = 1024: 297 -> 216 ms per evaluation)
+constexpr double kOzDigitCap = 4.0 * 1073741824.0;  // digit bytes per operand per K chunk
+
+// Error-bound guard. With S balanced 8-bit slices, truncation and the dropped
+// products t + u >= S bound every entry's error by (S + 2) 2^{2-8S} K
+// max|A_i| max|B_j| (gemm_ozaki.cu). The FP64 dot product the emulation
+// replaces has the classical worst-case bound gamma_K = K u / (1 - K u),
+// u = 2^-53, over the same K max|A_i| max|B_j|. The guard takes the fewest
+// slices whose bound does not exceed gamma_K, so the emulated product is never
+// less accurate, worst case, than the DMMA product it replaces (S = 6 for every
+// K >= 1024, S = 7 below); a forced Config.oz_slices overrides it (tests).
+int oz_guard_slices(long long K) {
+    const double u = std::ldexp(1.0, -53), gamma = static_cast<double>(K) * u / (1.0 - static_cast<double>(K) * u);
+    for (int S = 4; S <= kOzMaxSlices; ++S)
+        if ((S + 2) * std::ldexp(1.0, 2 - 8 * S) <= gamma) return S;
+    return kOzMaxSlices;
+}
+
+OzPlan oz_plan(long long K, long long rows, long long cols, bool same_operand, const DeviceConfig& dc) {
+    OzPlan p;
+    p.slices = dc.oz_slices > 0 ? dc.oz_slices : oz_guard_slices(K);
+    // S products of K * 128^2 per diagonal accumulator must stay below 2^31
+    const long long exact = ((1ll << 31) - 1) / (static_cast<long long>(p.slices) * 128 * 128) / 64 * 64;
+    const long long max_k = dc.oz_max_k > 0 ? std::min<long long>(dc.oz_max_k / 64 * 64, exact) : exact;
+    // fewest chunks whose digit panels stay within kOzDigitCap per operand (C5:
+    // 65536 rows x 65536 K would need 24 GiB of digits per operand; 4, 6, 8 and
+    // 12 chunks measured within 2% of each other there)
+    const long long rows_pad = (std::max(rows, cols) + 127) / 128 * 128;
+    const long long cap_k = std::max<long long>(64, static_cast<long long>(kOzDigitCap / (static_cast<double>(rows_pad) * p.slices)) / 64 * 64);
+    const long long limit = std::min(max_k, cap_k);
+    p.nchunks = (K + limit - 1) / limit;
+    p.kc = ((K + p.nchunks - 1) / p.nchunks + 63) / 64 * 64;  // chunk starts stay 512-byte aligned
+    while (p.kc > limit) {
+        ++p.nchunks;
+        p.kc = ((K + p.nchunks - 1) / p.nchunks + 63) / 64 * 64;
+    }
+    p.a_bytes = ozaki_slice_bytes(rows, p.kc, 128) * static_cast<std::size_t>(p.slices);
+    p.b_bytes = same_operand ? 0 : ozaki_slice_bytes(cols, p.kc, 128) * static_cast<std::size_t>(p.slices);
+    p.scratch_bytes = p.a_bytes + p.b_bytes + ozaki_work_entries() * sizeof(double) +
+                      sizeof(int) * static_cast<std::size_t>(rows + cols) + (std::size_t{96} << 20);  // + tail partials
+    return p;
+}
 
 // A single-factor operand whose row digits flatten to one stride (a
 // materialized Khatri-Rao operand of n^2 rows is one): its row stride, or -1.
@@ -233,46 +271,52 @@ bool Program::emulated_eligible(const GemmArgs& g) const {
     return flat_row_stride(g.a, n_) >= 0 && flat_row_stride(g.b, n_) >= 0;
 }
 
+// The transient device bytes an op needs while it runs, beyond its outputs:
+// the emulated GEMM's digit panels for one K chunk (the memory-bounded
+// schedule adds them at the op, so they are planned, not found at run time).
+std::size_t Program::op_scratch_bytes(const Op& op) const {
+    if (!op.gemm || !config_.device.fp64_emulation) return 0;
+    const long long rows = static_cast<long long>(ipow(n_, static_cast<int>(op.ra.size())));
+    const long long cols = static_cast<long long>(ipow(n_, static_cast<int>(op.rb.size())));
+    if (n_ < kOzMinK || rows < kOzMinDim || cols < kOzMinDim) return 0;
+    const bool same = op.fa.size() == 1 && op.fb.size() == 1 && op.fa[0].buf == op.fb[0].buf && rows == cols;
+    return oz_plan(n_, rows, cols, same, config_.device).scratch_bytes;
+}
+
 // Digits of both operands, the product (straight into a plain store's output,
 // else into scratch), then the fused epilogues over the stored product.
-// K beyond the exact int32 bound (C5: K = 65536) runs as equal K chunks of at
-// most kOzMaxK, each digitized on its own (per-chunk row exponents) and
-// accumulated into the outputs in chunk order: every epilogue is linear in C.
+// K beyond the exact int32 bound (C5: K = 65536) runs as equal K chunks (oz_plan),
+// each digitized on its own (per-chunk row exponents) and accumulated into the
+// outputs in chunk order: every epilogue is linear in C.
 int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
     cudaStream_t s = rt_->stream();
-    const long long nchunks = (g.n + kOzMaxK - 1) / kOzMaxK;  // fewest chunks (6 and 12 chunks: within 2%)
-    const long long kc = ((g.n + nchunks - 1) / nchunks + 63) / 64 * 64;  // chunk starts stay 512-byte aligned
-    if (nchunks > 1)  // a consumer of C^2 is not linear in C: the caller runs it on DMMA
-        for (int q = 0; q < set.count; ++q)
-            if (set.d[q].self_power != 1) return -1;
-    const std::size_t abytes = ozaki_slice_bytes(g.rows, kc, 128), bbytes = ozaki_slice_bytes(g.cols, kc, 128);
     // one set of digits when both operands are the same matrix view (A A^T)
     const long long ars = flat_row_stride(g.a, n_), brs = flat_row_stride(g.b, n_);
     const bool same = g.a.ptr[0] == g.b.ptr[0] && g.rows == g.cols && ars == brs && g.a.kstride[0] == g.b.kstride[0];
-    // the digits are scratch the memory-bounded schedule did not plan for: if
-    // they do not fit now, the GEMM runs on DMMA instead (caller's fallback)
-    std::vector<void*> got;
-    auto grab = [&](std::size_t bytes) -> void* {
-        void* q = nullptr;
-        if (cudaMallocAsync(&q, bytes, s) != cudaSuccess) {
-            cudaGetLastError();
-            return nullptr;
-        }
-        got.push_back(q);
-        return q;
-    };
-    int8_t* da = static_cast<int8_t*>(grab(abytes * kOzSlices));
-    int* ea = static_cast<int*>(grab(sizeof(int) * static_cast<std::size_t>(g.rows)));
-    int8_t* db = same ? da : static_cast<int8_t*>(grab(bbytes * kOzSlices));
-    int* eb = same ? ea : static_cast<int*>(grab(sizeof(int) * static_cast<std::size_t>(g.cols)));
-    double* work = static_cast<double*>(grab(ozaki_work_entries() * sizeof(double)));
-    if (!da || !ea || !db || !eb || !work) {
-        for (void* q : got) cudaFreeAsync(q, s);
-        return -1;
-    }
+    const OzPlan oz = oz_plan(g.n, g.rows, g.cols, same, config_.device);
+    const int S = oz.slices;
+    const long long kc = oz.kc;
+    if (oz.nchunks > 1)  // a consumer of C^2 is not linear in C: the caller runs it on DMMA
+        for (int q = 0; q < set.count; ++q)
+            if (set.d[q].self_power != 1) return -1;
+    // digit panels: slabs the schedule planned for (op_scratch_bytes); the
+    // choice of engine depends only on the plan, never on a failed allocation,
+    // so row-sharded ranks always agree on it
+    int8_t* da = static_cast<int8_t*>(rt_->raw_alloc(oz.a_bytes));
+    int8_t* db = same ? da : static_cast<int8_t*>(rt_->raw_alloc(oz.b_bytes));
+    int* ea = static_cast<int*>(rt_->raw_alloc(sizeof(int) * static_cast<std::size_t>(g.rows), false));
+    int* eb = same ? ea : static_cast<int*>(rt_->raw_alloc(sizeof(int) * static_cast<std::size_t>(g.cols), false));
+    double* work = static_cast<double*>(rt_->raw_alloc(ozaki_work_entries() * sizeof(double), false));
     const bool sym = g.symmetric_out && g.rows == g.cols;
     int launched = 0;
     long long tiles = 0;
+    auto split = [&](const double* x, long long rows, long long k, long long rs, long long ks, int8_t* out, int* exps,
+                     const std::vector<int>* panels) {
+        const int l = ozaki_split(x, rows, k, rs, ks, 128, S, out, exps, s, panels);
+        if (l < 0) fail(ErrorCode::CudaError, "executor: Ozaki digit split failed");
+        check_cuda(cudaPeekAtLastError(), "Ozaki digit split launch");
+        launched += l;
+    };
     for (long long k0 = 0; k0 < g.n; k0 += kc) {
         const long long k = std::min(kc, g.n - k0);
         const double* xa = g.a.ptr[0] + k0 * g.a.kstride[0];
@@ -290,7 +334,7 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
         p.mpad = (g.rows + 127) / 128 * 128;
         p.npad = (g.cols + 127) / 128 * 128;
         p.kpad = (k + 63) / 64 * 64;
-        p.slices = kOzSlices;
+        p.slices = S;
         p.symmetric = sym ? 1 : 0;
         p.accumulate = k0 == 0 ? g.accumulate : 1;
         p.epis = set;  // the same fused consumers (and partial slots) as the DMMA kernel's
@@ -309,29 +353,35 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
                 u.insert(u.end(), pb.begin(), pb.end());
                 std::sort(u.begin(), u.end());
                 u.erase(std::unique(u.begin(), u.end()), u.end());
-                launched += ozaki_split(xa, g.rows, k, ars, g.a.kstride[0], 128, kOzSlices, da, ea, s, &u);
+                split(xa, g.rows, k, ars, g.a.kstride[0], da, ea, &u);
             } else {
-                launched += ozaki_split(xa, g.rows, k, ars, g.a.kstride[0], 128, kOzSlices, da, ea, s, &pa);
-                launched += ozaki_split(xb, g.cols, k, brs, g.b.kstride[0], 128, kOzSlices, db, eb, s, &pb);
+                split(xa, g.rows, k, ars, g.a.kstride[0], da, ea, &pa);
+                split(xb, g.cols, k, brs, g.b.kstride[0], db, eb, &pb);
             }
         } else {
-            launched += ozaki_split(xa, g.rows, k, ars, g.a.kstride[0], 128, kOzSlices, da, ea, s);
-            if (!same) launched += ozaki_split(xb, g.cols, k, brs, g.b.kstride[0], 128, kOzSlices, db, eb, s);
+            split(xa, g.rows, k, ars, g.a.kstride[0], da, ea, nullptr);
+            if (!same) split(xb, g.cols, k, brs, g.b.kstride[0], db, eb, nullptr);
         }
         const int l = launch_ozaki_gemm(p, s);
-        if (l < 0) fail(ErrorCode::InvalidArgument, "executor: emulated GEMM launch failed");
+        if (l < 0) fail(ErrorCode::CudaError, "executor: emulated GEMM launch failed");
+        check_cuda(cudaPeekAtLastError(), "emulated GEMM launch");
         launched += l;
     }
     if (stats_) {
         const std::uint64_t tile = 128ull * 128ull * static_cast<std::uint64_t>((g.n + 63) / 64 * 64);
-        const std::uint64_t products = static_cast<std::uint64_t>(kOzSlices * (kOzSlices + 1) / 2);
+        const std::uint64_t products = static_cast<std::uint64_t>(S * (S + 1) / 2);
         stats_->int8_ops += 2 * static_cast<std::uint64_t>(tiles) * tile * products;
         const std::uint64_t full = static_cast<std::uint64_t>(g.rows) * static_cast<std::uint64_t>(g.cols) *
                                    static_cast<std::uint64_t>(g.n);
         const std::uint64_t tm = static_cast<std::uint64_t>((g.rows + 127) / 128);
         stats_->emulated_macs += sym ? full / (tm * tm) * (tm * (tm + 1) / 2) : full;  // as gemm_macs counts it
+        stats_->oz_slices = static_cast<std::uint64_t>(S);
     }
-    for (void* q : got) cudaFreeAsync(q, s);
+    rt_->raw_free(da, oz.a_bytes);
+    if (!same) rt_->raw_free(db, oz.b_bytes);
+    rt_->release(reinterpret_cast<double*>(ea));
+    if (!same) rt_->release(reinterpret_cast<double*>(eb));
+    rt_->release(work);
     return launched;
 }
 

@@ -725,6 +725,11 @@ void Program::make_schedule(double budget) {
             if (!e.ext && e.out >= 0) outs[i].push_back(e.out);
     }
     auto size = [&](int b) { return 8.0 * static_cast<double>(ipow(n_, bufs_[static_cast<std::size_t>(b)].order)); };
+    // transient bytes while the op runs (emulated-GEMM digit panels): counted
+    // at the op, after its outputs are allocated and before its inputs are freed
+    std::vector<double> scratch(N, 0.0);
+    for (std::size_t i = 0; i < N; ++i)
+        if (!ops_[i].dead) scratch[i] = static_cast<double>(op_scratch_bytes(ops_[i]));
     std::vector<char> big(N, 0);
     for (std::size_t i = 0; i < N; ++i)
         for (int b : outs[i]) big[i] |= bufs_[static_cast<std::size_t>(b)].order >= 2;
@@ -761,7 +766,7 @@ void Program::make_schedule(double budget) {
             st.avail[static_cast<std::size_t>(b)] = 1;
             st.live += size(b);
         }
-        st.peak = std::max(st.peak, st.live);
+        st.peak = std::max(st.peak, st.live + scratch[i]);
         for (int b : reads[i])
             if (--st.left[static_cast<std::size_t>(b)] == 0 && !bufs_[static_cast<std::size_t>(b)].input && !keep_.count(b))
                 st.live -= size(b);
@@ -846,6 +851,7 @@ void Program::make_schedule(double budget) {
     }
     schedule_ = best.order;
     sched_peak_ = best.peak;
+    sched_fits_ = found;
 }
 
 void Program::optimize(double budget_bytes) {
@@ -859,6 +865,7 @@ void Program::optimize(double budget_bytes) {
         const std::vector<Op> before = ops_;
         const std::vector<std::size_t> sched = schedule_;
         const double peak = sched_peak_;
+        const bool fits = sched_fits_;
         const std::uint64_t fused = stats_ ? stats_->fused_epilogues : 0;
         fuse_sweeps();
         if (ops_.size() != before.size()) {
@@ -868,10 +875,19 @@ void Program::optimize(double budget_bytes) {
                 ops_ = before;
                 schedule_ = sched;
                 sched_peak_ = peak;
+                sched_fits_ = fits;
                 if (stats_) stats_->fused_epilogues = fused;
             }
         }
     }
+    // a program that cannot fit the device fails here, typed, before anything
+    // is launched (the reference throws MemoryCapExceeded before allocating,
+    // tensor.cpp:9-23); plan-only programs (no runtime) just report the peak
+    if (rt_ && budget_bytes > 0 && !sched_fits_ && sched_peak_ > budget_bytes)
+        fail(ErrorCode::MemoryCapExceeded,
+             "device program needs " + std::to_string(static_cast<long long>(sched_peak_ / 1048576.0)) +
+                 " MiB at its peak (inputs, live intermediates and GEMM digit scratch) but the device budget is " +
+                 std::to_string(static_cast<long long>(budget_bytes / 1048576.0)) + " MiB");
     for (SymBuf& b : bufs_) b.last_use = -1;
     for (std::size_t pos = 0; pos < schedule_.size(); ++pos)
         for_each_read(ops_[schedule_[pos]],

@@ -31,9 +31,9 @@ void check_cuda(cudaError_t e, const char* what) {
 DeviceBuffer::~DeviceBuffer() {
     for (auto& r : ready) cudaEventDestroy(r.second);
     if (ptr && !borrowed && rt) {
-        cudaFreeAsync(ptr, rt->stream());
         if (std::getenv("USTATS_SCHED_DEBUG") && entries() * 8 > (1ull << 30))
             std::fprintf(stderr, "[free] %.2f GiB\n", entries() * 8 / 1073741824.0);
+        rt->raw_free(ptr, std::max<std::uint64_t>(entries(), 1) * sizeof(double));
     }
 }
 
@@ -75,7 +75,7 @@ Runtime::Runtime(int device) : device_(device) {
     }
 }
 
-Runtime::~Runtime() {}
+Runtime::~Runtime() {}  // process teardown: the driver reclaims device memory
 
 void Runtime::refresh_free_bytes() {
     std::size_t free_b = 0, total_b = 0;
@@ -88,7 +88,7 @@ void Runtime::refresh_free_bytes() {
         cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
         pooled = static_cast<double>(reserved > used ? reserved - used : 0);
     }
-    free_bytes_ = static_cast<double>(free_b) + pooled;
+    free_bytes_ = static_cast<double>(free_b) + pooled + idle_slab_bytes();
     agree_free_bytes();
 }
 
@@ -97,29 +97,95 @@ Buf Runtime::allocate(int order, long long n) {
     b->order = order;
     b->n = n;
     b->rt = this;
-    void* p = nullptr;
     const std::size_t bytes = std::max<std::uint64_t>(b->entries(), 1) * sizeof(double);
-    cudaError_t e = cudaMallocAsync(&p, bytes, cur_);
-    if (e == cudaErrorMemoryAllocation) {
-        // the pool keeps freed blocks (release threshold = inf); a large request
-        // that no freed block fits (e.g. after the emulated GEMM's digit
-        // scratch) needs them handed back first: drain, trim, retry once
-        cudaGetLastError();
-        cudaDeviceSynchronize();
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, device_) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
-        e = cudaMallocAsync(&p, bytes, cur_);
+    b->ptr = static_cast<double*>(raw_alloc(bytes));
+    b->slab = bytes >= kSlabMin;
+    return b;
+}
+
+void* Runtime::slab_get(std::size_t bytes) {
+    for (std::size_t i = 0; i < idle_.size(); ++i)
+        if (idle_[i].bytes == bytes) {
+            Slab s = idle_[i];
+            idle_.erase(idle_.begin() + static_cast<std::ptrdiff_t>(i));
+            check_cuda(cudaStreamWaitEvent(cur_, s.freed, 0), "wait slab release");
+            cudaEventDestroy(s.freed);
+            return s.ptr;
+        }
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();  // the allocation error only
+        return nullptr;
     }
-    if (e != cudaSuccess || std::getenv("USTATS_SCHED_DEBUG")) {
+    return p;
+}
+
+void Runtime::slab_put(void* p, std::size_t bytes) {
+    Slab s{p, bytes, nullptr};
+    if (cudaEventCreateWithFlags(&s.freed, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(s.freed, cur_) != cudaSuccess) {
+        cudaGetLastError();
+        cudaStreamSynchronize(cur_);
+        if (s.freed) cudaEventDestroy(s.freed);
+        cudaFree(p);
+        return;
+    }
+    idle_.push_back(s);
+}
+
+double Runtime::idle_slab_bytes() const {
+    double t = 0;
+    for (const Slab& s : idle_) t += static_cast<double>(s.bytes);
+    return t;
+}
+
+void Runtime::reclaim() {
+    sync();  // this runtime's streams only: every pending user of an idle slab has finished
+    for (Slab& s : idle_) {
+        cudaEventDestroy(s.freed);
+        cudaFree(s.ptr);
+    }
+    idle_.clear();
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device_) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+}
+
+void* Runtime::raw_alloc(std::size_t bytes, bool slab_ok) {
+    bytes = std::max<std::size_t>(bytes, 8);
+    auto attempt = [&]() -> void* {
+        if (slab_ok && bytes >= kSlabMin) return slab_get(bytes);
+        void* p = nullptr;
+        const cudaError_t e = cudaMallocAsync(&p, bytes, cur_);
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();  // clears exactly this allocation error
+            return nullptr;
+        }
+        check_cuda(e, "cudaMallocAsync");
+        return p;
+    };
+    void* p = attempt();
+    if (!p) {
+        reclaim();
+        p = attempt();
+    }
+    if (!p || std::getenv("USTATS_SCHED_DEBUG")) {
         std::size_t fr = 0, tot = 0;
         cudaMemGetInfo(&fr, &tot);
-        if (e != cudaSuccess || bytes > (1ull << 30))
+        if (!p || bytes > (1ull << 30))
             std::fprintf(stderr, "[alloc] %.2f GiB -> %s (free %.2f / %.2f GiB)\n", bytes / 1073741824.0,
-                         cudaGetErrorString(e), fr / 1073741824.0, tot / 1073741824.0);
+                         p ? "ok" : "out of memory", fr / 1073741824.0, tot / 1073741824.0);
     }
-    check_cuda(e, "cudaMallocAsync");
-    b->ptr = static_cast<double*>(p);
-    return b;
+    if (!p)
+        fail(ErrorCode::MemoryCapExceeded, "device allocation of " + std::to_string(bytes) +
+                                               " bytes failed after reclaiming idle memory (the memory-bounded "
+                                               "schedule exceeded the device)");
+    return p;
+}
+
+void Runtime::raw_free(void* p, std::size_t bytes) {
+    if (!p) return;
+    if (std::max<std::size_t>(bytes, 8) >= kSlabMin) slab_put(p, std::max<std::size_t>(bytes, 8));
+    else cudaFreeAsync(p, cur_);
 }
 
 Buf Runtime::borrow(const double* ptr, int order, long long n) {
@@ -133,9 +199,7 @@ Buf Runtime::borrow(const double* ptr, int order, long long n) {
 }
 
 double* Runtime::scratch(std::size_t entries) {
-    void* p = nullptr;
-    check_cuda(cudaMallocAsync(&p, std::max<std::size_t>(entries, 1) * sizeof(double), cur_), "cudaMallocAsync");
-    return static_cast<double*>(p);
+    return static_cast<double*>(raw_alloc(std::max<std::size_t>(entries, 1) * sizeof(double), false));
 }
 
 void Runtime::release(double* p) {

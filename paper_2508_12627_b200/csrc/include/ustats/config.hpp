@@ -34,6 +34,13 @@ struct DeviceConfig {
     /// Device-memory budget for inputs + live intermediates of one statistic's
     /// program (0 = free device memory at execution; plan-only: 179 GiB).
     std::uint64_t memory_budget_bytes = 0;
+    /// Digit slices of the emulated FP64 GEMM (0 = the error-bound guard's
+    /// choice, see gemm_ozaki.cu / DESIGN.md 2.3a; 4..7 forces a count).
+    int oz_slices = 0;
+    /// Longest K an emulated GEMM runs in one pass (0 = the int32-exact bound,
+    /// 21000); longer K runs as equal K chunks summed in FP64 (tests lower it
+    /// to exercise the chunked path at small n).
+    long long oz_max_k = 0;
 };
 
 struct Config {

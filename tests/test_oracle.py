@@ -64,8 +64,8 @@ def test_oracle_vs_reference_golden(fixture):
             seen.add(id(f))
             hashes.append(hashlib.sha256(np.ascontiguousarray(f).tobytes()).hexdigest())
     assert list(g["sha256"]) == hashes, "regenerated inputs differ from the fixture's bytes"
-    if name == "C5" and n > 512:
-        pytest.skip("numpy restatement too slow at this size on CPU")
+    if (name == "C5" and n > 512) or (name == "C4" and n > 96):
+        pytest.skip("numpy restatement too slow at this size on CPU (fixture checked on the GPU)")
     u, rows = O.u_statistic(factors, sig, m)
     v = np.array([r[2] for r in rows])
     assert np.array_equal(np.array([r[0] for r in rows]), g["rgs"])
