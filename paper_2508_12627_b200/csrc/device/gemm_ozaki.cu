@@ -19,8 +19,11 @@
 // Operand digits live in global memory pre-tiled in the tensor core's K-major
 // "core matrix" layout (tiles of TH rows x 64 bytes: four 16-byte K chunks,
 // each TH rows x 16 B), so each stage is a handful of 1-D bulk copies.
+#include <cuda.h>
+
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <map>
 #include <mutex>
@@ -509,6 +512,351 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): two SMs of one TPC compute a 256 x 128
+// output pair tile with M = 256 MMAs issued by the even CTA. Each CTA stages
+// its own 128 rows of A and HALF of B (64 of the 128 columns): the B bytes per
+// SM halve, so L2 -> SM traffic per int8 op drops by a third against the
+// single-SM kernel, whose 128 x 128 tiles pin it at the L2 throughput cap
+// (C2: 11.7 TB/s of TMA reads, tensor pipe 76%). Same two passes over K, same
+// per-CTA TMEM accumulators (128 lanes x 128 columns per diagonal), same
+// epilogue. Both CTAs stage through 3-D tensor maps over the digit layout
+// (one TMA per slice and operand: A box 128 rows, B box 64 rows x four 16-byte
+// K columns) with the cta_group::2 form, whose transaction bytes land on the
+// even CTA's barrier: the MMA issuer waits on one barrier per stage.
+constexpr int OZ2_SLOTS = 18;                  // digit slots per operand in the ring
+constexpr int OZ2_A = OZ_BM * OZ_SK;           // 8 KiB: 128 rows x 64 B of one slice
+constexpr int OZ2_B = (OZ_BN / 2) * OZ_SK;     // 4 KiB: this CTA's 64 columns of one slice
+constexpr long long OZ2_GROUP = OZ_GROUP / 2;  // pair rows per tile group (16 tile rows)
+__host__ __device__ constexpr int oz2_stages(int per_stage) {
+    return OZ2_SLOTS / per_stage < 8 ? OZ2_SLOTS / per_stage : 8;
+}
+
+struct Oz2Smem {
+    union {
+        struct {
+            int8_t a[OZ2_SLOTS][OZ2_A];
+            int8_t b[OZ2_SLOTS][OZ2_B];
+        } st;
+        double tile[epi::BM * epi::TP];
+    } u;
+    unsigned long long full[8], empty[8], full1[8], empty1[8], done[2], drained;
+    double red[OZ_EPI / 32];
+    int bexp[OZ_BN];
+    double bscale[OZ_BN];
+    int bwide;
+    unsigned tmem;
+};
+
+// Pair tiles: pair row pm covers tile rows 2 pm, 2 pm + 1. Symmetric: every
+// pair whose first tile is on or above the diagonal (2 pm <= tn); the odd tile
+// of a diagonal pair (2 pm + 1 > tn) is computed and dropped.
+__host__ __device__ __forceinline__ long long oz2_pair_count(const OzakiArgs& p) {
+    const long long T_m = p.mpad / OZ_BM, T_n = p.npad / OZ_BN, P_m = (T_m + 1) / 2;
+    if (!p.symmetric) return P_m * T_n;
+    long long c = 0;
+    for (long long tn = 0; tn < T_n; ++tn) c += tn / 2 + 1;
+    return c;
+}
+__host__ __device__ __forceinline__ void oz2_pair_of(const OzakiArgs& p, long long bid, long long* pm, long long* tn) {
+    const long long T_m = p.mpad / OZ_BM, T_n = p.npad / OZ_BN, P_m = (T_m + 1) / 2;
+    if (!p.symmetric) {  // groups of OZ2_GROUP pair rows x all columns, column-major inside
+        const long long width = OZ2_GROUP * T_n;
+        const long long g = bid / width, m0 = g * OZ2_GROUP;
+        const long long gsz = (P_m - m0) < OZ2_GROUP ? (P_m - m0) : OZ2_GROUP;
+        const long long rem = bid - g * width;
+        *pm = m0 + rem % gsz;
+        *tn = rem / gsz;
+        return;
+    }
+    // column groups of OZ_GROUP columns: the pair-row groups fully above the
+    // diagonal block first (column-major inside), then the diagonal block
+    const long long gn = (T_n + OZ_GROUP - 1) / OZ_GROUP;
+    for (long long J = 0; J < gn; ++J) {
+        const long long n0 = J * OZ_GROUP, w = (n0 + OZ_GROUP < T_n) ? OZ_GROUP : T_n - n0;
+        const long long above = (n0 / 2) * w;  // pair rows 0 .. n0/2 - 1
+        long long diag = 0;
+        for (long long c = n0; c < n0 + w; ++c) diag += c / 2 - n0 / 2 + 1;
+        if (bid >= above + diag) {
+            bid -= above + diag;
+            continue;
+        }
+        if (bid < above) {
+            const long long I = bid / (OZ2_GROUP * w), r = bid - I * OZ2_GROUP * w;
+            *pm = I * OZ2_GROUP + r % OZ2_GROUP;
+            *tn = n0 + r / OZ2_GROUP;
+            return;
+        }
+        bid -= above;
+        for (long long c = n0; c < n0 + w; ++c) {
+            const long long h = c / 2 - n0 / 2 + 1;
+            if (bid < h) {
+                *pm = n0 / 2 + bid;
+                *tn = c;
+                return;
+            }
+            bid -= h;
+        }
+    }
+    *pm = 0;
+    *tn = 0;
+}
+
+__device__ __forceinline__ unsigned oz2_cta_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void oz2_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the even CTA's copy of barrier b (its own copy when called there)
+__device__ __forceinline__ void oz2_arrive_leader(unsigned long long* b) {
+    unsigned remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(su32(b)));
+    // default (cta-scope) semantics, as CUTLASS's 2-SM pipelines use: a
+    // cluster-scope release / acquire emits an L1 invalidate (CCTL.IVALL) per
+    // stage on the MMA issuer's critical path
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void oz2_wait_cluster(unsigned long long* b, unsigned parity) { bar_wait(b, parity); }
+// tcgen05.commit to the barrier at the same offset in both CTAs of the pair
+__device__ __forceinline__ void oz2_commit(unsigned long long* bar) {
+    asm volatile(
+        "{\n.reg .pred e;\n.reg .b16 m;\nmov.b16 m, 3;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}\n" ::"r"(
+            su32(bar)));
+}
+
+// One stage of diagonals [D0, D1) from slots SLOT0.. (M = 256 over the pair, N = 128).
+template <int S, int D0, int D1, int SLOT0>
+__device__ __forceinline__ void oz2_issue_stage(unsigned tmem, unsigned long long desc_a, unsigned long long desc_b,
+                                                unsigned idesc, bool first0) {
+#pragma unroll
+    for (int ks = 0; ks < OZ_SK / 32; ++ks) {
+        const bool first = first0 && ks == 0;
+#pragma unroll
+        for (int d = D0; d < D1; ++d)
+#pragma unroll
+            for (int t = 0; t <= d; ++t) {
+                const int u = d - t;
+                if (t >= S || u >= S) continue;
+                // 32-byte k-step = two 16-byte core-matrix columns (A: 128 rows, B: 64 rows each)
+                const unsigned a_off = (SLOT0 + t) * OZ2_A + ks * 2 * OZ_BM * 16;
+                const unsigned b_off = (SLOT0 + u) * OZ2_B + ks * 2 * (OZ_BN / 2) * 16;
+                const unsigned acc = tmem + static_cast<unsigned>((d - D0) * OZ_BN);
+                const unsigned accumulate = (first && t == 0) ? 0u : 1u;
+                asm volatile(
+                    "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+                    "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(acc),
+                    "l"(desc_a + (a_off >> 4)), "l"(desc_b + (b_off >> 4)), "r"(idesc), "r"(accumulate));
+            }
+    }
+}
+// stage q of a ring of NST stages of NS slots each (compile-time slot base)
+template <int S, int D0, int D1, int NS, int NST, int Q = 0>
+__device__ __forceinline__ void oz2_issue(int q, unsigned tmem, unsigned long long da, unsigned long long db,
+                                          unsigned idesc, bool first) {
+    if (q == Q) oz2_issue_stage<S, D0, D1, Q * NS>(tmem, da, db, idesc, first);
+    else if constexpr (Q + 1 < NST) oz2_issue<S, D0, D1, NS, NST, Q + 1>(q, tmem, da, db, idesc, first);
+}
+
+// 3-D view of a digit buffer: (64 rows x 16 B as 128 8-byte words, 2 row
+// halves, K columns of every tile of every panel of every slice): a
+// (128, 2 or 1, 4) box is one tile's slice, all of it (A) or one half (B)
+__device__ __forceinline__ void oz2_tma(void* dst, const CUtensorMap* map, int half, int col, unsigned leader_bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+        "%4}], [%5];" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(0), "r"(half), "r"(col), "r"(leader_bar)
+        : "memory");
+}
+__device__ __forceinline__ unsigned oz2_leader_addr(const void* p) {
+    unsigned remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(su32(p)));
+    return remote;
+}
+
+template <int S>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_THREADS, 1)
+    ozaki_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                          const __grid_constant__ OzakiArgs p) {
+    extern __shared__ __align__(128) unsigned char oz_raw[];
+    Oz2Smem& sm = *reinterpret_cast<Oz2Smem*>(oz_raw);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const unsigned rank = oz2_cta_rank();
+    constexpr int split = oz_pass_split(S);  // pass 1: diagonals [0, split); pass 0: [split, S)
+    constexpr int P0 = oz2_stages(S), P1 = oz2_stages(split);
+    long long pm, tn;
+    oz2_pair_of(p, p.tile_begin + static_cast<long long>(blockIdx.x >> 1), &pm, &tn);
+    const long long T_m = p.mpad / OZ_BM;
+    const long long tm = 2 * pm + rank;
+    const bool tile_ok = tm < T_m && !(p.symmetric && tm > tn);
+    const long long ktiles = p.kpad / OZ_BK;
+    const long long tile_bytes = OZ_BM * OZ_BK;
+    const long long tm_load = tm < T_m ? tm : T_m - 1;  // a missing odd panel: load any (its rows are dropped)
+    // column coordinate of (slice t, panel, k-tile k): ((t * panels + panel) * ktiles + k) * 4
+    const long long acol0 = tm_load * ktiles * 4, a_sl = T_m * ktiles * 4;
+    const long long bcol0 = tn * ktiles * 4, b_sl = (p.npad / OZ_BN) * ktiles * 4;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&sm.tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    if (tid == 128) {
+        for (int s = 0; s < 8; ++s) {
+            bar_init(&sm.full[s], 1);
+            bar_init(&sm.empty[s], 1);
+            bar_init(&sm.full1[s], 1);
+            bar_init(&sm.empty1[s], 1);
+        }
+        bar_init(&sm.done[0], 1);
+        bar_init(&sm.done[1], 1);
+        bar_init(&sm.drained, 2 * OZ_EPI / 32);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    oz2_cluster_sync();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const unsigned tmem = sm.tmem;
+
+    if (tid == 128) {  // producer (both CTAs): own A panel, own half of the B panel, bytes counted on the even CTA
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&map_a)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&map_b)) : "memory");
+        auto load_stage = [&](long long k, int ns, int slot0, unsigned long long* bar) {
+            if (rank == 0) bar_expect(bar, static_cast<unsigned>(2 * ns * (OZ2_A + OZ2_B)));  // both CTAs' bytes
+            const unsigned lb = oz2_leader_addr(bar);
+            for (int t = 0; t < ns; ++t) {
+                oz2_tma(sm.u.st.a[slot0 + t], &map_a, 0, static_cast<int>(acol0 + t * a_sl + k * 4), lb);
+                oz2_tma(sm.u.st.b[slot0 + t], &map_b, static_cast<int>(rank),
+                        static_cast<int>(bcol0 + t * b_sl + k * 4), lb);
+            }
+        };
+        if constexpr (split < S) {
+#pragma unroll 1
+            for (long long k = 0; k < ktiles; ++k) {
+                const int s = static_cast<int>(k % P0);
+                if (k >= P0) bar_wait(&sm.empty[s], static_cast<unsigned>(((k / P0) - 1) & 1));
+                load_stage(k, S, s * S, &sm.full[s]);
+            }
+            bar_wait(&sm.done[0], 0);  // every pass-0 MMA has read its operands: the slots are free
+        }
+#pragma unroll 1
+        for (long long k = 0; k < ktiles; ++k) {
+            const int q = static_cast<int>(k % P1);
+            if (k >= P1) bar_wait(&sm.empty1[q], static_cast<unsigned>(((k / P1) - 1) & 1));
+            load_stage(k, split, q * split, &sm.full1[q]);
+        }
+    } else if (warp == 5 && rank == 0) {  // MMA issuer (even CTA): kind::i8, s32 accumulators, M = 256, N = 128
+        const unsigned idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((OZ_BN >> 3) << 17) | (((2 * OZ_BM) >> 4) << 24);
+        const unsigned long long da = umma_desc(su32(sm.u.st.a[0]), OZ_BM * 16, 128);
+        const unsigned long long db = umma_desc(su32(sm.u.st.b[0]), (OZ_BN / 2) * 16, 128);
+        if constexpr (split < S) {
+#pragma unroll 1
+            for (long long k = 0; k < ktiles; ++k) {
+                const int s = static_cast<int>(k % P0);
+                oz2_wait_cluster(&sm.full[s], static_cast<unsigned>((k / P0) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                oz2_issue<S, split, S, S, P0>(s, tmem, da, db, idesc, k == 0);
+                oz2_commit(&sm.empty[s]);
+            }
+            oz2_commit(&sm.done[0]);
+            oz2_wait_cluster(&sm.drained, 0);  // both CTAs read pass 0 out of TMEM
+            asm volatile("tcgen05.fence::after_thread_sync;");
+        }
+#pragma unroll 1
+        for (long long k = 0; k < ktiles; ++k) {
+            const int q = static_cast<int>(k % P1);
+            oz2_wait_cluster(&sm.full1[q], static_cast<unsigned>((k / P1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            oz2_issue<S, 0, split, split, P1>(q, tmem, da, db, idesc, k == 0);
+            oz2_commit(&sm.empty1[q]);
+        }
+        oz2_commit(&sm.done[1]);
+    } else if (warp < 4 || warp >= 6) {  // epilogue warps (both CTAs): as in ozaki_gemm_kernel
+        const int quarter = warp & 3, half = warp >= 6 ? 1 : 0;
+        const int et = half * 128 + quarter * 32 + lane;
+        const int rt = quarter * 32 + lane;
+        const int cb = half * (OZ_BN / 2);
+        const long long row = tm * OZ_BM + rt;
+        const bool row_ok = tile_ok && row < p.m;
+        auto sync_epi = [] { asm volatile("bar.sync 1, 256;" ::: "memory"); };
+        if (et == 0) sm.bwide = 0;
+        sync_epi();
+        if (et < OZ_BN) {
+            const long long col = tn * OZ_BN + et;
+            const int eb = col < p.n ? p.b_exp[col] : kOzNoColumn;
+            sm.bexp[et] = eb;
+            const bool pad = eb == kOzNoColumn, narrow = eb >= -511 && eb <= 511;
+            sm.bscale[et] = (pad || !narrow) ? 0.0 : __longlong_as_double(static_cast<long long>(eb + 1023) << 52);
+            if (!pad && !narrow) sm.bwide = 1;
+        }
+        sync_epi();
+        const int ea = row_ok ? p.a_exp[row] : 0;
+        const bool narrow = !sm.bwide && ea >= -511 && ea <= 511;
+        const double sa = row_ok ? __longlong_as_double(static_cast<long long>(ea + 1023) << 52) : 0.0;
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        if (smid >= static_cast<unsigned>(kOzWorkSlots)) __trap();
+        double* work = p.work + static_cast<long long>(smid) * (OZ_BM * OZ_BN) + rt;
+        const unsigned lane_base = tmem + (static_cast<unsigned>(quarter * 32) << 16);
+        if constexpr (split < S) {
+            bar_wait(&sm.done[0], 0);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+            for (int c0 = cb; c0 < cb + OZ_BN / 2; c0 += 16) {
+                double v[16];
+                oz_drain<split, S>(lane_base, c0, v, false);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) work[(c0 + j) * OZ_BM] = v[j];
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) oz2_arrive_leader(&sm.drained);
+        }
+        double h0[16], h1[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            h0[j] = split < S ? work[(cb + j) * OZ_BM] : 0.0;
+            h1[j] = split < S ? work[(cb + 16 + j) * OZ_BM] : 0.0;
+        }
+        bar_wait(&sm.done[1], 0);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+        for (int c0 = cb; c0 < cb + OZ_BN / 2; c0 += 16) {
+            double v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                v[j] = h0[j];
+                h0[j] = h1[j];
+                if (c0 + 32 < cb + OZ_BN / 2) h1[j] = split < S ? work[(c0 + 32 + j) * OZ_BM] : 0.0;
+            }
+            oz_drain<0, split>(lane_base, c0, v, true);
+            if (narrow)
+#pragma unroll
+                for (int j = 0; j < 16; ++j) sm.u.tile[rt * epi::TP + c0 + j] = (v[j] * sa) * sm.bscale[c0 + j];
+            else
+                for (int j = 0; j < 16; ++j) {
+                    const int eb = sm.bexp[c0 + j];
+                    sm.u.tile[rt * epi::TP + c0 + j] = (row_ok && eb != kOzNoColumn) ? oz_scale(v[j], ea + eb) : 0.0;
+                }
+        }
+        sync_epi();
+        if (tile_ok) {
+            // dense slot of the tile: the finalizers sum ozaki_tile_count slots
+            const long long T_n = p.npad / OZ_BN;
+            const long long slot = p.symmetric ? tn * (tn + 1) / 2 + tm : tm * T_n + tn;
+            epi::apply<OZ_EPI>(p.epis, p.m, p.n, p.accumulate, sm.u.tile, tm * OZ_BM, tn * OZ_BN, tm, tn,
+                               p.symmetric && tm != tn, slot, sm.red, et, sync_epi);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    oz2_cluster_sync();  // no CTA leaves while its pair may still signal its barriers or use its TMEM
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 // Row exponents: e_i with max_k |x_ik| < 2^e_i (0 for an all-zero row).
 __global__ void oz_row_exponents(const double* __restrict__ x, long long rows, long long k, long long rs, long long ks,
                                  int* __restrict__ exps, const int* __restrict__ panels) {
@@ -717,9 +1065,78 @@ void launch_oz(const OzakiArgs& p, long long tiles, cudaStream_t s) {
     ozaki_gemm_kernel<S><<<static_cast<unsigned>(tiles), OZ_THREADS, bytes, s>>>(p);
 }
 
+using OzEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+OzEncodeFn oz_encoder() {
+    static OzEncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<OzEncodeFn>(f);
+    });
+    return fn;
+}
+// digits of `slices` slices of `panels` 128-row panels x ktiles tiles as
+// (16 B, 128 rows, 4 * ktiles * panels * slices K columns); box rows = box_rows
+bool oz2_encode(CUtensorMap* map, const int8_t* base, long long panels, long long ktiles, int slices, int box_rows) {
+    OzEncodeFn fn = oz_encoder();
+    if (!fn) return false;
+    // 8-byte elements: the innermost box run is 64 rows x 16 B = 1 KiB contiguous
+    // (a 16-byte innermost run measured 1.8x slower: TMA moves short rows poorly)
+    const cuuint64_t dims[3] = {128, 2, static_cast<cuuint64_t>(4 * ktiles * panels * slices)};
+    const cuuint64_t strides[2] = {64 * 16, 128 * 16};
+    const cuuint32_t box[3] = {128, static_cast<cuuint32_t>(box_rows / 64), 4}, estr[3] = {1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<int8_t*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int S>
+bool launch_oz2(const OzakiArgs& p, long long pairs, cudaStream_t s) {
+    CUtensorMap ma, mb;
+    const long long ktiles = p.kpad / OZ_BK;
+    if (!oz2_encode(&ma, p.a, p.mpad / OZ_BM, ktiles, p.slices, OZ_BM) ||
+        !oz2_encode(&mb, p.b, p.npad / OZ_BN, ktiles, p.slices, OZ_BN / 2))
+        return false;
+    const int bytes = static_cast<int>(sizeof(Oz2Smem));
+    set_max_smem_once(reinterpret_cast<const void*>(ozaki_gemm_2sm_kernel<S>), bytes);
+    ozaki_gemm_2sm_kernel<S><<<static_cast<unsigned>(2 * pairs), OZ_THREADS, bytes, s>>>(ma, mb, p);
+    return true;
+}
+
+// The CTA-pair kernel (default; USTATS_OZ_2SM=0 selects the single-SM one):
+// whole launches only (a row-sharded tile range keeps the single-SM tile list).
+bool oz2_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("USTATS_OZ_2SM");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 int launch_ozaki_gemm(const OzakiArgs& in, cudaStream_t s) {
     if (in.kpad % OZ_BK != 0) return -1;
     if (static_cast<long long>(in.slices) * in.kpad * 128 * 128 >= (1ll << 31)) return -1;  // int32 diagonals exact
+    if (oz2_enabled() && in.tile_count < 0 && in.tile_begin == 0 && in.mpad >= 2 * OZ_BM) {
+        OzakiArgs p = in;
+        p.prefetch = 0;
+        p.tail_split = 1;
+        const long long pairs = oz2_pair_count(p);
+        bool ok = false;
+        switch (p.slices) {
+            case 4: ok = launch_oz2<4>(p, pairs, s); break;
+            case 5: ok = launch_oz2<5>(p, pairs, s); break;
+            case 6: ok = launch_oz2<6>(p, pairs, s); break;
+            case 7: ok = launch_oz2<7>(p, pairs, s); break;
+            default: return -1;
+        }
+        if (ok) return 1 + launch_epilogue_finalize(p.m, p.n, p.epis, ozaki_tile_count(p), p.accumulate, s);
+        // no tensor-map encoder: the single-SM kernel below
+    }
     OzakiArgs p = in;
     // warming L2 k-tiles ahead of the bulk copies (p.prefetch > 0) paid with the
     // 2-stage ring of the first version (C2 +2%); with pass 1 on its deeper ring
