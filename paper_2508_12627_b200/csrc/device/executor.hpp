@@ -21,6 +21,7 @@
 // tallied on a counting walk of the reference's own order.
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cstdint>
 #include <map>
@@ -112,6 +113,15 @@ class Runtime {
     bool has_comm() const { return comm_ != nullptr; }
     int comm_world() const { return comm_world_; }
     void allreduce_sum(double* p, std::size_t count);
+    // row sharding: every rank's slab (offset, entries) to every rank, in place
+    void allgather_rows(double* p, const std::vector<std::pair<long long, long long>>& slabs);
+    struct P2P {
+        bool send = true;
+        int peer = 0;
+        double* buf = nullptr;
+        std::size_t count = 0;
+    };
+    void sendrecv(const std::vector<P2P>& ops);  // one NCCL group
 
     enum Kind { kGemm = 0, kStream = 1, kOther = 2 };
     struct Profile {
@@ -236,6 +246,30 @@ struct Op {
     bool dead = false;
 };
 
+// Row-sharded execution plan (shard.cpp): every rank owns rows [lo_r, hi_r)
+// of dim 0 of every intermediate; buffers are replicated (every rank holds
+// all of it), row-sharded (each rank its rows) or partial (each rank holds a
+// summand). Collectives appear only where an op needs a buffer in a state
+// it is not in: all-gather of row slabs, all-reduce of a partial (vectors and
+// scalars only), and the transpose exchange of a symmetric product computed
+// as triangle blocks. The term vector is partial until ONE final all-reduce.
+struct ShardCollective {
+    enum Kind : int { Gather = 0, Reduce = 1, Exchange = 2 } kind = Gather;
+    int buf = -1;
+};
+struct ShardStep {
+    enum Mode : int { Repl = 0, Rows = 1, Part = 2 } mode = Repl;
+    int shard_id = -1;    // iteration id sliced by rows (stream: placed first; gemm: the row id)
+    bool swap = false;    // gemm: operands swapped (symmetric product; the row side is op.fb)
+    bool tri = false;     // gemm: symmetric product as blocks (r, r + d), d <= W / 2, then exchanged
+    std::vector<ShardCollective> before, after;
+};
+
+struct TriPiece {
+    long long r0 = 0, r1 = 0, c0 = 0, c1 = 0;  // C[r0:r1, c0:c1], rows owned by the computing rank
+    int col_owner = 0;                          // owner of rows [c0, c1): receives the transpose
+};
+
 class Program {
   public:
     Program(Runtime* rt, long long n, const Config& config, DevStats* stats)
@@ -290,6 +324,17 @@ class Program {
     void rebind_inputs(const std::vector<Buf>& reals);
     void release_buffers();  // drop every device reference after a run
     void set_stats(DevStats* stats) { stats_ = stats; }
+    // Plans row-sharded execution over `world` ranks (host only, identical on
+    // every rank); dump(): one line per scheduled op plus the collective bytes.
+    void plan_shards(int world);
+    std::string shard_dump(int rank) const;
+    // rows [lo, hi) of dim 0 that rank r owns (every buffer, every op)
+    long long row_lo(int r) const {
+        const int W = std::max(1, shard_planned_world_);
+        return r >= W ? n_ : (n_ * r / W) & ~1LL;
+    }
+    // the pieces of a symmetric product rank r computes (shard.cpp)
+    std::vector<TriPiece> tri_pieces(int r) const;
 
   private:
     std::string desc(const View& v, const std::vector<int>& dims) const;
@@ -304,6 +349,17 @@ class Program {
     std::pair<long long, long long> sweep_strides(const View& v, int row_id, int col_id) const;
     bool tma_plain(const View& v, const std::vector<int>& rows, int e) const;
     void launch(Op& op);
+    void execute_sharded(int world, bool emulate);
+    void run_collective(const ShardCollective& c, bool emulate);
+    void run_tri_gemm(const Op& op, double* out, bool emulate);
+    const ShardStep* step_ = nullptr;      // the current op's shard step (row sharding)
+    bool shard_emulate_ = false;           // virtual ranks on one device (collectives are no-ops)
+    // a block of a GEMM (run_tri_gemm): rows [first, second) of its row id, columns of its column id
+    std::pair<long long, long long> block_rows_{-1, -1}, block_cols_{-1, -1};
+    std::vector<ShardStep> shard_;         // per schedule position
+    std::vector<int> shard_dist_;          // per buffer: final ShardStep::Mode after the plan
+    int shard_planned_world_ = 0;
+    double shard_bytes_[3] = {0, 0, 0};    // per rank and evaluation: gather / reduce / exchange bytes received
     void run_stream(const Op& op, double* out);
     void run_gemm(const Op& op, double* out);
     double* ptr(int buf) const;

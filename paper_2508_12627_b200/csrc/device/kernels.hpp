@@ -187,6 +187,9 @@ int launch_sum_slices(const double* slices, int C, long long len, double* out, i
 // Zeroes the diagonal entries of rows [r0, r1) of an n x n matrix (a panel
 // of a chunked upload).
 int launch_zero_diagonal_rows(double* data, long long n, long long r0, long long r1, cudaStream_t s);
+// dst[c * dst_pitch + r] = src[r * src_pitch + c] for r < rows, c < cols.
+int launch_transpose(const double* src, long long rows, long long cols, long long src_pitch, double* dst,
+                     long long dst_pitch, cudaStream_t s);
 // flag[0] = 0 if the n x n matrix is bitwise symmetric, else 1.
 int launch_symmetry_check(const double* data, long long n, int* flag, cudaStream_t s);
 

@@ -628,6 +628,7 @@ std::vector<double> eliminate_host(const std::vector<const double*>& inputs, con
 std::string plan_summary(const std::vector<IndexTuple>& zero_sig, int m, long long n, const Config& config,
                          bool inputs_symmetric, Program::Totals* totals) {
     TermPlan plan = plan_terms(zero_sig, m, n, LatticeMode::Sparsified, config);
+    if (config.device.shard_rows) plan.owner.assign(plan.owner.size(), 0);  // every rank records every term
     DevStats stats;
     Program prog(nullptr, n, config, &stats);
     // Declared-symmetric inputs: every order-2 factor is the same matrix (the
@@ -651,7 +652,13 @@ std::string plan_summary(const std::vector<IndexTuple>& zero_sig, int m, long lo
     if (totals) *totals = prog.totals();
     std::string head = "terms=" + std::to_string(plan.rgs.size()) + " shared_hits=" + std::to_string(stats.shared_hits) +
                        " ref_madds=" + std::to_string(stats.ref_madds) + "\n";
-    return head + prog.dump();
+    std::string tail;
+    const int W = config.device.world_size;
+    if (config.device.shard_rows && W > 1) {  // the row-sharding plan this rank would run
+        prog.plan_shards(W);
+        tail = "-- shard plan\n" + prog.shard_dump(config.device.rank);
+    }
+    return head + prog.dump() + tail;
 }
 
 }  // namespace ustats::dev

@@ -31,8 +31,8 @@ void Program::run_sweep(const Op& op) {
     a.r0 = 0;
     a.r1 = n_;
     if (slice_world_ > 1) {
-        a.r0 = n_ * slice_rank_ / slice_world_;
-        a.r1 = n_ * (slice_rank_ + 1) / slice_world_;
+        a.r0 = row_lo(slice_rank_);
+        a.r1 = row_lo(slice_rank_ + 1);
         a.accumulate = 1;
         if (a.r1 <= a.r0) return;
     }
@@ -109,6 +109,12 @@ void Program::run_stream(const Op& op, double* out) {
         sums.erase(std::find(sums.begin(), sums.end(), best));
         sums.push_back(best);
     }
+    // row sharding of a reduction to a scalar: the planned id is sliced (dim 0)
+    const int shard_id = (slice_world_ > 1 && step_) ? step_->shard_id : -1;
+    if (shard_id >= 0 && out_ids.empty() && sums.size() > 1 && sums.front() != shard_id) {
+        sums.erase(std::find(sums.begin(), sums.end(), shard_id));
+        sums.insert(sums.begin(), shard_id);
+    }
     // The output dim along which the big non-symmetric operand is contiguous
     // may not be the layout's last (C4: b9{1:1024 2:1 3:n^2} summed over 1
     // into (2,3)): iterate it fastest, one thread per output, writing through
@@ -160,6 +166,17 @@ void Program::run_stream(const Op& op, double* out) {
             const int other = std::countr_zero(v.ids & ~bit(fast));
             std::swap(v.stride[static_cast<std::size_t>(fast)], v.stride[static_cast<std::size_t>(other)]);
         }
+    // a row-sharded symmetric matrix read through its transpose: read it by
+    // rows along the sliced id (this rank holds only those rows)
+    if (shard_id >= 0)
+        for (View& v : factors) {
+            const SymBuf& sb = bufs_[static_cast<std::size_t>(v.buf)];
+            if (sb.input || !sb.symmetric || sb.order != 2 || std::popcount(v.ids) != 2 || !(v.ids & bit(shard_id)))
+                continue;
+            if (v.stride[static_cast<std::size_t>(shard_id)] >= n_) continue;
+            const int other = std::countr_zero(v.ids & ~bit(shard_id));
+            std::swap(v.stride[static_cast<std::size_t>(shard_id)], v.stride[static_cast<std::size_t>(other)]);
+        }
     StreamArgs a;
     a.nf = static_cast<int>(factors.size());
     a.n_out = static_cast<int>(out_ids.size());
@@ -188,7 +205,7 @@ void Program::run_stream(const Op& op, double* out) {
         if (dims.empty()) {
             if (slice_rank_ != 0) return;
         } else {
-            const long long lo = n_ * slice_rank_ / slice_world_, hi = n_ * (slice_rank_ + 1) / slice_world_;
+            const long long lo = row_lo(slice_rank_), hi = row_lo(slice_rank_ + 1);
             if (hi <= lo) return;
             a.n0 = hi - lo;
             for (int f = 0; f < a.nf; ++f) a.ptr[f] += lo * a.stride[f][0];
@@ -426,16 +443,29 @@ void Program::run_gemm(const Op& op, double* out) {
     g.out = out;
     int launched = -1;
     double* scratch = nullptr;
-    const bool multi_path = !op.epis.empty() || (op.symmetric_out && gemm_tma_eligible(g, nullptr, nullptr));
-    if (slice_world_ > 1) {
-        // row sharding: a contiguous range of the tile list per rank
-        const bool tri = multi_path && op.symmetric_out && g.rows == g.cols;
-        const long long total = gemm_tile_total(g, tri);
-        g.tile_begin = total * slice_rank_ / slice_world_;
-        g.tile_count = total * (slice_rank_ + 1) / slice_world_ - g.tile_begin;
+    // Row sharding (shard.cpp): this rank's row panel [lo, hi) of the row id
+    // over every column, or one block of a symmetric product (run_tri_gemm,
+    // `out` is then the block's own rows x cols buffer). Operand pointers are
+    // offset, so every engine sees a smaller plain GEMM.
+    long long row_off = 0;  // first row of the panel (flattened rows: times n^(|ra| - 1))
+    if (block_rows_.first >= 0) {
+        for (int f = 0; f < g.a.nf; ++f) g.a.ptr[f] += block_rows_.first * g.a.rstride[f][0];
+        for (int f = 0; f < g.b.nf; ++f) g.b.ptr[f] += block_cols_.first * g.b.rstride[f][0];
+        g.rows = block_rows_.second - block_rows_.first;
+        g.cols = block_cols_.second - block_cols_.first;
+    } else if (slice_world_ > 1) {
+        const long long lo = row_lo(slice_rank_), hi = row_lo(slice_rank_ + 1);
+        if (hi <= lo) return;
+        const long long inner = static_cast<long long>(ipow(n_, static_cast<int>(op.ra.size()) - 1));
+        for (int f = 0; f < g.a.nf; ++f) g.a.ptr[f] += lo * g.a.rstride[f][0];
+        row_off = lo * inner;
+        g.rows = (hi - lo) * inner;
+        if (g.out) g.out += row_off * g.cols;
+        out = g.out;
+        g.symmetric_out = 0;
         g.accumulate = 1;
-        if (g.tile_count <= 0) return;
     }
+    const bool multi_path = !op.epis.empty() || (g.symmetric_out && gemm_tma_eligible(g, nullptr, nullptr));
     if (multi_path) {
         EpiSet set;
         std::size_t part_total = 0;
@@ -457,6 +487,7 @@ void Program::run_gemm(const Op& op, double* out) {
                 d.wptr[f] = ptr(v.buf);
                 d.wr[f] = v.stride[static_cast<std::size_t>(e.row_id)];
                 d.wc[f] = v.stride[static_cast<std::size_t>(e.col_id)];
+                d.wptr[f] += row_off * d.wr[f];  // a row panel reads its rows of the weights
                 // a symmetric matrix reads the same transposed: make the column stride unit
                 if (bufs_[static_cast<std::size_t>(v.buf)].symmetric && d.wr[f] == 1 && d.wc[f] == n_) {
                     d.wr[f] = n_;
@@ -483,6 +514,8 @@ void Program::run_gemm(const Op& op, double* out) {
                 }
                 d.out = b.real->ptr;
             }
+            // a row panel's row-indexed outputs start at its first row
+            if (d.mode == kEpiSumCols || (d.mode == kEpiStore && !d.transpose)) d.out += row_off * (d.mode == kEpiStore ? g.cols : 1);
             part_total += gemm_epi_partial_entries(g, d.mode);
         }
         scratch = part_total ? rt_->scratch(part_total) : nullptr;
@@ -497,8 +530,8 @@ void Program::run_gemm(const Op& op, double* out) {
         // launch the column-ordered tile triangle in pieces, each as soon as
         // the panels it reads have landed (upload/compute overlap).
         const DeviceBuffer* src = bufs_[static_cast<std::size_t>(fa[0].buf)].real.get();
-        const bool chunked = slice_world_ == 1 && op.symmetric_out && g.rows == g.cols && fa[0].buf == fb[0].buf &&
-                             src && src->ready.size() > 1;
+        const bool chunked = slice_world_ == 1 && block_rows_.first < 0 && g.symmetric_out && g.rows == g.cols &&
+                             fa[0].buf == fb[0].buf && src && src->ready.size() > 1;
         rt_->begin(Runtime::kGemm);
         if (emulated_eligible(g)) {
             // the emulated GEMM digitizes whole operands: an input still arriving
@@ -614,18 +647,13 @@ void Program::run_gemm(const Op& op, double* out) {
     check_cuda(cudaGetLastError(), "gemm launch");
     rt_->release(scratch);
     if (stats_) {
-        const bool tri = op.symmetric_out && g.rows == g.cols && gemm_tma_eligible(g, nullptr, nullptr);
+        const bool tri = g.symmetric_out && g.rows == g.cols && gemm_tma_eligible(g, nullptr, nullptr);
         const long long tm = (g.rows + 127) / 128;
         const std::uint64_t full = static_cast<std::uint64_t>(g.rows) * static_cast<std::uint64_t>(g.cols) *
                                    static_cast<std::uint64_t>(n_);
-        std::uint64_t macs = tri ? full / static_cast<std::uint64_t>(tm * tm) *
-                                       static_cast<std::uint64_t>(tm * (tm + 1) / 2)
-                                 : full;
-        if (slice_world_ > 1 && g.tile_count >= 0) {
-            const long long total = gemm_tile_total(g, tri);
-            macs = static_cast<std::uint64_t>(static_cast<double>(macs) * static_cast<double>(g.tile_count) /
-                                              static_cast<double>(total));
-        }
+        const std::uint64_t macs = tri ? full / static_cast<std::uint64_t>(tm * tm) *
+                                             static_cast<std::uint64_t>(tm * (tm + 1) / 2)
+                                       : full;
         stats_->gemm_macs += macs;
         ++stats_->gemm_launches;
         stats_->kernel_launches += static_cast<std::uint64_t>(launched);
@@ -649,7 +677,8 @@ void Program::launch(Op& op) {
         b.real->symmetric = b.symmetric;
         out = b.real->ptr;
     }
-    if (op.gemm) run_gemm(op, out);
+    if (op.gemm && step_ && step_->tri && slice_world_ > 1) run_tri_gemm(op, out, shard_emulate_);
+    else if (op.gemm) run_gemm(op, out);
     else run_stream(op, out);
 }
 
@@ -664,40 +693,8 @@ void Program::execute() {
     const int emulate = dc.shard_rows && dc.emulate_world > 1 ? dc.emulate_world : 0;
     const int world = emulate ? emulate : (dc.shard_rows ? std::max(1, dc.world_size) : 1);
     if (world > 1) {
-        // Row sharding: each op runs as a slice per rank into zeroed outputs;
-        // with NCCL one all-reduce per materialized output completes it, in
-        // emulation the virtual ranks' slices accumulate on this device.
-        const bool collective = !emulate && rt_->has_comm();
-        if (!emulate && !collective) fail(ErrorCode::CollectiveError, "row sharding needs us_nccl_init first");
-        rt_->set_stream(rt_->main_stream());
-        for (const SymBuf& b : bufs_)
-            if (b.input && b.real && !b.real->ready.empty())
-                check_cuda(cudaStreamWaitEvent(rt_->main_stream(), b.real->ready.back().second, 0), "wait upload");
-        slice_world_ = world;
-        for (std::size_t pos = 0; pos < schedule_.size(); ++pos) {
-            Op& op = ops_[schedule_[pos]];
-            for (int r = (emulate ? 0 : dc.rank); r < (emulate ? world : dc.rank + 1); ++r) {
-                slice_rank_ = r;
-                launch(op);
-            }
-            if (collective) {
-                auto reduce = [&](int b) {
-                    SymBuf& sb = bufs_[static_cast<std::size_t>(b)];
-                    if (sb.real) rt_->allreduce_sum(sb.real->ptr, sb.real->entries());
-                };
-                if (!op.ext && op.out >= 0 && (!op.gemm || op.store)) reduce(op.out);
-                for (const Op::Epi& e : op.epis)
-                    if (!e.ext && e.out >= 0) reduce(e.out);
-            }
-            for_each_read(op, [&](const View& v) {
-                SymBuf& b = bufs_[static_cast<std::size_t>(v.buf)];
-                if (!b.input && b.last_use == static_cast<int>(pos) && b.real && b.real.use_count() == 1 &&
-                    !keep_.count(v.buf))
-                    b.real.reset();
-            });
-        }
-        slice_world_ = 1;
-        slice_rank_ = 0;
+        if (!emulate && !rt_->has_comm()) fail(ErrorCode::CollectiveError, "row sharding needs us_nccl_init first");
+        execute_sharded(world, emulate != 0);
         return;
     }
     bool has_gemm = false;

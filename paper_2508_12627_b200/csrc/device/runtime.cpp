@@ -221,10 +221,16 @@ struct NcclApi {
     using Init = int (*)(void**, int, std::array<char, 128>, int);
     using AllReduce = int (*)(const void*, void*, std::size_t, int, int, void*, cudaStream_t);
     using ErrStr = const char* (*)(int);
+    using Bcast = int (*)(const void*, void*, std::size_t, int, int, void*, cudaStream_t);
+    using P2POp = int (*)(const void*, std::size_t, int, int, void*, cudaStream_t);  // ncclSend / ncclRecv
+    using Group = int (*)();
     GetId get_id = nullptr;
     Init init = nullptr;
     AllReduce all_reduce = nullptr;
     ErrStr err = nullptr;
+    Bcast bcast = nullptr;
+    P2POp send = nullptr, recv = nullptr;
+    Group group_start = nullptr, group_end = nullptr;
 };
 
 const NcclApi& nccl() {
@@ -238,6 +244,11 @@ const NcclApi& nccl() {
         api.init = reinterpret_cast<NcclApi::Init>(dlsym(h, "ncclCommInitRank"));
         api.all_reduce = reinterpret_cast<NcclApi::AllReduce>(dlsym(h, "ncclAllReduce"));
         api.err = reinterpret_cast<NcclApi::ErrStr>(dlsym(h, "ncclGetErrorString"));
+        api.bcast = reinterpret_cast<NcclApi::Bcast>(dlsym(h, "ncclBroadcast"));
+        api.send = reinterpret_cast<NcclApi::P2POp>(dlsym(h, "ncclSend"));
+        api.recv = reinterpret_cast<NcclApi::P2POp>(dlsym(h, "ncclRecv"));
+        api.group_start = reinterpret_cast<NcclApi::Group>(dlsym(h, "ncclGroupStart"));
+        api.group_end = reinterpret_cast<NcclApi::Group>(dlsym(h, "ncclGroupEnd"));
     });
     if (!api.get_id || !api.init || !api.all_reduce) fail(ErrorCode::CollectiveError, "libnccl.so.2 not available");
     return api;
@@ -282,6 +293,35 @@ void Runtime::allreduce_sum(double* p, std::size_t count) {
     if (!comm_ || comm_world_ <= 1 || count == 0) return;
     constexpr int kNcclFloat64 = 8, kNcclSum = 0;  // nccl.h enum values
     nccl_check(nccl().all_reduce(p, p, count, kNcclFloat64, kNcclSum, comm_, cur_), "ncclAllReduce");
+}
+
+// Row slabs [off_r, off_r + len_r) of every rank to every rank, in place:
+// one broadcast per rank inside one NCCL group (slabs may differ in size).
+void Runtime::allgather_rows(double* p, const std::vector<std::pair<long long, long long>>& slabs) {
+    if (!comm_ || comm_world_ <= 1) return;
+    const NcclApi& api = nccl();
+    if (!api.bcast || !api.group_start || !api.group_end) fail(ErrorCode::CollectiveError, "ncclBroadcast not available");
+    constexpr int kNcclFloat64 = 8;
+    nccl_check(api.group_start(), "ncclGroupStart");
+    for (std::size_t r = 0; r < slabs.size(); ++r)
+        if (slabs[r].second > 0)
+            nccl_check(api.bcast(p + slabs[r].first, p + slabs[r].first, static_cast<std::size_t>(slabs[r].second),
+                                 kNcclFloat64, static_cast<int>(r), comm_, cur_),
+                       "ncclBroadcast");
+    nccl_check(api.group_end(), "ncclGroupEnd");
+}
+
+void Runtime::sendrecv(const std::vector<P2P>& ops) {
+    if (!comm_ || comm_world_ <= 1 || ops.empty()) return;
+    const NcclApi& api = nccl();
+    if (!api.send || !api.recv || !api.group_start || !api.group_end)
+        fail(ErrorCode::CollectiveError, "ncclSend / ncclRecv not available");
+    constexpr int kNcclFloat64 = 8;
+    nccl_check(api.group_start(), "ncclGroupStart");
+    for (const P2P& o : ops)
+        nccl_check((o.send ? api.send : api.recv)(o.buf, o.count, kNcclFloat64, o.peer, comm_, cur_),
+                   o.send ? "ncclSend" : "ncclRecv");
+    nccl_check(api.group_end(), "ncclGroupEnd");
 }
 
 void Runtime::begin(Kind k) {

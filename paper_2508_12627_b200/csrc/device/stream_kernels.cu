@@ -836,6 +836,32 @@ int launch_zero_diagonal_rows(double* data, long long n, long long r0, long long
     return 1;
 }
 
+// 32 x 32 tiles through shared memory (one padding column: conflict-free
+// column reads), 8 rows per thread: coalesced reads and writes.
+__global__ void __launch_bounds__(256) transpose_kernel(const double* __restrict__ src, long long rows, long long cols,
+                                                        long long sp, double* __restrict__ dst, long long dp) {
+    __shared__ double t[32][33];
+    const long long r0 = static_cast<long long>(blockIdx.y) * 32, c0 = static_cast<long long>(blockIdx.x) * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int i = ty; i < 32; i += 8) {
+        const long long r = r0 + i, c = c0 + tx;
+        if (r < rows && c < cols) t[i][tx] = src[r * sp + c];
+    }
+    __syncthreads();
+    for (int i = ty; i < 32; i += 8) {
+        const long long c = c0 + i, r = r0 + tx;
+        if (r < rows && c < cols) dst[c * dp + r] = t[tx][i];
+    }
+}
+
+int launch_transpose(const double* src, long long rows, long long cols, long long src_pitch, double* dst,
+                     long long dst_pitch, cudaStream_t s) {
+    if (rows <= 0 || cols <= 0) return 0;
+    const dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+    transpose_kernel<<<grid, 256, 0, s>>>(src, rows, cols, src_pitch, dst, dst_pitch);
+    return 1;
+}
+
 int launch_symmetry_check(const double* data, long long n, int* flag, cudaStream_t s) {
     cudaMemsetAsync(flag, 0, sizeof(int), s);
     unsigned long long blocks = (static_cast<unsigned long long>(n) * n + 255) / 256;

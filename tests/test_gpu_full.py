@@ -133,3 +133,21 @@ def test_signed_cancellation_emulated_vs_reference(engine):
         _, _, v, _ = REF.u_terms(mats, sig, m, threads=0)
         scale = float(np.max(np.abs(v)))
         assert float(np.max(np.abs(got.v - v))) <= TOL * scale
+
+
+@pytest.mark.parametrize("fixture,world", [("C5_n2048.npz", 8), ("C5_n1024.npz", 3), ("C4_n96.npz", 4),
+                                           ("C3_n1024.npz", 8), ("C2_n1024.npz", 2)])
+def test_golden_row_sharded(engine, fixture, world):
+    # the multi-GPU decomposition (row panels, triangle pieces + transpose
+    # exchange, partial reductions, one final all-reduce of the V-terms) run by
+    # `world` virtual ranks, pinned to the REFERENCE's goldens
+    from paper_2508_12627_b200.workloads import generate
+    g = np.load(GOLDEN / fixture)
+    name, n = fixture.split("_n")
+    n = int(n.split(".")[0])
+    factors, sig, m, _ = generate(name, n)
+    cfg = engine.Config(memory_cap_entries=max(2 ** 31, n ** 3 + 1), shard_rows=True, emulate_world=world)
+    got = engine.u_terms(factors, sig, m, cfg)
+    scale = float(np.max(np.abs(g["v"])))
+    assert float(np.max(np.abs(got.v - g["v"]))) <= TOL * scale
+    assert abs(got.value - float(g["u"])) <= TOL * scale

@@ -246,10 +246,13 @@ def test_hoif_tau_closed_forms(engine):
 
 
 @pytest.mark.parametrize("name,n,world", [("C2", 200, 3), ("C3", 130, 4), ("C4", 40, 3), ("C5", 130, 5),
-                                          ("C1", 101, 2)])
+                                          ("C1", 101, 2), ("C5", 300, 8), ("C5", 257, 2), ("C4", 48, 4),
+                                          ("C3", 384, 8)])
 def test_row_sharding_emulated(engine, name, n, world):
-    # every op split into `world` slices (GEMM tile ranges, leading-index
-    # ranges) accumulated on one device in lockstep == the unsharded result
+    # the row-sharding plan (shard.cpp) run by `world` virtual ranks on one
+    # device, one after the other: row panels of every op, symmetric products
+    # as balanced triangle pieces with their transposes stored by the column
+    # owner, partial reductions accumulated == the unsharded result
     from paper_2508_12627_b200.workloads import generate
     factors, sig, m, _ = generate(name, n)
     base = engine.u_terms(factors, sig, m)
@@ -362,7 +365,7 @@ def test_data_path_repeatable_at_scale(engine, name, n):
 
 @pytest.mark.parametrize("name,n,world", [("C2", 2304, 3), ("C3", 2048, 2)])
 def test_emulated_gemm_row_sharding(engine, name, n, world):
-    # the INT8-emulated GEMM (n >= 2048) over virtual ranks' tile ranges == unsharded;
+    # the INT8-emulated GEMM (n >= 2048) over virtual ranks' row panels / pieces == unsharded;
     # both within the north-star tolerance of the DMMA path
     from paper_2508_12627_b200.workloads import generate
     factors, sig, m, _ = generate(name, n)
@@ -395,9 +398,9 @@ def test_emulated_gemm_k_chunks(engine, name, n):
 
 
 def test_emulated_gemm_k_chunks_row_sharded(engine):
-    # the multi-GPU decomposition of C5 (row sharding: each rank a range of every
-    # GEMM's tile list, digitizing only its panels, per K chunk), on virtual
-    # ranks in lockstep: equal to the unsharded K-chunked evaluation
+    # the multi-GPU decomposition of C5 (row sharding: each rank its row panel
+    # or triangle pieces of every GEMM, digitizing only its operand rows, per K
+    # chunk), on virtual ranks: equal to the unsharded K-chunked evaluation
     from paper_2508_12627_b200.workloads import generate
     factors, sig, m, _ = generate("C5", 21056)
     base = engine.u_terms(factors, sig, m)
