@@ -124,6 +124,15 @@ US_API int us_u_statistic_data(const char* kernel, const double* data, int64_t n
  * us_motif_count: motif_count (motifs.hpp:47-48) of motif id "r1".."r8" in the
  *   graph on vertices 0..n-1 given by edge_count (u, v) pairs (host int32);
  *   NonIntegerResult when the scaled count is not integral. */
+/* hoif_tau (hoif.hpp:44-48, hoif.cpp:74-100) with the truncation basis
+ * phi(z) = z[0..k) (truncation_phi, hoif.cpp:37-47) on a sample of n rows
+ * [A, Y, Z_1..Z_{d-2}] (row-major, host or device): the two component
+ * matrices are tensorized on the device, the chain orders 2..m run as one
+ * program, and the alternating-sign combination accumulates in long double.
+ * InvalidArgument for m < 2, k < 1 or d < 2 + k; SampleTooSmall for n < m. */
+US_API int us_hoif_tau(int32_t m, int32_t k, const double* data, int64_t n, int32_t d, int32_t on_device,
+                       const us_config* cfg, double* tau_out, us_stats* stats);
+
 US_API int us_dcov_squared(const double* x, int32_t dx, const double* y, int32_t dy, int64_t n,
                            int32_t on_device, const us_config* cfg, double* out, us_stats* stats);
 US_API int us_motif_count(int64_t n, int64_t edge_count, const int32_t* edges, const char* motif_id,

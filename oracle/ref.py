@@ -42,6 +42,7 @@ def lib():
         _lib.ref_complexity_report.argtypes = [C.c_int, I32P, I32P, C.c_int, I32P, C.POINTER(C.c_uint64),
                                                C.POINTER(C.c_uint64), C.c_char_p, C.c_int]
         _lib.ref_dcov_squared.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, F64P]
+        _lib.ref_hoif_tau.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, F64P]
         _lib.ref_motif_count.argtypes = [C.c_int, C.c_int, I32P, C.c_char_p, C.c_int, C.POINTER(C.c_longlong)]
         _lib.ref_last_error.restype = C.c_char_p
     return _lib
@@ -193,6 +194,14 @@ def dcov_squared(x, y, threads=0):
     out = C.c_double()
     _check(lib().ref_dcov_squared(x.ctypes.data, x.shape[1], y.ctypes.data, y.shape[1], x.shape[0], threads,
                                   C.byref(out)))
+    return out.value
+
+
+def hoif_tau(m, k, data, threads=0):
+    """The reference's hoif_tau with truncation_phi(k) on rows [A, Y, Z...]."""
+    x = np.ascontiguousarray(data, dtype=np.float64)
+    out = C.c_double()
+    _check(lib().ref_hoif_tau(m, k, x.ctypes.data, x.shape[0], x.shape[1], threads, C.byref(out)))
     return out.value
 
 

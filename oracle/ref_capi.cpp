@@ -313,6 +313,21 @@ int ref_dcov_squared(const double* x, int dx, const double* y, int dy, int n, in
     }
 }
 
+// hoif_tau (hoif.cpp:74-100) with truncation_phi(k) on rows [A, Y, Z...].
+int ref_hoif_tau(int m, int k, const double* data, int n, int d, int threads, double* out) {
+    try {
+        std::vector<ustats::Observation> rows(static_cast<std::size_t>(n));
+        for (int i = 0; i < n; ++i)
+            rows[static_cast<std::size_t>(i)].assign(data + static_cast<std::size_t>(i) * d,
+                                                     data + static_cast<std::size_t>(i + 1) * d);
+        ustats::Sample s(std::move(rows));
+        *out = ustats::hoif_tau(m, ustats::truncation_phi(k), s, config_of(threads, 0));
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
 // motif_count (motifs.cpp:53-69) on the graph over vertices 0..n-1.
 int ref_motif_count(int n, int edge_count, const int* edges, const char* id, int threads, long long* out) {
     try {

@@ -100,6 +100,7 @@ SIGNATURES = {
     "us_optimize_order": (C.c_int, [i32, P(i32), P(i32), i32, P(i32), P(i32), P(i32)]),
     "us_treewidth": (C.c_int, [i32, i32, P(i32), P(i32), P(i32)]),
     "us_dcov_squared": (C.c_int, [C.c_void_p, i32, C.c_void_p, i32, i64, i32, P(UsConfig), P(f64), P(UsStats)]),
+    "us_hoif_tau": (C.c_int, [i32, i32, C.c_void_p, i64, i32, i32, P(UsConfig), P(f64), P(UsStats)]),
     "us_motif_count": (C.c_int, [i64, i64, P(i32), C.c_char_p, P(UsConfig), P(i64), P(UsStats)]),
     "us_dgemm": (C.c_int, [i32, i32, i32, i64, i64, i64, C.c_void_p, C.c_void_p, C.c_void_p, P(f64)]),
     "us_complexity_report": (C.c_int, [i32, P(i32), P(i32), i32, P(UsConfig), P(UsComplexity), C.c_char_p, i32]),

@@ -216,33 +216,19 @@ def u_statistic_batch(problems, config: Config | None = None, with_stats: bool =
     return (vals, st.as_dict()) if with_stats else vals
 
 
-def hoif_tau(m: int, k: int, data, config: Config | None = None) -> float:
-    """hoif_tau (hoif.cpp:74-100): sum_{j=2..m} (-1)^j sum_{l=0..j-2} C(j-2,l)
-    (n-l)!/n! U(hoif:l+2:k), with every chain order evaluated in ONE program
-    (the reference makes m-1 separate u_statistic calls)."""
-    from math import comb
-    x = np.asarray(data, dtype=np.float64)
-    n = x.shape[0]
-    if m < 2:
-        raise UStatsError("InvalidArgument", "statistic order must be >= 2")
-    if n < m:
-        raise UStatsError("SampleTooSmall", f"need at least {m} observations, have {n}")
-    factors, _, _ = kernel_tensors(f"hoif:{m}:{k}", x)
-    middle, last = (factors[0] if m > 2 else None), factors[-1]
-    problems = []
-    for order in range(2, m + 1):
-        fs = [middle] * (order - 2) + [last]
-        problems.append((fs, [[i, i + 1] for i in range(order - 1)], order))
-    u = dict(zip(range(2, m + 1), u_statistic_batch(problems, config)))
-    tau = 0.0
-    for j in range(2, m + 1):
-        sign = 1.0 if j % 2 == 0 else -1.0
-        for l in range(j - 1):
-            w = 1.0
-            for i in range(l):
-                w /= (n - i)
-            tau += sign * comb(j - 2, l) * w * u[l + 2]
-    return tau
+def hoif_tau(m: int, k: int, data, config: Config | None = None, with_stats: bool = False):
+    """hoif_tau (hoif.cpp:74-100) with phi = truncation_phi(k) on a sample of
+    rows [A, Y, Z...] (host array or CUDA tensor): the component matrices are
+    tensorized on the GPU, every chain order 2..m runs in ONE program (the
+    reference makes m - 1 separate u_statistic calls) and the combination
+    accumulates in long double, as the reference does (us_hoif_tau)."""
+    p, n, d, on_device, keep = _sample_arg(data, "data")
+    out = N.f64()
+    st = N.UsStats()
+    _check(N.lib().us_hoif_tau(m, k, C.c_void_p(p), n, d, on_device, C.byref((config or Config()).native()),
+                               C.byref(out), C.byref(st)))
+    del keep
+    return (out.value, st.as_dict()) if with_stats else out.value
 
 
 def u_statistic_unsparsified_tensors(factors, signature, m: int | None = None, config: Config | None = None):

@@ -251,6 +251,16 @@ int us_dcov_squared(const double* x, int32_t dx, const double* y, int32_t dy, in
     });
 }
 
+int us_hoif_tau(int32_t m, int32_t k, const double* data, int64_t n, int32_t d, int32_t on_device, const us_config* cfg,
+                double* tau_out, us_stats* stats) {
+    return guarded([&] {
+        if (!data || !tau_out) ustats::fail(ustats::ErrorCode::InvalidArgument, "null argument");
+        auto r = ustats::dev::hoif_tau_data(m, k, data, n, d, on_device != 0, to_config(cfg));
+        *tau_out = r.value;
+        export_dev(r, cfg ? cfg->rank : 0, stats);
+    });
+}
+
 int us_motif_count(int64_t n, int64_t edge_count, const int32_t* edges, const char* motif_id, const us_config* cfg,
                    int64_t* count, us_stats* stats) {
     return guarded([&] {

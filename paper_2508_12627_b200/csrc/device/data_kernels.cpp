@@ -321,6 +321,77 @@ StatisticResult dcov_squared(const double* x, int dx, const double* y, int dy, l
     return r;
 }
 
+double hoif_combine(int m, long long n, const std::vector<double>& u) {
+    auto binom = [](int a, int b) {
+        std::uint64_t v = 1;
+        for (int i = 0; i < b; ++i) v = v * static_cast<std::uint64_t>(a - i) / static_cast<std::uint64_t>(i + 1);
+        return v;
+    };
+    long double tau = 0.0L;
+    for (int j = 2; j <= m; ++j) {
+        const double sign = j % 2 == 0 ? 1.0 : -1.0;
+        for (int l = 0; l + 2 <= j; ++l) {
+            long double w = 1.0L;  // (n - l)! / n!
+            for (int i = 0; i < l; ++i) w /= static_cast<long double>(n - i);
+            tau += sign * static_cast<long double>(binom(j - 2, l)) * w *
+                   static_cast<long double>(u[static_cast<std::size_t>(l + 2)]);
+        }
+    }
+    return static_cast<double>(tau);
+}
+
+StatisticResult hoif_tau_data(int m, int k, const double* data, long long n, int d, bool on_device,
+                              const Config& config) {
+    if (m < 2) fail(ErrorCode::InvalidArgument, "statistic order must be >= 2");
+    if (k < 1) fail(ErrorCode::InvalidArgument, "basis size must be >= 1");
+    if (d < 2 + k) fail(ErrorCode::InvalidArgument, "covariate block shorter than the basis");
+    if (n < m)
+        fail(ErrorCode::SampleTooSmall, "need at least " + std::to_string(m) + " observations, have " + std::to_string(n));
+    checked_entry_count(2, static_cast<int>(n), config);
+    Runtime& rt = Runtime::get(config.device.device);
+    cudaStream_t s = rt.main_stream();
+    rt.set_stream(s);
+    Buf sample;
+    const double* x = data;
+    if (!on_device) {
+        sample = rt.allocate(1, n * d);
+        check_cuda(cudaMemcpyAsync(sample->ptr, data, static_cast<std::size_t>(n * d) * sizeof(double),
+                                   cudaMemcpyHostToDevice, s),
+                   "upload sample");
+        x = sample->ptr;
+    }
+    // A_x phi(Z_x).phi(Z_y) A_y (middle) and A_x phi(Z_x).phi(Z_y) Y_y (last)
+    Buf last = rt.allocate(2, n), middle;
+    launch_scaled_gram(x, n, d, 0, 1, 2, k, last->ptr, s);
+    std::uint64_t launches = 1;
+    if (m > 2) {
+        middle = rt.allocate(2, n);
+        launch_scaled_gram(x, n, d, 0, 0, 2, k, middle->ptr, s);
+        ++launches;
+    }
+    check_cuda(cudaGetLastError(), "tensorize");
+    std::vector<StatisticSpec> specs;
+    for (int order = 2; order <= m; ++order) {
+        StatisticSpec sp;
+        sp.m = order;
+        for (int i = 0; i + 1 < order; ++i) {
+            sp.sig.push_back({i, i + 1});
+            const bool mid = i + 2 < order;
+            sp.inputs.push_back(mid ? middle->ptr : last->ptr);
+            sp.symmetric.push_back(0);  // probed: (A_x dot) A_y and (A_y dot) A_x may differ in the last bit
+        }
+        specs.push_back(std::move(sp));
+    }
+    Config cfg = config;
+    cfg.device.donate_inputs = true;
+    auto res = lattice_batch(specs, true, n, LatticeMode::Sparsified, cfg);
+    std::vector<double> u(static_cast<std::size_t>(m + 1), 0.0);
+    for (int order = 2; order <= m; ++order) u[static_cast<std::size_t>(order)] = res[static_cast<std::size_t>(order - 2)].value;
+    StatisticResult r = merged(res, hoif_combine(m, n, u));
+    r.stats.kernel_launches += launches;
+    return r;
+}
+
 const std::vector<MotifSpec>& motif_catalog() {
     // induced patterns on 3-4 vertices (motifs.hpp:33-36): edges that must be
     // present / absent, automorphism counts

@@ -480,6 +480,15 @@ std::vector<double> eliminate_host(const std::vector<const double*>& inputs, con
 
 double combine_terms(const std::vector<double>& terms);
 
+// hoif_tau's combination of the chain statistics u[2..m] (hoif.cpp:88-97):
+// sum_j (-1)^j sum_l C(j-2, l) (n-l)!/n! u[l+2], accumulated in long double.
+double hoif_combine(int m, long long n, const std::vector<double>& u);
+// hoif_tau with the truncation basis phi(z) = z[0..k) on a sample [A, Y, Z...]
+// (n x d, row-major, host or device): both component matrices tensorized on
+// the device, the chain orders 2..m in one program.
+StatisticResult hoif_tau_data(int m, int k, const double* data, long long n, int d, bool on_device,
+                              const Config& config);
+
 // Plan-only view of a statistic (no GPU): the optimized Program's ops and totals.
 std::string plan_summary(const std::vector<IndexTuple>& zero_sig, int m, long long n, const Config& config,
                          bool inputs_symmetric, Program::Totals* totals);

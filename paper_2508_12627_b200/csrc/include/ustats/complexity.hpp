@@ -13,6 +13,8 @@
 #include "ustats/config.hpp"
 #include "ustats/notation.hpp"
 
+// the public C++ API is exported from libustats_b200.so (built -fvisibility=hidden)
+#pragma GCC visibility push(default)
 namespace ustats {
 
 struct ComplexityReport {
@@ -37,3 +39,4 @@ ComplexityReport complexity_report(const std::vector<IndexTuple>& signature, int
 std::vector<IndexTuple> chain_signature(int m);
 
 }  // namespace ustats
+#pragma GCC visibility pop

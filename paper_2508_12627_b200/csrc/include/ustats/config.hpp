@@ -6,6 +6,8 @@
 
 #include <cstdint>
 
+// the public C++ API is exported from libustats_b200.so (built -fvisibility=hidden)
+#pragma GCC visibility push(default)
 namespace ustats {
 
 enum class OrderStrategy { Auto, GreedyMinDegree, GreedyMinFill, Exhaustive };
@@ -57,3 +59,4 @@ struct Config {
 };
 
 }  // namespace ustats
+#pragma GCC visibility pop

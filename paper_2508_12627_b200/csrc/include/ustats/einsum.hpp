@@ -13,6 +13,8 @@
 #include "ustats/ordering.hpp"
 #include "ustats/tensor.hpp"
 
+// the public C++ API is exported from libustats_b200.so (built -fvisibility=hidden)
+#pragma GCC visibility push(default)
 namespace ustats {
 
 struct ExecStats {
@@ -31,3 +33,4 @@ std::pair<DenseTensor, IndexTuple> eliminate_index(std::span<const DenseTensor> 
                                                    ExecStats* stats = nullptr);
 
 }  // namespace ustats
+#pragma GCC visibility pop

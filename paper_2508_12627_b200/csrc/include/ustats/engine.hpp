@@ -13,6 +13,8 @@
 #include "ustats/partition.hpp"
 #include "ustats/tensor.hpp"
 
+// the public C++ API is exported from libustats_b200.so (built -fvisibility=hidden)
+#pragma GCC visibility push(default)
 namespace ustats {
 
 struct RunStats {
@@ -52,3 +54,4 @@ double u_statistic_tensors(std::span<const DenseTensor> tensors,
                            std::vector<double>* terms = nullptr);
 
 }  // namespace ustats
+#pragma GCC visibility pop

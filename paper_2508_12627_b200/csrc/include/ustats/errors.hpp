@@ -6,6 +6,8 @@
 #include <stdexcept>
 #include <string>
 
+// the public C++ API is exported from libustats_b200.so (built -fvisibility=hidden)
+#pragma GCC visibility push(default)
 namespace ustats {
 
 enum class ErrorCode {
@@ -46,3 +48,4 @@ class Error : public std::runtime_error {
 [[noreturn]] void fail(ErrorCode code, const std::string& message);
 
 }  // namespace ustats
+#pragma GCC visibility pop

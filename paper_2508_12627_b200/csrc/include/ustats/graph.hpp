@@ -6,6 +6,8 @@
 
 #include "ustats/notation.hpp"
 
+// the public C++ API is exported from libustats_b200.so (built -fvisibility=hidden)
+#pragma GCC visibility push(default)
 namespace ustats {
 
 class SetPartition;
@@ -39,3 +41,4 @@ SimpleGraph eliminate_vertex(const SimpleGraph& g, int v);
 SimpleGraph quotient_graph(const SimpleGraph& g, const SetPartition& partition);
 
 }  // namespace ustats
+#pragma GCC visibility pop

@@ -8,6 +8,8 @@
 
 #include "ustats/notation.hpp"
 
+// the public C++ API is exported from libustats_b200.so (built -fvisibility=hidden)
+#pragma GCC visibility push(default)
 namespace ustats {
 
 using Observation = std::vector<double>;
@@ -36,3 +38,4 @@ struct MDKernel {
 MDKernel prod2_kernel();
 
 }  // namespace ustats
+#pragma GCC visibility pop

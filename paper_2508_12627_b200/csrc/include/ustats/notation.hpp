@@ -5,6 +5,8 @@
 #include <string>
 #include <vector>
 
+// the public C++ API is exported from libustats_b200.so (built -fvisibility=hidden)
+#pragma GCC visibility push(default)
 namespace ustats {
 
 using IndexTuple = std::vector<int>;
@@ -25,3 +27,4 @@ EinsumNotation validate_notation(const std::vector<IndexTuple>& raw_inputs,
                                  const IndexTuple& raw_output = {});
 
 }  // namespace ustats
+#pragma GCC visibility pop

@@ -7,6 +7,8 @@
 #include "ustats/config.hpp"
 #include "ustats/notation.hpp"
 
+// the public C++ API is exported from libustats_b200.so (built -fvisibility=hidden)
+#pragma GCC visibility push(default)
 namespace ustats {
 
 struct EliminationOrder {
@@ -27,3 +29,4 @@ std::vector<std::vector<int>> optimal_orders(const EinsumNotation& notation, int
                                              std::size_t limit);
 
 }  // namespace ustats
+#pragma GCC visibility pop

@@ -8,6 +8,8 @@
 
 #include "ustats/notation.hpp"
 
+// the public C++ API is exported from libustats_b200.so (built -fvisibility=hidden)
+#pragma GCC visibility push(default)
 namespace ustats {
 
 class SetPartition {
@@ -66,3 +68,4 @@ std::vector<IndexTuple> induced_signature(const std::vector<IndexTuple>& signatu
                                           const SetPartition& partition);
 
 }  // namespace ustats
+#pragma GCC visibility pop

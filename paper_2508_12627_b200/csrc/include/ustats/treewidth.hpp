@@ -6,6 +6,8 @@
 #include "ustats/config.hpp"
 #include "ustats/graph.hpp"
 
+// the public C++ API is exported from libustats_b200.so (built -fvisibility=hidden)
+#pragma GCC visibility push(default)
 namespace ustats {
 
 struct TreewidthResult {
@@ -22,3 +24,4 @@ int degeneracy(const SimpleGraph& g);
 int max_treewidth_by_edges(int e);
 
 }  // namespace ustats
+#pragma GCC visibility pop
