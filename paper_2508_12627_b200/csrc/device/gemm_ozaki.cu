@@ -560,13 +560,44 @@ __host__ __device__ __forceinline__ long long oz2_pair_count(const OzakiArgs& p)
 }
 __host__ __device__ __forceinline__ void oz2_pair_of(const OzakiArgs& p, long long bid, long long* pm, long long* tn) {
     const long long T_m = p.mpad / OZ_BM, T_n = p.npad / OZ_BN, P_m = (T_m + 1) / 2;
-    if (!p.symmetric) {  // groups of OZ2_GROUP pair rows x all columns, column-major inside
-        const long long width = OZ2_GROUP * T_n;
-        const long long g = bid / width, m0 = g * OZ2_GROUP;
-        const long long gsz = (P_m - m0) < OZ2_GROUP ? (P_m - m0) : OZ2_GROUP;
+    if (!p.symmetric) {  // groups of G pair rows x all columns, column-major inside
+        const long long G = p.group2 > 0 ? p.group2 : OZ2_GROUP;
+        const long long width = G * T_n;
+        const long long g = bid / width, m0 = g * G;
+        const long long gsz = (P_m - m0) < G ? (P_m - m0) : G;
         const long long rem = bid - g * width;
         *pm = m0 + rem % gsz;
         *tn = rem / gsz;
+        return;
+    }
+    if (p.sym_group2 > 0) {
+        // groups of G pair rows x their columns (tn >= 2 pm), column-major
+        // inside: the group's A panels stay in L2 while the B panels stream by
+        const long long G = p.sym_group2;
+        for (long long m0 = 0; m0 < P_m; m0 += G) {
+            const long long gsz = (P_m - m0) < G ? (P_m - m0) : G;
+            long long total = 0;
+            for (long long q = m0; q < m0 + gsz; ++q) total += T_n - 2 * q;
+            if (bid >= total) {
+                bid -= total;
+                continue;
+            }
+            long long c = 2 * m0;
+            for (; c < 2 * (m0 + gsz - 1); ++c) {  // the ramp: pair rows m0 .. c / 2
+                const long long h = c / 2 - m0 + 1;
+                if (bid < h) {
+                    *pm = m0 + bid;
+                    *tn = c;
+                    return;
+                }
+                bid -= h;
+            }
+            *pm = m0 + bid % gsz;
+            *tn = c + bid / gsz;
+            return;
+        }
+        *pm = 0;
+        *tn = 0;
         return;
     }
     // column groups of OZ_GROUP columns: the pair-row groups fully above the
@@ -671,6 +702,15 @@ __device__ __forceinline__ void oz2_tma(void* dst, const CUtensorMap* map, int h
         "l"(reinterpret_cast<unsigned long long>(map)), "r"(0), "r"(half), "r"(col), "r"(leader_bar)
         : "memory");
 }
+// the same with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void oz2_tma_hint(void* dst, const CUtensorMap* map, int half, int col, unsigned leader_bar,
+                                             unsigned long long policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+        "[%1, {%2, %3, %4}], [%5], %6;" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(0), "r"(half), "r"(col), "r"(leader_bar), "l"(policy)
+        : "memory");
+}
 __device__ __forceinline__ unsigned oz2_leader_addr(const void* p) {
     unsigned remote;
     asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(su32(p)));
@@ -724,9 +764,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_THREADS, 1)
     if (tid == 128) {  // producer (both CTAs): own A panel, own half of the B panel, bytes counted on the even CTA
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&map_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&map_b)) : "memory");
+        unsigned long long pol_a = 0, pol_b = 0;  // A panels are re-read across the row group's columns
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_a));
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_b));
         auto load_stage = [&](long long k, int ns, int slot0, unsigned long long* bar) {
             if (rank == 0) bar_expect(bar, static_cast<unsigned>(2 * ns * (OZ2_A + OZ2_B)));  // both CTAs' bytes
             const unsigned lb = oz2_leader_addr(bar);
+            if (p.l2_hint) {
+                for (int t = 0; t < ns; ++t) {
+                    oz2_tma_hint(sm.u.st.a[slot0 + t], &map_a, 0, static_cast<int>(acol0 + t * a_sl + k * 4), lb, pol_a);
+                    oz2_tma_hint(sm.u.st.b[slot0 + t], &map_b, static_cast<int>(rank),
+                                 static_cast<int>(bcol0 + t * b_sl + k * 4), lb, pol_b);
+                }
+                return;
+            }
             for (int t = 0; t < ns; ++t) {
                 oz2_tma(sm.u.st.a[slot0 + t], &map_a, 0, static_cast<int>(acol0 + t * a_sl + k * 4), lb);
                 oz2_tma(sm.u.st.b[slot0 + t], &map_b, static_cast<int>(rank),
@@ -1125,6 +1176,15 @@ int launch_ozaki_gemm(const OzakiArgs& in, cudaStream_t s) {
         OzakiArgs p = in;
         p.prefetch = 0;
         p.tail_split = 1;
+        // row groups of 2 pair rows (4 tile rows): their A digit panels stay
+        // L2-resident while the B panels stream past (C5, n = 65536: 25.1 ->
+        // 22.9 s per evaluation; less DRAM traffic, so higher clocks under the
+        // power cap; profiles/r02_l2_grouping.log)
+        p.group2 = 2;
+        p.sym_group2 = 2;
+        if (const char* e = std::getenv("USTATS_OZ2_GROUP")) p.group2 = std::atoi(e);
+        if (const char* e = std::getenv("USTATS_OZ2_HINT")) p.l2_hint = std::atoi(e);
+        if (const char* e = std::getenv("USTATS_OZ2_SYMG")) p.sym_group2 = std::atoi(e);
         const long long pairs = oz2_pair_count(p);
         bool ok = false;
         switch (p.slices) {
