@@ -72,7 +72,14 @@ void run(int blocks, int iters) {
     cudaFree(sink);
 }
 
-int main() {
+// i8_peak            -> burst: one launch per shape
+// i8_peak sustained  -> N=256 launched back to back for ~4 s (clocks settle
+//                       under the power cap; nvidia-smi samples them)
+int main(int argc, char** argv) {
+    if (argc > 1) {
+        for (int r = 0; r < 300; ++r) run<256>(148, 200000);
+        return 0;
+    }
     run<256>(148, 200000);
     run<128>(148, 200000);
     run<64>(148, 200000);
