@@ -231,7 +231,8 @@ void Program::run_stream(const Op& op, double* out) {
 constexpr long long kOzMinDim = 1024;   // below, DMMA is as fast and needs no digit pass
 constexpr long long kOzMinK = 1024;     // shorter K: per-tile drains and digit passes outweigh the MMA savings
                                         // (C4's Khatri-Rao GEMMs, K = 1024: 297 -> 216 ms per evaluation)
-constexpr double kOzDigitCap = 4.0 * 1073741824.0;  // digit bytes per operand per K chunk
+constexpr double kOzDigitCap = 8.0 * 1073741824.0;  // digit bytes per operand per K chunk (C4: 4 GiB split its
+                                                    // K = 1024 GEMMs in two, 112 -> 158 ms per evaluation)
 
 // Error-bound guard. With S balanced 8-bit slices, truncation and the dropped
 // products t + u >= S bound every entry's error by (S + 2) 2^{2-8S} K
@@ -258,7 +259,9 @@ OzPlan oz_plan(long long K, long long rows, long long cols, bool same_operand, c
     // 65536 rows x 65536 K would need 24 GiB of digits per operand; 4, 6, 8 and
     // 12 chunks measured within 2% of each other there)
     const long long rows_pad = (std::max(rows, cols) + 127) / 128 * 128;
-    const long long cap_k = std::max<long long>(64, static_cast<long long>(kOzDigitCap / (static_cast<double>(rows_pad) * p.slices)) / 64 * 64);
+    double cap = kOzDigitCap;
+    if (const char* e = std::getenv("USTATS_OZ_DIGIT_CAP_GB")) cap = std::atof(e) * 1073741824.0;
+    const long long cap_k = std::max<long long>(64, static_cast<long long>(cap / (static_cast<double>(rows_pad) * p.slices)) / 64 * 64);
     const long long limit = std::min(max_k, cap_k);
     p.nchunks = (K + limit - 1) / limit;
     p.kc = ((K + p.nchunks - 1) / p.nchunks + 63) / 64 * 64;  // chunk starts stay 512-byte aligned
