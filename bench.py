@@ -46,6 +46,7 @@ sys.path.insert(0, str(ROOT))
 FP64_PEAK_TFLOPS = 37.04      # mma.sync f64 m8n8k4 issue-rate probe (best configuration)
 FP64_CUBLAS_TFLOPS = 36.17    # cuBLAS DGEMM 16384^3 on this pool (profiles/r01_fp64_peak_probe.log)
 INT8_PEAK_TOPS = 4542.7       # tcgen05.mma kind::i8 M128 N256 K32 on 148 SMs, median of 300 back-to-back launches
+PROBE_MHZ = 1965.0            # SM clock the probes ran at
 
 
 def measured_peaks() -> dict:
@@ -473,6 +474,12 @@ def main():
                     "kernel": "stream kernels", "kernel_ms_per_step": stream_ms,
                     "kernel_share_of_step": stream_ms / ms_step, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                     "traffic": ncu_traffic(name, "stream")}
+    clk = clocks.summary()
+    if roofline.get("bound") == "tensor" and roofline.get("achieved") and clk.get("sm_mhz"):
+        # the probe peaks were measured at 1965 MHz; a power-capped run's tensor
+        # pipes run at the sampled median clock (sw_power_cap): the fraction of
+        # the peak at that clock says how busy the kernel keeps them
+        roofline["frac_at_sampled_clock"] = roofline["achieved"] / (roofline["peak"] * clk["sm_mhz"] / PROBE_MHZ)
     line = {
         "metric": "U-statistic exact evals/sec", "value": 1e3 / ms_step * 1, "unit": "evals/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -493,7 +500,7 @@ def main():
         "u": u_val,
         "roofline": roofline,
         "gpu_launches": int(st["kernel_launches"]) * args.steps,
-        "clocks": clocks.summary(),
+        "clocks": clk,
         "stats_per_step": {k: st[k] for k in ("multiply_adds", "executed_gemm_macs", "executed_stream_entries",
                                                "gemm_launches", "stream_launches", "shared_hits",
                                                "emulated_gemm_macs", "int8_tensor_ops", "oz_slices")},
