@@ -540,7 +540,7 @@ struct Oz2Smem {
         } st;
         double tile[epi::BM * epi::TP];
     } u;
-    unsigned long long full[8], empty[8], full1[8], empty1[8], done[2], drained;
+    unsigned long long full[8], empty[8], full1[8], empty1[8], done[2], drained, tmem_free, epi_done;
     double red[OZ_EPI / 32];
     int bexp[OZ_BN];
     double bscale[OZ_BN];
@@ -702,21 +702,21 @@ __device__ __forceinline__ void oz2_tma(void* dst, const CUtensorMap* map, int h
         "l"(reinterpret_cast<unsigned long long>(map)), "r"(0), "r"(half), "r"(col), "r"(leader_bar)
         : "memory");
 }
-// the same with an L2 eviction-priority policy (createpolicy)
-__device__ __forceinline__ void oz2_tma_hint(void* dst, const CUtensorMap* map, int half, int col, unsigned leader_bar,
-                                             unsigned long long policy) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
-        "[%1, {%2, %3, %4}], [%5], %6;" ::"r"(su32(dst)),
-        "l"(reinterpret_cast<unsigned long long>(map)), "r"(0), "r"(half), "r"(col), "r"(leader_bar), "l"(policy)
-        : "memory");
-}
 __device__ __forceinline__ unsigned oz2_leader_addr(const void* p) {
     unsigned remote;
     asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(su32(p)));
     return remote;
 }
 
+// Persistent over pair tiles: cluster c runs tiles c, c + P, c + 2P, ...
+// (P = gridDim.x / 2; a full grid runs one tile per cluster). Stage counters
+// and barrier phases carry across tiles; the producer starts tile j + 1 only
+// after its CTA's epilogue released the staging tile (epi_done), the MMA
+// issuer only after both CTAs drained the accumulators (tmem_free). With
+// p.lockstep the producers of every CTA meet at a wave barrier in global
+// memory before each tile (bounded spin: a CTA that is not resident only
+// delays the others by the timeout), so all tiles of a wave stream K in
+// step and the digit panels they share are read from DRAM once.
 template <int S>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_THREADS, 1)
     ozaki_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
@@ -727,17 +727,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_THREADS, 1)
     const unsigned rank = oz2_cta_rank();
     constexpr int split = oz_pass_split(S);  // pass 1: diagonals [0, split); pass 0: [split, S)
     constexpr int P0 = oz2_stages(S), P1 = oz2_stages(split);
-    long long pm, tn;
-    oz2_pair_of(p, p.tile_begin + static_cast<long long>(blockIdx.x >> 1), &pm, &tn);
-    const long long T_m = p.mpad / OZ_BM;
-    const long long tm = 2 * pm + rank;
-    const bool tile_ok = tm < T_m && !(p.symmetric && tm > tn);
+    const long long T_m = p.mpad / OZ_BM, T_n = p.npad / OZ_BN;
     const long long ktiles = p.kpad / OZ_BK;
-    const long long tile_bytes = OZ_BM * OZ_BK;
-    const long long tm_load = tm < T_m ? tm : T_m - 1;  // a missing odd panel: load any (its rows are dropped)
-    // column coordinate of (slice t, panel, k-tile k): ((t * panels + panel) * ktiles + k) * 4
-    const long long acol0 = tm_load * ktiles * 4, a_sl = T_m * ktiles * 4;
-    const long long bcol0 = tn * ktiles * 4, b_sl = (p.npad / OZ_BN) * ktiles * 4;
+    const long long P = gridDim.x >> 1, cl = blockIdx.x >> 1, pairs = p.pairs;
+    struct Tile {
+        long long pm, tn, tm, tm_load;
+        bool ok;
+    };
+    auto tile_at = [&](long long it) {
+        Tile t;
+        oz2_pair_of(p, p.tile_begin + it, &t.pm, &t.tn);
+        t.tm = 2 * t.pm + rank;
+        t.ok = t.tm < T_m && !(p.symmetric && t.tm > t.tn);
+        t.tm_load = t.tm < T_m ? t.tm : T_m - 1;  // a missing odd panel: load any (its rows are dropped)
+        return t;
+    };
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&sm.tmem)));
@@ -753,6 +757,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_THREADS, 1)
         bar_init(&sm.done[0], 1);
         bar_init(&sm.done[1], 1);
         bar_init(&sm.drained, 2 * OZ_EPI / 32);
+        bar_init(&sm.tmem_free, 2 * OZ_EPI / 32);
+        bar_init(&sm.epi_done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -764,142 +770,170 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_THREADS, 1)
     if (tid == 128) {  // producer (both CTAs): own A panel, own half of the B panel, bytes counted on the even CTA
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&map_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&map_b)) : "memory");
-        unsigned long long pol_a = 0, pol_b = 0;  // A panels are re-read across the row group's columns
-        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_a));
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_b));
-        auto load_stage = [&](long long k, int ns, int slot0, unsigned long long* bar) {
-            if (rank == 0) bar_expect(bar, static_cast<unsigned>(2 * ns * (OZ2_A + OZ2_B)));  // both CTAs' bytes
-            const unsigned lb = oz2_leader_addr(bar);
-            if (p.l2_hint) {
-                for (int t = 0; t < ns; ++t) {
-                    oz2_tma_hint(sm.u.st.a[slot0 + t], &map_a, 0, static_cast<int>(acol0 + t * a_sl + k * 4), lb, pol_a);
-                    oz2_tma_hint(sm.u.st.b[slot0 + t], &map_b, static_cast<int>(rank),
-                                 static_cast<int>(bcol0 + t * b_sl + k * 4), lb, pol_b);
+        const long long a_sl = T_m * ktiles * 4, b_sl = T_n * ktiles * 4;
+        long long g0 = 0, g1 = 0, target = 0;
+        int j = 0;
+        for (long long it = cl; it < pairs; it += P, ++j) {
+            const Tile t = tile_at(it);
+            // column coordinate of (slice, panel, k-tile k): ((slice * panels + panel) * ktiles + k) * 4
+            const long long acol0 = t.tm_load * ktiles * 4, bcol0 = t.tn * ktiles * 4;
+            auto load_stage = [&](long long k, int ns, int slot0, unsigned long long* bar) {
+                if (rank == 0) bar_expect(bar, static_cast<unsigned>(2 * ns * (OZ2_A + OZ2_B)));  // both CTAs' bytes
+                const unsigned lb = oz2_leader_addr(bar);
+                for (int q = 0; q < ns; ++q) {
+                    oz2_tma(sm.u.st.a[slot0 + q], &map_a, 0, static_cast<int>(acol0 + q * a_sl + k * 4), lb);
+                    oz2_tma(sm.u.st.b[slot0 + q], &map_b, static_cast<int>(rank),
+                            static_cast<int>(bcol0 + q * b_sl + k * 4), lb);
                 }
-                return;
+            };
+            if (j > 0) {
+                bar_wait(&sm.epi_done, static_cast<unsigned>((j - 1) & 1));  // the staging tile is free again
+                if (p.wave_ctr) {  // wave barrier: every CTA that runs iteration j
+                    const long long here = pairs - static_cast<long long>(j) * P;
+                    target += 2 * (here < P ? here : P);
+                    atomicAdd(p.wave_ctr, 1ull);
+                    unsigned long long t0, now, seen;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(seen) : "l"(p.wave_ctr) : "memory");
+                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                    } while (seen < static_cast<unsigned long long>(target) && now - t0 < 200000ull);
+                }
             }
-            for (int t = 0; t < ns; ++t) {
-                oz2_tma(sm.u.st.a[slot0 + t], &map_a, 0, static_cast<int>(acol0 + t * a_sl + k * 4), lb);
-                oz2_tma(sm.u.st.b[slot0 + t], &map_b, static_cast<int>(rank),
-                        static_cast<int>(bcol0 + t * b_sl + k * 4), lb);
-            }
-        };
-        if constexpr (split < S) {
+            if constexpr (split < S) {
 #pragma unroll 1
-            for (long long k = 0; k < ktiles; ++k) {
-                const int s = static_cast<int>(k % P0);
-                if (k >= P0) bar_wait(&sm.empty[s], static_cast<unsigned>(((k / P0) - 1) & 1));
-                load_stage(k, S, s * S, &sm.full[s]);
+                for (long long k = 0; k < ktiles; ++k, ++g0) {
+                    const int s = static_cast<int>(g0 % P0);
+                    if (g0 >= P0) bar_wait(&sm.empty[s], static_cast<unsigned>(((g0 / P0) - 1) & 1));
+                    load_stage(k, S, s * S, &sm.full[s]);
+                }
+                bar_wait(&sm.done[0], static_cast<unsigned>(j & 1));  // every pass-0 MMA has read its operands
             }
-            bar_wait(&sm.done[0], 0);  // every pass-0 MMA has read its operands: the slots are free
-        }
 #pragma unroll 1
-        for (long long k = 0; k < ktiles; ++k) {
-            const int q = static_cast<int>(k % P1);
-            if (k >= P1) bar_wait(&sm.empty1[q], static_cast<unsigned>(((k / P1) - 1) & 1));
-            load_stage(k, split, q * split, &sm.full1[q]);
+            for (long long k = 0; k < ktiles; ++k, ++g1) {
+                const int q = static_cast<int>(g1 % P1);
+                if (g1 >= P1) bar_wait(&sm.empty1[q], static_cast<unsigned>(((g1 / P1) - 1) & 1));
+                load_stage(k, split, q * split, &sm.full1[q]);
+            }
         }
     } else if (warp == 5 && rank == 0) {  // MMA issuer (even CTA): kind::i8, s32 accumulators, M = 256, N = 128
         const unsigned idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((OZ_BN >> 3) << 17) | (((2 * OZ_BM) >> 4) << 24);
         const unsigned long long da = umma_desc(su32(sm.u.st.a[0]), OZ_BM * 16, 128);
         const unsigned long long db = umma_desc(su32(sm.u.st.b[0]), (OZ_BN / 2) * 16, 128);
-        if constexpr (split < S) {
-#pragma unroll 1
-            for (long long k = 0; k < ktiles; ++k) {
-                const int s = static_cast<int>(k % P0);
-                oz2_wait_cluster(&sm.full[s], static_cast<unsigned>((k / P0) & 1));
+        long long g0 = 0, g1 = 0;
+        int j = 0;
+        for (long long it = cl; it < pairs; it += P, ++j) {
+            if (j > 0) {  // both CTAs have read the previous tile's accumulators
+                oz2_wait_cluster(&sm.tmem_free, static_cast<unsigned>((j - 1) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                oz2_issue<S, split, S, S, P0>(s, tmem, da, db, idesc, k == 0);
-                oz2_commit(&sm.empty[s]);
             }
-            oz2_commit(&sm.done[0]);
-            oz2_wait_cluster(&sm.drained, 0);  // both CTAs read pass 0 out of TMEM
-            asm volatile("tcgen05.fence::after_thread_sync;");
-        }
+            if constexpr (split < S) {
 #pragma unroll 1
-        for (long long k = 0; k < ktiles; ++k) {
-            const int q = static_cast<int>(k % P1);
-            oz2_wait_cluster(&sm.full1[q], static_cast<unsigned>((k / P1) & 1));
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            oz2_issue<S, 0, split, split, P1>(q, tmem, da, db, idesc, k == 0);
-            oz2_commit(&sm.empty1[q]);
+                for (long long k = 0; k < ktiles; ++k, ++g0) {
+                    const int s = static_cast<int>(g0 % P0);
+                    oz2_wait_cluster(&sm.full[s], static_cast<unsigned>((g0 / P0) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    oz2_issue<S, split, S, S, P0>(s, tmem, da, db, idesc, k == 0);
+                    oz2_commit(&sm.empty[s]);
+                }
+                oz2_commit(&sm.done[0]);
+                oz2_wait_cluster(&sm.drained, static_cast<unsigned>(j & 1));  // both CTAs read pass 0 out of TMEM
+                asm volatile("tcgen05.fence::after_thread_sync;");
+            }
+#pragma unroll 1
+            for (long long k = 0; k < ktiles; ++k, ++g1) {
+                const int q = static_cast<int>(g1 % P1);
+                oz2_wait_cluster(&sm.full1[q], static_cast<unsigned>((g1 / P1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                oz2_issue<S, 0, split, split, P1>(q, tmem, da, db, idesc, k == 0);
+                oz2_commit(&sm.empty1[q]);
+            }
+            oz2_commit(&sm.done[1]);
         }
-        oz2_commit(&sm.done[1]);
     } else if (warp < 4 || warp >= 6) {  // epilogue warps (both CTAs): as in ozaki_gemm_kernel
         const int quarter = warp & 3, half = warp >= 6 ? 1 : 0;
         const int et = half * 128 + quarter * 32 + lane;
         const int rt = quarter * 32 + lane;
         const int cb = half * (OZ_BN / 2);
-        const long long row = tm * OZ_BM + rt;
-        const bool row_ok = tile_ok && row < p.m;
         auto sync_epi = [] { asm volatile("bar.sync 1, 256;" ::: "memory"); };
-        if (et == 0) sm.bwide = 0;
-        sync_epi();
-        if (et < OZ_BN) {
-            const long long col = tn * OZ_BN + et;
-            const int eb = col < p.n ? p.b_exp[col] : kOzNoColumn;
-            sm.bexp[et] = eb;
-            const bool pad = eb == kOzNoColumn, narrow = eb >= -511 && eb <= 511;
-            sm.bscale[et] = (pad || !narrow) ? 0.0 : __longlong_as_double(static_cast<long long>(eb + 1023) << 52);
-            if (!pad && !narrow) sm.bwide = 1;
-        }
-        sync_epi();
-        const int ea = row_ok ? p.a_exp[row] : 0;
-        const bool narrow = !sm.bwide && ea >= -511 && ea <= 511;
-        const double sa = row_ok ? __longlong_as_double(static_cast<long long>(ea + 1023) << 52) : 0.0;
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         if (smid >= static_cast<unsigned>(kOzWorkSlots)) __trap();
         double* work = p.work + static_cast<long long>(smid) * (OZ_BM * OZ_BN) + rt;
         const unsigned lane_base = tmem + (static_cast<unsigned>(quarter * 32) << 16);
-        if constexpr (split < S) {
-            bar_wait(&sm.done[0], 0);
+        int j = 0;
+        for (long long it = cl; it < pairs; it += P, ++j) {
+            const Tile t = tile_at(it);
+            const long long row = t.tm * OZ_BM + rt;
+            const bool row_ok = t.ok && row < p.m;
+            if (et == 0) sm.bwide = 0;
+            sync_epi();
+            if (et < OZ_BN) {
+                const long long col = t.tn * OZ_BN + et;
+                const int eb = col < p.n ? p.b_exp[col] : kOzNoColumn;
+                sm.bexp[et] = eb;
+                const bool pad = eb == kOzNoColumn, narrow = eb >= -511 && eb <= 511;
+                sm.bscale[et] = (pad || !narrow) ? 0.0 : __longlong_as_double(static_cast<long long>(eb + 1023) << 52);
+                if (!pad && !narrow) sm.bwide = 1;
+            }
+            sync_epi();
+            const int ea = row_ok ? p.a_exp[row] : 0;
+            const bool narrow = !sm.bwide && ea >= -511 && ea <= 511;
+            const double sa = row_ok ? __longlong_as_double(static_cast<long long>(ea + 1023) << 52) : 0.0;
+            if constexpr (split < S) {
+                bar_wait(&sm.done[0], static_cast<unsigned>(j & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+                for (int c0 = cb; c0 < cb + OZ_BN / 2; c0 += 16) {
+                    double v[16];
+                    oz_drain<split, S>(lane_base, c0, v, false);
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) work[(c0 + q) * OZ_BM] = v[q];
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) oz2_arrive_leader(&sm.drained);
+            }
+            double h0[16], h1[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                h0[q] = split < S ? work[(cb + q) * OZ_BM] : 0.0;
+                h1[q] = split < S ? work[(cb + 16 + q) * OZ_BM] : 0.0;
+            }
+            bar_wait(&sm.done[1], static_cast<unsigned>(j & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll 1
             for (int c0 = cb; c0 < cb + OZ_BN / 2; c0 += 16) {
                 double v[16];
-                oz_drain<split, S>(lane_base, c0, v, false);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) work[(c0 + j) * OZ_BM] = v[j];
+                for (int q = 0; q < 16; ++q) {
+                    v[q] = h0[q];
+                    h0[q] = h1[q];
+                    if (c0 + 32 < cb + OZ_BN / 2) h1[q] = split < S ? work[(c0 + 32 + q) * OZ_BM] : 0.0;
+                }
+                oz_drain<0, split>(lane_base, c0, v, true);
+                if (narrow)
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) sm.u.tile[rt * epi::TP + c0 + q] = (v[q] * sa) * sm.bscale[c0 + q];
+                else
+                    for (int q = 0; q < 16; ++q) {
+                        const int eb = sm.bexp[c0 + q];
+                        sm.u.tile[rt * epi::TP + c0 + q] = (row_ok && eb != kOzNoColumn) ? oz_scale(v[q], ea + eb) : 0.0;
+                    }
             }
+            // the accumulators are read: the next tile's MMAs may overwrite them
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
-            if (lane == 0) oz2_arrive_leader(&sm.drained);
-        }
-        double h0[16], h1[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            h0[j] = split < S ? work[(cb + j) * OZ_BM] : 0.0;
-            h1[j] = split < S ? work[(cb + 16 + j) * OZ_BM] : 0.0;
-        }
-        bar_wait(&sm.done[1], 0);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll 1
-        for (int c0 = cb; c0 < cb + OZ_BN / 2; c0 += 16) {
-            double v[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                v[j] = h0[j];
-                h0[j] = h1[j];
-                if (c0 + 32 < cb + OZ_BN / 2) h1[j] = split < S ? work[(c0 + 32 + j) * OZ_BM] : 0.0;
+            if (lane == 0) oz2_arrive_leader(&sm.tmem_free);
+            sync_epi();
+            if (t.ok) {
+                // dense slot of the tile: the finalizers sum ozaki_tile_count slots
+                const long long slot = p.symmetric ? t.tn * (t.tn + 1) / 2 + t.tm : t.tm * T_n + t.tn;
+                epi::apply<OZ_EPI>(p.epis, p.m, p.n, p.accumulate, sm.u.tile, t.tm * OZ_BM, t.tn * OZ_BN, t.tm, t.tn,
+                                   p.symmetric && t.tm != t.tn, slot, sm.red, et, sync_epi);
             }
-            oz_drain<0, split>(lane_base, c0, v, true);
-            if (narrow)
-#pragma unroll
-                for (int j = 0; j < 16; ++j) sm.u.tile[rt * epi::TP + c0 + j] = (v[j] * sa) * sm.bscale[c0 + j];
-            else
-                for (int j = 0; j < 16; ++j) {
-                    const int eb = sm.bexp[c0 + j];
-                    sm.u.tile[rt * epi::TP + c0 + j] = (row_ok && eb != kOzNoColumn) ? oz_scale(v[j], ea + eb) : 0.0;
-                }
-        }
-        sync_epi();
-        if (tile_ok) {
-            // dense slot of the tile: the finalizers sum ozaki_tile_count slots
-            const long long T_n = p.npad / OZ_BN;
-            const long long slot = p.symmetric ? tn * (tn + 1) / 2 + tm : tm * T_n + tn;
-            epi::apply<OZ_EPI>(p.epis, p.m, p.n, p.accumulate, sm.u.tile, tm * OZ_BM, tn * OZ_BN, tm, tn,
-                               p.symmetric && tm != tn, slot, sm.red, et, sync_epi);
+            sync_epi();  // every epilogue thread is done with the staging tile
+            if (et == 0) bar_arrive(&sm.epi_done);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -1147,7 +1181,7 @@ bool oz2_encode(CUtensorMap* map, const int8_t* base, long long panels, long lon
 }
 
 template <int S>
-bool launch_oz2(const OzakiArgs& p, long long pairs, cudaStream_t s) {
+bool launch_oz2(const OzakiArgs& p, long long clusters, cudaStream_t s) {
     CUtensorMap ma, mb;
     const long long ktiles = p.kpad / OZ_BK;
     if (!oz2_encode(&ma, p.a, p.mpad / OZ_BM, ktiles, p.slices, OZ_BM) ||
@@ -1155,7 +1189,7 @@ bool launch_oz2(const OzakiArgs& p, long long pairs, cudaStream_t s) {
         return false;
     const int bytes = static_cast<int>(sizeof(Oz2Smem));
     set_max_smem_once(reinterpret_cast<const void*>(ozaki_gemm_2sm_kernel<S>), bytes);
-    ozaki_gemm_2sm_kernel<S><<<static_cast<unsigned>(2 * pairs), OZ_THREADS, bytes, s>>>(ma, mb, p);
+    ozaki_gemm_2sm_kernel<S><<<static_cast<unsigned>(2 * clusters), OZ_THREADS, bytes, s>>>(ma, mb, p);
     return true;
 }
 
@@ -1182,18 +1216,37 @@ int launch_ozaki_gemm(const OzakiArgs& in, cudaStream_t s) {
         // power cap; profiles/r02_l2_grouping.log)
         p.group2 = 2;
         p.sym_group2 = 2;
-        if (const char* e = std::getenv("USTATS_OZ2_GROUP")) p.group2 = std::atoi(e);
-        if (const char* e = std::getenv("USTATS_OZ2_HINT")) p.l2_hint = std::atoi(e);
-        if (const char* e = std::getenv("USTATS_OZ2_SYMG")) p.sym_group2 = std::atoi(e);
         const long long pairs = oz2_pair_count(p);
+        p.pairs = pairs;
+        // persistent: one cluster per SM pair looping over the pair tiles;
+        // long-K launches also keep their waves in lock step (wave barrier)
+        const long long ktiles = p.kpad / OZ_BK;
+        int persist = 1, lockstep = ktiles >= 64 ? 1 : 0;
+        if (const char* e = std::getenv("USTATS_OZ2_PERSIST")) persist = std::atoi(e);
+        if (const char* e = std::getenv("USTATS_OZ2_LOCKSTEP")) lockstep = std::atoi(e);
+        if (lockstep && persist) p.group2 = p.sym_group2 = 8;  // square waves: fewest distinct panels
+        if (const char* e = std::getenv("USTATS_OZ2_GROUP")) p.group2 = std::atoi(e);
+        if (const char* e = std::getenv("USTATS_OZ2_SYMG")) p.sym_group2 = std::atoi(e);
+        const long long slots = ozaki_sm_count() / 2;
+        const long long clusters = persist ? std::min(pairs, slots) : pairs;
+        if (persist && lockstep && pairs > clusters) {
+            if (cudaPeekAtLastError() != cudaSuccess) return -1;
+            if (cudaMallocAsync(reinterpret_cast<void**>(&p.wave_ctr), sizeof(unsigned long long), s) != cudaSuccess) {
+                cudaGetLastError();  // exactly this allocation error: run without the wave barrier
+                p.wave_ctr = nullptr;
+            } else {
+                cudaMemsetAsync(p.wave_ctr, 0, sizeof(unsigned long long), s);
+            }
+        }
         bool ok = false;
         switch (p.slices) {
-            case 4: ok = launch_oz2<4>(p, pairs, s); break;
-            case 5: ok = launch_oz2<5>(p, pairs, s); break;
-            case 6: ok = launch_oz2<6>(p, pairs, s); break;
-            case 7: ok = launch_oz2<7>(p, pairs, s); break;
+            case 4: ok = launch_oz2<4>(p, clusters, s); break;
+            case 5: ok = launch_oz2<5>(p, clusters, s); break;
+            case 6: ok = launch_oz2<6>(p, clusters, s); break;
+            case 7: ok = launch_oz2<7>(p, clusters, s); break;
             default: return -1;
         }
+        if (p.wave_ctr) cudaFreeAsync(p.wave_ctr, s);
         if (ok) return 1 + launch_epilogue_finalize(p.m, p.n, p.epis, ozaki_tile_count(p), p.accumulate, s);
         // no tensor-map encoder: the single-SM kernel below
     }

@@ -211,8 +211,9 @@ struct OzakiArgs {
     long long tile_count = -1;   // -1: to the end of the tile list
     int prefetch = 0;            // k-tiles ahead the producer warms L2 (set by launch_ozaki_gemm)
     int group2 = 0;              // CTA-pair kernel, non-symmetric: pair rows per tile group (0 = default)
-    int l2_hint = 0;             // CTA-pair kernel: A digits evict_last, B digits evict_first in L2
     int sym_group2 = 0;          // CTA-pair kernel, symmetric: pair rows per row group (0 = column groups)
+    long long pairs = 0;         // CTA-pair kernel: pair tiles of the launch (clusters loop over them)
+    unsigned long long* wave_ctr = nullptr;  // CTA-pair kernel: wave-barrier counter (null: no lock step)
     double* work = nullptr;      // 128 x 128 doubles per SM (ozaki_work_entries): the high-diagonal partial
     // last partial wave split along K (set by launch_ozaki_gemm): launch-relative
     // tiles >= tail_from run as tail_split CTAs each over a K range; the last
