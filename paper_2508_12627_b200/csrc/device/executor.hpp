@@ -341,6 +341,7 @@ class Program {
     bool power_of(const View& v, int* base, int* pw) const;
     int new_buf(int order, bool symmetric);
     void fuse_epilogues();
+    void lazy_operands();
     void fuse_sweeps();
     void run_sweep(const Op& op);
     bool emulated_eligible(const GemmArgs& g) const;
@@ -350,6 +351,22 @@ class Program {
     bool tma_plain(const View& v, const std::vector<int>& rows, int e) const;
     void launch(Op& op);
     void execute_sharded(int world, bool emulate);
+    // Digits of an emulated GEMM operand kept for the next GEMM that reads the
+    // same operand (one K chunk, single-GPU execution; C4: its Khatri-Rao
+    // operand feeds three GEMMs): key -> buffers and the uses still to come
+    struct CachedDigits {
+        int8_t* d = nullptr;
+        int* e = nullptr;
+        std::size_t bytes = 0;
+        long long rows = 0;
+        int uses = 0;
+    };
+    std::map<std::string, CachedDigits> digits_;
+    std::map<std::string, int> digit_uses_;
+    std::string key_a_, key_b_;  // operand keys of the GEMM being launched (run_gemm -> run_emulated)
+    std::string operand_key(const std::vector<View>& fs, const std::vector<int>& rows, int e) const;
+    void plan_digit_reuse();
+    void drop_digits();
     void run_collective(const ShardCollective& c, bool emulate);
     void run_tri_gemm(const Op& op, double* out, bool emulate);
     const ShardStep* step_ = nullptr;      // the current op's shard step (row sharding)

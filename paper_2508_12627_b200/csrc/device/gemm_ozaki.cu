@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <map>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "epilogue.cuh"
@@ -771,8 +772,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_THREADS, 1)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&map_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&map_b)) : "memory");
         const long long a_sl = T_m * ktiles * 4, b_sl = T_n * ktiles * 4;
-        long long g0 = 0, g1 = 0, target = 0;
+        long long g0 = 0, g1 = 0, target = 0, target1 = 0;
         int j = 0;
+        // bounded spin until *ctr reaches `want` (globaltimer ns)
+        auto wave_wait = [&](unsigned long long* ctr, long long want) {
+            atomicAdd(ctr, 1ull);
+            unsigned long long t0, now, seen;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            do {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(seen) : "l"(ctr) : "memory");
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            } while (seen < static_cast<unsigned long long>(want) && now - t0 < 200000ull);
+        };
         for (long long it = cl; it < pairs; it += P, ++j) {
             const Tile t = tile_at(it);
             // column coordinate of (slice, panel, k-tile k): ((slice * panels + panel) * ktiles + k) * 4
@@ -791,13 +802,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_THREADS, 1)
                 if (p.wave_ctr) {  // wave barrier: every CTA that runs iteration j
                     const long long here = pairs - static_cast<long long>(j) * P;
                     target += 2 * (here < P ? here : P);
-                    atomicAdd(p.wave_ctr, 1ull);
-                    unsigned long long t0, now, seen;
-                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-                    do {
-                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(seen) : "l"(p.wave_ctr) : "memory");
-                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-                    } while (seen < static_cast<unsigned long long>(target) && now - t0 < 200000ull);
+                    wave_wait(p.wave_ctr, target);
                 }
             }
             if constexpr (split < S) {
@@ -808,6 +813,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_THREADS, 1)
                     load_stage(k, S, s * S, &sm.full[s]);
                 }
                 bar_wait(&sm.done[0], static_cast<unsigned>(j & 1));  // every pass-0 MMA has read its operands
+                if (p.wave_ctr && p.resync) {  // re-align the wave before pass 1 re-streams K
+                    const long long here = pairs - static_cast<long long>(j) * P;
+                    target1 += 2 * (here < P ? here : P);
+                    wave_wait(p.wave_ctr + 1, target1);
+                }
             }
 #pragma unroll 1
             for (long long k = 0; k < ktiles; ++k, ++g1) {
@@ -1023,6 +1033,120 @@ __global__ void __launch_bounds__(256) oz_split_rows(const double* __restrict__ 
     oz_digits16(xv, e, slices, slice_bytes, out + off);
 }
 
+// Lazy (Khatri-Rao / Hadamard) operands: value(r, k) = prod_f F_f[off_f(r) +
+// kstride_f k], off_f(r) = sum_d digit_d(r) rstride_f[d] (r in base n, most
+// significant digit first) -- the GEMM operand is never materialized in FP64;
+// its digits are formed straight from the (L2-resident) factors.
+struct OzLazy {
+    int nf = 0, nr = 1;
+    long long n = 1;
+    const double* ptr[kMaxGemmFactors] = {};
+    long long rstride[kMaxGemmFactors][kMaxRowDims] = {};
+    long long kstride[kMaxGemmFactors] = {};
+};
+__device__ __forceinline__ void oz_lazy_bases(const OzLazy& z, long long r, long long k0, const double* (&base)[kMaxGemmFactors]) {
+    long long off[kMaxGemmFactors];
+#pragma unroll
+    for (int f = 0; f < kMaxGemmFactors; ++f) off[f] = 0;
+    long long rr = r;
+    for (int d = z.nr - 1; d >= 0; --d) {
+        const long long dig = rr % z.n;
+        rr /= z.n;
+#pragma unroll
+        for (int f = 0; f < kMaxGemmFactors; ++f)
+            if (f < z.nf) off[f] += dig * z.rstride[f][d];
+    }
+#pragma unroll
+    for (int f = 0; f < kMaxGemmFactors; ++f)
+        if (f < z.nf) base[f] = z.ptr[f] + off[f] + k0 * z.kstride[f];
+}
+// vec: every factor has unit K stride and 16-byte aligned rows (double2 loads)
+template <int NF, bool VEC>
+__global__ void oz_row_exponents_lazy(OzLazy z, long long rows, long long k0, long long k, int* __restrict__ exps) {
+    const long long r = blockIdx.x * static_cast<long long>(blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    const double* base[kMaxGemmFactors];
+    oz_lazy_bases(z, r, k0, base);
+    double mx = 0.0;
+    if constexpr (VEC) {
+        for (long long c = 2 * lane; c + 1 < k; c += 64) {
+            double2 v = make_double2(1.0, 1.0);
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                const double2 w = __ldg(reinterpret_cast<const double2*>(base[f] + c));
+                v.x *= w.x;
+                v.y *= w.y;
+            }
+            mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
+        }
+        if ((k & 1) && lane == 0) {
+            double v = 1.0;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) v *= __ldg(base[f] + (k - 1));
+            mx = fmax(mx, fabs(v));
+        }
+    } else {
+        for (long long c = lane; c < k; c += 32) {
+            double v = 1.0;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) v *= __ldg(base[f] + c * z.kstride[f]);
+            mx = fmax(mx, fabs(v));
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) {
+        int e = 0;
+        if (mx > 0.0) frexp(mx, &e);
+        exps[r] = e;
+    }
+}
+// a thread per (row, 16 values), rows across the warp (as oz_split_rows)
+template <int NF, bool VEC>
+__global__ void __launch_bounds__(256) oz_split_lazy(OzLazy z, long long rows, long long k0, long long k,
+                                                     const int* __restrict__ exps, long long kpad, int slices,
+                                                     long long slice_bytes, int8_t* __restrict__ out) {
+    const int rr = threadIdx.x & 127;
+    const long long rt = blockIdx.x;
+    const long long R = rt * OZ_BM + rr;
+    const long long c0 = (static_cast<long long>(blockIdx.y) * 2 + (threadIdx.x >> 7)) * 16;
+    double xv[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) xv[j] = 0.0;
+    if (R < rows) {
+        const double* base[kMaxGemmFactors];
+        oz_lazy_bases(z, R, k0, base);
+        if (VEC && c0 + 16 <= k) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) xv[j] = 1.0;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                const double2* src = reinterpret_cast<const double2*>(base[f] + c0);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const double2 w = __ldg(src + j);
+                    xv[2 * j] *= w.x;
+                    xv[2 * j + 1] *= w.y;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) xv[j] = c0 + j < k ? 1.0 : 0.0;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                const long long ks = z.kstride[f];
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (c0 + j < k) xv[j] *= __ldg(base[f] + (c0 + j) * ks);
+            }
+        }
+    }
+    const int e = R < rows ? exps[R] : 0;
+    const long long kt = c0 / OZ_BK, cin = (c0 % OZ_BK) / 16;
+    const long long off = (rt * (kpad / OZ_BK) + kt) * (OZ_BM * OZ_BK) + cin * (OZ_BM * 16) + rr * 16;
+    oz_digits16(xv, e, slices, slice_bytes, out + off);
+}
+
 constexpr int OZ_SPLIT_THREADS = 256;
 __global__ void __launch_bounds__(OZ_SPLIT_THREADS) oz_split(const double* __restrict__ x, long long rows, long long k,
                                                             long long rs, long long ks, const int* __restrict__ exps,
@@ -1096,6 +1220,49 @@ int ozaki_split(const double* x, long long rows, long long k, long long rs, long
         oz_split<<<static_cast<unsigned>(npanels * (kp / OZ_BK)), OZ_SPLIT_THREADS, smem, s>>>(
             x, rows, k, rs, ks, exps, tile_rows, kp, slices, rp * kp, out, dpanels);
     if (dpanels) cudaFreeAsync(dpanels, s);
+    return 2;
+}
+
+int ozaki_split_lazy(const GemmSide& side, long long n, long long rows, long long k0, long long k, int slices,
+                     int8_t* out, int* exps, cudaStream_t s) {
+    if (slices < 1 || slices > kOzMaxSlices || side.nf < 1 || side.nf > kMaxGemmFactors || side.nr > kMaxRowDims)
+        return -1;
+    OzLazy z;
+    z.nf = side.nf;
+    z.nr = side.nr;
+    z.n = n;
+    for (int f = 0; f < side.nf; ++f) {
+        z.ptr[f] = side.ptr[f];
+        z.kstride[f] = side.kstride[f];
+        for (int d = 0; d < side.nr; ++d) z.rstride[f][d] = side.rstride[f][d];
+    }
+    const long long rp = (rows + OZ_BM - 1) / OZ_BM * OZ_BM;
+    const long long kp = (k + OZ_BK - 1) / OZ_BK * OZ_BK;
+    // unit K strides, even row offsets and 16-byte aligned bases: double2 loads
+    bool vec = true;
+    for (int f = 0; f < z.nf; ++f) {
+        vec &= z.kstride[f] == 1 && (reinterpret_cast<std::uintptr_t>(z.ptr[f] + k0) & 15) == 0;
+        for (int d = 0; d < z.nr; ++d) vec &= (z.rstride[f][d] & 1) == 0;
+    }
+    const dim3 eg(static_cast<unsigned>((rows + 7) / 8)), sg(static_cast<unsigned>(rp / OZ_BM), static_cast<unsigned>(kp / 32));
+    auto go = [&](auto nf) {
+        constexpr int NF = decltype(nf)::value;
+        if (vec) {
+            oz_row_exponents_lazy<NF, true><<<eg, 256, 0, s>>>(z, rows, k0, k, exps);
+            oz_split_lazy<NF, true><<<sg, 256, 0, s>>>(z, rows, k0, k, exps, kp, slices, rp * kp, out);
+        } else {
+            oz_row_exponents_lazy<NF, false><<<eg, 256, 0, s>>>(z, rows, k0, k, exps);
+            oz_split_lazy<NF, false><<<sg, 256, 0, s>>>(z, rows, k0, k, exps, kp, slices, rp * kp, out);
+        }
+    };
+    switch (z.nf) {
+        case 2: go(std::integral_constant<int, 2>{}); break;
+        case 3: go(std::integral_constant<int, 3>{}); break;
+        case 4: go(std::integral_constant<int, 4>{}); break;
+        case 5: go(std::integral_constant<int, 5>{}); break;
+        case 6: go(std::integral_constant<int, 6>{}); break;
+        default: return -1;
+    }
     return 2;
 }
 
@@ -1231,12 +1398,13 @@ int launch_ozaki_gemm(const OzakiArgs& in, cudaStream_t s) {
         const long long clusters = persist ? std::min(pairs, slots) : pairs;
         if (persist && lockstep && pairs > clusters) {
             if (cudaPeekAtLastError() != cudaSuccess) return -1;
-            if (cudaMallocAsync(reinterpret_cast<void**>(&p.wave_ctr), sizeof(unsigned long long), s) != cudaSuccess) {
+            if (cudaMallocAsync(reinterpret_cast<void**>(&p.wave_ctr), 2 * sizeof(unsigned long long), s) != cudaSuccess) {
                 cudaGetLastError();  // exactly this allocation error: run without the wave barrier
                 p.wave_ctr = nullptr;
             } else {
-                cudaMemsetAsync(p.wave_ctr, 0, sizeof(unsigned long long), s);
+                cudaMemsetAsync(p.wave_ctr, 0, 2 * sizeof(unsigned long long), s);
             }
+            if (const char* e = std::getenv("USTATS_OZ2_RESYNC")) p.resync = std::atoi(e);
         }
         bool ok = false;
         switch (p.slices) {

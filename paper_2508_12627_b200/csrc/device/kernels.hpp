@@ -213,7 +213,8 @@ struct OzakiArgs {
     int group2 = 0;              // CTA-pair kernel, non-symmetric: pair rows per tile group (0 = default)
     int sym_group2 = 0;          // CTA-pair kernel, symmetric: pair rows per row group (0 = column groups)
     long long pairs = 0;         // CTA-pair kernel: pair tiles of the launch (clusters loop over them)
-    unsigned long long* wave_ctr = nullptr;  // CTA-pair kernel: wave-barrier counter (null: no lock step)
+    unsigned long long* wave_ctr = nullptr;  // CTA-pair kernel: wave-barrier counters [tile start, pass 1] (null: none)
+    int resync = 0;              // CTA-pair kernel: also meet before pass 1
     double* work = nullptr;      // 128 x 128 doubles per SM (ozaki_work_entries): the high-diagonal partial
     // last partial wave split along K (set by launch_ozaki_gemm): launch-relative
     // tiles >= tail_from run as tail_split CTAs each over a K range; the last
@@ -229,6 +230,10 @@ std::size_t ozaki_slice_bytes(long long rows, long long k, int tile_rows);
 // with `panels`, only those 128-row panels are written.
 int ozaki_split(const double* x, long long rows, long long k, long long rs, long long ks, int tile_rows, int slices,
                 int8_t* out, int* exps, cudaStream_t s, const std::vector<int>* panels = nullptr);
+// Digits of a lazy operand (GemmSide: a product of factors, rows in base n)
+// over K columns [k0, k0 + k), formed from the factors without an FP64 copy.
+int ozaki_split_lazy(const GemmSide& side, long long n, long long rows, long long k0, long long k, int slices,
+                     int8_t* out, int* exps, cudaStream_t s);
 long long ozaki_tile_count(const OzakiArgs& p);
 // The 128-row panels of A and of B that the tiles [tile_begin, tile_begin + tile_count) read.
 void ozaki_tile_panels(const OzakiArgs& p, std::vector<int>* a_panels, std::vector<int>* b_panels);

@@ -285,10 +285,15 @@ long long flat_row_stride(const GemmSide& s, long long n) {
     return s.rstride[0][s.nr - 1];
 }
 
+// A lazy operand (a product of factors: a Khatri-Rao / Hadamard operand the
+// optimizer left unmaterialized, Program::lazy_operands) is digitized
+// straight from its factors (ozaki_split_lazy).
+bool lazy_side(const GemmSide& s) { return s.nf >= 2 && s.nf <= kMaxGemmFactors && s.nr <= kMaxRowDims; }
+
 bool Program::emulated_eligible(const GemmArgs& g) const {
     if (!config_.device.fp64_emulation) return false;
     if (g.n < kOzMinK || g.rows < kOzMinDim || g.cols < kOzMinDim) return false;
-    return flat_row_stride(g.a, n_) >= 0 && flat_row_stride(g.b, n_) >= 0;
+    return (flat_row_stride(g.a, n_) >= 0 || lazy_side(g.a)) && (flat_row_stride(g.b, n_) >= 0 || lazy_side(g.b));
 }
 
 // The transient device bytes an op needs while it runs, beyond its outputs:
@@ -308,24 +313,81 @@ std::size_t Program::op_scratch_bytes(const Op& op) const {
 // K beyond the exact int32 bound (C5: K = 65536) runs as equal K chunks (oz_plan),
 // each digitized on its own (per-chunk row exponents) and accumulated into the
 // outputs in chunk order: every epilogue is linear in C.
+// The canonical description of a GEMM operand (factor buffers and their row /
+// K strides, a symmetric matrix read K-contiguous as run_gemm reads it): two
+// GEMMs with the same key digitize the same values.
+std::string Program::operand_key(const std::vector<View>& fs, const std::vector<int>& rows, int e) const {
+    std::vector<std::string> parts;
+    for (View v : fs) {
+        if (bufs_[static_cast<std::size_t>(v.buf)].symmetric && std::popcount(v.ids) == 2 && (v.ids & bit(e)) &&
+            v.stride[static_cast<std::size_t>(e)] != 1) {
+            const int other = std::countr_zero(v.ids & ~bit(e));
+            std::swap(v.stride[static_cast<std::size_t>(e)], v.stride[static_cast<std::size_t>(other)]);
+        }
+        std::string k = "b" + std::to_string(v.buf) + ":";
+        for (int id : rows) k += std::to_string(v.stride[static_cast<std::size_t>(id)]) + ",";
+        k += "k" + std::to_string(v.stride[static_cast<std::size_t>(e)]);
+        parts.push_back(k);
+    }
+    std::sort(parts.begin(), parts.end());
+    std::string key = std::to_string(rows.size()) + "|";
+    for (const auto& p : parts) key += p + ";";
+    return key;
+}
+
+// How many emulated single-chunk GEMMs read each operand (single-GPU runs).
+void Program::plan_digit_reuse() {
+    digit_uses_.clear();
+    if (!config_.device.fp64_emulation || n_ < kOzMinK) return;
+    for (std::size_t i : schedule_) {
+        const Op& op = ops_[i];
+        if (op.dead || !op.gemm) continue;
+        const long long rows = static_cast<long long>(ipow(n_, static_cast<int>(op.ra.size())));
+        const long long cols = static_cast<long long>(ipow(n_, static_cast<int>(op.rb.size())));
+        if (rows < kOzMinDim || cols < kOzMinDim) continue;
+        if (oz_plan(n_, rows, cols, false, config_.device).nchunks != 1) continue;
+        const std::string ka = operand_key(op.fa, op.ra, op.e), kb = operand_key(op.fb, op.rb, op.e);
+        ++digit_uses_[ka];
+        if (kb != ka) ++digit_uses_[kb];
+    }
+}
+
+void Program::drop_digits() {
+    for (auto& [key, c] : digits_) {
+        rt_->raw_free(c.d, c.bytes);
+        rt_->release(reinterpret_cast<double*>(c.e));
+    }
+    digits_.clear();
+}
+
 int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
     cudaStream_t s = rt_->stream();
     // one set of digits when both operands are the same matrix view (A A^T)
     const long long ars = flat_row_stride(g.a, n_), brs = flat_row_stride(g.b, n_);
-    const bool same = g.a.ptr[0] == g.b.ptr[0] && g.rows == g.cols && ars == brs && g.a.kstride[0] == g.b.kstride[0];
+    const bool same = ars >= 0 && brs >= 0 && g.a.ptr[0] == g.b.ptr[0] && g.rows == g.cols && ars == brs &&
+                      g.a.kstride[0] == g.b.kstride[0];
     const OzPlan oz = oz_plan(g.n, g.rows, g.cols, same, config_.device);
     const int S = oz.slices;
     const long long kc = oz.kc;
     if (oz.nchunks > 1)  // a consumer of C^2 is not linear in C: the caller runs it on DMMA
         for (int q = 0; q < set.count; ++q)
             if (set.d[q].self_power != 1) return -1;
+    // digit reuse across GEMMs (one K chunk, whole operands, memory to spare)
+    const bool reuse = oz.nchunks == 1 && slice_world_ == 1 && block_rows_.first < 0 && g.tile_count < 0 &&
+                       !key_a_.empty() && budget_ > 0 && (same || key_a_ != key_b_);
+    auto cached = [&](const std::string& key) -> CachedDigits* {
+        auto it = digits_.find(key);
+        return (reuse && it != digits_.end()) ? &it->second : nullptr;
+    };
+    CachedDigits* ca = cached(key_a_);
+    CachedDigits* cb = same ? nullptr : cached(key_b_);
     // digit panels: slabs the schedule planned for (op_scratch_bytes); the
     // choice of engine depends only on the plan, never on a failed allocation,
     // so row-sharded ranks always agree on it
-    int8_t* da = static_cast<int8_t*>(rt_->raw_alloc(oz.a_bytes));
-    int8_t* db = same ? da : static_cast<int8_t*>(rt_->raw_alloc(oz.b_bytes));
-    int* ea = static_cast<int*>(rt_->raw_alloc(sizeof(int) * static_cast<std::size_t>(g.rows), false));
-    int* eb = same ? ea : static_cast<int*>(rt_->raw_alloc(sizeof(int) * static_cast<std::size_t>(g.cols), false));
+    int8_t* da = ca ? ca->d : static_cast<int8_t*>(rt_->raw_alloc(oz.a_bytes));
+    int8_t* db = same ? da : cb ? cb->d : static_cast<int8_t*>(rt_->raw_alloc(oz.b_bytes));
+    int* ea = ca ? ca->e : static_cast<int*>(rt_->raw_alloc(sizeof(int) * static_cast<std::size_t>(g.rows), false));
+    int* eb = same ? ea : cb ? cb->e : static_cast<int*>(rt_->raw_alloc(sizeof(int) * static_cast<std::size_t>(g.cols), false));
     double* work = static_cast<double*>(rt_->raw_alloc(ozaki_work_entries() * sizeof(double), false));
     const bool sym = g.symmetric_out && g.rows == g.cols;
     int launched = 0;
@@ -337,6 +399,13 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
         check_cuda(cudaPeekAtLastError(), "Ozaki digit split launch");
         launched += l;
     };
+    auto split_lazy = [&](const GemmSide& side, long long rows, long long k0, long long k, int8_t* out, int* exps) {
+        const int l = ozaki_split_lazy(side, n_, rows, k0, k, S, out, exps, s);
+        if (l < 0) fail(ErrorCode::CudaError, "executor: lazy Ozaki digit split failed");
+        check_cuda(cudaPeekAtLastError(), "lazy Ozaki digit split launch");
+        launched += l;
+    };
+    const bool lazy_a = ars < 0, lazy_b = brs < 0;
     for (long long k0 = 0; k0 < g.n; k0 += kc) {
         const long long k = std::min(kc, g.n - k0);
         const double* xa = g.a.ptr[0] + k0 * g.a.kstride[0];
@@ -365,7 +434,21 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
         tiles = p.tile_count >= 0 ? p.tile_count : ozaki_tile_count(p);
         p.work = work;
         // digits: all panels, or under row sharding only the panels this rank's tiles read
-        if (g.tile_count >= 0) {
+        if (ca || cb) {  // reused digits for one side (one chunk: k0 == 0)
+            if (!ca) {
+                if (lazy_a) split_lazy(g.a, g.rows, k0, k, da, ea);
+                else split(xa, g.rows, k, ars, g.a.kstride[0], da, ea, nullptr);
+            }
+            if (!cb && !same) {
+                if (lazy_b) split_lazy(g.b, g.cols, k0, k, db, eb);
+                else split(xb, g.cols, k, brs, g.b.kstride[0], db, eb, nullptr);
+            }
+        } else if (lazy_a || lazy_b) {
+            if (lazy_a) split_lazy(g.a, g.rows, k0, k, da, ea);
+            else split(xa, g.rows, k, ars, g.a.kstride[0], da, ea, nullptr);
+            if (lazy_b) split_lazy(g.b, g.cols, k0, k, db, eb);
+            else split(xb, g.cols, k, brs, g.b.kstride[0], db, eb, nullptr);
+        } else if (g.tile_count >= 0) {
             std::vector<int> pa, pb;
             ozaki_tile_panels(p, &pa, &pb);
             if (same) {
@@ -397,10 +480,31 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
         stats_->emulated_macs += sym ? full / (tm * tm) * (tm * (tm + 1) / 2) : full;  // as gemm_macs counts it
         stats_->oz_slices = static_cast<std::uint64_t>(S);
     }
-    rt_->raw_free(da, oz.a_bytes);
-    if (!same) rt_->raw_free(db, oz.b_bytes);
-    rt_->release(reinterpret_cast<double*>(ea));
-    if (!same) rt_->release(reinterpret_cast<double*>(eb));
+    // keep or release each side's digits: a later GEMM reading the same
+    // operand reuses them while the schedule's headroom covers them
+    auto settle = [&](const std::string& key, CachedDigits* hit, int8_t* d, int* e, std::size_t bytes, long long rows) {
+        if (hit) {
+            if (--hit->uses <= 0) {
+                rt_->raw_free(hit->d, hit->bytes);
+                rt_->release(reinterpret_cast<double*>(hit->e));
+                digits_.erase(key);
+            }
+            return;
+        }
+        auto u = digit_uses_.find(key);
+        double held = 0;
+        for (const auto& [k2, c] : digits_) held += static_cast<double>(c.bytes);
+        const bool keep = reuse && u != digit_uses_.end() && u->second > 1 &&
+                          budget_ - sched_peak_ >= 2.0 * (held + static_cast<double>(bytes)) + 2e9;
+        if (keep) {
+            digits_[key] = CachedDigits{d, e, bytes, rows, u->second - 1};
+            return;
+        }
+        rt_->raw_free(d, bytes);
+        rt_->release(reinterpret_cast<double*>(e));
+    };
+    settle(key_a_, ca, da, ea, oz.a_bytes, g.rows);
+    if (!same) settle(key_b_, cb, db, eb, oz.b_bytes, g.cols);
     rt_->release(work);
     return launched;
 }
@@ -433,6 +537,8 @@ void Program::run_gemm(const Op& op, double* out) {
         if (!rows.empty() && big.stride[static_cast<std::size_t>(rows.back())] == 1) return 0;
         return 1;
     };
+    key_a_ = operand_key(op.fa, op.ra, op.e);
+    key_b_ = operand_key(op.fb, op.rb, op.e);
     GemmArgs g;
     fill(g.a, fa, op.ra);
     fill(g.b, fb, op.rb);
@@ -700,6 +806,11 @@ void Program::execute() {
         execute_sharded(world, emulate != 0);
         return;
     }
+    plan_digit_reuse();
+    struct DropDigits {  // cached digits never outlive one execution
+        Program* p;
+        ~DropDigits() { p->drop_digits(); }
+    } drop_guard{this};
     bool has_gemm = false;
     for (std::size_t i : schedule_) has_gemm |= ops_[i].gemm;
     const bool multi =

@@ -854,9 +854,98 @@ void Program::make_schedule(double budget) {
     sched_fits_ = found;
 }
 
+// Lazy GEMM operands. A multi-factor operand is recorded as an elementwise
+// stream op forming it k-major (Program::gemm's `lower`); when that product
+// is read only as a whole operand of GEMMs that run emulated, it is never
+// materialized: the op is dropped and each GEMM reads the factors directly,
+// their digits formed straight from them (ozaki_split_lazy). C4: its two
+// n^3 Khatri-Rao operands (8.6 GB each in FP64) are written, read for the
+// row exponents and read again for the digits no more.
+void Program::lazy_operands() {
+    if (!config_.device.fp64_emulation || n_ < 1024) return;
+    std::vector<int> readers(bufs_.size(), 0);
+    for (const Op& op : ops_)
+        if (!op.dead) for_each_read(op, [&](const View& v) { ++readers[static_cast<std::size_t>(v.buf)]; });
+    auto flat_rows = [&](const View& v, const std::vector<int>& rows) {
+        for (std::size_t d = 1; d < rows.size(); ++d)
+            if (v.stride[static_cast<std::size_t>(rows[d - 1])] != v.stride[static_cast<std::size_t>(rows[d])] * n_)
+                return false;
+        return true;
+    };
+    for (Op& s : ops_) {
+        if (s.dead || s.gemm || s.sweep || s.ext || s.sum != 0 || s.out < 0 || keep_.count(s.out)) continue;
+        if (s.factors.size() < 2 || s.factors.size() > static_cast<std::size_t>(kMaxGemmFactors)) continue;
+        const int b = s.out, order = static_cast<int>(s.out_ids.size());
+        if (order < 2) continue;
+        // every reader: a GEMM holding b as the single view of one operand, emulated by size
+        std::vector<std::pair<Op*, bool>> uses;  // (gemm, on side a)
+        bool ok = true;
+        int seen = 0;
+        for (Op& g : ops_) {
+            if (g.dead) continue;
+            int here = 0;
+            for_each_read(g, [&](const View& v) { here += v.buf == b; });
+            if (!here) continue;
+            seen += here;
+            const bool on_a = g.gemm && g.fa.size() == 1 && g.fa[0].buf == b;
+            const bool on_b = g.gemm && g.fb.size() == 1 && g.fb[0].buf == b;
+            const std::uint64_t rows = ipow(n_, static_cast<int>(g.ra.size())), cols = ipow(n_, static_cast<int>(g.rb.size()));
+            if (here != 1 || !(on_a || on_b) || rows < 1024 || cols < 1024) {
+                ok = false;
+                break;
+            }
+            // the other operand must be a plain matrix view (or itself lazy)
+            const std::vector<View>& other = on_a ? g.fb : g.fa;
+            if (other.size() == 1 && !flat_rows(other[0], on_a ? g.rb : g.ra)) {
+                ok = false;
+                break;
+            }
+            uses.emplace_back(&g, on_a);
+        }
+        if (!ok || uses.empty() || seen != readers[static_cast<std::size_t>(b)]) continue;
+        // compose each use: GEMM id -> axis of b -> the stream op's id
+        std::vector<std::vector<View>> composed;
+        for (auto& [g, on_a] : uses) {
+            const View& v = on_a ? g->fa[0] : g->fb[0];
+            std::vector<int> axis_src(static_cast<std::size_t>(order), -1);  // axis -> GEMM id
+            for (int id : ids_of(v.ids)) {
+                const long long st = v.stride[static_cast<std::size_t>(id)];
+                int a = -1;
+                for (int x = 0; x < order; ++x)
+                    if (st == static_cast<long long>(ipow(n_, order - 1 - x))) a = x;
+                if (a < 0 || axis_src[static_cast<std::size_t>(a)] >= 0) {
+                    ok = false;
+                    break;
+                }
+                axis_src[static_cast<std::size_t>(a)] = id;
+            }
+            if (!ok) break;
+            for (int x = 0; x < order; ++x) ok &= axis_src[static_cast<std::size_t>(x)] >= 0;
+            if (!ok) break;
+            std::vector<View> fs;
+            for (const View& f : s.factors) {
+                View c;
+                c.buf = f.buf;
+                for (int x = 0; x < order; ++x) {
+                    const int sid = s.out_ids[static_cast<std::size_t>(x)], gid = axis_src[static_cast<std::size_t>(x)];
+                    if (!(f.ids & bit(sid))) continue;
+                    c.ids |= bit(gid);
+                    c.stride[static_cast<std::size_t>(gid)] = f.stride[static_cast<std::size_t>(sid)];
+                }
+                fs.push_back(c);
+            }
+            composed.push_back(std::move(fs));
+        }
+        if (!ok) continue;
+        for (std::size_t u = 0; u < uses.size(); ++u) (uses[u].second ? uses[u].first->fa : uses[u].first->fb) = composed[u];
+        s.dead = true;
+    }
+}
+
 void Program::optimize(double budget_bytes) {
     budget_ = budget_bytes;
     if (config_.device.fuse_epilogues) fuse_epilogues();
+    lazy_operands();
     make_schedule(budget_bytes);
     if (config_.device.fuse_epilogues) {
         // sweeps tie their consumers' operands together; keep them only if

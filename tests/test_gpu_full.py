@@ -151,3 +151,21 @@ def test_golden_row_sharded(engine, fixture, world):
     scale = float(np.max(np.abs(g["v"])))
     assert float(np.max(np.abs(got.v - g["v"]))) <= TOL * scale
     assert abs(got.value - float(g["u"])) <= TOL * scale
+
+
+@pytest.mark.parametrize("world", [0, 3])
+def test_lazy_khatri_rao_C4_full(engine, world):
+    # C4 at its BASELINE n = 1024: the Khatri-Rao GEMM operands are never
+    # materialized (their digits are formed from the factors, ozaki_split_lazy);
+    # per V-term within the north-star tolerance of the IEEE FP64 (DMMA) run,
+    # whose operands ARE materialized; also row-sharded over virtual ranks
+    from paper_2508_12627_b200.workloads import generate
+    factors, sig, m, _ = generate("C4", 1024)
+    cap = 1024 ** 3 + 1
+    cfg = engine.Config(memory_cap_entries=cap, shard_rows=world > 0, emulate_world=world)
+    got = engine.u_terms(factors, sig, m, cfg)
+    assert got.stats["int8_tensor_ops"] > 0
+    exact = engine.u_terms(factors, sig, m, engine.Config(memory_cap_entries=cap, fp64_emulation=False))
+    scale = float(np.max(np.abs(exact.v)))
+    assert float(np.max(np.abs(got.v - exact.v))) <= TOL * scale
+    assert abs(got.value - exact.value) <= TOL * scale
