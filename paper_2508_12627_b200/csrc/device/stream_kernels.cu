@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(256) stream_elementwise_pairs(StreamArgs a, un
 
 // Long rows: the block's threads share each row (C3: 8192 pairs per row).
 template <int NF>
-__global__ void __launch_bounds__(256) stream_reduce_all_pairs_block(StreamArgs a, unsigned long long rows,
+__global__ void __launch_bounds__(256, 4) stream_reduce_all_pairs_block(StreamArgs a, unsigned long long rows,
                                                                      long long inner_n, double* partial) {
     __shared__ double red[32];
     const int D = a.n_sum;
@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(256) stream_reduce_all_pairs_block(StreamArgs 
 // over the row's pairs: short rows (C4: n = 1024) no longer pay the row
 // setup per few loads.
 template <int NF>
-__global__ void __launch_bounds__(256) stream_reduce_all_pairs(StreamArgs a, unsigned long long rows,
+__global__ void __launch_bounds__(256, 4) stream_reduce_all_pairs(StreamArgs a, unsigned long long rows,
                                                                long long inner_n, double* partial) {
     __shared__ double red[32];
     const int D = a.n_sum;
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(256) stream_reduce_all_pairs(StreamArgs a, uns
 }
 
 template <int NF>
-__global__ void __launch_bounds__(256) stream_reduce_warp_pairs(StreamArgs a, unsigned long long outputs,
+__global__ void __launch_bounds__(256, 4) stream_reduce_warp_pairs(StreamArgs a, unsigned long long outputs,
                                                                 unsigned long long srows) {
     const int lane = threadIdx.x & 31;
     const unsigned long long o =
