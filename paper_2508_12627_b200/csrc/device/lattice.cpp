@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <numeric>
 #include <string>
@@ -257,8 +258,23 @@ PlanEntry* store_plan(int device, const std::string& key, std::unique_ptr<PlanEn
 
 }  // namespace
 
+// One evaluation at a time per device: a cached Program (its buffers, term
+// slots and launch order) and the Runtime's current stream / profiling state
+// are shared, and ctypes releases the GIL during the call, so two host
+// threads evaluating on one device are serialized here (different devices
+// run concurrently).
 std::vector<StatisticResult> lattice_batch(const std::vector<StatisticSpec>& specs, bool inputs_on_device,
                                            long long n, LatticeMode mode, const Config& config) {
+    static std::mutex table_mu;
+    static std::map<int, std::unique_ptr<std::mutex>> per_device;
+    std::mutex* mu = nullptr;
+    {
+        std::lock_guard<std::mutex> lock(table_mu);
+        auto& slot = per_device[config.device.device];
+        if (!slot) slot = std::make_unique<std::mutex>();
+        mu = slot.get();
+    }
+    std::lock_guard<std::mutex> lock(*mu);
     return lattice_batch_impl(specs, inputs_on_device, n, mode, config, true);
 }
 
