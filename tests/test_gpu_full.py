@@ -70,7 +70,7 @@ def test_relabeling_invariance_C4(engine):
 
 
 # ---- round 2: the K-chunked emulated GEMM pinned to the REFERENCE (not to DMMA)
-@pytest.mark.parametrize("fixture,max_k", [("C5_n4096.npz", 1024), ("C5_n4096.npz", 1472), ("C2_n8192.npz", 2048),
+@pytest.mark.parametrize("fixture,max_k", [("C5_n4096.npz", 1024), ("C5_n4096.npz", 1472), ("C5_n8192.npz", 2048), ("C2_n8192.npz", 2048),
                                            ("C3_n4096.npz", 1024)])
 def test_golden_k_chunked_emulation(engine, fixture, max_k):
     # oz_max_k lowers the per-pass K so n = 4096 / 8192 runs as 3-8 K chunks
@@ -135,7 +135,7 @@ def test_signed_cancellation_emulated_vs_reference(engine):
         assert float(np.max(np.abs(got.v - v))) <= TOL * scale
 
 
-@pytest.mark.parametrize("fixture,world", [("C5_n2048.npz", 8), ("C5_n1024.npz", 3), ("C4_n96.npz", 4),
+@pytest.mark.parametrize("fixture,world", [("C5_n2048.npz", 8), ("C5_n8192.npz", 8), ("C5_n1024.npz", 3), ("C4_n96.npz", 4),
                                            ("C3_n1024.npz", 8), ("C2_n1024.npz", 2)])
 def test_golden_row_sharded(engine, fixture, world):
     # the multi-GPU decomposition (row panels, triangle pieces + transpose
