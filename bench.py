@@ -47,6 +47,16 @@ FP64_PEAK_TFLOPS = 37.04      # mma.sync f64 m8n8k4 issue-rate probe (best confi
 FP64_CUBLAS_TFLOPS = 36.17    # cuBLAS DGEMM 16384^3 on this pool (profiles/r01_fp64_peak_probe.log)
 INT8_PEAK_TOPS = 4542.7       # tcgen05.mma kind::i8 M128 N256 K32 on 148 SMs, median of 300 back-to-back launches
 PROBE_MHZ = 1965.0            # SM clock the probes ran at
+# The issue-rate probe multiplies one resident tile of small constants: 390-530 W,
+# no power cap. The same MMA stream on uniformly random int8 digits (what a digit
+# GEMM feeds the tensor cores) rotated MMA to MMA, back to back for ~4 s, hits the
+# 1000 W cap with NO data movement at all: median 1680 MHz, 3867 TOPS
+# (tools/probe/peaks_random.sh -> profiles/r02_int8_sustained_probe.log). That is
+# the sustained INT8 ceiling of this GPU on real data; the library INT8 GEMM
+# (torch._int_mm -> cuBLASLt, 16384^3) measured beside it: 2678 TOPS burst,
+# 2019 TOPS sustained (862 MHz under the cap).
+INT8_SUSTAINED_TOPS = 3867.3
+INT8_LIBRARY_GEMM_TOPS = {"burst": 2678.3, "sustained": 2019.4}
 
 
 def measured_peaks() -> dict:
@@ -453,9 +463,15 @@ def main():
                     "fp64_equivalent_tflops": 2.0 * st["executed_gemm_macs"] / (gemm_ms * 1e-3) / 1e12
                     if gemm_ms > 0 else None,
                     "fp64_dmma_peak_tflops": FP64_PEAK_TFLOPS,
-                    "peak_source": f"measured INT8 tcgen05 issue-rate probe {INT8_PEAK_TOPS} TOPS (M128 N256 K32, "
-                                   f"148 SMs, 1965 MHz, profiles/r02_peak_probes.log); MEASURED_PEAKS.json has no "
-                                   f"INT8 entry",
+                    "peak_source": f"burst: measured INT8 tcgen05 issue-rate probe {INT8_PEAK_TOPS} TOPS (M128 N256 K32, "
+                                   f"148 SMs, constant operands, 1965 MHz, 530 W, profiles/r02_peak_probes.log); "
+                                   f"MEASURED_PEAKS.json has no INT8 entry",
+                    "peak_sustained": INT8_SUSTAINED_TOPS,
+                    "frac_sustained": achieved / INT8_SUSTAINED_TOPS if achieved else None,
+                    "peak_sustained_source": "the same probe on random int8 digits rotated MMA to MMA for 4 s: power-capped "
+                                             "(1000 W) at 1680 MHz with no data movement "
+                                             "(profiles/r02_int8_sustained_probe.log)",
+                    "library_int8_gemm_tops": INT8_LIBRARY_GEMM_TOPS,
                     "traffic": ncu_traffic(name, "gemm")}
     elif st["executed_gemm_macs"] > 0:
         achieved = 2.0 * st["executed_gemm_macs"] / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None

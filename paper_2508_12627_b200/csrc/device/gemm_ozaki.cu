@@ -985,18 +985,34 @@ __device__ __forceinline__ double oz_pow2_mul(double x, int sh) {
 
 // The S digit words of 16 consecutive values of one row (exponent e) to
 // out[t * slice_bytes], t = 0 (most significant) .. S-1.
+// Balanced base-256 digits without a per-digit carry chain: with
+// C = sum_t 128 * 256^t, m + C is non-negative (|m| < 2^{8S-2} < C) and its
+// plain bytes u_t satisfy m = sum_t (u_t - 128) 256^t, so the balanced digit
+// is u_t - 128 = u_t ^ 0x80 as an int8 (the representation with digits in
+// [-128, 127] is unique: the same digits the carry chain produced). One
+// 64-bit add and xor per value; the bytes are gathered into the slice words
+// with byte permutes (three per word).
 __device__ __forceinline__ void oz_digits16(const double (&xv)[16], int e, int slices, long long slice_bytes,
                                             int8_t* __restrict__ out) {
-    long long m[16];
+    const unsigned long long C = 0x8080808080808080ull >> (8 * (8 - slices));
+    unsigned lo[16], hi[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) m[j] = static_cast<long long>(oz_pow2_mul(xv[j], 8 * slices - 2 - e));
-    for (int t = slices - 1; t >= 0; --t) {  // least significant digit first
-        unsigned w[4] = {0, 0, 0, 0};
+    for (int j = 0; j < 16; ++j) {
+        const long long m = static_cast<long long>(oz_pow2_mul(xv[j], 8 * slices - 2 - e));
+        const unsigned long long u = (static_cast<unsigned long long>(m) + C) ^ C;
+        lo[j] = static_cast<unsigned>(u);
+        hi[j] = static_cast<unsigned>(u >> 32);
+    }
+    for (int t = 0; t < slices; ++t) {
+        const int b = slices - 1 - t;  // byte of u holding digit t
+        const unsigned sel = static_cast<unsigned>(b & 3) | (static_cast<unsigned>(4 + (b & 3)) << 4);
+        unsigned w[4];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int dg = static_cast<int>(static_cast<signed char>(m[j] & 0xFF));  // in [-128, 127]
-            m[j] = (m[j] - dg) >> 8;                                                  // exact
-            w[j >> 2] |= (static_cast<unsigned>(dg) & 0xFFu) << ((j & 3) * 8);
+        for (int g = 0; g < 4; ++g) {
+            const unsigned p01 = b < 4 ? __byte_perm(lo[4 * g], lo[4 * g + 1], sel) : __byte_perm(hi[4 * g], hi[4 * g + 1], sel);
+            const unsigned p23 = b < 4 ? __byte_perm(lo[4 * g + 2], lo[4 * g + 3], sel)
+                                       : __byte_perm(hi[4 * g + 2], hi[4 * g + 3], sel);
+            w[g] = __byte_perm(p01, p23, 0x5410);
         }
         *reinterpret_cast<uint4*>(out + t * slice_bytes) = make_uint4(w[0], w[1], w[2], w[3]);
     }
@@ -1147,6 +1163,68 @@ __global__ void __launch_bounds__(256) oz_split_lazy(OzLazy z, long long rows, l
     oz_digits16(xv, e, slices, slice_bytes, out + off);
 }
 
+// Unit-K-stride factors (VEC): the block's 128 rows x 32 values are formed
+// with lanes along K (a half warp reads one row's 256 contiguous bytes of
+// every factor as double2, so a warp instruction touches 2 lines instead of
+// the 32 a row-per-lane read does: the row-per-lane form ran at the L1
+// wavefront rate, 1.2-1.7 TB/s of digits) and staged as FP64 products in
+// shared memory (pitch 33: conflict-free for the row-per-lane digit phase,
+// which is unchanged: 512-byte coalesced slice stores per warp).
+template <int NF>
+__global__ void __launch_bounds__(256) oz_split_lazy_tiled(OzLazy z, long long rows, long long k0, long long k,
+                                                           const int* __restrict__ exps, long long kpad, int slices,
+                                                           long long slice_bytes, int8_t* __restrict__ out) {
+    constexpr int P = 33;
+    __shared__ double tile[OZ_BM * P];
+    __shared__ long long offs[NF][OZ_BM];
+    const long long rt = blockIdx.x;
+    const long long cb = static_cast<long long>(blockIdx.y) * 32;  // first K value of the block
+    if (threadIdx.x < OZ_BM) {
+        const long long R = rt * OZ_BM + threadIdx.x;
+        const double* base[kMaxGemmFactors];
+        if (R < rows) oz_lazy_bases(z, R, k0, base);
+#pragma unroll
+        for (int f = 0; f < NF; ++f) offs[f][threadIdx.x] = R < rows ? base[f] - z.ptr[f] : 0;
+    }
+    __syncthreads();
+    const int kp2 = threadIdx.x & 15;  // K pair within the 32 values
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int rr = (threadIdx.x >> 4) + 16 * i;
+        const long long c = cb + 2 * kp2;
+        double2 v = make_double2(0.0, 0.0);
+        if (rt * OZ_BM + rr < rows && c < k) {
+            if (c + 1 < k) {
+                v = make_double2(1.0, 1.0);
+#pragma unroll
+                for (int f = 0; f < NF; ++f) {
+                    const double2 w = __ldg(reinterpret_cast<const double2*>(z.ptr[f] + offs[f][rr] + c));
+                    v.x *= w.x;
+                    v.y *= w.y;
+                }
+            } else {  // odd K: the last value alone
+                v.x = 1.0;
+#pragma unroll
+                for (int f = 0; f < NF; ++f) v.x *= __ldg(z.ptr[f] + offs[f][rr] + c);
+            }
+        }
+        tile[rr * P + 2 * kp2] = v.x;
+        tile[rr * P + 2 * kp2 + 1] = v.y;
+    }
+    __syncthreads();
+    const int rr = threadIdx.x & 127;
+    const int half = threadIdx.x >> 7;
+    const long long R = rt * OZ_BM + rr;
+    const long long c0 = cb + half * 16;
+    double xv[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) xv[j] = tile[rr * P + half * 16 + j];
+    const int e = R < rows ? exps[R] : 0;
+    const long long kt = c0 / OZ_BK, cin = (c0 % OZ_BK) / 16;
+    const long long off = (rt * (kpad / OZ_BK) + kt) * (OZ_BM * OZ_BK) + cin * (OZ_BM * 16) + rr * 16;
+    oz_digits16(xv, e, slices, slice_bytes, out + off);
+}
+
 constexpr int OZ_SPLIT_THREADS = 256;
 __global__ void __launch_bounds__(OZ_SPLIT_THREADS) oz_split(const double* __restrict__ x, long long rows, long long k,
                                                             long long rs, long long ks, const int* __restrict__ exps,
@@ -1249,7 +1327,7 @@ int ozaki_split_lazy(const GemmSide& side, long long n, long long rows, long lon
         constexpr int NF = decltype(nf)::value;
         if (vec) {
             oz_row_exponents_lazy<NF, true><<<eg, 256, 0, s>>>(z, rows, k0, k, exps);
-            oz_split_lazy<NF, true><<<sg, 256, 0, s>>>(z, rows, k0, k, exps, kp, slices, rp * kp, out);
+            oz_split_lazy_tiled<NF><<<sg, 256, 0, s>>>(z, rows, k0, k, exps, kp, slices, rp * kp, out);
         } else {
             oz_row_exponents_lazy<NF, false><<<eg, 256, 0, s>>>(z, rows, k0, k, exps);
             oz_split_lazy<NF, false><<<sg, 256, 0, s>>>(z, rows, k0, k, exps, kp, slices, rp * kp, out);

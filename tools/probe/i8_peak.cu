@@ -11,14 +11,28 @@ __device__ __forceinline__ unsigned long long desc(unsigned a, unsigned lbo, uns
            ((unsigned long long)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
 }
 
-template <int N>
+// RANDOM: eight distinct A and B operand tiles of uniformly random int8 digits
+// (the data a real digit GEMM feeds the tensor cores), rotated MMA to MMA, so
+// the operand buses and multipliers toggle as they do under load; otherwise
+// one resident tile of small constants (pure issue rate, little switching).
+template <int N, bool RANDOM = false>
 __global__ void peak(int iters, int* sink) {
-    __shared__ __align__(1024) int8_t a[128 * 32];
-    __shared__ __align__(1024) int8_t b[N * 32];
+    constexpr int T = RANDOM ? 8 : 1;
+    extern __shared__ __align__(1024) int8_t smem[];
+    int8_t* a = smem;
+    int8_t* b = smem + T * 128 * 32;
     __shared__ unsigned tmem;
     __shared__ __align__(8) unsigned long long bar;
-    for (int i = threadIdx.x; i < 128 * 32; i += blockDim.x) a[i] = (int8_t)(i & 7);
-    for (int i = threadIdx.x; i < N * 32; i += blockDim.x) b[i] = (int8_t)(i & 3);
+    if (RANDOM) {
+        for (int i = threadIdx.x; i < T * (128 + N) * 32; i += blockDim.x) {
+            unsigned h = (unsigned)i * 2654435761u + blockIdx.x * 40503u;
+            h ^= h >> 15; h *= 2246822519u; h ^= h >> 13;
+            smem[i] = (int8_t)(h & 0xFF);
+        }
+    } else {
+        for (int i = threadIdx.x; i < 128 * 32; i += blockDim.x) a[i] = (int8_t)(i & 7);
+        for (int i = threadIdx.x; i < N * 32; i += blockDim.x) b[i] = (int8_t)(i & 3);
+    }
     if (threadIdx.x < 32) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tmem)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -36,8 +50,13 @@ __global__ void peak(int iters, int* sink) {
         const unsigned long long da = desc(su32(a), 128 * 16, 128), db = desc(su32(b), N * 16, 128);
         for (int i = 0; i < iters; ++i) {
             const unsigned acc = tmem + (unsigned)((i & 1) * N);
+            // descriptor start addresses are in 16-byte units: step to the next tile
+            const unsigned long long ta = da + (unsigned long long)((i % T) * (128 * 32 / 16));
+            const unsigned long long tb = db + (unsigned long long)(((i / 3) % T) * (N * 32 / 16));
+            // random data: restart the accumulation every 512 MMAs (int32 stays exact)
+            const int accumulate = RANDOM ? ((i & 511) > 1 ? 1 : 0) : (i > 1 ? 1 : 0);
             asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(acc),
-                         "l"(da), "l"(db), "r"(idesc), "r"(i > 1 ? 1 : 0));
+                         "l"(ta), "l"(tb), "r"(idesc), "r"(accumulate));
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)));
     }
@@ -52,30 +71,37 @@ __global__ void peak(int iters, int* sink) {
     if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-template <int N>
+template <int N, bool RANDOM = false>
 void run(int blocks, int iters) {
     int* sink;
     cudaMalloc(&sink, blocks * sizeof(int));
-    peak<N><<<blocks, 128>>>(100, sink);
+    const int bytes = (RANDOM ? 8 : 1) * (128 + N) * 32;
+    cudaFuncSetAttribute(peak<N, RANDOM>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    peak<N, RANDOM><<<blocks, 128, bytes>>>(100, sink);
     cudaDeviceSynchronize();
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    peak<N><<<blocks, 128>>>(iters, sink);
+    peak<N, RANDOM><<<blocks, 128, bytes>>>(iters, sink);
     cudaEventRecord(e1);
     cudaError_t e = cudaEventSynchronize(e1);
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     const double ops = 2.0 * 128 * N * 32 * (double)iters * blocks;
-    printf("N=%d blocks=%d iters=%d: %.3f ms, %.1f TOPS (%s)\n", N, blocks, iters, ms, ops / ms / 1e9, cudaGetErrorString(e));
+    printf("N=%d%s blocks=%d iters=%d: %.3f ms, %.1f TOPS (%s)\n", N, RANDOM ? " random-digits" : "", blocks, iters, ms, ops / ms / 1e9, cudaGetErrorString(e));
     cudaFree(sink);
 }
 
 // i8_peak            -> burst: one launch per shape
 // i8_peak sustained  -> N=256 launched back to back for ~4 s (clocks settle
 //                       under the power cap; nvidia-smi samples them)
+// i8_peak random     -> the same with random int8 operands rotated MMA to MMA
 int main(int argc, char** argv) {
+    if (argc > 1 && argv[1][0] == 'r') {  // random digits, back to back for ~4 s
+        for (int r = 0; r < 300; ++r) run<256, true>(148, 200000);
+        return 0;
+    }
     if (argc > 1) {
         for (int r = 0; r < 300; ++r) run<256>(148, 200000);
         return 0;
