@@ -192,7 +192,9 @@ StatisticResult u_statistic_data(const std::string& spec, const double* data, lo
             const int F = ncols * kmax;
             Buf z = rt.allocate(1, n * F), y = rt.allocate(1, n * F), g = rt.allocate(1, static_cast<long long>(F) * F);
             launch_cosine_features(x, n, d, ncols, kmax, z->ptr, s);
-            launch_thin_gram(z->ptr, n, F, g->ptr, s);
+            const long long gram_scratch = thin_gram_scratch_entries(n, F);
+            Buf gp = gram_scratch ? rt.allocate(1, gram_scratch) : nullptr;
+            launch_thin_gram(z->ptr, n, F, g->ptr, gp ? gp->ptr : nullptr, s);
             std::vector<double> G(static_cast<std::size_t>(F * F));
             check_cuda(cudaMemcpyAsync(G.data(), g->ptr, G.size() * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
             check_cuda(cudaStreamSynchronize(s), "sync");
@@ -213,7 +215,7 @@ StatisticResult u_statistic_data(const std::string& spec, const double* data, lo
             e.count = 1;
             e.d[0].mode = kEpiStore;
             e.d[0].out = b->ptr;
-            launches += 3;  // features, thin Gram, Z M
+            launches += gram_scratch ? 4 : 3;  // features, thin Gram (+ its finalizer), Z M
             const int gl = launch_gemm_multi(a, e, s);
             launches += gl > 0 ? static_cast<std::uint64_t>(gl) : 1;
             if (gl < 0) {  // operands not TMA-eligible (odd F): plain product

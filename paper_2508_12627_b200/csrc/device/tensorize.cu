@@ -222,7 +222,52 @@ __global__ void cosine_features(const double* __restrict__ x, long long n, int d
     }
 }
 
-// G = Z^T Z / n for a thin Z (n x F, F <= 128): one block per (f, g) pair,
+// G = Z^T Z / n for a thin Z (n x F). Each block takes a contiguous range of
+// rows, stages 32-row tiles of Z in shared memory with coalesced loads and
+// accumulates its F x F partial Gram in registers (thread t: entries
+// t, t + 256, ...; rows in order); gram_finalize then sums the block partials
+// in block order. Fixed order throughout: deterministic, and G is bitwise
+// symmetric (entry (f, h) and (h, f) add the same products in the same order).
+constexpr int kGramRows = 32, kGramMaxF = 64, kGramPerThread = kGramMaxF * kGramMaxF / 256;
+__global__ void __launch_bounds__(256) thin_gram_partial(const double* __restrict__ z, long long n, int F,
+                                                         double* __restrict__ partial) {
+    __shared__ double tile[kGramRows][kGramMaxF + 1];
+    const long long B = gridDim.x;
+    const long long lo = n * blockIdx.x / B, hi = n * (blockIdx.x + 1) / B;
+    double acc[kGramPerThread];
+#pragma unroll
+    for (int q = 0; q < kGramPerThread; ++q) acc[q] = 0.0;
+    for (long long r0 = lo; r0 < hi; r0 += kGramRows) {
+        const int rows = static_cast<int>(hi - r0 < kGramRows ? hi - r0 : kGramRows);
+        __syncthreads();
+        for (int e = threadIdx.x; e < rows * F; e += 256) tile[e / F][e % F] = z[r0 * F + e];
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kGramPerThread; ++q) {
+            const int e = threadIdx.x + 256 * q;
+            if (e < F * F) {
+                const int f = e / F, h = e % F;
+                double s = acc[q];
+                for (int r = 0; r < rows; ++r) s += tile[r][f] * tile[r][h];
+                acc[q] = s;
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kGramPerThread; ++q) {
+        const int e = threadIdx.x + 256 * q;
+        if (e < F * F) partial[static_cast<long long>(blockIdx.x) * F * F + e] = acc[q];
+    }
+}
+__global__ void gram_finalize(const double* __restrict__ partial, int blocks, int F, long long n, double* __restrict__ g) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= F * F) return;
+    double s = 0.0;
+    for (int b = 0; b < blocks; ++b) s += partial[static_cast<long long>(b) * F * F + e];
+    g[e] = s / static_cast<double>(n);
+}
+
+// Fallback for wide feature sets (F > 64): one block per (f, g) pair,
 // fixed-order strided sums + tree (deterministic).
 __global__ void thin_gram(const double* __restrict__ z, long long n, int F, double* __restrict__ g) {
     __shared__ double red[256];
@@ -238,16 +283,18 @@ __global__ void thin_gram(const double* __restrict__ z, long long n, int F, doub
     if (threadIdx.x == 0) g[f * F + h] = red[0] / static_cast<double>(n);
 }
 
-// Y = Z M (n x F times a small dense F x F).
+// Y = Z M (n x F times a small dense F x F): a thread per output entry, the
+// F products summed in order (lanes along the output row: M reads coalesce,
+// the Z row is a warp-wide broadcast).
 __global__ void times_small(const double* __restrict__ z, long long n, int F, const double* __restrict__ M,
                             double* __restrict__ y) {
-    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    if (i >= n) return;
-    for (int c = 0; c < F; ++c) {
-        double s = 0.0;
-        for (int r = 0; r < F; ++r) s += z[i * F + r] * M[r * F + c];
-        y[i * F + c] = s;
-    }
+    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (e >= n * F) return;
+    const long long i = e / F;
+    const int c = static_cast<int>(e - i * F);
+    double s = 0.0;
+    for (int r = 0; r < F; ++r) s += __ldg(z + i * F + r) * __ldg(M + r * F + c);
+    y[e] = s;
 }
 
 }  // namespace
@@ -308,12 +355,25 @@ void launch_cosine_features(const double* x, long long n, int d, int ncols, int 
     cosine_features<<<static_cast<unsigned>((n + 127) / 128), 128, 0, s>>>(x, n, d, ncols, kmax, z);
 }
 
-void launch_thin_gram(const double* z, long long n, int F, double* g, cudaStream_t s) {
+long long thin_gram_scratch_entries(long long n, int F) {
+    if (F > kGramMaxF) return 0;
+    long long blocks = (n + 4 * kGramRows - 1) / (4 * kGramRows);  // at least 128 rows per block
+    if (blocks > 296) blocks = 296;
+    return blocks * F * F;
+}
+
+void launch_thin_gram(const double* z, long long n, int F, double* g, double* partial, cudaStream_t s) {
+    if (F <= kGramMaxF) {
+        const int blocks = static_cast<int>(thin_gram_scratch_entries(n, F) / (static_cast<long long>(F) * F));
+        thin_gram_partial<<<static_cast<unsigned>(blocks), 256, 0, s>>>(z, n, F, partial);
+        gram_finalize<<<static_cast<unsigned>((F * F + 255) / 256), 256, 0, s>>>(partial, blocks, F, n, g);
+        return;
+    }
     thin_gram<<<dim3(static_cast<unsigned>(F), static_cast<unsigned>(F)), 256, 0, s>>>(z, n, F, g);
 }
 
 void launch_times_small(const double* z, long long n, int F, const double* M, double* y, cudaStream_t s) {
-    times_small<<<static_cast<unsigned>((n + 127) / 128), 128, 0, s>>>(z, n, F, M, y);
+    times_small<<<static_cast<unsigned>((n * F + 255) / 256), 256, 0, s>>>(z, n, F, M, y);
 }
 
 }  // namespace ustats::dev

@@ -22,7 +22,9 @@ void launch_scaled_gram(const double* x, long long n, int d, int col_left, int c
                         cudaStream_t s);
 void launch_column(const double* x, long long n, int d, int c, double* out, cudaStream_t s);
 void launch_cosine_features(const double* x, long long n, int d, int ncols, int kmax, double* z, cudaStream_t s);
-void launch_thin_gram(const double* z, long long n, int F, double* g, cudaStream_t s);
+// G = Z^T Z / n; `partial` holds thin_gram_scratch_entries(n, F) doubles (0: none needed).
+long long thin_gram_scratch_entries(long long n, int F);
+void launch_thin_gram(const double* z, long long n, int F, double* g, double* partial, cudaStream_t s);
 void launch_times_small(const double* z, long long n, int F, const double* M, double* y, cudaStream_t s);
 
 struct StatisticResult;
