@@ -84,6 +84,9 @@ struct StreamArgs {
     // the buffer's layout; output dim d sits at out[sum_d digit_d * ostride[d]]
     int permuted_out = 0;
     long long ostride[kMaxDims] = {};
+    // mult[0]: multiplicity of factor 0 (1..4): identical views of one tensor
+    // merged by launch_stream into one load raised to a power (paired kernels only)
+    int mult[kMaxFactors] = {1, 1, 1, 1, 1, 1, 1, 1};
 };
 
 // One GEMM operand: value(r, k) = prod_f ptr_f[ off_f(r) + kstride_f * k ]

@@ -110,6 +110,17 @@ void with_nf(int nf, Fn&& fn) {
     }
 }
 
+// Calls fn(std::integral_constant<int, M0>) for the multiplicity of factor 0 (1..4).
+template <typename Fn>
+void with_m0(int m0, Fn&& fn) {
+    switch (m0) {
+        case 2: fn(std::integral_constant<int, 2>{}); break;
+        case 3: fn(std::integral_constant<int, 3>{}); break;
+        case 4: fn(std::integral_constant<int, 4>{}); break;
+        default: fn(std::integral_constant<int, 1>{}); break;
+    }
+}
+
 // ------------------------------------------------ paired (16-byte) fast path
 // When every factor walks the inner dim with stride 1 (loaded as double2) or
 // 0 (a per-line constant), lines are streamed as aligned pairs: 16-byte
@@ -129,7 +140,20 @@ __device__ __forceinline__ void line_offsets(const StreamArgs& a, unsigned long 
     }
 }
 
-template <int NF>
+// x^M for a compile-time multiplicity (identical views of one tensor merged by
+// launch_stream into factor 0): M - 1 multiplies at most, for M = 4 two.
+template <int M>
+__device__ __forceinline__ double pow_small(double x) {
+    if constexpr (M == 1) return x;
+    else if constexpr (M == 2) return x * x;
+    else if constexpr (M == 3) return x * x * x;
+    else {
+        const double x2 = x * x;
+        return x2 * x2;
+    }
+}
+
+template <int NF, int M0 = 1>
 struct PairLine {
     const double2* p[NF];
     double c[NF];
@@ -140,7 +164,7 @@ struct PairLine {
             const double* q = a.ptr[f] + off[f];
             unit[f] = a.stride[f][inner] != 0;
             p[f] = reinterpret_cast<const double2*>(q);
-            c[f] = unit[f] ? 0.0 : __ldg(q);
+            c[f] = unit[f] ? 0.0 : (f == 0 ? pow_small<M0>(__ldg(q)) : __ldg(q));
         }
     }
     __device__ __forceinline__ double2 at(long long q) const {
@@ -148,7 +172,11 @@ struct PairLine {
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
             if (unit[f]) {
-                const double2 x = __ldg(p[f] + q);
+                double2 x = __ldg(p[f] + q);
+                if (f == 0) {
+                    x.x = pow_small<M0>(x.x);
+                    x.y = pow_small<M0>(x.y);
+                }
                 v.x *= x.x;
                 v.y *= x.y;
             } else {
@@ -336,7 +364,7 @@ __global__ void stream_reduce_thread(StreamArgs a, unsigned long long outputs,
 
 // Paired variants of the three kernels above (inner extent even, every
 // factor's inner stride 0 or 1, 16-byte aligned lines).
-template <int NF>
+template <int NF, int M0>
 __global__ void __launch_bounds__(256) stream_elementwise_pairs(StreamArgs a, unsigned long long rows,
                                                                 long long inner_n) {
     const int inner = a.n_out - 1, rdim = a.n_out - 2;
@@ -354,7 +382,7 @@ __global__ void __launch_bounds__(256) stream_elementwise_pairs(StreamArgs a, un
             digit = rdim > 0 ? static_cast<long long>(row % static_cast<unsigned long long>(a.n)) : 0;
             fresh = false;
         }
-        PairLine<NF> L;
+        PairLine<NF, M0> L;
         L.setup(a, off, inner);
         double2* out = reinterpret_cast<double2*>(a.out + row * inner_n);
         for (long long q = threadIdx.x; q < pairs; q += blockDim.x) {
@@ -379,7 +407,7 @@ __global__ void __launch_bounds__(256) stream_elementwise_pairs(StreamArgs a, un
 }
 
 // Long rows: the block's threads share each row (C3: 8192 pairs per row).
-template <int NF>
+template <int NF, int M0>
 __global__ void __launch_bounds__(256, 4) stream_reduce_all_pairs_block(StreamArgs a, unsigned long long rows,
                                                                      long long inner_n, double* partial) {
     __shared__ double red[32];
@@ -391,7 +419,7 @@ __global__ void __launch_bounds__(256, 4) stream_reduce_all_pairs_block(StreamAr
     for (unsigned long long row = lo; row < hi; ++row) {
         long long off[NF];
         line_offsets<NF>(a, row, 0, D - 1, off);
-        PairLine<NF> L;
+        PairLine<NF, M0> L;
         L.setup(a, off, inner);
         acc += L.sum(threadIdx.x, inner_n >> 1, blockDim.x);
     }
@@ -403,7 +431,7 @@ __global__ void __launch_bounds__(256, 4) stream_reduce_all_pairs_block(StreamAr
 // odometer on the last row dim (one division per wrap, not per row), lanes
 // over the row's pairs: short rows (C4: n = 1024) no longer pay the row
 // setup per few loads.
-template <int NF>
+template <int NF, int M0>
 __global__ void __launch_bounds__(256, 4) stream_reduce_all_pairs(StreamArgs a, unsigned long long rows,
                                                                long long inner_n, double* partial) {
     __shared__ double red[32];
@@ -425,7 +453,7 @@ __global__ void __launch_bounds__(256, 4) stream_reduce_all_pairs(StreamArgs a, 
             digit = rdim > 0 ? static_cast<long long>(row % static_cast<unsigned long long>(a.n)) : 0;
             fresh = false;
         }
-        PairLine<NF> L;
+        PairLine<NF, M0> L;
         L.setup(a, off, inner);
         acc += L.sum(lane, inner_n >> 1, 32);
         ++digit;
@@ -440,7 +468,7 @@ __global__ void __launch_bounds__(256, 4) stream_reduce_all_pairs(StreamArgs a, 
     if (threadIdx.x == 0) partial[blockIdx.x] = t;
 }
 
-template <int NF>
+template <int NF, int M0>
 __global__ void __launch_bounds__(256, 4) stream_reduce_warp_pairs(StreamArgs a, unsigned long long outputs,
                                                                 unsigned long long srows) {
     const int lane = threadIdx.x & 31;
@@ -456,7 +484,7 @@ __global__ void __launch_bounds__(256, 4) stream_reduce_warp_pairs(StreamArgs a,
         line_offsets<NF>(a, sr, a.n_out, a.n_sum - 1, off);
 #pragma unroll
         for (int f = 0; f < NF; ++f) off[f] += base[f];
-        PairLine<NF> L;
+        PairLine<NF, M0> L;
         L.setup(a, off, inner);
         acc += L.sum(lane, a.n >> 1, 32);
     }
@@ -565,6 +593,59 @@ bool pairs_ok(const StreamArgs& a, int inner, long long inner_n, int dims) {
 }
 }  // namespace
 
+namespace {
+// Identical views of one tensor (same base, same stride on every iteration
+// dim: A_ij A_ij, or both orientations of a symmetric matrix after the
+// planner made them unit-stride) become ONE factor with a multiplicity: the
+// paired kernels load it once and raise it to the power (pow_small). C3's
+// sum B^4 r e read B through four views (L1-hit loads competing with the DRAM
+// stream for LSU slots: 3.0 TB/s); merged it streams like a one-matrix op.
+StreamArgs merge_identical_views(const StreamArgs& a) {
+    const int dims = a.n_out + a.n_sum;
+    auto same = [&](int f, int g) {
+        if (a.ptr[f] != a.ptr[g]) return false;
+        for (int k = 0; k < dims; ++k)
+            if (a.stride[f][k] != a.stride[g][k]) return false;
+        return true;
+    };
+    // the view with the most copies (first such)
+    int best = -1, best_count = 1;
+    for (int f = 0; f < a.nf; ++f) {
+        int count = 0;
+        for (int g = 0; g < a.nf; ++g) count += same(f, g);
+        if (count > best_count) {
+            best = f;
+            best_count = count;
+        }
+    }
+    if (best < 0) return a;
+    const int m0 = best_count > 4 ? 4 : best_count;
+    StreamArgs d = a;
+    int nf = 0, dropped = 0;
+    auto put_factor = [&](int f) {
+        d.ptr[nf] = a.ptr[f];
+        for (int k = 0; k < kMaxDims; ++k) d.stride[nf][k] = a.stride[f][k];
+        ++nf;
+    };
+    put_factor(best);
+    for (int f = 0; f < a.nf; ++f) {
+        if (f == best) continue;
+        if (same(f, best) && dropped < m0 - 1) {
+            ++dropped;
+            continue;
+        }
+        put_factor(f);
+    }
+    for (int f = nf; f < kMaxFactors; ++f) {
+        d.ptr[f] = nullptr;
+        for (int k = 0; k < kMaxDims; ++k) d.stride[f][k] = 0;
+    }
+    d.nf = nf;
+    d.mult[0] = m0;
+    return d;
+}
+}  // namespace
+
 int launch_stream(const StreamArgs& args, double* scratch, std::size_t scratch_entries,
                   int sm_count, cudaStream_t s) {
     StreamArgs a = args;
@@ -583,11 +664,14 @@ int launch_stream(const StreamArgs& args, double* scratch, std::size_t scratch_e
         const unsigned long long rows = a.n_out >= 2 ? span(a, a.n_out - 1) : 1;
         const long long inner_n = a.n_out == 1 ? ext0(a) : a.n;
         if (pairs_ok(a, a.n_out - 1, inner_n, a.n_out) && (reinterpret_cast<unsigned long long>(a.out) & 15) == 0) {
-            with_nf(a.nf, [&](auto nf) {
-                auto k = stream_elementwise_pairs<decltype(nf)::value>;
-                unsigned long long blocks = static_cast<unsigned long long>(sm_count) * resident_blocks(k);
-                if (blocks > rows) blocks = rows;
-                k<<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(a, rows, inner_n);
+            const StreamArgs m = merge_identical_views(a);
+            with_nf(m.nf, [&](auto nf) {
+                with_m0(m.mult[0], [&](auto m0) {
+                    auto k = stream_elementwise_pairs<decltype(nf)::value, decltype(m0)::value>;
+                    unsigned long long blocks = static_cast<unsigned long long>(sm_count) * resident_blocks(k);
+                    if (blocks > rows) blocks = rows;
+                    k<<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(m, rows, inner_n);
+                });
             });
             return 1;
         }
@@ -604,15 +688,19 @@ int launch_stream(const StreamArgs& args, double* scratch, std::size_t scratch_e
         // one full wave of resident blocks (never more than the scratch holds)
         int blocks = blocks_for_all(rows, inner_n, sm_count);
         const bool pairs = pairs_ok(a, D - 1, inner_n, D);
-        with_nf(a.nf, [&](auto nf) {
-            constexpr int NF = decltype(nf)::value;
-            auto k = pairs ? stream_reduce_all_pairs<NF> : stream_reduce_all<NF>;
-            // many short rows: a warp per row range; few long rows: blocks share rows
-            if (pairs && (inner_n > 4096 || rows < 4ull * static_cast<unsigned long long>(sm_count) * 64))
-                k = stream_reduce_all_pairs_block<NF>;
-            const int wave = sm_count * resident_blocks(k);
-            if (blocks > wave) blocks = wave;
-            k<<<blocks, kThreads, 0, s>>>(a, rows, inner_n, scratch);
+        const StreamArgs m = pairs ? merge_identical_views(a) : a;
+        with_nf(m.nf, [&](auto nf) {
+            with_m0(m.mult[0], [&](auto m0) {
+                constexpr int NF = decltype(nf)::value;
+                constexpr int M0 = decltype(m0)::value;
+                auto k = !pairs ? stream_reduce_all<NF> : stream_reduce_all_pairs<NF, M0>;
+                // many short rows: a warp per row range; few long rows: blocks share rows
+                if (pairs && (inner_n > 4096 || rows < 4ull * static_cast<unsigned long long>(sm_count) * 64))
+                    k = stream_reduce_all_pairs_block<NF, M0>;
+                const int wave = sm_count * resident_blocks(k);
+                if (blocks > wave) blocks = wave;
+                k<<<blocks, kThreads, 0, s>>>(m, rows, inner_n, scratch);
+            });
         });
         finalize_scalar<<<1, 1024, 0, s>>>(scratch, static_cast<unsigned long long>(blocks), a.scale, a.out,
                                            a.accumulate);
@@ -631,13 +719,16 @@ int launch_stream(const StreamArgs& args, double* scratch, std::size_t scratch_e
         const unsigned long long srows = ipow(a.n, a.n_sum - 1);
         const unsigned long long blocks = (outputs + (kThreads / 32) - 1) / (kThreads / 32);
         const bool pairs = pairs_ok(a, last, a.n, last + 1);
-        with_nf(a.nf, [&](auto nf) {
+        const StreamArgs m = pairs ? merge_identical_views(a) : a;
+        with_nf(m.nf, [&](auto nf) {
+            constexpr int NF = decltype(nf)::value;
             if (pairs)
-                stream_reduce_warp_pairs<decltype(nf)::value>
-                    <<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(a, outputs, srows);
+                with_m0(m.mult[0], [&](auto m0) {
+                    stream_reduce_warp_pairs<NF, decltype(m0)::value>
+                        <<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(m, outputs, srows);
+                });
             else
-                stream_reduce_warp<decltype(nf)::value>
-                    <<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(a, outputs, srows);
+                stream_reduce_warp<NF><<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(m, outputs, srows);
         });
         return 1;
     }
