@@ -55,7 +55,8 @@ typedef struct us_config {
     int32_t emulate_world;       /* row sharding over this many virtual ranks on one device (tests) */
     uint64_t memory_budget_bytes; /* device bytes the memory-bounded schedule may plan for (0 = free memory) */
     int32_t oz_slices;           /* emulated-GEMM digit slices (0 = error-bound guard; 4..7 forced) */
-    int32_t reserved0;
+    int32_t oz_min_dim;          /* smallest rows / cols / K of an emulated GEMM (0 = 1024; tests lower it to
+                                    pin the emulated path against the reference at sizes its CPU run reaches) */
     int64_t oz_max_k;            /* longest emulated K per pass (0 = 21000, the int32-exact bound) */
 } us_config;
 

@@ -29,7 +29,7 @@ class UsConfig(C.Structure):
         ("emulate_world", i32),
         ("memory_budget_bytes", u64),
         ("oz_slices", i32),
-        ("reserved0", i32),
+        ("oz_min_dim", i32),
         ("oz_max_k", i64),
     ]
 

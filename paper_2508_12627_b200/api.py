@@ -63,6 +63,7 @@ class Config:
     memory_budget_bytes: int = 0  # device bytes the memory-bounded schedule may use (0 = free memory)
     oz_slices: int = 0           # emulated-GEMM digit slices (0 = error-bound guard, 4..7 forced)
     oz_max_k: int = 0            # longest emulated K per pass (0 = 21000); longer K runs in chunks
+    oz_min_dim: int = 0          # smallest rows / cols / K of an emulated GEMM (0 = 1024; tests lower it)
 
     def native(self) -> N.UsConfig:
         c = N.UsConfig()
@@ -85,6 +86,7 @@ class Config:
         c.memory_budget_bytes = self.memory_budget_bytes
         c.oz_slices = self.oz_slices
         c.oz_max_k = self.oz_max_k
+        c.oz_min_dim = self.oz_min_dim
         return c
 
 

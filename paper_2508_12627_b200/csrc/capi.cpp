@@ -72,6 +72,9 @@ ustats::Config to_config(const us_config* c) {
     if (c->oz_max_k < 0 || (c->oz_max_k > 0 && c->oz_max_k < 64))
         ustats::fail(ustats::ErrorCode::InvalidArgument, "oz_max_k must be 0 (auto) or >= 64");
     cfg.device.oz_max_k = c->oz_max_k;
+    if (c->oz_min_dim < 0 || (c->oz_min_dim > 0 && c->oz_min_dim < 128))
+        ustats::fail(ustats::ErrorCode::InvalidArgument, "oz_min_dim must be 0 (1024) or >= 128");
+    cfg.device.oz_min_dim = c->oz_min_dim;
     return cfg;
 }
 

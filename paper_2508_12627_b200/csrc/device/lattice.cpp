@@ -218,7 +218,7 @@ std::string plan_key(const std::vector<StatisticSpec>& specs, const std::vector<
                     "," + std::to_string(d.rank) + "," +
                     std::to_string(d.world_size) + "," + std::to_string(d.emulate_world) + "," +
                     std::to_string(d.memory_budget_bytes) + "," + std::to_string(d.oz_slices) + "," +
-                    std::to_string(d.oz_max_k) + "|";
+                    std::to_string(d.oz_max_k) + "," + std::to_string(d.oz_min_dim) + "|";
     for (const Buf& b : uniq) k += std::to_string(b->order) + (b->symmetric ? "s" : "g");
     for (std::size_t q = 0; q < specs.size(); ++q) {
         k += "|" + std::to_string(specs[q].m) + ":";

@@ -228,9 +228,11 @@ void Program::run_stream(const Op& op, double* out) {
 
 // FP64 emulation on the INT8 tensor cores (gemm_ozaki.cu) for large plain
 // products whose K keeps every digit diagonal exact in int32.
-constexpr long long kOzMinDim = 1024;   // below, DMMA is as fast and needs no digit pass
-constexpr long long kOzMinK = 1024;     // shorter K: per-tile drains and digit passes outweigh the MMA savings
-                                        // (C4's Khatri-Rao GEMMs, K = 1024: 297 -> 216 ms per evaluation)
+// Smallest rows / cols / K of an emulated GEMM: below 1024, DMMA is as fast and
+// needs no digit pass, and per-tile drains outweigh the MMA savings (C4's
+// Khatri-Rao GEMMs, K = 1024: 297 -> 216 ms per evaluation). Config.oz_min_dim
+// lowers it (tests pin the emulated path at sizes the CPU reference reaches).
+long long oz_min_dim(const DeviceConfig& dc) { return dc.oz_min_dim > 0 ? dc.oz_min_dim : 1024; }
 constexpr double kOzDigitCap = 8.0 * 1073741824.0;  // digit bytes per operand per K chunk (C4: 4 GiB split its
                                                     // K = 1024 GEMMs in two, 112 -> 158 ms per evaluation)
 
@@ -292,7 +294,8 @@ bool lazy_side(const GemmSide& s) { return s.nf >= 2 && s.nf <= kMaxGemmFactors 
 
 bool Program::emulated_eligible(const GemmArgs& g) const {
     if (!config_.device.fp64_emulation) return false;
-    if (g.n < kOzMinK || g.rows < kOzMinDim || g.cols < kOzMinDim) return false;
+    const long long lo = oz_min_dim(config_.device);
+    if (g.n < lo || g.rows < lo || g.cols < lo) return false;
     return (flat_row_stride(g.a, n_) >= 0 || lazy_side(g.a)) && (flat_row_stride(g.b, n_) >= 0 || lazy_side(g.b));
 }
 
@@ -303,7 +306,8 @@ std::size_t Program::op_scratch_bytes(const Op& op) const {
     if (!op.gemm || !config_.device.fp64_emulation) return 0;
     const long long rows = static_cast<long long>(ipow(n_, static_cast<int>(op.ra.size())));
     const long long cols = static_cast<long long>(ipow(n_, static_cast<int>(op.rb.size())));
-    if (n_ < kOzMinK || rows < kOzMinDim || cols < kOzMinDim) return 0;
+    const long long lo = oz_min_dim(config_.device);
+    if (n_ < lo || rows < lo || cols < lo) return 0;
     const bool same = op.fa.size() == 1 && op.fb.size() == 1 && op.fa[0].buf == op.fb[0].buf && rows == cols;
     return oz_plan(n_, rows, cols, same, config_.device).scratch_bytes;
 }
@@ -338,13 +342,14 @@ std::string Program::operand_key(const std::vector<View>& fs, const std::vector<
 // How many emulated single-chunk GEMMs read each operand (single-GPU runs).
 void Program::plan_digit_reuse() {
     digit_uses_.clear();
-    if (!config_.device.fp64_emulation || n_ < kOzMinK) return;
+    const long long lo = oz_min_dim(config_.device);
+    if (!config_.device.fp64_emulation || n_ < lo) return;
     for (std::size_t i : schedule_) {
         const Op& op = ops_[i];
         if (op.dead || !op.gemm) continue;
         const long long rows = static_cast<long long>(ipow(n_, static_cast<int>(op.ra.size())));
         const long long cols = static_cast<long long>(ipow(n_, static_cast<int>(op.rb.size())));
-        if (rows < kOzMinDim || cols < kOzMinDim) continue;
+        if (rows < lo || cols < lo) continue;
         if (oz_plan(n_, rows, cols, false, config_.device).nchunks != 1) continue;
         const std::string ka = operand_key(op.fa, op.ra, op.e), kb = operand_key(op.fb, op.rb, op.e);
         ++digit_uses_[ka];

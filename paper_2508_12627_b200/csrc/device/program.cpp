@@ -862,7 +862,8 @@ void Program::make_schedule(double budget) {
 // n^3 Khatri-Rao operands (8.6 GB each in FP64) are written, read for the
 // row exponents and read again for the digits no more.
 void Program::lazy_operands() {
-    if (!config_.device.fp64_emulation || n_ < 1024) return;
+    const std::uint64_t lo = config_.device.oz_min_dim > 0 ? static_cast<std::uint64_t>(config_.device.oz_min_dim) : 1024;
+    if (!config_.device.fp64_emulation || static_cast<std::uint64_t>(n_) < lo) return;
     std::vector<int> readers(bufs_.size(), 0);
     for (const Op& op : ops_)
         if (!op.dead) for_each_read(op, [&](const View& v) { ++readers[static_cast<std::size_t>(v.buf)]; });
@@ -895,7 +896,7 @@ void Program::lazy_operands() {
             const std::uint64_t rows = ipow(n_, static_cast<int>(g.ra.size())), cols = ipow(n_, static_cast<int>(g.rb.size()));
             // fused epilogues need plain TMA operands on the DMMA path (row panels
             // too short for the INT8 path fall back to it): plain stores only
-            if (here != 1 || !(on_a || on_b) || rows < 1024 || cols < 1024 || !g.epis.empty()) {
+            if (here != 1 || !(on_a || on_b) || rows < lo || cols < lo || !g.epis.empty()) {
                 ok = false;
                 break;
             }

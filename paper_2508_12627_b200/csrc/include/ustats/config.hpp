@@ -43,6 +43,10 @@ struct DeviceConfig {
     /// 21000); longer K runs as equal K chunks summed in FP64 (tests lower it
     /// to exercise the chunked path at small n).
     long long oz_max_k = 0;
+    /// Smallest rows / cols / K of a GEMM that runs emulated (0 = 1024: below,
+    /// DMMA is as fast and needs no digit pass). Tests lower it so the emulated
+    /// and lazy-operand paths run at sizes the CPU reference reaches.
+    int oz_min_dim = 0;
 };
 
 struct Config {

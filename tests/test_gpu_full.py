@@ -95,6 +95,37 @@ def test_golden_k_chunked_emulation(engine, fixture, max_k):
     assert abs(got.value - float(g["u"])) <= TOL * scale
 
 
+@pytest.mark.parametrize("fixture,world", [("C4_n256.npz", 1), ("C4_n384.npz", 1), ("C4_n512.npz", 1), ("C4_n384.npz", 3),
+                                            ("C3_n1024.npz", 1), ("C5_n512.npz", 1), ("C1_n2000.npz", 1)])
+def test_golden_emulated_at_reference_sizes(engine, fixture, world):
+    # oz_min_dim lowers the size threshold of the INT8-emulated GEMM, so the
+    # paths the BASELINE sizes take -- Khatri-Rao GEMMs with lazy (never
+    # materialized) n^3 operands, digit reuse across GEMMs, emulated symmetric
+    # products with fused epilogues -- run at sizes the CPU reference reaches
+    # and are compared with the reference library's golden terms (C4's full
+    # n = 1024 needs ~1 h and ~300 GB on the host).
+    from paper_2508_12627_b200.workloads import generate
+    path = GOLDEN / fixture
+    if not path.exists():
+        pytest.skip("fixture not generated")
+    g = np.load(path)
+    name, n = fixture.split("_n")
+    n = int(n.split(".")[0])
+    factors, sig, m, _ = generate(name, n)
+    kw = dict(shard_rows=True, emulate_world=world) if world > 1 else {}
+    cfg = engine.Config(oz_min_dim=128, memory_cap_entries=max(2 ** 31, n ** 3 + 1), **kw)
+    got = engine.u_terms(factors, sig, m, cfg)
+    if name != "C1":
+        assert got.stats["int8_tensor_ops"] > 0 and got.stats["emulated_gemm_macs"] == got.stats["executed_gemm_macs"]
+    if name == "C4" and world == 1:
+        # the n^3 Khatri-Rao operands stay lazy: fewer stream ops than the DMMA plan
+        plain = engine.u_terms(factors, sig, m, engine.Config(memory_cap_entries=max(2 ** 31, n ** 3 + 1)))
+        assert got.stats["stream_launches"] < plain.stats["stream_launches"]
+    scale = float(np.max(np.abs(g["v"])))
+    assert float(np.max(np.abs(got.v - g["v"]))) <= TOL * scale
+    assert abs(got.value - float(g["u"])) <= TOL * scale
+
+
 def test_guard_picks_six_slices_and_forced_counts(engine):
     # the error-bound guard: the fewest slices whose worst-case entry bound
     # (S+2) 2^(2-8S) does not exceed the FP64 dot product's gamma_K -> 6 for
