@@ -67,9 +67,11 @@ class Runtime {
 
     cudaStream_t stream() const { return cur_; }  // where allocations / launches go now
     cudaStream_t main_stream() const { return stream_; }
-    cudaStream_t side_stream() const { return side_; }
-    cudaStream_t copy_stream() const { return copy_; }
-    cudaStream_t prep_stream() const { return prep_; }
+    // the auxiliary streams note that they were handed out: sync() waits only
+    // for those (eight cudaStreamSynchronize calls per evaluation otherwise)
+    cudaStream_t side_stream() { used_ |= 1; return side_; }
+    cudaStream_t copy_stream() { used_ |= 2; return copy_; }
+    cudaStream_t prep_stream() { used_ |= 4; return prep_; }
     // Device memory available to this engine: free memory when the runtime was
     // created (the stream-ordered pool then recycles it). cudaMemGetInfo can
     // stall for tens of ms, so it is re-queried only for programs that need
@@ -78,7 +80,7 @@ class Runtime {
     void refresh_free_bytes();
     void agree_free_bytes();  // row sharding: every rank plans with the communicator's minimum
     static constexpr int kChunkStreams = 4;
-    cudaStream_t chunk_stream(int i) const { return chunk_[i % kChunkStreams]; }
+    cudaStream_t chunk_stream(int i) { used_ |= 8; return chunk_[i % kChunkStreams]; }
     // bitwise-symmetry results of host inputs seen before (speculation key)
     std::map<std::pair<const void*, long long>, bool> symmetry_seen;
     void set_stream(cudaStream_t s) { cur_ = s; }
@@ -89,7 +91,8 @@ class Runtime {
     Buf borrow(const double* ptr, int order, long long n);
     double* scratch(std::size_t entries);
     void release(double* p);
-    void sync();
+    void sync();          // end of an evaluation: waits for the main stream and every auxiliary stream it used
+    void wait_streams();  // the same wait in the middle of one (keeps the used-stream notes)
 
     // Large buffers (>= kSlabMin: n^2 intermediates, Ozaki digit panels) come
     // from a cache of exact-size slabs instead of the stream-ordered pool: a
@@ -143,6 +146,7 @@ class Runtime {
     cudaStream_t prep_ = nullptr;  // per-panel sparsify / probe kernels behind the copies (high priority)
     cudaStream_t chunk_[kChunkStreams] = {};  // concurrent per-panel GEMM pieces
     cudaStream_t cur_ = nullptr;
+    unsigned used_ = 0;  // auxiliary streams handed out since the last sync (bit 0 side, 1 copy, 2 prep, 3 chunk)
     void* comm_ = nullptr;
     int comm_world_ = 1;
     double free_bytes_ = 0;

@@ -295,7 +295,13 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
     for (const auto& sp : specs) total_factors += sp.sig.size();
     int* flags = nullptr;
     DevStats upload_stats;
-    if (config.device.exploit_symmetry)
+    // probe flags only when some matrix input is not symmetric by construction
+    // (device-tensorized components are: no allocation, events or frees then)
+    bool may_probe = false;
+    for (const auto& sp : specs)
+        for (std::size_t k = 0; k < sp.sig.size(); ++k)
+            may_probe |= sp.sig[k].size() == 2 && !(k < sp.symmetric.size() && sp.symmetric[k]);
+    if (config.device.exploit_symmetry && may_probe)
         check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&flags), sizeof(int) * total_factors + 4, rt.stream()),
                    "alloc flags");
     for (std::size_t q = 0; q < specs.size(); ++q) tensors[q].assign(specs[q].sig.size(), nullptr);

@@ -832,7 +832,7 @@ void Program::execute() {
         const int dims = static_cast<int>(op.out_ids.size()) + std::popcount(op.sum);
         return dims <= 2;
     };
-    cudaStream_t streams[2] = {rt_->main_stream(), rt_->side_stream()};
+    cudaStream_t streams[2] = {rt_->main_stream(), multi ? rt_->side_stream() : rt_->main_stream()};
     const std::size_t N = ops_.size();
     if (multi && !launch_ordered_) {
         launch_ordered_ = true;  // a cached program re-executes in the same order

@@ -140,7 +140,7 @@ double Runtime::idle_slab_bytes() const {
 }
 
 void Runtime::reclaim() {
-    sync();  // this runtime's streams only: every pending user of an idle slab has finished
+    wait_streams();  // this runtime's streams only: every pending user of an idle slab has finished
     for (Slab& s : idle_) {
         cudaEventDestroy(s.freed);
         cudaFree(s.ptr);
@@ -207,10 +207,17 @@ void Runtime::release(double* p) {
 }
 
 void Runtime::sync() {
-    for (auto& c : chunk_) check_cuda(cudaStreamSynchronize(c), "cudaStreamSynchronize");
-    check_cuda(cudaStreamSynchronize(copy_), "cudaStreamSynchronize");
-    check_cuda(cudaStreamSynchronize(prep_), "cudaStreamSynchronize");
-    check_cuda(cudaStreamSynchronize(side_), "cudaStreamSynchronize");
+    wait_streams();
+    used_ = 0;  // the evaluation is over: the next one notes its own streams
+}
+
+void Runtime::wait_streams() {
+    const unsigned used = used_;
+    if (used & 8)
+        for (auto& c : chunk_) check_cuda(cudaStreamSynchronize(c), "cudaStreamSynchronize");
+    if (used & 2) check_cuda(cudaStreamSynchronize(copy_), "cudaStreamSynchronize");
+    if (used & 4) check_cuda(cudaStreamSynchronize(prep_), "cudaStreamSynchronize");
+    if (used & 1) check_cuda(cudaStreamSynchronize(side_), "cudaStreamSynchronize");
     check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
 }
 
