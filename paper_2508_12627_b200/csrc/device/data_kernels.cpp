@@ -185,7 +185,7 @@ StatisticResult u_statistic_data(const std::string& spec, const double* data, lo
             ++launches;
         } else if (p[0] == "rbf") {
             b = rt.allocate(2, n);
-            launch_rbf(x, n, d, std::stod(p[1]), b->ptr, s);
+            launch_rbf(x, n, d, std::stod(p[1]), b->ptr, s, /*zero_diag=*/true);  // sparsified as it is written
             ++launches;
         } else {  // proj: B = Z (Z^T Z / n)^{-1} Z^T as the symmetric product (Z M)(Z M)^T
             const int ncols = std::stoi(p[1]), kmax = std::stoi(p[2]);
@@ -242,6 +242,7 @@ StatisticResult u_statistic_data(const std::string& spec, const double* data, lo
         // RBF entries are computed once per unordered pair and mirrored; the
         // projection is a mirrored symmetric GEMM: both bitwise symmetric
         spec_in.symmetric.push_back(rec.rfind("rbf", 0) == 0 || rec.rfind("proj", 0) == 0);
+        spec_in.sparsified.push_back(rec.rfind("rbf", 0) == 0);
     }
     Config cfg = config;
     cfg.device.donate_inputs = true;  // our own tensors: sparsify in place

@@ -481,6 +481,9 @@ struct StatisticSpec {
     // per input: symmetric by construction (device-built kernels), so the
     // bitwise symmetry probe is skipped; empty = probe every matrix
     std::vector<char> symmetric;
+    // per input: already sparsified by its device tensorizer (repeated-index
+    // entries written as zero): the separate sparsify pass is skipped
+    std::vector<char> sparsified;
 };
 std::vector<StatisticResult> lattice_batch(const std::vector<StatisticSpec>& specs, bool inputs_on_device,
                                            long long n, LatticeMode mode, const Config& config);

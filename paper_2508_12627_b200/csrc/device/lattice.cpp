@@ -364,7 +364,7 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
                            "upload");
             }
             rt.begin(Runtime::kOther);
-            if (mode == LatticeMode::Sparsified && !panels)
+            if (mode == LatticeMode::Sparsified && !panels && !(k < sp.sparsified.size() && sp.sparsified[k]))
                 upload_stats.kernel_launches += static_cast<std::uint64_t>(launch_sparsify(b->ptr, order, n, rt.stream()));
             if (order == 2 && k < sp.symmetric.size() && sp.symmetric[k]) {
                 b->symmetric = config.device.exploit_symmetry;  // known by construction: no probe

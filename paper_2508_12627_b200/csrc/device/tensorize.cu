@@ -13,7 +13,8 @@ namespace {
 
 // A_ij = exp(-scale * sum_c (x_ic - x_jc)^2). The squared differences are
 // summed in coordinate order, so A is bitwise symmetric.
-__global__ void rbf(const double* __restrict__ x, long long n, int d, double scale, double* __restrict__ out) {
+__global__ void rbf(const double* __restrict__ x, long long n, int d, double scale, double* __restrict__ out,
+                    int zero_diag) {
     const long long j = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     const long long i = blockIdx.y;
     if (j >= n) return;
@@ -24,7 +25,7 @@ __global__ void rbf(const double* __restrict__ x, long long n, int d, double sca
         const double t = xi[c] - xj[c];
         s += t * t;
     }
-    out[i * n + j] = exp(-scale * s);
+    out[i * n + j] = (zero_diag && i == j) ? 0.0 : exp(-scale * s);
 }
 
 // Symmetric tiled pair kernels: one 32x32 tile pair (ti <= tj) per block,
@@ -38,7 +39,7 @@ __global__ void rbf(const double* __restrict__ x, long long n, int d, double sca
 constexpr int kPairTile = 32, kPairMaxDim = 64;
 template <int KIND>
 __global__ void pair_sym(const double* __restrict__ x, long long n, int d, int c0, int dc, double scale,
-                         double* __restrict__ out) {
+                         double* __restrict__ out, int zero_diag) {
     const int ti = blockIdx.y, tj = blockIdx.x;
     if (ti > tj) return;
     __shared__ double xi[kPairTile][kPairMaxDim + 1], xj[kPairTile][kPairMaxDim + 1];
@@ -60,7 +61,8 @@ __global__ void pair_sym(const double* __restrict__ x, long long n, int d, int c
             const double u = xi[ri][c] - xj[cj][c];
             s += u * u;
         }
-        const double v = KIND == 0 ? exp(-scale * s) : sqrt(s);
+        double v = KIND == 0 ? exp(-scale * s) : sqrt(s);
+        if (zero_diag && ti == tj && ri == cj) v = 0.0;  // sparsified on the fly (tensor.cpp:54-76)
         t[ri][cj] = v;
         if (i0 + ri < n && j0 + cj < n) out[(i0 + ri) * n + j0 + cj] = v;
     }
@@ -82,7 +84,7 @@ __global__ void pair_sym(const double* __restrict__ x, long long n, int d, int c
 constexpr int kBlkTile = 64, kBlkDim = 32;
 template <int KIND>
 __global__ void __launch_bounds__(256) pair_sym_blocked(const double* __restrict__ x, long long n, int d, int c0,
-                                                        int dc, double scale, double* __restrict__ out) {
+                                                        int dc, double scale, double* __restrict__ out, int zero_diag) {
     const int ti = blockIdx.y, tj = blockIdx.x;
     if (ti > tj) return;
     // coordinate-major point blocks; reused afterwards as the transposed 64 x 64 tile
@@ -122,6 +124,10 @@ __global__ void __launch_bounds__(256) pair_sym_blocked(const double* __restrict
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) s[a][b] = KIND == 0 ? exp(-scale * s[a][b]) : sqrt(s[a][b]);
+    if (zero_diag && ti == tj && ty == tx) {  // sparsified on the fly (tensor.cpp:54-76)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) s[a][a] = 0.0;
+    }
     const long long ib = i0 + ty * 4, jb = j0 + tx * 4;
     const bool full = i0 + kBlkTile <= n && j0 + kBlkTile <= n && (n & 1) == 0;
 #pragma unroll
@@ -299,30 +305,31 @@ __global__ void times_small(const double* __restrict__ z, long long n, int F, co
 
 }  // namespace
 
-void launch_rbf(const double* x, long long n, int d, double bandwidth, double* out, cudaStream_t s) {
+void launch_rbf(const double* x, long long n, int d, double bandwidth, double* out, cudaStream_t s, bool zero_diag) {
     const double scale = 0.5 / (bandwidth * bandwidth);
     if (d <= kBlkDim) {
         const unsigned T = static_cast<unsigned>((n + kBlkTile - 1) / kBlkTile);
-        pair_sym_blocked<0><<<dim3(T, T), 256, 0, s>>>(x, n, d, 0, d, scale, out);
+        pair_sym_blocked<0><<<dim3(T, T), 256, 0, s>>>(x, n, d, 0, d, scale, out, zero_diag ? 1 : 0);
         return;
     }
     if (d <= kPairMaxDim) {
         const unsigned T = static_cast<unsigned>((n + kPairTile - 1) / kPairTile);
-        pair_sym<0><<<dim3(T, T), dim3(kPairTile, 8), 0, s>>>(x, n, d, 0, d, scale, out);
+        pair_sym<0><<<dim3(T, T), dim3(kPairTile, 8), 0, s>>>(x, n, d, 0, d, scale, out, zero_diag ? 1 : 0);
         return;
     }
-    rbf<<<dim3(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(n)), 256, 0, s>>>(x, n, d, scale, out);
+    rbf<<<dim3(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(n)), 256, 0, s>>>(x, n, d, scale, out,
+                                                                                                  zero_diag ? 1 : 0);
 }
 
 void launch_distance(const double* x, long long n, int d, int c0, int dc, double* out, cudaStream_t s) {
     if (dc <= kBlkDim) {
         const unsigned T = static_cast<unsigned>((n + kBlkTile - 1) / kBlkTile);
-        pair_sym_blocked<1><<<dim3(T, T), 256, 0, s>>>(x, n, d, c0, dc, 0.0, out);
+        pair_sym_blocked<1><<<dim3(T, T), 256, 0, s>>>(x, n, d, c0, dc, 0.0, out, 0);
         return;
     }
     if (dc <= kPairMaxDim) {
         const unsigned T = static_cast<unsigned>((n + kPairTile - 1) / kPairTile);
-        pair_sym<1><<<dim3(T, T), dim3(kPairTile, 8), 0, s>>>(x, n, d, c0, dc, 0.0, out);
+        pair_sym<1><<<dim3(T, T), dim3(kPairTile, 8), 0, s>>>(x, n, d, c0, dc, 0.0, out, 0);
         return;
     }
     distance<<<dim3(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(n)), 256, 0, s>>>(x, n, d, c0, dc,

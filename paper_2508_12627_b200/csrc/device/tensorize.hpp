@@ -12,7 +12,9 @@
 
 namespace ustats::dev {
 
-void launch_rbf(const double* x, long long n, int d, double bandwidth, double* out, cudaStream_t s);
+// zero_diag: write the sparsified matrix directly (zero diagonal, tensor.cpp:54-76)
+void launch_rbf(const double* x, long long n, int d, double bandwidth, double* out, cudaStream_t s,
+                bool zero_diag = false);
 // Euclidean distance matrix over sample columns [c0, c0 + dc) (row stride d).
 void launch_distance(const double* x, long long n, int d, int c0, int dc, double* out, cudaStream_t s);
 // Adjacency indicator a and co-indicator b (zero diagonal) of an edge list
