@@ -60,6 +60,20 @@ def test_configs_medium(engine, name, n):
     check_u(engine, factors, sig, m)
 
 
+@pytest.mark.parametrize("name,n,extra", [("C4", 130, {}), ("C4", 136, {}), ("C5", 200, {}), ("C3", 258, {}),
+                                          ("C2", 300, {}), ("C4", 132, dict(shard_rows=True, emulate_world=3)),
+                                          ("C5", 520, dict(oz_max_k=128))])
+def test_emulated_paths_ragged_small(engine, name, n, extra):
+    # the INT8-emulated GEMM, the lazy Khatri-Rao digit split (shared-memory
+    # staged, lanes along K), K chunks and row panels at sizes that are not
+    # multiples of the 128-row digit panels / 64-byte K tiles (oz_min_dim
+    # lowers the emulation threshold), against the reference
+    from paper_2508_12627_b200.workloads import generate
+    factors, sig, m, _ = generate(name, n)
+    got, _ = check_u(engine, factors, sig, m, engine.Config(oz_min_dim=128, memory_cap_entries=2 ** 40, **extra))
+    assert got.stats["int8_tensor_ops"] > 0
+
+
 def random_kernel(m, rng):
     # acceptance_main.cpp:92-125 shape: one or two covering tuples + up to two extras
     slots = list(range(m))
