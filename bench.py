@@ -389,14 +389,27 @@ def main():
             ms = float(t.item())
         return ms / k, last
 
+    # Repeated small data-API evaluations (n <= 4096) replay one captured CUDA
+    # graph; the engine's per-class event records would switch that off, so for
+    # those configs the kernel-class times come from a separate profiled pass
+    # right after the timed region (same inputs, same build), not from inside it.
+    separate_profile = use_data and world == 1 and n <= 4096
     with ClockSampler(local) as clocks:
         clocks.wait_ready()
         for _ in range(args.warmup):
             step(dfac, True)
-        us.profile(enable=True, reset=True, device=local)
+        if not separate_profile:
+            us.profile(enable=True, reset=True, device=local)
+        replays0 = us.graph_replays(local)
         t_start = time.time()
         ms_step, (u_val, r) = timed(dfac, True, args.steps)
         clocks.mark(t_start, time.time())
+        replayed = us.graph_replays(local) - replays0
+        if separate_profile:
+            us.profile(enable=True, reset=True, device=local)
+            for _ in range(args.steps):
+                _, r = step(dfac, True)
+            torch.cuda.synchronize()
         prof = us.profile(enable=False, reset=True, device=local)
     e2e = None
     step_s = ms_step * 1e-3
@@ -521,6 +534,9 @@ def main():
                                                "gemm_launches", "stream_launches", "shared_hits",
                                                "emulated_gemm_macs", "int8_tensor_ops", "oz_slices")},
         "stream_ms_per_step": stream_ms,
+        "graph_replayed_steps": int(replayed),
+        "kernel_times_from": ("a separate profiled pass of the same steps (event records inside the timed region "
+                              "would disable the CUDA-graph replay)") if separate_profile else "the timed region",
     }
     if e2e:
         line["e2e"] = e2e

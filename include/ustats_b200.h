@@ -51,7 +51,9 @@ typedef struct us_config {
                                     bit5 row sharding across ranks (else V-term sharding),
                                     bit6 serial launch (one stream),
                                     bit7 exact DMMA only (no INT8 tensor-core emulation of
-                                    large FP64 GEMMs); US_FLAGS_DEFAULT = 0xF */
+                                    large FP64 GEMMs),
+                                    bit8 no CUDA-graph replay of repeated small data-API calls;
+                                    US_FLAGS_DEFAULT = 0xF */
     int32_t emulate_world;       /* row sharding over this many virtual ranks on one device (tests) */
     uint64_t memory_budget_bytes; /* device bytes the memory-bounded schedule may plan for (0 = free memory) */
     int32_t oz_slices;           /* emulated-GEMM digit slices (0 = error-bound guard; 4..7 forced) */
@@ -246,6 +248,9 @@ US_API int us_dgemm(int32_t method, int32_t slices, int32_t symmetric, int64_t m
 /* The engine's CUDA stream on `device` (cudaStream_t as void*), so callers can
  * order their own work / record events against it. */
 US_API int us_device_stream(int32_t device, void** stream_out);
+/* How many evaluations on `device` ran as a replayed CUDA graph so far
+ * (us_u_statistic_data on repeated small problems; flags bit8 turns it off). */
+US_API int us_graph_replays(int32_t device, uint64_t* count_out);
 /* Kernel-class timing (CUDA events on the engine stream): enable != 0 turns it
  * on; ms_out[3] / groups_out[3] receive accumulated milliseconds and launch
  * groups for {GEMM, stream, other}; reset != 0 clears the totals after reading.

@@ -6,7 +6,7 @@ broadcast-product-reduce streams) behind the C-ABI in include/ustats_b200.h.
 """
 from .api import (  # noqa: F401
     Config, UStatsError, UTerms, bell_number, combine_terms, device_count, device_stream, einsum,
-    profile, nccl_init, nccl_unique_id,
+    profile, nccl_init, nccl_unique_id, graph_replays,
     eliminate_index, kernel_tensors, optimize_order, plan_summary, plan_terms, restricted_v_tensors, survivors, treewidth,
     ComplexityReport, chain_signature, complexity_report, dgemm,
     u_statistic, u_statistic_batch, u_statistic_tensors, u_statistic_unsparsified_tensors, u_terms,

@@ -111,6 +111,7 @@ SIGNATURES = {
     "us_device_count": (C.c_int, [P(i32)]),
     "us_device_synchronize": (C.c_int, [i32]),
     "us_device_stream": (C.c_int, [i32, P(C.c_void_p)]),
+    "us_graph_replays": (C.c_int, [i32, P(u64)]),
     "us_profile": (C.c_int, [i32, i32, i32, P(f64), P(u64)]),
 }
 

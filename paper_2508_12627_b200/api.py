@@ -59,6 +59,7 @@ class Config:
     shard_rows: bool = False     # multi-GPU: row-shard every op (else V-term sharding)
     serial_launch: bool = False  # one CUDA stream (no GEMM / reduction overlap)
     fp64_emulation: bool = True  # large FP64 GEMMs on the INT8 tensor cores (Ozaki digits); False = DMMA only
+    graph_replay: bool = True    # repeated small u_statistic(spec, data) calls replay one captured CUDA graph
     emulate_world: int = 0       # row sharding over virtual ranks on one device (tests)
     memory_budget_bytes: int = 0  # device bytes the memory-bounded schedule may use (0 = free memory)
     oz_slices: int = 0           # emulated-GEMM digit slices (0 = error-bound guard, 4..7 forced)
@@ -81,7 +82,7 @@ class Config:
         c.flags = (1 if self.share else 0) | (2 if self.fuse_epilogues else 0) | \
                   (4 if self.symmetry else 0) | (8 if self.reorder else 0) | (16 if self.donate_inputs else 0) | \
                   (32 if self.shard_rows else 0) | (64 if self.serial_launch else 0) | \
-                  (0 if self.fp64_emulation else 128)
+                  (0 if self.fp64_emulation else 128) | (0 if self.graph_replay else 256)
         c.emulate_world = self.emulate_world
         c.memory_budget_bytes = self.memory_budget_bytes
         c.oz_slices = self.oz_slices
@@ -571,6 +572,13 @@ def device_stream(device: int = -1) -> int:
     h = C.c_void_p()
     _check(N.lib().us_device_stream(device, C.byref(h)))
     return h.value or 0
+
+
+def graph_replays(device: int = -1) -> int:
+    """Evaluations on `device` that ran as a replayed CUDA graph so far."""
+    c = N.u64()
+    _check(N.lib().us_graph_replays(device, C.byref(c)))
+    return int(c.value)
 
 
 def profile(enable: bool = True, reset: bool = True, device: int = -1) -> dict:

@@ -64,6 +64,7 @@ ustats::Config to_config(const us_config* c) {
     cfg.device.shard_rows = c->flags & 32;
     cfg.device.serial_launch = c->flags & 64;
     cfg.device.fp64_emulation = !(c->flags & 128);
+    cfg.device.graph_replay = !(c->flags & 256);
     cfg.device.emulate_world = c->emulate_world;
     cfg.device.memory_budget_bytes = c->memory_budget_bytes;
     if (c->oz_slices != 0 && (c->oz_slices < 4 || c->oz_slices > 7))
@@ -672,6 +673,10 @@ int us_dgemm(int32_t method, int32_t slices, int32_t symmetric, int64_t m, int64
         if (ea) cudaFree(ea);
         if (eb) cudaFree(eb);
     });
+}
+
+int us_graph_replays(int32_t device, uint64_t* count_out) {
+    return guarded([&] { *count_out = ustats::dev::graph_replays(ustats::dev::Runtime::get(device).device()); });
 }
 
 int us_device_stream(int32_t device, void** stream_out) {

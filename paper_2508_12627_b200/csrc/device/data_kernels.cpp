@@ -2,15 +2,19 @@
 // device from the raw sample, evaluate the U-statistic (engine.cpp:173-193
 // with tensorize, engine.cpp:108-136, moved to the GPU).
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <map>
+#include <memory>
+#include <mutex>
 #include <string>
 
 #include "executor.hpp"
 #include "kernels.hpp"
 #include "tensorize.hpp"
 #include "ustats/errors.hpp"
+#include "ustats/partition.hpp"
 #include "ustats/tensor.hpp"
 
 namespace ustats::dev {
@@ -146,6 +150,57 @@ DataKernel parse_data_kernel(const std::string& spec, int d) {
          "unknown kernel spec '" + spec + "' (prod2 | hoif:<j>:<k> | rbf:<shape>:<h> | proj:<m>:<kmax>)");
 }
 
+namespace {
+
+// Replay cache of the data API (small n): the whole evaluation of a repeated
+// call -- sample upload, tensorization, every kernel of the cached plan, the
+// D2H of the terms -- is captured once as a CUDA graph and launched as one
+// node chain afterwards (a bootstrap loop calls u_statistic thousands of
+// times on the same buffers; the evaluation is launch-bound there). Keyed by
+// the spec, the shape, the data pointer and the config; dropped when the plan
+// cache evicts (the graph refers to the plan's term slots).
+struct ReplayEntry {
+    int calls = 0;
+    bool dead = false;
+    std::uint64_t generation = 0, used = 0;
+    std::unique_ptr<GraphCapture> cap;
+    StatisticResult result;  // everything but the term values
+};
+constexpr long long kReplayMaxN = 4096;
+constexpr std::size_t kReplayEntries = 8;
+std::map<std::string, ReplayEntry>& replay_cache(int device) {
+    static auto* all = new std::map<int, std::map<std::string, ReplayEntry>>();  // under the device mutex
+    return (*all)[device];
+}
+
+std::atomic<std::uint64_t> g_replays[64];
+
+bool host_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+StatisticResult recombine(const ReplayEntry& e) {
+    StatisticResult r = e.result;
+    const GraphCapture& c = *e.cap;
+    for (std::size_t t = 0; t < c.T; ++t) r.v[t] = c.host_v[t];
+    for (const auto& [dup, src] : c.alias) r.v[dup] = r.v[src];
+    for (std::size_t t = 0; t < c.T; ++t) r.terms[t] = static_cast<double>(r.mu[t]) * r.v[t];
+    r.value = combine_terms(r.terms);
+    return r;
+}
+
+StatisticResult u_statistic_data_once(const DataKernel& k, const double* data, long long n, int d, bool on_device,
+                                      const Config& config, double* tensorize_seconds);
+
+}  // namespace
+
+std::uint64_t graph_replays(int device) { return g_replays[static_cast<unsigned>(device) & 63].load(); }
+
 StatisticResult u_statistic_data(const std::string& spec, const double* data, long long n, int d, bool on_device,
                                  const Config& config, double* tensorize_seconds) {
     const DataKernel k = parse_data_kernel(spec, d);
@@ -154,6 +209,76 @@ StatisticResult u_statistic_data(const std::string& spec, const double* data, lo
              "need at least " + std::to_string(k.m) + " observations, have " + std::to_string(n));
     for (std::size_t c = 0; c < k.sig.size(); ++c)
         checked_entry_count(static_cast<int>(k.sig[c].size()), static_cast<int>(n), config);
+    Runtime& rt = Runtime::get(config.device.device);
+    std::lock_guard<std::recursive_mutex> lock(device_mutex(rt.device()));
+    const DeviceConfig& dc = config.device;
+    const bool eligible = dc.graph_replay && n <= kReplayMaxN && !dc.shard_rows && dc.world_size <= 1 &&
+                          !rt.profiling() && k.m <= 10 && (on_device || host_pinned(data));
+    if (!eligible) return u_statistic_data_once(k, data, n, d, on_device, config, tensorize_seconds);
+
+    auto& cache = replay_cache(rt.device());
+    static std::atomic<std::uint64_t> clock{0};
+    const std::string key = spec + "|" + std::to_string(n) + "x" + std::to_string(d) + "|" +
+                            std::to_string(reinterpret_cast<std::uintptr_t>(data)) + (on_device ? "d|" : "h|") +
+                            config_key(config);
+    auto it = cache.find(key);
+    if (it == cache.end()) {
+        while (cache.size() >= kReplayEntries) {
+            auto lru = cache.begin();
+            for (auto j = cache.begin(); j != cache.end(); ++j)
+                if (j->second.used < lru->second.used) lru = j;
+            cache.erase(lru);
+        }
+        it = cache.emplace(key, ReplayEntry{}).first;
+    }
+    ReplayEntry& e = it->second;
+    e.used = ++clock;
+    if (e.cap && e.generation != plan_generation(rt.device())) {  // the plan it was captured from is gone
+        e.cap.reset();
+        e.calls = 0;
+    }
+    if (e.cap && e.cap->exec) {
+        check_cuda(cudaGraphLaunch(e.cap->exec, rt.main_stream()), "cudaGraphLaunch");
+        rt.sync();
+        ++g_replays[static_cast<unsigned>(rt.device()) & 63];
+        if (tensorize_seconds) *tensorize_seconds = 0.0;
+        return recombine(e);
+    }
+    if (e.dead || e.calls < 1) {  // first call: records and caches the plan
+        ++e.calls;
+        return u_statistic_data_once(k, data, n, d, on_device, config, tensorize_seconds);
+    }
+    // second call with the same arguments: capture it
+    auto cap = std::make_unique<GraphCapture>();
+    cap->capacity = static_cast<std::size_t>(bell_number(k.m));
+    check_cuda(cudaMallocHost(reinterpret_cast<void**>(&cap->host_v), sizeof(double) * cap->capacity), "cudaMallocHost");
+    rt.set_stream(rt.main_stream());
+    check_cuda(cudaStreamBeginCapture(rt.main_stream(), cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    active_capture() = cap.get();
+    try {
+        StatisticResult r = u_statistic_data_once(k, data, n, d, on_device, config, tensorize_seconds);
+        if (!cap->launched) fail(ErrorCode::CudaError, "graph capture did not complete");
+        e.generation = plan_generation(rt.device());
+        e.result = r;
+        e.cap = std::move(cap);
+        return r;
+    } catch (...) {
+        // not capturable (an allocation that had to synchronize, a missing plan ...):
+        // discard the capture and evaluate the plain way from now on
+        active_capture() = nullptr;
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(rt.main_stream(), &g);
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        e.dead = true;
+    }
+    return u_statistic_data_once(k, data, n, d, on_device, config, tensorize_seconds);
+}
+
+namespace {
+
+StatisticResult u_statistic_data_once(const DataKernel& k, const double* data, long long n, int d, bool on_device,
+                                      const Config& config, double* tensorize_seconds) {
     Runtime& rt = Runtime::get(config.device.device);
     cudaStream_t s = rt.main_stream();
     rt.set_stream(s);
@@ -246,10 +371,19 @@ StatisticResult u_statistic_data(const std::string& spec, const double* data, lo
     }
     Config cfg = config;
     cfg.device.donate_inputs = true;  // our own tensors: sparsify in place
+    // under a graph capture the tensors and the sample are released inside it
+    // (every allocation of a replayed graph must be freed by the graph)
+    if (GraphCapture* cap = active_capture())
+        cap->before_sync = [&] {
+            built.clear();
+            sample.reset();
+        };
     auto res = lattice_batch({spec_in}, true, n, LatticeMode::Sparsified, cfg);
     res[0].stats.kernel_launches += launches;
     return res[0];
 }
+
+}  // namespace
 
 }  // namespace ustats::dev
 

@@ -32,6 +32,9 @@
 
 #include <cuda_runtime.h>
 
+#include <functional>
+#include <mutex>
+
 #include "kernels.hpp"
 #include "ustats/config.hpp"
 #include "ustats/notation.hpp"
@@ -132,6 +135,7 @@ class Runtime {
         std::uint64_t groups[3] = {0, 0, 0};
     };
     void profile_enable(bool on) { profiling_ = on; }
+    bool profiling() const { return profiling_; }
     void begin(Kind k);
     void end(Kind k);
     Profile collect(bool reset);
@@ -485,6 +489,27 @@ struct StatisticSpec {
     // entries written as zero): the separate sparsify pass is skipped
     std::vector<char> sparsified;
 };
+// Graph replay of a small cached evaluation (data_kernels.cpp). While a
+// capture is active on this thread, lattice_batch_impl requires a cached plan,
+// copies the term values into the capture's pinned buffer and, where it would
+// synchronize, releases the caller's device buffers (before_sync), ends the
+// capture, instantiates the graph and launches it once; the evaluation then
+// finishes as usual. Later calls launch the graph and recombine the terms.
+struct GraphCapture {
+    cudaGraphExec_t exec = nullptr;
+    double* host_v = nullptr;  // pinned, capacity doubles
+    std::size_t capacity = 0, T = 0;
+    std::vector<std::pair<std::size_t, std::size_t>> alias;  // (duplicate term, source term)
+    std::function<void()> before_sync;
+    bool launched = false;
+    ~GraphCapture();
+};
+GraphCapture*& active_capture();                // thread-local; nullptr = none
+std::recursive_mutex& device_mutex(int device);  // one evaluation at a time per device
+std::uint64_t plan_generation(int device);       // bumps whenever a cached plan is evicted
+std::string config_key(const Config& c);
+std::uint64_t graph_replays(int device);          // evaluations served by a replayed graph
+
 std::vector<StatisticResult> lattice_batch(const std::vector<StatisticSpec>& specs, bool inputs_on_device,
                                            long long n, LatticeMode mode, const Config& config);
 std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>& specs, bool inputs_on_device,

@@ -207,18 +207,8 @@ PlanCache& plan_cache(int device) {
 
 std::string plan_key(const std::vector<StatisticSpec>& specs, const std::vector<std::vector<int>>& slot,
                      const std::vector<Buf>& uniq, long long n, LatticeMode mode, const Config& c, double budget) {
-    const DeviceConfig& d = c.device;
     std::string k = std::to_string(n) + "|" + std::to_string(static_cast<int>(mode)) + "|" +
-                    std::to_string(static_cast<long long>(budget / 8.589934592e9)) + "|" +
-                    std::to_string(c.memory_cap_entries) + "," + std::to_string(static_cast<int>(c.strategy)) + "," +
-                    std::to_string(c.exhaustive_index_bound) + "," + std::to_string(c.exact_treewidth_bound) + "|" +
-                    std::to_string(d.share_subexpressions) + std::to_string(d.fuse_epilogues) +
-                    std::to_string(d.exploit_symmetry) + std::to_string(d.reorder_for_sharing) +
-                    std::to_string(d.serial_launch) + std::to_string(d.shard_rows) + std::to_string(d.fp64_emulation) +
-                    "," + std::to_string(d.rank) + "," +
-                    std::to_string(d.world_size) + "," + std::to_string(d.emulate_world) + "," +
-                    std::to_string(d.memory_budget_bytes) + "," + std::to_string(d.oz_slices) + "," +
-                    std::to_string(d.oz_max_k) + "," + std::to_string(d.oz_min_dim) + "|";
+                    std::to_string(static_cast<long long>(budget / 8.589934592e9)) + "|" + config_key(c) + "|";
     for (const Buf& b : uniq) k += std::to_string(b->order) + (b->symmetric ? "s" : "g");
     for (std::size_t q = 0; q < specs.size(); ++q) {
         k += "|" + std::to_string(specs[q].m) + ":";
@@ -230,6 +220,8 @@ std::string plan_key(const std::vector<StatisticSpec>& specs, const std::vector<
     }
     return k;
 }
+
+std::uint64_t g_plan_generation[64] = {};
 
 PlanEntry* find_plan(int device, const std::string& key) {
     if (std::getenv("USTATS_NO_PLAN_CACHE")) return nullptr;
@@ -250,6 +242,7 @@ PlanEntry* store_plan(int device, const std::string& key, std::unique_ptr<PlanEn
         for (auto it = pc.entries.begin(); it != pc.entries.end(); ++it)
             if (it->second->used < lru->second->used) lru = it;
         pc.entries.erase(lru);
+        ++g_plan_generation[static_cast<unsigned>(device) & 63];  // captured graphs refer to evicted term slots
     }
     PlanEntry* raw = e.get();
     pc.entries[key] = std::move(e);
@@ -263,18 +256,42 @@ PlanEntry* store_plan(int device, const std::string& key, std::unique_ptr<PlanEn
 // are shared, and ctypes releases the GIL during the call, so two host
 // threads evaluating on one device are serialized here (different devices
 // run concurrently).
+GraphCapture::~GraphCapture() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (host_v) cudaFreeHost(host_v);
+}
+
+GraphCapture*& active_capture() {
+    thread_local GraphCapture* cap = nullptr;
+    return cap;
+}
+
+std::recursive_mutex& device_mutex(int device) {
+    static std::mutex table_mu;
+    static std::map<int, std::unique_ptr<std::recursive_mutex>> per_device;
+    std::lock_guard<std::mutex> lock(table_mu);
+    auto& slot = per_device[device];
+    if (!slot) slot = std::make_unique<std::recursive_mutex>();
+    return *slot;
+}
+
+std::uint64_t plan_generation(int device) { return g_plan_generation[static_cast<unsigned>(device) & 63]; }
+
+std::string config_key(const Config& c) {
+    const DeviceConfig& d = c.device;
+    return std::to_string(c.memory_cap_entries) + "," + std::to_string(static_cast<int>(c.strategy)) + "," +
+           std::to_string(c.exhaustive_index_bound) + "," + std::to_string(c.exact_treewidth_bound) + "|" +
+           std::to_string(d.share_subexpressions) + std::to_string(d.fuse_epilogues) +
+           std::to_string(d.exploit_symmetry) + std::to_string(d.reorder_for_sharing) +
+           std::to_string(d.serial_launch) + std::to_string(d.shard_rows) + std::to_string(d.fp64_emulation) + "," +
+           std::to_string(d.rank) + "," + std::to_string(d.world_size) + "," + std::to_string(d.emulate_world) + "," +
+           std::to_string(d.memory_budget_bytes) + "," + std::to_string(d.oz_slices) + "," +
+           std::to_string(d.oz_max_k) + "," + std::to_string(d.oz_min_dim);
+}
+
 std::vector<StatisticResult> lattice_batch(const std::vector<StatisticSpec>& specs, bool inputs_on_device,
                                            long long n, LatticeMode mode, const Config& config) {
-    static std::mutex table_mu;
-    static std::map<int, std::unique_ptr<std::mutex>> per_device;
-    std::mutex* mu = nullptr;
-    {
-        std::lock_guard<std::mutex> lock(table_mu);
-        auto& slot = per_device[config.device.device];
-        if (!slot) slot = std::make_unique<std::mutex>();
-        mu = slot.get();
-    }
-    std::lock_guard<std::mutex> lock(*mu);
+    std::lock_guard<std::recursive_mutex> lock(device_mutex(Runtime::get(config.device.device).device()));
     return lattice_batch_impl(specs, inputs_on_device, n, mode, config, true);
 }
 
@@ -442,6 +459,9 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
     const std::string key = plan_key(specs, slot, uniq, n, mode, config, budget);
     PlanEntry* entry = find_plan(rt.device(), key);
     const bool hit = entry != nullptr;
+    GraphCapture* cap = active_capture();
+    if (cap && (!hit || flags || config.device.shard_rows))  // recording allocates persistent state: never inside a capture
+        fail(ErrorCode::CudaError, "graph capture needs a cached single-GPU plan with inputs symmetric by construction");
     if (!hit) {
         // Record every statistic into one program (sub-contractions shared
         // across them), optimize it, and keep it: a later call with the same
@@ -500,7 +520,9 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
     // row sharding: every term value is a sum of per-rank partials
     if (config.device.shard_rows && config.device.emulate_world <= 1 && rt.has_comm()) rt.allreduce_sum(d_v, T);
     std::vector<double> v(T, 0.0);
-    if (T) check_cuda(cudaMemcpyAsync(v.data(), d_v, sizeof(double) * T, cudaMemcpyDeviceToHost, rt.stream()), "D2H");
+    if (cap && T > cap->capacity) fail(ErrorCode::CudaError, "graph capture: term buffer too small");
+    double* host_v = cap ? cap->host_v : v.data();  // a captured copy lands in the capture's pinned buffer
+    if (T) check_cuda(cudaMemcpyAsync(host_v, d_v, sizeof(double) * T, cudaMemcpyDeviceToHost, rt.stream()), "D2H");
     std::vector<int> spec_flags(speculative.size(), 0);
     for (std::size_t i = 0; i < speculative.size(); ++i)  // in prep-stream order: after the probe itself
         check_cuda(cudaMemcpyAsync(&spec_flags[i], std::get<1>(speculative[i]), sizeof(int), cudaMemcpyDeviceToHost,
@@ -517,7 +539,24 @@ std::vector<StatisticResult> lattice_batch_impl(const std::vector<StatisticSpec>
     tensors.clear();
     by_ptr.clear();
     probes.clear();
+    if (cap) {
+        // everything of this evaluation is enqueued: close the capture where the
+        // evaluation would synchronize, and run the graph once for this call
+        if (cap->before_sync) cap->before_sync();
+        cap->T = T;
+        cap->alias = term_alias;
+        cudaGraph_t graph = nullptr;
+        check_cuda(cudaStreamEndCapture(rt.main_stream(), &graph), "cudaStreamEndCapture");
+        active_capture() = nullptr;
+        const cudaError_t inst = cudaGraphInstantiate(&cap->exec, graph, 0);
+        cudaGraphDestroy(graph);
+        check_cuda(inst, "cudaGraphInstantiate");
+        check_cuda(cudaGraphLaunch(cap->exec, rt.main_stream()), "cudaGraphLaunch");
+        cap->launched = true;
+    }
     rt.sync();
+    if (cap)
+        for (std::size_t t = 0; t < T; ++t) v[t] = cap->host_v[t];
     bool mispredicted = false;
     for (std::size_t i = 0; i < speculative.size(); ++i)
         if (spec_flags[i] != 0) {

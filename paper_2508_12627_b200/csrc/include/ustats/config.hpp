@@ -47,6 +47,9 @@ struct DeviceConfig {
     /// DMMA is as fast and needs no digit pass). Tests lower it so the emulated
     /// and lazy-operand paths run at sizes the CPU reference reaches.
     int oz_min_dim = 0;
+    /// Replay repeated small data-API evaluations (same spec, shape, buffers
+    /// and config, n <= 4096) as one captured CUDA graph.
+    bool graph_replay = true;
 };
 
 struct Config {

@@ -422,3 +422,50 @@ def test_emulated_gemm_k_chunks_row_sharded(engine):
     assert sharded.stats["int8_tensor_ops"] > 0
     scale = np.max(np.abs(base.v))
     assert np.max(np.abs(sharded.v - base.v)) <= 1e-12 * scale
+
+
+def test_graph_replay_of_repeated_small_evaluations(engine):
+    # u_statistic(spec, data) on the same buffers: call 1 records the plan,
+    # call 2 captures the whole evaluation (upload, tensorization, kernels,
+    # D2H of the terms) as a CUDA graph, later calls replay it. Same kernels in
+    # the same order: bit-identical to the plain path; new contents of the same
+    # buffer are picked up; what cannot be captured falls back silently.
+    import torch
+    from paper_2508_12627_b200.workloads import generate, generate_data
+    plain = engine.Config(graph_replay=False)
+    data, spec, m, _ = generate_data("C1", 600)
+    X = torch.from_numpy(data).cuda()
+    base = engine.u_statistic(spec, X, config=plain)
+    factors, sig, _, _ = generate("C1", 600)
+    u_ref, _, _, v = oracle_terms(factors, sig, m)
+    assert abs(base - u_ref) <= TOL * np.max(np.abs(v))
+    before = engine.graph_replays()
+    vals = [engine.u_statistic(spec, X) for _ in range(6)]
+    assert all(x == base for x in vals), (vals, base)
+    assert engine.graph_replays() - before >= 3
+    u, st = engine.u_statistic(spec, X, with_stats=True)
+    assert u == base and st["partitions_evaluated"] == len(v)
+    # the replayed graph reads the buffer again: new data, new value
+    rng = np.random.default_rng(7)
+    X.copy_(torch.from_numpy(rng.normal(size=data.shape)))
+    torch.cuda.synchronize()
+    changed = engine.u_statistic(spec, X)
+    assert changed == engine.u_statistic(spec, X, config=plain) and changed != base
+    # pinned host sample (H2D inside the graph)
+    H = torch.from_numpy(data).pin_memory()
+    before = engine.graph_replays()
+    assert all(engine.u_statistic(spec, H) == base for _ in range(5))
+    assert engine.graph_replays() - before >= 2
+    # pageable host memory is not eligible; the projection kernel's host Cholesky cannot be captured
+    assert all(engine.u_statistic(spec, data) == base for _ in range(3))
+    d3, spec3, _, _ = generate_data("C3", 200)
+    X3 = torch.from_numpy(d3).cuda()
+    base3 = engine.u_statistic(spec3, X3, config=plain)
+    assert all(engine.u_statistic(spec3, X3) == base3 for _ in range(4))
+    # a GEMM-bearing plan (two streams joined inside the capture)
+    d2, spec2, _, _ = generate_data("C2", 384)
+    X2 = torch.from_numpy(d2).cuda()
+    base2 = engine.u_statistic(spec2, X2, config=plain)
+    before = engine.graph_replays()
+    assert all(engine.u_statistic(spec2, X2) == base2 for _ in range(5))
+    assert engine.graph_replays() - before >= 2
