@@ -197,7 +197,9 @@ struct OzPlan {
     std::size_t a_bytes = 0, b_bytes = 0, scratch_bytes = 0;
 };
 int oz_guard_slices(long long K);
-OzPlan oz_plan(long long K, long long rows, long long cols, bool same_operand, const DeviceConfig& dc);
+// long_chunks: the op's place in the schedule leaves room for bigger digit panels (fewer K chunks)
+OzPlan oz_plan(long long K, long long rows, long long cols, bool same_operand, const DeviceConfig& dc,
+               bool long_chunks = false);
 
 // ------------------------------------------------------------------ Program
 struct View {
@@ -245,6 +247,9 @@ struct Op {
     std::vector<Epi> epis;
     bool store = true;
     bool symmetric_out = false;
+    // emulated GEMM: the schedule leaves room at this op for the larger digit
+    // panels (fewer K chunks; make_schedule decides from the live set)
+    bool long_chunks = false;
     // sweep: one pass over the matrix factors[0] (row-major view) feeding the
     // consumers in `epis` (row_id = the matrix's row index)
     bool sweep = false;
@@ -372,6 +377,7 @@ class Program {
     std::map<std::string, CachedDigits> digits_;
     std::map<std::string, int> digit_uses_;
     std::string key_a_, key_b_;  // operand keys of the GEMM being launched (run_gemm -> run_emulated)
+    bool cur_long_chunks_ = false;  // the GEMM being launched may use the larger digit panels
     std::string operand_key(const std::vector<View>& fs, const std::vector<int>& rows, int e) const;
     void plan_digit_reuse();
     void drop_digits();

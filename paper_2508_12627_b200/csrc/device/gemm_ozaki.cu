@@ -179,6 +179,15 @@ __host__ __device__ __forceinline__ void oz_tile_of(const OzakiArgs& p, long lon
 #endif
 __host__ __device__ constexpr int oz_pass_split(int S) { return S <= 4 ? S : S - OZ_PASS0_ACC; }
 static_assert(oz_pass_split(7) <= 4 && 7 - oz_pass_split(7) <= 4, "TMEM holds 4 accumulators of 128 columns");
+// Pass 0 of S > 4 slices holds three diagonals, which leaves one 128-column
+// accumulator of TMEM spare: the top diagonal d = S - 1 (S products per k, the
+// most of any) is split over two accumulators -- products t < oz_top_half(S)
+// into its own, the rest into the spare one -- and the two are added in FP64
+// when pass 0 drains. No int32 accumulator then sums more than S - 1 products,
+// so K up to (2^31 - 1) / ((S - 1) 128^2) stays exact (S = 6: 26176 instead of
+// 21824: C5's K = 65536 can run as 3 chunks instead of 4 where memory allows).
+__host__ __device__ constexpr bool oz_top_split(int S, int D0, int D1) { return S > 4 && D1 == S && D1 - D0 == OZ_PASS0_ACC; }
+__host__ __device__ constexpr int oz_top_half(int S) { return (S + 1) / 2; }
 
 // Issued by the whole MMA warp: every operand is warp-uniform (one base
 // descriptor plus compile-time offsets), so the descriptors stay in uniform
@@ -199,8 +208,9 @@ __device__ __forceinline__ void oz_issue_stage(unsigned tmem, unsigned long long
                 if (t >= S || u >= S) continue;
                 const unsigned a_off = (SLOT0 + t) * OZ_TILE_STAGE + ks * 2 * OZ_BM * 16;
                 const unsigned bo = b_off + (SLOT0 + u) * OZ_TILE_STAGE + ks * 2 * OZ_BN * 16;
-                const unsigned acc = tmem + static_cast<unsigned>((d - D0) * OZ_BN);
-                const unsigned accumulate = (first && t == 0) ? 0u : 1u;
+                const bool spare = oz_top_split(S, D0, D1) && d == S - 1 && t >= oz_top_half(S);
+                const unsigned acc = tmem + static_cast<unsigned>((spare ? OZ_PASS0_ACC : d - D0) * OZ_BN);
+                const unsigned accumulate = (first && (t == 0 || (spare && t == oz_top_half(S)))) ? 0u : 1u;
                 asm volatile(
                     "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
                     "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(acc),
@@ -245,11 +255,14 @@ __device__ __forceinline__ double oz_scale(double v, int e) {
 
 // Adds the diagonals [D0, D1) of columns c0..c0+15 (this thread's TMEM lane) to
 // v, smallest contributions first: all loads in flight, one wait.
-template <int D0, int D1>
+// TOP: the top diagonal's second accumulator (oz_top_split) sits after the
+// D1 - D0 regular ones; both halves are exact integers, added in FP64.
+template <int D0, int D1, bool TOP = false>
 __device__ __forceinline__ void oz_drain(unsigned lane_base, int c0, double (&v)[16], bool add) {
-    unsigned r[D1 - D0][16];
+    constexpr int NA = D1 - D0 + (TOP ? 1 : 0);
+    unsigned r[NA][16];
 #pragma unroll
-    for (int d = D0; d < D1; ++d) tmem_ld16_async(lane_base + static_cast<unsigned>((d - D0) * OZ_BN + c0), r[d - D0]);
+    for (int a = 0; a < NA; ++a) tmem_ld16_async(lane_base + static_cast<unsigned>(a * OZ_BN + c0), r[a]);
     tmem_wait_ld(r);
     if (!add)
 #pragma unroll
@@ -258,7 +271,11 @@ __device__ __forceinline__ void oz_drain(unsigned lane_base, int c0, double (&v)
     for (int d = D1 - 1; d >= D0; --d) {
         const double scale = __longlong_as_double(static_cast<long long>(1023 - 8 * d - 12) << 52);  // 2^{-8d-12}
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] += static_cast<double>(static_cast<int>(r[d - D0][j])) * scale;
+        for (int j = 0; j < 16; ++j) {
+            double x = static_cast<double>(static_cast<int>(r[d - D0][j]));
+            if (TOP && d == D1 - 1) x += static_cast<double>(static_cast<int>(r[NA - 1][j]));
+            v[j] += x * scale;
+        }
     }
 }
 
@@ -420,7 +437,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) ozaki_gemm_kernel(OzakiArgs p) 
 #pragma unroll 1
             for (int c0 = cb; c0 < cb + OZ_BN / 2; c0 += 16) {
                 double v[16];
-                oz_drain<split, S>(lane_base, c0, v, false);
+                oz_drain<split, S, oz_top_split(S, split, S)>(lane_base, c0, v, false);
 #pragma unroll
                 for (int j = 0; j < 16; ++j) work[(c0 + j) * OZ_BM] = v[j];
             }
@@ -676,8 +693,9 @@ __device__ __forceinline__ void oz2_issue_stage(unsigned tmem, unsigned long lon
                 // 32-byte k-step = two 16-byte core-matrix columns (A: 128 rows, B: 64 rows each)
                 const unsigned a_off = (SLOT0 + t) * OZ2_A + ks * 2 * OZ_BM * 16;
                 const unsigned b_off = (SLOT0 + u) * OZ2_B + ks * 2 * (OZ_BN / 2) * 16;
-                const unsigned acc = tmem + static_cast<unsigned>((d - D0) * OZ_BN);
-                const unsigned accumulate = (first && t == 0) ? 0u : 1u;
+                const bool spare = oz_top_split(S, D0, D1) && d == S - 1 && t >= oz_top_half(S);
+                const unsigned acc = tmem + static_cast<unsigned>((spare ? OZ_PASS0_ACC : d - D0) * OZ_BN);
+                const unsigned accumulate = (first && (t == 0 || (spare && t == oz_top_half(S)))) ? 0u : 1u;
                 asm volatile(
                     "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
                     "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(acc),
@@ -896,7 +914,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_THREADS, 1)
 #pragma unroll 1
                 for (int c0 = cb; c0 < cb + OZ_BN / 2; c0 += 16) {
                     double v[16];
-                    oz_drain<split, S>(lane_base, c0, v, false);
+                    oz_drain<split, S, oz_top_split(S, split, S)>(lane_base, c0, v, false);
 #pragma unroll
                     for (int q = 0; q < 16; ++q) work[(c0 + q) * OZ_BM] = v[q];
                 }
@@ -1450,7 +1468,8 @@ bool oz2_enabled() {
 
 int launch_ozaki_gemm(const OzakiArgs& in, cudaStream_t s) {
     if (in.kpad % OZ_BK != 0) return -1;
-    if (static_cast<long long>(in.slices) * in.kpad * 128 * 128 >= (1ll << 31)) return -1;  // int32 diagonals exact
+    // int32 accumulators exact: at most S products each, S - 1 with the split top diagonal (S > 4)
+    if (static_cast<long long>(in.slices > 4 ? in.slices - 1 : in.slices) * in.kpad * 128 * 128 >= (1ll << 31)) return -1;
     if (oz2_enabled() && in.tile_count < 0 && in.tile_begin == 0 && in.mpad >= 2 * OZ_BM) {
         OzakiArgs p = in;
         p.prefetch = 0;

@@ -233,8 +233,11 @@ void Program::run_stream(const Op& op, double* out) {
 // Khatri-Rao GEMMs, K = 1024: 297 -> 216 ms per evaluation). Config.oz_min_dim
 // lowers it (tests pin the emulated path at sizes the CPU reference reaches).
 long long oz_min_dim(const DeviceConfig& dc) { return dc.oz_min_dim > 0 ? dc.oz_min_dim : 1024; }
-constexpr double kOzDigitCap = 8.0 * 1073741824.0;  // digit bytes per operand per K chunk (C4: 4 GiB split its
-                                                    // K = 1024 GEMMs in two, 112 -> 158 ms per evaluation)
+constexpr double kOzDigitCap = 6.5 * 1073741824.0;  // digit bytes per operand per K chunk (C4: 4 GiB split its
+                                                    // K = 1024 GEMMs in two, 112 -> 158 ms per evaluation; C5:
+                                                    // four chunks of 16384, 6.0 GiB per operand)
+constexpr double kOzDigitCapLong = 8.25 * 1073741824.0;  // where the schedule has room (Op::long_chunks): C5 runs
+                                                         // three chunks of 21888 (8.02 GiB per operand) there
 
 // Error-bound guard. With S balanced 8-bit slices, truncation and the dropped
 // products t + u >= S bound every entry's error by (S + 2) 2^{2-8S} K
@@ -251,17 +254,20 @@ int oz_guard_slices(long long K) {
     return kOzMaxSlices;
 }
 
-OzPlan oz_plan(long long K, long long rows, long long cols, bool same_operand, const DeviceConfig& dc) {
+OzPlan oz_plan(long long K, long long rows, long long cols, bool same_operand, const DeviceConfig& dc,
+               bool long_chunks) {
     OzPlan p;
     p.slices = dc.oz_slices > 0 ? dc.oz_slices : oz_guard_slices(K);
-    // S products of K * 128^2 per diagonal accumulator must stay below 2^31
-    const long long exact = ((1ll << 31) - 1) / (static_cast<long long>(p.slices) * 128 * 128) / 64 * 64;
+    // the products of K * 128^2 one int32 accumulator sums must stay below 2^31: S on the top
+    // diagonal, S - 1 since the kernels split it over two accumulators (S > 4, gemm_ozaki.cu)
+    const long long per_acc = p.slices > 4 ? p.slices - 1 : p.slices;
+    const long long exact = ((1ll << 31) - 1) / (per_acc * 128 * 128) / 64 * 64;
     const long long max_k = dc.oz_max_k > 0 ? std::min<long long>(dc.oz_max_k / 64 * 64, exact) : exact;
     // fewest chunks whose digit panels stay within kOzDigitCap per operand (C5:
     // 65536 rows x 65536 K would need 24 GiB of digits per operand; 4, 6, 8 and
     // 12 chunks measured within 2% of each other there)
     const long long rows_pad = (std::max(rows, cols) + 127) / 128 * 128;
-    double cap = kOzDigitCap;
+    double cap = long_chunks ? kOzDigitCapLong : kOzDigitCap;
     if (const char* e = std::getenv("USTATS_OZ_DIGIT_CAP_GB")) cap = std::atof(e) * 1073741824.0;
     const long long cap_k = std::max<long long>(64, static_cast<long long>(cap / (static_cast<double>(rows_pad) * p.slices)) / 64 * 64);
     const long long limit = std::min(max_k, cap_k);
@@ -309,7 +315,7 @@ std::size_t Program::op_scratch_bytes(const Op& op) const {
     const long long lo = oz_min_dim(config_.device);
     if (n_ < lo || rows < lo || cols < lo) return 0;
     const bool same = op.fa.size() == 1 && op.fb.size() == 1 && op.fa[0].buf == op.fb[0].buf && rows == cols;
-    return oz_plan(n_, rows, cols, same, config_.device).scratch_bytes;
+    return oz_plan(n_, rows, cols, same, config_.device, op.long_chunks).scratch_bytes;
 }
 
 // Digits of both operands, the product (straight into a plain store's output,
@@ -371,7 +377,7 @@ int Program::run_emulated(const GemmArgs& g, const EpiSet& set) {
     const long long ars = flat_row_stride(g.a, n_), brs = flat_row_stride(g.b, n_);
     const bool same = ars >= 0 && brs >= 0 && g.a.ptr[0] == g.b.ptr[0] && g.rows == g.cols && ars == brs &&
                       g.a.kstride[0] == g.b.kstride[0];
-    const OzPlan oz = oz_plan(g.n, g.rows, g.cols, same, config_.device);
+    const OzPlan oz = oz_plan(g.n, g.rows, g.cols, same, config_.device, cur_long_chunks_);
     const int S = oz.slices;
     const long long kc = oz.kc;
     if (oz.nchunks > 1)  // a consumer of C^2 is not linear in C: the caller runs it on DMMA
@@ -544,6 +550,7 @@ void Program::run_gemm(const Op& op, double* out) {
     };
     key_a_ = operand_key(op.fa, op.ra, op.e);
     key_b_ = operand_key(op.fb, op.rb, op.e);
+    cur_long_chunks_ = op.long_chunks && slice_world_ == 1 && block_rows_.first < 0;
     GemmArgs g;
     fill(g.a, fa, op.ra);
     fill(g.b, fb, op.rb);

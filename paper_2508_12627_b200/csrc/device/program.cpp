@@ -711,6 +711,7 @@ std::pair<long long, long long> Program::sweep_strides(const View& v, int row_id
 // once (C5: 412 GB); the search finds orders that fit one B200.
 void Program::make_schedule(double budget) {
     const std::size_t N = ops_.size();
+    for (Op& op : ops_) op.long_chunks = false;  // decided at the end, from this schedule's slack
     std::vector<std::vector<int>> reads(N), outs(N);
     std::vector<int> consumers(bufs_.size(), 0);
     for (std::size_t i = 0; i < N; ++i) {
@@ -852,6 +853,28 @@ void Program::make_schedule(double budget) {
     schedule_ = best.order;
     sched_peak_ = best.peak;
     sched_fits_ = found;
+    // Fewer, longer K chunks for the emulated GEMMs whose place in this order
+    // leaves room for the larger digit panels (C5: 3 chunks of 21888 need
+    // 2 x 8.02 GiB where 4 chunks of 16384 need 2 x 6 GiB; each chunk less saves
+    // a read-modify-write pass over the outputs and a drain per tile). Decided
+    // per op from the live set at that op, with 2 GiB to spare; the schedule's
+    // peak never rises above the budget.
+    if (found && budget > 0 && rt_ && !config_.device.shard_rows) {
+        State st = s0;
+        for (std::size_t i : best.order) {
+            Op& op = ops_[i];
+            double live_with_outputs = st.live;
+            for (int b : outs[i]) live_with_outputs += size(b);
+            if (op.gemm && !op.dead && scratch[i] > 0) {
+                op.long_chunks = true;
+                const double longer = static_cast<double>(op_scratch_bytes(op));
+                if (longer <= scratch[i] || live_with_outputs + longer + 2.0 * 1073741824.0 > budget) op.long_chunks = false;
+                else scratch[i] = longer;
+            }
+            run(st, i);
+        }
+        sched_peak_ = std::max(sched_peak_, st.peak);
+    }
 }
 
 // Lazy GEMM operands. A multi-factor operand is recorded as an elementwise
