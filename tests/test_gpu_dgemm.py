@@ -61,3 +61,23 @@ def test_ozaki_exponents_beyond_the_fast_scaling_range(engine):
     assert np.all(np.abs(got - ref) <= 1e-12 * scale)
     c = engine.dgemm(a, a, "ozaki", 7, symmetric=True)
     assert np.array_equal(c, c.T)
+
+
+def test_ozaki_int32_accumulators_at_the_exact_bound(engine):
+    # S = 6, K = 26112: just under the int32-exact bound (26176) that splitting
+    # the top digit diagonal over two TMEM accumulators allows (21824 before).
+    # Every value has the digits (63, 127, 127, 127, 127, 127): all digit
+    # products are positive and near the largest possible, so the fullest
+    # accumulator (five products on diagonal 4) reaches 98% of 2^31 -- one more
+    # product in it, or an unsplit top diagonal (six), would wrap around.
+    k = 26112
+    x = float(0x3F7F7F7F7F7F) / 2.0 ** 46
+    a = np.full((256, k), x)
+    b = np.full((384, k), x)
+    ref = k * x * x
+    got = engine.dgemm(a, b, "ozaki", 6)
+    assert got.shape == (256, 384)
+    assert np.max(np.abs(got - ref)) <= 1e-11 * ref
+    # signs alternate along K in A: the products cancel pairwise and the result is exactly 0
+    a2 = a * np.where(np.arange(k) % 2 == 0, 1.0, -1.0)
+    assert np.max(np.abs(engine.dgemm(a2, b, "ozaki", 6))) <= 1e-11 * ref
